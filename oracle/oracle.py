@@ -1,0 +1,477 @@
+"""ctypes front-end for the CPU checkers -- TEST INFRASTRUCTURE ONLY.
+
+Two checkers live under oracle/:
+
+* ``C``   -- oracle/liboracle.so, the plain-C restatement of the reference
+  hot path (oracle/zen_oracle.c, every function cites zen/*.hpp lines).
+* ``Ref`` -- oracle/_ref/libzenref.so, the reference's own headers compiled in
+  place from /root/reference by oracle/Makefile (a thin extern "C" shim).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this
+module.  The product (paper_2309_13254_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libzenref.so")
+
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+
+OK, INVALID, SERIAL_OVERFLOW, OUTSIDE, MALFORMED, EMPTY, MISMATCH = 0, 1, 2, 3, 4, 5, 6
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg="", partition=-1):
+        super().__init__(f"oracle error {code}: {msg}")
+        self.code = code
+        self.partition = partition
+
+
+def _u64(a):
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class _ZoFamily(C.Structure):
+    _fields_ = [("partition_seed", C.c_uint64), ("slot_seeds", C.c_uint64 * 16),
+                ("partitions", C.c_uint32), ("k", C.c_uint32)]
+
+
+class _ZoParams(C.Structure):
+    _fields_ = [("rehash_depth", C.c_uint32), ("r1_multiplier", C.c_double),
+                ("r2_ratio", C.c_double), ("lanes", C.c_uint32), ("seed", C.c_uint64)]
+
+
+@dataclass
+class HashResult:
+    parts_idx: list
+    parts_val: list
+    serial_writes: int = 0
+    placed_at_depth: list | None = None
+    slots: np.ndarray | None = None
+    slot_vals: np.ndarray | None = None
+    depth_of: np.ndarray | None = None
+
+
+@dataclass
+class BPResult:
+    idx: np.ndarray
+    val: np.ndarray
+    ledger: np.ndarray  # [2 stages][4 fields][n]
+    balance: tuple | None
+    counts: np.ndarray | None = None
+    agg_counts: np.ndarray | None = None
+
+
+class COracle:
+    """The C restatement (oracle/zen_oracle.c)."""
+
+    def __init__(self, path=ORACLE_SO):
+        L = self.lib = C.CDLL(path)
+        L.zo_mix64.restype = C.c_uint64
+        L.zo_mix64.argtypes = [C.c_uint64]
+        L.zo_derive_seed.restype = C.c_uint64
+        L.zo_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.zo_family_make.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(_ZoFamily)]
+        L.zo_family_make_worker.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                            C.POINTER(_ZoFamily)]
+        L.zo_partition_of_many.argtypes = [u64p, C.c_uint64, C.c_uint64, C.c_uint32, u32p]
+        L.zo_family_slot_of.restype = C.c_uint64
+        L.zo_family_slot_of.argtypes = [C.POINTER(_ZoFamily), C.c_uint64, C.c_uint32, C.c_uint64]
+        L.zo_hierarchical_hash.argtypes = [
+            u64p, f32p, C.c_uint64, C.c_uint64, C.POINTER(_ZoFamily), C.c_uint64, C.c_uint64,
+            u64p, f32p, u64p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
+            u64p, C.POINTER(C.c_int64)]
+        L.zo_to_sparse.restype = C.c_uint64
+        L.zo_to_sparse.argtypes = [f32p, C.c_uint64, u64p, f32p]
+        L.zo_merge_sum.restype = C.c_uint64
+        L.zo_merge_sum.argtypes = [u64p, f32p, C.c_uint64, u64p, f32p, C.c_uint64, u64p, f32p]
+        L.zo_universe_create.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.zo_universe_destroy.argtypes = [C.c_void_p]
+        L.zo_universe_size.restype = C.c_uint64
+        L.zo_universe_size.argtypes = [C.c_void_p, C.c_uint32]
+        L.zo_universe_list.restype = C.POINTER(C.c_uint64)
+        L.zo_universe_list.argtypes = [C.c_void_p, C.c_uint32]
+        L.zo_hash_bitmap_encode.argtypes = [C.c_void_p, C.c_uint32, u64p, f32p, C.c_uint64, u8p,
+                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.zo_hash_bitmap_decode.argtypes = [C.c_void_p, C.c_uint32, u8p, C.c_uint64, C.c_uint64,
+                                            u64p, f32p]
+        L.zo_bp_sync.argtypes = [
+            C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), u64p,
+            C.POINTER(_ZoParams), C.c_void_p, u64p, f32p, C.POINTER(C.c_uint64), u64p, u64p, u64p,
+            f64p, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_uint32)]
+        L.zo_bp_sizes.argtypes = [C.c_double, C.c_double, C.c_uint64, C.c_uint32,
+                                  C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+
+    # -- hash family -------------------------------------------------------
+    def mix64(self, x):
+        return self.lib.zo_mix64(x)
+
+    def derive_seed(self, m, s):
+        return self.lib.zo_derive_seed(m, s)
+
+    def family(self, seed, n, k, worker=None):
+        f = _ZoFamily()
+        rc = (self.lib.zo_family_make(seed, n, k, C.byref(f)) if worker is None else
+              self.lib.zo_family_make_worker(seed, worker, n, k, C.byref(f)))
+        if rc:
+            raise OracleError(rc, "family")
+        return f
+
+    def family_seeds(self, seed, n, k, worker=None):
+        f = self.family(seed, n, k, worker)
+        return [f.partition_seed] + [f.slot_seeds[i] for i in range(k)]
+
+    def partition_of(self, idx, pseed, n):
+        idx = _u64(idx)
+        out = np.empty(idx.size, np.uint32)
+        self.lib.zo_partition_of_many(idx, idx.size, pseed, n, out)
+        return out
+
+    def slot_of(self, fam, index, rnd, r1):
+        return self.lib.zo_family_slot_of(C.byref(fam), index, rnd, r1)
+
+    # -- hierarchical hash ------------------------------------------------
+    def hierarchical_hash(self, m, idx, val, fam, r1, r2, layout=False):
+        idx, val = _u64(idx), _f32(val)
+        n, k = fam.partitions, fam.k
+        oi = np.empty(max(idx.size, 1), np.uint64)
+        ov = np.empty(max(idx.size, 1), np.float32)
+        pc = np.zeros(n, np.uint64)
+        cells = n * (r1 + r2)
+        slots = np.zeros(max(cells, 1), np.uint64) if layout else None
+        svals = np.zeros(max(cells, 1), np.float32) if layout else None
+        depth = np.zeros(max(idx.size, 1), np.uint32) if layout else None
+        serial = C.c_uint64(0)
+        pad = np.zeros(k, np.uint64)
+        ovf = C.c_int64(-1)
+        rc = self.lib.zo_hierarchical_hash(
+            idx, val, idx.size, m, C.byref(fam), r1, r2, oi, ov, pc,
+            slots.ctypes.data if layout else None, svals.ctypes.data if layout else None,
+            depth.ctypes.data if layout else None, C.byref(serial), pad, C.byref(ovf))
+        if rc == SERIAL_OVERFLOW:
+            raise OracleError(rc, "serial overflow", ovf.value)
+        if rc:
+            raise OracleError(rc, "hierarchical_hash")
+        offs = np.concatenate([[0], np.cumsum(pc)]).astype(np.int64)
+        res = HashResult([oi[offs[p]:offs[p + 1]].copy() for p in range(n)],
+                         [ov[offs[p]:offs[p + 1]].copy() for p in range(n)],
+                         int(serial.value), [int(x) for x in pad])
+        if layout:
+            res.slots, res.slot_vals, res.depth_of = slots[:cells], svals[:cells], depth[:idx.size]
+        return res
+
+    def to_sparse(self, dense):
+        dense = _f32(dense)
+        idx = np.empty(max(dense.size, 1), np.uint64)
+        val = np.empty(max(dense.size, 1), np.float32)
+        c = self.lib.zo_to_sparse(dense, dense.size, idx, val)
+        return idx[:c].copy(), val[:c].copy()
+
+    def merge_sum(self, ia, va, ib, vb):
+        ia, va, ib, vb = _u64(ia), _f32(va), _u64(ib), _f32(vb)
+        io = np.empty(max(ia.size + ib.size, 1), np.uint64)
+        vo = np.empty(max(ia.size + ib.size, 1), np.float32)
+        c = self.lib.zo_merge_sum(ia, va, ia.size, ib, vb, ib.size, io, vo)
+        return io[:c].copy(), vo[:c].copy()
+
+    def aggregate(self, tensors):
+        ai, av = _u64(tensors[0][0]), _f32(tensors[0][1])
+        for ti, tv in tensors[1:]:
+            ai, av = self.merge_sum(ai, av, ti, tv)
+        return ai, av
+
+    # -- universe / codec -------------------------------------------------
+    def universe(self, m, n, pseed):
+        return _Universe(self, m, n, pseed)
+
+    # -- BP ----------------------------------------------------------------
+    def bp_sizes(self, r1m, r2r, nnz, n):
+        a, b = C.c_uint64(), C.c_uint64()
+        self.lib.zo_bp_sizes(r1m, r2r, nnz, n, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def bp_sync(self, m, inputs, k=3, r1_multiplier=2.0, r2_ratio=0.1, seed=1, universe=None):
+        n = len(inputs)
+        ins = [(_u64(i), _f32(v)) for i, v in inputs]
+        nnz = np.array([i.size for i, _ in ins], np.uint64)
+        ip = (C.c_void_p * n)(*[i.ctypes.data for i, _ in ins])
+        vp = (C.c_void_p * n)(*[v.ctypes.data for _, v in ins])
+        p = _ZoParams(k, r1_multiplier, r2_ratio, 1, seed)
+        u = universe or self.universe(m, n, self.derive_seed(seed, 0))
+        tot = int(nnz.sum())
+        oi = np.empty(max(tot, 1), np.uint64)
+        ov = np.empty(max(tot, 1), np.float32)
+        oc = C.c_uint64(0)
+        ledger = np.zeros(8 * n, np.uint64)
+        counts = np.zeros(n * n, np.uint64)
+        agg = np.zeros(n, np.uint64)
+        bal = np.zeros(2, np.float64)
+        bv = C.c_int(0)
+        op, ow = C.c_int64(-1), C.c_uint32(0)
+        rc = self.lib.zo_bp_sync(n, m, ip, vp, nnz, C.byref(p), u.h, oi, ov, C.byref(oc), ledger,
+                                 counts, agg, bal, C.byref(bv), C.byref(op), C.byref(ow))
+        if rc == SERIAL_OVERFLOW:
+            e = OracleError(rc, "serial overflow", op.value)
+            e.worker = ow.value
+            raise e
+        if rc:
+            raise OracleError(rc, "bp_sync")
+        c = oc.value
+        return BPResult(oi[:c].copy(), ov[:c].copy(), ledger.reshape(2, 4, n),
+                        (bal[0], bal[1]) if bv.value else None, counts.reshape(n, n), agg)
+
+
+class _Universe:
+    def __init__(self, co, m, n, pseed):
+        self.co, self.m, self.n, self.pseed = co, m, n, pseed
+        h = C.c_void_p()
+        rc = co.lib.zo_universe_create(m, n, pseed, C.byref(h))
+        if rc:
+            raise OracleError(rc, "universe")
+        self.h = h
+
+    def __del__(self):
+        try:
+            self.co.lib.zo_universe_destroy(self.h)
+        except Exception:
+            pass
+
+    def size(self, s):
+        return int(self.co.lib.zo_universe_size(self.h, s))
+
+    def indices(self, s):
+        sz = self.size(s)
+        p = self.co.lib.zo_universe_list(self.h, s)
+        return np.ctypeslib.as_array(p, shape=(max(sz, 1),))[:sz].copy()
+
+    def encode(self, s, idx, val):
+        idx, val = _u64(idx), _f32(val)
+        nbytes = (self.size(s) + 7) // 8 + 4 * idx.size
+        payload = np.zeros(max(nbytes, 1), np.uint8)
+        bits, bad = C.c_uint64(), C.c_uint64()
+        rc = self.co.lib.zo_hash_bitmap_encode(self.h, s, idx, val, idx.size, payload,
+                                               C.byref(bits), C.byref(bad))
+        if rc:
+            raise OracleError(rc, f"encode (index {bad.value})")
+        return payload[:nbytes], bits.value
+
+    def decode(self, s, payload, count):
+        payload = np.ascontiguousarray(payload, np.uint8)
+        idx = np.empty(max(count, 1), np.uint64)
+        val = np.empty(max(count, 1), np.float32)
+        rc = self.co.lib.zo_hash_bitmap_decode(self.h, s, payload, payload.size, count, idx, val)
+        if rc:
+            raise OracleError(rc, "decode")
+        return idx[:count].copy(), val[:count].copy()
+
+
+class RefOracle:
+    """The reference itself (oracle/_ref/libzenref.so, compiled from /root/reference)."""
+
+    def __init__(self, path=REF_SO):
+        L = self.lib = C.CDLL(path)
+        L.ref_last_partition.restype = C.c_int64
+        L.ref_last_message.restype = C.c_char_p
+        L.ref_mix64.restype = C.c_uint64
+        L.ref_mix64.argtypes = [C.c_uint64]
+        L.ref_derive_seed.restype = C.c_uint64
+        L.ref_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_family.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, u64p]
+        L.ref_partition_of_many.argtypes = [u64p, C.c_uint64, C.c_uint64, C.c_uint32, u32p]
+        L.ref_slot_of_many.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                       u64p, C.c_uint64, C.c_uint64, u64p]
+        L.ref_hierarchical_hash.argtypes = [
+            C.c_uint64, u64p, f32p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_int, C.c_uint32,
+            C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint32, u64p, f32p, u64p, u64p]
+        L.ref_slot_layout.argtypes = [
+            C.c_uint64, u64p, f32p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_int, C.c_uint32,
+            C.c_uint32, C.c_uint64, C.c_uint64, u64p, f32p, u32p, C.POINTER(C.c_int64)]
+        L.ref_to_sparse.restype = C.c_uint64
+        L.ref_to_sparse.argtypes = [f32p, C.c_uint64, u64p, f32p]
+        L.ref_generate.argtypes = [C.c_uint64, C.c_uint32, C.c_double, C.c_double, C.c_double,
+                                   C.c_double, C.c_uint64, u64p, f32p, C.POINTER(C.c_uint64)]
+        L.ref_universe_size.restype = C.c_uint64
+        L.ref_universe_size.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32]
+        L.ref_hash_bitmap_encode.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, u64p,
+                                             f32p, C.c_uint64, u8p, C.POINTER(C.c_uint64),
+                                             C.POINTER(C.c_uint64)]
+        L.ref_hash_bitmap_decode.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, u8p,
+                                             C.c_uint64, C.c_uint64, u64p, f32p,
+                                             C.POINTER(C.c_uint64)]
+        L.ref_bp_sync.argtypes = [
+            C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), u64p, C.c_uint32,
+            C.c_double, C.c_double, C.c_uint32, C.c_uint64, C.c_int, u64p, f32p,
+            C.POINTER(C.c_uint64), u64p, f64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_aggregate.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p),
+                                    C.POINTER(C.c_void_p), u64p, u64p, f32p, C.POINTER(C.c_uint64)]
+        L.ref_bench_step.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), C.c_uint32,
+                                     C.c_double, C.c_double, C.c_uint32, C.c_uint64, C.c_int, f64p,
+                                     C.POINTER(C.c_uint64)]
+
+    def _check(self, rc, what):
+        if rc:
+            raise OracleError(rc, f"{what}: {self.lib.ref_last_message().decode()}",
+                              self.lib.ref_last_partition())
+
+    def mix64(self, x):
+        return self.lib.ref_mix64(x)
+
+    def derive_seed(self, m, s):
+        return self.lib.ref_derive_seed(m, s)
+
+    def family_seeds(self, seed, n, k, worker=None):
+        out = np.zeros(k + 1, np.uint64)
+        self._check(self.lib.ref_family(seed, worker or 0, n, k, int(worker is not None), out),
+                    "family")
+        return [int(x) for x in out]
+
+    def partition_of(self, idx, pseed, n):
+        idx = _u64(idx)
+        out = np.empty(idx.size, np.uint32)
+        self.lib.ref_partition_of_many(idx, idx.size, pseed, n, out)
+        return out
+
+    def slot_of(self, seed, n, k, idx, r1, worker=None):
+        idx = _u64(idx)
+        out = np.empty(idx.size * k, np.uint64)
+        self.lib.ref_slot_of_many(seed, worker or 0, n, k, int(worker is not None), idx, idx.size,
+                                  r1, out)
+        return out.reshape(idx.size, k)
+
+    def hierarchical_hash(self, m, idx, val, seed, n, k, r1, r2, worker=None, lanes=1,
+                          stats=True):
+        idx, val = _u64(idx), _f32(val)
+        oi = np.empty(max(idx.size, 1), np.uint64)
+        ov = np.empty(max(idx.size, 1), np.float32)
+        pc = np.zeros(n, np.uint64)
+        st = np.zeros(k + 1, np.uint64)
+        self._check(self.lib.ref_hierarchical_hash(m, idx, val, idx.size, seed, worker or 0,
+                                                   int(worker is not None), n, k, r1, r2, lanes,
+                                                   oi, ov, pc, st), "hierarchical_hash")
+        offs = np.concatenate([[0], np.cumsum(pc)]).astype(np.int64)
+        return HashResult([oi[offs[p]:offs[p + 1]].copy() for p in range(n)],
+                          [ov[offs[p]:offs[p + 1]].copy() for p in range(n)],
+                          int(st[0]), [int(x) for x in st[1:]])
+
+    def slot_layout(self, m, idx, val, seed, n, k, r1, r2, worker=None):
+        idx, val = _u64(idx), _f32(val)
+        cells = n * (r1 + r2)
+        slots = np.zeros(max(cells, 1), np.uint64)
+        svals = np.zeros(max(cells, 1), np.float32)
+        depth = np.zeros(max(idx.size, 1), np.uint32)
+        ovf = C.c_int64(-1)
+        self._check(self.lib.ref_slot_layout(m, idx, val, idx.size, seed, worker or 0,
+                                             int(worker is not None), n, k, r1, r2, slots, svals,
+                                             depth, C.byref(ovf)), "slot_layout")
+        return slots[:cells], svals[:cells], depth[:idx.size], ovf.value
+
+    def to_sparse(self, dense):
+        dense = _f32(dense)
+        idx = np.empty(max(dense.size, 1), np.uint64)
+        val = np.empty(max(dense.size, 1), np.float32)
+        c = self.lib.ref_to_sparse(dense, dense.size, idx, val)
+        return idx[:c].copy(), val[:c].copy()
+
+    def generate(self, m, nodes, density, omega, seed, hot_fraction=0.125, hot_mass=0.125):
+        z = int(np.ceil(density * m))
+        idx = np.zeros(max(z * nodes, 1), np.uint64)
+        val = np.zeros(max(z * nodes, 1), np.float32)
+        zz = C.c_uint64()
+        self._check(self.lib.ref_generate(m, nodes, density, omega, hot_fraction, hot_mass, seed,
+                                          idx, val, C.byref(zz)), "generate")
+        z = zz.value
+        return [(idx[w * z:(w + 1) * z].copy(), val[w * z:(w + 1) * z].copy())
+                for w in range(nodes)]
+
+    def universe_size(self, m, n, pseed, s):
+        return int(self.lib.ref_universe_size(m, n, pseed, s))
+
+    def hash_bitmap_encode(self, m, n, pseed, s, idx, val):
+        idx, val = _u64(idx), _f32(val)
+        size = self.universe_size(m, n, pseed, s)
+        payload = np.zeros((size + 7) // 8 + 4 * idx.size + 1, np.uint8)
+        bits, plen = C.c_uint64(), C.c_uint64()
+        self._check(self.lib.ref_hash_bitmap_encode(m, n, pseed, s, idx, val, idx.size, payload,
+                                                    C.byref(bits), C.byref(plen)), "encode")
+        return payload[:plen.value].copy(), bits.value
+
+    def hash_bitmap_decode(self, m, n, pseed, s, payload, count):
+        payload = np.ascontiguousarray(payload, np.uint8)
+        idx = np.empty(max(count, 1), np.uint64)
+        val = np.empty(max(count, 1), np.float32)
+        oc = C.c_uint64()
+        self._check(self.lib.ref_hash_bitmap_decode(m, n, pseed, s, payload, payload.size, count,
+                                                    idx, val, C.byref(oc)), "decode")
+        return idx[:oc.value].copy(), val[:oc.value].copy()
+
+    def _ptrs(self, inputs):
+        n = len(inputs)
+        ins = [(_u64(i), _f32(v)) for i, v in inputs]
+        nnz = np.array([i.size for i, _ in ins], np.uint64)
+        ip = (C.c_void_p * n)(*[i.ctypes.data for i, _ in ins])
+        vp = (C.c_void_p * n)(*[v.ctypes.data for _, v in ins])
+        return ins, nnz, ip, vp
+
+    def bp_sync(self, m, inputs, k=3, r1_multiplier=2.0, r2_ratio=0.1, seed=1, lanes=1,
+                retries=0):
+        n = len(inputs)
+        ins, nnz, ip, vp = self._ptrs(inputs)
+        tot = int(nnz.sum())
+        oi = np.empty(max(tot, 1), np.uint64)
+        ov = np.empty(max(tot, 1), np.float32)
+        oc = C.c_uint64()
+        ledger = np.zeros(8 * n, np.uint64)
+        bal = np.zeros(2, np.float64)
+        bv, eq = C.c_int(0), C.c_int(0)
+        self._check(self.lib.ref_bp_sync(n, m, ip, vp, nnz, k, r1_multiplier, r2_ratio, lanes,
+                                         seed, retries, oi, ov, C.byref(oc), ledger, bal,
+                                         C.byref(bv), C.byref(eq)), "bp_sync")
+        assert eq.value == 1
+        c = oc.value
+        return BPResult(oi[:c].copy(), ov[:c].copy(), ledger.reshape(2, 4, n),
+                        (bal[0], bal[1]) if bv.value else None)
+
+    def aggregate(self, m, inputs):
+        ins, nnz, ip, vp = self._ptrs(inputs)
+        tot = int(nnz.sum())
+        oi = np.empty(max(tot, 1), np.uint64)
+        ov = np.empty(max(tot, 1), np.float32)
+        oc = C.c_uint64()
+        self._check(self.lib.ref_aggregate(len(inputs), m, ip, vp, nnz, oi, ov, C.byref(oc)),
+                    "aggregate")
+        return oi[:oc.value].copy(), ov[:oc.value].copy()
+
+    def bench_step(self, m, dense_list, k=3, r1_multiplier=2.0, r2_ratio=0.1, lanes=1, seed=1,
+                   reps=1):
+        n = len(dense_list)
+        ds = [_f32(d) for d in dense_list]
+        dp = (C.c_void_p * n)(*[d.ctypes.data for d in ds])
+        t = np.zeros(3, np.float64)
+        rn = C.c_uint64()
+        self._check(self.lib.ref_bench_step(n, m, dp, k, r1_multiplier, r2_ratio, lanes, seed,
+                                            reps, t, C.byref(rn)), "bench_step")
+        return {"to_sparse_ms": t[0], "sync_ms": t[1], "table_ms": t[2], "result_nnz": rn.value}
+
+
+def c_oracle():
+    return COracle()
+
+
+def ref_oracle():
+    """The compiled reference, or None when oracle/_ref was never built."""
+    return RefOracle() if os.path.exists(REF_SO) else None

@@ -1,0 +1,173 @@
+"""Pin the C restatement (oracle/zen_oracle.c) to the reference's own outputs.
+
+The fixtures in tests/golden/ were produced by oracle/make_golden.py through
+oracle/_ref/libzenref.so -- the unmodified reference headers compiled in
+place.  These tests run on CPU; they are what makes the oracle trustworthy
+before it is used to check the CUDA path.
+"""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import OracleError
+
+U64MAX = 2**64 - 1
+
+
+def test_hash_family_known_answers(co):
+    g = load_golden("hash_kat")
+    for x, y in zip(g["mix_in"], g["mix_out"]):
+        assert co.mix64(int(x)) == int(y)
+    for (a, b), y in zip(g["derive_in"], g["derive_out"]):
+        assert co.derive_seed(int(a), int(b)) == int(y)
+    for row in g["families"]:
+        seed, n, k, worker = (int(v) for v in row[:4])
+        seeds = co.family_seeds(seed, n, k, None if worker == U64MAX else worker)
+        assert seeds == [int(v) for v in row[4:5 + k]]
+    idx = g["part_idx"]
+    for pseed, n in g["part_cases"]:
+        np.testing.assert_array_equal(co.partition_of(idx, int(pseed), int(n)),
+                                      g[f"part_{pseed}_{n}"])
+
+
+def test_slot_hash_known_answers(co):
+    g = load_golden("hash_kat")
+    idx = g["part_idx"][:2048]
+    for (seed, n, k, r1, w) in [(1, 8, 3, 160000, 0), (99, 2, 4, 7, 3), (5, 16, 3, 1, 1)]:
+        fam = co.family(seed, n, k, worker=w)
+        want = g[f"slot_{seed}_{n}_{k}_{r1}_{w}"]
+        got = np.array([[co.slot_of(fam, int(x), r, r1) for r in range(1, k + 1)] for x in idx])
+        np.testing.assert_array_equal(got, want)
+
+
+def _hcases():
+    g = load_golden("hhash")
+    return g, int(g["ncases"][0])
+
+
+def test_hierarchical_hash_layout_stats_parts(co):
+    g, nc = _hcases()
+    saw_fallback = saw_overflow = saw_serial = 0
+    for i in range(nc):
+        p = f"c{i}_"
+        m, seed, worker, n, k, r1, r2 = (int(v) for v in g[p + "meta"])
+        fam = co.family(seed, n, k, worker=None if worker < 0 else worker)
+        idx, val = g[p + "idx"], g[p + "val"]
+        ovf = int(g[p + "overflow"][0])
+        if ovf >= 0:
+            with pytest.raises(OracleError) as e:
+                co.hierarchical_hash(m, idx, val, fam, r1, r2)
+            assert e.value.partition == ovf
+            saw_overflow += 1
+            continue
+        res = co.hierarchical_hash(m, idx, val, fam, r1, r2, layout=True)
+        np.testing.assert_array_equal(res.slots, g[p + "slots"])
+        np.testing.assert_array_equal(res.slot_vals, g[p + "slot_vals"])
+        np.testing.assert_array_equal(res.depth_of, g[p + "depth"])
+        np.testing.assert_array_equal(np.concatenate(res.parts_idx), g[p + "parts_idx"])
+        np.testing.assert_array_equal(np.concatenate(res.parts_val), g[p + "parts_val"])
+        np.testing.assert_array_equal([x.size for x in res.parts_idx], g[p + "part_count"])
+        assert [res.serial_writes] + res.placed_at_depth == list(g[p + "stats"])
+        # a partition used the fallback scan when its serial keys exceed r2
+        part = co.partition_of(idx, fam.partition_seed, n)
+        serial = np.bincount(part[res.depth_of == 0], minlength=n) if idx.size else np.zeros(n)
+        saw_fallback += int((serial > r2).any())
+        saw_serial += int(res.serial_writes > 0)
+    assert saw_overflow >= 2 and saw_fallback >= 1 and saw_serial >= 3
+
+
+def test_to_sparse_golden(co):
+    g = load_golden("to_sparse")
+    for name in ["mixed", "rows", "one", "allnz"]:
+        idx, val = co.to_sparse(g[name + "_dense"])
+        np.testing.assert_array_equal(idx, g[name + "_idx"])
+        np.testing.assert_array_equal(val.view(np.uint32), g[name + "_val"].view(np.uint32))
+
+
+def test_hash_bitmap_codec_golden(co):
+    g = load_golden("codec")
+    seed, bits = (int(v) for v in g["fig7"])
+    u = co.universe(15, 3, seed)
+    payload, b = u.encode(0, np.array([5, 7], np.uint64), np.array([0.3, 0.9], np.float32))
+    assert b == bits and payload[0] & 0b111 == 0b110
+    np.testing.assert_array_equal(payload, g["fig7_payload"])
+    for row in g["universe_sizes"]:
+        m, n, pseed = (int(v) for v in row[:3])
+        if m > 1_000_000:
+            continue
+        u = co.universe(m, n, pseed)
+        assert [u.size(s) for s in range(n)] == [int(v) for v in row[3:3 + n]]
+        assert sum(u.size(s) for s in range(n)) == m  # Σ|I_s| = M (codec_test.cpp:189-203)
+    for i in range(int(g["ncases"][0])):
+        p = f"e{i}_"
+        m, n, pseed, s, bits = (int(v) for v in g[p + "meta"])
+        u = co.universe(m, n, pseed)
+        payload, b = u.encode(s, g[p + "idx"], g[p + "val"])
+        assert b == bits
+        np.testing.assert_array_equal(payload, g[p + "payload"])
+        idx, val = u.decode(s, g[p + "payload"], g[p + "idx"].size)
+        np.testing.assert_array_equal(idx, g[p + "idx"])
+        np.testing.assert_array_equal(val, g[p + "val"])
+
+
+def test_hash_bitmap_rejects_foreign_index_and_bad_payload(co):
+    u = co.universe(100, 4, 9)
+    own0 = set(u.indices(0).tolist())
+    foreign = next(i for i in range(100) if i not in own0)
+    with pytest.raises(OracleError):
+        u.encode(0, np.array([foreign], np.uint64), np.ones(1, np.float32))
+    payload, _ = u.encode(0, u.indices(0)[:2], np.ones(2, np.float32))
+    with pytest.raises(OracleError):
+        u.decode(0, payload[:-1], 2)  # size mismatch (codec.hpp:336-337)
+    with pytest.raises(OracleError):
+        u.decode(0, np.concatenate([payload, np.zeros(4, np.uint8)]), 3)  # popcount mismatch
+
+
+def test_bp_sync_golden(co):
+    g = load_golden("bp")
+    for i in range(int(g["ncases"][0])):
+        p = f"b{i}_"
+        n, m, gseed, seed, k = (int(v) for v in g[p + "meta"])
+        r1m, r2r, _, _ = (float(v) for v in g[p + "params"])
+        ins = [(g[p + f"in{w}_idx"], g[p + f"in{w}_val"]) for w in range(n)]
+        code, part = (int(v) for v in g[p + "error"])
+        if code:
+            with pytest.raises(OracleError) as e:
+                co.bp_sync(m, ins, k=k, r1_multiplier=r1m, r2_ratio=r2r, seed=seed)
+            assert e.value.code == code and e.value.partition == part
+            continue
+        res = co.bp_sync(m, ins, k=k, r1_multiplier=r1m, r2_ratio=r2r, seed=seed)
+        np.testing.assert_array_equal(res.idx, g[p + "idx"])
+        np.testing.assert_array_equal(res.val, g[p + "val"])
+        np.testing.assert_array_equal(res.ledger, g[p + "ledger"])
+        np.testing.assert_allclose(res.balance, g[p + "balance"], rtol=0, atol=0)
+
+
+def test_oracle_matches_live_reference_random(co, ro):
+    """Where the reference is compiled here, cross-check on fresh random inputs too."""
+    rng = np.random.default_rng(99)
+    for trial in range(60):
+        m = int(rng.integers(10, 20000))
+        z = int(rng.integers(0, m // 2 + 1))
+        idx = np.sort(rng.choice(m, z, replace=False)).astype(np.uint64)
+        val = rng.standard_normal(z).astype(np.float32)
+        n, k = int(rng.integers(1, 9)), int(rng.integers(1, 5))
+        seed, w = int(rng.integers(0, 2**62)), int(rng.integers(0, 8))
+        r1 = int(rng.integers(1, 2 * z // n + 3))
+        r2 = int(rng.integers(1, r1 + 3))
+        fam = co.family(seed, n, k, worker=w)
+        slots, svals, depth, ovf = ro.slot_layout(m, idx, val, seed, n, k, r1, r2, worker=w)
+        if ovf >= 0:
+            with pytest.raises(OracleError) as e:
+                co.hierarchical_hash(m, idx, val, fam, r1, r2)
+            assert e.value.partition == ovf
+            continue
+        res = co.hierarchical_hash(m, idx, val, fam, r1, r2, layout=True)
+        np.testing.assert_array_equal(res.slots, slots)
+        np.testing.assert_array_equal(res.depth_of, depth)
+    for n in [2, 5, 8]:
+        ins = ro.generate(30000, n, 0.01, 0.3, 1000 + n)
+        a, b = co.bp_sync(30000, ins, seed=n), ro.bp_sync(30000, ins, seed=n)
+        np.testing.assert_array_equal(a.idx, b.idx)
+        np.testing.assert_array_equal(a.val, b.val)
+        np.testing.assert_array_equal(a.ledger, b.ledger)
