@@ -1,0 +1,41 @@
+# Build of the product library (sm_100a only) and the test-only CPU checkers.
+#   make            -> paper_2309_13254_b200/lib/libzen_b200.so + oracle/
+#   make lib        -> the CUDA library only
+NVCC ?= /usr/local/cuda/bin/nvcc
+CUDA_HOME ?= /usr/local/cuda
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr \
+           -Iinclude -Ipaper_2309_13254_b200/csrc
+CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -Wextra -Iinclude -Ipaper_2309_13254_b200/csrc \
+            -I$(CUDA_HOME)/include
+SRC := paper_2309_13254_b200/csrc
+OBJ := build/obj
+LIB := paper_2309_13254_b200/lib/libzen_b200.so
+CU := $(wildcard $(SRC)/*.cu)
+CUOBJ := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU))
+HDRS := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/zen_b200.h
+
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+
+$(OBJ)/capi.o: $(SRC)/capi.cpp $(HDRS)
+	@mkdir -p $(OBJ)
+	g++ $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(CUOBJ) $(OBJ)/capi.o
+	@mkdir -p $(dir $(LIB))
+	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(CUDA_HOME)/lib64 -lcudart_static -lrt -ldl -lpthread
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all lib oracle clean

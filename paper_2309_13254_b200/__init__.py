@@ -1,0 +1,15 @@
+"""B200-native Balanced-Parallelism sparse gradient synchronisation (Zen, arXiv 2309.13254).
+
+The product is paper_2309_13254_b200/lib/libzen_b200.so (sm_100a kernels + C++
+host) behind the C-ABI in include/zen_b200.h; this package is its Python
+mirror of the reference operator API.
+"""
+from ._lib import EXPORTED, LIB_PATH, STAGE_NAMES, load  # noqa: F401
+from .zen import (  # noqa: F401
+    BalanceDetails, BPSynchronizer, CapacityError, CollisionStats, CudaError, DenseTensor,
+    EmptyTensor, EncodedMessage, Error, HashFamily, HashLayout, HashParams, HashUniverse,
+    HashUniverseTable, IndexOutsideUniverse, MalformedPayload, PartitionedSparseTensor,
+    PeerTimeout, SerialOverflow, SimNet, SparseTensor, SyncOutcome, TrafficReport,
+    UniverseMismatch, WireFormat, aggregate, bp_universe_table, collision_stats, context, decode,
+    derive_seed, encode, hash_memory_layout, hierarchical_hash, imbalance_pull, imbalance_push,
+    partition_of, run_balanced_parallelism, run_bp_with_retry, to_sparse)

@@ -1,0 +1,1449 @@
+// capi.cpp -- C++ host side of the C-ABI (include/zen_b200.h).
+//
+// Owns devices, streams, workspaces and the cross-GPU plumbing; every byte of
+// gradient data is touched only by the sm_100a kernels in k_*.cu.  There is no
+// CPU fallback: a missing or non-sm_100 device is an error.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "zen_b200.h"
+#include "zen_internal.h"
+
+namespace zen {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// extra small kernels (k_util.cu)
+void launch_dump_slots(const unsigned long long* slots, uint64_t cells, uint32_t epoch,
+                       const float* vals, uint64_t* out_slots, float* out_vals,
+                       cudaStream_t stream);
+void launch_meta_depth(const uint32_t* meta, uint64_t count, uint32_t* out, cudaStream_t stream);
+void launch_universe_indices(const OwnWord* own, uint64_t nwords, uint64_t* out,
+                             cudaStream_t stream);
+void launch_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t stream);
+}  // namespace zen
+
+using namespace zen;
+
+namespace {
+
+thread_local std::string t_msg;
+thread_local int64_t t_part = -1;
+thread_local uint64_t t_index = 0;
+
+zen_status fail(zen_status s, const std::string& msg, int64_t part = -1) {
+  t_msg = msg;
+  t_part = part;
+  return s;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      cudaGetLastError();                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? ZEN_E_OOM : ZEN_E_CUDA,             \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+    }                                                                                   \
+  } while (0)
+
+#define CKR(expr)                       \
+  do {                                  \
+    zen_status s_ = (expr);             \
+    if (s_ != ZEN_OK) return s_;        \
+  } while (0)
+
+constexpr uint64_t kG = 0x9e3779b97f4a7c15ULL;
+
+uint64_t h_mix64(uint64_t x) {  // zen/hashing.hpp:18-25
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+uint64_t h_derive(uint64_t m, uint64_t s) {  // zen/hashing.hpp:37-39
+  return h_mix64(m ^ h_mix64(s + 0x5851f42d4c957f2dULL));
+}
+
+DevFamily fold(const zen_hash_family& f) {
+  DevFamily d{};
+  d.pc = kG * (f.partition_seed + 1);
+  for (uint32_t i = 0; i < f.k; ++i) d.sc[i] = kG * (f.slot_seeds[i] + 1);
+  d.n = f.partitions;
+  d.k = f.k;
+  return d;
+}
+
+uint32_t planes_for(uint32_t n) {
+  if (n <= 1) return 0;
+  uint32_t b = 0;
+  while ((1u << b) < n) ++b;
+  return b;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct DevGuard {
+  int prev = 0;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// RAII list of device allocations
+struct DevMem {
+  std::vector<void*> ptrs;
+  ~DevMem() { release(); }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+  template <typename T>
+  zen_status alloc(T** out, size_t count, bool zero = true) {
+    void* p = nullptr;
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    CK(cudaMalloc(&p, bytes));
+    ptrs.push_back(p);
+    if (zero) CK(cudaMemset(p, 0, bytes));
+    *out = static_cast<T*>(p);
+    return ZEN_OK;
+  }
+};
+
+template <typename T>
+zen_status upload(T* d, const T* h, size_t count) {
+  CK(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice));
+  return ZEN_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ ctx ----
+
+struct zen_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+};
+
+extern "C" {
+
+uint32_t zen_abi_version(void) { return ZEN_B200_ABI_VERSION; }
+
+const char* zen_status_string(zen_status s) {
+  switch (s) {
+    case ZEN_OK: return "ok";
+    case ZEN_E_INVALID: return "invalid argument";
+    case ZEN_E_SERIAL_OVERFLOW: return "serial overflow";
+    case ZEN_E_INDEX_OUTSIDE_UNIVERSE: return "index outside universe";
+    case ZEN_E_MALFORMED: return "malformed payload";
+    case ZEN_E_EMPTY: return "empty tensor";
+    case ZEN_E_UNIVERSE_MISMATCH: return "universe mismatch";
+    case ZEN_E_CUDA: return "cuda error";
+    case ZEN_E_PEER: return "peer setup error";
+    case ZEN_E_OOM: return "out of device memory";
+    case ZEN_E_TIMEOUT: return "peer timeout";
+    case ZEN_E_CAPACITY: return "capacity exceeded";
+  }
+  return "unknown";
+}
+const char* zen_last_error_message(void) { return t_msg.c_str(); }
+int64_t zen_last_error_partition(void) { return t_part; }
+uint64_t zen_last_error_index(void) { return t_index; }
+uint64_t zen_kernel_launches(void) { return g_launches.load(); }
+
+uint64_t zen_derive_seed(uint64_t master, uint64_t stream) { return h_derive(master, stream); }
+
+zen_status zen_hash_family_make(uint64_t seed, uint32_t n, uint32_t k, zen_hash_family* out) {
+  // HashFamily::make, zen/hashing.hpp:51-60
+  if (!out) return fail(ZEN_E_INVALID, "null output");
+  if (n == 0) return fail(ZEN_E_INVALID, "hash family needs at least one partition");
+  if (k == 0) return fail(ZEN_E_INVALID, "hash family needs at least one slot hash");
+  if (k > ZEN_MAX_K) return fail(ZEN_E_INVALID, "rehash depth above ZEN_MAX_K");
+  std::memset(out, 0, sizeof(*out));
+  out->partitions = n;
+  out->k = k;
+  out->partition_seed = h_derive(seed, 0);
+  for (uint32_t i = 0; i < k; ++i) out->slot_seeds[i] = h_derive(seed, 1 + i);
+  return ZEN_OK;
+}
+
+zen_status zen_hash_family_make_worker(uint64_t shared, uint32_t worker, uint32_t n, uint32_t k,
+                                       zen_hash_family* out) {
+  // HashFamily::make_worker, zen/hashing.hpp:64-69
+  CKR(zen_hash_family_make(shared, n, k, out));
+  for (uint32_t i = 0; i < k; ++i) out->slot_seeds[i] = h_derive(shared, (uint64_t(worker) + 2) * 1024 + i);
+  return ZEN_OK;
+}
+
+zen_status zen_ctx_create(int device, zen_ctx** out) {
+  if (!out) return fail(ZEN_E_INVALID, "null output");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(ZEN_E_CUDA, "no CUDA device: the zen_b200 path has no CPU fallback");
+  }
+  if (device < 0 || device >= count) return fail(ZEN_E_INVALID, "device ordinal out of range");
+  cudaDeviceProp prop{};
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(ZEN_E_CUDA, std::string("zen_b200 kernels are built for sm_100a; device is ") +
+                                prop.name);
+  auto* c = new zen_ctx();
+  c->device = device;
+  DevGuard g(device);
+  e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(ZEN_E_CUDA, cudaGetErrorString(e));
+  }
+  c->stream = c->own;
+  *out = c;
+  return ZEN_OK;
+}
+
+void zen_ctx_destroy(zen_ctx* c) {
+  if (!c) return;
+  DevGuard g(c->device);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+}
+
+zen_status zen_ctx_set_stream(zen_ctx* c, void* s) {
+  if (!c) return fail(ZEN_E_INVALID, "null ctx");
+  c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+  return ZEN_OK;
+}
+void* zen_ctx_stream(zen_ctx* c) { return c ? (void*)c->stream : nullptr; }
+zen_status zen_ctx_synchronize(zen_ctx* c) {
+  if (!c) return fail(ZEN_E_INVALID, "null ctx");
+  DevGuard g(c->device);
+  CK(cudaStreamSynchronize(c->stream));
+  return ZEN_OK;
+}
+
+// ------------------------------------------------------------ standalone ----
+
+zen_status zen_partition_of(zen_ctx* c, const uint64_t* d_idx, uint64_t count, uint64_t pseed,
+                            uint32_t n, uint32_t* d_out) {
+  if (!c || (!d_idx && count) || (!d_out && count)) return fail(ZEN_E_INVALID, "null argument");
+  if (n == 0) return fail(ZEN_E_INVALID, "partition count must be at least 1");
+  if (!count) return ZEN_OK;
+  DevGuard g(c->device);
+  launch_partition_of(d_idx, count, kG * (pseed + 1), n, d_out, c->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  return ZEN_OK;
+}
+
+zen_status zen_to_sparse(zen_ctx* c, const float* d_dense, uint64_t m, uint64_t* d_idx,
+                         float* d_val, uint64_t capacity, uint64_t* nnz) {
+  if (!c || !d_dense || !nnz) return fail(ZEN_E_INVALID, "null argument");
+  if (m == 0) return fail(ZEN_E_INVALID, "dense tensor must have at least one element");  // tensor.hpp:24
+  DevGuard g(c->device);
+  DevMem mem;
+  const uint64_t ntiles = (m + kExtractTile - 1) / kExtractTile;
+  unsigned long long* status;
+  LookbackCtl* ctl;
+  uint64_t* d_count;
+  uint32_t* err;
+  CKR(mem.alloc(&status, ntiles));
+  CKR(mem.alloc(&ctl, 1));
+  CKR(mem.alloc(&d_count, 1));
+  CKR(mem.alloc(&err, 1));
+  LookbackCtl h{0, 0, 1, 0};
+  CKR(upload(ctl, &h, 1));
+  launch_extract<uint64_t>(d_dense, m, d_idx, d_val, d_count, capacity, status, ctl, err,
+                           c->stream);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(nnz, d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (*nnz > capacity) return fail(ZEN_E_CAPACITY, "output capacity below the non-zero count");
+  return ZEN_OK;
+}
+
+zen_status zen_hierarchical_hash(zen_ctx* c, const uint64_t* d_idx, const float* d_val,
+                                 uint64_t count, uint64_t universe, const zen_hash_family* fam,
+                                 uint64_t r1, uint64_t r2, uint64_t* d_out_idx, float* d_out_val,
+                                 uint64_t* part_count, uint64_t* d_slots, float* d_slot_vals,
+                                 uint32_t* d_depth, zen_collision_stats* stats) {
+  // validation: zen/hashing.hpp:184-187
+  if (!c || !fam || !part_count) return fail(ZEN_E_INVALID, "null argument");
+  const uint32_t n = fam->partitions, k = fam->k;
+  if (n == 0) return fail(ZEN_E_INVALID, "hierarchical hash needs at least one partition");
+  if (n > ZEN_MAX_PARTITIONS) return fail(ZEN_E_INVALID, "partition count above ZEN_MAX_PARTITIONS");
+  if (k == 0 || k > ZEN_MAX_K) return fail(ZEN_E_INVALID, "rehash depth out of range");
+  if (r1 < 1) return fail(ZEN_E_INVALID, "parallel region must have at least one slot");
+  if (universe > kKeyMask) return fail(ZEN_E_INVALID, "universe above 2^40 - 1");
+  if (count && (!d_idx || !d_val || !d_out_idx || !d_out_val))
+    return fail(ZEN_E_INVALID, "null tensor pointer");
+  DevGuard g(c->device);
+  const uint64_t stride = r1 + r2;
+  const uint64_t cells = uint64_t(n) * stride;
+  const uint64_t cap = std::max<uint64_t>(count, 1);
+  const uint64_t ntiles = (cap + kHashTile - 1) / kHashTile;
+  DevMem mem;
+  HashArgs<uint64_t> a{};
+  a.idx = d_idx;
+  a.val = d_val;
+  a.fam = fold(*fam);
+  CKR(mem.alloc(&a.hdr, 1));
+  CKR(mem.alloc(&a.slots, cells, false));
+  CK(cudaMemset(a.slots, 0xFF, std::max<size_t>(cells * 8, 16)));
+  const bool dump = d_slots || d_slot_vals;
+  if (dump) CKR(mem.alloc(&a.slot_vals, cells));
+  CKR(mem.alloc(&a.meta, cap));
+  CKR(mem.alloc(&a.tile_cnt, ntiles * n));
+  CKR(mem.alloc(&a.tile_scnt, ntiles * n));
+  CKR(mem.alloc(&a.load, n));
+  CKR(mem.alloc(&a.sload, n));
+  CKR(mem.alloc(&a.part_off, n));
+  CKR(mem.alloc(&a.fallback, n));
+  CKR(mem.alloc(&a.stats, n * (k + 1)));
+  CKR(mem.alloc(&a.fb_stats, n * (k + 1)));
+  CKR(mem.alloc(&a.stats_out, k + 1));
+  a.dst_table = 0;
+  a.out_idx = d_out_idx;
+  a.out_val = d_out_val;
+  a.cap = cap;
+  a.stride_cap = stride;
+  HashHdr h{};
+  h.count = count;
+  h.r1 = r1;
+  h.r2 = r2;
+  h.derive = 0;
+  h.epoch = 0;
+  h.bad_index = ~0ull;
+  CKR(upload(a.hdr, &h, 1));
+  launch_hash<uint64_t>(a, n, k, c->stream);
+  CK(cudaGetLastError());
+  HashHdr hr{};
+  std::vector<uint32_t> load(n);
+  std::vector<uint64_t> st(k + 1);
+  CK(cudaMemcpyAsync(&hr, a.hdr, sizeof(hr), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(load.data(), a.load, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(st.data(), a.stats_out, (k + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (dump) {
+    launch_dump_slots(a.slots, cells, 1, a.slot_vals, d_slots, d_slot_vals, c->stream);
+  }
+  if (d_depth && count) launch_meta_depth(a.meta, count, d_depth, c->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  if (hr.status & kErrCapacity) return fail(ZEN_E_CAPACITY, "hash workspace capacity");
+  if (hr.ovf_word != ~0ull) {  // zen/hashing.hpp:221-222
+    const uint32_t p = uint32_t(hr.ovf_word & 0xFFFF);
+    return fail(ZEN_E_SERIAL_OVERFLOW,
+                "hash partition " + std::to_string(p) +
+                    " exceeded its slot capacity (r2 too small for this workload)",
+                p);
+  }
+  for (uint32_t p = 0; p < n; ++p) part_count[p] = load[p];
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->k = k;
+    stats->serial_writes = st[0];
+    for (uint32_t d = 0; d < k; ++d) stats->placed_at_depth[d] = st[1 + d];
+  }
+  return ZEN_OK;
+}
+
+}  // extern "C"
+
+// --------------------------------------------------------------- universe ----
+
+struct zen_universe {
+  zen_ctx* ctx = nullptr;
+  uint64_t m = 0;
+  uint32_t n = 0;
+  uint64_t pseed = 0;
+  uint32_t nplanes = 0;
+  uint64_t nwords = 0, nchunks = 0;
+  std::vector<uint64_t> bs;
+  DevMem mem;
+  unsigned long long* planes = nullptr;
+  uint32_t* cprefix = nullptr;
+  uint64_t* d_bs = nullptr;
+  std::vector<OwnWord*> own;
+  std::vector<uint32_t*> sel;
+  std::vector<uint32_t> nq;
+
+  zen_status build() {
+    nplanes = planes_for(n);
+    nwords = (m + 63) / 64;
+    nchunks = (nwords + 31) / 32;
+    CKR(mem.alloc(&planes, std::max<uint64_t>(nwords * nplanes, 1)));
+    CKR(mem.alloc(&cprefix, nchunks * n));
+    CKR(mem.alloc(&d_bs, n));
+    launch_tables_planes(m, n, kG * (pseed + 1), nplanes, planes, cprefix, ctx->stream);
+    launch_tables_scan(cprefix, nchunks, n, d_bs, ctx->stream);
+    CK(cudaGetLastError());
+    bs.resize(n);
+    CK(cudaMemcpyAsync(bs.data(), d_bs, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    own.assign(n, nullptr);
+    sel.assign(n, nullptr);
+    nq.assign(n, 0);
+    return ZEN_OK;
+  }
+  // {mask, rank base} per word and select samples for server s (lazy)
+  zen_status ensure_own(uint32_t s) {
+    if (own[s]) return ZEN_OK;
+    const uint32_t q = uint32_t((bs[s] + kAggChunk - 1) / kAggChunk);
+    nq[s] = q;
+    const uint64_t nsel = std::max<uint32_t>(q, 1) + 1;
+    CKR(mem.alloc(&own[s], nwords));
+    CKR(mem.alloc(&sel[s], nsel, false));
+    std::vector<uint32_t> init(nsel, uint32_t(m));
+    CKR(upload(sel[s], init.data(), nsel));
+    launch_tables_own(m, n, s, nplanes, planes, cprefix, own[s], sel[s], q, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return ZEN_OK;
+  }
+};
+
+namespace {
+
+// Decoder scratch for a set of present servers; shared by the standalone codec
+// and the BP receiver.
+struct Decoder {
+  DevMem mem;
+  uint32_t* bpre = nullptr;
+  uint32_t* bpre_blk = nullptr;
+  uint32_t* blk_start = nullptr;
+  uint64_t* nwords_s = nullptr;
+  uint32_t* popc_total = nullptr;
+  unsigned long long* lb_status = nullptr;
+  LookbackCtl* lb_ctl = nullptr;
+  uint64_t words_stride = 0, blk_stride = 0;
+  uint32_t total_blocks = 0;
+  uint64_t ntiles = 0;
+
+  zen_status init(const zen_universe* u, const std::vector<bool>& present) {
+    const uint32_t n = u->n;
+    std::vector<uint32_t> bstart(n + 1, 0);
+    std::vector<uint64_t> nws(n, 0);
+    for (uint32_t s = 0; s < n; ++s) {
+      nws[s] = (u->bs[s] + 63) / 64;
+      words_stride = std::max(words_stride, nws[s]);
+      const uint32_t nb = present[s] ? uint32_t((nws[s] + kPrefixBlockWords - 1) / kPrefixBlockWords) : 0u;
+      blk_stride = std::max<uint64_t>(blk_stride, nb);
+      bstart[s + 1] = bstart[s] + nb;
+    }
+    total_blocks = bstart[n];
+    words_stride = std::max<uint64_t>(words_stride, 1);
+    blk_stride = std::max<uint64_t>(blk_stride, 1);
+    CKR(mem.alloc(&bpre, words_stride * n));
+    CKR(mem.alloc(&bpre_blk, blk_stride * n));
+    CKR(mem.alloc(&blk_start, n + 1));
+    CKR(mem.alloc(&nwords_s, n));
+    CKR(mem.alloc(&popc_total, n));
+    CKR(upload(blk_start, bstart.data(), n + 1));
+    CKR(upload(nwords_s, nws.data(), n));
+    ntiles = (u->nwords + kDecodeTileWords - 1) / kDecodeTileWords;
+    CKR(mem.alloc(&lb_status, std::max<uint64_t>(ntiles, 1)));
+    CKR(mem.alloc(&lb_ctl, 1));
+    LookbackCtl h{0, 0, 1, 0};
+    CKR(upload(lb_ctl, &h, 1));
+    return ZEN_OK;
+  }
+  void fill(DecodeArgs& a, const zen_universe* u) const {
+    a.n = u->n;
+    a.m = u->m;
+    a.nplanes = u->nplanes;
+    a.planes = u->planes;
+    a.cprefix = u->cprefix;
+    a.bs = u->d_bs;
+    a.bpre = bpre;
+    a.bpre_blk = bpre_blk;
+    a.words_stride = words_stride;
+    a.blk_stride = blk_stride;
+    a.lb_status = lb_status;
+    a.lb_ctl = lb_ctl;
+    a.popc_total = popc_total;
+  }
+  void launch(const DecodeArgs& a, cudaStream_t st) const {
+    launch_decode_parts(a, blk_start, nwords_s, total_blocks, st);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+zen_status zen_universe_create(zen_ctx* c, uint64_t m, uint32_t n, uint64_t pseed,
+                               zen_universe** out) {
+  if (!c || !out) return fail(ZEN_E_INVALID, "null argument");
+  if (n == 0) return fail(ZEN_E_INVALID, "hash universe table needs at least one server");
+  if (n > ZEN_MAX_PARTITIONS) return fail(ZEN_E_INVALID, "server count above ZEN_MAX_PARTITIONS");
+  if (m == 0 || m >= 0xFFFFFFFFull) return fail(ZEN_E_INVALID, "universe must be in [1, 2^32-1)");
+  DevGuard g(c->device);
+  auto u = std::make_unique<zen_universe>();
+  u->ctx = c;
+  u->m = m;
+  u->n = n;
+  u->pseed = pseed;
+  CKR(u->build());
+  *out = u.release();
+  return ZEN_OK;
+}
+
+void zen_universe_destroy(zen_universe* u) {
+  if (!u) return;
+  DevGuard g(u->ctx->device);
+  delete u;
+}
+
+uint64_t zen_universe_size(const zen_universe* u, uint32_t s) {
+  return (u && s < u->n) ? u->bs[s] : 0;
+}
+
+zen_status zen_universe_indices(zen_universe* u, uint32_t s, uint64_t* d_out) {
+  if (!u || s >= u->n) return fail(ZEN_E_INVALID, "bad universe/server");
+  DevGuard g(u->ctx->device);
+  CKR(u->ensure_own(s));
+  launch_universe_indices(u->own[s], u->nwords, d_out, u->ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(u->ctx->stream));
+  return ZEN_OK;
+}
+
+zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d_idx,
+                                  const float* d_val, uint64_t count, uint8_t* d_payload,
+                                  uint64_t* index_bits, uint64_t* payload_bytes) {
+  if (!u || s >= u->n) return fail(ZEN_E_INVALID, "bad universe/server");
+  if (count && (!d_idx || !d_val)) return fail(ZEN_E_INVALID, "null tensor");
+  zen_ctx* c = u->ctx;
+  DevGuard g(c->device);
+  CKR(u->ensure_own(s));
+  const uint64_t bs = u->bs[s];
+  const uint64_t nw = (bs + 63) / 64;
+  const uint64_t bitmap_bytes = (bs + 7) / 8;
+  DevMem mem;
+  uint32_t* keys;
+  unsigned long long* bits;
+  float* vals;
+  HashHdr* hdr;
+  unsigned long long* lbs;
+  LookbackCtl* ctl;
+  uint64_t* aggc;
+  uint64_t* d_cnt;
+  const uint32_t** in_idx;
+  const float** in_val;
+  unsigned long long** dst_bits;
+  float** dst_vals;
+  CKR(mem.alloc(&keys, std::max<uint64_t>(count, 1)));
+  CKR(mem.alloc(&bits, std::max<uint64_t>(nw, 1)));
+  CKR(mem.alloc(&vals, std::max<uint64_t>(count, 1)));
+  CKR(mem.alloc(&hdr, 1));
+  CKR(mem.alloc(&lbs, std::max<uint32_t>(u->nq[s], 1)));
+  CKR(mem.alloc(&ctl, 1));
+  CKR(mem.alloc(&aggc, 1));
+  CKR(mem.alloc(&d_cnt, 1));
+  CKR(mem.alloc(&in_idx, 1));
+  CKR(mem.alloc(&in_val, 1));
+  CKR(mem.alloc(&dst_bits, 1));
+  CKR(mem.alloc(&dst_vals, 1));
+  HashHdr h{};
+  h.bad_index = ~0ull;
+  CKR(upload(hdr, &h, 1));
+  LookbackCtl lc{0, 0, 1, 0};
+  CKR(upload(ctl, &lc, 1));
+  CKR(upload(d_cnt, &count, 1));
+  const uint32_t* ki = keys;
+  const float* vi = d_val;
+  CKR(upload(in_idx, &ki, 1));
+  CKR(upload(in_val, &vi, 1));
+  CKR(upload(dst_bits, &bits, 1));
+  CKR(upload(dst_vals, &vals, 1));
+  if (count) launch_u64_to_u32(d_idx, keys, count, c->stream);
+  AggArgs a{};
+  a.n = 1;
+  a.s = s;
+  a.m = u->m;
+  a.in_idx = in_idx;
+  a.in_val = in_val;
+  a.in_hdr = nullptr;
+  a.in_count = d_cnt;
+  a.own = u->own[s];
+  a.sel = u->sel[s];
+  a.bs = bs;
+  a.ndst = 1;
+  a.dst_bits = dst_bits;
+  a.dst_vals = dst_vals;
+  a.dst_hdr = nullptr;
+  a.val_cap = count;
+  a.lb_status = lbs;
+  a.lb_ctl = ctl;
+  a.agg_count = aggc;
+  a.hdr = hdr;
+  a.wait_push = 0;
+  launch_aggregate(a, c->stream);
+  CK(cudaGetLastError());
+  HashHdr hr{};
+  uint64_t u_count = 0;
+  CK(cudaMemcpyAsync(&hr, hdr, sizeof(hr), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&u_count, aggc, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (hr.status & kErrOutside) {  // universe_positions, zen/codec.hpp:152-154
+    t_index = hr.bad_index;
+    return fail(ZEN_E_INDEX_OUTSIDE_UNIVERSE, "index " + std::to_string(hr.bad_index) +
+                                                  " is not owned by server " + std::to_string(s));
+  }
+  if (u_count != count) return fail(ZEN_E_INVALID, "tensor indices not sorted/unique or >= M");
+  if (bitmap_bytes)
+    CK(cudaMemcpyAsync(d_payload, bits, bitmap_bytes, cudaMemcpyDeviceToDevice, c->stream));
+  if (count)
+    CK(cudaMemcpyAsync(d_payload + bitmap_bytes, vals, count * 4, cudaMemcpyDeviceToDevice,
+                       c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (index_bits) *index_bits = bs;
+  if (payload_bytes) *payload_bytes = bitmap_bytes + 4 * count;
+  return ZEN_OK;
+}
+
+zen_status zen_hash_bitmap_decode(zen_universe* u, uint32_t s, const uint8_t* d_payload,
+                                  uint64_t payload_bytes, uint64_t count, uint64_t* d_idx,
+                                  float* d_val) {
+  if (!u || s >= u->n) return fail(ZEN_E_INVALID, "bad universe/server");
+  if (u->n > ZEN_MAX_WORKERS) return fail(ZEN_E_INVALID, "decode supports n <= ZEN_MAX_WORKERS");
+  zen_ctx* c = u->ctx;
+  DevGuard g(c->device);
+  const uint64_t bs = u->bs[s];
+  const uint64_t nw = (bs + 63) / 64;
+  const uint64_t bitmap_bytes = (bs + 7) / 8;
+  if (payload_bytes != bitmap_bytes + 4 * count)  // zen/codec.hpp:336-337
+    return fail(ZEN_E_MALFORMED, "hash bitmap payload size mismatch");
+  DevMem mem;
+  unsigned long long* bits;
+  float* vals;
+  HashHdr* hdr;
+  uint64_t* out_count;
+  const unsigned long long** bits_t;
+  const float** vals_t;
+  CKR(mem.alloc(&bits, std::max<uint64_t>(nw, 1)));
+  CKR(mem.alloc(&vals, std::max<uint64_t>(count, 1)));
+  CKR(mem.alloc(&hdr, 1));
+  CKR(mem.alloc(&out_count, 1));
+  CKR(mem.alloc(&bits_t, u->n));
+  CKR(mem.alloc(&vals_t, u->n));
+  if (bitmap_bytes)
+    CK(cudaMemcpyAsync(bits, d_payload, bitmap_bytes, cudaMemcpyDeviceToDevice, c->stream));
+  if (count)
+    CK(cudaMemcpyAsync(vals, d_payload + bitmap_bytes, count * 4, cudaMemcpyDeviceToDevice,
+                       c->stream));
+  std::vector<const unsigned long long*> hb(u->n, nullptr);
+  std::vector<const float*> hv(u->n, nullptr);
+  hb[s] = bits;
+  hv[s] = vals;
+  CKR(upload(bits_t, hb.data(), u->n));
+  CKR(upload(vals_t, hv.data(), u->n));
+  std::vector<bool> present(u->n, false);
+  present[s] = true;
+  Decoder dec;
+  CKR(dec.init(u, present));
+  uint64_t* tmp_idx;
+  float* tmp_val;
+  CKR(mem.alloc(&tmp_idx, std::max<uint64_t>(count, 1)));
+  CKR(mem.alloc(&tmp_val, std::max<uint64_t>(count, 1)));
+  DecodeArgs a{};
+  dec.fill(a, u);
+  a.bits = bits_t;
+  a.vals = vals_t;
+  a.pull_hdr = nullptr;
+  a.out_idx = tmp_idx;
+  a.out_val = tmp_val;
+  a.out_count = out_count;
+  a.out_cap = count;
+  a.hdr = hdr;
+  a.wait_pull = 0;
+  dec.launch(a, c->stream);
+  CK(cudaGetLastError());
+  std::vector<uint32_t> popc(u->n);
+  uint64_t oc = 0;
+  CK(cudaMemcpyAsync(popc.data(), dec.popc_total, u->n * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&oc, out_count, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (popc[s] != count || oc != count)  // zen/codec.hpp:342
+    return fail(ZEN_E_MALFORMED, "hash bitmap population mismatch");
+  if (count) {
+    CK(cudaMemcpyAsync(d_idx, tmp_idx, count * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(d_val, tmp_val, count * 4, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return ZEN_OK;
+}
+
+}  // extern "C"
+
+// --------------------------------------------------------------------- BP ----
+
+namespace {
+
+// Byte layout of one node's receive arena (identical on every rank, so peers
+// can compute each other's sub-pointers from the base alone).
+struct ArenaLayout {
+  size_t inbox_idx = 0, inbox_val = 0, push_hdr = 0, pull_hdr = 0;
+  std::vector<size_t> pull_bits, pull_vals;
+  size_t bytes = 0;
+};
+
+ArenaLayout make_layout(uint32_t n, uint64_t cap, const std::vector<uint64_t>& nw,
+                        const std::vector<uint64_t>& valcap, bool with_pull) {
+  ArenaLayout L;
+  size_t off = 0;
+  L.inbox_idx = off;
+  off += align256(size_t(n) * cap * 4);
+  L.inbox_val = off;
+  off += align256(size_t(n) * cap * 4);
+  L.push_hdr = off;
+  off += align256(n * sizeof(PushHdr));
+  L.pull_hdr = off;
+  off += align256(n * sizeof(PullHdr));
+  L.pull_bits.assign(n, 0);
+  L.pull_vals.assign(n, 0);
+  if (with_pull) {
+    for (uint32_t s = 0; s < n; ++s) {
+      L.pull_bits[s] = off;
+      off += align256(std::max<uint64_t>(nw[s], 1) * 8);
+    }
+    for (uint32_t s = 0; s < n; ++s) {
+      L.pull_vals[s] = off;
+      off += align256(std::max<uint64_t>(valcap[s], 1) * 4);
+    }
+  }
+  L.bytes = off;
+  return L;
+}
+
+struct Arena {
+  char* base = nullptr;
+  bool owned = false;
+  uint32_t* inbox_idx(const ArenaLayout& L) const { return (uint32_t*)(base + L.inbox_idx); }
+  float* inbox_val(const ArenaLayout& L) const { return (float*)(base + L.inbox_val); }
+  PushHdr* push_hdr(const ArenaLayout& L) const { return (PushHdr*)(base + L.push_hdr); }
+  PullHdr* pull_hdr(const ArenaLayout& L) const { return (PullHdr*)(base + L.pull_hdr); }
+  unsigned long long* bits(const ArenaLayout& L, uint32_t s) const {
+    return (unsigned long long*)(base + L.pull_bits[s]);
+  }
+  float* vals(const ArenaLayout& L, uint32_t s) const { return (float*)(base + L.pull_vals[s]); }
+};
+
+struct Worker {
+  uint32_t id = 0;
+  uint32_t* keys = nullptr;
+  float* vals = nullptr;
+  HashArgs<uint32_t> a{};
+  unsigned long long* ex_status = nullptr;
+  LookbackCtl* ex_ctl = nullptr;
+  uint32_t epoch_runs = 0;
+  uint64_t h_count = 0;  // staging for sparse inputs (stable address)
+};
+
+struct Server {
+  uint32_t id = 0;
+  AggArgs a{};
+  unsigned long long* lb_status = nullptr;
+  LookbackCtl* lb_ctl = nullptr;
+  uint64_t* agg_count = nullptr;
+};
+
+constexpr int kRing = 1024;
+
+}  // namespace
+
+struct zen_bp {
+  zen_ctx* ctx = nullptr;
+  uint32_t n = 0, rank = 0;
+  bool local = true;
+  uint64_t m = 0, cap = 0, stride_cap = 0;
+  zen_hash_params params{};
+  std::unique_ptr<zen_universe> uni;
+  DevMem mem;
+  std::vector<Worker> workers;
+  std::vector<Server> servers;
+  ArenaLayout L, L0;  // L: with pull (rank / arena 0), L0: inbox only (local arenas 1..n-1)
+  std::vector<Arena> arenas;  // local: n; rank: n (own + mapped peers)
+  bool connected = false;
+  Decoder dec;
+  DecodeArgs da{};
+  uint64_t* out_idx = nullptr;
+  float* out_val = nullptr;
+  uint64_t* out_count = nullptr;
+  uint64_t out_cap = 0;
+  std::vector<uint64_t> nw, valcap;
+  // host view after zen_bp_wait
+  bool collected = false;
+  uint64_t h_result = 0;
+  std::vector<uint64_t> h_counts, h_nnz, h_agg;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // kRing * (ZEN_STAGES + 1)
+  uint64_t ev_head = 0, ev_tail = 0;
+  double stage_ms[ZEN_STAGES] = {0, 0, 0, 0};
+  uint64_t timed = 0;
+  uint32_t kernels_per_sync = 0;
+  // e2e staging
+  std::vector<float*> dense_dev;
+
+  Arena& arena_of(uint32_t r) { return arenas[r]; }
+  const ArenaLayout& layout_of(uint32_t r) const { return (local && r != 0) ? L0 : L; }
+};
+
+namespace {
+
+zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
+  const uint32_t n = bp->n, k = bp->params.rehash_depth;
+  const uint64_t cap = bp->cap;
+  const uint64_t ntiles = (cap + kHashTile - 1) / kHashTile;
+  DevMem& mem = bp->mem;
+  CKR(mem.alloc(&w.keys, cap));
+  CKR(mem.alloc(&w.vals, cap));
+  HashArgs<uint32_t>& a = w.a;
+  a.idx = w.keys;
+  a.val = w.vals;
+  CKR(mem.alloc(&a.hdr, 1));
+  CKR(mem.alloc(&a.slots, size_t(n) * bp->stride_cap, false));
+  CK(cudaMemset(a.slots, 0xFF, size_t(n) * bp->stride_cap * 8));
+  a.slot_vals = nullptr;
+  CKR(mem.alloc(&a.meta, cap));
+  CKR(mem.alloc(&a.tile_cnt, ntiles * n));
+  CKR(mem.alloc(&a.tile_scnt, ntiles * n));
+  CKR(mem.alloc(&a.load, n));
+  CKR(mem.alloc(&a.sload, n));
+  CKR(mem.alloc(&a.part_off, n));
+  CKR(mem.alloc(&a.fallback, n));
+  CKR(mem.alloc(&a.stats, n * (ZEN_MAX_K + 1)));
+  CKR(mem.alloc(&a.fb_stats, n * (ZEN_MAX_K + 1)));
+  CKR(mem.alloc(&a.stats_out, ZEN_MAX_K + 1));
+  a.dst_table = 1;
+  a.cap = cap;
+  a.dst_cap = cap;
+  a.stride_cap = bp->stride_cap;
+  a.me = w.id;
+  uint32_t** dst_idx;
+  float** dst_val;
+  PushHdr** push_hdr;
+  CKR(mem.alloc(&dst_idx, n));
+  CKR(mem.alloc(&dst_val, n));
+  CKR(mem.alloc(&push_hdr, n));
+  a.dst_idx = dst_idx;
+  a.dst_val = dst_val;
+  a.push_hdr = push_hdr;
+  HashHdr h{};
+  h.derive = 1;
+  h.r1_mult = bp->params.r1_multiplier;
+  h.r2_ratio = bp->params.r2_ratio;
+  h.bad_index = ~0ull;
+  CKR(upload(a.hdr, &h, 1));
+  const uint64_t ext_tiles = (bp->m + kExtractTile - 1) / kExtractTile;
+  CKR(mem.alloc(&w.ex_status, ext_tiles));
+  CKR(mem.alloc(&w.ex_ctl, 1));
+  LookbackCtl lc{0, 0, 1, 0};
+  CKR(upload(w.ex_ctl, &lc, 1));
+  zen_hash_family f;
+  CKR(zen_hash_family_make_worker(bp->params.seed, w.id, n, k, &f));
+  a.fam = fold(f);
+  return ZEN_OK;
+}
+
+zen_status bp_alloc_server(zen_bp* bp, Server& s) {
+  const uint32_t n = bp->n;
+  DevMem& mem = bp->mem;
+  CKR(bp->uni->ensure_own(s.id));
+  const uint32_t nq = std::max<uint32_t>(bp->uni->nq[s.id], 1);
+  CKR(mem.alloc(&s.lb_status, nq));
+  CKR(mem.alloc(&s.lb_ctl, 1));
+  LookbackCtl lc{0, 0, 1, 0};
+  CKR(upload(s.lb_ctl, &lc, 1));
+  CKR(mem.alloc(&s.agg_count, 1));
+  AggArgs& a = s.a;
+  a.n = n;
+  a.s = s.id;
+  a.m = bp->m;
+  const uint32_t** in_idx;
+  const float** in_val;
+  const PushHdr** in_hdr;
+  CKR(mem.alloc(&in_idx, n));
+  CKR(mem.alloc(&in_val, n));
+  CKR(mem.alloc(&in_hdr, n));
+  a.in_idx = in_idx;
+  a.in_val = in_val;
+  a.in_hdr = in_hdr;
+  a.in_count = nullptr;
+  a.own = bp->uni->own[s.id];
+  a.sel = bp->uni->sel[s.id];
+  a.bs = bp->uni->bs[s.id];
+  a.ndst = bp->local ? 1 : n;
+  unsigned long long** db;
+  float** dv;
+  PullHdr** dh;
+  CKR(mem.alloc(&db, a.ndst));
+  CKR(mem.alloc(&dv, a.ndst));
+  CKR(mem.alloc(&dh, a.ndst));
+  a.dst_bits = db;
+  a.dst_vals = dv;
+  a.dst_hdr = dh;
+  a.val_cap = bp->valcap[s.id];
+  a.lb_status = s.lb_status;
+  a.lb_ctl = s.lb_ctl;
+  a.agg_count = s.agg_count;
+  a.wait_push = bp->local ? 0 : 1;
+  return ZEN_OK;
+}
+
+// fill the device pointer tables once all arenas are known
+zen_status bp_wire(zen_bp* bp) {
+  const uint32_t n = bp->n;
+  for (auto& w : bp->workers) {
+    std::vector<uint32_t*> di(n);
+    std::vector<float*> dv(n);
+    std::vector<PushHdr*> ph(n);
+    for (uint32_t p = 0; p < n; ++p) {
+      const Arena& A = bp->arena_of(p);
+      const ArenaLayout& L = bp->layout_of(p);
+      di[p] = A.inbox_idx(L) + size_t(w.id) * bp->cap;
+      dv[p] = A.inbox_val(L) + size_t(w.id) * bp->cap;
+      ph[p] = A.push_hdr(L) + w.id;
+    }
+    CKR(upload(const_cast<uint32_t**>(w.a.dst_idx), di.data(), n));
+    CKR(upload(const_cast<float**>(w.a.dst_val), dv.data(), n));
+    CKR(upload(const_cast<PushHdr**>(w.a.push_hdr), ph.data(), n));
+  }
+  for (auto& s : bp->servers) {
+    const Arena& A = bp->arena_of(s.id);
+    const ArenaLayout& L = bp->layout_of(s.id);
+    std::vector<const uint32_t*> ii(n);
+    std::vector<const float*> iv(n);
+    std::vector<const PushHdr*> ih(n);
+    for (uint32_t w = 0; w < n; ++w) {
+      ii[w] = A.inbox_idx(L) + size_t(w) * bp->cap;
+      iv[w] = A.inbox_val(L) + size_t(w) * bp->cap;
+      ih[w] = A.push_hdr(L) + w;
+    }
+    CKR(upload(const_cast<const uint32_t**>(s.a.in_idx), ii.data(), n));
+    CKR(upload(const_cast<const float**>(s.a.in_val), iv.data(), n));
+    CKR(upload(const_cast<const PushHdr**>(s.a.in_hdr), ih.data(), n));
+    std::vector<unsigned long long*> db(s.a.ndst);
+    std::vector<float*> dvv(s.a.ndst);
+    std::vector<PullHdr*> dh(s.a.ndst);
+    for (uint32_t d = 0; d < s.a.ndst; ++d) {
+      const uint32_t r = bp->local ? 0 : d;  // local: one shared pull inbox (arena 0)
+      const Arena& R = bp->arena_of(r);
+      db[d] = R.bits(bp->L, s.id);
+      dvv[d] = R.vals(bp->L, s.id);
+      dh[d] = R.pull_hdr(bp->L) + s.id;
+    }
+    CKR(upload(const_cast<unsigned long long**>(s.a.dst_bits), db.data(), s.a.ndst));
+    CKR(upload(const_cast<float**>(s.a.dst_vals), dvv.data(), s.a.ndst));
+    CKR(upload(const_cast<PullHdr**>(s.a.dst_hdr), dh.data(), s.a.ndst));
+  }
+  // receiver: this node's pull inbox (local: arena 0)
+  const Arena& R = bp->arena_of(bp->local ? 0 : bp->rank);
+  std::vector<const unsigned long long*> hb(n);
+  std::vector<const float*> hv(n);
+  std::vector<const PullHdr*> hh(n);
+  for (uint32_t s = 0; s < n; ++s) {
+    hb[s] = R.bits(bp->L, s);
+    hv[s] = R.vals(bp->L, s);
+    hh[s] = R.pull_hdr(bp->L) + s;
+  }
+  CKR(upload(const_cast<const unsigned long long**>(bp->da.bits), hb.data(), n));
+  CKR(upload(const_cast<const float**>(bp->da.vals), hv.data(), n));
+  CKR(upload(const_cast<const PullHdr**>(bp->da.pull_hdr), hh.data(), n));
+  bp->connected = true;
+  return ZEN_OK;
+}
+
+uint64_t stride_cap_for(const zen_hash_params& p, uint64_t cap, uint32_t n) {
+  uint64_t r1 = (uint64_t)std::ceil(p.r1_multiplier * double(cap) / double(n));
+  r1 = std::max<uint64_t>(r1, 1);
+  uint64_t r2 = (uint64_t)std::ceil(p.r2_ratio * double(r1));
+  r2 = std::max<uint64_t>(r2, 1);
+  return r1 + r2;
+}
+
+}  // namespace
+
+extern "C" {
+
+zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t universe,
+                         uint64_t max_nnz, const zen_hash_params* params, zen_bp** out) {
+  if (!c || !params || !out) return fail(ZEN_E_INVALID, "null argument");
+  if (n == 0 || n > ZEN_MAX_WORKERS) return fail(ZEN_E_INVALID, "worker count must be 1..16");
+  if (rank != ZEN_BP_LOCAL && rank >= n) return fail(ZEN_E_INVALID, "rank out of range");
+  if (universe == 0 || universe >= 0xFFFFFFFFull)
+    return fail(ZEN_E_INVALID, "universe must be in [1, 2^32-1)");
+  if (params->rehash_depth == 0 || params->rehash_depth > ZEN_MAX_K)
+    return fail(ZEN_E_INVALID, "rehash depth out of range");
+  if (!(params->r1_multiplier > 0) || !(params->r2_ratio > 0))
+    return fail(ZEN_E_INVALID, "r1_multiplier and r2_ratio must be positive");
+  DevGuard g(c->device);
+  auto bp = std::make_unique<zen_bp>();
+  bp->ctx = c;
+  bp->n = n;
+  bp->local = rank == ZEN_BP_LOCAL;
+  bp->rank = bp->local ? 0 : rank;
+  bp->m = universe;
+  bp->cap = std::max<uint64_t>(std::min<uint64_t>(max_nnz, universe), 1);
+  bp->params = *params;
+  bp->stride_cap = stride_cap_for(*params, bp->cap, n);
+  // universe tables for (M, n, derive_seed(seed, 0)) -- bp_universe_table, zen/schemes.hpp:332-335
+  bp->uni = std::make_unique<zen_universe>();
+  bp->uni->ctx = c;
+  bp->uni->m = universe;
+  bp->uni->n = n;
+  bp->uni->pseed = h_derive(params->seed, 0);
+  CKR(bp->uni->build());
+  bp->nw.resize(n);
+  bp->valcap.resize(n);
+  for (uint32_t s = 0; s < n; ++s) {
+    bp->nw[s] = (bp->uni->bs[s] + 63) / 64;
+    bp->valcap[s] = std::min<uint64_t>(bp->uni->bs[s], uint64_t(n) * bp->cap);
+  }
+  bp->L = make_layout(n, bp->cap, bp->nw, bp->valcap, true);
+  bp->L0 = make_layout(n, bp->cap, bp->nw, bp->valcap, false);
+  const uint32_t nlocal = bp->local ? n : 1;
+  for (uint32_t i = 0; i < nlocal; ++i) {
+    Worker w;
+    w.id = bp->local ? i : bp->rank;
+    bp->workers.push_back(w);
+    Server s;
+    s.id = w.id;
+    bp->servers.push_back(s);
+  }
+  for (auto& w : bp->workers) CKR(bp_alloc_worker(bp.get(), w));
+  for (auto& s : bp->servers) CKR(bp_alloc_server(bp.get(), s));
+  // arenas
+  bp->arenas.assign(n, Arena{});
+  for (uint32_t r = 0; r < n; ++r) {
+    if (!bp->local && r != bp->rank) continue;
+    const ArenaLayout& L = bp->layout_of(r);
+    void* p = nullptr;
+    CK(cudaMalloc(&p, L.bytes));
+    CK(cudaMemset(p, 0, L.bytes));
+    bp->arenas[r].base = (char*)p;
+    bp->arenas[r].owned = true;
+  }
+  // receiver
+  std::vector<bool> present(n, true);
+  CKR(bp->dec.init(bp->uni.get(), present));
+  bp->out_cap = std::min<uint64_t>(universe, uint64_t(n) * bp->cap);
+  CKR(bp->mem.alloc(&bp->out_idx, bp->out_cap));
+  CKR(bp->mem.alloc(&bp->out_val, bp->out_cap));
+  CKR(bp->mem.alloc(&bp->out_count, 1));
+  DecodeArgs& da = bp->da;
+  bp->dec.fill(da, bp->uni.get());
+  const unsigned long long** bits_t;
+  const float** vals_t;
+  const PullHdr** ph_t;
+  CKR(bp->mem.alloc(&bits_t, n));
+  CKR(bp->mem.alloc(&vals_t, n));
+  CKR(bp->mem.alloc(&ph_t, n));
+  da.bits = bits_t;
+  da.vals = vals_t;
+  da.pull_hdr = ph_t;
+  da.out_idx = bp->out_idx;
+  da.out_val = bp->out_val;
+  da.out_count = bp->out_count;
+  da.out_cap = bp->out_cap;
+  da.hdr = bp->workers[0].a.hdr;
+  da.wait_pull = bp->local ? 0 : 1;
+  for (auto& s : bp->servers) {
+    const Worker* w = nullptr;
+    for (auto& ww : bp->workers)
+      if (ww.id == s.id) w = &ww;
+    s.a.hdr = w->a.hdr;
+  }
+  if (bp->local || n == 1) CKR(bp_wire(bp.get()));
+  CK(cudaDeviceSynchronize());
+  *out = bp.release();
+  return ZEN_OK;
+}
+
+void zen_bp_destroy(zen_bp* bp) {
+  if (!bp) return;
+  DevGuard g(bp->ctx->device);
+  cudaDeviceSynchronize();
+  for (uint32_t r = 0; r < bp->arenas.size(); ++r) {
+    if (!bp->arenas[r].base) continue;
+    if (bp->arenas[r].owned)
+      cudaFree(bp->arenas[r].base);
+    else
+      cudaIpcCloseMemHandle(bp->arenas[r].base);
+  }
+  for (auto e : bp->ev) cudaEventDestroy(e);
+  for (auto p : bp->dense_dev) cudaFree(p);
+  delete bp;
+}
+
+zen_status zen_bp_set_params(zen_bp* bp, const zen_hash_params* p) {
+  if (!bp || !p) return fail(ZEN_E_INVALID, "null argument");
+  if (p->rehash_depth == 0 || p->rehash_depth > ZEN_MAX_K)
+    return fail(ZEN_E_INVALID, "rehash depth out of range");
+  if (p->seed != bp->params.seed) return fail(ZEN_E_INVALID, "changing the seed needs a new zen_bp");
+  DevGuard g(bp->ctx->device);
+  CK(cudaStreamSynchronize(bp->ctx->stream));
+  bp->params = *p;
+  const uint64_t sc = stride_cap_for(*p, bp->cap, bp->n);
+  for (auto& w : bp->workers) {
+    if (sc > bp->stride_cap) {
+      unsigned long long* slots;
+      CKR(bp->mem.alloc(&slots, size_t(bp->n) * sc, false));
+      CK(cudaMemset(slots, 0xFF, size_t(bp->n) * sc * 8));
+      w.a.slots = slots;
+      w.a.stride_cap = sc;
+      uint32_t zero = 0;
+      CK(cudaMemcpy(&w.a.hdr->epoch, &zero, 4, cudaMemcpyHostToDevice));
+      w.epoch_runs = 0;
+    }
+    CK(cudaMemcpy(&w.a.hdr->r1_mult, &p->r1_multiplier, 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(&w.a.hdr->r2_ratio, &p->r2_ratio, 8, cudaMemcpyHostToDevice));
+    zen_hash_family f;
+    CKR(zen_hash_family_make_worker(p->seed, w.id, bp->n, p->rehash_depth, &f));
+    w.a.fam = fold(f);
+  }
+  bp->stride_cap = std::max(bp->stride_cap, sc);
+  return ZEN_OK;
+}
+
+zen_status zen_bp_ipc_handle(zen_bp* bp, void* out) {
+  if (!bp || !out) return fail(ZEN_E_INVALID, "null argument");
+  if (bp->local) return fail(ZEN_E_INVALID, "local-mode synchroniser has no IPC handle");
+  DevGuard g(bp->ctx->device);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, bp->arenas[bp->rank].base));
+  std::memcpy(out, &h, sizeof(h));
+  return ZEN_OK;
+}
+
+zen_status zen_bp_connect(zen_bp* bp, const void* handles) {
+  if (!bp || !handles) return fail(ZEN_E_INVALID, "null argument");
+  if (bp->local) return ZEN_OK;
+  DevGuard g(bp->ctx->device);
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (uint32_t r = 0; r < bp->n; ++r) {
+    if (r == bp->rank || bp->arenas[r].base) continue;
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ZEN_E_PEER, std::string("cudaIpcOpenMemHandle(rank ") + std::to_string(r) +
+                                  "): " + cudaGetErrorString(e));
+    }
+    bp->arenas[r].base = (char*)p;
+    bp->arenas[r].owned = false;
+  }
+  CKR(bp_wire(bp));
+  CK(cudaDeviceSynchronize());
+  return ZEN_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+void record(zen_bp* bp, int stage) {
+  if (!bp->timing) return;
+  const uint64_t slot = bp->ev_head % kRing;
+  cudaEventRecord(bp->ev[slot * (ZEN_STAGES + 1) + stage], bp->ctx->stream);
+}
+
+zen_status bp_run(zen_bp* bp, bool from_dense, const float* const* dense) {
+  if (!bp->connected) return fail(ZEN_E_PEER, "zen_bp_connect has not been called");
+  DevGuard g(bp->ctx->device);
+  cudaStream_t st = bp->ctx->stream;
+  const uint64_t before = g_launches.load();
+  bp->collected = false;
+  if (bp->timing && bp->ev_head - bp->ev_tail >= (uint64_t)kRing)
+    return fail(ZEN_E_INVALID, "timing ring full: call zen_bp_stage_times");
+  record(bp, 0);
+  if (from_dense) {
+    for (size_t i = 0; i < bp->workers.size(); ++i) {
+      Worker& w = bp->workers[i];
+      launch_extract<uint32_t>(dense[i], bp->m, w.keys, w.vals, &w.a.hdr->count, bp->cap,
+                               w.ex_status, w.ex_ctl, &w.a.hdr->status, st);
+    }
+  }
+  record(bp, 1);
+  for (auto& w : bp->workers) {
+    if (++w.epoch_runs >= 0xFFFFF0u) {  // epoch wrap: refill the hash memory once
+      launch_fill_u64(w.a.slots, size_t(bp->n) * w.a.stride_cap, ~0ull, st);
+      CK(cudaMemsetAsync(&w.a.hdr->epoch, 0, 4, st));
+      w.epoch_runs = 1;
+    }
+    launch_hash<uint32_t>(w.a, bp->n, bp->params.rehash_depth, st);
+  }
+  record(bp, 2);
+  for (auto& s : bp->servers) launch_aggregate(s.a, st);
+  record(bp, 3);
+  bp->dec.launch(bp->da, st);
+  record(bp, 4);
+  CK(cudaGetLastError());
+  if (bp->timing) ++bp->ev_head;
+  bp->kernels_per_sync = uint32_t(g_launches.load() - before);
+  return ZEN_OK;
+}
+
+zen_status bp_collect(zen_bp* bp) {
+  if (bp->collected) return ZEN_OK;
+  const uint32_t n = bp->n;
+  cudaStream_t st = bp->ctx->stream;
+  const uint32_t me = bp->local ? 0 : bp->rank;
+  const Arena& A = bp->arena_of(me);
+  std::vector<PushHdr> ph(n);
+  std::vector<PullHdr> pl(n);
+  CK(cudaMemcpyAsync(ph.data(), A.push_hdr(bp->L), n * sizeof(PushHdr), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(pl.data(), A.pull_hdr(bp->L), n * sizeof(PullHdr), cudaMemcpyDeviceToHost, st));
+  std::vector<HashHdr> hh(bp->workers.size());
+  for (size_t i = 0; i < bp->workers.size(); ++i)
+    CK(cudaMemcpyAsync(&hh[i], bp->workers[i].a.hdr, sizeof(HashHdr), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&bp->h_result, bp->out_count, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  uint32_t status = 0;
+  for (auto& h : hh) status |= h.status;
+  for (uint32_t w = 0; w < n; ++w) status |= ph[w].status | pl[w].status;
+  if (status) {  // sticky device errors are reported once, then cleared
+    for (auto& w : bp->workers) CK(cudaMemsetAsync(&w.a.hdr->status, 0, 4, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  if (status & kErrTimeout) return fail(ZEN_E_TIMEOUT, "a peer never signalled (check that every rank calls sync)");
+  if (status & kErrCapacity) return fail(ZEN_E_CAPACITY, "nnz above the max_nnz the synchroniser was created with");
+  bp->h_counts.assign(size_t(n) * n, 0);
+  bp->h_nnz.assign(n, 0);
+  bp->h_agg.assign(n, 0);
+  for (uint32_t w = 0; w < n; ++w) {
+    for (uint32_t s = 0; s < n; ++s) bp->h_counts[size_t(w) * n + s] = ph[w].counts[s];
+    bp->h_nnz[w] = ph[w].nnz;
+    bp->h_agg[w] = pl[w].agg_count;
+  }
+  for (uint32_t w = 0; w < n; ++w) {  // run_balanced_parallelism throws at the first worker
+    if (ph[w].ovf_word != ~0ull) {
+      const uint32_t p = uint32_t(ph[w].ovf_word & 0xFFFF);
+      return fail(ZEN_E_SERIAL_OVERFLOW,
+                  "hash partition " + std::to_string(p) +
+                      " exceeded its slot capacity (r2 too small for this workload)",
+                  p);
+    }
+  }
+  if (status & kErrOutside) return fail(ZEN_E_INDEX_OUTSIDE_UNIVERSE, "index outside universe");
+  if (bp->h_result > bp->out_cap) return fail(ZEN_E_CAPACITY, "result above capacity");
+  bp->collected = true;
+  return ZEN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+zen_status zen_bp_sync_dense(zen_bp* bp, const float* const* d_dense) {
+  if (!bp || !d_dense) return fail(ZEN_E_INVALID, "null argument");
+  for (size_t i = 0; i < bp->workers.size(); ++i)
+    if (!d_dense[i]) return fail(ZEN_E_INVALID, "null dense gradient");
+  return bp_run(bp, true, d_dense);
+}
+
+zen_status zen_bp_sync_sparse(zen_bp* bp, const uint64_t* const* d_idx, const float* const* d_val,
+                              const uint64_t* nnz) {
+  if (!bp || !d_idx || !d_val || !nnz) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  cudaStream_t st = bp->ctx->stream;
+  for (size_t i = 0; i < bp->workers.size(); ++i) {
+    Worker& w = bp->workers[i];
+    if (nnz[i] > bp->cap) return fail(ZEN_E_CAPACITY, "nnz above max_nnz");
+    w.h_count = nnz[i];
+    if (nnz[i]) {
+      launch_u64_to_u32(d_idx[i], w.keys, nnz[i], st);
+      CK(cudaMemcpyAsync(w.vals, d_val[i], nnz[i] * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaMemcpyAsync(&w.a.hdr->count, &w.h_count, 8, cudaMemcpyHostToDevice, st));
+  }
+  return bp_run(bp, false, nullptr);
+}
+
+zen_status zen_bp_wait(zen_bp* bp) {
+  if (!bp) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  return bp_collect(bp);
+}
+
+zen_status zen_bp_result(zen_bp* bp, const uint64_t** d_idx, const float** d_val,
+                         uint64_t* count) {
+  if (!bp) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  CKR(bp_collect(bp));
+  if (d_idx) *d_idx = bp->out_idx;
+  if (d_val) *d_val = bp->out_val;
+  if (count) *count = bp->h_result;
+  return ZEN_OK;
+}
+
+zen_status zen_bp_copy_result(zen_bp* bp, uint64_t* d_idx, float* d_val, uint64_t capacity,
+                              uint64_t* count) {
+  if (!bp || !count) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  CKR(bp_collect(bp));
+  *count = bp->h_result;
+  if (bp->h_result > capacity) return fail(ZEN_E_CAPACITY, "result buffer too small");
+  cudaStream_t st = bp->ctx->stream;
+  if (bp->h_result) {
+    CK(cudaMemcpyAsync(d_idx, bp->out_idx, bp->h_result * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(d_val, bp->out_val, bp->h_result * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return ZEN_OK;
+}
+
+zen_status zen_bp_traffic(zen_bp* bp, uint64_t* ledger, uint64_t* counts, uint64_t* agg) {
+  if (!bp) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  CKR(bp_collect(bp));
+  const uint32_t n = bp->n;
+  if (counts) std::memcpy(counts, bp->h_counts.data(), size_t(n) * n * 8);
+  if (agg) std::memcpy(agg, bp->h_agg.data(), n * 8);
+  if (ledger) {  // the SimNet ledger of run_balanced_parallelism, zen/schemes.hpp:369-372, :386-388
+    std::memset(ledger, 0, sizeof(uint64_t) * 8 * n);
+    auto at = [&](int st, int f, uint32_t node) -> uint64_t& { return ledger[(st * 4 + f) * n + node]; };
+    for (uint32_t w = 0; w < n; ++w)
+      for (uint32_t s = 0; s < n; ++s) {
+        const uint64_t c = bp->h_counts[size_t(w) * n + s];
+        if (s == w || c == 0) continue;
+        at(0, 0, w) += 96 * c;  // COO: 64-bit index + 32-bit value (zen/codec.hpp:186-189)
+        at(0, 1, s) += 96 * c;
+        at(0, 2, s) += 64 * c;
+        at(0, 3, s) += 32 * c;
+      }
+    for (uint32_t s = 0; s < n; ++s) {
+      const uint64_t ib = bp->uni->bs[s], vb = 32 * bp->h_agg[s];  // codec.hpp:202-207
+      for (uint32_t w = 0; w < n; ++w) {
+        if (w == s) continue;
+        at(1, 0, s) += ib + vb;
+        at(1, 1, w) += ib + vb;
+        at(1, 2, w) += ib;
+        at(1, 3, w) += vb;
+      }
+    }
+  }
+  return ZEN_OK;
+}
+
+zen_status zen_bp_balance(zen_bp* bp, double* push, double* pull, int* valid) {
+  if (!bp) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  CKR(bp_collect(bp));
+  const uint32_t n = bp->n;
+  bool all = true;
+  for (uint32_t w = 0; w < n; ++w) all = all && bp->h_nnz[w] > 0;
+  if (valid) *valid = all ? 1 : 0;
+  if (!all) return ZEN_OK;
+  double worst = 0.0;  // imbalance_push, zen/hashing.hpp:296-308
+  for (uint32_t w = 0; w < n; ++w)
+    for (uint32_t s = 0; s < n; ++s)
+      worst = std::max(worst, double(n) * double(bp->h_counts[size_t(w) * n + s]) / double(bp->h_nnz[w]));
+  if (push) *push = worst;
+  uint64_t uni = 0;  // imbalance_pull, zen/hashing.hpp:311-320
+  for (uint32_t s = 0; s < n; ++s) uni += bp->h_agg[s];
+  double wp = 0.0;
+  for (uint32_t s = 0; s < n; ++s) wp = std::max(wp, double(n) * double(bp->h_agg[s]) / double(uni));
+  if (pull) *pull = wp;
+  return ZEN_OK;
+}
+
+zen_status zen_bp_collision_stats(zen_bp* bp, uint32_t worker, zen_collision_stats* out) {
+  if (!bp || !out) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  CKR(bp_collect(bp));
+  for (auto& w : bp->workers) {
+    if (w.id != worker) continue;
+    const uint32_t k = bp->params.rehash_depth;
+    std::vector<uint64_t> st(k + 1);
+    CK(cudaMemcpy(st.data(), w.a.stats_out, (k + 1) * 8, cudaMemcpyDeviceToHost));
+    std::memset(out, 0, sizeof(*out));
+    out->k = k;
+    out->serial_writes = st[0];
+    for (uint32_t d = 0; d < k; ++d) out->placed_at_depth[d] = st[1 + d];
+    return ZEN_OK;
+  }
+  return fail(ZEN_E_INVALID, "worker not hosted by this synchroniser");
+}
+
+zen_status zen_bp_enable_timing(zen_bp* bp, int on) {
+  if (!bp) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  if (on && bp->ev.empty()) {
+    bp->ev.resize(size_t(kRing) * (ZEN_STAGES + 1));
+    for (auto& e : bp->ev) CK(cudaEventCreate(&e));
+  }
+  bp->timing = on != 0;
+  return ZEN_OK;
+}
+
+zen_status zen_bp_stage_times(zen_bp* bp, double* ms, uint64_t* syncs) {
+  if (!bp) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  CK(cudaStreamSynchronize(bp->ctx->stream));
+  for (; bp->ev_tail < bp->ev_head; ++bp->ev_tail) {
+    const uint64_t slot = bp->ev_tail % kRing;
+    for (uint32_t s = 0; s < ZEN_STAGES; ++s) {
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, bp->ev[slot * (ZEN_STAGES + 1) + s],
+                              bp->ev[slot * (ZEN_STAGES + 1) + s + 1]));
+      bp->stage_ms[s] += t;
+    }
+    ++bp->timed;
+  }
+  for (uint32_t s = 0; s < ZEN_STAGES; ++s) {
+    if (ms) ms[s] = bp->stage_ms[s];
+    bp->stage_ms[s] = 0;
+  }
+  if (syncs) *syncs = bp->timed;
+  bp->timed = 0;
+  return ZEN_OK;
+}
+
+uint32_t zen_bp_kernels_per_sync(const zen_bp* bp) { return bp ? bp->kernels_per_sync : 0; }
+
+zen_status zen_bp_sync_host(zen_bp* bp, const float* const* h_dense, uint64_t* h_idx,
+                            float* h_val, uint64_t capacity, uint64_t* count) {
+  if (!bp || !h_dense || !count) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  cudaStream_t st = bp->ctx->stream;
+  if (bp->dense_dev.empty()) {
+    for (size_t i = 0; i < bp->workers.size(); ++i) {
+      void* p = nullptr;
+      CK(cudaMalloc(&p, bp->m * 4));
+      bp->dense_dev.push_back((float*)p);
+    }
+  }
+  for (size_t i = 0; i < bp->workers.size(); ++i)
+    CK(cudaMemcpyAsync(bp->dense_dev[i], h_dense[i], bp->m * 4, cudaMemcpyHostToDevice, st));
+  CKR(bp_run(bp, true, bp->dense_dev.data()));
+  CKR(bp_collect(bp));
+  *count = bp->h_result;
+  if (bp->h_result > capacity) return fail(ZEN_E_CAPACITY, "host result buffer too small");
+  if (bp->h_result) {
+    CK(cudaMemcpyAsync(h_idx, bp->out_idx, bp->h_result * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_val, bp->out_val, bp->h_result * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return ZEN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// k_util.cu -- small device helpers behind the standalone C-ABI operators:
+// HashMemory dumps (reference 0 = empty sentinel), CollisionStats depths, and
+// the materialised universe list I_s.
+#include "zen_common.cuh"
+
+namespace zen {
+extern void count_launch();
+namespace {
+
+using namespace zen_dev;
+
+__global__ void k_dump_slots(const unsigned long long* __restrict__ slots, uint64_t cells,
+                             uint64_t ew, const float* __restrict__ vals,
+                             uint64_t* __restrict__ out_slots, float* __restrict__ out_vals) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < cells;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long w = slots[c];
+    const bool live = (w & ~kKeyMask) == ew;
+    if (out_slots) out_slots[c] = live ? (w & kKeyMask) : 0ull;  // index+1, 0 = empty
+    if (out_vals) out_vals[c] = live ? vals[c] : 0.0f;
+  }
+}
+
+__global__ void k_meta_depth(const uint32_t* __restrict__ meta, uint64_t count,
+                             uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = meta[i] >> 16;
+}
+
+__global__ void k_universe_indices(const OwnWord* __restrict__ own, uint64_t nwords,
+                                   uint64_t* __restrict__ out) {
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    const OwnWord o = own[w];
+    uint64_t m = o.mask;
+    uint64_t pos = o.prefix;
+    while (m) {
+      const uint32_t b = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      out[pos++] = w * 64 + b;
+    }
+  }
+}
+
+__global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
+                             uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+inline unsigned grid_for(uint64_t work) {
+  uint64_t g = (work + 255) / 256;
+  if (g < 1) g = 1;
+  return (unsigned)(g < 148 * 8 ? g : 148 * 8);
+}
+
+}  // namespace
+
+void launch_dump_slots(const unsigned long long* slots, uint64_t cells, uint32_t epoch,
+                       const float* vals, uint64_t* out_slots, float* out_vals,
+                       cudaStream_t stream) {
+  const uint64_t ew = (uint64_t)(0xFFFFFFu - (epoch & 0xFFFFFFu)) << kKeyBits;
+  k_dump_slots<<<grid_for(cells), 256, 0, stream>>>(slots, cells, ew, vals, out_slots, out_vals);
+  count_launch();
+}
+
+void launch_meta_depth(const uint32_t* meta, uint64_t count, uint32_t* out, cudaStream_t stream) {
+  k_meta_depth<<<grid_for(count), 256, 0, stream>>>(meta, count, out);
+  count_launch();
+}
+
+void launch_universe_indices(const OwnWord* own, uint64_t nwords, uint64_t* out,
+                             cudaStream_t stream) {
+  k_universe_indices<<<grid_for(nwords), 256, 0, stream>>>(own, nwords, out);
+  count_launch();
+}
+
+void launch_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t stream) {
+  k_u32_to_u64<<<grid_for(n), 256, 0, stream>>>(in, out, n);
+  count_launch();
+}
+
+}  // namespace zen

@@ -1,0 +1,248 @@
+// zen_common.cuh -- device building blocks shared by the sm_100a kernels.
+//
+// * the reference hash family (zen/hashing.hpp:18-88), bit-exact on device;
+// * warp/block scans and the decoupled look-back used by every stream
+//   compaction on the path (extraction, aggregate+encode, decode);
+// * system-scope acquire/release helpers for the NVLink peer flags.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "zen_internal.h"
+
+namespace zen_dev {
+
+// ---- hash family: zen/hashing.hpp:18-39 -----------------------------------
+// mix64 is the splitmix64 finalizer; seeded_hash(x, s) = mix64(x + G*(s+1))
+// with wrapping u64 arithmetic, so the per-seed constant G*(s+1) is folded on
+// the host (DevFamily.pc / .sc) and the device does one add + mix per hash.
+// map_to_range(h, r) = (u128(h) * r) >> 64 is exactly __umul64hi(h, r).
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+
+// key = index + 1 (zen/hashing.hpp:44-45, :73-76, :79-81)
+__device__ __forceinline__ uint32_t part_of(const zen::DevFamily& f, uint64_t key) {
+  return (uint32_t)__umul64hi(mix64(key + f.pc), (uint64_t)f.n);
+}
+__device__ __forceinline__ uint64_t slot_of(const zen::DevFamily& f, uint64_t key, uint32_t t,
+                                            uint64_t r1) {  // t is 0-based (round t+1)
+  return __umul64hi(mix64(key + f.sc[t]), r1);
+}
+__device__ __forceinline__ uint32_t part_of_seed(uint64_t pc, uint32_t n, uint64_t key) {
+  return (uint32_t)__umul64hi(mix64(key + pc), (uint64_t)n);
+}
+
+// ---- bit helpers ------------------------------------------------------------
+__device__ __forceinline__ uint64_t lowmask64(uint32_t b) {  // b in [0, 64]
+  return b >= 64 ? ~0ull : ((1ull << b) - 1ull);
+}
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+// position of the (q+1)-th set bit of a 64-bit mask (q < popc(mask))
+__device__ __forceinline__ uint32_t select64(uint64_t mask, uint32_t q) {
+  const uint32_t lo = (uint32_t)mask, hi = (uint32_t)(mask >> 32);
+  const uint32_t cl = __popc(lo);
+  if (q < cl) return __fns(lo, 0, (int)q + 1);
+  return 32 + __fns(hi, 0, (int)(q - cl) + 1);
+}
+// software pdep: deposit the low popc(mask) bits of src into mask's set bits,
+// iterating only over the set bits of src.
+__device__ __forceinline__ uint64_t deposit64(uint64_t src, uint64_t mask) {
+  uint64_t r = 0;
+  while (src) {
+    const uint32_t q = __ffsll((long long)src) - 1;
+    src &= src - 1;
+    r |= 1ull << select64(mask, q);
+  }
+  return r;
+}
+
+// ---- scans ------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_sum(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane_id() >= (uint32_t)o) v += u;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan (blockDim multiple of 32, <= 1024). `smem` needs
+// 33 slots. Returns the exclusive prefix; *total receives the block sum.
+template <typename T>
+__device__ __forceinline__ T block_exclusive_sum(T v, T* smem, T* total) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T inc = warp_inclusive_sum(v);
+  if (lane == 31) smem[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T s = lane < nw ? smem[lane] : T(0);
+    T si = warp_inclusive_sum(s);
+    if (lane < nw) smem[lane] = si - s;
+    if (lane == nw - 1) smem[32] = si;
+  }
+  __syncthreads();
+  T r = smem[warp] + inc - v;
+  *total = smem[32];
+  __syncthreads();
+  return r;
+}
+
+// ---- decoupled look-back ----------------------------------------------------
+// Status word per tile: [63:40] launch tag (24 bits), [39:38] flag, [37:0] value.
+// Tags come from a per-kernel control block {ticket, done, tag} that the last
+// block of every launch advances, so no memset is needed between launches and
+// the whole sequence stays CUDA-graph replayable.
+constexpr uint64_t LB_FLAG_AGG = 1ull, LB_FLAG_PRE = 2ull;
+constexpr uint64_t LB_VAL_MASK = (1ull << 38) - 1ull;
+
+__device__ __forceinline__ uint64_t lb_pack(uint32_t tag, uint64_t flag, uint64_t v) {
+  return ((uint64_t)(tag & 0xFFFFFFu) << 40) | (flag << 38) | (v & LB_VAL_MASK);
+}
+__device__ __forceinline__ uint64_t ld_relaxed_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Called by every thread of warp 0 of the tile's block after the block knows
+// its aggregate; returns the exclusive prefix of the tile (same on all lanes).
+__device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, uint32_t tile,
+                                                  uint32_t tag, uint64_t aggregate) {
+  const uint32_t lane = lane_id();
+  if (tile == 0) {
+    if (lane == 0) {
+      __threadfence();
+      st_relaxed_gpu(status, lb_pack(tag, LB_FLAG_PRE, aggregate));
+    }
+    return 0;
+  }
+  if (lane == 0) {
+    __threadfence();
+    st_relaxed_gpu(status + tile, lb_pack(tag, LB_FLAG_AGG, aggregate));
+  }
+  uint64_t exclusive = 0;
+  int64_t base = (int64_t)tile - 1;
+  const uint64_t tagbits = (uint64_t)(tag & 0xFFFFFFu);
+  while (true) {
+    const int64_t t = base - (int64_t)lane;
+    uint64_t w = 0, flag = 0, val = 0;
+    if (t >= 0) {
+      do {
+        w = ld_relaxed_gpu(status + t);
+        flag = ((w >> 40) == tagbits) ? ((w >> 38) & 3ull) : 0ull;
+      } while (flag == 0);
+      val = w & LB_VAL_MASK;
+    } else {
+      flag = LB_FLAG_PRE;  // virtual predecessor of tile 0
+      val = 0;
+    }
+    const uint32_t pre_mask = __ballot_sync(0xffffffffu, flag == LB_FLAG_PRE);
+    // first lane (closest predecessor) holding an inclusive prefix
+    const uint32_t stop = __ffs(pre_mask) - 1;  // pre_mask != 0 only if some lane saw PRE
+    uint64_t contrib = (pre_mask && lane > stop) ? 0 : val;
+    if (pre_mask == 0) contrib = val;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+    exclusive += contrib;
+    if (pre_mask) break;
+    base -= 32;
+  }
+  if (lane == 0) {
+    __threadfence();
+    st_relaxed_gpu(status + tile, lb_pack(tag, LB_FLAG_PRE, exclusive + aggregate));
+  }
+  return exclusive;
+}
+
+// Dynamic tile ticket; ensures tiles start in order so look-back progresses.
+__device__ __forceinline__ uint32_t take_ticket(zen::LookbackCtl* ctl, uint32_t* smem_slot) {
+  if (threadIdx.x == 0) *smem_slot = atomicAdd(&ctl->ticket, 1u);
+  __syncthreads();
+  const uint32_t t = *smem_slot;
+  __syncthreads();
+  return t;
+}
+// Last block to finish resets the ticket and advances the tag.  Returns true
+// (on every thread of the block) for that last block; must be called by all
+// threads.  `sys` upgrades the fence to system scope (peer-visible stores).
+__device__ __forceinline__ bool finish_tile(zen::LookbackCtl* ctl, uint32_t ntiles,
+                                            bool sys = false) {
+  __shared__ uint32_t s_is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (sys) __threadfence_system(); else __threadfence();
+    const uint32_t d = atomicAdd(&ctl->done, 1u);
+    s_is_last = (d == ntiles - 1) ? 1u : 0u;
+    if (s_is_last) {
+      ctl->ticket = 0;
+      ctl->done = 0;
+      uint32_t t = (ctl->tag + 1u) & 0xFFFFFFu;
+      ctl->tag = t ? t : 1u;  // 0 is reserved for "never written"
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return s_is_last != 0;
+}
+
+// ---- system-scope flags (NVLink peers) -------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *flag >= want (acquire, system scope). Returns false on timeout.
+__device__ __forceinline__ bool wait_flag(const unsigned long long* flag, uint64_t want,
+                                          uint64_t timeout_ns) {
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_sys(flag) < want) {
+    if (globaltimer_ns() - t0 > timeout_ns) return false;
+    __nanosleep(64);
+  }
+  return true;
+}
+
+// 256-bit streaming load (sm_100 ld.v8): read once, no L1 allocation, evict
+// first from L2 (keeps the resident tables/hash memory in the 126 MB L2 while
+// the dense gradient streams through).  p must be 32-byte aligned.
+struct f8 {
+  float v[8];
+};
+__device__ __forceinline__ f8 ld_stream_f8(const void* p) {
+  uint32_t r[8];
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "l"(p));
+  f8 o;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o.v[i] = __uint_as_float(r[i]);
+  return o;
+}
+
+}  // namespace zen_dev

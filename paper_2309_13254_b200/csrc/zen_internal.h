@@ -1,0 +1,204 @@
+// zen_internal.h -- structures shared by the host orchestrator and the
+// sm_100a kernels, plus the kernel launcher declarations.  Not part of the
+// public C-ABI (include/zen_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace zen {
+
+constexpr uint32_t kMaxK = 16;          // rehash depth supported on device
+constexpr uint32_t kMaxPartitions = 512;   // n for the standalone hash
+constexpr uint32_t kMaxWorkers = 16;    // n for the fused BP pipeline
+constexpr uint32_t kHashTile = 2048;    // keys per hash tile (256 threads x 8)
+constexpr uint32_t kExtractTile = 8192; // floats per extraction tile
+constexpr uint32_t kAggChunk = 4096;    // ranks per aggregate/encode chunk
+constexpr uint32_t kDecodeTileWords = 256;  // 64-index words per decode tile
+constexpr uint32_t kPrefixBlockWords = 8192;  // bitmap words per popcount-prefix block
+constexpr uint64_t kKeyBits = 40;       // slot word: [63:40] epoch, [39:0] index+1
+constexpr uint64_t kKeyMask = (1ull << kKeyBits) - 1ull;
+constexpr uint64_t kPeerTimeoutNs = 30ull * 1000ull * 1000ull * 1000ull;
+
+// HashFamily folded for the device: pc = G*(partition_seed+1), sc[i] =
+// G*(slot_seed_i+1) with G = 0x9e3779b97f4a7c15 (zen/hashing.hpp:27-29).
+struct DevFamily {
+  uint64_t pc;
+  uint64_t sc[kMaxK];
+  uint32_t n;
+  uint32_t k;
+};
+
+struct LookbackCtl {
+  uint32_t ticket;
+  uint32_t done;
+  uint32_t tag;
+  uint32_t pad;
+};
+
+// Per-run hash-stage header in device memory.  r1/r2 may be derived on device
+// from the extracted nnz (zen/schemes.hpp:363-367) so a whole BP iteration is
+// free of host round trips.
+struct HashHdr {
+  uint64_t count;        // z (input keys)
+  uint64_t r1, r2, stride;
+  uint64_t ovf_word;     // min over dropped keys of (key << 16 | p); ~0 = none
+  uint32_t epoch;        // hash-memory epoch (1 .. 0xFFFFFE)
+  uint32_t ntiles;
+  uint32_t derive;       // 1: compute r1/r2 from count with r1_mult/r2_ratio
+  uint32_t done;         // scatter blocks finished
+  uint32_t iter;         // BP iteration counter (peer flag value)
+  uint32_t fallback_any;
+  uint32_t status;       // device-side error bits (kErr*), sticky until read
+  uint32_t fb_done;      // fallback blocks finished
+  double r1_mult, r2_ratio;
+  uint64_t bad_index;    // IndexOutsideUniverse witness (min), ~0 = none
+};
+
+constexpr uint32_t kErrTimeout = 1u, kErrOutside = 2u, kErrCapacity = 4u;
+
+// Header a worker writes into every server's inbox (peer memory) after its
+// scatter: its whole count row so every rank can rebuild the n x n matrix
+// (TrafficReport / imbalance) without another exchange.
+struct PushHdr {
+  unsigned long long flag;  // = iteration when the data below is valid
+  uint64_t nnz;             // worker's z
+  uint64_t ovf_word;        // worker's overflow witness
+  uint32_t counts[kMaxWorkers];  // |I_w^s| for s = 0..n-1
+  uint32_t status;
+  uint32_t pad;
+};
+
+// Header a server writes into every receiver's pull inbox after encoding.
+struct PullHdr {
+  unsigned long long flag;
+  uint64_t agg_count;  // U_s
+  uint64_t bad_index;
+  uint32_t status;
+  uint32_t pad;
+};
+
+// Per-64-index word record of the server's own universe: which of the 64
+// indices it owns and how many of its indices precede the word (the rank base
+// for HashBitmap positions, zen/codec.hpp:146-158).
+struct OwnWord {
+  uint64_t mask;
+  uint32_t prefix;
+  uint32_t pad;
+};
+
+// ---- kernel launchers (implemented in k_*.cu) ------------------------------
+// All are asynchronous on `stream`; counts live in device memory.
+
+// extraction: dense fp32 -> sorted COO (K = uint32_t or uint64_t)
+template <typename K>
+void launch_extract(const float* dense, uint64_t m, K* out_idx, float* out_val, uint64_t* d_count,
+                    uint64_t capacity, unsigned long long* status, LookbackCtl* ctl,
+                    uint32_t* d_status_bits, cudaStream_t stream);
+
+void launch_partition_of(const uint64_t* idx, uint64_t count, uint64_t pc, uint32_t n,
+                         uint32_t* out, cudaStream_t stream);
+
+template <typename K>
+struct HashArgs {
+  const K* idx;
+  const float* val;
+  DevFamily fam;
+  HashHdr* hdr;
+  unsigned long long* slots;  // n * stride_cap words
+  float* slot_vals;           // optional (layout dump)
+  uint32_t* meta;             // [cap] p | depth << 16
+  uint32_t* tile_cnt;         // [ntiles_cap * n]
+  uint32_t* tile_scnt;        // [ntiles_cap * n]
+  uint32_t* load;             // [n]
+  uint32_t* sload;            // [n] serial keys per partition
+  uint64_t* part_off;         // [n] exclusive offsets (contiguous output mode)
+  uint32_t* fallback;         // [n]
+  uint32_t* stats;            // [n * (k+1)] depth histogram per partition
+  uint32_t* fb_stats;         // [n * (k+1)]
+  uint64_t* stats_out;        // [k+1] final: serial, depth1..k
+  // scatter destinations
+  int dst_table;              // 0: contiguous out (out_idx + part_off[p]); 1: pointer tables
+  K* out_idx;
+  float* out_val;
+  K* const* dst_idx;          // [n] device pointer table
+  float* const* dst_val;      // [n]
+  uint64_t dst_cap;           // capacity per destination part
+  uint64_t cap;               // key capacity (grid sizing)
+  uint64_t stride_cap;        // r1 + r2 capacity of the hash memory
+  // push signalling (pipeline): headers in each server's inbox
+  PushHdr* const* push_hdr;   // [n] or nullptr
+  uint32_t me;
+};
+
+template <typename K>
+void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream);
+
+// universe tables (HashUniverseTable, zen/codec.hpp:47-72) as bit planes
+void launch_tables_planes(uint64_t m, uint32_t n, uint64_t pc, uint32_t nplanes,
+                          unsigned long long* planes, uint32_t* chunk_cnt, cudaStream_t stream);
+void launch_tables_scan(uint32_t* chunk_cnt_to_prefix, uint64_t nchunks, uint32_t n,
+                        uint64_t* totals, cudaStream_t stream);
+void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
+                       const unsigned long long* planes, const uint32_t* cprefix, OwnWord* own,
+                       uint32_t* sel, uint64_t nsel, cudaStream_t stream);
+
+// aggregate + HashBitmap encode of one server (fused)
+struct AggArgs {
+  uint32_t n, s;
+  uint64_t m;
+  const uint32_t* const* in_idx;  // [n] parts w -> s, worker order
+  const float* const* in_val;
+  const PushHdr* const* in_hdr;   // [n] headers (counts) or nullptr
+  const uint64_t* in_count;       // [n] counts when in_hdr == nullptr
+  const OwnWord* own;
+  const uint32_t* sel;
+  uint64_t bs;                    // |I_s|
+  uint32_t ndst;
+  unsigned long long* const* dst_bits;  // [ndst]
+  float* const* dst_vals;               // [ndst]
+  PullHdr* const* dst_hdr;              // [ndst] or nullptr
+  uint64_t val_cap;
+  unsigned long long* lb_status;
+  LookbackCtl* lb_ctl;
+  uint64_t* agg_count;            // U_s (device)
+  HashHdr* hdr;                   // epoch / error bits / bad index
+  int wait_push;                  // wait for in_hdr[w]->flag >= hdr->iter
+};
+void launch_aggregate(const AggArgs& a, cudaStream_t stream);
+
+// decode of all servers' HashBitmap messages into the global sorted result
+struct DecodeArgs {
+  uint32_t n;
+  uint64_t m;
+  uint32_t nplanes;
+  const unsigned long long* planes;
+  const uint32_t* cprefix;                 // [nchunks32 * n]
+  const unsigned long long* const* bits;   // [n] (nullptr: server absent)
+  const float* const* vals;                // [n]
+  const uint64_t* bs;                      // [n] |I_s| (device)
+  const PullHdr* const* pull_hdr;          // [n] or nullptr
+  const uint64_t* agg_count;               // [n] (device) when pull_hdr == nullptr
+  uint32_t* bpre;                          // [n * words_cap] word popcount prefix (local)
+  uint32_t* bpre_blk;                      // [n * blocks_cap]
+  uint64_t words_stride;                   // per-server stride in bpre
+  uint64_t blk_stride;
+  uint64_t* out_idx;
+  float* out_val;
+  uint64_t* out_count;
+  uint64_t out_cap;
+  unsigned long long* lb_status;
+  LookbackCtl* lb_ctl;
+  HashHdr* hdr;
+  int wait_pull;
+  uint32_t* popc_total;                    // [n] per-server popcount (malformed check)
+};
+// d_blk_start[n+1]: first prefix block of each server; d_nwords_s[n]: bitmap words
+void launch_decode_parts(const DecodeArgs& a, const uint32_t* d_blk_start,
+                         const uint64_t* d_nwords_s, uint32_t total_blocks, cudaStream_t stream);
+
+// small helpers
+void launch_u64_to_u32(const uint64_t* in, uint32_t* out, uint64_t n, cudaStream_t stream);
+void launch_fill_u64(unsigned long long* p, uint64_t n, uint64_t v, cudaStream_t stream);
+
+}  // namespace zen
