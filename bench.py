@@ -1,0 +1,401 @@
+#!/usr/bin/env python3
+"""Benchmark of the Balanced-Parallelism sparse gradient sync on B200.
+
+Workload (BASELINE.json north_star target / configs[3]): a 1M x 64 fp32
+embedding gradient per worker at 1% density (10,000 live rows of 64 non-zero
+elements, integer values 1..16 so sums are exact), shared core omega = 0.5 of
+the rows, the rest Zipf(1.05)-skewed over rows; n = N workers, one per GPU
+(weak scaling: per-GPU work fixed).  One step = one full BP synchronisation:
+extraction -> hierarchical hash + push -> aggregate + HashBitmap encode + pull
+-> decode, dense gradients already in HBM.  Inputs (256 MB/GPU) exceed the
+126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ... (one rank per GPU;
+push/pull are NVLink stores into peer inboxes mapped with CUDA IPC).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse grad sync ms/iter (1/2/4/8 B200) + hash Mnnz/s as % HBM/NVLink roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--rows", type=int, default=1_000_000)
+    ap.add_argument("--width", type=int, default=64)
+    ap.add_argument("--density", type=float, default=0.01)
+    ap.add_argument("--omega", type=float, default=0.5)
+    ap.add_argument("--zipf", type=float, default=1.05)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--emulate", type=int, default=0,
+                    help="extra: also time n emulated workers on one GPU (local mode)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- workload ----
+
+def live_rows(rows, per_worker, n, omega, zipf, seed):
+    """Row ids per worker: a shared core of ceil(omega*z) rows + the remainder
+    drawn without replacement from a Zipf(zipf) row popularity (ranks randomly
+    permuted over row ids), Gumbel-top-k sampling, fixed seeds."""
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(rows)
+    logw = np.empty(rows)
+    logw[perm] = -zipf * np.log(np.arange(1, rows + 1))
+    core_n = int(np.ceil(omega * per_worker))
+    g = rng.gumbel(size=rows)
+    core = np.argpartition(-(logw + g), core_n)[:core_n] if core_n else np.zeros(0, np.int64)
+    out = []
+    for w in range(n):
+        r = np.random.default_rng(seed * 1000 + 17 + w)
+        key = logw + r.gumbel(size=rows)
+        key[core] = -np.inf
+        rest = per_worker - core_n
+        extra = np.argpartition(-key, rest)[:rest] if rest else np.zeros(0, np.int64)
+        out.append(np.sort(np.concatenate([core, extra])))
+    return out
+
+
+def dense_gradient(rows, width, live, seed):
+    r = np.random.default_rng(seed)
+    g = np.zeros((rows, width), np.float32)
+    g[live] = r.integers(1, 17, (live.size, width)).astype(np.float32)
+    return g.ravel()
+
+
+# ----------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------ CPU baseline ----
+
+def cpu_reference_step(args, n, dense_list, budget_s=12.0):
+    """The reference's own CPU path (oracle/_ref: reference headers compiled in
+    place): to_sparse of every worker + run_balanced_parallelism with a
+    prebuilt table and lanes = host cores (n == 1: hierarchical_hash, the
+    reference rejects n < 2).  Bounded sample: repeat until ~budget_s."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import ref_oracle, COracle
+    m = args.rows * args.width
+    cores = os.cpu_count() or 1
+    ro = ref_oracle()
+    kind = "reference"
+    if ro is None:  # never on a box that ran build(); kept for completeness
+        kind = "port"
+        co = COracle()
+        t0 = time.perf_counter()
+        ins = [co.to_sparse(d) for d in dense_list]
+        if n >= 2:
+            co.bp_sync(m, ins, seed=args.seed)
+        dt = (time.perf_counter() - t0) * 1e3
+        return {"value": dt, "unit": "ms/iter", "cores": 1, "kind": kind,
+                "sample": f"1 step of the full workload, n={n}"}
+    first = ro.bench_step(m, dense_list, lanes=cores, seed=args.seed, reps=1)
+    step = first["to_sparse_ms"] + first["sync_ms"]
+    reps = int(max(1, min(20, budget_s * 1e3 // max(step, 1.0))))
+    res = ro.bench_step(m, dense_list, lanes=cores, seed=args.seed, reps=reps) if reps > 1 else first
+    val = res["to_sparse_ms"] + res["sync_ms"]
+    return {"value": round(val, 3), "unit": "ms/iter", "cores": cores, "kind": kind,
+            "sample": (f"{reps + (1 if reps > 1 else 0)} full steps of the {args.rows}x{args.width} "
+                       f"workload, n={n} workers simulated serially (to_sparse "
+                       f"{res['to_sparse_ms']:.1f} ms + sync {res['sync_ms']:.1f} ms; one-time "
+                       f"universe table {res['table_ms']:.0f} ms excluded)"),
+            "stages_ms": {"to_sparse": round(res["to_sparse_ms"], 3),
+                          "sync": round(res["sync_ms"], 3), "table_once": round(res["table_ms"], 1)}}
+
+
+# --------------------------------------------------------------- our arm ----
+
+def config_dict(args, n, z):
+    return {"workload": f"embedding gradient {args.rows}x{args.width} fp32, {args.density:.2%} "
+                        f"density per worker (row-structured, omega={args.omega}, "
+                        f"Zipf({args.zipf}) rows), n={n} workers (1 per GPU), BP sync",
+            "rows": args.rows, "width": args.width, "universe": args.rows * args.width,
+            "nnz_per_worker": z, "n_workers": n, "hash": {"k": 3, "r1_multiplier": 2.0,
+                                                          "r2_ratio": 0.1, "seed": args.seed},
+            "l2": "inputs larger than L2 (256 MB dense fp32 per GPU > 126 MB L2); no flush",
+            "parallelism": f"dp{n}"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n = max(args.gpus, world)
+    m = args.rows * args.width
+    per_worker_rows = int(np.ceil(args.density * args.rows))
+    z = per_worker_rows * args.width
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        rows = live_rows(args.rows, per_worker_rows, n, args.omega, args.zipf, args.seed)
+        dense = [dense_gradient(args.rows, args.width, rows[w], args.seed + w) for w in range(n)]
+        vals = []
+        base = cpu_reference_step(args, n, dense, budget_s=2.0)
+        k = max(1, args.steps)
+        for _ in range(min(k, 5)):
+            vals.append(cpu_reference_step(args, n, dense, budget_s=0.0)["value"])
+        v = float(np.median(vals))
+        line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms/iter",
+                "n_gpus": args.gpus, "steps": len(vals), "warmup": 1, "ms_per_step": round(v, 3),
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": config_dict(args, n, z),
+                "cpu_baseline": {"value": round(v, 3), "unit": "ms/iter", "cores": base["cores"],
+                                 "kind": base["kind"], "sample": base["sample"]},
+                "e2e": {"value": round(v, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_2309_13254_b200 as zen
+
+    rows = live_rows(args.rows, per_worker_rows, n, args.omega, args.zipf, args.seed)
+    host = dense_gradient(args.rows, args.width, rows[rank], args.seed + rank)
+    d_dense = torch.from_numpy(host).cuda()
+    params = zen.HashParams(seed=args.seed)
+    bp = zen.BPSynchronizer(n, m, max_nnz=int(z * 1.25) + 4096, params=params,
+                            rank=None if n == 1 else rank)
+    if n > 1:
+        bp.connect_process_group()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        bp.sync_dense([d_dense])
+    bp.wait()
+    # correctness guard on the benchmarked configuration (cheap identity checks)
+    cnt = bp.result_count()
+    assert cnt >= z and cnt <= n * z, f"result size {cnt} out of range"
+    bp.stage_times()  # reset
+    bp.enable_timing(True)
+    launches0 = zen.load().zen_kernel_launches()
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            bp.sync_dense([d_dense])
+        e1.record(stream)
+        barrier()
+    launches = zen.load().zen_kernel_launches() - launches0
+    bp.wait()
+    ms = e0.elapsed_time(e1) / args.steps
+    stage_ms, timed = bp.stage_times()
+    bp.enable_timing(False)
+    stage_ms = stage_ms / max(timed, 1)
+    if dist:
+        t = torch.tensor([ms] + list(stage_ms), device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, stage_ms = float(t[0]), t[1:].cpu().numpy()
+    ledger, counts, agg = bp.ledger()
+    union = int(bp.result_count())
+
+    # e2e: host (pinned) dense -> H2D -> sync -> D2H result, through the C-ABI
+    e2e = None
+    if not args.no_e2e:
+        pin = torch.from_numpy(host).pin_memory()
+        cap = n * z + 16
+        oi = torch.empty(cap, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+        ov = torch.empty(cap, dtype=torch.float32).pin_memory().numpy()
+        hd = [pin.numpy()]
+        bp.sync_host(hd, oi, ov)
+        barrier()
+        k2 = max(3, min(args.steps, 10))
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(k2):
+            got = bp.sync_host(hd, oi, ov)
+        t1.record(stream)
+        barrier()
+        e2e_ms = t0.elapsed_time(t1) / k2
+        if dist:
+            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t[0])
+        e2e = {"value": round(e2e_ms, 4), "unit": "ms/iter", "h2d_bytes_per_step": 4 * m * n,
+               "d2h_bytes_per_step": 12 * got * n,
+               "path": "zen_bp_sync_host (C-ABI): pinned host dense -> device -> host result"}
+
+    # extra: n workers emulated on one GPU (local mode), e.g. the 8-worker headline
+    emu = None
+    if args.emulate and rank == 0 and world == 1:
+        ne = args.emulate
+        rows_e = live_rows(args.rows, per_worker_rows, ne, args.omega, args.zipf, args.seed)
+        dd = [torch.from_numpy(dense_gradient(args.rows, args.width, rows_e[w], args.seed + w)).cuda()
+              for w in range(ne)]
+        be = zen.BPSynchronizer(ne, m, max_nnz=int(z * 1.25) + 4096, params=params)
+        for _ in range(3):
+            be.sync_dense(dd)
+        be.wait()
+        be.enable_timing(True)
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        ke = max(3, args.steps // 2)
+        for _ in range(ke):
+            be.sync_dense(dd)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        be.wait()
+        sms, kk = be.stage_times()
+        emu = {"workers": ne, "ms_per_sync_one_gpu": round(a0.elapsed_time(a1) / ke, 4),
+               "stage_ms": {nm: round(float(x) / max(kk, 1), 4)
+                            for nm, x in zip(zen.STAGE_NAMES, sms)},
+               "union": be.result_count()}
+        del be, dd
+
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # roofline of the dominant kernel (extraction: streams the 256 MB dense gradient)
+    peak, peak_src = measured_peaks()
+    ext_ms = float(stage_ms[0])
+    alg_bytes = 4 * m + 12 * z  # 4M + E*z, E = 12 B (u64 index + f32 value)
+    achieved = alg_bytes / (ext_ms * 1e-3) / 1e9 if ext_ms > 0 else None
+    traffic = ncu_traffic().get("k_extract")
+    roofline = {"kernel": "k_extract (non-zero extraction, HBM-bound)", "bound": "hbm",
+                "achieved": round(achieved, 1) if achieved else None, "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
+                "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
+                "peak_source": peak_src,
+                "launch_ms": round(ext_ms, 5)}
+    hash_ms = float(stage_ms[1])
+    hash_bytes = 24 * z  # 2*E*z
+    total_nnz = n * z
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms/iter", "n_gpus": n,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (row-structured embedding gradients, integer values)",
+        "config": config_dict(args, n, z),
+        "throughput_mnnz_per_s": round(total_nnz / (ms * 1e-3) / 1e6, 1),
+        "stage_ms": {nm: round(float(x), 5) for nm, x in zip(zen.STAGE_NAMES, stage_ms)},
+        "hash_stage": {"mnnz_per_s": round(z / (hash_ms * 1e-3) / 1e6, 1) if hash_ms else None,
+                       "algorithmic_bytes": hash_bytes,
+                       "hbm_frac": round(hash_bytes / (hash_ms * 1e-3) / 1e9 / peak, 4) if hash_ms else None,
+                       "note": "includes the fused NVLink push (scatter into owner inboxes)"},
+        "exchange": {"push_bytes_sent_per_gpu_max": int(ledger[0, 0].max() // 96 * 8),
+                     "pull_bytes_recv_per_gpu_max": int(ledger[1, 1].max() // 8),
+                     "note": "push wire: u32 index + f32 value (WireFormat::coo(32) layout); "
+                             "pull: HashBitmap bits + f32 values; ledger bits use the reference "
+                             "widths (64-bit COO)"},
+        "union_nnz": union, "gpu_launches": int(launches),
+        "kernels_per_sync": bp.kernels_per_sync(),
+        "roofline": roofline,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if emu:
+        line["emulated_local"] = emu
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_reference_step(args, n, [host])
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

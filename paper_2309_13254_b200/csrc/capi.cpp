@@ -29,6 +29,8 @@ void launch_meta_depth(const uint32_t* meta, uint64_t count, uint32_t* out, cuda
 void launch_universe_indices(const OwnWord* own, uint64_t nwords, uint64_t* out,
                              cudaStream_t stream);
 void launch_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t stream);
+void launch_check_owned(const uint64_t* idx, uint64_t count, uint64_t m, const OwnWord* own,
+                        HashHdr* hdr, cudaStream_t stream);
 }  // namespace zen
 
 using namespace zen;
@@ -573,7 +575,10 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   CKR(upload(in_val, &vi, 1));
   CKR(upload(dst_bits, &bits, 1));
   CKR(upload(dst_vals, &vals, 1));
-  if (count) launch_u64_to_u32(d_idx, keys, count, c->stream);
+  if (count) {
+    launch_check_owned(d_idx, count, u->m, u->own[s], hdr, c->stream);
+    launch_u64_to_u32(d_idx, keys, count, c->stream);
+  }
   AggArgs a{};
   a.n = 1;
   a.s = s;

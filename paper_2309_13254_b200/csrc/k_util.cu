@@ -50,6 +50,21 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restri
     out[i] = in[i];
 }
 
+// universe_positions' ownership check (zen/codec.hpp:146-158): every index
+// must be < M and owned by the server; the smallest offender is reported.
+__global__ void k_check_owned(const uint64_t* __restrict__ idx, uint64_t count, uint64_t m,
+                              const OwnWord* __restrict__ own, HashHdr* hdr) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = idx[i];
+    const bool ok = x < m && ((own[x >> 6].mask >> (x & 63)) & 1ull);
+    if (!ok) {
+      atomicMin((unsigned long long*)&hdr->bad_index, (unsigned long long)x);
+      atomicOr(&hdr->status, kErrOutside);
+    }
+  }
+}
+
 inline unsigned grid_for(uint64_t work) {
   uint64_t g = (work + 255) / 256;
   if (g < 1) g = 1;
@@ -74,6 +89,12 @@ void launch_meta_depth(const uint32_t* meta, uint64_t count, uint32_t* out, cuda
 void launch_universe_indices(const OwnWord* own, uint64_t nwords, uint64_t* out,
                              cudaStream_t stream) {
   k_universe_indices<<<grid_for(nwords), 256, 0, stream>>>(own, nwords, out);
+  count_launch();
+}
+
+void launch_check_owned(const uint64_t* idx, uint64_t count, uint64_t m, const OwnWord* own,
+                        HashHdr* hdr, cudaStream_t stream) {
+  k_check_owned<<<grid_for(count), 256, 0, stream>>>(idx, count, m, own, hdr);
   count_launch();
 }
 

@@ -801,17 +801,18 @@ class BPSynchronizer:
     def kernels_per_sync(self) -> int:
         return int(_lib().zen_bp_kernels_per_sync(self.h))
 
-    def sync_host(self, host_dense, capacity: int):
-        """End to end from host buffers: returns (idx u64 ndarray, val f32 ndarray)."""
+    def sync_host(self, host_dense, out_idx: np.ndarray, out_val: np.ndarray) -> int:
+        """End to end from HOST buffers (pinned recommended): H2D of the dense
+        gradients, the sync, D2H of the result into out_idx (u64) / out_val
+        (f32).  Returns the result count."""
         k = self.local_workers
         arrs = [np.ascontiguousarray(h, dtype=np.float32) for h in host_dense]
         dp = (C.c_void_p * k)(*[a.ctypes.data for a in arrs])
-        oi = np.empty(max(capacity, 1), np.uint64)
-        ov = np.empty(max(capacity, 1), np.float32)
+        assert out_idx.dtype == np.uint64 and out_val.dtype == np.float32
         c = C.c_uint64()
-        _check(_lib().zen_bp_sync_host(self.h, dp, oi.ctypes.data, ov.ctypes.data, capacity,
-                                       C.byref(c)))
-        return oi[:c.value], ov[:c.value]
+        _check(_lib().zen_bp_sync_host(self.h, dp, out_idx.ctypes.data, out_val.ctypes.data,
+                                       min(out_idx.size, out_val.size), C.byref(c)))
+        return c.value
 
 
 _SYNC_CACHE: dict = {}

@@ -349,8 +349,10 @@ def test_bp_dense_pipeline_rows(zen, co):
         np.testing.assert_array_equal(counts, want.counts)
         np.testing.assert_array_equal(agg, want.agg_counts)
     # end to end from host buffers
-    hi, hv = bp.sync_host([x.cpu().numpy() for x in dense], capacity=m)
-    np.testing.assert_array_equal(hi, want.idx)
+    hi, hv = np.empty(m, np.uint64), np.empty(m, np.float32)
+    c = bp.sync_host([x.cpu().numpy() for x in dense], hi, hv)
+    np.testing.assert_array_equal(hi[:c], want.idx)
+    np.testing.assert_array_equal(bits(hv[:c]), bits(want.val))
 
 
 def test_bp_single_worker_pipeline(zen, co):
