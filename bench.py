@@ -234,6 +234,7 @@ def main():
 
     import torch
     torch.cuda.set_device(local_rank)
+    torch.cuda.set_stream(torch.cuda.Stream())  # non-legacy stream: the sync is graph-replayed
     dist = None
     if world > 1:
         import torch.distributed as dist

@@ -105,9 +105,11 @@ zen_status zen_hash_family_make_worker(uint64_t shared_seed, uint32_t worker, ui
 /* ---- device context ---------------------------------------------------- */
 zen_status zen_ctx_create(int device, zen_ctx** out);
 void zen_ctx_destroy(zen_ctx* ctx);
-/* use an external cudaStream_t (e.g. the framework's current stream); NULL
- * restores the context's own stream */
+/* use an external cudaStream_t (e.g. the framework's current stream; NULL is
+ * the legacy default stream).  zen_ctx_own_stream returns the context's own
+ * non-blocking stream (the initial one). */
 zen_status zen_ctx_set_stream(zen_ctx* ctx, void* cuda_stream);
+void* zen_ctx_own_stream(zen_ctx* ctx);
 void* zen_ctx_stream(zen_ctx* ctx);
 zen_status zen_ctx_synchronize(zen_ctx* ctx);
 
@@ -202,6 +204,9 @@ zen_status zen_bp_enable_timing(zen_bp* bp, int on);
 zen_status zen_bp_stage_times(zen_bp* bp, double* ms, uint64_t* syncs);
 /* kernels launched per sync (this rank) */
 uint32_t zen_bp_kernels_per_sync(const zen_bp* bp);
+/* replay dense syncs from a captured CUDA graph (default on; needs a
+ * non-legacy stream, see zen_ctx_set_stream) */
+zen_status zen_bp_use_graph(zen_bp* bp, int on);
 /* end to end from HOST buffers: H2D of the dense gradients (pinned host
  * memory recommended), the sync, D2H of the result. */
 zen_status zen_bp_sync_host(zen_bp* bp, const float* const* h_dense, uint64_t* h_idx,

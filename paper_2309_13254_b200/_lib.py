@@ -59,6 +59,7 @@ _SIGS = {
     "zen_ctx_destroy": (None, [vp]),
     "zen_ctx_set_stream": (C.c_int, [vp, vp]),
     "zen_ctx_stream": (vp, [vp]),
+    "zen_ctx_own_stream": (vp, [vp]),
     "zen_ctx_synchronize": (C.c_int, [vp]),
     "zen_partition_of": (C.c_int, [vp, vp, u64, u64, u32, vp]),
     "zen_to_sparse": (C.c_int, [vp, vp, u64, vp, vp, u64, P(u64)]),
@@ -86,6 +87,7 @@ _SIGS = {
     "zen_bp_enable_timing": (C.c_int, [vp, C.c_int]),
     "zen_bp_stage_times": (C.c_int, [vp, vp, P(u64)]),
     "zen_bp_kernels_per_sync": (u32, [vp]),
+    "zen_bp_use_graph": (C.c_int, [vp, C.c_int]),
     "zen_bp_sync_host": (C.c_int, [vp, P(vp), vp, vp, u64, P(u64)]),
 }
 

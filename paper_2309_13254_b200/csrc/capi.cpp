@@ -230,9 +230,10 @@ void zen_ctx_destroy(zen_ctx* c) {
 
 zen_status zen_ctx_set_stream(zen_ctx* c, void* s) {
   if (!c) return fail(ZEN_E_INVALID, "null ctx");
-  c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+  c->stream = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream
   return ZEN_OK;
 }
+void* zen_ctx_own_stream(zen_ctx* c) { return c ? (void*)c->own : nullptr; }
 void* zen_ctx_stream(zen_ctx* c) { return c ? (void*)c->stream : nullptr; }
 zen_status zen_ctx_synchronize(zen_ctx* c) {
   if (!c) return fail(ZEN_E_INVALID, "null ctx");
@@ -262,18 +263,16 @@ zen_status zen_to_sparse(zen_ctx* c, const float* d_dense, uint64_t m, uint64_t*
   DevGuard g(c->device);
   DevMem mem;
   const uint64_t ntiles = (m + kExtractTile - 1) / kExtractTile;
-  unsigned long long* status;
-  LookbackCtl* ctl;
+  ExtractWs<uint64_t> ws{};
   uint64_t* d_count;
   uint32_t* err;
-  CKR(mem.alloc(&status, ntiles));
-  CKR(mem.alloc(&ctl, 1));
+  CKR(mem.alloc(&ws.st_idx, ntiles * kExtractTile, false));
+  CKR(mem.alloc(&ws.st_val, ntiles * kExtractTile, false));
+  CKR(mem.alloc(&ws.tile_cnt, ntiles));
+  CKR(mem.alloc(&ws.tile_base, ntiles));
   CKR(mem.alloc(&d_count, 1));
   CKR(mem.alloc(&err, 1));
-  LookbackCtl h{0, 0, 1, 0};
-  CKR(upload(ctl, &h, 1));
-  launch_extract<uint64_t>(d_dense, m, d_idx, d_val, d_count, capacity, status, ctl, err,
-                           c->stream);
+  launch_extract<uint64_t>(d_dense, m, ws, d_idx, d_val, d_count, capacity, err, c->stream);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(nnz, d_count, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -383,7 +382,6 @@ struct zen_universe {
   uint32_t* cprefix = nullptr;
   uint64_t* d_bs = nullptr;
   std::vector<OwnWord*> own;
-  std::vector<uint32_t*> sel;
   std::vector<uint32_t> nq;
 
   zen_status build() {
@@ -400,21 +398,15 @@ struct zen_universe {
     CK(cudaMemcpyAsync(bs.data(), d_bs, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     own.assign(n, nullptr);
-    sel.assign(n, nullptr);
     nq.assign(n, 0);
     return ZEN_OK;
   }
   // {mask, rank base} per word and select samples for server s (lazy)
   zen_status ensure_own(uint32_t s) {
     if (own[s]) return ZEN_OK;
-    const uint32_t q = uint32_t((bs[s] + kAggChunk - 1) / kAggChunk);
-    nq[s] = q;
-    const uint64_t nsel = std::max<uint32_t>(q, 1) + 1;
+    nq[s] = std::max<uint32_t>(uint32_t((bs[s] + kAggChunk - 1) / kAggChunk), 1u);
     CKR(mem.alloc(&own[s], nwords));
-    CKR(mem.alloc(&sel[s], nsel, false));
-    std::vector<uint32_t> init(nsel, uint32_t(m));
-    CKR(upload(sel[s], init.data(), nsel));
-    launch_tables_own(m, n, s, nplanes, planes, cprefix, own[s], sel[s], q, ctx->stream);
+    launch_tables_own(m, n, s, nplanes, planes, cprefix, own[s], nullptr, 0, ctx->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     return ZEN_OK;
@@ -432,8 +424,7 @@ struct Decoder {
   uint32_t* blk_start = nullptr;
   uint64_t* nwords_s = nullptr;
   uint32_t* popc_total = nullptr;
-  unsigned long long* lb_status = nullptr;
-  LookbackCtl* lb_ctl = nullptr;
+  uint64_t* tile_base = nullptr;
   uint64_t words_stride = 0, blk_stride = 0;
   uint32_t total_blocks = 0;
   uint64_t ntiles = 0;
@@ -460,10 +451,7 @@ struct Decoder {
     CKR(upload(blk_start, bstart.data(), n + 1));
     CKR(upload(nwords_s, nws.data(), n));
     ntiles = (u->nwords + kDecodeTileWords - 1) / kDecodeTileWords;
-    CKR(mem.alloc(&lb_status, std::max<uint64_t>(ntiles, 1)));
-    CKR(mem.alloc(&lb_ctl, 1));
-    LookbackCtl h{0, 0, 1, 0};
-    CKR(upload(lb_ctl, &h, 1));
+    CKR(mem.alloc(&tile_base, std::max<uint64_t>(ntiles, 1)));
     return ZEN_OK;
   }
   void fill(DecodeArgs& a, const zen_universe* u) const {
@@ -477,14 +465,26 @@ struct Decoder {
     a.bpre_blk = bpre_blk;
     a.words_stride = words_stride;
     a.blk_stride = blk_stride;
-    a.lb_status = lb_status;
-    a.lb_ctl = lb_ctl;
+    a.tile_base = tile_base;
     a.popc_total = popc_total;
   }
   void launch(const DecodeArgs& a, cudaStream_t st) const {
     launch_decode_parts(a, blk_start, nwords_s, total_blocks, st);
   }
 };
+
+// scratch of the look-back-free aggregate + encode (see k_codec.cu)
+zen_status alloc_agg_ws(DevMem& mem, AggArgs& a, uint32_t nparts, uint64_t cap, uint64_t bs) {
+  a.nq = std::max<uint32_t>(uint32_t((bs + kAggChunk - 1) / kAggChunk), 1u);
+  a.cap = std::max<uint64_t>(cap, 1);
+  CKR(mem.alloc(&a.rank, size_t(nparts) * a.cap, false));
+  CKR(mem.alloc(&a.start, size_t(nparts) * (a.nq + 1), false));
+  CKR(mem.alloc(&a.staging, size_t(a.nq) * kAggChunk, false));
+  CKR(mem.alloc(&a.chunk_cnt, a.nq));
+  CKR(mem.alloc(&a.chunk_base, a.nq));
+  CKR(mem.alloc(&a.done, 1));
+  return ZEN_OK;
+}
 
 }  // namespace
 
@@ -543,8 +543,6 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   unsigned long long* bits;
   float* vals;
   HashHdr* hdr;
-  unsigned long long* lbs;
-  LookbackCtl* ctl;
   uint64_t* aggc;
   uint64_t* d_cnt;
   const uint32_t** in_idx;
@@ -555,8 +553,6 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   CKR(mem.alloc(&bits, std::max<uint64_t>(nw, 1)));
   CKR(mem.alloc(&vals, std::max<uint64_t>(count, 1)));
   CKR(mem.alloc(&hdr, 1));
-  CKR(mem.alloc(&lbs, std::max<uint32_t>(u->nq[s], 1)));
-  CKR(mem.alloc(&ctl, 1));
   CKR(mem.alloc(&aggc, 1));
   CKR(mem.alloc(&d_cnt, 1));
   CKR(mem.alloc(&in_idx, 1));
@@ -566,8 +562,6 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   HashHdr h{};
   h.bad_index = ~0ull;
   CKR(upload(hdr, &h, 1));
-  LookbackCtl lc{0, 0, 1, 0};
-  CKR(upload(ctl, &lc, 1));
   CKR(upload(d_cnt, &count, 1));
   const uint32_t* ki = keys;
   const float* vi = d_val;
@@ -577,6 +571,14 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   CKR(upload(dst_vals, &vals, 1));
   if (count) {
     launch_check_owned(d_idx, count, u->m, u->own[s], hdr, c->stream);
+    HashHdr hc{};
+    CK(cudaMemcpyAsync(&hc, hdr, sizeof(hc), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (hc.status & kErrOutside) {  // universe_positions, zen/codec.hpp:152-154
+      t_index = hc.bad_index;
+      return fail(ZEN_E_INDEX_OUTSIDE_UNIVERSE, "index " + std::to_string(hc.bad_index) +
+                                                    " is not owned by server " + std::to_string(s));
+    }
     launch_u64_to_u32(d_idx, keys, count, c->stream);
   }
   AggArgs a{};
@@ -588,15 +590,13 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   a.in_hdr = nullptr;
   a.in_count = d_cnt;
   a.own = u->own[s];
-  a.sel = u->sel[s];
   a.bs = bs;
+  CKR(alloc_agg_ws(mem, a, 1, count, bs));
   a.ndst = 1;
   a.dst_bits = dst_bits;
   a.dst_vals = dst_vals;
   a.dst_hdr = nullptr;
   a.val_cap = count;
-  a.lb_status = lbs;
-  a.lb_ctl = ctl;
   a.agg_count = aggc;
   a.hdr = hdr;
   a.wait_push = 0;
@@ -756,8 +756,7 @@ struct Worker {
   uint32_t* keys = nullptr;
   float* vals = nullptr;
   HashArgs<uint32_t> a{};
-  unsigned long long* ex_status = nullptr;
-  LookbackCtl* ex_ctl = nullptr;
+  ExtractWs<uint32_t> ex{};
   uint32_t epoch_runs = 0;
   uint64_t h_count = 0;  // staging for sparse inputs (stable address)
 };
@@ -765,8 +764,6 @@ struct Worker {
 struct Server {
   uint32_t id = 0;
   AggArgs a{};
-  unsigned long long* lb_status = nullptr;
-  LookbackCtl* lb_ctl = nullptr;
   uint64_t* agg_count = nullptr;
 };
 
@@ -807,6 +804,14 @@ struct zen_bp {
   uint32_t kernels_per_sync = 0;
   // e2e staging
   std::vector<float*> dense_dev;
+  // CUDA graph of the dense sync
+  bool use_graph = true;
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t gdef = nullptr;
+  std::vector<const void*> gkey;
+  std::vector<cudaEvent_t> gev;
+  std::vector<cudaGraphNode_t> gev_nodes;
+  uint32_t graph_kernels = 0;
 
   Arena& arena_of(uint32_t r) { return arenas[r]; }
   const ArenaLayout& layout_of(uint32_t r) const { return (local && r != 0) ? L0 : L; }
@@ -859,10 +864,10 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   h.bad_index = ~0ull;
   CKR(upload(a.hdr, &h, 1));
   const uint64_t ext_tiles = (bp->m + kExtractTile - 1) / kExtractTile;
-  CKR(mem.alloc(&w.ex_status, ext_tiles));
-  CKR(mem.alloc(&w.ex_ctl, 1));
-  LookbackCtl lc{0, 0, 1, 0};
-  CKR(upload(w.ex_ctl, &lc, 1));
+  CKR(mem.alloc(&w.ex.st_idx, ext_tiles * kExtractTile, false));
+  CKR(mem.alloc(&w.ex.st_val, ext_tiles * kExtractTile, false));
+  CKR(mem.alloc(&w.ex.tile_cnt, ext_tiles));
+  CKR(mem.alloc(&w.ex.tile_base, ext_tiles));
   zen_hash_family f;
   CKR(zen_hash_family_make_worker(bp->params.seed, w.id, n, k, &f));
   a.fam = fold(f);
@@ -873,11 +878,6 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   const uint32_t n = bp->n;
   DevMem& mem = bp->mem;
   CKR(bp->uni->ensure_own(s.id));
-  const uint32_t nq = std::max<uint32_t>(bp->uni->nq[s.id], 1);
-  CKR(mem.alloc(&s.lb_status, nq));
-  CKR(mem.alloc(&s.lb_ctl, 1));
-  LookbackCtl lc{0, 0, 1, 0};
-  CKR(upload(s.lb_ctl, &lc, 1));
   CKR(mem.alloc(&s.agg_count, 1));
   AggArgs& a = s.a;
   a.n = n;
@@ -894,8 +894,8 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   a.in_hdr = in_hdr;
   a.in_count = nullptr;
   a.own = bp->uni->own[s.id];
-  a.sel = bp->uni->sel[s.id];
   a.bs = bp->uni->bs[s.id];
+  CKR(alloc_agg_ws(mem, a, n, bp->cap, a.bs));
   a.ndst = bp->local ? 1 : n;
   unsigned long long** db;
   float** dv;
@@ -907,8 +907,6 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   a.dst_vals = dv;
   a.dst_hdr = dh;
   a.val_cap = bp->valcap[s.id];
-  a.lb_status = s.lb_status;
-  a.lb_ctl = s.lb_ctl;
   a.agg_count = s.agg_count;
   a.wait_push = bp->local ? 0 : 1;
   return ZEN_OK;
@@ -1095,6 +1093,9 @@ void zen_bp_destroy(zen_bp* bp) {
       cudaIpcCloseMemHandle(bp->arenas[r].base);
   }
   for (auto e : bp->ev) cudaEventDestroy(e);
+  for (auto e : bp->gev) cudaEventDestroy(e);
+  if (bp->gexec) cudaGraphExecDestroy(bp->gexec);
+  if (bp->gdef) cudaGraphDestroy(bp->gdef);
   for (auto p : bp->dense_dev) cudaFree(p);
   delete bp;
 }
@@ -1126,6 +1127,11 @@ zen_status zen_bp_set_params(zen_bp* bp, const zen_hash_params* p) {
     w.a.fam = fold(f);
   }
   bp->stride_cap = std::max(bp->stride_cap, sc);
+  if (bp->gexec) cudaGraphExecDestroy(bp->gexec);
+  if (bp->gdef) cudaGraphDestroy(bp->gdef);
+  bp->gexec = nullptr;
+  bp->gdef = nullptr;
+  bp->gkey.clear();
   return ZEN_OK;
 }
 
@@ -1171,39 +1177,114 @@ void record(zen_bp* bp, int stage) {
   cudaEventRecord(bp->ev[slot * (ZEN_STAGES + 1) + stage], bp->ctx->stream);
 }
 
+// Enqueue one synchronisation.  `ev` (ZEN_STAGES + 1 events) brackets the
+// stages when non-null.
+zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cudaEvent_t* ev) {
+  cudaStream_t st = bp->ctx->stream;
+  if (ev) CK(cudaEventRecordWithFlags(ev[0], st, cudaEventRecordExternal));
+  if (from_dense) {
+    for (size_t i = 0; i < bp->workers.size(); ++i) {
+      Worker& w = bp->workers[i];
+      launch_extract_tiles<uint32_t>(dense[i], bp->m, w.ex, &w.a.hdr->count, bp->cap,
+                                     &w.a.hdr->status, st);
+    }
+  }
+  if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
+  for (auto& w : bp->workers) {
+    if (from_dense) {  // compaction of the staged non-zeros fused with the placement
+      launch_hash_begin<uint32_t>(w.a, st);
+      launch_extract_compact_place<uint32_t>(bp->m, w.ex, w.keys, w.vals, bp->cap, w.a.fam,
+                                             w.a.hdr, w.a.slots, st);
+      launch_hash_rest<uint32_t>(w.a, bp->n, bp->params.rehash_depth, st);
+    } else {
+      launch_hash<uint32_t>(w.a, bp->n, bp->params.rehash_depth, st);
+    }
+  }
+  if (ev) CK(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
+  for (auto& s : bp->servers) launch_aggregate(s.a, st);
+  if (ev) CK(cudaEventRecordWithFlags(ev[3], st, cudaEventRecordExternal));
+  bp->dec.launch(bp->da, st);
+  if (ev) CK(cudaEventRecordWithFlags(ev[4], st, cudaEventRecordExternal));
+  CK(cudaGetLastError());
+  return ZEN_OK;
+}
+
+void bp_drop_graph(zen_bp* bp) {
+  if (bp->gexec) cudaGraphExecDestroy(bp->gexec);
+  if (bp->gdef) cudaGraphDestroy(bp->gdef);
+  bp->gexec = nullptr;
+  bp->gdef = nullptr;
+  bp->gkey.clear();
+}
+
 zen_status bp_run(zen_bp* bp, bool from_dense, const float* const* dense) {
   if (!bp->connected) return fail(ZEN_E_PEER, "zen_bp_connect has not been called");
   DevGuard g(bp->ctx->device);
   cudaStream_t st = bp->ctx->stream;
-  const uint64_t before = g_launches.load();
   bp->collected = false;
   if (bp->timing && bp->ev_head - bp->ev_tail >= (uint64_t)kRing)
     return fail(ZEN_E_INVALID, "timing ring full: call zen_bp_stage_times");
-  record(bp, 0);
-  if (from_dense) {
-    for (size_t i = 0; i < bp->workers.size(); ++i) {
-      Worker& w = bp->workers[i];
-      launch_extract<uint32_t>(dense[i], bp->m, w.keys, w.vals, &w.a.hdr->count, bp->cap,
-                               w.ex_status, w.ex_ctl, &w.a.hdr->status, st);
-    }
-  }
-  record(bp, 1);
   for (auto& w : bp->workers) {
     if (++w.epoch_runs >= 0xFFFFF0u) {  // epoch wrap: refill the hash memory once
       launch_fill_u64(w.a.slots, size_t(bp->n) * w.a.stride_cap, ~0ull, st);
       CK(cudaMemsetAsync(&w.a.hdr->epoch, 0, 4, st));
       w.epoch_runs = 1;
     }
-    launch_hash<uint32_t>(w.a, bp->n, bp->params.rehash_depth, st);
   }
-  record(bp, 2);
-  for (auto& s : bp->servers) launch_aggregate(s.a, st);
-  record(bp, 3);
-  bp->dec.launch(bp->da, st);
-  record(bp, 4);
-  CK(cudaGetLastError());
+  cudaEvent_t* ring = bp->timing ? &bp->ev[(bp->ev_head % kRing) * (ZEN_STAGES + 1)] : nullptr;
+  // CUDA-graph replay of the whole dense sync (not capturable on the legacy stream)
+  const bool graph = bp->use_graph && from_dense && st != nullptr;
+  if (!graph) {
+    const uint64_t before = g_launches.load();
+    CKR(bp_enqueue(bp, from_dense, dense, ring));
+    bp->kernels_per_sync = uint32_t(g_launches.load() - before);
+  } else {
+    std::vector<const void*> key(dense, dense + bp->workers.size());
+    key.push_back((const void*)st);
+    if (!bp->gexec || key != bp->gkey) {
+      bp_drop_graph(bp);
+      if (bp->gev.empty()) {
+        bp->gev.resize(ZEN_STAGES + 1);
+        for (auto& e : bp->gev) CK(cudaEventCreate(&e));
+      }
+      const uint64_t before = g_launches.load();
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      zen_status rc = bp_enqueue(bp, true, dense, bp->gev.data());
+      cudaGraph_t graph_def = nullptr;
+      cudaError_t e = cudaStreamEndCapture(st, &graph_def);
+      if (rc != ZEN_OK) {
+        if (graph_def) cudaGraphDestroy(graph_def);
+        return rc;
+      }
+      CK(e);
+      bp->graph_kernels = uint32_t(g_launches.load() - before);
+      g_launches.fetch_sub(bp->graph_kernels);  // counted again at each launch below
+      CK(cudaGraphInstantiate(&bp->gexec, graph_def, 0));
+      size_t nn = 0;
+      CK(cudaGraphGetNodes(graph_def, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      CK(cudaGraphGetNodes(graph_def, nodes.data(), &nn));
+      bp->gev_nodes.assign(ZEN_STAGES + 1, nullptr);
+      for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        CK(cudaGraphNodeGetType(nd, &t));
+        if (t != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t ev;
+        CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+        for (uint32_t i = 0; i <= ZEN_STAGES; ++i)
+          if (ev == bp->gev[i]) bp->gev_nodes[i] = nd;
+      }
+      bp->gdef = graph_def;
+      bp->gkey = key;
+    }
+    for (uint32_t i = 0; i <= ZEN_STAGES; ++i)  // retarget the stage events
+      CK(cudaGraphExecEventRecordNodeSetEvent(bp->gexec, bp->gev_nodes[i],
+                                              ring ? ring[i] : bp->gev[i]));
+    CK(cudaGraphLaunch(bp->gexec, st));
+    g_launches.fetch_add(bp->graph_kernels);
+    bp->kernels_per_sync = bp->graph_kernels;
+  }
   if (bp->timing) ++bp->ev_head;
-  bp->kernels_per_sync = uint32_t(g_launches.load() - before);
   return ZEN_OK;
 }
 
@@ -1424,6 +1505,12 @@ zen_status zen_bp_stage_times(zen_bp* bp, double* ms, uint64_t* syncs) {
 }
 
 uint32_t zen_bp_kernels_per_sync(const zen_bp* bp) { return bp ? bp->kernels_per_sync : 0; }
+
+zen_status zen_bp_use_graph(zen_bp* bp, int on) {
+  if (!bp) return fail(ZEN_E_INVALID, "null argument");
+  bp->use_graph = on != 0;
+  return ZEN_OK;
+}
 
 zen_status zen_bp_sync_host(zen_bp* bp, const float* const* h_dense, uint64_t* h_idx,
                             float* h_val, uint64_t capacity, uint64_t* count) {

@@ -128,55 +128,88 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
 
 constexpr int kAggThreads = 256;
 
-__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  return lo;
+__device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
+  return a.in_hdr ? *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s] : (uint32_t)a.in_count[w];
 }
 
-__global__ void __launch_bounds__(kAggThreads) k_aggregate(AggArgs a, uint32_t nq) {
-  __shared__ float acc[kAggChunk];
-  __shared__ uint32_t pres[kAggChunk / 32];
-  __shared__ uint32_t rng[2 * kMaxWorkers];
-  __shared__ uint32_t sscan[33];
-  __shared__ uint32_t s_ticket;
-  __shared__ uint64_t s_base;
-  const uint32_t n = a.n, s = a.s;
-  const uint32_t tag = *(volatile uint32_t*)&a.lb_ctl->tag;
-  const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
-  if (a.wait_push && threadIdx.x < n) {
+__device__ __forceinline__ void wait_push(const AggArgs& a) {
+  if (a.wait_push && threadIdx.x < a.n) {
+    const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
     if (!wait_flag(&a.in_hdr[threadIdx.x]->flag, iter, kPeerTimeoutNs))
       atomicOr(&a.hdr->status, kErrTimeout);
   }
   __syncthreads();
-  const uint32_t q = take_ticket(a.lb_ctl, &s_ticket);
-  const uint32_t lo = a.sel[q], hi = a.sel[q + 1];
-  if (threadIdx.x < 2 * n) {
-    const uint32_t w = threadIdx.x >> 1;
-    const uint32_t cnt = a.in_hdr ? *(volatile uint32_t*)&a.in_hdr[w]->counts[s]
-                                  : (uint32_t)a.in_count[w];
-    rng[threadIdx.x] = lower_bound_u32(a.in_idx[w], cnt, (threadIdx.x & 1) ? hi : lo);
+}
+
+__device__ __forceinline__ uint32_t rank_of(const OwnWord* own, uint32_t key) {
+  const OwnWord ow = own[key >> 6];
+  return ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
+}
+
+// Phase 1: rank of every received entry in I_s (HashBitmap position,
+// zen/codec.hpp:146-158) and, per worker, the first entry of every chunk.
+// Thread per (w, e) with e in [0, cnt_w] (e = cnt_w is the end sentinel).
+__global__ void __launch_bounds__(kAggThreads) k_agg_rank(AggArgs a) {
+  __shared__ uint64_t pre[kMaxWorkers + 1];
+  wait_push(a);
+  const uint32_t n = a.n;
+  if (threadIdx.x == 0) {
+    uint64_t acc = 0;
+    for (uint32_t w = 0; w < n; ++w) {
+      pre[w] = acc;
+      acc += (uint64_t)part_count(a, w) + 1;
+    }
+    pre[n] = acc;
   }
-  if (threadIdx.x < kAggChunk / 32) pres[threadIdx.x] = 0;
   __syncthreads();
-  const uint64_t r0 = (uint64_t)q * kAggChunk;
-  for (uint32_t w = 0; w < n; ++w) {  // worker order = the reference's left fold
-    const uint32_t* __restrict__ ix = a.in_idx[w];
-    const float* __restrict__ vx = a.in_val[w];
-    for (uint32_t e = rng[2 * w] + threadIdx.x; e < rng[2 * w + 1]; e += kAggThreads) {
+  const uint64_t total = pre[n];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t w = 0;
+    while (i >= pre[w + 1]) ++w;
+    const uint32_t e = (uint32_t)(i - pre[w]);
+    const uint32_t cnt = (uint32_t)(pre[w + 1] - pre[w] - 1);
+    const uint32_t* ix = a.in_idx[w];
+    int64_t c_e;
+    if (e < cnt) {
       const uint32_t key = ix[e];
-      const float v = vx[e];
       const OwnWord ow = a.own[key >> 6];
-      const uint32_t bit = key & 63u;
-      if (!((ow.mask >> bit) & 1ull)) {
+      if (!((ow.mask >> (key & 63u)) & 1ull)) {
         atomicMin((unsigned long long*)&a.hdr->bad_index, (unsigned long long)key);
         atomicOr(&a.hdr->status, kErrOutside);
-        continue;
       }
-      const uint32_t r = (uint32_t)(ow.prefix + __popcll(ow.mask & lowmask64(bit)) - r0);
+      const uint32_t r = ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
+      a.rank[(uint64_t)w * a.cap + e] = r;
+      c_e = r / kAggChunk;
+    } else {
+      c_e = a.nq;
+    }
+    const int64_t c_prev = e == 0 ? -1 : (int64_t)(rank_of(a.own, ix[e - 1]) / kAggChunk);
+    uint32_t* st = a.start + (uint64_t)w * (a.nq + 1);
+    for (int64_t c = c_prev + 1; c <= c_e; ++c) st[c] = e;
+  }
+}
+
+// Phase 2: one block per chunk of kAggChunk ranks.  Workers are folded in
+// order 0..n-1 (the reference's left fold, zen/schemes.hpp:377-378), in shared
+// memory; zero sums stay present.  The chunk's 64 bitmap words go straight to
+// every destination; its values are compacted into a chunk-local staging slot.
+__global__ void __launch_bounds__(kAggThreads) k_agg_chunk(AggArgs a) {
+  __shared__ float acc[kAggChunk];
+  __shared__ uint32_t pres[kAggChunk / 32];
+  __shared__ uint32_t sscan[33];
+  const uint32_t n = a.n, q = blockIdx.x;
+  if (threadIdx.x < kAggChunk / 32) pres[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t r0 = q * kAggChunk;
+  for (uint32_t w = 0; w < n; ++w) {
+    const uint32_t* st = a.start + (uint64_t)w * (a.nq + 1);
+    const uint32_t b = st[q], e = st[q + 1];
+    const uint32_t* __restrict__ rk = a.rank + (uint64_t)w * a.cap;
+    const float* __restrict__ vx = a.in_val[w];
+    for (uint32_t i = b + threadIdx.x; i < e; i += kAggThreads) {
+      const uint32_t r = rk[i] - r0;
+      const float v = vx[i];
       const uint32_t m = 1u << (r & 31);
       if (pres[r >> 5] & m) {
         acc[r] += v;
@@ -187,53 +220,83 @@ __global__ void __launch_bounds__(kAggThreads) k_aggregate(AggArgs a, uint32_t n
     }
     __syncthreads();
   }
-  // 16 ranks per thread, in rank order
-  const uint32_t bits16 = (pres[threadIdx.x >> 1] >> ((threadIdx.x & 1) * 16)) & 0xFFFFu;
-  uint32_t tot;
-  const uint32_t ex = block_exclusive_sum((uint32_t)__popc(bits16), sscan, &tot);
-  if (threadIdx.x < 32) {
-    const uint64_t base = lookback_warp(a.lb_status, q, tag, tot);
-    if (threadIdx.x == 0) {
-      s_base = base;
-      if (q == nq - 1) *a.agg_count = base + tot;
-    }
-  }
-  __syncthreads();
   const uint64_t nwords = (a.bs + 63) / 64;
   if (threadIdx.x < kAggChunk / 64) {
     const uint64_t j = (uint64_t)q * (kAggChunk / 64) + threadIdx.x;
     if (j < nwords) {
-      const unsigned long long word =
-          (unsigned long long)pres[2 * threadIdx.x] | ((unsigned long long)pres[2 * threadIdx.x + 1] << 32);
+      const unsigned long long word = (unsigned long long)pres[2 * threadIdx.x] |
+                                      ((unsigned long long)pres[2 * threadIdx.x + 1] << 32);
       for (uint32_t d = 0; d < a.ndst; ++d) a.dst_bits[d][j] = word;
+      if (a.dst_hdr) __threadfence_system();
     }
   }
-  if (bits16) {
-    uint64_t pos = s_base + ex;
-    uint32_t b = bits16;
-    while (b) {
-      const uint32_t i = __ffs(b) - 1;
-      b &= b - 1;
-      const float v = acc[threadIdx.x * 16 + i];
-      if (pos < a.val_cap)
-        for (uint32_t d = 0; d < a.ndst; ++d) a.dst_vals[d][pos] = v;
-      ++pos;
+  // 16 ranks per thread, in rank order
+  const uint32_t bits16 = (pres[threadIdx.x >> 1] >> ((threadIdx.x & 1) * 16)) & 0xFFFFu;
+  uint32_t tot;
+  uint32_t pos = block_exclusive_sum((uint32_t)__popc(bits16), sscan, &tot);
+  float* stg = a.staging + (uint64_t)q * kAggChunk;
+  uint32_t b = bits16;
+  while (b) {
+    const uint32_t i = __ffs(b) - 1;
+    b &= b - 1;
+    stg[pos++] = acc[threadIdx.x * 16 + i];
+  }
+  if (threadIdx.x == 0) a.chunk_cnt[q] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_agg_scan(AggArgs a) {
+  __shared__ uint64_t sscan[33];
+  uint64_t carry = 0;
+  for (uint32_t b = 0; b < a.nq; b += blockDim.x) {
+    const uint32_t t = b + threadIdx.x;
+    const uint64_t v = t < a.nq ? a.chunk_cnt[t] : 0u;
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_sum(v, sscan, &tot);
+    if (t < a.nq) a.chunk_base[t] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *a.agg_count = carry;
+}
+
+// Phase 4: one warp per chunk moves the staged values to their final position
+// in every destination (NVLink stores into peer pull inboxes in rank mode);
+// the last block publishes U_s and the pull flag with release semantics.
+__global__ void __launch_bounds__(256) k_agg_values(AggArgs a) {
+  __shared__ uint32_t s_last;
+  const uint32_t q = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (q < a.nq) {
+    const uint32_t cnt = a.chunk_cnt[q];
+    const uint64_t base = a.chunk_base[q];
+    const float* stg = a.staging + (uint64_t)q * kAggChunk;
+    for (uint32_t j = lane_id(); j < cnt; j += 32) {
+      const float v = stg[j];
+      if (base + j < a.val_cap)
+        for (uint32_t d = 0; d < a.ndst; ++d) a.dst_vals[d][base + j] = v;
     }
   }
-  const bool last = finish_tile(a.lb_ctl, nq, a.dst_hdr != nullptr);
-  if (last && a.dst_hdr) {  // pull signalling: publish U_s, then the flag
+  if (!a.dst_hdr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     __threadfence_system();
+    const uint32_t d = atomicAdd(a.done, 1u);
+    s_last = (d == gridDim.x - 1) ? 1u : 0u;
+    if (s_last) *a.done = 0;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence_system();
+    const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
     const uint64_t u = *(volatile uint64_t*)a.agg_count;
     const uint32_t st = *(volatile uint32_t*)&a.hdr->status;
     const uint64_t bad = *(volatile uint64_t*)&a.hdr->bad_index;
-    for (uint32_t d = threadIdx.x; d < a.ndst; d += kAggThreads) {
+    for (uint32_t d = threadIdx.x; d < a.ndst; d += blockDim.x) {
       a.dst_hdr[d]->agg_count = u;
       a.dst_hdr[d]->status = st;
       a.dst_hdr[d]->bad_index = bad;
     }
     __syncthreads();
     __threadfence_system();
-    for (uint32_t d = threadIdx.x; d < a.ndst; d += kAggThreads)
+    for (uint32_t d = threadIdx.x; d < a.ndst; d += blockDim.x)
       st_release_sys(&a.dst_hdr[d]->flag, (unsigned long long)iter);
   }
 }
@@ -246,8 +309,8 @@ __global__ void __launch_bounds__(256) k_bpre(DecodeArgs a, const uint32_t* blk_
                                              const uint64_t* nwords_s) {
   __shared__ uint32_t sscan[33];
   const uint32_t n = a.n;
-  const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
   if (a.wait_pull && threadIdx.x < n) {
+    const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
     if (a.bits[threadIdx.x] &&
         !wait_flag(&a.pull_hdr[threadIdx.x]->flag, iter, kPeerTimeoutNs))
       atomicOr(&a.hdr->status, kErrTimeout);
@@ -278,31 +341,71 @@ __global__ void __launch_bounds__(256) k_bpre(DecodeArgs a, const uint32_t* blk_
   if (threadIdx.x == 0) a.bpre_blk[s * a.blk_stride + blk] = tot;
 }
 
-__global__ void k_bpre_scan(DecodeArgs a, const uint32_t* blk_start) {
-  // one warp per server
-  const uint32_t s = threadIdx.x >> 5;
-  if (s >= a.n) return;
-  const uint32_t nb = blk_start[s + 1] - blk_start[s];
-  uint32_t* b = a.bpre_blk + s * a.blk_stride;
-  uint32_t carry = 0;
-  for (uint32_t i0 = 0; i0 < nb; i0 += 32) {
-    const uint32_t i = i0 + lane_id();
-    const uint32_t v = i < nb ? b[i] : 0u;
-    const uint32_t inc = warp_inclusive_sum(v);
-    if (i < nb) b[i] = carry + inc - v;
-    carry += __shfl_sync(0xffffffffu, inc, 31);
+// popcount of server s's bitmap bits [0, P)
+__device__ __forceinline__ uint64_t bitmap_prefix(const DecodeArgs& a, uint32_t s, uint64_t P,
+                                                  uint64_t nw) {
+  const uint64_t j = P >> 6;
+  const uint32_t o = (uint32_t)(P & 63);
+  if (j >= nw) return a.popc_total[s];
+  const unsigned long long* bits = a.bits[s];
+  return (uint64_t)a.bpre_blk[s * a.blk_stride + j / kPrefixBlockWords] +
+         a.bpre[s * a.words_stride + j] + (uint64_t)__popcll(bits[j] & lowmask64(o));
+}
+
+// One block: finish the bitmap prefixes (scan of block sums per server), then
+// the output size of every decode tile straight from the tables -- for server
+// s a tile covers the bit range [P_s(t), P_s(t+1)) of its bitmap -- and their
+// exclusive scan.  No data pass, no look-back.
+__global__ void __launch_bounds__(1024) k_dec_plan(DecodeArgs a, const uint32_t* blk_start,
+                                                   const uint64_t* nwords_s, uint32_t ntiles,
+                                                   uint64_t nchunks) {
+  __shared__ uint64_t sscan[33];
+  const uint32_t n = a.n;
+  {
+    const uint32_t s = threadIdx.x >> 5;
+    if (s < n) {
+      const uint32_t nb = blk_start[s + 1] - blk_start[s];
+      uint32_t* b = a.bpre_blk + s * a.blk_stride;
+      uint32_t carry = 0;
+      for (uint32_t i0 = 0; i0 < nb; i0 += 32) {
+        const uint32_t i = i0 + lane_id();
+        const uint32_t v = i < nb ? b[i] : 0u;
+        const uint32_t inc = warp_inclusive_sum(v);
+        if (i < nb) b[i] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane_id() == 0) a.popc_total[s] = carry;
+    }
   }
-  if (lane_id() == 0) a.popc_total[s] = carry;
+  __syncthreads();
+  uint64_t carry = 0;
+  constexpr uint32_t kChunksPerTile = kDecodeTileWords / 32;
+  for (uint32_t b = 0; b < ntiles; b += blockDim.x) {
+    const uint32_t t = b + threadIdx.x;
+    uint64_t v = 0;
+    if (t < ntiles) {
+      const uint64_t c0 = (uint64_t)t * kChunksPerTile, c1 = c0 + kChunksPerTile;
+      for (uint32_t s = 0; s < n; ++s) {
+        if (!a.bits[s]) continue;
+        const uint64_t nw = nwords_s[s];
+        const uint64_t P0 = a.cprefix[c0 * n + s];
+        const uint64_t P1 = c1 < nchunks ? (uint64_t)a.cprefix[c1 * n + s] : a.bs[s];
+        v += bitmap_prefix(a, s, P1, nw) - bitmap_prefix(a, s, P0, nw);
+      }
+    }
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_sum(v, sscan, &tot);
+    if (t < ntiles) a.tile_base[t] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *a.out_count = carry;
 }
 
 template <int NMAX>
-__global__ void __launch_bounds__(256) k_decode(DecodeArgs a, uint64_t nwords, uint32_t ntiles) {
+__global__ void __launch_bounds__(256) k_decode(DecodeArgs a, uint64_t nwords) {
   __shared__ uint32_t sscan[33];
-  __shared__ uint32_t s_ticket;
-  __shared__ uint64_t s_base;
   const uint32_t n = a.n;
-  const uint32_t tag = *(volatile uint32_t*)&a.lb_ctl->tag;
-  const uint32_t tile = take_ticket(a.lb_ctl, &s_ticket);
+  const uint32_t tile = blockIdx.x;
   const uint64_t w = (uint64_t)tile * kDecodeTileWords + threadIdx.x;
   const bool valid = w < nwords;
   unsigned long long pl[4] = {0, 0, 0, 0};
@@ -334,7 +437,7 @@ __global__ void __launch_bounds__(256) k_decode(DecodeArgs a, uint64_t nwords, u
         if (o + c > 64) x |= (uint64_t)bits[j + 1] << (64 - o);
         x &= lowmask64(c);
         if (x) {
-          pres[s] = deposit64(x, ms);
+          pres[s] = (c == 64) ? x : deposit64(x, ms);
           vbase[s] = a.bpre_blk[s * a.blk_stride + j / kPrefixBlockWords] +
                      a.bpre[s * a.words_stride + j] + (uint32_t)__popcll(w0 & lowmask64(o));
           G |= pres[s];
@@ -344,24 +447,14 @@ __global__ void __launch_bounds__(256) k_decode(DecodeArgs a, uint64_t nwords, u
   }
   uint32_t tot;
   const uint32_t ex = block_exclusive_sum((uint32_t)__popcll(G), sscan, &tot);
-  if (threadIdx.x < 32) {
-    const uint64_t base = lookback_warp(a.lb_status, tile, tag, tot);
-    if (threadIdx.x == 0) {
-      s_base = base;
-      if (tile == ntiles - 1) *a.out_count = base + tot;
-    }
-  }
-  __syncthreads();
-  uint64_t pos = s_base + ex;
+  uint64_t pos = a.tile_base[tile] + ex;
   while (G) {
     const uint32_t i = __ffsll((long long)G) - 1;
     G &= G - 1;
     float v = 0.0f;
 #pragma unroll
     for (int s = 0; s < NMAX; ++s) {
-      if ((pres[s] >> i) & 1ull) {
-        v = a.vals[s][vbase[s] + __popcll(pres[s] & lowmask64(i))];
-      }
+      if ((pres[s] >> i) & 1ull) v = a.vals[s][vbase[s] + __popcll(pres[s] & lowmask64(i))];
     }
     if (pos < a.out_cap) {
       a.out_idx[pos] = w * 64 + i;
@@ -369,7 +462,6 @@ __global__ void __launch_bounds__(256) k_decode(DecodeArgs a, uint64_t nwords, u
     }
     ++pos;
   }
-  finish_tile(a.lb_ctl, ntiles);
 }
 
 inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
@@ -405,27 +497,29 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
 }
 
 void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
-  const uint32_t nq = (uint32_t)((a.bs + kAggChunk - 1) / kAggChunk);
-  k_aggregate<<<nq ? nq : 1, kAggThreads, 0, stream>>>(a, nq ? nq : 1);
-  count_launch();
+  uint64_t tot_cap = (uint64_t)a.n * (a.cap + 1);
+  k_agg_rank<<<grid_for(tot_cap, kAggThreads, 148 * 8), kAggThreads, 0, stream>>>(a);
+  k_agg_chunk<<<a.nq, kAggThreads, 0, stream>>>(a);
+  k_agg_scan<<<1, 1024, 0, stream>>>(a);
+  k_agg_values<<<(a.nq + 7) / 8, 256, 0, stream>>>(a);
+  for (int i = 0; i < 4; ++i) count_launch();
 }
 
-// blk_start / nwords_s live in device memory right after the DecodeArgs
-// scratch (passed by the orchestrator through bpre_blk's tail); see engine.
 void launch_decode_parts(const DecodeArgs& a, const uint32_t* d_blk_start,
                          const uint64_t* d_nwords_s, uint32_t total_blocks, cudaStream_t stream) {
-  k_bpre<<<total_blocks ? total_blocks : 1, 256, 0, stream>>>(a, d_blk_start, d_nwords_s);
-  k_bpre_scan<<<1, 32 * kMaxWorkers, 0, stream>>>(a, d_blk_start);
   const uint64_t nwords = (a.m + 63) / 64;
   const uint32_t ntiles = (uint32_t)((nwords + kDecodeTileWords - 1) / kDecodeTileWords);
+  const uint64_t nchunks = (nwords + 31) / 32;
+  k_bpre<<<total_blocks ? total_blocks : 1, 256, 0, stream>>>(a, d_blk_start, d_nwords_s);
+  k_dec_plan<<<1, 1024, 0, stream>>>(a, d_blk_start, d_nwords_s, ntiles, nchunks);
   if (a.n <= 2)
-    k_decode<2><<<ntiles, 256, 0, stream>>>(a, nwords, ntiles);
+    k_decode<2><<<ntiles, 256, 0, stream>>>(a, nwords);
   else if (a.n <= 4)
-    k_decode<4><<<ntiles, 256, 0, stream>>>(a, nwords, ntiles);
+    k_decode<4><<<ntiles, 256, 0, stream>>>(a, nwords);
   else if (a.n <= 8)
-    k_decode<8><<<ntiles, 256, 0, stream>>>(a, nwords, ntiles);
+    k_decode<8><<<ntiles, 256, 0, stream>>>(a, nwords);
   else
-    k_decode<16><<<ntiles, 256, 0, stream>>>(a, nwords, ntiles);
+    k_decode<16><<<ntiles, 256, 0, stream>>>(a, nwords);
   for (int i = 0; i < 3; ++i) count_launch();
 }
 

@@ -432,20 +432,38 @@ inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
 }  // namespace
 
 template <typename K>
-void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
+void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream) {
+  k_hash_begin<K><<<1, 256, 0, stream>>>(a);
+  count_launch();
+}
+
+template <typename K>
+void launch_hash_rest(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
   const uint64_t ntiles_cap = (a.cap + kHashTile - 1) / kHashTile;
   const unsigned tile_grid = grid_for(ntiles_cap, 1, 148 * 8);
-  k_hash_begin<K><<<1, 256, 0, stream>>>(a);
-  k_place<K><<<grid_for(a.cap, kThreads, 148 * 16), kThreads, 0, stream>>>(a);
   k_post<K><<<tile_grid, kThreads, 2 * n * sizeof(uint32_t), stream>>>(a);
   k_hash_scan<K><<<1, 1024, 0, stream>>>(a);
   k_scatter<K><<<tile_grid, kThreads, 2 * kWarps * n * sizeof(uint32_t), stream>>>(a);
   k_fallback<K><<<grid_for(n, 1, 148), kThreads, 0, stream>>>(a);
-  for (int i = 0; i < 6; ++i) count_launch();
+  for (int i = 0; i < 4; ++i) count_launch();
+  (void)k;
 }
 
-template void launch_hash<uint32_t>(const HashArgs<uint32_t>&, uint32_t, uint32_t, cudaStream_t);
-template void launch_hash<uint64_t>(const HashArgs<uint64_t>&, uint32_t, uint32_t, cudaStream_t);
+template <typename K>
+void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
+  launch_hash_begin<K>(a, stream);
+  k_place<K><<<grid_for(a.cap, kThreads, 148 * 16), kThreads, 0, stream>>>(a);
+  count_launch();
+  launch_hash_rest<K>(a, n, k, stream);
+}
+
+#define ZEN_INST(K)                                                                         \
+  template void launch_hash<K>(const HashArgs<K>&, uint32_t, uint32_t, cudaStream_t);       \
+  template void launch_hash_begin<K>(const HashArgs<K>&, cudaStream_t);                     \
+  template void launch_hash_rest<K>(const HashArgs<K>&, uint32_t, uint32_t, cudaStream_t);
+ZEN_INST(uint32_t)
+ZEN_INST(uint64_t)
+#undef ZEN_INST
 
 void launch_partition_of(const uint64_t* idx, uint64_t count, uint64_t pc, uint32_t n,
                          uint32_t* out, cudaStream_t stream) {

@@ -90,11 +90,30 @@ struct OwnWord {
 // ---- kernel launchers (implemented in k_*.cu) ------------------------------
 // All are asynchronous on `stream`; counts live in device memory.
 
-// extraction: dense fp32 -> sorted COO (K = uint32_t or uint64_t)
+// extraction: dense fp32 -> sorted COO (K = uint32_t or uint64_t).
+// Workspace: tile-local staging of the non-zeros (ntiles * kExtractTile
+// entries), per-tile counts and exclusive bases.
 template <typename K>
-void launch_extract(const float* dense, uint64_t m, K* out_idx, float* out_val, uint64_t* d_count,
-                    uint64_t capacity, unsigned long long* status, LookbackCtl* ctl,
-                    uint32_t* d_status_bits, cudaStream_t stream);
+struct ExtractWs {
+  K* st_idx;
+  float* st_val;
+  uint32_t* tile_cnt;
+  uint64_t* tile_base;
+};
+template <typename K>
+void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* out_idx,
+                    float* out_val, uint64_t* d_count, uint64_t capacity, uint32_t* d_status_bits,
+                    cudaStream_t stream);
+// pipeline split: tiles + scan, then (after the hash begin) compaction fused
+// with the priority-claim placement
+template <typename K>
+void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws,
+                          uint64_t* d_count, uint64_t capacity, uint32_t* d_status_bits,
+                          cudaStream_t stream);
+template <typename K>
+void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx, float* out_val,
+                                  uint64_t capacity, const DevFamily& fam, HashHdr* hdr,
+                                  unsigned long long* slots, cudaStream_t stream);
 
 void launch_partition_of(const uint64_t* idx, uint64_t count, uint64_t pc, uint32_t n,
                          uint32_t* out, cudaStream_t stream);
@@ -131,8 +150,15 @@ struct HashArgs {
   uint32_t me;
 };
 
+// phases: begin (r1/r2, epoch, counters) | place | post..fallback.
+// launch_hash = all; the BP pipeline runs begin, then the fused
+// extraction-compaction+place, then launch_hash_rest.
 template <typename K>
 void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream);
+template <typename K>
+void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream);
+template <typename K>
+void launch_hash_rest(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream);
 
 // universe tables (HashUniverseTable, zen/codec.hpp:47-72) as bit planes
 void launch_tables_planes(uint64_t m, uint32_t n, uint64_t pc, uint32_t nplanes,
@@ -143,7 +169,9 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
                        const unsigned long long* planes, const uint32_t* cprefix, OwnWord* own,
                        uint32_t* sel, uint64_t nsel, cudaStream_t stream);
 
-// aggregate + HashBitmap encode of one server (fused)
+// aggregate + HashBitmap encode of one server (fused), look-back free:
+// rank (+ chunk starts) | chunk accumulate (+ bitmap words to every
+// destination) | scan | values to every destination (+ pull signalling).
 struct AggArgs {
   uint32_t n, s;
   uint64_t m;
@@ -152,17 +180,22 @@ struct AggArgs {
   const PushHdr* const* in_hdr;   // [n] headers (counts) or nullptr
   const uint64_t* in_count;       // [n] counts when in_hdr == nullptr
   const OwnWord* own;
-  const uint32_t* sel;
   uint64_t bs;                    // |I_s|
+  uint32_t nq;                    // chunks = ceil(bs / kAggChunk) (>= 1)
+  uint64_t cap;                   // per-part capacity (rank scratch stride)
+  uint32_t* rank;                 // [n * cap]
+  uint32_t* start;                // [n * (nq + 1)]
+  float* staging;                 // [nq * kAggChunk]
+  uint32_t* chunk_cnt;            // [nq]
+  uint64_t* chunk_base;           // [nq]
+  uint32_t* done;                 // blocks-finished counter (self-resetting)
   uint32_t ndst;
   unsigned long long* const* dst_bits;  // [ndst]
   float* const* dst_vals;               // [ndst]
   PullHdr* const* dst_hdr;              // [ndst] or nullptr
   uint64_t val_cap;
-  unsigned long long* lb_status;
-  LookbackCtl* lb_ctl;
   uint64_t* agg_count;            // U_s (device)
-  HashHdr* hdr;                   // epoch / error bits / bad index
+  HashHdr* hdr;                   // iteration / error bits / bad index
   int wait_push;                  // wait for in_hdr[w]->flag >= hdr->iter
 };
 void launch_aggregate(const AggArgs& a, cudaStream_t stream);
@@ -178,17 +211,15 @@ struct DecodeArgs {
   const float* const* vals;                // [n]
   const uint64_t* bs;                      // [n] |I_s| (device)
   const PullHdr* const* pull_hdr;          // [n] or nullptr
-  const uint64_t* agg_count;               // [n] (device) when pull_hdr == nullptr
-  uint32_t* bpre;                          // [n * words_cap] word popcount prefix (local)
-  uint32_t* bpre_blk;                      // [n * blocks_cap]
+  uint32_t* bpre;                          // [n * words_stride] word popcount prefix (local)
+  uint32_t* bpre_blk;                      // [n * blk_stride]
   uint64_t words_stride;                   // per-server stride in bpre
   uint64_t blk_stride;
+  uint64_t* tile_base;                     // [ntiles] output offset of each decode tile
   uint64_t* out_idx;
   float* out_val;
   uint64_t* out_count;
   uint64_t out_cap;
-  unsigned long long* lb_status;
-  LookbackCtl* lb_ctl;
   HashHdr* hdr;
   int wait_pull;
   uint32_t* popc_total;                    // [n] per-server popcount (malformed check)

@@ -798,6 +798,10 @@ class BPSynchronizer:
         _check(_lib().zen_bp_stage_times(self.h, ms.ctypes.data, C.byref(k)))
         return ms, k.value
 
+    def use_graph(self, on=True):
+        """Replay dense syncs from a captured CUDA graph (needs a non-default stream)."""
+        _check(_lib().zen_bp_use_graph(self.h, int(on)))
+
     def kernels_per_sync(self) -> int:
         return int(_lib().zen_bp_kernels_per_sync(self.h))
 

@@ -316,10 +316,15 @@ def test_bp_retry_policy(zen, ro):
     """run_bp_with_retry doubles r2_ratio after SerialOverflow (experiment.hpp:128-140)."""
     m, n = 1000, 2
     ins = ro.generate(m, n, 0.1, 0.0, 53)
-    p = zen.HashParams(r1_multiplier=0.5, r2_ratio=0.05)
-    want = ro.bp_sync(m, ins, r1_multiplier=0.5, r2_ratio=0.05, retries=4)
+    p = zen.HashParams(r1_multiplier=0.5, r2_ratio=0.1)
+    with pytest.raises(OracleError):  # needs the retries
+        ro.bp_sync(m, ins, r1_multiplier=0.5, r2_ratio=0.1)
+    with pytest.raises(zen.SerialOverflow):
+        zen.run_balanced_parallelism(_inputs(zen, m, ins), zen.SimNet(n, 1.0), p)
+    want = ro.bp_sync(m, ins, r1_multiplier=0.5, r2_ratio=0.1, retries=4)
     out = zen.run_bp_with_retry(_inputs(zen, m, ins), 1.0, p)
     np.testing.assert_array_equal(out.results[0].indices(), want.idx)
+    np.testing.assert_array_equal(bits(out.results[0].values()), bits(want.val))
 
 
 def test_bp_dense_pipeline_rows(zen, co):
@@ -338,8 +343,13 @@ def test_bp_dense_pipeline_rows(zen, co):
         pairs.append(co.to_sparse(g.ravel()))
     want = co.bp_sync(m, pairs, seed=1)
     bp = zen.BPSynchronizer(n, m, max_nnz=rows * d // 10)
-    for _ in range(3):  # repeated syncs reuse epochs / look-back tags
-        bp.sync_dense(dense)
+    side = torch.cuda.Stream()
+    for it in range(4):  # repeated syncs reuse epochs; it >= 2 replays the CUDA graph
+        if it < 2:
+            bp.sync_dense(dense)
+        else:
+            with torch.cuda.stream(side):
+                bp.sync_dense(dense)
         bp.wait()
         oi, ov = bp.result()
         np.testing.assert_array_equal(oi.cpu().numpy().view(np.uint64), want.idx)
