@@ -382,7 +382,6 @@ struct zen_universe {
   uint32_t* cprefix = nullptr;
   uint64_t* d_bs = nullptr;
   std::vector<OwnWord*> own;
-  std::vector<uint32_t> nq;
 
   zen_status build() {
     nplanes = planes_for(n);
@@ -398,13 +397,11 @@ struct zen_universe {
     CK(cudaMemcpyAsync(bs.data(), d_bs, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     own.assign(n, nullptr);
-    nq.assign(n, 0);
     return ZEN_OK;
   }
   // {mask, rank base} per word and select samples for server s (lazy)
   zen_status ensure_own(uint32_t s) {
     if (own[s]) return ZEN_OK;
-    nq[s] = std::max<uint32_t>(uint32_t((bs[s] + kAggChunk - 1) / kAggChunk), 1u);
     CKR(mem.alloc(&own[s], nwords));
     launch_tables_own(m, n, s, nplanes, planes, cprefix, own[s], nullptr, 0, ctx->stream);
     CK(cudaGetLastError());
@@ -424,10 +421,9 @@ struct Decoder {
   uint32_t* blk_start = nullptr;
   uint64_t* nwords_s = nullptr;
   uint32_t* popc_total = nullptr;
-  uint64_t* tile_base = nullptr;
+  uint32_t* done = nullptr;
   uint64_t words_stride = 0, blk_stride = 0;
   uint32_t total_blocks = 0;
-  uint64_t ntiles = 0;
 
   zen_status init(const zen_universe* u, const std::vector<bool>& present) {
     const uint32_t n = u->n;
@@ -448,10 +444,9 @@ struct Decoder {
     CKR(mem.alloc(&blk_start, n + 1));
     CKR(mem.alloc(&nwords_s, n));
     CKR(mem.alloc(&popc_total, n));
+    CKR(mem.alloc(&done, 1));
     CKR(upload(blk_start, bstart.data(), n + 1));
     CKR(upload(nwords_s, nws.data(), n));
-    ntiles = (u->nwords + kDecodeTileWords - 1) / kDecodeTileWords;
-    CKR(mem.alloc(&tile_base, std::max<uint64_t>(ntiles, 1)));
     return ZEN_OK;
   }
   void fill(DecodeArgs& a, const zen_universe* u) const {
@@ -461,28 +456,27 @@ struct Decoder {
     a.planes = u->planes;
     a.cprefix = u->cprefix;
     a.bs = u->d_bs;
+    a.nwords_s = nwords_s;
+    a.blk_start = blk_start;
+    a.total_blocks = total_blocks;
     a.bpre = bpre;
     a.bpre_blk = bpre_blk;
     a.words_stride = words_stride;
     a.blk_stride = blk_stride;
-    a.tile_base = tile_base;
+    a.done = done;
     a.popc_total = popc_total;
   }
-  void launch(const DecodeArgs& a, cudaStream_t st) const {
-    launch_decode_parts(a, blk_start, nwords_s, total_blocks, st);
-  }
+  void launch(const DecodeArgs& a, cudaStream_t st) const { launch_decode_parts(a, st); }
 };
 
-// scratch of the look-back-free aggregate + encode (see k_codec.cu)
-zen_status alloc_agg_ws(DevMem& mem, AggArgs& a, uint32_t nparts, uint64_t cap, uint64_t bs) {
-  a.nq = std::max<uint32_t>(uint32_t((bs + kAggChunk - 1) / kAggChunk), 1u);
-  a.cap = std::max<uint64_t>(cap, 1);
-  CKR(mem.alloc(&a.rank, size_t(nparts) * a.cap, false));
-  CKR(mem.alloc(&a.start, size_t(nparts) * (a.nq + 1), false));
-  CKR(mem.alloc(&a.staging, size_t(a.nq) * kAggChunk, false));
-  CKR(mem.alloc(&a.chunk_cnt, a.nq));
-  CKR(mem.alloc(&a.chunk_base, a.nq));
-  CKR(mem.alloc(&a.done, 1));
+// scratch of the aggregate + encode (see k_codec.cu)
+zen_status alloc_agg_ws(DevMem& mem, AggArgs& a, uint32_t nparts, uint64_t bs) {
+  a.nw = std::max<uint64_t>((bs + 63) / 64, 1);
+  a.nblk = uint32_t((a.nw + kPrefixBlockWords - 1) / kPrefixBlockWords);
+  CKR(mem.alloc(&a.pw, size_t(nparts) * a.nw));
+  CKR(mem.alloc(&a.pre, size_t(nparts + 1) * a.nw, false));
+  CKR(mem.alloc(&a.blk, size_t(nparts + 1) * a.nblk));
+  CKR(mem.alloc(&a.done, 2));
   return ZEN_OK;
 }
 
@@ -591,7 +585,7 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   a.in_count = d_cnt;
   a.own = u->own[s];
   a.bs = bs;
-  CKR(alloc_agg_ws(mem, a, 1, count, bs));
+  CKR(alloc_agg_ws(mem, a, 1, bs));
   a.ndst = 1;
   a.dst_bits = dst_bits;
   a.dst_vals = dst_vals;
@@ -895,7 +889,7 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   a.in_count = nullptr;
   a.own = bp->uni->own[s.id];
   a.bs = bp->uni->bs[s.id];
-  CKR(alloc_agg_ws(mem, a, n, bp->cap, a.bs));
+  CKR(alloc_agg_ws(mem, a, n, a.bs));
   a.ndst = bp->local ? 1 : n;
   unsigned long long** db;
   float** dv;

@@ -4,23 +4,23 @@
 //              the M x 8 B sorted lists: per 64-index word, ceil(log2 n) owner
 //              bit planes (the information minimum), per-32-word chunk prefix
 //              counts per server, and for each local server a {mask, rank
-//              base} record per word plus select samples every 4096 ranks.
+//              base} record per word.
 //  aggregate : per-owner sum (merge_sum left fold in worker order,
 //              zen/schemes.hpp:375-380; zen/tensor.hpp:133-167) FUSED with the
-//              HashBitmap encode (zen/codec.hpp:266-277).  A block owns 4096
-//              consecutive ranks of I_s: it binary-searches each worker's
-//              sorted part for the chunk, accumulates in shared memory worker
-//              by worker (bit-exact fold order, zero sums kept), and emits the
-//              64 bitmap words + the compacted values -- optionally straight
-//              into every receiver's pull inbox over NVLink (the pull fused
-//              with the encode).  Value offsets come from a decoupled look-back.
+//              HashBitmap encode (zen/codec.hpp:266-277): each worker's part
+//              becomes a presence bitmap over I_s; their OR is the HashBitmap,
+//              written straight into every receiver's pull inbox (NVLink
+//              stores in rank mode); popcount prefixes locate every value, and
+//              the values of a union bit are folded in worker order (bit-exact,
+//              zero sums kept).  Work ~ bitmap words + entries, no look-back.
 //  decode    : all servers' (bitmap, values) -> the global ascending result
 //              (decode zen/codec.hpp:333-347 + merge_disjoint
 //              zen/schemes.hpp:91-113).  Per global word, each server's owned
 //              positions are a contiguous bit range of its bitmap; a software
-//              pdep deposits them into the owner mask, and a popcount prefix of
-//              each bitmap locates the values.  Output order falls out of the
-//              global word order: no k-way merge.
+//              pdep deposits them into the owner mask; a tile's first output
+//              position is sum_s popcount_s(below the tile), so tiles are
+//              independent; warps expand set bits cooperatively (coalesced
+//              stores).  Output order falls out of the global word order.
 #include "zen_common.cuh"
 
 namespace zen {
@@ -115,11 +115,6 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
     if (w < nwords) {
       const uint32_t prefix = cprefix[chunk * n + s] + inc - c;
       own[w] = OwnWord{ms, prefix, 0u};
-      // select sample: the word holding rank q*kAggChunk
-      const uint64_t q = ((uint64_t)prefix + kAggChunk - 1) / kAggChunk;
-      const uint64_t r = q * kAggChunk;
-      if (c && r < (uint64_t)prefix + c && q < nsel)
-        sel[q] = (uint32_t)(w * 64 + select64(ms, (uint32_t)(r - prefix)));
     }
   }
 }
@@ -127,37 +122,28 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
 // ------------------------------------------------------------- aggregate ----
 
 constexpr int kAggThreads = 256;
+constexpr int kWPT = kPrefixBlockWords / 256;  // consecutive words per thread (8)
 
 __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
   return a.in_hdr ? *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s] : (uint32_t)a.in_count[w];
 }
 
-__device__ __forceinline__ void wait_push(const AggArgs& a) {
-  if (a.wait_push && threadIdx.x < a.n) {
+// Phase 1: every received entry sets its HashBitmap position (its rank in I_s,
+// zen/codec.hpp:146-158) in its worker's presence bitmap.
+__global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
+  __shared__ uint64_t pre[kMaxWorkers + 1];
+  const uint32_t n = a.n;
+  if (a.wait_push && threadIdx.x < n) {
     const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
     if (!wait_flag(&a.in_hdr[threadIdx.x]->flag, iter, kPeerTimeoutNs))
       atomicOr(&a.hdr->status, kErrTimeout);
   }
   __syncthreads();
-}
-
-__device__ __forceinline__ uint32_t rank_of(const OwnWord* own, uint32_t key) {
-  const OwnWord ow = own[key >> 6];
-  return ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
-}
-
-// Phase 1: rank of every received entry in I_s (HashBitmap position,
-// zen/codec.hpp:146-158) and, per worker, the first entry of every chunk.
-// Thread per (w, e) with e in [0, cnt_w] (e = cnt_w is the end sentinel).
-__global__ void __launch_bounds__(kAggThreads) k_agg_rank(AggArgs a) {
-  __shared__ uint64_t pre[kMaxWorkers + 1];
-  wait_push(a);
-  const uint32_t n = a.n;
   if (threadIdx.x == 0) {
     uint64_t acc = 0;
     for (uint32_t w = 0; w < n; ++w) {
       pre[w] = acc;
-      acc += (uint64_t)part_count(a, w) + 1;
+      acc += part_count(a, w);
     }
     pre[n] = acc;
   }
@@ -167,123 +153,190 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_rank(AggArgs a) {
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t w = 0;
     while (i >= pre[w + 1]) ++w;
-    const uint32_t e = (uint32_t)(i - pre[w]);
-    const uint32_t cnt = (uint32_t)(pre[w + 1] - pre[w] - 1);
-    const uint32_t* ix = a.in_idx[w];
-    int64_t c_e;
-    if (e < cnt) {
-      const uint32_t key = ix[e];
-      const OwnWord ow = a.own[key >> 6];
-      if (!((ow.mask >> (key & 63u)) & 1ull)) {
-        atomicMin((unsigned long long*)&a.hdr->bad_index, (unsigned long long)key);
-        atomicOr(&a.hdr->status, kErrOutside);
-      }
-      const uint32_t r = ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
-      a.rank[(uint64_t)w * a.cap + e] = r;
-      c_e = r / kAggChunk;
-    } else {
-      c_e = a.nq;
+    const uint32_t key = a.in_idx[w][i - pre[w]];
+    const OwnWord ow = a.own[key >> 6];
+    if (!((ow.mask >> (key & 63u)) & 1ull)) {
+      atomicMin((unsigned long long*)&a.hdr->bad_index, (unsigned long long)key);
+      atomicOr(&a.hdr->status, kErrOutside);
+      continue;
     }
-    const int64_t c_prev = e == 0 ? -1 : (int64_t)(rank_of(a.own, ix[e - 1]) / kAggChunk);
-    uint32_t* st = a.start + (uint64_t)w * (a.nq + 1);
-    for (int64_t c = c_prev + 1; c <= c_e; ++c) st[c] = e;
+    const uint32_t r = ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
+    atomicOr(a.pw + (uint64_t)w * a.nw + (r >> 6), 1ull << (r & 63u));
   }
 }
 
-// Phase 2: one block per chunk of kAggChunk ranks.  Workers are folded in
-// order 0..n-1 (the reference's left fold, zen/schemes.hpp:377-378), in shared
-// memory; zero sums stay present.  The chunk's 64 bitmap words go straight to
-// every destination; its values are compacted into a chunk-local staging slot.
-__global__ void __launch_bounds__(kAggThreads) k_agg_chunk(AggArgs a) {
-  __shared__ float acc[kAggChunk];
-  __shared__ uint32_t pres[kAggChunk / 32];
-  __shared__ uint32_t sscan[33];
-  const uint32_t n = a.n, q = blockIdx.x;
-  if (threadIdx.x < kAggChunk / 32) pres[threadIdx.x] = 0;
-  __syncthreads();
-  const uint32_t r0 = q * kAggChunk;
-  for (uint32_t w = 0; w < n; ++w) {
-    const uint32_t* st = a.start + (uint64_t)w * (a.nq + 1);
-    const uint32_t b = st[q], e = st[q + 1];
-    const uint32_t* __restrict__ rk = a.rank + (uint64_t)w * a.cap;
-    const float* __restrict__ vx = a.in_val[w];
-    for (uint32_t i = b + threadIdx.x; i < e; i += kAggThreads) {
-      const uint32_t r = rk[i] - r0;
-      const float v = vx[i];
-      const uint32_t m = 1u << (r & 31);
-      if (pres[r >> 5] & m) {
-        acc[r] += v;
-      } else {
-        acc[r] = v;
-        atomicOr(&pres[r >> 5], m);
-      }
-    }
-    __syncthreads();
-  }
-  const uint64_t nwords = (a.bs + 63) / 64;
-  if (threadIdx.x < kAggChunk / 64) {
-    const uint64_t j = (uint64_t)q * (kAggChunk / 64) + threadIdx.x;
-    if (j < nwords) {
-      const unsigned long long word = (unsigned long long)pres[2 * threadIdx.x] |
-                                      ((unsigned long long)pres[2 * threadIdx.x + 1] << 32);
-      for (uint32_t d = 0; d < a.ndst; ++d) a.dst_bits[d][j] = word;
-      if (a.dst_hdr) __threadfence_system();
-    }
-  }
-  // 16 ranks per thread, in rank order
-  const uint32_t bits16 = (pres[threadIdx.x >> 1] >> ((threadIdx.x & 1) * 16)) & 0xFFFFu;
-  uint32_t tot;
-  uint32_t pos = block_exclusive_sum((uint32_t)__popc(bits16), sscan, &tot);
-  float* stg = a.staging + (uint64_t)q * kAggChunk;
-  uint32_t b = bits16;
-  while (b) {
-    const uint32_t i = __ffs(b) - 1;
-    b &= b - 1;
-    stg[pos++] = acc[threadIdx.x * 16 + i];
-  }
-  if (threadIdx.x == 0) a.chunk_cnt[q] = tot;
-}
-
-__global__ void __launch_bounds__(1024) k_agg_scan(AggArgs a) {
-  __shared__ uint64_t sscan[33];
-  uint64_t carry = 0;
-  for (uint32_t b = 0; b < a.nq; b += blockDim.x) {
-    const uint32_t t = b + threadIdx.x;
-    const uint64_t v = t < a.nq ? a.chunk_cnt[t] : 0u;
-    uint64_t tot;
-    const uint64_t ex = block_exclusive_sum(v, sscan, &tot);
-    if (t < a.nq) a.chunk_base[t] = carry + ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) *a.agg_count = carry;
-}
-
-// Phase 4: one warp per chunk moves the staged values to their final position
-// in every destination (NVLink stores into peer pull inboxes in rank mode);
-// the last block publishes U_s and the pull flag with release semantics.
-__global__ void __launch_bounds__(256) k_agg_values(AggArgs a) {
+// Phase 2: U = OR_w P_w -> every destination; block-local popcount prefixes of
+// U and each P_w; the last block turns the block totals into exclusive
+// prefixes and records U_s.
+__global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
+  __shared__ uint32_t wsum[kMaxWorkers + 1][kAggThreads / 32];
   __shared__ uint32_t s_last;
-  const uint32_t q = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (q < a.nq) {
-    const uint32_t cnt = a.chunk_cnt[q];
-    const uint64_t base = a.chunk_base[q];
-    const float* stg = a.staging + (uint64_t)q * kAggChunk;
-    for (uint32_t j = lane_id(); j < cnt; j += 32) {
-      const float v = stg[j];
-      if (base + j < a.val_cap)
-        for (uint32_t d = 0; d < a.ndst; ++d) a.dst_vals[d][base + j] = v;
+  const uint32_t n = a.n, lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t j0 = (uint64_t)blockIdx.x * kPrefixBlockWords + (uint64_t)threadIdx.x * kWPT;
+  unsigned long long U[kWPT];
+  uint32_t cu[kWPT];
+#pragma unroll
+  for (int i = 0; i < kWPT; ++i) U[i] = 0;
+  // per worker: popcounts -> warp scan -> smem; OR into U
+  for (uint32_t x = 0; x <= n; ++x) {
+    uint32_t c[kWPT];
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < kWPT; ++i) {
+      const uint64_t j = j0 + i;
+      unsigned long long v = 0;
+      if (x < n) {
+        v = (j < a.nw) ? a.pw[(uint64_t)x * a.nw + j] : 0ull;
+        U[i] |= v;
+      } else {
+        v = U[i];
+      }
+      c[i] = __popcll(v);
+      t += c[i];
+    }
+    const uint32_t inc = warp_inclusive_sum(t);
+    if (lane == 31) wsum[x][warp] = inc;
+    // stash this thread's in-warp exclusive prefix + per-word prefix in `pre`
+    uint32_t run = inc - t;
+#pragma unroll
+    for (int i = 0; i < kWPT; ++i) {
+      cu[i] = run;  // temporarily the in-warp prefix
+      run += c[i];
+    }
+    uint32_t* out = a.pre + (uint64_t)x * a.nw;
+#pragma unroll
+    for (int i = 0; i < kWPT; ++i)
+      if (j0 + i < a.nw) out[j0 + i] = cu[i];
+  }
+  // write the union bitmap (the HashBitmap, LSB-first = little-endian words)
+#pragma unroll
+  for (int i = 0; i < kWPT; ++i) {
+    const uint64_t j = j0 + i;
+    if (j < a.nw)
+      for (uint32_t d = 0; d < a.ndst; ++d) a.dst_bits[d][j] = U[i];
+  }
+  __syncthreads();
+  // add the cross-warp prefix to the stored in-warp prefixes; block totals
+  for (uint32_t x = 0; x <= n; ++x) {
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kAggThreads / 32; ++w) {
+      const uint32_t v = wsum[x][w];
+      wpre += (w < (int)warp) ? v : 0u;
+      tot += v;
+    }
+    if (wpre) {
+      uint32_t* out = a.pre + (uint64_t)x * a.nw;
+#pragma unroll
+      for (int i = 0; i < kWPT; ++i)
+        if (j0 + i < a.nw) out[j0 + i] += wpre;
+    }
+    if (threadIdx.x == 0) a.blk[(uint64_t)x * a.nblk + blockIdx.x] = tot;
+  }
+  // last block: exclusive prefix of the block totals (one warp per bitmap)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (atomicAdd(&a.done[0], 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (uint32_t x = warp; x <= n; x += kAggThreads / 32) {
+    volatile uint32_t* b = a.blk + (uint64_t)x * a.nblk;
+    uint32_t carry = 0;
+    for (uint32_t i0 = 0; i0 < a.nblk; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t v = i < a.nblk ? b[i] : 0u;
+      const uint32_t inc = warp_inclusive_sum(v);
+      if (i < a.nblk) b[i] = carry + inc - v;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (x == n && lane == 0) *a.agg_count = carry;
+  }
+  if (threadIdx.x == 0) a.done[0] = 0;
+}
+
+// Phase 3: one thread per bitmap word stages its words in shared memory; the
+// warp then expands the union bits cooperatively (one output value per lane,
+// consecutive lanes -> consecutive positions).  Value of a union bit = fold
+// of its contributors' values in ascending worker order (zen/tensor.hpp:151-153).
+constexpr int kValThreads = 128;
+
+template <int NMAX>
+__global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
+  __shared__ unsigned long long spw[kValThreads][NMAX];
+  __shared__ uint32_t sbase[kValThreads][NMAX];
+  __shared__ uint32_t s_last;
+  const uint32_t n = a.n, lane = lane_id();
+  const uint64_t j = (uint64_t)blockIdx.x * kValThreads + threadIdx.x;
+  const bool valid = j < a.nw;
+  const uint32_t pb = (uint32_t)(j / kPrefixBlockWords);
+  unsigned long long U = 0;
+#pragma unroll
+  for (int w = 0; w < NMAX; ++w) {
+    unsigned long long v = 0;
+    uint32_t b = 0;
+    if (w < (int)n && valid) {
+      v = a.pw[(uint64_t)w * a.nw + j];
+      if (v) b = a.blk[(uint64_t)w * a.nblk + pb] + a.pre[(uint64_t)w * a.nw + j];
+    }
+    spw[threadIdx.x][w] = v;
+    sbase[threadIdx.x][w] = b;
+    U |= v;
+  }
+  const uint64_t ubase = (valid && U) ? (uint64_t)a.blk[(uint64_t)n * a.nblk + pb] +
+                                            a.pre[(uint64_t)n * a.nw + j] : 0ull;
+  const uint32_t c = __popcll(U);
+  const uint32_t inc = warp_inclusive_sum(c);
+  const uint32_t x = inc - c;
+  const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+  // output position of the warp's first value = ubase of its first non-empty lane
+  const uint32_t first = __ffs(__ballot_sync(0xffffffffu, c != 0));
+  const uint64_t wbase = first ? __shfl_sync(0xffffffffu, ubase, first - 1) : 0ull;
+  const uint32_t row0 = threadIdx.x & ~31u;
+  __syncwarp();
+  for (uint32_t k0 = 0; k0 < T; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    uint32_t L = 0;
+#pragma unroll
+    for (uint32_t step = 16; step >= 1; step >>= 1) {
+      const uint32_t xc = __shfl_sync(0xffffffffu, x, L + step);
+      if (xc <= k) L += step;
+    }
+    const unsigned long long UL = __shfl_sync(0xffffffffu, U, L);
+    const uint32_t xL = __shfl_sync(0xffffffffu, x, L);
+    if (k < T) {
+      const uint32_t bit = select64(UL, k - xL);
+      const uint64_t lm = lowmask64(bit);
+      float v = 0.0f;
+      bool seen = false;
+#pragma unroll
+      for (int w = 0; w < NMAX; ++w) {
+        if (w < (int)n) {
+          const unsigned long long pwv = spw[row0 + L][w];
+          if ((pwv >> bit) & 1ull) {
+            const float t = a.in_val[w][sbase[row0 + L][w] + __popcll(pwv & lm)];
+            v = seen ? v + t : t;
+            seen = true;
+          }
+        }
+      }
+      const uint64_t pos = wbase + k;
+      if (pos < a.val_cap)
+        for (uint32_t d = 0; d < a.ndst; ++d) a.dst_vals[d][pos] = v;
     }
   }
   if (!a.dst_hdr) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    const uint32_t d = atomicAdd(a.done, 1u);
-    s_last = (d == gridDim.x - 1) ? 1u : 0u;
-    if (s_last) *a.done = 0;
+    const uint32_t dn = atomicAdd(&a.done[1], 1u);
+    s_last = (dn == gridDim.x - 1) ? 1u : 0u;
+    if (s_last) a.done[1] = 0;
   }
   __syncthreads();
-  if (s_last) {
+  if (s_last) {  // pull signalling: publish U_s, then the flag (release, system scope)
     __threadfence_system();
     const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
     const uint64_t u = *(volatile uint64_t*)a.agg_count;
@@ -303,11 +356,12 @@ __global__ void __launch_bounds__(256) k_agg_values(AggArgs a) {
 
 // ---------------------------------------------------------------- decode ----
 
-// word popcount prefix of each server's bitmap, block-local (8192 words per
-// block; 256 threads x 32 contiguous words)
-__global__ void __launch_bounds__(256) k_bpre(DecodeArgs a, const uint32_t* blk_start,
-                                             const uint64_t* nwords_s) {
+// Word popcount prefix of each server's bitmap: block-local (2048 words per
+// block, 8 consecutive words per thread) + block totals; the last block turns
+// the totals into exclusive prefixes, per-server popcounts and |result|.
+__global__ void __launch_bounds__(256) k_bpre(DecodeArgs a) {
   __shared__ uint32_t sscan[33];
+  __shared__ uint32_t s_last;
   const uint32_t n = a.n;
   if (a.wait_pull && threadIdx.x < n) {
     const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
@@ -317,15 +371,15 @@ __global__ void __launch_bounds__(256) k_bpre(DecodeArgs a, const uint32_t* blk_
   }
   __syncthreads();
   uint32_t s = 0;
-  while (s + 1 < n && blockIdx.x >= blk_start[s + 1]) ++s;
-  const uint32_t blk = blockIdx.x - blk_start[s];
+  while (s + 1 < n && blockIdx.x >= a.blk_start[s + 1]) ++s;
+  const uint32_t blk = blockIdx.x - a.blk_start[s];
   const unsigned long long* bits = a.bits[s];
-  const uint64_t nw = nwords_s[s];
-  const uint64_t w0 = (uint64_t)blk * kPrefixBlockWords + threadIdx.x * 32ull;
-  uint32_t c[32];
+  const uint64_t nw = a.nwords_s[s];
+  const uint64_t w0 = (uint64_t)blk * kPrefixBlockWords + threadIdx.x * (uint64_t)kWPT;
+  uint32_t c[kWPT];
   uint32_t local = 0;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < kWPT; ++i) {
     c[i] = local;
     const uint64_t w = w0 + i;
     local += (bits && w < nw) ? (uint32_t)__popcll(bits[w]) : 0u;
@@ -334,80 +388,79 @@ __global__ void __launch_bounds__(256) k_bpre(DecodeArgs a, const uint32_t* blk_
   const uint32_t ex = block_exclusive_sum(local, sscan, &tot);
   uint32_t* out = a.bpre + s * a.words_stride;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < kWPT; ++i) {
     const uint64_t w = w0 + i;
     if (w < nw) out[w] = ex + c[i];
   }
-  if (threadIdx.x == 0) a.bpre_blk[s * a.blk_stride + blk] = tot;
-}
-
-// popcount of server s's bitmap bits [0, P)
-__device__ __forceinline__ uint64_t bitmap_prefix(const DecodeArgs& a, uint32_t s, uint64_t P,
-                                                  uint64_t nw) {
-  const uint64_t j = P >> 6;
-  const uint32_t o = (uint32_t)(P & 63);
-  if (j >= nw) return a.popc_total[s];
-  const unsigned long long* bits = a.bits[s];
-  return (uint64_t)a.bpre_blk[s * a.blk_stride + j / kPrefixBlockWords] +
-         a.bpre[s * a.words_stride + j] + (uint64_t)__popcll(bits[j] & lowmask64(o));
-}
-
-// One block: finish the bitmap prefixes (scan of block sums per server), then
-// the output size of every decode tile straight from the tables -- for server
-// s a tile covers the bit range [P_s(t), P_s(t+1)) of its bitmap -- and their
-// exclusive scan.  No data pass, no look-back.
-__global__ void __launch_bounds__(1024) k_dec_plan(DecodeArgs a, const uint32_t* blk_start,
-                                                   const uint64_t* nwords_s, uint32_t ntiles,
-                                                   uint64_t nchunks) {
-  __shared__ uint64_t sscan[33];
-  const uint32_t n = a.n;
-  {
-    const uint32_t s = threadIdx.x >> 5;
-    if (s < n) {
-      const uint32_t nb = blk_start[s + 1] - blk_start[s];
-      uint32_t* b = a.bpre_blk + s * a.blk_stride;
-      uint32_t carry = 0;
-      for (uint32_t i0 = 0; i0 < nb; i0 += 32) {
-        const uint32_t i = i0 + lane_id();
-        const uint32_t v = i < nb ? b[i] : 0u;
-        const uint32_t inc = warp_inclusive_sum(v);
-        if (i < nb) b[i] = carry + inc - v;
-        carry += __shfl_sync(0xffffffffu, inc, 31);
-      }
-      if (lane_id() == 0) a.popc_total[s] = carry;
+  if (threadIdx.x == 0) {
+    a.bpre_blk[s * a.blk_stride + blk] = tot;
+    __threadfence();
+    s_last = (atomicAdd(a.done, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  __shared__ uint64_t totals[kMaxWorkers];
+  for (uint32_t x = warp; x < n; x += 8) {
+    const uint32_t nb = a.blk_start[x + 1] - a.blk_start[x];
+    volatile uint32_t* b = a.bpre_blk + x * a.blk_stride;
+    uint32_t carry = 0;
+    for (uint32_t i0 = 0; i0 < nb; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t v = i < nb ? b[i] : 0u;
+      const uint32_t inc = warp_inclusive_sum(v);
+      if (i < nb) b[i] = carry + inc - v;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) {
+      a.popc_total[x] = carry;
+      totals[x] = carry;
     }
   }
   __syncthreads();
-  uint64_t carry = 0;
-  constexpr uint32_t kChunksPerTile = kDecodeTileWords / 32;
-  for (uint32_t b = 0; b < ntiles; b += blockDim.x) {
-    const uint32_t t = b + threadIdx.x;
-    uint64_t v = 0;
-    if (t < ntiles) {
-      const uint64_t c0 = (uint64_t)t * kChunksPerTile, c1 = c0 + kChunksPerTile;
-      for (uint32_t s = 0; s < n; ++s) {
-        if (!a.bits[s]) continue;
-        const uint64_t nw = nwords_s[s];
-        const uint64_t P0 = a.cprefix[c0 * n + s];
-        const uint64_t P1 = c1 < nchunks ? (uint64_t)a.cprefix[c1 * n + s] : a.bs[s];
-        v += bitmap_prefix(a, s, P1, nw) - bitmap_prefix(a, s, P0, nw);
-      }
-    }
-    uint64_t tot;
-    const uint64_t ex = block_exclusive_sum(v, sscan, &tot);
-    if (t < ntiles) a.tile_base[t] = carry + ex;
-    carry += tot;
+  if (threadIdx.x == 0) {
+    uint64_t u = 0;
+    for (uint32_t x = 0; x < n; ++x) u += totals[x];
+    *a.out_count = u;
+    *a.done = 0;
   }
-  if (threadIdx.x == 0) *a.out_count = carry;
 }
 
+// popcount of server s's bitmap bits [0, P)
+__device__ __forceinline__ uint64_t bitmap_prefix(const DecodeArgs& a, uint32_t s, uint64_t P) {
+  const uint64_t j = P >> 6;
+  const uint32_t o = (uint32_t)(P & 63);
+  if (j >= a.nwords_s[s]) return a.popc_total[s];
+  return (uint64_t)a.bpre_blk[s * a.blk_stride + j / kPrefixBlockWords] +
+         a.bpre[s * a.words_stride + j] + (uint64_t)__popcll(a.bits[s][j] & lowmask64(o));
+}
+
+// One block per 256 global words.  The tile's first output position is the
+// number of set bits of all servers below the tile -- sum_s prefix_s(P_s(tile))
+// -- so no scan over tiles is needed.  Per word, each server's owned
+// positions are a contiguous bit range of its bitmap (deposited into the owner
+// mask); the warp then expands its set bits cooperatively.
 template <int NMAX>
-__global__ void __launch_bounds__(256) k_decode(DecodeArgs a, uint64_t nwords) {
+__global__ void __launch_bounds__(kDecodeTileWords) k_decode(DecodeArgs a, uint64_t nwords) {
+  __shared__ unsigned long long spres[kDecodeTileWords][NMAX];
+  __shared__ uint32_t svb[kDecodeTileWords][NMAX];
   __shared__ uint32_t sscan[33];
-  const uint32_t n = a.n;
+  __shared__ uint64_t s_tile_base;
+  const uint32_t n = a.n, lane = lane_id();
   const uint32_t tile = blockIdx.x;
   const uint64_t w = (uint64_t)tile * kDecodeTileWords + threadIdx.x;
   const bool valid = w < nwords;
+  if (threadIdx.x < 32) {
+    uint64_t b = 0;
+    if (lane < n && a.bits[lane]) {
+      const uint64_t c0 = (uint64_t)tile * (kDecodeTileWords / 32);
+      b = bitmap_prefix(a, lane, a.cprefix[c0 * n + lane]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (lane == 0) s_tile_base = b;
+  }
   unsigned long long pl[4] = {0, 0, 0, 0};
   const uint64_t vmask = valid ? valid_mask(a.m, w) : 0ull;
   if (valid) {
@@ -416,13 +469,11 @@ __global__ void __launch_bounds__(256) k_decode(DecodeArgs a, uint64_t nwords) {
       if (j < a.nplanes) pl[j] = a.planes[w * a.nplanes + j];
   }
   const uint64_t chunk = w >> 5;
-  uint64_t pres[NMAX];
-  uint32_t vbase[NMAX];
   uint64_t G = 0;
 #pragma unroll
   for (int s = 0; s < NMAX; ++s) {
-    pres[s] = 0;
-    vbase[s] = 0;
+    unsigned long long pres = 0;
+    uint32_t vb = 0;
     if (s < (int)n) {
       const uint64_t ms = owner_mask4(pl, a.nplanes, (uint32_t)s, vmask);
       const uint32_t c = __popcll(ms);
@@ -433,34 +484,55 @@ __global__ void __launch_bounds__(256) k_decode(DecodeArgs a, uint64_t nwords) {
         const uint64_t j = P >> 6;
         const uint32_t o = (uint32_t)(P & 63);
         const unsigned long long w0 = bits[j];
-        uint64_t x = w0 >> o;
-        if (o + c > 64) x |= (uint64_t)bits[j + 1] << (64 - o);
-        x &= lowmask64(c);
-        if (x) {
-          pres[s] = (c == 64) ? x : deposit64(x, ms);
-          vbase[s] = a.bpre_blk[s * a.blk_stride + j / kPrefixBlockWords] +
-                     a.bpre[s * a.words_stride + j] + (uint32_t)__popcll(w0 & lowmask64(o));
-          G |= pres[s];
+        uint64_t xb = w0 >> o;
+        if (o + c > 64) xb |= (uint64_t)bits[j + 1] << (64 - o);
+        xb &= lowmask64(c);
+        if (xb) {
+          pres = (c == 64) ? xb : deposit64(xb, ms);
+          vb = a.bpre_blk[s * a.blk_stride + j / kPrefixBlockWords] +
+               a.bpre[s * a.words_stride + j] + (uint32_t)__popcll(w0 & lowmask64(o));
+          G |= pres;
         }
       }
     }
+    spres[threadIdx.x][s] = pres;
+    svb[threadIdx.x][s] = vb;
   }
+  const uint32_t cnt = __popcll(G);
   uint32_t tot;
-  const uint32_t ex = block_exclusive_sum((uint32_t)__popcll(G), sscan, &tot);
-  uint64_t pos = a.tile_base[tile] + ex;
-  while (G) {
-    const uint32_t i = __ffsll((long long)G) - 1;
-    G &= G - 1;
-    float v = 0.0f;
+  const uint32_t bex = block_exclusive_sum(cnt, sscan, &tot);  // syncs: smem visible
+  const uint32_t inc = warp_inclusive_sum(cnt);
+  const uint32_t x = inc - cnt;
+  const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+  const uint64_t wbase = s_tile_base + __shfl_sync(0xffffffffu, bex - x, 0);
+  const uint32_t row0 = threadIdx.x & ~31u;
+  for (uint32_t k0 = 0; k0 < T; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    uint32_t L = 0;
 #pragma unroll
-    for (int s = 0; s < NMAX; ++s) {
-      if ((pres[s] >> i) & 1ull) v = a.vals[s][vbase[s] + __popcll(pres[s] & lowmask64(i))];
+    for (uint32_t step = 16; step >= 1; step >>= 1) {
+      const uint32_t xc = __shfl_sync(0xffffffffu, x, L + step);
+      if (xc <= k) L += step;
     }
-    if (pos < a.out_cap) {
-      a.out_idx[pos] = w * 64 + i;
-      a.out_val[pos] = v;
+    const unsigned long long GL = __shfl_sync(0xffffffffu, G, L);
+    const uint32_t xL = __shfl_sync(0xffffffffu, x, L);
+    if (k < T) {
+      const uint32_t bit = select64(GL, k - xL);
+      const uint64_t lm = lowmask64(bit);
+      float v = 0.0f;
+#pragma unroll
+      for (int s = 0; s < NMAX; ++s) {
+        if (s < (int)n) {
+          const unsigned long long p = spres[row0 + L][s];
+          if ((p >> bit) & 1ull) v = a.vals[s][svb[row0 + L][s] + __popcll(p & lm)];
+        }
+      }
+      const uint64_t pos = wbase + k;
+      if (pos < a.out_cap) {
+        a.out_idx[pos] = ((uint64_t)tile * kDecodeTileWords + row0 + L) * 64 + bit;
+        a.out_val[pos] = v;
+      }
     }
-    ++pos;
   }
 }
 
@@ -497,30 +569,37 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
 }
 
 void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
-  uint64_t tot_cap = (uint64_t)a.n * (a.cap + 1);
-  k_agg_rank<<<grid_for(tot_cap, kAggThreads, 148 * 8), kAggThreads, 0, stream>>>(a);
-  k_agg_chunk<<<a.nq, kAggThreads, 0, stream>>>(a);
-  k_agg_scan<<<1, 1024, 0, stream>>>(a);
-  k_agg_values<<<(a.nq + 7) / 8, 256, 0, stream>>>(a);
-  for (int i = 0; i < 4; ++i) count_launch();
+  uint64_t cap_entries = 0;
+  (void)cap_entries;
+  cudaMemsetAsync(a.pw, 0, (size_t)a.n * a.nw * 8, stream);
+  k_agg_mark<<<148 * 8, kAggThreads, 0, stream>>>(a);
+  k_agg_union<<<a.nblk, kAggThreads, 0, stream>>>(a);
+  const unsigned g = (unsigned)((a.nw + kValThreads - 1) / kValThreads);
+  if (a.n <= 2)
+    k_agg_values<2><<<g, kValThreads, 0, stream>>>(a);
+  else if (a.n <= 4)
+    k_agg_values<4><<<g, kValThreads, 0, stream>>>(a);
+  else if (a.n <= 8)
+    k_agg_values<8><<<g, kValThreads, 0, stream>>>(a);
+  else
+    k_agg_values<16><<<g, kValThreads, 0, stream>>>(a);
+  for (int i = 0; i < 3; ++i) count_launch();
 }
 
-void launch_decode_parts(const DecodeArgs& a, const uint32_t* d_blk_start,
-                         const uint64_t* d_nwords_s, uint32_t total_blocks, cudaStream_t stream) {
+void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {
   const uint64_t nwords = (a.m + 63) / 64;
   const uint32_t ntiles = (uint32_t)((nwords + kDecodeTileWords - 1) / kDecodeTileWords);
-  const uint64_t nchunks = (nwords + 31) / 32;
-  k_bpre<<<total_blocks ? total_blocks : 1, 256, 0, stream>>>(a, d_blk_start, d_nwords_s);
-  k_dec_plan<<<1, 1024, 0, stream>>>(a, d_blk_start, d_nwords_s, ntiles, nchunks);
+  k_bpre<<<a.total_blocks ? a.total_blocks : 1, 256, 0, stream>>>(a);
+  constexpr unsigned T = kDecodeTileWords;
   if (a.n <= 2)
-    k_decode<2><<<ntiles, 256, 0, stream>>>(a, nwords);
+    k_decode<2><<<ntiles, T, 0, stream>>>(a, nwords);
   else if (a.n <= 4)
-    k_decode<4><<<ntiles, 256, 0, stream>>>(a, nwords);
+    k_decode<4><<<ntiles, T, 0, stream>>>(a, nwords);
   else if (a.n <= 8)
-    k_decode<8><<<ntiles, 256, 0, stream>>>(a, nwords);
+    k_decode<8><<<ntiles, T, 0, stream>>>(a, nwords);
   else
-    k_decode<16><<<ntiles, 256, 0, stream>>>(a, nwords);
-  for (int i = 0; i < 3; ++i) count_launch();
+    k_decode<16><<<ntiles, T, 0, stream>>>(a, nwords);
+  for (int i = 0; i < 2; ++i) count_launch();
 }
 
 }  // namespace zen

@@ -13,9 +13,9 @@ constexpr uint32_t kMaxPartitions = 512;   // n for the standalone hash
 constexpr uint32_t kMaxWorkers = 16;    // n for the fused BP pipeline
 constexpr uint32_t kHashTile = 2048;    // keys per hash tile (256 threads x 8)
 constexpr uint32_t kExtractTile = 8192; // floats per extraction tile
-constexpr uint32_t kAggChunk = 4096;    // ranks per aggregate/encode chunk
-constexpr uint32_t kDecodeTileWords = 256;  // 64-index words per decode tile
-constexpr uint32_t kPrefixBlockWords = 8192;  // bitmap words per popcount-prefix block
+constexpr uint32_t kDecodeTileWords = 128;  // 64-index words per decode tile (= block size)
+constexpr uint32_t kPrefixBlockWords = 2048;  // bitmap words per popcount-prefix block
+                                              // (256 threads x 8 consecutive words)
 constexpr uint64_t kKeyBits = 40;       // slot word: [63:40] epoch, [39:0] index+1
 constexpr uint64_t kKeyMask = (1ull << kKeyBits) - 1ull;
 constexpr uint64_t kPeerTimeoutNs = 30ull * 1000ull * 1000ull * 1000ull;
@@ -169,9 +169,16 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
                        const unsigned long long* planes, const uint32_t* cprefix, OwnWord* own,
                        uint32_t* sel, uint64_t nsel, cudaStream_t stream);
 
-// aggregate + HashBitmap encode of one server (fused), look-back free:
-// rank (+ chunk starts) | chunk accumulate (+ bitmap words to every
-// destination) | scan | values to every destination (+ pull signalling).
+// aggregate + HashBitmap encode of one server, look-back free and
+// proportional to (bitmap words + entries):
+//  mark   : every received entry sets its rank bit in its worker's presence
+//           bitmap P_w (a part is sorted by rank, so entry i of part w is the
+//           i-th set bit of P_w);
+//  union  : U = OR_w P_w, written straight into every destination's pull
+//           inbox (the HashBitmap, NVLink stores in rank mode), plus popcount
+//           prefixes of U and of every P_w;
+//  values : per set bit of U, fold the contributors' values in worker order
+//           (the reference's left fold) and store the value at its rank in U.
 struct AggArgs {
   uint32_t n, s;
   uint64_t m;
@@ -181,14 +188,12 @@ struct AggArgs {
   const uint64_t* in_count;       // [n] counts when in_hdr == nullptr
   const OwnWord* own;
   uint64_t bs;                    // |I_s|
-  uint32_t nq;                    // chunks = ceil(bs / kAggChunk) (>= 1)
-  uint64_t cap;                   // per-part capacity (rank scratch stride)
-  uint32_t* rank;                 // [n * cap]
-  uint32_t* start;                // [n * (nq + 1)]
-  float* staging;                 // [nq * kAggChunk]
-  uint32_t* chunk_cnt;            // [nq]
-  uint64_t* chunk_base;           // [nq]
-  uint32_t* done;                 // blocks-finished counter (self-resetting)
+  uint64_t nw;                    // ceil(bs / 64) (>= 1)
+  uint32_t nblk;                  // ceil(nw / kPrefixBlockWords)
+  unsigned long long* pw;         // [n * nw] per-worker presence, zeroed per sync
+  uint32_t* pre;                  // [(n + 1) * nw] block-local exclusive popcounts (U = n)
+  uint32_t* blk;                  // [(n + 1) * nblk] block totals -> exclusive prefixes
+  uint32_t* done;                 // [2] blocks-finished counters (self-resetting)
   uint32_t ndst;
   unsigned long long* const* dst_bits;  // [ndst]
   float* const* dst_vals;               // [ndst]
@@ -210,12 +215,15 @@ struct DecodeArgs {
   const unsigned long long* const* bits;   // [n] (nullptr: server absent)
   const float* const* vals;                // [n]
   const uint64_t* bs;                      // [n] |I_s| (device)
+  const uint64_t* nwords_s;                // [n] bitmap words per server (device)
+  const uint32_t* blk_start;               // [n + 1] first prefix block of each server
+  uint32_t total_blocks;
   const PullHdr* const* pull_hdr;          // [n] or nullptr
-  uint32_t* bpre;                          // [n * words_stride] word popcount prefix (local)
-  uint32_t* bpre_blk;                      // [n * blk_stride]
+  uint32_t* bpre;                          // [n * words_stride] block-local word popcount prefix
+  uint32_t* bpre_blk;                      // [n * blk_stride] block totals -> exclusive prefix
   uint64_t words_stride;                   // per-server stride in bpre
   uint64_t blk_stride;
-  uint64_t* tile_base;                     // [ntiles] output offset of each decode tile
+  uint32_t* done;                          // blocks-finished counter (self-resetting)
   uint64_t* out_idx;
   float* out_val;
   uint64_t* out_count;
@@ -224,9 +232,7 @@ struct DecodeArgs {
   int wait_pull;
   uint32_t* popc_total;                    // [n] per-server popcount (malformed check)
 };
-// d_blk_start[n+1]: first prefix block of each server; d_nwords_s[n]: bitmap words
-void launch_decode_parts(const DecodeArgs& a, const uint32_t* d_blk_start,
-                         const uint64_t* d_nwords_s, uint32_t total_blocks, cudaStream_t stream);
+void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream);
 
 // small helpers
 void launch_u64_to_u32(const uint64_t* in, uint32_t* out, uint64_t n, cudaStream_t stream);
