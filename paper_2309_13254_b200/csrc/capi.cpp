@@ -324,6 +324,7 @@ zen_status zen_hierarchical_hash(zen_ctx* c, const uint64_t* d_idx, const float*
   a.out_idx = d_out_idx;
   a.out_val = d_out_val;
   a.cap = cap;
+  a.tiles_cap = ntiles;
   a.stride_cap = stride;
   HashHdr h{};
   h.count = count;
@@ -839,6 +840,7 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   CKR(mem.alloc(&a.stats_out, ZEN_MAX_K + 1));
   a.dst_table = 1;
   a.cap = cap;
+  a.tiles_cap = ntiles;
   a.dst_cap = cap;
   a.stride_cap = bp->stride_cap;
   a.me = w.id;
@@ -1179,14 +1181,12 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   if (from_dense) {
     for (size_t i = 0; i < bp->workers.size(); ++i) {
       Worker& w = bp->workers[i];
-      launch_extract_tiles<uint32_t>(dense[i], bp->m, w.ex, &w.a.hdr->count, bp->cap,
-                                     &w.a.hdr->status, st);
+      launch_extract_tiles_begin<uint32_t>(dense[i], bp->m, w.ex, w.a, bp->cap, st);
     }
   }
   if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
   for (auto& w : bp->workers) {
     if (from_dense) {  // compaction of the staged non-zeros fused with the placement
-      launch_hash_begin<uint32_t>(w.a, st);
       launch_extract_compact_place<uint32_t>(bp->m, w.ex, w.keys, w.vals, bp->cap, w.a.fam,
                                              w.a.hdr, w.a.slots, st);
       launch_hash_rest<uint32_t>(w.a, bp->n, bp->params.rehash_depth, st);

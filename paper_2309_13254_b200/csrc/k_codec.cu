@@ -155,13 +155,20 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
     while (i >= pre[w + 1]) ++w;
     const uint32_t key = a.in_idx[w][i - pre[w]];
     const OwnWord ow = a.own[key >> 6];
-    if (!((ow.mask >> (key & 63u)) & 1ull)) {
+    const bool owned = (ow.mask >> (key & 63u)) & 1ull;
+    if (!owned) {
       atomicMin((unsigned long long*)&a.hdr->bad_index, (unsigned long long)key);
       atomicOr(&a.hdr->status, kErrOutside);
-      continue;
     }
     const uint32_t r = ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
-    atomicOr(a.pw + (uint64_t)w * a.nw + (r >> 6), 1ull << (r & 63u));
+    // consecutive keys share bitmap words: one atomic per distinct word per warp
+    unsigned long long* word = owned ? a.pw + (uint64_t)w * a.nw + (r >> 6) : nullptr;
+    const uint64_t bit = owned ? 1ull << (r & 63u) : 0ull;
+    const uint32_t grp = __match_any_sync(__activemask(), (unsigned long long)word);
+    const uint32_t lo = __reduce_or_sync(grp, (uint32_t)bit);
+    const uint32_t hi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
+    if (owned && lane_id() == (uint32_t)(__ffs(grp) - 1))
+      atomicOr(word, ((unsigned long long)hi << 32) | lo);
   }
 }
 

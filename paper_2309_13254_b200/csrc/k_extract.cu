@@ -12,11 +12,15 @@
 //     embedding rows cost only their read); per-iteration warp scans give each
 //     lane its in-order offset, and the tile's non-zeros land tile-locally in a
 //     staging area.  Fully parallel: every block is independent.
-//  2. k_extract_scan: one block scans the per-tile counts.
-//  3. k_extract_compact: one warp per tile moves its staged entries to the
-//     final ascending position.  In the BP pipeline the same pass runs the
-//     hierarchical hash's priority claim for every key it moves (fused place).
+//  2. k_extract_scan: one block scans the per-tile counts (in the BP pipeline
+//     the same block then starts the hash run: r1/r2 from the count).
+//  3. k_extract_compact: one thread per output position finds its tile by a
+//     binary search over the tile bases (balanced however skewed the tiles
+//     are) and moves the entry to its final ascending position.  In the BP
+//     pipeline the same thread runs the hierarchical hash's priority claim for
+//     the key it moves (fused place).
 #include "zen_common.cuh"
+#include "zen_hash_dev.cuh"
 
 namespace zen {
 extern void count_launch();
@@ -100,88 +104,71 @@ __global__ void __launch_bounds__(kThreads, 4)
   }
 }
 
+template <typename K, bool BEGIN>
 __global__ void __launch_bounds__(1024) k_extract_scan(uint32_t* __restrict__ tile_cnt,
                                                        uint32_t ntiles, uint64_t* d_count,
                                                        uint64_t capacity, uint32_t* err,
-                                                       uint64_t* tile_base) {
+                                                       uint64_t* tile_base, HashArgs<K> ha) {
   __shared__ uint64_t sscan[33];
+  constexpr int E = 8;
   uint64_t carry = 0;
-  for (uint32_t b = 0; b < ntiles; b += blockDim.x) {
-    const uint32_t t = b + threadIdx.x;
-    const uint64_t v = t < ntiles ? tile_cnt[t] : 0u;
+  for (uint32_t b = 0; b < ntiles; b += blockDim.x * E) {
+    const uint32_t t0 = b + threadIdx.x * E;
+    uint32_t v[E];
+    uint64_t local = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      v[e] = (t0 + e < ntiles) ? tile_cnt[t0 + e] : 0u;
+      local += v[e];
+    }
     uint64_t tot;
-    const uint64_t ex = block_exclusive_sum(v, sscan, &tot);
-    if (t < ntiles) tile_base[t] = carry + ex;
+    uint64_t ex = carry + block_exclusive_sum(local, sscan, &tot);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (t0 + e < ntiles) tile_base[t0 + e] = ex;
+      ex += v[e];
+    }
     carry += tot;
   }
   if (threadIdx.x == 0) {
     *d_count = carry;
     if (carry > capacity) atomicOr(err, kErrCapacity);
   }
-}
-
-__device__ __forceinline__ uint64_t epoch_word(uint32_t epoch) {
-  return (uint64_t)(0xFFFFFFu - (epoch & 0xFFFFFFu)) << kKeyBits;
-}
-
-// Priority claim of one key (see k_hash.cu): smallest key wins every slot.
-__device__ __forceinline__ void place_key(const DevFamily& fam, unsigned long long* slots,
-                                          uint64_t key, uint64_t r1, uint64_t stride, uint64_t ew) {
-  const uint32_t p = part_of(fam, key);
-  unsigned long long* base = slots + (uint64_t)p * stride;
-  uint64_t cur = key;
-  uint32_t t = 0;
-  const uint32_t k = fam.k;
-  while (true) {
-    const uint64_t c = slot_of(fam, cur, t, r1);
-    const unsigned long long old = atomicMin(base + c, (unsigned long long)(ew | cur));
-    if (old > (ew | kKeyMask)) break;
-    const uint64_t ok = old & kKeyMask;
-    if (ok > cur) {
-      cur = ok;
-      uint32_t f = 0;
-      while (f < k && slot_of(fam, cur, f, r1) != c) ++f;
-      t = f + 1;
-    } else {
-      ++t;
-    }
-    if (t >= k) break;
+  if (BEGIN) {
+    __syncthreads();
+    hash_begin_body(ha);
   }
 }
 
-// one warp per extraction tile; optionally fuses the hash placement
+// one thread per output position (balanced); optionally fuses the placement
 template <typename K, bool PLACE>
 __global__ void __launch_bounds__(256)
     k_extract_compact(const K* __restrict__ st_idx, const float* __restrict__ st_val,
-                      const uint32_t* __restrict__ tile_cnt, const uint64_t* __restrict__ tile_base,
-                      uint32_t ntiles, K* __restrict__ out_idx, float* __restrict__ out_val,
-                      uint64_t capacity, DevFamily fam, HashHdr* hdr,
-                      unsigned long long* slots) {
-  const uint32_t tile = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (tile >= ntiles) return;
-  uint64_t r1 = 0, stride = 0, ew = 0;
-  bool place = PLACE;
-  if (PLACE) {
-    place = !(hdr->status & kErrCapacity);
-    r1 = hdr->r1;
-    stride = hdr->stride;
-    ew = epoch_word(hdr->epoch);
+                      const uint64_t* __restrict__ tile_base, uint32_t ntiles,
+                      const uint64_t* d_count, K* __restrict__ out_idx,
+                      float* __restrict__ out_val, uint64_t capacity, DevFamily fam,
+                      HashHdr* hdr, unsigned long long* slots) {
+  const uint64_t z = *d_count;
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= z || i >= capacity) return;
+  uint32_t lo = 0, hi = ntiles;  // largest t with tile_base[t] <= i
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (tile_base[mid] <= i) lo = mid; else hi = mid;
   }
-  const uint32_t cnt = tile_cnt[tile];
-  const uint64_t base = tile_base[tile];
-  const uint64_t src = (uint64_t)tile * kExtractTile;
-  for (uint32_t j = lane_id(); j < cnt; j += 32) {
-    const K x = st_idx[src + j];
-    const float v = st_val[src + j];
-    if (base + j < capacity) {
-      out_idx[base + j] = x;
-      out_val[base + j] = v;
-      if (PLACE && place) place_key(fam, slots, (uint64_t)x + 1, r1, stride, ew);
-    }
+  const uint64_t src = (uint64_t)lo * kExtractTile + (i - tile_base[lo]);
+  const K x = st_idx[src];
+  out_idx[i] = x;
+  out_val[i] = st_val[src];
+  if (PLACE) {
+    if (hdr->status & kErrCapacity) return;
+    place_key(fam, slots, (uint64_t)x + 1, hdr->r1, hdr->stride, epoch_word(hdr->epoch));
   }
 }
 
 }  // namespace
+
+inline unsigned blocks_for(uint64_t n) { return (unsigned)std::max<uint64_t>((n + 255) / 256, 1); }
 
 template <typename K>
 void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* out_idx,
@@ -189,22 +176,21 @@ void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* o
                     cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
   k_extract_tiles<K><<<ntiles, kThreads, 0, stream>>>(dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
-  k_extract_scan<<<1, 1024, 0, stream>>>(ws.tile_cnt, ntiles, d_count, capacity, d_status_bits,
-                                         ws.tile_base);
-  k_extract_compact<K, false><<<(ntiles + 7) / 8, 256, 0, stream>>>(
-      ws.st_idx, ws.st_val, ws.tile_cnt, ws.tile_base, ntiles, out_idx, out_val, capacity,
+  k_extract_scan<K, false><<<1, 1024, 0, stream>>>(ws.tile_cnt, ntiles, d_count, capacity,
+                                                   d_status_bits, ws.tile_base, HashArgs<K>{});
+  k_extract_compact<K, false><<<blocks_for(std::min<uint64_t>(capacity, m)), 256, 0, stream>>>(
+      ws.st_idx, ws.st_val, ws.tile_base, ntiles, d_count, out_idx, out_val, capacity,
       DevFamily{}, nullptr, nullptr);
   for (int i = 0; i < 3; ++i) count_launch();
 }
 
 template <typename K>
-void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws,
-                          uint64_t* d_count, uint64_t capacity, uint32_t* d_status_bits,
-                          cudaStream_t stream) {
+void launch_extract_tiles_begin(const float* dense, uint64_t m, const ExtractWs<K>& ws,
+                                const HashArgs<K>& ha, uint64_t capacity, cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
   k_extract_tiles<K><<<ntiles, kThreads, 0, stream>>>(dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
-  k_extract_scan<<<1, 1024, 0, stream>>>(ws.tile_cnt, ntiles, d_count, capacity, d_status_bits,
-                                         ws.tile_base);
+  k_extract_scan<K, true><<<1, 1024, 0, stream>>>(ws.tile_cnt, ntiles, &ha.hdr->count, capacity,
+                                                  &ha.hdr->status, ws.tile_base, ha);
   count_launch();
   count_launch();
 }
@@ -214,8 +200,8 @@ void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx
                                   uint64_t capacity, const DevFamily& fam, HashHdr* hdr,
                                   unsigned long long* slots, cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  k_extract_compact<K, true><<<(ntiles + 7) / 8, 256, 0, stream>>>(
-      ws.st_idx, ws.st_val, ws.tile_cnt, ws.tile_base, ntiles, out_idx, out_val, capacity, fam,
+  k_extract_compact<K, true><<<blocks_for(std::min<uint64_t>(capacity, m)), 256, 0, stream>>>(
+      ws.st_idx, ws.st_val, ws.tile_base, ntiles, &hdr->count, out_idx, out_val, capacity, fam,
       hdr, slots);
   count_launch();
 }
@@ -223,8 +209,8 @@ void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx
 #define ZEN_INST(K)                                                                              \
   template void launch_extract<K>(const float*, uint64_t, const ExtractWs<K>&, K*, float*,      \
                                   uint64_t*, uint64_t, uint32_t*, cudaStream_t);                 \
-  template void launch_extract_tiles<K>(const float*, uint64_t, const ExtractWs<K>&, uint64_t*, \
-                                        uint64_t, uint32_t*, cudaStream_t);                      \
+  template void launch_extract_tiles_begin<K>(const float*, uint64_t, const ExtractWs<K>&,     \
+                                              const HashArgs<K>&, uint64_t, cudaStream_t);       \
   template void launch_extract_compact_place<K>(uint64_t, const ExtractWs<K>&, K*, float*,      \
                                                 uint64_t, const DevFamily&, HashHdr*,           \
                                                 unsigned long long*, cudaStream_t);

@@ -12,25 +12,29 @@
 //            in ascending key order = the reference's lanes=1 greedy, for ANY
 //            thread schedule.  Older epochs carry larger words, so stale slots
 //            lose automatically: no memset of the hash memory per run.
-//  post    : per key, the first probe whose slot holds it gives the depth
-//            (CollisionStats); otherwise it is serial.  Per-tile, per-partition
-//            key and serial counts.
-//  scan    : per-partition exclusive offsets over tiles; overflow (load >
-//            r1+r2) and fallback (serial > r2) detection.
-//  scatter : stable multi-split by h0 -> the partitioned output (ascending
-//            within each part, as from_pairs sorts, zen/tensor.hpp:48-59);
-//            serial keys take slot r1 + (ascending serial rank); overflow
-//            witness = the (r1+r2+1)-th key of each overfull partition, the
-//            globally smallest one is the reference's first drop
-//            (zen/hashing.hpp:176-177).  In the BP pipeline the parts are
-//            stored straight into the owner GPU's inbox over NVLink (peer
-//            pointers), fusing the push with the partitioning.
+//  post    : one key per thread, 256-key tiles.  The first probe whose slot
+//            holds the key gives its depth (CollisionStats), else it is serial.
+//            match_any + per-warp counts give every key its stable rank inside
+//            the tile among same-partition keys (and among same-partition
+//            serial keys); both ranks are packed into meta with p and depth.
+//  scan    : one block per partition scans its per-tile counts (tile-major
+//            layout), detecting overflow (load > r1+r2) and fallback
+//            (serial > r2).
+//  scatter : one key per thread: position = tile offset + packed rank, i.e. a
+//            stable multi-split by h0 -> the partitioned output, ascending
+//            within each part (from_pairs sorts, zen/tensor.hpp:48-59).  Serial
+//            keys take slot r1 + (ascending serial rank).  Overflow witness =
+//            the (r1+r2+1)-th key of an overfull partition; the globally
+//            smallest one is the reference's first drop (zen/hashing.hpp:176-177).
+//            In the BP pipeline the parts are stored straight into the owner
+//            GPU's inbox over NVLink (peer pointers): the push is fused here.
 //  fallback: partitions whose serial keys exceed r2 hit the order-dependent
-//            fallback scan (zen/hashing.hpp:170-175): they are replayed
+//            fallback scan (zen/hashing.hpp:170-175) and are replayed
 //            sequentially (rare: ~3% serial vs r2 = 10% of r1).
 #include <cmath>
 
 #include "zen_common.cuh"
+#include "zen_hash_dev.cuh"
 
 namespace zen {
 extern void count_launch();
@@ -41,41 +45,11 @@ using namespace zen_dev;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;
-
-__device__ __forceinline__ uint64_t epoch_word(uint32_t epoch) {
-  return (uint64_t)(0xFFFFFFu - (epoch & 0xFFFFFFu)) << kKeyBits;
-}
+static_assert(kHashTile == kThreads, "one key per thread");
 
 template <typename K>
 __global__ void k_hash_begin(HashArgs<K> a) {
-  HashHdr* h = a.hdr;
-  const uint32_t n = a.fam.n, k = a.fam.k;
-  if (threadIdx.x == 0) {
-    const uint64_t z = h->count;
-    if (h->derive) {  // zen/schemes.hpp:363-367
-      uint64_t r1 = (uint64_t)ceil(h->r1_mult * (double)z / (double)n);
-      if (r1 < 1) r1 = 1;
-      uint64_t r2 = (uint64_t)ceil(h->r2_ratio * (double)r1);
-      if (r2 < 1) r2 = 1;
-      h->r1 = r1;
-      h->r2 = r2;
-    }
-    h->stride = h->r1 + h->r2;
-    h->epoch = h->epoch + 1u;
-    h->ovf_word = ~0ull;
-    h->done = 0;
-    h->fb_done = 0;
-    h->fallback_any = 0;
-    h->ntiles = (uint32_t)((z + kHashTile - 1) / kHashTile);
-    h->iter = h->iter + 1u;
-    h->bad_index = ~0ull;
-    if (z > a.cap || h->stride > a.stride_cap) atomicOr(&h->status, kErrCapacity);
-  }
-  for (uint32_t i = threadIdx.x; i < n * (k + 1); i += blockDim.x) {
-    a.stats[i] = 0;
-    a.fb_stats[i] = 0;
-  }
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) a.fallback[i] = 0;
+  hash_begin_body(a);
 }
 
 template <typename K>
@@ -84,237 +58,186 @@ __global__ void __launch_bounds__(kThreads) k_place(HashArgs<K> a) {
   if (h->status & kErrCapacity) return;
   const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
   const uint64_t ew = epoch_word(h->epoch);
-  const uint32_t k = a.fam.k;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < z;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = (uint64_t)a.idx[i] + 1;
-    const uint32_t p = part_of(a.fam, key);
-    unsigned long long* base = a.slots + (uint64_t)p * stride;
-    uint64_t cur = key;
-    uint32_t t = 0;
-    while (true) {
-      const uint64_t c = slot_of(a.fam, cur, t, r1);
-      const unsigned long long old = atomicMin(base + c, (unsigned long long)(ew | cur));
-      if (old > (ew | kKeyMask)) break;  // empty or stale epoch: cur now holds c
-      const uint64_t ok = old & kKeyMask;
-      if (ok > cur) {  // cur displaced a larger key: that key resumes after c
-        cur = ok;
-        uint32_t f = 0;
-        while (f < k && slot_of(a.fam, cur, f, r1) != c) ++f;
-        t = f + 1;
-      } else {
-        ++t;  // rejected by a smaller key
-      }
-      if (t >= k) break;  // cur ends serial
-    }
-  }
+       i += (uint64_t)gridDim.x * blockDim.x)
+    place_key(a.fam, a.slots, (uint64_t)a.idx[i] + 1, r1, stride, ew);
 }
 
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_post(HashArgs<K> a) {
   extern __shared__ uint32_t sm[];
   const uint32_t n = a.fam.n, k = a.fam.k;
-  uint32_t* cnt = sm;
-  uint32_t* scnt = sm + n;
+  uint32_t* wc = sm;               // [kWarps][n] key counts  -> cross-warp prefixes
+  uint32_t* ws = sm + kWarps * n;  // [kWarps][n] serial counts
   const HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
+  const uint32_t tile = blockIdx.x;
+  const uint32_t ntiles = h->ntiles;
+  if (tile >= ntiles) return;
   const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
   const uint64_t ew = epoch_word(h->epoch);
-  const uint32_t ntiles = h->ntiles;
-  const uint32_t lane = lane_id();
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (uint32_t q = threadIdx.x; q < n; q += kThreads) cnt[q] = scnt[q] = 0;
-    __syncthreads();
-#pragma unroll 1
-    for (int j = 0; j < (int)(kHashTile / kThreads); ++j) {
-      const uint64_t i = (uint64_t)tile * kHashTile + (uint64_t)j * kThreads + threadIdx.x;
-      const bool valid = i < z;
-      uint32_t p = kInvalid, depth = 0;
-      if (valid) {
-        const uint64_t key = (uint64_t)a.idx[i] + 1;
-        p = part_of(a.fam, key);
-        const uint64_t base = (uint64_t)p * stride;
-        for (uint32_t t = 0; t < k; ++t) {
-          const uint64_t c = slot_of(a.fam, key, t, r1);
-          if (a.slots[base + c] == (ew | key)) {
-            depth = t + 1;
-            if (a.slot_vals) a.slot_vals[base + c] = a.val[i];
-            break;
-          }
-        }
-        a.meta[i] = p | (depth << 16);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t q = threadIdx.x; q < kWarps * n; q += kThreads) wc[q] = ws[q] = 0;
+  const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
+  const bool valid = i < z;
+  uint32_t p = kInvalid, depth = 0;
+  if (valid) {
+    const uint64_t key = (uint64_t)a.idx[i] + 1;
+    p = part_of(a.fam, key);
+    const uint64_t base = (uint64_t)p * stride;
+    for (uint32_t t = 0; t < k; ++t) {
+      const uint64_t c = slot_of(a.fam, key, t, r1);
+      if (a.slots[base + c] == (ew | key)) {
+        depth = t + 1;
+        if (a.slot_vals) a.slot_vals[base + c] = a.val[i];
+        break;
       }
-      const uint32_t g = __match_any_sync(0xffffffffu, p);
-      if (valid && lane == (uint32_t)(__ffs(g) - 1)) atomicAdd(&cnt[p], (uint32_t)__popc(g));
-      const uint32_t ks = (valid && depth == 0) ? p : kInvalid;
-      const uint32_t gs = __match_any_sync(0xffffffffu, ks);
-      if (ks != kInvalid && lane == (uint32_t)(__ffs(gs) - 1))
-        atomicAdd(&scnt[p], (uint32_t)__popc(gs));
-      const uint32_t kd = valid ? (p * 32u + depth) : kInvalid;
-      const uint32_t gd = __match_any_sync(0xffffffffu, kd);
-      if (valid && lane == (uint32_t)(__ffs(gd) - 1))
-        atomicAdd(&a.stats[p * (k + 1) + depth], (uint32_t)__popc(gd));
     }
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < n; q += kThreads) {
-      a.tile_cnt[(uint64_t)tile * n + q] = cnt[q];
-      a.tile_scnt[(uint64_t)tile * n + q] = scnt[q];
+  }
+  __syncthreads();
+  const uint32_t g = __match_any_sync(0xffffffffu, p);
+  const uint32_t ks = (valid && depth == 0) ? p : kInvalid;
+  const uint32_t gs = __match_any_sync(0xffffffffu, ks);
+  const uint32_t wr = __popc(g & lanemask_lt()), wsr = __popc(gs & lanemask_lt());
+  if (valid && lane == (uint32_t)(__ffs(g) - 1)) wc[warp * n + p] = __popc(g);
+  if (ks != kInvalid && lane == (uint32_t)(__ffs(gs) - 1)) ws[warp * n + p] = __popc(gs);
+  const uint32_t kd = valid ? (p * 32u + depth) : kInvalid;
+  const uint32_t gd = __match_any_sync(0xffffffffu, kd);
+  if (valid && lane == (uint32_t)(__ffs(gd) - 1))
+    atomicAdd(&a.stats[p * (k + 1) + depth], (uint32_t)__popc(gd));
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < n; q += kThreads) {  // cross-warp exclusive prefixes
+    uint32_t acc = 0, sacc = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t t = wc[w * n + q], st = ws[w * n + q];
+      wc[w * n + q] = acc;
+      ws[w * n + q] = sacc;
+      acc += t;
+      sacc += st;
     }
-    __syncthreads();
+    a.tile_cnt[(uint64_t)q * a.tiles_cap + tile] = acc;
+    a.tile_scnt[(uint64_t)q * a.tiles_cap + tile] = sacc;
+  }
+  __syncthreads();
+  if (valid) {
+    const uint32_t rank = wc[warp * n + p] + wr;
+    const uint32_t srank = depth == 0 ? ws[warp * n + p] + wsr : 0u;
+    a.meta[i] = pack_meta(p, depth, rank, srank);
   }
 }
 
+// one block per partition: exclusive scans of its tile counts (in place)
 template <typename K>
 __global__ void __launch_bounds__(1024) k_hash_scan(HashArgs<K> a) {
   __shared__ uint32_t sscan[33];
   HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
-  const uint32_t n = a.fam.n;
+  const uint32_t p = blockIdx.x;
   const uint32_t ntiles = h->ntiles;
-  for (uint32_t p = 0; p < n; ++p) {
-    for (int pass = 0; pass < 2; ++pass) {
-      uint32_t* arr = pass == 0 ? a.tile_cnt : a.tile_scnt;
-      uint32_t carry = 0;
-      for (uint32_t b = 0; b < ntiles; b += blockDim.x) {
-        const uint32_t t = b + threadIdx.x;
-        const uint32_t v = t < ntiles ? arr[(uint64_t)t * n + p] : 0u;
-        uint32_t tot;
-        const uint32_t ex = block_exclusive_sum(v, sscan, &tot);
-        if (t < ntiles) arr[(uint64_t)t * n + p] = carry + ex;
-        carry += tot;
+  constexpr int E = 4;
+  for (int pass = 0; pass < 2; ++pass) {
+    uint32_t* arr = (pass == 0 ? a.tile_cnt : a.tile_scnt) + (uint64_t)p * a.tiles_cap;
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < ntiles; b += blockDim.x * E) {
+      const uint32_t t0 = b + threadIdx.x * E;
+      uint32_t v[E], local = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        v[e] = (t0 + e < ntiles) ? arr[t0 + e] : 0u;
+        local += v[e];
       }
-      if (threadIdx.x == 0) (pass == 0 ? a.load : a.sload)[p] = carry;
+      uint32_t tot;
+      uint32_t ex = carry + block_exclusive_sum(local, sscan, &tot);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (t0 + e < ntiles) arr[t0 + e] = ex;
+        ex += v[e];
+      }
+      carry += tot;
     }
+    if (threadIdx.x == 0) (pass == 0 ? a.load : a.sload)[p] = carry;
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    uint64_t off = 0;
-    uint32_t any = 0;
-    for (uint32_t p = 0; p < n; ++p) {
-      a.part_off[p] = off;
-      off += a.load[p];
-      const uint32_t fb = (a.sload[p] > h->r2 && a.load[p] <= h->r1 + h->r2) ? 1u : 0u;
-      a.fallback[p] = fb;
-      any |= fb;
-    }
-    h->fallback_any = any;
+    const uint32_t fb =
+        (a.sload[p] > h->r2 && (uint64_t)a.load[p] <= h->r1 + h->r2) ? 1u : 0u;
+    a.fallback[p] = fb;
+    if (fb) atomicOr(&h->fallback_any, 1u);
   }
 }
 
-// Stable multi-split.  Warp w of a tile owns keys [w*256, w*256+256) and walks
-// them in 8 iterations of 32, so (warp, iteration, lane) is ascending key order.
-// Pass 1 keeps each key's rank among same-partition keys of its warp (match_any
-// + a per-warp running count); the block then turns per-warp totals into
-// cross-warp prefixes; pass 2 stores.
+// One key per thread: stable multi-split store (+ serial slots, overflow witness)
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
-  extern __shared__ uint32_t sm[];
+  extern __shared__ uint64_t soff[];  // [n] part offsets (contiguous mode)
+  __shared__ uint32_t s_last;
   const uint32_t n = a.fam.n;
-  uint32_t* wrun = sm;               // [kWarps][n]
-  uint32_t* wsrun = sm + kWarps * n; // [kWarps][n]
   HashHdr* h = a.hdr;
   const bool ok = !(h->status & kErrCapacity);
   const uint64_t z = h->count, r1 = h->r1, r2 = h->r2, stride = h->stride;
   const uint64_t ew = epoch_word(h->epoch);
-  const uint32_t ntiles = ok ? h->ntiles : 0u;
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  constexpr int kIt = kHashTile / kThreads;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (uint32_t q = threadIdx.x; q < kWarps * n; q += kThreads) wrun[q] = wsrun[q] = 0;
-    __syncthreads();
-    uint32_t meta[kIt], rank[kIt], srank[kIt];
-    const uint64_t i0 = (uint64_t)tile * kHashTile + (uint64_t)warp * (kHashTile / kWarps) + lane;
-#pragma unroll
-    for (int j = 0; j < kIt; ++j) {
-      const uint64_t i = i0 + (uint64_t)j * 32;
-      const bool valid = i < z;
-      meta[j] = valid ? a.meta[i] : kInvalid;
-      const uint32_t p = valid ? (meta[j] & 0xFFFFu) : kInvalid;
-      const uint32_t g = __match_any_sync(0xffffffffu, p);
-      const uint32_t ks = (valid && (meta[j] >> 16) == 0) ? p : kInvalid;
-      const uint32_t gs = __match_any_sync(0xffffffffu, ks);
-      uint32_t b = 0, sb = 0;
-      if (valid) b = wrun[warp * n + p];
-      if (ks != kInvalid) sb = wsrun[warp * n + p];
-      rank[j] = b + __popc(g & lanemask_lt());
-      srank[j] = sb + __popc(gs & lanemask_lt());
-      __syncwarp();
-      if (valid && lane == (uint32_t)(__ffs(g) - 1)) wrun[warp * n + p] = b + __popc(g);
-      if (ks != kInvalid && lane == (uint32_t)(__ffs(gs) - 1)) wsrun[warp * n + p] = sb + __popc(gs);
-      __syncwarp();
+  const uint32_t tile = blockIdx.x;
+  if (!a.dst_table && threadIdx.x == 0) {
+    uint64_t off = 0;
+    for (uint32_t q = 0; q < n; ++q) {
+      soff[q] = off;
+      off += a.load[q];
     }
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < n; q += kThreads) {
-      uint32_t acc = 0, sacc = 0;
-      for (int w = 0; w < kWarps; ++w) {
-        const uint32_t t = wrun[w * n + q], st = wsrun[w * n + q];
-        wrun[w * n + q] = acc;
-        wsrun[w * n + q] = sacc;
-        acc += t;
-        sacc += st;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kIt; ++j) {
-      if (meta[j] == kInvalid) continue;
-      const uint64_t i = i0 + (uint64_t)j * 32;
-      const uint32_t p = meta[j] & 0xFFFFu, depth = meta[j] >> 16;
-      const K x = a.idx[i];
-      const float v = a.val[i];
-      const uint64_t key = (uint64_t)x + 1;
-      const uint64_t pos = (uint64_t)a.tile_cnt[(uint64_t)tile * n + p] + wrun[warp * n + p] + rank[j];
-      if (a.dst_table) {
-        if (pos < a.dst_cap) {
-          a.dst_idx[p][pos] = x;
-          a.dst_val[p][pos] = v;
-        } else {
-          atomicOr(&h->status, kErrCapacity);
-        }
+  }
+  __syncthreads();
+  const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
+  if (ok && tile < h->ntiles && i < z) {
+    const uint32_t meta = a.meta[i];
+    const uint32_t p = meta_part(meta), depth = meta_depth(meta);
+    const K x = a.idx[i];
+    const float v = a.val[i];
+    const uint64_t key = (uint64_t)x + 1;
+    const uint64_t pos = (uint64_t)a.tile_cnt[(uint64_t)p * a.tiles_cap + tile] + meta_rank(meta);
+    if (a.dst_table) {
+      if (pos < a.dst_cap) {
+        a.dst_idx[p][pos] = x;
+        a.dst_val[p][pos] = v;
       } else {
-        a.out_idx[a.part_off[p] + pos] = x;
-        a.out_val[a.part_off[p] + pos] = v;
+        atomicOr(&h->status, kErrCapacity);
       }
-      if (pos == r1 + r2) atomicMin((unsigned long long*)&h->ovf_word, (key << 16) | p);
-      if (depth == 0) {
-        const uint64_t spos =
-            (uint64_t)a.tile_scnt[(uint64_t)tile * n + p] + wsrun[warp * n + p] + srank[j];
-        if (spos < r2) {
-          const uint64_t s = (uint64_t)p * stride + r1 + spos;
-          a.slots[s] = ew | key;
-          if (a.slot_vals) a.slot_vals[s] = v;
-        }
+    } else {
+      a.out_idx[soff[p] + pos] = x;
+      a.out_val[soff[p] + pos] = v;
+    }
+    if (pos == r1 + r2) atomicMin((unsigned long long*)&h->ovf_word, (key << 16) | p);
+    if (depth == 0) {
+      const uint64_t spos =
+          (uint64_t)a.tile_scnt[(uint64_t)p * a.tiles_cap + tile] + meta_srank(meta);
+      if (spos < r2) {
+        const uint64_t s = (uint64_t)p * stride + r1 + spos;
+        a.slots[s] = ew | key;
+        if (a.slot_vals) a.slot_vals[s] = v;
       }
     }
-    __syncthreads();
   }
   // push signalling: the last block publishes this worker's count row to every
   // server (peer memory) with release semantics, after all blocks' stores.
-  if (a.push_hdr) {
-    __shared__ uint32_t s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      s_last = (atomicAdd(&h->done, 1u) == gridDim.x - 1) ? 1u : 0u;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence_system();
-      const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
-      const uint32_t st = *(volatile uint32_t*)&h->status;
-      for (uint32_t s = threadIdx.x; s < n; s += kThreads) {
-        PushHdr* ph = a.push_hdr[s];
-        ph->nnz = z;
-        ph->ovf_word = ovf;
-        ph->status = st;
-        for (uint32_t q = 0; q < n; ++q) ph->counts[q] = a.load[q];
-      }
-      __syncthreads();
-      __threadfence_system();
-      for (uint32_t s = threadIdx.x; s < n; s += kThreads)
-        st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
-    }
+  if (!a.push_hdr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = (atomicAdd(&h->done, 1u) == gridDim.x - 1) ? 1u : 0u;
   }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence_system();
+  const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
+  const uint32_t st = *(volatile uint32_t*)&h->status;
+  for (uint32_t s = threadIdx.x; s < n; s += kThreads) {
+    PushHdr* ph = a.push_hdr[s];
+    ph->nnz = z;
+    ph->ovf_word = ovf;
+    ph->status = st;
+    for (uint32_t q = 0; q < n; ++q) ph->counts[q] = ok ? a.load[q] : 0u;
+  }
+  __syncthreads();
+  __threadfence_system();
+  for (uint32_t s = threadIdx.x; s < n; s += kThreads)
+    st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
 }
 
 // Sequential replay of partitions that reached the fallback scan, exactly as
@@ -328,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
   __shared__ uint32_t fstat[kMaxK + 1];
   HashHdr* h = a.hdr;
   const uint32_t n = a.fam.n, k = a.fam.k;
-  const bool ok = !(h->status & kErrCapacity) && h->ovf_word == ~0ull;
+  const bool ok = !(h->status & kErrCapacity) && h->ovf_word == ~0ull && h->fallback_any;
   for (uint32_t p = blockIdx.x; ok && p < n; p += gridDim.x) {
     if (!a.fallback[p]) continue;
     const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
@@ -340,7 +263,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
     uint64_t cursor = r1;
     for (uint64_t c0 = 0; c0 < z; c0 += kThreads) {
       const uint64_t i = c0 + threadIdx.x;
-      const bool mine = i < z && (a.meta[i] & 0xFFFFu) == p;
+      const bool mine = i < z && meta_part(a.meta[i]) == p;
       const uint32_t bal = __ballot_sync(0xffffffffu, mine);
       if (lane_id() == 0) wcount[threadIdx.x >> 5] = __popc(bal);
       __syncthreads();
@@ -377,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
             base[slot] = ew | key;
             if (a.slot_vals) a.slot_vals[(uint64_t)p * stride + slot] = a.val[ii];
           }
-          a.meta[ii] = p | (depth << 16);
+          a.meta[ii] = pack_meta(p, depth, meta_rank(a.meta[ii]), 0);
           fstat[depth] += 1;
         }
       }
@@ -439,11 +362,10 @@ void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream) {
 
 template <typename K>
 void launch_hash_rest(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
-  const uint64_t ntiles_cap = (a.cap + kHashTile - 1) / kHashTile;
-  const unsigned tile_grid = grid_for(ntiles_cap, 1, 148 * 8);
-  k_post<K><<<tile_grid, kThreads, 2 * n * sizeof(uint32_t), stream>>>(a);
-  k_hash_scan<K><<<1, 1024, 0, stream>>>(a);
-  k_scatter<K><<<tile_grid, kThreads, 2 * kWarps * n * sizeof(uint32_t), stream>>>(a);
+  const unsigned tiles = (unsigned)std::max<uint64_t>(a.tiles_cap, 1);
+  k_post<K><<<tiles, kThreads, 2 * kWarps * n * sizeof(uint32_t), stream>>>(a);
+  k_hash_scan<K><<<n, 1024, 0, stream>>>(a);
+  k_scatter<K><<<tiles, kThreads, n * sizeof(uint64_t), stream>>>(a);
   k_fallback<K><<<grid_for(n, 1, 148), kThreads, 0, stream>>>(a);
   for (int i = 0; i < 4; ++i) count_launch();
   (void)k;

@@ -2,6 +2,7 @@
 // HashMemory dumps (reference 0 = empty sentinel), CollisionStats depths, and
 // the materialised universe list I_s.
 #include "zen_common.cuh"
+#include "zen_hash_dev.cuh"
 
 namespace zen {
 extern void count_launch();
@@ -25,7 +26,7 @@ __global__ void k_meta_depth(const uint32_t* __restrict__ meta, uint64_t count,
                              uint32_t* __restrict__ out) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
        i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = meta[i] >> 16;
+    out[i] = meta_depth(meta[i]);
 }
 
 __global__ void k_universe_indices(const OwnWord* __restrict__ own, uint64_t nwords,

@@ -1,0 +1,88 @@
+// zen_hash_dev.cuh -- device pieces of the hierarchical hash shared by the
+// hash kernels and the extraction compaction (which fuses the placement).
+#pragma once
+
+#include "zen_common.cuh"
+
+namespace zen_dev {
+
+// slot word epoch field: newer runs carry smaller words (see k_hash.cu)
+__device__ __forceinline__ uint64_t epoch_word(uint32_t epoch) {
+  return (uint64_t)(0xFFFFFFu - (epoch & 0xFFFFFFu)) << zen::kKeyBits;
+}
+
+// Priority claim of one key (deferred acceptance, smallest key wins):
+// reproduces place_index's parallel-region layout of the lanes=1 run
+// (zen/hashing.hpp:155-163) for any thread schedule.
+__device__ __forceinline__ void place_key(const zen::DevFamily& fam, unsigned long long* slots,
+                                          uint64_t key, uint64_t r1, uint64_t stride,
+                                          uint64_t ew) {
+  const uint32_t p = part_of(fam, key);
+  unsigned long long* base = slots + (uint64_t)p * stride;
+  uint64_t cur = key;
+  uint32_t t = 0;
+  const uint32_t k = fam.k;
+  while (true) {
+    const uint64_t c = slot_of(fam, cur, t, r1);
+    const unsigned long long old = atomicMin(base + c, (unsigned long long)(ew | cur));
+    if (old > (ew | zen::kKeyMask)) break;  // empty or stale epoch: cur now holds c
+    const uint64_t ok = old & zen::kKeyMask;
+    if (ok > cur) {  // cur displaced a larger key: it resumes after its first c
+      cur = ok;
+      uint32_t f = 0;
+      while (f < k && slot_of(fam, cur, f, r1) != c) ++f;
+      t = f + 1;
+    } else {
+      ++t;  // rejected by a smaller key
+    }
+    if (t >= k) break;  // cur ends serial
+  }
+}
+
+// meta word of a key after the post pass: partition (9 bits), depth (5),
+// stable rank in its 256-key tile among same-partition keys (8) and among
+// same-partition serial keys (8).
+__device__ __forceinline__ uint32_t pack_meta(uint32_t p, uint32_t depth, uint32_t rank,
+                                              uint32_t srank) {
+  return p | (depth << 9) | (rank << 14) | (srank << 22);
+}
+__device__ __forceinline__ uint32_t meta_part(uint32_t m) { return m & 0x1FFu; }
+__device__ __forceinline__ uint32_t meta_depth(uint32_t m) { return (m >> 9) & 0x1Fu; }
+__device__ __forceinline__ uint32_t meta_rank(uint32_t m) { return (m >> 14) & 0xFFu; }
+__device__ __forceinline__ uint32_t meta_srank(uint32_t m) { return (m >> 22) & 0xFFu; }
+
+// per-run header reset + r1/r2 from the (device-resident) key count,
+// zen/schemes.hpp:363-367.  Called by one block.
+template <typename K>
+__device__ __forceinline__ void hash_begin_body(const zen::HashArgs<K>& a) {
+  zen::HashHdr* h = a.hdr;
+  const uint32_t n = a.fam.n, k = a.fam.k;
+  if (threadIdx.x == 0) {
+    const uint64_t z = h->count;
+    if (h->derive) {
+      uint64_t r1 = (uint64_t)ceil(h->r1_mult * (double)z / (double)n);
+      if (r1 < 1) r1 = 1;
+      uint64_t r2 = (uint64_t)ceil(h->r2_ratio * (double)r1);
+      if (r2 < 1) r2 = 1;
+      h->r1 = r1;
+      h->r2 = r2;
+    }
+    h->stride = h->r1 + h->r2;
+    h->epoch = h->epoch + 1u;
+    h->ovf_word = ~0ull;
+    h->done = 0;
+    h->fb_done = 0;
+    h->fallback_any = 0;
+    h->ntiles = (uint32_t)((z + zen::kHashTile - 1) / zen::kHashTile);
+    h->iter = h->iter + 1u;
+    h->bad_index = ~0ull;
+    if (z > a.cap || h->stride > a.stride_cap) atomicOr(&h->status, zen::kErrCapacity);
+  }
+  for (uint32_t i = threadIdx.x; i < n * (k + 1); i += blockDim.x) {
+    a.stats[i] = 0;
+    a.fb_stats[i] = 0;
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) a.fallback[i] = 0;
+}
+
+}  // namespace zen_dev

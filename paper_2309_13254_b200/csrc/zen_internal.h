@@ -11,7 +11,7 @@ namespace zen {
 constexpr uint32_t kMaxK = 16;          // rehash depth supported on device
 constexpr uint32_t kMaxPartitions = 512;   // n for the standalone hash
 constexpr uint32_t kMaxWorkers = 16;    // n for the fused BP pipeline
-constexpr uint32_t kHashTile = 2048;    // keys per hash tile (256 threads x 8)
+constexpr uint32_t kHashTile = 256;     // keys per hash tile (one per thread)
 constexpr uint32_t kExtractTile = 8192; // floats per extraction tile
 constexpr uint32_t kDecodeTileWords = 128;  // 64-index words per decode tile (= block size)
 constexpr uint32_t kPrefixBlockWords = 2048;  // bitmap words per popcount-prefix block
@@ -104,12 +104,13 @@ template <typename K>
 void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* out_idx,
                     float* out_val, uint64_t* d_count, uint64_t capacity, uint32_t* d_status_bits,
                     cudaStream_t stream);
-// pipeline split: tiles + scan, then (after the hash begin) compaction fused
-// with the priority-claim placement
+// pipeline split: tiles + scan fused with the hash begin, then the
+// compaction fused with the priority-claim placement
 template <typename K>
-void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws,
-                          uint64_t* d_count, uint64_t capacity, uint32_t* d_status_bits,
-                          cudaStream_t stream);
+struct HashArgs;
+template <typename K>
+void launch_extract_tiles_begin(const float* dense, uint64_t m, const ExtractWs<K>& ws,
+                                const HashArgs<K>& ha, uint64_t capacity, cudaStream_t stream);
 template <typename K>
 void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx, float* out_val,
                                   uint64_t capacity, const DevFamily& fam, HashHdr* hdr,
@@ -126,9 +127,10 @@ struct HashArgs {
   HashHdr* hdr;
   unsigned long long* slots;  // n * stride_cap words
   float* slot_vals;           // optional (layout dump)
-  uint32_t* meta;             // [cap] p | depth << 16
-  uint32_t* tile_cnt;         // [ntiles_cap * n]
-  uint32_t* tile_scnt;        // [ntiles_cap * n]
+  uint32_t* meta;             // [cap] packed p | depth | tile ranks (zen_hash_dev.cuh)
+  uint32_t* tile_cnt;         // [n][tiles_cap] per-tile counts -> exclusive offsets
+  uint32_t* tile_scnt;        // [n][tiles_cap] serial counts -> offsets
+  uint64_t tiles_cap;         // ceil(cap / kHashTile)
   uint32_t* load;             // [n]
   uint32_t* sload;            // [n] serial keys per partition
   uint64_t* part_off;         // [n] exclusive offsets (contiguous output mode)
