@@ -337,10 +337,14 @@ def main():
         torch.cuda.synchronize()
         be.wait()
         sms, kk = be.stage_times()
+        nzr = np.zeros(args.rows, bool)
+        for w in range(ne):
+            nzr[rows_e[w]] = True
+        union = be.result_count()
         emu = {"workers": ne, "ms_per_sync_one_gpu": round(a0.elapsed_time(a1) / ke, 4),
                "stage_ms": {nm: round(float(x) / max(kk, 1), 4)
                             for nm, x in zip(zen.STAGE_NAMES, sms)},
-               "union": be.result_count()}
+               "union": union, "union_ok": bool(union == int(nzr.sum()) * args.width)}
         del be, dd
 
     if rank != 0:

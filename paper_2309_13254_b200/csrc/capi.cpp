@@ -438,7 +438,7 @@ struct Decoder {
       bstart[s + 1] = bstart[s] + nb;
     }
     total_blocks = bstart[n];
-    words_stride = std::max<uint64_t>(words_stride, 1);
+    words_stride = (std::max<uint64_t>(words_stride, 1) + 7) & ~uint64_t(7);
     blk_stride = std::max<uint64_t>(blk_stride, 1);
     CKR(mem.alloc(&bpre, words_stride * n));
     CKR(mem.alloc(&bpre_blk, blk_stride * n));
@@ -473,9 +473,10 @@ struct Decoder {
 // scratch of the aggregate + encode (see k_codec.cu)
 zen_status alloc_agg_ws(DevMem& mem, AggArgs& a, uint32_t nparts, uint64_t bs) {
   a.nw = std::max<uint64_t>((bs + 63) / 64, 1);
+  a.nws = (a.nw + 7) & ~uint64_t(7);
   a.nblk = uint32_t((a.nw + kPrefixBlockWords - 1) / kPrefixBlockWords);
-  CKR(mem.alloc(&a.pw, size_t(nparts) * a.nw));
-  CKR(mem.alloc(&a.pre, size_t(nparts + 1) * a.nw, false));
+  CKR(mem.alloc(&a.pw, size_t(nparts) * a.nws));
+  CKR(mem.alloc(&a.pre, size_t(nparts + 1) * a.nws, false));
   CKR(mem.alloc(&a.blk, size_t(nparts + 1) * a.nblk));
   CKR(mem.alloc(&a.done, 2));
   return ZEN_OK;
@@ -545,7 +546,7 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   unsigned long long** dst_bits;
   float** dst_vals;
   CKR(mem.alloc(&keys, std::max<uint64_t>(count, 1)));
-  CKR(mem.alloc(&bits, std::max<uint64_t>(nw, 1)));
+  CKR(mem.alloc(&bits, (std::max<uint64_t>(nw, 1) + 7) & ~uint64_t(7)));
   CKR(mem.alloc(&vals, std::max<uint64_t>(count, 1)));
   CKR(mem.alloc(&hdr, 1));
   CKR(mem.alloc(&aggc, 1));
@@ -638,7 +639,7 @@ zen_status zen_hash_bitmap_decode(zen_universe* u, uint32_t s, const uint8_t* d_
   uint64_t* out_count;
   const unsigned long long** bits_t;
   const float** vals_t;
-  CKR(mem.alloc(&bits, std::max<uint64_t>(nw, 1)));
+  CKR(mem.alloc(&bits, (std::max<uint64_t>(nw, 1) + 7) & ~uint64_t(7)));
   CKR(mem.alloc(&vals, std::max<uint64_t>(count, 1)));
   CKR(mem.alloc(&hdr, 1));
   CKR(mem.alloc(&out_count, 1));
@@ -844,6 +845,7 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   a.dst_cap = cap;
   a.stride_cap = bp->stride_cap;
   a.me = w.id;
+  a.peer = bp->local ? 0 : 1;
   uint32_t** dst_idx;
   float** dst_val;
   PushHdr** push_hdr;
@@ -905,6 +907,7 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   a.val_cap = bp->valcap[s.id];
   a.agg_count = s.agg_count;
   a.wait_push = bp->local ? 0 : 1;
+  a.peer = bp->local ? 0 : 1;
   return ZEN_OK;
 }
 

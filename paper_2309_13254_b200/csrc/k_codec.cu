@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
     }
     const uint32_t r = ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
     // consecutive keys share bitmap words: one atomic per distinct word per warp
-    unsigned long long* word = owned ? a.pw + (uint64_t)w * a.nw + (r >> 6) : nullptr;
+    unsigned long long* word = owned ? a.pw + (uint64_t)w * a.nws + (r >> 6) : nullptr;
     const uint64_t bit = owned ? 1ull << (r & 63u) : 0ull;
     const uint32_t grp = __match_any_sync(__activemask(), (unsigned long long)word);
     const uint32_t lo = __reduce_or_sync(grp, (uint32_t)bit);
@@ -175,55 +175,64 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
 // Phase 2: U = OR_w P_w -> every destination; block-local popcount prefixes of
 // U and each P_w; the last block turns the block totals into exclusive
 // prefixes and records U_s.
+__device__ __forceinline__ void load8(const unsigned long long* p, unsigned long long (&v)[kWPT]) {
+  const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p);  // 64 B, 64 B aligned
+#pragma unroll
+  for (int i = 0; i < kWPT / 2; ++i) {
+    const ulonglong2 t = q[i];
+    v[2 * i] = t.x;
+    v[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void store8(unsigned long long* p, const unsigned long long (&v)[kWPT]) {
+  ulonglong2* q = reinterpret_cast<ulonglong2*>(p);
+#pragma unroll
+  for (int i = 0; i < kWPT / 2; ++i) q[i] = make_ulonglong2(v[2 * i], v[2 * i + 1]);
+}
+__device__ __forceinline__ void store8u(uint32_t* p, const uint32_t (&v)[kWPT]) {
+  uint4* q = reinterpret_cast<uint4*>(p);  // 32 B, 32 B aligned
+  q[0] = make_uint4(v[0], v[1], v[2], v[3]);
+  q[1] = make_uint4(v[4], v[5], v[6], v[7]);
+}
+
+// Phase 2: U = OR_w P_w -> every destination; block-local popcount prefixes of
+// U and each P_w (8 consecutive words per thread, 64-byte vector accesses; rows
+// padded to 8 words); the last block turns the block totals into exclusive
+// prefixes and records U_s.
 __global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
   __shared__ uint32_t wsum[kMaxWorkers + 1][kAggThreads / 32];
+  __shared__ uint32_t inw[kMaxWorkers + 1][kAggThreads];
   __shared__ uint32_t s_last;
   const uint32_t n = a.n, lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t j0 = (uint64_t)blockIdx.x * kPrefixBlockWords + (uint64_t)threadIdx.x * kWPT;
+  const bool live = j0 < a.nw;
   unsigned long long U[kWPT];
-  uint32_t cu[kWPT];
 #pragma unroll
   for (int i = 0; i < kWPT; ++i) U[i] = 0;
-  // per worker: popcounts -> warp scan -> smem; OR into U
   for (uint32_t x = 0; x <= n; ++x) {
-    uint32_t c[kWPT];
+    unsigned long long v[kWPT];
+    if (x < n) {
+      if (live) load8(a.pw + (uint64_t)x * a.nws + j0, v);
+      else
+#pragma unroll
+        for (int i = 0; i < kWPT; ++i) v[i] = 0;
+#pragma unroll
+      for (int i = 0; i < kWPT; ++i) U[i] |= v[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < kWPT; ++i) v[i] = U[i];
+    }
     uint32_t t = 0;
 #pragma unroll
-    for (int i = 0; i < kWPT; ++i) {
-      const uint64_t j = j0 + i;
-      unsigned long long v = 0;
-      if (x < n) {
-        v = (j < a.nw) ? a.pw[(uint64_t)x * a.nw + j] : 0ull;
-        U[i] |= v;
-      } else {
-        v = U[i];
-      }
-      c[i] = __popcll(v);
-      t += c[i];
-    }
+    for (int i = 0; i < kWPT; ++i) t += __popcll(v[i]);
     const uint32_t inc = warp_inclusive_sum(t);
     if (lane == 31) wsum[x][warp] = inc;
-    // stash this thread's in-warp exclusive prefix + per-word prefix in `pre`
-    uint32_t run = inc - t;
-#pragma unroll
-    for (int i = 0; i < kWPT; ++i) {
-      cu[i] = run;  // temporarily the in-warp prefix
-      run += c[i];
-    }
-    uint32_t* out = a.pre + (uint64_t)x * a.nw;
-#pragma unroll
-    for (int i = 0; i < kWPT; ++i)
-      if (j0 + i < a.nw) out[j0 + i] = cu[i];
+    inw[x][threadIdx.x] = inc - t;
   }
-  // write the union bitmap (the HashBitmap, LSB-first = little-endian words)
-#pragma unroll
-  for (int i = 0; i < kWPT; ++i) {
-    const uint64_t j = j0 + i;
-    if (j < a.nw)
-      for (uint32_t d = 0; d < a.ndst; ++d) a.dst_bits[d][j] = U[i];
-  }
+  // the union bitmap (the HashBitmap: LSB-first = little-endian words)
+  if (live)
+    for (uint32_t d = 0; d < a.ndst; ++d) store8(a.dst_bits[d] + j0, U);
   __syncthreads();
-  // add the cross-warp prefix to the stored in-warp prefixes; block totals
   for (uint32_t x = 0; x <= n; ++x) {
     uint32_t wpre = 0, tot = 0;
 #pragma unroll
@@ -232,13 +241,21 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
       wpre += (w < (int)warp) ? v : 0u;
       tot += v;
     }
-    if (wpre) {
-      uint32_t* out = a.pre + (uint64_t)x * a.nw;
-#pragma unroll
-      for (int i = 0; i < kWPT; ++i)
-        if (j0 + i < a.nw) out[j0 + i] += wpre;
-    }
     if (threadIdx.x == 0) a.blk[(uint64_t)x * a.nblk + blockIdx.x] = tot;
+    if (!live) continue;
+    unsigned long long v[kWPT];
+    if (x < n) load8(a.pw + (uint64_t)x * a.nws + j0, v);  // L1/L2 hit
+    else
+#pragma unroll
+      for (int i = 0; i < kWPT; ++i) v[i] = U[i];
+    uint32_t pre[kWPT];
+    uint32_t run = wpre + inw[x][threadIdx.x];
+#pragma unroll
+    for (int i = 0; i < kWPT; ++i) {
+      pre[i] = run;
+      run += __popcll(v[i]);
+    }
+    store8u(a.pre + (uint64_t)x * a.nws + j0, pre);
   }
   // last block: exclusive prefix of the block totals (one warp per bitmap)
   __syncthreads();
@@ -285,15 +302,15 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
     unsigned long long v = 0;
     uint32_t b = 0;
     if (w < (int)n && valid) {
-      v = a.pw[(uint64_t)w * a.nw + j];
-      if (v) b = a.blk[(uint64_t)w * a.nblk + pb] + a.pre[(uint64_t)w * a.nw + j];
+      v = a.pw[(uint64_t)w * a.nws + j];
+      if (v) b = a.blk[(uint64_t)w * a.nblk + pb] + a.pre[(uint64_t)w * a.nws + j];
     }
     spw[threadIdx.x][w] = v;
     sbase[threadIdx.x][w] = b;
     U |= v;
   }
   const uint64_t ubase = (valid && U) ? (uint64_t)a.blk[(uint64_t)n * a.nblk + pb] +
-                                            a.pre[(uint64_t)n * a.nw + j] : 0ull;
+                                            a.pre[(uint64_t)n * a.nws + j] : 0ull;
   const uint32_t c = __popcll(U);
   const uint32_t inc = warp_inclusive_sum(c);
   const uint32_t x = inc - c;
@@ -337,14 +354,14 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
   if (!a.dst_hdr) return;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    fence_for(a.peer);
     const uint32_t dn = atomicAdd(&a.done[1], 1u);
     s_last = (dn == gridDim.x - 1) ? 1u : 0u;
     if (s_last) a.done[1] = 0;
   }
   __syncthreads();
   if (s_last) {  // pull signalling: publish U_s, then the flag (release, system scope)
-    __threadfence_system();
+    fence_for(a.peer);
     const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
     const uint64_t u = *(volatile uint64_t*)a.agg_count;
     const uint32_t st = *(volatile uint32_t*)&a.hdr->status;
@@ -355,7 +372,7 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
       a.dst_hdr[d]->bad_index = bad;
     }
     __syncthreads();
-    __threadfence_system();
+    fence_for(a.peer);
     for (uint32_t d = threadIdx.x; d < a.ndst; d += blockDim.x)
       st_release_sys(&a.dst_hdr[d]->flag, (unsigned long long)iter);
   }
@@ -383,21 +400,22 @@ __global__ void __launch_bounds__(256) k_bpre(DecodeArgs a) {
   const unsigned long long* bits = a.bits[s];
   const uint64_t nw = a.nwords_s[s];
   const uint64_t w0 = (uint64_t)blk * kPrefixBlockWords + threadIdx.x * (uint64_t)kWPT;
+  unsigned long long v[kWPT];
+  const bool live = bits && w0 < nw;
+  if (live) load8(bits + w0, v);  // rows are padded to 8 words
   uint32_t c[kWPT];
   uint32_t local = 0;
 #pragma unroll
   for (int i = 0; i < kWPT; ++i) {
     c[i] = local;
-    const uint64_t w = w0 + i;
-    local += (bits && w < nw) ? (uint32_t)__popcll(bits[w]) : 0u;
+    local += live ? (uint32_t)__popcll(v[i]) : 0u;
   }
   uint32_t tot;
   const uint32_t ex = block_exclusive_sum(local, sscan, &tot);
-  uint32_t* out = a.bpre + s * a.words_stride;
+  if (live) {
 #pragma unroll
-  for (int i = 0; i < kWPT; ++i) {
-    const uint64_t w = w0 + i;
-    if (w < nw) out[w] = ex + c[i];
+    for (int i = 0; i < kWPT; ++i) c[i] += ex;
+    store8u(a.bpre + s * a.words_stride + w0, c);
   }
   if (threadIdx.x == 0) {
     a.bpre_blk[s * a.blk_stride + blk] = tot;
@@ -578,7 +596,7 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
 void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
   uint64_t cap_entries = 0;
   (void)cap_entries;
-  cudaMemsetAsync(a.pw, 0, (size_t)a.n * a.nw * 8, stream);
+  cudaMemsetAsync(a.pw, 0, (size_t)a.n * a.nws * 8, stream);
   k_agg_mark<<<148 * 8, kAggThreads, 0, stream>>>(a);
   k_agg_union<<<a.nblk, kAggThreads, 0, stream>>>(a);
   const unsigned g = (unsigned)((a.nw + kValThreads - 1) / kValThreads);

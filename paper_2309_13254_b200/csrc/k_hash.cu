@@ -219,12 +219,12 @@ __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
   if (!a.push_hdr) return;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    fence_for(a.peer);
     s_last = (atomicAdd(&h->done, 1u) == gridDim.x - 1) ? 1u : 0u;
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence_system();
+  fence_for(a.peer);
   const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
   const uint32_t st = *(volatile uint32_t*)&h->status;
   for (uint32_t s = threadIdx.x; s < n; s += kThreads) {
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
     for (uint32_t q = 0; q < n; ++q) ph->counts[q] = ok ? a.load[q] : 0u;
   }
   __syncthreads();
-  __threadfence_system();
+  fence_for(a.peer);
   for (uint32_t s = threadIdx.x; s < n; s += kThreads)
     st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
 }

@@ -210,6 +210,13 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const unsigned long long* p) 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// release fence: system scope when peers (other GPUs) read what we wrote
+__device__ __forceinline__ void fence_for(bool peer) {
+  if (peer)
+    __threadfence_system();
+  else
+    __threadfence();
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -150,6 +150,7 @@ struct HashArgs {
   // push signalling (pipeline): headers in each server's inbox
   PushHdr* const* push_hdr;   // [n] or nullptr
   uint32_t me;
+  int peer;                   // destinations include other GPUs (system-scope release)
 };
 
 // phases: begin (r1/r2, epoch, counters) | place | post..fallback.
@@ -191,9 +192,10 @@ struct AggArgs {
   const OwnWord* own;
   uint64_t bs;                    // |I_s|
   uint64_t nw;                    // ceil(bs / 64) (>= 1)
+  uint64_t nws;                   // row stride of pw / pre: nw rounded up to 8 words
   uint32_t nblk;                  // ceil(nw / kPrefixBlockWords)
-  unsigned long long* pw;         // [n * nw] per-worker presence, zeroed per sync
-  uint32_t* pre;                  // [(n + 1) * nw] block-local exclusive popcounts (U = n)
+  unsigned long long* pw;         // [n * nws] per-worker presence, zeroed per sync
+  uint32_t* pre;                  // [(n + 1) * nws] block-local exclusive popcounts (U = n)
   uint32_t* blk;                  // [(n + 1) * nblk] block totals -> exclusive prefixes
   uint32_t* done;                 // [2] blocks-finished counters (self-resetting)
   uint32_t ndst;
@@ -204,6 +206,7 @@ struct AggArgs {
   uint64_t* agg_count;            // U_s (device)
   HashHdr* hdr;                   // iteration / error bits / bad index
   int wait_push;                  // wait for in_hdr[w]->flag >= hdr->iter
+  int peer;                       // destinations include other GPUs (system-scope release)
 };
 void launch_aggregate(const AggArgs& a, cudaStream_t stream);
 

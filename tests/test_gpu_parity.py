@@ -401,3 +401,36 @@ def test_bp_collision_stats_match_reference(zen, co, ro):
         st = bp.collision_stats(w)
         assert st.serial_writes == want.serial_writes
         assert st.placed_at_depth == want.placed_at_depth
+
+
+@pytest.mark.parametrize("n,rows", [(8, 1_000_000), (3, 400_000)])
+def test_bp_full_size_properties(zen, n, rows):
+    """BASELINE-size local sync (1M x 64 fp32, 1%/worker, n=8 emulated on one GPU)
+    checked through size-independent properties: the result index set is the
+    union of the inputs and every value is the exact integer sum."""
+    torch = pytest.importorskip("torch")
+    import bench
+    d = 64
+    per = int(np.ceil(0.01 * rows))
+    live = bench.live_rows(rows, per, n, 0.5, 1.05, 1)
+    dense = [torch.from_numpy(bench.dense_gradient(rows, d, live[w], 1 + w)).cuda() for w in range(n)]
+    bp = zen.BPSynchronizer(n, rows * d, max_nnz=per * d + 4096)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        bp.sync_dense(dense)
+        bp.sync_dense(dense)  # graph replay
+    bp.wait()
+    oi, ov = bp.result()
+    acc = torch.zeros(rows * d, dtype=torch.float64, device="cuda")
+    for x in dense:
+        acc += x.double()
+    nzr = torch.zeros(rows, dtype=torch.bool, device="cuda")
+    for w in range(n):
+        nzr[torch.from_numpy(live[w]).cuda()] = True
+    want_idx = (torch.nonzero(nzr).view(-1, 1) * d + torch.arange(d, device="cuda")).view(-1)
+    assert oi.numel() == want_idx.numel()
+    assert torch.equal(oi, want_idx)
+    assert torch.equal(ov.double(), acc[oi])
+    led, counts, agg = bp.ledger()
+    assert int(agg.sum()) == oi.numel()
+    assert int(counts.sum()) == sum(int(torch.count_nonzero(x)) for x in dense)
