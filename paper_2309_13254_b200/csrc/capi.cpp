@@ -903,7 +903,7 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   CKR(mem.alloc(&dh, a.ndst));
   a.dst_bits = db;
   a.dst_vals = dv;
-  a.dst_hdr = dh;
+  a.dst_hdr = bp->local ? nullptr : dh;
   a.val_cap = bp->valcap[s.id];
   a.agg_count = s.agg_count;
   a.wait_push = bp->local ? 0 : 1;
@@ -955,7 +955,7 @@ zen_status bp_wire(zen_bp* bp) {
     }
     CKR(upload(const_cast<unsigned long long**>(s.a.dst_bits), db.data(), s.a.ndst));
     CKR(upload(const_cast<float**>(s.a.dst_vals), dvv.data(), s.a.ndst));
-    CKR(upload(const_cast<PullHdr**>(s.a.dst_hdr), dh.data(), s.a.ndst));
+    if (s.a.dst_hdr) CKR(upload(const_cast<PullHdr**>(s.a.dst_hdr), dh.data(), s.a.ndst));
   }
   // receiver: this node's pull inbox (local: arena 0)
   const Arena& R = bp->arena_of(bp->local ? 0 : bp->rank);
@@ -1317,6 +1317,10 @@ zen_status bp_collect(zen_bp* bp) {
     bp->h_nnz[w] = ph[w].nnz;
     bp->h_agg[w] = pl[w].agg_count;
   }
+  if (bp->local)  // no pull headers in local mode: U_s from each server's counter
+    for (auto& s : bp->servers) {
+      CK(cudaMemcpy(&bp->h_agg[s.id], s.agg_count, 8, cudaMemcpyDeviceToHost));
+    }
   for (uint32_t w = 0; w < n; ++w) {  // run_balanced_parallelism throws at the first worker
     if (ph[w].ovf_word != ~0ull) {
       const uint32_t p = uint32_t(ph[w].ovf_word & 0xFFFF);

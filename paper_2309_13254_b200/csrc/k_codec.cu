@@ -267,17 +267,10 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
   if (!s_last) return;
   __threadfence();
   for (uint32_t x = warp; x <= n; x += kAggThreads / 32) {
-    volatile uint32_t* b = a.blk + (uint64_t)x * a.nblk;
-    uint32_t carry = 0;
-    for (uint32_t i0 = 0; i0 < a.nblk; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const uint32_t v = i < a.nblk ? b[i] : 0u;
-      const uint32_t inc = warp_inclusive_sum(v);
-      if (i < a.nblk) b[i] = carry + inc - v;
-      carry += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    if (x == n && lane == 0) *a.agg_count = carry;
+    const uint32_t total = warp_exscan_l2(a.blk + (uint64_t)x * a.nblk, a.nblk);
+    if (x == n && lane == 0) *a.agg_count = total;
   }
+  __syncthreads();
   if (threadIdx.x == 0) a.done[0] = 0;
 }
 
@@ -291,7 +284,6 @@ template <int NMAX>
 __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
   __shared__ unsigned long long spw[kValThreads][NMAX];
   __shared__ uint32_t sbase[kValThreads][NMAX];
-  __shared__ uint32_t s_last;
   const uint32_t n = a.n, lane = lane_id();
   const uint64_t j = (uint64_t)blockIdx.x * kValThreads + threadIdx.x;
   const bool valid = j < a.nw;
@@ -351,31 +343,26 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
         for (uint32_t d = 0; d < a.ndst; ++d) a.dst_vals[d][pos] = v;
     }
   }
-  if (!a.dst_hdr) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_for(a.peer);
-    const uint32_t dn = atomicAdd(&a.done[1], 1u);
-    s_last = (dn == gridDim.x - 1) ? 1u : 0u;
-    if (s_last) a.done[1] = 0;
+}
+
+// Pull signalling (rank mode): one block after the values kernel -- the kernel
+// boundary completes every NVLink store of the encode -- publishes U_s and
+// then the flag with release semantics at system scope.
+__global__ void k_agg_signal(AggArgs a) {
+  __threadfence_system();
+  const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
+  const uint64_t u = *(volatile uint64_t*)a.agg_count;
+  const uint32_t st = *(volatile uint32_t*)&a.hdr->status;
+  const uint64_t bad = *(volatile uint64_t*)&a.hdr->bad_index;
+  for (uint32_t d = threadIdx.x; d < a.ndst; d += blockDim.x) {
+    a.dst_hdr[d]->agg_count = u;
+    a.dst_hdr[d]->status = st;
+    a.dst_hdr[d]->bad_index = bad;
   }
   __syncthreads();
-  if (s_last) {  // pull signalling: publish U_s, then the flag (release, system scope)
-    fence_for(a.peer);
-    const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
-    const uint64_t u = *(volatile uint64_t*)a.agg_count;
-    const uint32_t st = *(volatile uint32_t*)&a.hdr->status;
-    const uint64_t bad = *(volatile uint64_t*)&a.hdr->bad_index;
-    for (uint32_t d = threadIdx.x; d < a.ndst; d += blockDim.x) {
-      a.dst_hdr[d]->agg_count = u;
-      a.dst_hdr[d]->status = st;
-      a.dst_hdr[d]->bad_index = bad;
-    }
-    __syncthreads();
-    fence_for(a.peer);
-    for (uint32_t d = threadIdx.x; d < a.ndst; d += blockDim.x)
-      st_release_sys(&a.dst_hdr[d]->flag, (unsigned long long)iter);
-  }
+  __threadfence_system();
+  for (uint32_t d = threadIdx.x; d < a.ndst; d += blockDim.x)
+    st_release_sys(&a.dst_hdr[d]->flag, (unsigned long long)iter);
 }
 
 // ---------------------------------------------------------------- decode ----
@@ -429,18 +416,10 @@ __global__ void __launch_bounds__(256) k_bpre(DecodeArgs a) {
   __shared__ uint64_t totals[kMaxWorkers];
   for (uint32_t x = warp; x < n; x += 8) {
     const uint32_t nb = a.blk_start[x + 1] - a.blk_start[x];
-    volatile uint32_t* b = a.bpre_blk + x * a.blk_stride;
-    uint32_t carry = 0;
-    for (uint32_t i0 = 0; i0 < nb; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const uint32_t v = i < nb ? b[i] : 0u;
-      const uint32_t inc = warp_inclusive_sum(v);
-      if (i < nb) b[i] = carry + inc - v;
-      carry += __shfl_sync(0xffffffffu, inc, 31);
-    }
+    const uint32_t total = warp_exscan_l2(a.bpre_blk + x * a.blk_stride, nb);
     if (lane == 0) {
-      a.popc_total[x] = carry;
-      totals[x] = carry;
+      a.popc_total[x] = total;
+      totals[x] = total;
     }
   }
   __syncthreads();
@@ -609,6 +588,10 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
   else
     k_agg_values<16><<<g, kValThreads, 0, stream>>>(a);
   for (int i = 0; i < 3; ++i) count_launch();
+  if (a.dst_hdr) {
+    k_agg_signal<<<1, 32, 0, stream>>>(a);
+    count_launch();
+  }
 }
 
 void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {

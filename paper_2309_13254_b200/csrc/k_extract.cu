@@ -148,10 +148,23 @@ __global__ void __launch_bounds__(256)
                       const uint64_t* d_count, K* __restrict__ out_idx,
                       float* __restrict__ out_val, uint64_t capacity, DevFamily fam,
                       HashHdr* hdr, unsigned long long* slots) {
+  __shared__ uint32_t s_range[2];
   const uint64_t z = *d_count;
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x;
+  const uint64_t i = b0 + threadIdx.x;
+  if (b0 >= z || b0 >= capacity) return;
+  if (threadIdx.x < 2) {  // tiles of the block's first and last position
+    const uint64_t q = threadIdx.x == 0 ? b0 : min(min(z, capacity), b0 + blockDim.x) - 1;
+    uint32_t lo = 0, hi = ntiles;  // largest t with tile_base[t] <= q
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (tile_base[mid] <= q) lo = mid; else hi = mid;
+    }
+    s_range[threadIdx.x] = lo;
+  }
+  __syncthreads();
   if (i >= z || i >= capacity) return;
-  uint32_t lo = 0, hi = ntiles;  // largest t with tile_base[t] <= i
+  uint32_t lo = s_range[0], hi = s_range[1] + 1;
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
     if (tile_base[mid] <= i) lo = mid; else hi = mid;

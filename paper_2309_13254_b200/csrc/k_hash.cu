@@ -169,7 +169,6 @@ __global__ void __launch_bounds__(1024) k_hash_scan(HashArgs<K> a) {
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
   extern __shared__ uint64_t soff[];  // [n] part offsets (contiguous mode)
-  __shared__ uint32_t s_last;
   const uint32_t n = a.fam.n;
   HashHdr* h = a.hdr;
   const bool ok = !(h->status & kErrCapacity);
@@ -214,35 +213,14 @@ __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
       }
     }
   }
-  // push signalling: the last block publishes this worker's count row to every
-  // server (peer memory) with release semantics, after all blocks' stores.
-  if (!a.push_hdr) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_for(a.peer);
-    s_last = (atomicAdd(&h->done, 1u) == gridDim.x - 1) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  fence_for(a.peer);
-  const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
-  const uint32_t st = *(volatile uint32_t*)&h->status;
-  for (uint32_t s = threadIdx.x; s < n; s += kThreads) {
-    PushHdr* ph = a.push_hdr[s];
-    ph->nnz = z;
-    ph->ovf_word = ovf;
-    ph->status = st;
-    for (uint32_t q = 0; q < n; ++q) ph->counts[q] = ok ? a.load[q] : 0u;
-  }
-  __syncthreads();
-  fence_for(a.peer);
-  for (uint32_t s = threadIdx.x; s < n; s += kThreads)
-    st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
 }
 
 // Sequential replay of partitions that reached the fallback scan, exactly as
 // place_index (zen/hashing.hpp:155-179) in ascending key order; the last block
-// then folds the per-partition histograms into CollisionStats.
+// then folds the per-partition histograms into CollisionStats and publishes
+// the push: this worker's count row into every server's inbox header, then the
+// flag (release, system scope).  The scatter kernel has completed by then, so
+// every part store -- NVLink stores into peer inboxes in rank mode -- is done.
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
   __shared__ uint32_t list[kThreads];
@@ -316,14 +294,31 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
     s_last = (atomicAdd(&h->fb_done, 1u) == gridDim.x - 1) ? 1u : 0u;
   }
   __syncthreads();
-  if (s_last && threadIdx.x <= k) {
-    __threadfence();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x <= k) {
     uint64_t s = 0;
     for (uint32_t p = 0; p < n; ++p)
       s += (a.fallback[p] ? ((volatile uint32_t*)a.fb_stats)[p * (k + 1) + threadIdx.x]
                           : ((volatile uint32_t*)a.stats)[p * (k + 1) + threadIdx.x]);
     a.stats_out[threadIdx.x] = s;
   }
+  if (!a.push_hdr) return;
+  fence_for(a.peer);
+  const bool cap_ok = !(h->status & kErrCapacity);
+  const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
+  const uint32_t st = *(volatile uint32_t*)&h->status;
+  for (uint32_t s = threadIdx.x; s < n; s += kThreads) {
+    PushHdr* ph = a.push_hdr[s];
+    ph->nnz = h->count;
+    ph->ovf_word = ovf;
+    ph->status = st;
+    for (uint32_t q = 0; q < n; ++q) ph->counts[q] = cap_ok ? a.load[q] : 0u;
+  }
+  __syncthreads();
+  fence_for(a.peer);
+  for (uint32_t s = threadIdx.x; s < n; s += kThreads)
+    st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
 }
 
 __global__ void k_partition_of(const uint64_t* __restrict__ idx, uint64_t count, uint64_t pc,

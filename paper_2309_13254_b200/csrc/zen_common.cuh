@@ -100,6 +100,27 @@ __device__ __forceinline__ T block_exclusive_sum(T v, T* smem, T* total) {
   return r;
 }
 
+// In-place exclusive scan of cnt u32 values by ONE warp, for "last block"
+// finishing passes: each lane owns a contiguous chunk; loads go through L2
+// (ld.cg, the values were written by other blocks) and are batched, so the
+// cost is ~2 L2 round trips rather than cnt/32 serial ones.  Returns the total.
+__device__ __forceinline__ uint32_t warp_exscan_l2(uint32_t* b, uint32_t cnt) {
+  const uint32_t lane = lane_id(), per = (cnt + 31) / 32;
+  const uint32_t lo = min(lane * per, cnt), hi = min(lo + per, cnt);
+  uint32_t sum = 0;
+#pragma unroll 8
+  for (uint32_t i = lo; i < hi; ++i) sum += __ldcg(b + i);
+  const uint32_t inc = warp_inclusive_sum(sum);
+  uint32_t run = inc - sum;
+#pragma unroll 8
+  for (uint32_t i = lo; i < hi; ++i) {
+    const uint32_t v = __ldcg(b + i);
+    __stcg(b + i, run);
+    run += v;
+  }
+  return __shfl_sync(0xffffffffu, inc, 31);
+}
+
 // ---- decoupled look-back ----------------------------------------------------
 // Status word per tile: [63:40] launch tag (24 bits), [39:38] flag, [37:0] value.
 // Tags come from a per-kernel control block {ticket, done, tag} that the last

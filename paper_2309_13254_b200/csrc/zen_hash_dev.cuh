@@ -58,25 +58,29 @@ __device__ __forceinline__ void hash_begin_body(const zen::HashArgs<K>& a) {
   zen::HashHdr* h = a.hdr;
   const uint32_t n = a.fam.n, k = a.fam.k;
   if (threadIdx.x == 0) {
+    // all header loads issue together, then the stores (one round trip each)
     const uint64_t z = h->count;
-    if (h->derive) {
-      uint64_t r1 = (uint64_t)ceil(h->r1_mult * (double)z / (double)n);
+    const uint32_t derive = h->derive, epoch = h->epoch, iter = h->iter;
+    const double r1m = h->r1_mult, r2r = h->r2_ratio;
+    uint64_t r1 = h->r1, r2 = h->r2;
+    if (derive) {
+      r1 = (uint64_t)ceil(r1m * (double)z / (double)n);
       if (r1 < 1) r1 = 1;
-      uint64_t r2 = (uint64_t)ceil(h->r2_ratio * (double)r1);
+      r2 = (uint64_t)ceil(r2r * (double)r1);
       if (r2 < 1) r2 = 1;
       h->r1 = r1;
       h->r2 = r2;
     }
-    h->stride = h->r1 + h->r2;
-    h->epoch = h->epoch + 1u;
+    h->stride = r1 + r2;
+    h->epoch = epoch + 1u;
     h->ovf_word = ~0ull;
     h->done = 0;
     h->fb_done = 0;
     h->fallback_any = 0;
     h->ntiles = (uint32_t)((z + zen::kHashTile - 1) / zen::kHashTile);
-    h->iter = h->iter + 1u;
+    h->iter = iter + 1u;
     h->bad_index = ~0ull;
-    if (z > a.cap || h->stride > a.stride_cap) atomicOr(&h->status, zen::kErrCapacity);
+    if (z > a.cap || r1 + r2 > a.stride_cap) atomicOr(&h->status, zen::kErrCapacity);
   }
   for (uint32_t i = threadIdx.x; i < n * (k + 1); i += blockDim.x) {
     a.stats[i] = 0;
