@@ -212,6 +212,11 @@ zen_status zen_bp_use_graph(zen_bp* bp, int on);
 zen_status zen_bp_sync_host(zen_bp* bp, const float* const* h_dense, uint64_t* h_idx,
                             float* h_val, uint64_t capacity, uint64_t* count);
 
+/* diagnostics (tests only): what = 0 -> a local worker's compacted keys (u32
+ * indices); what = 1 -> the part `worker` pushed into local `server`'s inbox */
+zen_status zen_bp_debug_part(zen_bp* bp, int what, uint32_t server, uint32_t worker,
+                             uint32_t* h_idx, float* h_val, uint64_t capacity, uint64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -108,6 +108,17 @@ struct DevGuard {
   }
 };
 
+// Stream that orders setup-time zeroing and uploads.  PyTorch streams are
+// cudaStreamNonBlocking, so legacy-stream cudaMemset/cudaMemcpy would NOT be
+// ordered before kernels on the framework's stream: every API entry point
+// scopes this to its context stream.
+thread_local cudaStream_t t_setup = nullptr;
+struct SetupStream {
+  cudaStream_t prev;
+  explicit SetupStream(cudaStream_t s) : prev(t_setup) { t_setup = s; }
+  ~SetupStream() { t_setup = prev; }
+};
+
 // RAII list of device allocations
 struct DevMem {
   std::vector<void*> ptrs;
@@ -122,7 +133,7 @@ struct DevMem {
     const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
     CK(cudaMalloc(&p, bytes));
     ptrs.push_back(p);
-    if (zero) CK(cudaMemset(p, 0, bytes));
+    if (zero) CK(cudaMemsetAsync(p, 0, bytes, t_setup));
     *out = static_cast<T*>(p);
     return ZEN_OK;
   }
@@ -130,7 +141,8 @@ struct DevMem {
 
 template <typename T>
 zen_status upload(T* d, const T* h, size_t count) {
-  CK(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice));
+  CK(cudaMemcpyAsync(d, h, count * sizeof(T), cudaMemcpyHostToDevice, t_setup));
+  CK(cudaStreamSynchronize(t_setup));  // h may be a temporary
   return ZEN_OK;
 }
 
@@ -261,6 +273,7 @@ zen_status zen_to_sparse(zen_ctx* c, const float* d_dense, uint64_t m, uint64_t*
   if (!c || !d_dense || !nnz) return fail(ZEN_E_INVALID, "null argument");
   if (m == 0) return fail(ZEN_E_INVALID, "dense tensor must have at least one element");  // tensor.hpp:24
   DevGuard g(c->device);
+  SetupStream setup_(c->stream);
   DevMem mem;
   const uint64_t ntiles = (m + kExtractTile - 1) / kExtractTile;
   ExtractWs<uint64_t> ws{};
@@ -296,6 +309,7 @@ zen_status zen_hierarchical_hash(zen_ctx* c, const uint64_t* d_idx, const float*
   if (count && (!d_idx || !d_val || !d_out_idx || !d_out_val))
     return fail(ZEN_E_INVALID, "null tensor pointer");
   DevGuard g(c->device);
+  SetupStream setup_(c->stream);
   const uint64_t stride = r1 + r2;
   const uint64_t cells = uint64_t(n) * stride;
   const uint64_t cap = std::max<uint64_t>(count, 1);
@@ -307,10 +321,11 @@ zen_status zen_hierarchical_hash(zen_ctx* c, const uint64_t* d_idx, const float*
   a.fam = fold(*fam);
   CKR(mem.alloc(&a.hdr, 1));
   CKR(mem.alloc(&a.slots, cells, false));
-  CK(cudaMemset(a.slots, 0xFF, std::max<size_t>(cells * 8, 16)));
+  CK(cudaMemsetAsync(a.slots, 0xFF, std::max<size_t>(cells * 8, 16), t_setup));
   const bool dump = d_slots || d_slot_vals;
   if (dump) CKR(mem.alloc(&a.slot_vals, cells));
   CKR(mem.alloc(&a.meta, cap));
+  CKR(mem.alloc(&a.pmeta, cap));
   CKR(mem.alloc(&a.tile_cnt, ntiles * n));
   CKR(mem.alloc(&a.tile_scnt, ntiles * n));
   CKR(mem.alloc(&a.load, n));
@@ -493,6 +508,7 @@ zen_status zen_universe_create(zen_ctx* c, uint64_t m, uint32_t n, uint64_t psee
   if (n > ZEN_MAX_PARTITIONS) return fail(ZEN_E_INVALID, "server count above ZEN_MAX_PARTITIONS");
   if (m == 0 || m >= 0xFFFFFFFFull) return fail(ZEN_E_INVALID, "universe must be in [1, 2^32-1)");
   DevGuard g(c->device);
+  SetupStream setup_(c->stream);
   auto u = std::make_unique<zen_universe>();
   u->ctx = c;
   u->m = m;
@@ -516,6 +532,7 @@ uint64_t zen_universe_size(const zen_universe* u, uint32_t s) {
 zen_status zen_universe_indices(zen_universe* u, uint32_t s, uint64_t* d_out) {
   if (!u || s >= u->n) return fail(ZEN_E_INVALID, "bad universe/server");
   DevGuard g(u->ctx->device);
+  SetupStream setup_(u->ctx->stream);
   CKR(u->ensure_own(s));
   launch_universe_indices(u->own[s], u->nwords, d_out, u->ctx->stream);
   CK(cudaGetLastError());
@@ -530,6 +547,7 @@ zen_status zen_hash_bitmap_encode(zen_universe* u, uint32_t s, const uint64_t* d
   if (count && (!d_idx || !d_val)) return fail(ZEN_E_INVALID, "null tensor");
   zen_ctx* c = u->ctx;
   DevGuard g(c->device);
+  SetupStream setup_(c->stream);
   CKR(u->ensure_own(s));
   const uint64_t bs = u->bs[s];
   const uint64_t nw = (bs + 63) / 64;
@@ -627,6 +645,7 @@ zen_status zen_hash_bitmap_decode(zen_universe* u, uint32_t s, const uint8_t* d_
   if (u->n > ZEN_MAX_WORKERS) return fail(ZEN_E_INVALID, "decode supports n <= ZEN_MAX_WORKERS");
   zen_ctx* c = u->ctx;
   DevGuard g(c->device);
+  SetupStream setup_(c->stream);
   const uint64_t bs = u->bs[s];
   const uint64_t nw = (bs + 63) / 64;
   const uint64_t bitmap_bytes = (bs + 7) / 8;
@@ -800,6 +819,9 @@ struct zen_bp {
   uint32_t kernels_per_sync = 0;
   // e2e staging
   std::vector<float*> dense_dev;
+  // hash-memory side path stream + fork/join events
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   // CUDA graph of the dense sync
   bool use_graph = true;
   cudaGraphExec_t gexec = nullptr;
@@ -827,9 +849,10 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   a.val = w.vals;
   CKR(mem.alloc(&a.hdr, 1));
   CKR(mem.alloc(&a.slots, size_t(n) * bp->stride_cap, false));
-  CK(cudaMemset(a.slots, 0xFF, size_t(n) * bp->stride_cap * 8));
+  CK(cudaMemsetAsync(a.slots, 0xFF, size_t(n) * bp->stride_cap * 8, t_setup));
   a.slot_vals = nullptr;
   CKR(mem.alloc(&a.meta, cap));
+  CKR(mem.alloc(&a.pmeta, cap));
   CKR(mem.alloc(&a.tile_cnt, ntiles * n));
   CKR(mem.alloc(&a.tile_scnt, ntiles * n));
   CKR(mem.alloc(&a.load, n));
@@ -998,6 +1021,7 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
   if (!(params->r1_multiplier > 0) || !(params->r2_ratio > 0))
     return fail(ZEN_E_INVALID, "r1_multiplier and r2_ratio must be positive");
   DevGuard g(c->device);
+  SetupStream setup_(c->stream);
   auto bp = std::make_unique<zen_bp>();
   bp->ctx = c;
   bp->n = n;
@@ -1022,6 +1046,9 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
   }
   bp->L = make_layout(n, bp->cap, bp->nw, bp->valcap, true);
   bp->L0 = make_layout(n, bp->cap, bp->nw, bp->valcap, false);
+  CK(cudaStreamCreateWithFlags(&bp->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&bp->fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&bp->join, cudaEventDisableTiming));
   const uint32_t nlocal = bp->local ? n : 1;
   for (uint32_t i = 0; i < nlocal; ++i) {
     Worker w;
@@ -1040,7 +1067,7 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
     const ArenaLayout& L = bp->layout_of(r);
     void* p = nullptr;
     CK(cudaMalloc(&p, L.bytes));
-    CK(cudaMemset(p, 0, L.bytes));
+    CK(cudaMemsetAsync(p, 0, L.bytes, t_setup));
     bp->arenas[r].base = (char*)p;
     bp->arenas[r].owned = true;
   }
@@ -1093,6 +1120,9 @@ void zen_bp_destroy(zen_bp* bp) {
   }
   for (auto e : bp->ev) cudaEventDestroy(e);
   for (auto e : bp->gev) cudaEventDestroy(e);
+  if (bp->fork) cudaEventDestroy(bp->fork);
+  if (bp->join) cudaEventDestroy(bp->join);
+  if (bp->side) cudaStreamDestroy(bp->side);
   if (bp->gexec) cudaGraphExecDestroy(bp->gexec);
   if (bp->gdef) cudaGraphDestroy(bp->gdef);
   for (auto p : bp->dense_dev) cudaFree(p);
@@ -1105,6 +1135,7 @@ zen_status zen_bp_set_params(zen_bp* bp, const zen_hash_params* p) {
     return fail(ZEN_E_INVALID, "rehash depth out of range");
   if (p->seed != bp->params.seed) return fail(ZEN_E_INVALID, "changing the seed needs a new zen_bp");
   DevGuard g(bp->ctx->device);
+  SetupStream setup_(bp->ctx->stream);
   CK(cudaStreamSynchronize(bp->ctx->stream));
   bp->params = *p;
   const uint64_t sc = stride_cap_for(*p, bp->cap, bp->n);
@@ -1112,15 +1143,15 @@ zen_status zen_bp_set_params(zen_bp* bp, const zen_hash_params* p) {
     if (sc > bp->stride_cap) {
       unsigned long long* slots;
       CKR(bp->mem.alloc(&slots, size_t(bp->n) * sc, false));
-      CK(cudaMemset(slots, 0xFF, size_t(bp->n) * sc * 8));
+      CK(cudaMemsetAsync(slots, 0xFF, size_t(bp->n) * sc * 8, t_setup));
       w.a.slots = slots;
       w.a.stride_cap = sc;
       uint32_t zero = 0;
-      CK(cudaMemcpy(&w.a.hdr->epoch, &zero, 4, cudaMemcpyHostToDevice));
+      CKR(upload(&w.a.hdr->epoch, &zero, 1));
       w.epoch_runs = 0;
     }
-    CK(cudaMemcpy(&w.a.hdr->r1_mult, &p->r1_multiplier, 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(&w.a.hdr->r2_ratio, &p->r2_ratio, 8, cudaMemcpyHostToDevice));
+    CKR(upload(&w.a.hdr->r1_mult, &p->r1_multiplier, 1));
+    CKR(upload(&w.a.hdr->r2_ratio, &p->r2_ratio, 1));
     zen_hash_family f;
     CKR(zen_hash_family_make_worker(p->seed, w.id, bp->n, p->rehash_depth, &f));
     w.a.fam = fold(f);
@@ -1148,6 +1179,7 @@ zen_status zen_bp_connect(zen_bp* bp, const void* handles) {
   if (!bp || !handles) return fail(ZEN_E_INVALID, "null argument");
   if (bp->local) return ZEN_OK;
   DevGuard g(bp->ctx->device);
+  SetupStream setup_(bp->ctx->stream);
   const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
   for (uint32_t r = 0; r < bp->n; ++r) {
     if (r == bp->rank || bp->arenas[r].base) continue;
@@ -1188,20 +1220,27 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     }
   }
   if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
+  // data path on `st`; the hash-memory side path of each worker forks onto
+  // bp->side and joins at the end of the sync
   for (auto& w : bp->workers) {
-    if (from_dense) {  // compaction of the staged non-zeros fused with the placement
+    if (from_dense) {
       launch_extract_compact_place<uint32_t>(bp->m, w.ex, w.keys, w.vals, bp->cap, w.a.fam,
-                                             w.a.hdr, w.a.slots, st);
-      launch_hash_rest<uint32_t>(w.a, bp->n, bp->params.rehash_depth, st);
+                                             w.a.hdr, w.a.slots, /*place=*/false, st);
     } else {
-      launch_hash<uint32_t>(w.a, bp->n, bp->params.rehash_depth, st);
+      launch_hash_begin<uint32_t>(w.a, st);
     }
+    CK(cudaEventRecord(bp->fork, st));
+    CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
+    launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side);
+    launch_hash_critical<uint32_t>(w.a, bp->n, st);
   }
   if (ev) CK(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
   for (auto& s : bp->servers) launch_aggregate(s.a, st);
   if (ev) CK(cudaEventRecordWithFlags(ev[3], st, cudaEventRecordExternal));
   bp->dec.launch(bp->da, st);
   if (ev) CK(cudaEventRecordWithFlags(ev[4], st, cudaEventRecordExternal));
+  CK(cudaEventRecord(bp->join, bp->side));
+  CK(cudaStreamWaitEvent(st, bp->join, 0));
   CK(cudaGetLastError());
   return ZEN_OK;
 }
@@ -1456,6 +1495,7 @@ zen_status zen_bp_balance(zen_bp* bp, double* push, double* pull, int* valid) {
 zen_status zen_bp_collision_stats(zen_bp* bp, uint32_t worker, zen_collision_stats* out) {
   if (!bp || !out) return fail(ZEN_E_INVALID, "null argument");
   DevGuard g(bp->ctx->device);
+  SetupStream setup_(bp->ctx->stream);
   CKR(bp_collect(bp));
   for (auto& w : bp->workers) {
     if (w.id != worker) continue;
@@ -1517,6 +1557,7 @@ zen_status zen_bp_sync_host(zen_bp* bp, const float* const* h_dense, uint64_t* h
                             float* h_val, uint64_t capacity, uint64_t* count) {
   if (!bp || !h_dense || !count) return fail(ZEN_E_INVALID, "null argument");
   DevGuard g(bp->ctx->device);
+  SetupStream setup_(bp->ctx->stream);
   cudaStream_t st = bp->ctx->stream;
   if (bp->dense_dev.empty()) {
     for (size_t i = 0; i < bp->workers.size(); ++i) {
@@ -1540,3 +1581,53 @@ zen_status zen_bp_sync_host(zen_bp* bp, const float* const* h_dense, uint64_t* h
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- debug ----
+// Test/diagnostic access to a local worker's compacted keys and a local
+// server's inbox part (what worker `w` pushed to it).  Not on the hot path.
+extern "C" zen_status zen_bp_debug_part(zen_bp* bp, int what, uint32_t server, uint32_t worker,
+                                        uint32_t* h_idx, float* h_val, uint64_t cap,
+                                        uint64_t* count) {
+  if (!bp || !count) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(bp->ctx->device);
+  CK(cudaStreamSynchronize(bp->ctx->stream));
+  if (what == 0) {  // compacted keys of a local worker
+    for (auto& w : bp->workers) {
+      if (w.id != worker) continue;
+      HashHdr h{};
+      CK(cudaMemcpy(&h, w.a.hdr, sizeof(h), cudaMemcpyDeviceToHost));
+      *count = h.count;
+      const uint64_t c = std::min(cap, h.count);
+      CK(cudaMemcpy(h_idx, w.keys, c * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(h_val, w.vals, c * 4, cudaMemcpyDeviceToHost));
+      return ZEN_OK;
+    }
+    return fail(ZEN_E_INVALID, "worker not local");
+  }
+  if (what == 2 || what == 3) {  // 2: server's pull bitmap words; 3: own table (mask, prefix)
+    if (server >= bp->n) return fail(ZEN_E_INVALID, "bad server");
+    if (what == 2) {
+      const Arena& R = bp->arena_of(bp->local ? 0 : bp->rank);
+      const uint64_t nw = bp->nw[server];
+      *count = nw;
+      CK(cudaMemcpy(h_idx, R.bits(bp->L, server), std::min(cap, nw) * 8, cudaMemcpyDeviceToHost));
+      return ZEN_OK;
+    }
+    CKR(bp->uni->ensure_own(server));
+    *count = bp->uni->nwords;
+    CK(cudaMemcpy(h_idx, bp->uni->own[server], std::min(cap, bp->uni->nwords) * 16,
+                  cudaMemcpyDeviceToHost));
+    return ZEN_OK;
+  }
+  // inbox part worker -> server (server must be local)
+  const Arena& A = bp->arena_of(server);
+  if (!A.base || (!bp->local && server != bp->rank)) return fail(ZEN_E_INVALID, "server not local");
+  const ArenaLayout& L = bp->layout_of(server);
+  PushHdr ph{};
+  CK(cudaMemcpy(&ph, A.push_hdr(L) + worker, sizeof(ph), cudaMemcpyDeviceToHost));
+  *count = ph.counts[server];
+  const uint64_t c = std::min<uint64_t>(cap, ph.counts[server]);
+  CK(cudaMemcpy(h_idx, A.inbox_idx(L) + size_t(worker) * bp->cap, c * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h_val, A.inbox_val(L) + size_t(worker) * bp->cap, c * 4, cudaMemcpyDeviceToHost));
+  return ZEN_OK;
+}

@@ -211,11 +211,17 @@ void launch_extract_tiles_begin(const float* dense, uint64_t m, const ExtractWs<
 template <typename K>
 void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx, float* out_val,
                                   uint64_t capacity, const DevFamily& fam, HashHdr* hdr,
-                                  unsigned long long* slots, cudaStream_t stream) {
+                                  unsigned long long* slots, bool place, cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  k_extract_compact<K, true><<<blocks_for(std::min<uint64_t>(capacity, m)), 256, 0, stream>>>(
-      ws.st_idx, ws.st_val, ws.tile_base, ntiles, &hdr->count, out_idx, out_val, capacity, fam,
-      hdr, slots);
+  const unsigned g = blocks_for(std::min<uint64_t>(capacity, m));
+  if (place)
+    k_extract_compact<K, true><<<g, 256, 0, stream>>>(ws.st_idx, ws.st_val, ws.tile_base, ntiles,
+                                                      &hdr->count, out_idx, out_val, capacity,
+                                                      fam, hdr, slots);
+  else
+    k_extract_compact<K, false><<<g, 256, 0, stream>>>(ws.st_idx, ws.st_val, ws.tile_base,
+                                                       ntiles, &hdr->count, out_idx, out_val,
+                                                       capacity, fam, hdr, slots);
   count_launch();
 }
 
@@ -226,7 +232,7 @@ void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx
                                               const HashArgs<K>&, uint64_t, cudaStream_t);       \
   template void launch_extract_compact_place<K>(uint64_t, const ExtractWs<K>&, K*, float*,      \
                                                 uint64_t, const DevFamily&, HashHdr*,           \
-                                                unsigned long long*, cudaStream_t);
+                                                unsigned long long*, bool, cudaStream_t);
 ZEN_INST(uint32_t)
 ZEN_INST(uint64_t)
 #undef ZEN_INST

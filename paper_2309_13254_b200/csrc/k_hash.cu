@@ -1,8 +1,24 @@
 // k_hash.cu -- hierarchical hashing (Algorithm 1; zen/hashing.hpp:121-262) on sm_100a.
 //
 // Bit-exact with the reference's single-lane run (the only layout the
-// reference defines deterministically, zen/hashing.hpp:212-213 and :259-262):
+// reference defines deterministically, zen/hashing.hpp:212-213 and :259-262).
+// Split into two independent paths so that the hash memory placement -- which
+// the parts do not depend on -- runs off the critical path of a BP sync:
 //
+// DATA PATH (feeds the push):
+//  part    : one key per thread, 256-key tiles: h0 partition and the key's
+//            stable rank inside its tile among same-partition keys
+//            (match_any + per-warp counts); per-(partition, tile) counts.
+//  scan    : one block per partition scans its tile counts -> loads.
+//  scatter : position = tile offset + rank, i.e. a stable multi-split by h0 ->
+//            the parts, ascending as from_pairs sorts (zen/tensor.hpp:48-59).
+//            In the BP pipeline the destinations are the owners' inboxes, so
+//            the push (NVLink stores in rank mode) is fused here.  Overflow
+//            (load > r1+r2) depends on the loads only: its witness is the
+//            (r1+r2+1)-th key of an overfull partition, the globally smallest
+//            of which is the reference's first drop (zen/hashing.hpp:176-177).
+//
+// SIDE PATH (hash memory layout + CollisionStats, concurrent with the push):
 //  place   : lock-free PRIORITY CLAIM.  Slots are u64 words
 //            [63:40] = 0xFFFFFF - epoch, [39:0] = index+1; a key proposes with
 //            atomicMin, so the smallest key wins every slot it ever asks for
@@ -12,25 +28,14 @@
 //            in ascending key order = the reference's lanes=1 greedy, for ANY
 //            thread schedule.  Older epochs carry larger words, so stale slots
 //            lose automatically: no memset of the hash memory per run.
-//  post    : one key per thread, 256-key tiles.  The first probe whose slot
-//            holds the key gives its depth (CollisionStats), else it is serial.
-//            match_any + per-warp counts give every key its stable rank inside
-//            the tile among same-partition keys (and among same-partition
-//            serial keys); both ranks are packed into meta with p and depth.
-//  scan    : one block per partition scans its per-tile counts (tile-major
-//            layout), detecting overflow (load > r1+r2) and fallback
-//            (serial > r2).
-//  scatter : one key per thread: position = tile offset + packed rank, i.e. a
-//            stable multi-split by h0 -> the partitioned output, ascending
-//            within each part (from_pairs sorts, zen/tensor.hpp:48-59).  Serial
-//            keys take slot r1 + (ascending serial rank).  Overflow witness =
-//            the (r1+r2+1)-th key of an overfull partition; the globally
-//            smallest one is the reference's first drop (zen/hashing.hpp:176-177).
-//            In the BP pipeline the parts are stored straight into the owner
-//            GPU's inbox over NVLink (peer pointers): the push is fused here.
+//  depth   : the first probe whose slot holds the key gives its depth, else it
+//            is serial; stable serial ranks per tile; depth histogram.
+//  serial  : per-partition scan of serial counts; serial keys take slot
+//            r1 + (ascending serial rank).
 //  fallback: partitions whose serial keys exceed r2 hit the order-dependent
 //            fallback scan (zen/hashing.hpp:170-175) and are replayed
 //            sequentially (rare: ~3% serial vs r2 = 10% of r1).
+#include <algorithm>
 #include <cmath>
 
 #include "zen_common.cuh"
@@ -52,6 +57,144 @@ __global__ void k_hash_begin(HashArgs<K> a) {
   hash_begin_body(a);
 }
 
+// ------------------------------------------------------------- data path ----
+
+template <typename K>
+__global__ void __launch_bounds__(kThreads) k_part(HashArgs<K> a) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t n = a.fam.n;
+  uint32_t* wc = sm;  // [kWarps][n] key counts -> cross-warp prefixes
+  const HashHdr* h = a.hdr;
+  if (h->status & kErrCapacity) return;
+  const uint32_t tile = blockIdx.x;
+  if (tile >= h->ntiles) return;
+  const uint64_t z = h->count;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t q = threadIdx.x; q < kWarps * n; q += kThreads) wc[q] = 0;
+  const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
+  const bool valid = i < z;
+  const uint32_t p = valid ? part_of(a.fam, (uint64_t)a.idx[i] + 1) : kInvalid;
+  __syncthreads();
+  const uint32_t g = __match_any_sync(0xffffffffu, p);
+  const uint32_t wr = __popc(g & lanemask_lt());
+  if (valid && lane == (uint32_t)(__ffs(g) - 1)) wc[warp * n + p] = __popc(g);
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < n; q += kThreads) {
+    uint32_t acc = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t t = wc[w * n + q];
+      wc[w * n + q] = acc;
+      acc += t;
+    }
+    a.tile_cnt[(uint64_t)q * a.tiles_cap + tile] = acc;
+  }
+  __syncthreads();
+  if (valid) a.pmeta[i] = p | ((wc[warp * n + p] + wr) << 16);
+}
+
+// exclusive scan of `ntiles` per-tile counts, in place (one block)
+__device__ __forceinline__ uint32_t block_scan_tiles(uint32_t* arr, uint32_t ntiles,
+                                                     uint32_t* sscan) {
+  constexpr int E = 4;
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < ntiles; b += blockDim.x * E) {
+    const uint32_t t0 = b + threadIdx.x * E;
+    uint32_t v[E], local = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      v[e] = (t0 + e < ntiles) ? arr[t0 + e] : 0u;
+      local += v[e];
+    }
+    uint32_t tot;
+    uint32_t ex = carry + block_exclusive_sum(local, sscan, &tot);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (t0 + e < ntiles) arr[t0 + e] = ex;
+      ex += v[e];
+    }
+    carry += tot;
+  }
+  return carry;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(1024) k_part_scan(HashArgs<K> a) {
+  __shared__ uint32_t sscan[33];
+  HashHdr* h = a.hdr;
+  if (h->status & kErrCapacity) return;
+  const uint32_t p = blockIdx.x;
+  const uint32_t total =
+      block_scan_tiles(a.tile_cnt + (uint64_t)p * a.tiles_cap, h->ntiles, sscan);
+  if (threadIdx.x == 0) a.load[p] = total;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
+  extern __shared__ uint64_t soff[];  // [n] part offsets (contiguous mode)
+  const uint32_t n = a.fam.n;
+  HashHdr* h = a.hdr;
+  const bool ok = !(h->status & kErrCapacity);
+  const uint64_t z = h->count, r1 = h->r1, r2 = h->r2;
+  const uint32_t tile = blockIdx.x;
+  if (!a.dst_table) {
+    if (threadIdx.x == 0) {
+      uint64_t off = 0;
+      for (uint32_t q = 0; q < n; ++q) {
+        soff[q] = off;
+        off += a.load[q];
+      }
+    }
+    __syncthreads();
+  }
+  const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
+  if (!ok || tile >= h->ntiles || i >= z) return;
+  const uint32_t pm = a.pmeta[i];
+  const uint32_t p = pm & 0xFFFFu;
+  const K x = a.idx[i];
+  const float v = a.val[i];
+  const uint64_t pos = (uint64_t)a.tile_cnt[(uint64_t)p * a.tiles_cap + tile] + (pm >> 16);
+  if (a.dst_table) {
+    if (pos < a.dst_cap) {
+      a.dst_idx[p][pos] = x;
+      a.dst_val[p][pos] = v;
+    } else {
+      atomicOr(&h->status, kErrCapacity);
+    }
+  } else {
+    a.out_idx[soff[p] + pos] = x;
+    a.out_val[soff[p] + pos] = v;
+  }
+  if (pos == r1 + r2)
+    atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)x + 1) << 16) | p);
+}
+
+// Push signalling: one block after the scatter (the kernel boundary completes
+// every part store, NVLink stores in rank mode): this worker's count row into
+// every server's inbox header, then the flag (release, system scope).
+template <typename K>
+__global__ void k_push_signal(HashArgs<K> a) {
+  HashHdr* h = a.hdr;
+  const uint32_t n = a.fam.n;
+  fence_for(a.peer);
+  const bool cap_ok = !(h->status & kErrCapacity);
+  const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
+  const uint32_t st = *(volatile uint32_t*)&h->status;
+  const uint64_t z = h->count;
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+    PushHdr* ph = a.push_hdr[s];
+    ph->nnz = z;
+    ph->ovf_word = ovf;
+    ph->status = st;
+    for (uint32_t q = 0; q < n; ++q) ph->counts[q] = cap_ok ? a.load[q] : 0u;
+  }
+  __syncthreads();
+  fence_for(a.peer);
+  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x)
+    st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
+}
+
+// ------------------------------------------------------------- side path ----
+
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_place(HashArgs<K> a) {
   const HashHdr* h = a.hdr;
@@ -64,20 +207,18 @@ __global__ void __launch_bounds__(kThreads) k_place(HashArgs<K> a) {
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kThreads) k_post(HashArgs<K> a) {
+__global__ void __launch_bounds__(kThreads) k_depth(HashArgs<K> a) {
   extern __shared__ uint32_t sm[];
   const uint32_t n = a.fam.n, k = a.fam.k;
-  uint32_t* wc = sm;               // [kWarps][n] key counts  -> cross-warp prefixes
-  uint32_t* ws = sm + kWarps * n;  // [kWarps][n] serial counts
+  uint32_t* ws = sm;  // [kWarps][n] serial counts -> cross-warp prefixes
   const HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
   const uint32_t tile = blockIdx.x;
-  const uint32_t ntiles = h->ntiles;
-  if (tile >= ntiles) return;
+  if (tile >= h->ntiles) return;
   const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
   const uint64_t ew = epoch_word(h->epoch);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint32_t q = threadIdx.x; q < kWarps * n; q += kThreads) wc[q] = ws[q] = 0;
+  for (uint32_t q = threadIdx.x; q < kWarps * n; q += kThreads) ws[q] = 0;
   const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
   const bool valid = i < z;
   uint32_t p = kInvalid, depth = 0;
@@ -95,132 +236,65 @@ __global__ void __launch_bounds__(kThreads) k_post(HashArgs<K> a) {
     }
   }
   __syncthreads();
-  const uint32_t g = __match_any_sync(0xffffffffu, p);
   const uint32_t ks = (valid && depth == 0) ? p : kInvalid;
   const uint32_t gs = __match_any_sync(0xffffffffu, ks);
-  const uint32_t wr = __popc(g & lanemask_lt()), wsr = __popc(gs & lanemask_lt());
-  if (valid && lane == (uint32_t)(__ffs(g) - 1)) wc[warp * n + p] = __popc(g);
+  const uint32_t wsr = __popc(gs & lanemask_lt());
   if (ks != kInvalid && lane == (uint32_t)(__ffs(gs) - 1)) ws[warp * n + p] = __popc(gs);
   const uint32_t kd = valid ? (p * 32u + depth) : kInvalid;
   const uint32_t gd = __match_any_sync(0xffffffffu, kd);
   if (valid && lane == (uint32_t)(__ffs(gd) - 1))
     atomicAdd(&a.stats[p * (k + 1) + depth], (uint32_t)__popc(gd));
   __syncthreads();
-  for (uint32_t q = threadIdx.x; q < n; q += kThreads) {  // cross-warp exclusive prefixes
-    uint32_t acc = 0, sacc = 0;
+  for (uint32_t q = threadIdx.x; q < n; q += kThreads) {
+    uint32_t acc = 0;
     for (int w = 0; w < kWarps; ++w) {
-      const uint32_t t = wc[w * n + q], st = ws[w * n + q];
-      wc[w * n + q] = acc;
-      ws[w * n + q] = sacc;
+      const uint32_t t = ws[w * n + q];
+      ws[w * n + q] = acc;
       acc += t;
-      sacc += st;
     }
-    a.tile_cnt[(uint64_t)q * a.tiles_cap + tile] = acc;
-    a.tile_scnt[(uint64_t)q * a.tiles_cap + tile] = sacc;
+    a.tile_scnt[(uint64_t)q * a.tiles_cap + tile] = acc;
   }
   __syncthreads();
-  if (valid) {
-    const uint32_t rank = wc[warp * n + p] + wr;
-    const uint32_t srank = depth == 0 ? ws[warp * n + p] + wsr : 0u;
-    a.meta[i] = pack_meta(p, depth, rank, srank);
-  }
+  if (valid) a.meta[i] = pack_meta(p, depth, 0, depth == 0 ? ws[warp * n + p] + wsr : 0u);
 }
 
-// one block per partition: exclusive scans of its tile counts (in place)
 template <typename K>
-__global__ void __launch_bounds__(1024) k_hash_scan(HashArgs<K> a) {
+__global__ void __launch_bounds__(1024) k_serial_scan(HashArgs<K> a) {
   __shared__ uint32_t sscan[33];
   HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
   const uint32_t p = blockIdx.x;
-  const uint32_t ntiles = h->ntiles;
-  constexpr int E = 4;
-  for (int pass = 0; pass < 2; ++pass) {
-    uint32_t* arr = (pass == 0 ? a.tile_cnt : a.tile_scnt) + (uint64_t)p * a.tiles_cap;
-    uint32_t carry = 0;
-    for (uint32_t b = 0; b < ntiles; b += blockDim.x * E) {
-      const uint32_t t0 = b + threadIdx.x * E;
-      uint32_t v[E], local = 0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        v[e] = (t0 + e < ntiles) ? arr[t0 + e] : 0u;
-        local += v[e];
-      }
-      uint32_t tot;
-      uint32_t ex = carry + block_exclusive_sum(local, sscan, &tot);
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if (t0 + e < ntiles) arr[t0 + e] = ex;
-        ex += v[e];
-      }
-      carry += tot;
-    }
-    if (threadIdx.x == 0) (pass == 0 ? a.load : a.sload)[p] = carry;
-  }
+  const uint32_t total =
+      block_scan_tiles(a.tile_scnt + (uint64_t)p * a.tiles_cap, h->ntiles, sscan);
   if (threadIdx.x == 0) {
-    const uint32_t fb =
-        (a.sload[p] > h->r2 && (uint64_t)a.load[p] <= h->r1 + h->r2) ? 1u : 0u;
+    a.sload[p] = total;
+    const uint32_t fb = (total > h->r2 && (uint64_t)a.load[p] <= h->r1 + h->r2) ? 1u : 0u;
     a.fallback[p] = fb;
     if (fb) atomicOr(&h->fallback_any, 1u);
   }
 }
 
-// One key per thread: stable multi-split store (+ serial slots, overflow witness)
 template <typename K>
-__global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
-  extern __shared__ uint64_t soff[];  // [n] part offsets (contiguous mode)
-  const uint32_t n = a.fam.n;
+__global__ void __launch_bounds__(kThreads) k_serial_scatter(HashArgs<K> a) {
   HashHdr* h = a.hdr;
-  const bool ok = !(h->status & kErrCapacity);
-  const uint64_t z = h->count, r1 = h->r1, r2 = h->r2, stride = h->stride;
-  const uint64_t ew = epoch_word(h->epoch);
+  if (h->status & kErrCapacity) return;
   const uint32_t tile = blockIdx.x;
-  if (!a.dst_table && threadIdx.x == 0) {
-    uint64_t off = 0;
-    for (uint32_t q = 0; q < n; ++q) {
-      soff[q] = off;
-      off += a.load[q];
-    }
-  }
-  __syncthreads();
   const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
-  if (ok && tile < h->ntiles && i < z) {
-    const uint32_t meta = a.meta[i];
-    const uint32_t p = meta_part(meta), depth = meta_depth(meta);
-    const K x = a.idx[i];
-    const float v = a.val[i];
-    const uint64_t key = (uint64_t)x + 1;
-    const uint64_t pos = (uint64_t)a.tile_cnt[(uint64_t)p * a.tiles_cap + tile] + meta_rank(meta);
-    if (a.dst_table) {
-      if (pos < a.dst_cap) {
-        a.dst_idx[p][pos] = x;
-        a.dst_val[p][pos] = v;
-      } else {
-        atomicOr(&h->status, kErrCapacity);
-      }
-    } else {
-      a.out_idx[soff[p] + pos] = x;
-      a.out_val[soff[p] + pos] = v;
-    }
-    if (pos == r1 + r2) atomicMin((unsigned long long*)&h->ovf_word, (key << 16) | p);
-    if (depth == 0) {
-      const uint64_t spos =
-          (uint64_t)a.tile_scnt[(uint64_t)p * a.tiles_cap + tile] + meta_srank(meta);
-      if (spos < r2) {
-        const uint64_t s = (uint64_t)p * stride + r1 + spos;
-        a.slots[s] = ew | key;
-        if (a.slot_vals) a.slot_vals[s] = v;
-      }
-    }
+  if (tile >= h->ntiles || i >= h->count) return;
+  const uint32_t m = a.meta[i];
+  if (meta_depth(m) != 0) return;
+  const uint32_t p = meta_part(m);
+  const uint64_t spos = (uint64_t)a.tile_scnt[(uint64_t)p * a.tiles_cap + tile] + meta_srank(m);
+  if (spos < h->r2) {
+    const uint64_t s = (uint64_t)p * h->stride + h->r1 + spos;
+    a.slots[s] = epoch_word(h->epoch) | ((uint64_t)a.idx[i] + 1);
+    if (a.slot_vals) a.slot_vals[s] = a.val[i];
   }
 }
 
 // Sequential replay of partitions that reached the fallback scan, exactly as
 // place_index (zen/hashing.hpp:155-179) in ascending key order; the last block
-// then folds the per-partition histograms into CollisionStats and publishes
-// the push: this worker's count row into every server's inbox header, then the
-// flag (release, system scope).  The scatter kernel has completed by then, so
-// every part store -- NVLink stores into peer inboxes in rank mode -- is done.
+// folds the per-partition histograms into CollisionStats.
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
   __shared__ uint32_t list[kThreads];
@@ -278,7 +352,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
             base[slot] = ew | key;
             if (a.slot_vals) a.slot_vals[(uint64_t)p * stride + slot] = a.val[ii];
           }
-          a.meta[ii] = pack_meta(p, depth, meta_rank(a.meta[ii]), 0);
+          a.meta[ii] = pack_meta(p, depth, 0, 0);
           fstat[depth] += 1;
         }
       }
@@ -287,7 +361,6 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
     if (threadIdx.x <= k) a.fb_stats[p * (k + 1) + threadIdx.x] = fstat[threadIdx.x];
     __syncthreads();
   }
-  // finalize CollisionStats (serial, depth 1..k) over partitions
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -296,30 +369,16 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x <= k) {
+  if (threadIdx.x <= k) {  // CollisionStats: serial, depth 1..k
     uint64_t s = 0;
     for (uint32_t p = 0; p < n; ++p)
       s += (a.fallback[p] ? ((volatile uint32_t*)a.fb_stats)[p * (k + 1) + threadIdx.x]
                           : ((volatile uint32_t*)a.stats)[p * (k + 1) + threadIdx.x]);
     a.stats_out[threadIdx.x] = s;
   }
-  if (!a.push_hdr) return;
-  fence_for(a.peer);
-  const bool cap_ok = !(h->status & kErrCapacity);
-  const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
-  const uint32_t st = *(volatile uint32_t*)&h->status;
-  for (uint32_t s = threadIdx.x; s < n; s += kThreads) {
-    PushHdr* ph = a.push_hdr[s];
-    ph->nnz = h->count;
-    ph->ovf_word = ovf;
-    ph->status = st;
-    for (uint32_t q = 0; q < n; ++q) ph->counts[q] = cap_ok ? a.load[q] : 0u;
-  }
-  __syncthreads();
-  fence_for(a.peer);
-  for (uint32_t s = threadIdx.x; s < n; s += kThreads)
-    st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
 }
+
+// ----------------------------------------------------------------- utils ----
 
 __global__ void k_partition_of(const uint64_t* __restrict__ idx, uint64_t count, uint64_t pc,
                                uint32_t n, uint32_t* __restrict__ out) {
@@ -356,28 +415,45 @@ void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream) {
 }
 
 template <typename K>
-void launch_hash_rest(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
+void launch_hash_critical(const HashArgs<K>& a, uint32_t n, cudaStream_t stream) {
   const unsigned tiles = (unsigned)std::max<uint64_t>(a.tiles_cap, 1);
-  k_post<K><<<tiles, kThreads, 2 * kWarps * n * sizeof(uint32_t), stream>>>(a);
-  k_hash_scan<K><<<n, 1024, 0, stream>>>(a);
-  k_scatter<K><<<tiles, kThreads, n * sizeof(uint64_t), stream>>>(a);
+  k_part<K><<<tiles, kThreads, kWarps * n * sizeof(uint32_t), stream>>>(a);
+  k_part_scan<K><<<n, 1024, 0, stream>>>(a);
+  k_scatter<K><<<tiles, kThreads, a.dst_table ? 0 : n * sizeof(uint64_t), stream>>>(a);
+  for (int i = 0; i < 3; ++i) count_launch();
+  if (a.push_hdr) {
+    k_push_signal<K><<<1, 32, 0, stream>>>(a);
+    count_launch();
+  }
+}
+
+template <typename K>
+void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream) {
+  const unsigned tiles = (unsigned)std::max<uint64_t>(a.tiles_cap, 1);
+  if (place) {
+    k_place<K><<<grid_for(a.cap, kThreads, 148 * 16), kThreads, 0, stream>>>(a);
+    count_launch();
+  }
+  k_depth<K><<<tiles, kThreads, kWarps * n * sizeof(uint32_t), stream>>>(a);
+  k_serial_scan<K><<<n, 1024, 0, stream>>>(a);
+  k_serial_scatter<K><<<tiles, kThreads, 0, stream>>>(a);
   k_fallback<K><<<grid_for(n, 1, 148), kThreads, 0, stream>>>(a);
   for (int i = 0; i < 4; ++i) count_launch();
-  (void)k;
 }
 
 template <typename K>
 void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
   launch_hash_begin<K>(a, stream);
-  k_place<K><<<grid_for(a.cap, kThreads, 148 * 16), kThreads, 0, stream>>>(a);
-  count_launch();
-  launch_hash_rest<K>(a, n, k, stream);
+  launch_hash_critical<K>(a, n, stream);
+  launch_hash_side<K>(a, n, true, stream);
+  (void)k;
 }
 
 #define ZEN_INST(K)                                                                         \
   template void launch_hash<K>(const HashArgs<K>&, uint32_t, uint32_t, cudaStream_t);       \
   template void launch_hash_begin<K>(const HashArgs<K>&, cudaStream_t);                     \
-  template void launch_hash_rest<K>(const HashArgs<K>&, uint32_t, uint32_t, cudaStream_t);
+  template void launch_hash_critical<K>(const HashArgs<K>&, uint32_t, cudaStream_t);        \
+  template void launch_hash_side<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t);
 ZEN_INST(uint32_t)
 ZEN_INST(uint64_t)
 #undef ZEN_INST

@@ -114,7 +114,7 @@ void launch_extract_tiles_begin(const float* dense, uint64_t m, const ExtractWs<
 template <typename K>
 void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx, float* out_val,
                                   uint64_t capacity, const DevFamily& fam, HashHdr* hdr,
-                                  unsigned long long* slots, cudaStream_t stream);
+                                  unsigned long long* slots, bool place, cudaStream_t stream);
 
 void launch_partition_of(const uint64_t* idx, uint64_t count, uint64_t pc, uint32_t n,
                          uint32_t* out, cudaStream_t stream);
@@ -127,7 +127,8 @@ struct HashArgs {
   HashHdr* hdr;
   unsigned long long* slots;  // n * stride_cap words
   float* slot_vals;           // optional (layout dump)
-  uint32_t* meta;             // [cap] packed p | depth | tile ranks (zen_hash_dev.cuh)
+  uint32_t* meta;             // [cap] side path: packed p | depth | serial rank (zen_hash_dev.cuh)
+  uint32_t* pmeta;            // [cap] data path: p | (rank in tile among same-p keys) << 16
   uint32_t* tile_cnt;         // [n][tiles_cap] per-tile counts -> exclusive offsets
   uint32_t* tile_scnt;        // [n][tiles_cap] serial counts -> offsets
   uint64_t tiles_cap;         // ceil(cap / kHashTile)
@@ -153,15 +154,18 @@ struct HashArgs {
   int peer;                   // destinations include other GPUs (system-scope release)
 };
 
-// phases: begin (r1/r2, epoch, counters) | place | post..fallback.
-// launch_hash = all; the BP pipeline runs begin, then the fused
-// extraction-compaction+place, then launch_hash_rest.
+// The hash run = begin (r1/r2, epoch, counters) + a DATA path (partition
+// ranks, scan, scatter = the push, push signal) + a SIDE path (placement,
+// depths, serial slots, fallback, CollisionStats) that the BP pipeline runs on
+// a forked stream, concurrently with the exchange.  launch_hash = all, serial.
 template <typename K>
 void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream);
 template <typename K>
 void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream);
 template <typename K>
-void launch_hash_rest(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream);
+void launch_hash_critical(const HashArgs<K>& a, uint32_t n, cudaStream_t stream);
+template <typename K>
+void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream);
 
 // universe tables (HashUniverseTable, zen/codec.hpp:47-72) as bit planes
 void launch_tables_planes(uint64_t m, uint32_t n, uint64_t pc, uint32_t nplanes,

@@ -798,6 +798,17 @@ class BPSynchronizer:
         _check(_lib().zen_bp_stage_times(self.h, ms.ctypes.data, C.byref(k)))
         return ms, k.value
 
+    def debug_part(self, what: int, server: int, worker: int, cap: int):
+        """Diagnostics: (u32 idx, f32 val) of a local worker's keys (what=0) or
+        of the part `worker` pushed to local `server` (what=1)."""
+        oi = np.empty(max(cap, 1), np.uint32)
+        ov = np.empty(max(cap, 1), np.float32)
+        c = C.c_uint64()
+        _check(_lib().zen_bp_debug_part(self.h, what, server, worker, oi.ctypes.data,
+                                        ov.ctypes.data, cap, C.byref(c)))
+        k = min(c.value, cap)
+        return oi[:k], ov[:k], c.value
+
     def use_graph(self, on=True):
         """Replay dense syncs from a captured CUDA graph (needs a non-default stream)."""
         _check(_lib().zen_bp_use_graph(self.h, int(on)))
