@@ -1,0 +1,84 @@
+"""One rank of a multi-GPU Balanced-Parallelism parity run (launched by
+torchrun from tests/test_multi_gpu.py or by hand:
+
+  torchrun --standalone --nproc-per-node 2 tests/mgpu_worker.py [rows] [width] [density]
+
+Each rank is worker+server `rank`; push/pull are NVLink stores into peer
+inboxes mapped with CUDA IPC.  Every rank checks its result against the CPU
+oracle (bit-exact indices, values and TrafficReport ledger) -- test infra.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+
+def main():
+    rows = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
+    width = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+    density = float(sys.argv[3]) if len(sys.argv) > 3 else 0.01
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import bench
+    import paper_2309_13254_b200 as zen
+    from oracle import COracle
+
+    per = int(np.ceil(density * rows))
+    m = rows * width
+    live = bench.live_rows(rows, per, world, 0.5, 1.05, 3)
+    dense = [bench.dense_gradient(rows, width, live[w], 3 + w) for w in range(world)]
+    mine = torch.from_numpy(dense[rank]).cuda()
+    bp = zen.BPSynchronizer(world, m, max_nnz=per * width + 1024, params=zen.HashParams(seed=5),
+                            rank=rank)
+    bp.connect_process_group()
+    co = COracle()
+    want = co.bp_sync(m, [co.to_sparse(d) for d in dense], seed=5)
+    ok = True
+    side = torch.cuda.Stream()
+    for it in range(4):  # eager, then CUDA-graph replays on a side stream
+        if it < 2:
+            bp.sync_dense([mine])
+        else:
+            with torch.cuda.stream(side):
+                bp.sync_dense([mine])
+        bp.wait()
+        oi, ov = bp.result()
+        gi = oi.cpu().numpy().view(np.uint64)
+        gv = ov.cpu().numpy()
+        good = np.array_equal(gi, want.idx) and np.array_equal(gv.view(np.uint32),
+                                                               want.val.view(np.uint32))
+        led, counts, agg = bp.ledger()
+        good = good and np.array_equal(led, want.ledger) and np.array_equal(counts, want.counts)
+        bal = bp.balance()
+        good = good and bal is not None and bal.push_imbalance == want.balance[0] \
+            and bal.pull_imbalance == want.balance[1]
+        if not good:
+            print(f"RANK {rank} iter {it} MISMATCH: {gi.size} vs {want.idx.size}", flush=True)
+            ok = False
+    st = bp.collision_stats(rank)
+    r1, r2 = co.bp_sizes(2.0, 0.1, int(np.count_nonzero(dense[rank])), world)
+    wi, wv = co.to_sparse(dense[rank])
+    ref = co.hierarchical_hash(m, wi, wv, co.family(5, world, 3, worker=rank), r1, r2)
+    if st.serial_writes != ref.serial_writes or st.placed_at_depth != ref.placed_at_depth:
+        print(f"RANK {rank} collision stats mismatch", flush=True)
+        ok = False
+    flag = torch.tensor([0 if ok else 1], device="cuda")
+    dist.all_reduce(flag)
+    if rank == 0:
+        print("MGPU " + ("OK" if int(flag.item()) == 0 else "FAIL") + f" n={world} M={m}", flush=True)
+    dist.barrier()
+    del bp
+    dist.destroy_process_group()
+    sys.exit(0 if int(flag.item()) == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
