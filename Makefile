@@ -15,9 +15,17 @@ CU := $(wildcard $(SRC)/*.cu)
 CUOBJ := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU))
 HDRS := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/zen_b200.h
 
-all: lib oracle
+all: lib oracle compat_test
 
 lib: $(LIB)
+
+# C++ drop-in test (include/zen_b200/compat.hpp), runs on a GPU box
+COMPAT_TEST := build/compat_test
+compat_test: $(COMPAT_TEST)
+$(COMPAT_TEST): tests/cpp/compat_test.cpp include/zen_b200/compat.hpp include/zen_b200.h $(LIB)
+	@mkdir -p build
+	g++ -O2 -std=c++17 -Wall -Wextra -Iinclude -I$(CUDA_HOME)/include -o $@ $< \
+	    -L$(dir $(LIB)) -lzen_b200 -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))' -L$(CUDA_HOME)/lib64 -lcudart
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -38,4 +46,4 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle clean compat_test

@@ -38,7 +38,7 @@ extern "C" {
 #define ZEN_MAX_WORKERS 16u      /* n for the fused BP pipeline and the codec */
 #define ZEN_IPC_HANDLE_BYTES 64u /* cudaIpcMemHandle_t */
 #define ZEN_BP_LOCAL 0xFFFFFFFFu /* zen_bp_create rank: emulate all n workers on one GPU */
-#define ZEN_STAGES 4u            /* extract | hash+push | aggregate+encode+pull | decode */
+#define ZEN_STAGES 4u /* extract kernel | hash+push | aggregate+encode+pull | decode (incl. pull wait) */
 
 /* zen/errors.hpp:10-84 plus the device-side failure classes */
 typedef enum zen_status {

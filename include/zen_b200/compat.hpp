@@ -1,0 +1,619 @@
+// zen_b200/compat.hpp -- header-only C++ drop-in for the reference's
+// Balanced-Parallelism operator API (/root/reference/proj/include/zen/*.hpp),
+// backed by the sm_100a kernels behind the C-ABI (include/zen_b200.h).
+//
+// Same names, argument meaning and exception types as the reference, in
+// namespace zen_b200 (a reference user switches with `namespace zen = zen_b200;`
+// for the operators below):
+//
+//   reference                                   here
+//   zen::Error & subclasses (errors.hpp)        zen_b200::Error & subclasses
+//   zen::SparseTensor / DenseTensor (tensor.hpp) zen_b200::SparseTensor / DenseTensor
+//   zen::to_sparse (tensor.hpp:94)              zen_b200::to_sparse
+//   zen::HashFamily (hashing.hpp:46)            zen_b200::HashFamily
+//   zen::partition_of (hashing.hpp:85)          zen_b200::partition_of
+//   zen::hierarchical_hash (hashing.hpp:251)    zen_b200::hierarchical_hash
+//   zen::collision_stats (hashing.hpp:259)      zen_b200::collision_stats
+//   zen::imbalance_push/pull (hashing.hpp:296)  zen_b200::imbalance_push/pull
+//   zen::HashUniverseTable (codec.hpp:47)       zen_b200::HashUniverseTable
+//   zen::encode/decode, HashBitmap (codec.hpp)  zen_b200::encode/decode
+//   zen::SimNet / TrafficReport (simnet.hpp)    zen_b200::SimNet / TrafficReport
+//   zen::HashParams / SyncOutcome (schemes.hpp) zen_b200::HashParams / SyncOutcome
+//   zen::run_balanced_parallelism (schemes.hpp:341)  zen_b200::run_balanced_parallelism
+//   zen::bp_universe_table (schemes.hpp:332)    zen_b200::bp_universe_table
+//   zen::run_bp_with_retry (experiment.hpp:128) zen_b200::run_bp_with_retry
+//
+// Host containers stay std::vector (value semantics, as in the reference); the
+// device copies are made per call.  For a device-resident, allocation-free
+// sync use the zen_bp_* C-ABI directly (bench.py does).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "zen_b200.h"
+
+namespace zen_b200 {
+
+// ---- errors: zen/errors.hpp:10-84 ------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& w) : std::runtime_error(w) {}
+};
+class EmptyTensor : public Error {
+ public:
+  explicit EmptyTensor(const std::string& w = "operation requires a non-empty tensor") : Error(w) {}
+};
+class UniverseMismatch : public Error {
+ public:
+  explicit UniverseMismatch(const std::string& w = "tensors have different universe sizes")
+      : Error(w) {}
+};
+class SerialOverflow : public Error {
+ public:
+  explicit SerialOverflow(uint32_t partition, const std::string& w = "")
+      : Error(w.empty() ? "hash partition " + std::to_string(partition) +
+                              " exceeded its slot capacity (r2 too small for this workload)"
+                        : w),
+        partition_(partition) {}
+  uint32_t partition() const { return partition_; }
+
+ private:
+  uint32_t partition_;
+};
+class IndexOutsideUniverse : public Error {
+ public:
+  explicit IndexOutsideUniverse(const std::string& w) : Error(w) {}
+};
+class MalformedPayload : public Error {
+ public:
+  explicit MalformedPayload(const std::string& w) : Error(w) {}
+};
+class SelfSend : public Error {
+ public:
+  explicit SelfSend(const std::string& w = "a node cannot send a message to itself") : Error(w) {}
+};
+class UnbalancedLedger : public Error {
+ public:
+  explicit UnbalancedLedger(const std::string& w = "sent and received byte totals disagree")
+      : Error(w) {}
+};
+class DeviceError : public Error {  // no CPU fallback exists
+ public:
+  explicit DeviceError(const std::string& w) : Error(w) {}
+};
+
+namespace detail {
+inline void check(zen_status s) {
+  if (s == ZEN_OK) return;
+  const std::string msg = zen_last_error_message();
+  switch (s) {
+    case ZEN_E_SERIAL_OVERFLOW: throw SerialOverflow(uint32_t(zen_last_error_partition()), msg);
+    case ZEN_E_INDEX_OUTSIDE_UNIVERSE: throw IndexOutsideUniverse(msg);
+    case ZEN_E_MALFORMED: throw MalformedPayload(msg);
+    case ZEN_E_EMPTY: throw EmptyTensor(msg);
+    case ZEN_E_UNIVERSE_MISMATCH: throw UniverseMismatch(msg);
+    case ZEN_E_CUDA:
+    case ZEN_E_PEER:
+    case ZEN_E_OOM:
+    case ZEN_E_TIMEOUT: throw DeviceError(msg);
+    default: throw Error(msg);
+  }
+}
+
+// device buffer
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  explicit DBuf(size_t count) : n(count) {
+    if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess)
+      throw DeviceError("cudaMalloc failed");
+  }
+  DBuf(const std::vector<T>& h) : DBuf(h.size()) {
+    if (!h.empty()) cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+  }
+  ~DBuf() { cudaFree(p); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  std::vector<T> host(size_t count) const {
+    std::vector<T> h(count);
+    if (count) cudaMemcpy(h.data(), p, count * sizeof(T), cudaMemcpyDeviceToHost);
+    return h;
+  }
+};
+
+// one context per process (device 0 unless ZEN_B200_DEVICE says otherwise)
+inline zen_ctx* ctx() {
+  static std::unique_ptr<zen_ctx, void (*)(zen_ctx*)> c = [] {
+    int dev = 0;
+    if (const char* e = std::getenv("ZEN_B200_DEVICE")) dev = std::atoi(e);
+    cudaSetDevice(dev);
+    zen_ctx* h = nullptr;
+    check(zen_ctx_create(dev, &h));
+    // the legacy default stream: ordered with the blocking cudaMemcpy calls
+    // this header uses for its per-call host<->device copies
+    check(zen_ctx_set_stream(h, nullptr));
+    return std::unique_ptr<zen_ctx, void (*)(zen_ctx*)>(h, zen_ctx_destroy);
+  }();
+  return c.get();
+}
+}  // namespace detail
+
+// ---- data model: zen/tensor.hpp:19-91 ---------------------------------------
+struct DenseTensor {
+  std::vector<float> values;
+  DenseTensor() = default;
+  explicit DenseTensor(std::vector<float> v) : values(std::move(v)) {
+    if (values.empty()) throw Error("dense tensor must have at least one element");
+  }
+  uint64_t size() const { return values.size(); }
+};
+
+class SparseTensor {
+ public:
+  SparseTensor() : universe_(1) {}
+  SparseTensor(uint64_t universe, std::vector<uint64_t> indices, std::vector<float> values)
+      : universe_(universe), indices_(std::move(indices)), values_(std::move(values)) {
+    if (universe_ == 0) throw Error("sparse tensor universe must be at least 1");
+    if (indices_.size() != values_.size()) throw Error("sparse tensor index/value lengths differ");
+    if (!std::is_sorted(indices_.begin(), indices_.end())) {
+      std::vector<size_t> o(indices_.size());
+      for (size_t i = 0; i < o.size(); ++i) o[i] = i;
+      std::sort(o.begin(), o.end(), [this](size_t a, size_t b) { return indices_[a] < indices_[b]; });
+      std::vector<uint64_t> ii(o.size());
+      std::vector<float> vv(o.size());
+      for (size_t i = 0; i < o.size(); ++i) {
+        ii[i] = indices_[o[i]];
+        vv[i] = values_[o[i]];
+      }
+      indices_.swap(ii);
+      values_.swap(vv);
+    }
+    for (size_t i = 0; i < indices_.size(); ++i) {
+      if (indices_[i] >= universe_) throw Error("sparse tensor index outside [0, M)");
+      if (i > 0 && indices_[i] == indices_[i - 1]) throw Error("duplicate index in sparse tensor");
+    }
+  }
+  static SparseTensor from_pairs(uint64_t universe, std::vector<std::pair<uint64_t, float>> pairs) {
+    std::sort(pairs.begin(), pairs.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    std::vector<uint64_t> i(pairs.size());
+    std::vector<float> v(pairs.size());
+    for (size_t k = 0; k < pairs.size(); ++k) {
+      i[k] = pairs[k].first;
+      v[k] = pairs[k].second;
+    }
+    return SparseTensor(universe, std::move(i), std::move(v));
+  }
+  uint64_t universe() const { return universe_; }
+  uint64_t nnz() const { return indices_.size(); }
+  bool empty() const { return indices_.empty(); }
+  const std::vector<uint64_t>& indices() const { return indices_; }
+  const std::vector<float>& values() const { return values_; }
+  friend bool operator==(const SparseTensor& a, const SparseTensor& b) {
+    return a.universe_ == b.universe_ && a.indices_ == b.indices_ &&
+           a.values_.size() == b.values_.size() &&
+           std::memcmp(a.values_.data(), b.values_.data(), a.values_.size() * 4) == 0;
+  }
+  friend bool operator!=(const SparseTensor& a, const SparseTensor& b) { return !(a == b); }
+
+ private:
+  uint64_t universe_;
+  std::vector<uint64_t> indices_;
+  std::vector<float> values_;
+};
+
+// zen::to_sparse (tensor.hpp:94-104), on the GPU
+inline SparseTensor to_sparse(const DenseTensor& dense) {
+  const uint64_t m = dense.size();
+  if (m == 0) throw Error("dense tensor must have at least one element");
+  detail::DBuf<float> d(dense.values);
+  detail::DBuf<uint64_t> oi(m);
+  detail::DBuf<float> ov(m);
+  uint64_t nnz = 0;
+  detail::check(zen_to_sparse(detail::ctx(), d.p, m, oi.p, ov.p, m, &nnz));
+  return SparseTensor(m, oi.host(nnz), ov.host(nnz));
+}
+
+// ---- hashing: zen/hashing.hpp -----------------------------------------------
+struct PartitionedSparseTensor {
+  std::vector<SparseTensor> parts;
+  uint64_t total_nnz() const {
+    uint64_t s = 0;
+    for (auto& p : parts) s += p.nnz();
+    return s;
+  }
+};
+
+struct CollisionStats {
+  uint64_t serial_writes = 0;
+  std::vector<uint64_t> placed_at_depth;
+  uint64_t total() const {
+    uint64_t s = serial_writes;
+    for (auto c : placed_at_depth) s += c;
+    return s;
+  }
+};
+
+struct HashFamily {
+  uint64_t partition_seed = 0;
+  std::vector<uint64_t> slot_seeds;
+  uint32_t partitions = 1;
+
+  static HashFamily make(uint64_t seed, uint32_t n, uint32_t k) {
+    zen_hash_family f;
+    detail::check(zen_hash_family_make(seed, n, k, &f));
+    return from(f);
+  }
+  static HashFamily make_worker(uint64_t shared, uint32_t worker, uint32_t n, uint32_t k) {
+    zen_hash_family f;
+    detail::check(zen_hash_family_make_worker(shared, worker, n, k, &f));
+    return from(f);
+  }
+  uint32_t depth() const { return uint32_t(slot_seeds.size()); }
+  zen_hash_family c() const {
+    zen_hash_family f{};
+    f.partition_seed = partition_seed;
+    for (size_t i = 0; i < slot_seeds.size(); ++i) f.slot_seeds[i] = slot_seeds[i];
+    f.partitions = partitions;
+    f.k = depth();
+    return f;
+  }
+
+ private:
+  static HashFamily from(const zen_hash_family& f) {
+    HashFamily h;
+    h.partition_seed = f.partition_seed;
+    h.slot_seeds.assign(f.slot_seeds, f.slot_seeds + f.k);
+    h.partitions = f.partitions;
+    return h;
+  }
+};
+
+// zen::partition_of (hashing.hpp:85-88), batched on the GPU
+inline std::vector<uint32_t> partition_of(const std::vector<uint64_t>& idx, uint64_t pseed,
+                                          uint32_t n) {
+  detail::DBuf<uint64_t> d(idx);
+  detail::DBuf<uint32_t> o(idx.size());
+  detail::check(zen_partition_of(detail::ctx(), d.p, idx.size(), pseed, n, o.p));
+  return o.host(idx.size());
+}
+
+namespace detail {
+inline std::pair<PartitionedSparseTensor, CollisionStats> run_hierarchical_hash(
+    const SparseTensor& t, uint32_t n, const HashFamily& family, uint64_t r1, uint64_t r2,
+    uint32_t lanes) {
+  if (family.partitions != n) throw Error("hash family partition count mismatch");
+  if (lanes < 1) throw Error("lane count must be at least 1");
+  const uint64_t z = t.nnz();
+  DBuf<uint64_t> di(t.indices());
+  DBuf<float> dv(t.values());
+  DBuf<uint64_t> oi(z);
+  DBuf<float> ov(z);
+  std::vector<uint64_t> pc(n);
+  zen_collision_stats st;
+  const zen_hash_family f = family.c();
+  check(zen_hierarchical_hash(ctx(), di.p, dv.p, z, t.universe(), &f, r1, r2, oi.p, ov.p,
+                              pc.data(), nullptr, nullptr, nullptr, &st));
+  auto hi = oi.host(z);
+  auto hv = ov.host(z);
+  PartitionedSparseTensor out;
+  uint64_t off = 0;
+  for (uint32_t p = 0; p < n; ++p) {
+    out.parts.emplace_back(t.universe(),
+                           std::vector<uint64_t>(hi.begin() + off, hi.begin() + off + pc[p]),
+                           std::vector<float>(hv.begin() + off, hv.begin() + off + pc[p]));
+    off += pc[p];
+  }
+  CollisionStats cs;
+  cs.serial_writes = st.serial_writes;
+  cs.placed_at_depth.assign(st.placed_at_depth, st.placed_at_depth + st.k);
+  return {std::move(out), std::move(cs)};
+}
+}  // namespace detail
+
+inline PartitionedSparseTensor hierarchical_hash(const SparseTensor& t, uint32_t n,
+                                                 const HashFamily& family, uint64_t r1,
+                                                 uint64_t r2, uint32_t lanes = 1) {
+  return detail::run_hierarchical_hash(t, n, family, r1, r2, lanes).first;
+}
+
+inline CollisionStats collision_stats(const SparseTensor& t, uint32_t n, const HashFamily& family,
+                                      uint64_t r1, uint64_t r2) {
+  return detail::run_hierarchical_hash(t, n, family, r1, r2, 1).second;
+}
+
+inline double imbalance_push(const std::vector<PartitionedSparseTensor>& per_worker) {
+  if (per_worker.empty()) throw Error("imbalance requires at least one worker");
+  double worst = 0.0;
+  for (const auto& w : per_worker) {
+    const uint64_t total = w.total_nnz();
+    if (total == 0) throw EmptyTensor("imbalance undefined for a worker with no gradients");
+    const double n = double(w.parts.size());
+    for (const auto& p : w.parts) worst = std::max(worst, n * double(p.nnz()) / double(total));
+  }
+  return worst;
+}
+
+inline double imbalance_pull(const std::vector<uint64_t>& loads, uint64_t union_size) {
+  if (loads.empty()) throw Error("imbalance requires at least one server");
+  if (union_size == 0) throw EmptyTensor("imbalance undefined for an empty union");
+  const double n = double(loads.size());
+  double worst = 0.0;
+  for (auto l : loads) worst = std::max(worst, n * double(l) / double(union_size));
+  return worst;
+}
+
+// ---- codec: zen/codec.hpp ---------------------------------------------------
+enum class WireKind : uint8_t { Coo = 1, Bitmap = 2, TensorBlock = 3, HashBitmap = 4 };
+struct WireFormat {
+  WireKind kind = WireKind::HashBitmap;
+  static WireFormat hash_bitmap() { return {WireKind::HashBitmap}; }
+};
+
+struct EncodedMessage {
+  WireFormat format;
+  uint64_t universe_size = 0;
+  uint64_t count = 0;
+  uint64_t index_bits = 0;
+  uint64_t value_bits = 0;
+  std::vector<uint8_t> payload;
+  uint64_t payload_bits() const { return index_bits + value_bits; }
+};
+
+class HashUniverseTable;
+struct HashUniverse {
+  uint32_t server_id = 0;
+  uint64_t universe_size = 0;
+  const HashUniverseTable* table = nullptr;
+  std::vector<uint64_t> indices_copy() const;
+};
+
+class HashUniverseTable {
+ public:
+  HashUniverseTable(uint64_t universe_size, uint32_t servers, uint64_t partition_seed)
+      : m_(universe_size), n_(servers), pseed_(partition_seed) {
+    if (servers == 0) throw Error("hash universe table needs at least one server");
+    zen_universe* u = nullptr;
+    detail::check(zen_universe_create(detail::ctx(), m_, n_, pseed_, &u));
+    u_.reset(u);
+    for (uint32_t s = 0; s < n_; ++s) us_.push_back(HashUniverse{s, m_, this});
+  }
+  uint64_t universe_size() const { return m_; }
+  uint32_t servers() const { return n_; }
+  uint64_t partition_seed() const { return pseed_; }
+  const HashUniverse& universe(uint32_t s) const { return us_.at(s); }
+  uint64_t size(uint32_t s) const { return zen_universe_size(u_.get(), s); }
+  zen_universe* handle() const { return u_.get(); }
+
+ private:
+  struct Del {
+    void operator()(zen_universe* u) const { zen_universe_destroy(u); }
+  };
+  uint64_t m_;
+  uint32_t n_;
+  uint64_t pseed_;
+  std::unique_ptr<zen_universe, Del> u_;
+  std::vector<HashUniverse> us_;
+};
+
+inline std::vector<uint64_t> HashUniverse::indices_copy() const {
+  const uint64_t sz = table->size(server_id);
+  detail::DBuf<uint64_t> d(sz);
+  detail::check(zen_universe_indices(table->handle(), server_id, d.p));
+  return d.host(sz);
+}
+
+inline HashUniverseTable bp_universe_table(uint64_t universe_size, uint32_t servers,
+                                           uint64_t seed) {
+  return HashUniverseTable(universe_size, servers, zen_derive_seed(seed, 0));
+}
+
+// encode(t, WireFormat::hash_bitmap(), &universe) -- codec.hpp:266-277
+inline EncodedMessage encode(const SparseTensor& t, const WireFormat& fmt,
+                             const HashUniverse* universe) {
+  if (fmt.kind != WireKind::HashBitmap) throw Error("only the HashBitmap format is on the path");
+  if (universe == nullptr) throw Error("hash bitmap requires a hash universe");
+  const auto* tab = universe->table;
+  const uint32_t s = universe->server_id;
+  const uint64_t bytes = (tab->size(s) + 7) / 8 + 4 * t.nnz();
+  detail::DBuf<uint64_t> di(t.indices());
+  detail::DBuf<float> dv(t.values());
+  detail::DBuf<uint8_t> dp(bytes);
+  uint64_t bits = 0, plen = 0;
+  detail::check(zen_hash_bitmap_encode(tab->handle(), s, di.p, dv.p, t.nnz(), dp.p, &bits, &plen));
+  EncodedMessage msg;
+  msg.format = fmt;
+  msg.universe_size = t.universe();
+  msg.count = t.nnz();
+  msg.index_bits = bits;
+  msg.value_bits = 32 * t.nnz();
+  msg.payload = dp.host(plen);
+  return msg;
+}
+
+// decode(msg, &universe) -- codec.hpp:333-347
+inline SparseTensor decode(const EncodedMessage& msg, const HashUniverse* universe) {
+  if (universe == nullptr) throw Error("hash bitmap requires the encoding universe");
+  detail::DBuf<uint8_t> dp(msg.payload);
+  detail::DBuf<uint64_t> oi(msg.count);
+  detail::DBuf<float> ov(msg.count);
+  detail::check(zen_hash_bitmap_decode(universe->table->handle(), universe->server_id, dp.p,
+                                       msg.payload.size(), msg.count, oi.p, ov.p));
+  return SparseTensor(msg.universe_size, oi.host(msg.count), ov.host(msg.count));
+}
+
+// ---- transport ledger: zen/simnet.hpp ---------------------------------------
+struct StageRecord {
+  std::vector<uint64_t> sent_bits, recv_bits, recv_index_bits, recv_value_bits;
+  double stage_time = 0.0;
+  explicit StageRecord(uint32_t n)
+      : sent_bits(n, 0), recv_bits(n, 0), recv_index_bits(n, 0), recv_value_bits(n, 0) {}
+};
+
+struct TrafficReport {
+  uint32_t nodes = 0;
+  double bandwidth = 0.0;
+  std::vector<StageRecord> stages;
+  uint64_t total_sent_bits = 0, total_recv_bits = 0, total_index_bits = 0, total_value_bits = 0;
+  double simulated_time = 0.0;
+};
+
+// The reference's accounting network.  On B200 the bytes really move over
+// NVLink; this keeps the deterministic bit ledger (stage time = max recv / b).
+class SimNet {
+ public:
+  SimNet(uint32_t nodes, double bandwidth, double latency = 0.0)
+      : n_(nodes), b_(bandwidth), lat_(latency) {
+    if (nodes == 0) throw Error("network needs at least one node");
+    if (bandwidth <= 0.0) throw Error("bandwidth must be positive");
+  }
+  uint32_t nodes() const { return n_; }
+  double bandwidth() const { return b_; }
+  // ledger[2][4][n] as produced by zen_bp_traffic
+  void record(const std::vector<uint64_t>& ledger, uint64_t messages) {
+    if (final_) throw Error("cannot send after finalize");
+    for (uint32_t st = 0; st < 2; ++st) {
+      while (stages_.size() <= st) stages_.emplace_back(n_);
+      for (uint32_t v = 0; v < n_; ++v) {
+        stages_[st].sent_bits[v] += ledger[(st * 4 + 0) * n_ + v];
+        stages_[st].recv_bits[v] += ledger[(st * 4 + 1) * n_ + v];
+        stages_[st].recv_index_bits[v] += ledger[(st * 4 + 2) * n_ + v];
+        stages_[st].recv_value_bits[v] += ledger[(st * 4 + 3) * n_ + v];
+      }
+    }
+    lat_charges_ += lat_ * double(messages);
+  }
+  TrafficReport finalize() {  // simnet.hpp:87-111
+    if (final_) throw Error("network already finalized");
+    final_ = true;
+    TrafficReport r;
+    r.nodes = n_;
+    r.bandwidth = b_;
+    r.stages = std::move(stages_);
+    for (auto& s : r.stages) {
+      uint64_t sent = 0, recv = 0, mx = 0;
+      for (uint32_t v = 0; v < n_; ++v) {
+        sent += s.sent_bits[v];
+        recv += s.recv_bits[v];
+        mx = std::max(mx, s.recv_bits[v]);
+        r.total_index_bits += s.recv_index_bits[v];
+        r.total_value_bits += s.recv_value_bits[v];
+      }
+      if (sent != recv) throw UnbalancedLedger();
+      s.stage_time = double(mx) / b_;
+      r.total_sent_bits += sent;
+      r.total_recv_bits += recv;
+      r.simulated_time += s.stage_time;
+    }
+    r.simulated_time += lat_charges_;
+    return r;
+  }
+
+ private:
+  uint32_t n_;
+  double b_, lat_, lat_charges_ = 0.0;
+  bool final_ = false;
+  std::vector<StageRecord> stages_;
+};
+
+// ---- Balanced Parallelism: zen/schemes.hpp:330-417 --------------------------
+struct HashParams {
+  uint32_t rehash_depth = 3;
+  double r1_multiplier = 2.0;
+  double r2_ratio = 0.1;
+  uint32_t lanes = 1;
+  uint64_t seed = 1;
+};
+
+struct BalanceDetails {
+  double push_imbalance = 1.0;
+  double pull_imbalance = 1.0;
+};
+
+struct SyncOutcome {
+  std::vector<SparseTensor> results;
+  TrafficReport traffic;
+  std::optional<BalanceDetails> balance;
+};
+
+inline SyncOutcome run_balanced_parallelism(const std::vector<SparseTensor>& inputs, SimNet& net,
+                                            const HashParams& params = {},
+                                            const HashUniverseTable* table = nullptr) {
+  if (inputs.size() < 2) throw Error("synchronization needs at least two nodes");
+  if (inputs.size() != net.nodes()) throw Error("input count must match the network size");
+  for (const auto& t : inputs)
+    if (t.universe() != inputs.front().universe()) throw UniverseMismatch();
+  const uint32_t n = uint32_t(inputs.size());
+  const uint64_t m = inputs.front().universe();
+  if (table && (table->universe_size() != m || table->servers() != n ||
+                table->partition_seed() != zen_derive_seed(params.seed, 0)))
+    throw Error("hash universe table does not match this run");
+  uint64_t cap = 1;
+  for (const auto& t : inputs) cap = std::max<uint64_t>(cap, t.nnz());
+  zen_hash_params hp{params.rehash_depth, params.r1_multiplier, params.r2_ratio, params.lanes,
+                     params.seed};
+  zen_bp* bp = nullptr;
+  detail::check(zen_bp_create(detail::ctx(), n, ZEN_BP_LOCAL, m, cap, &hp, &bp));
+  std::unique_ptr<zen_bp, void (*)(zen_bp*)> guard(bp, zen_bp_destroy);
+  std::vector<std::unique_ptr<detail::DBuf<uint64_t>>> di;
+  std::vector<std::unique_ptr<detail::DBuf<float>>> dv;
+  std::vector<const uint64_t*> ip;
+  std::vector<const float*> vp;
+  std::vector<uint64_t> nnz;
+  for (const auto& t : inputs) {
+    di.emplace_back(new detail::DBuf<uint64_t>(t.indices()));
+    dv.emplace_back(new detail::DBuf<float>(t.values()));
+    ip.push_back(di.back()->p);
+    vp.push_back(dv.back()->p);
+    nnz.push_back(t.nnz());
+  }
+  detail::check(zen_bp_sync_sparse(bp, ip.data(), vp.data(), nnz.data()));
+  detail::check(zen_bp_wait(bp));
+  uint64_t count = 0;
+  detail::check(zen_bp_result(bp, nullptr, nullptr, &count));
+  detail::DBuf<uint64_t> oi(count);
+  detail::DBuf<float> ov(count);
+  detail::check(zen_bp_copy_result(bp, oi.p, ov.p, count, &count));
+  SparseTensor result(m, oi.host(count), ov.host(count));
+  std::vector<uint64_t> ledger(8 * n), counts(size_t(n) * n), agg(n);
+  detail::check(zen_bp_traffic(bp, ledger.data(), counts.data(), agg.data()));
+  uint64_t msgs = uint64_t(n) * (n - 1);  // pull: always sent (schemes.hpp:387-388)
+  for (uint32_t w = 0; w < n; ++w)
+    for (uint32_t s = 0; s < n; ++s) msgs += (s != w && counts[size_t(w) * n + s]) ? 1 : 0;
+  net.record(ledger, msgs);
+  SyncOutcome out;
+  out.results.assign(n, result);
+  out.traffic = net.finalize();
+  double push = 0, pull = 0;
+  int valid = 0;
+  detail::check(zen_bp_balance(bp, &push, &pull, &valid));
+  if (valid) out.balance = BalanceDetails{push, pull};
+  return out;
+}
+
+// zen::run_bp_with_retry (experiment.hpp:128-140)
+inline SyncOutcome run_bp_with_retry(const std::vector<SparseTensor>& inputs, double bandwidth,
+                                     HashParams params, const HashUniverseTable* table = nullptr,
+                                     int max_retries = 4) {
+  for (int attempt = 0;; ++attempt) {
+    SimNet net(uint32_t(inputs.size()), bandwidth);
+    try {
+      return run_balanced_parallelism(inputs, net, params, table);
+    } catch (const SerialOverflow&) {
+      if (attempt >= max_retries) throw;
+      params.r2_ratio *= 2.0;
+    }
+  }
+}
+
+}  // namespace zen_b200

@@ -1213,13 +1213,12 @@ void record(zen_bp* bp, int stage) {
 zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cudaEvent_t* ev) {
   cudaStream_t st = bp->ctx->stream;
   if (ev) CK(cudaEventRecordWithFlags(ev[0], st, cudaEventRecordExternal));
-  if (from_dense) {
-    for (size_t i = 0; i < bp->workers.size(); ++i) {
-      Worker& w = bp->workers[i];
-      launch_extract_tiles_begin<uint32_t>(dense[i], bp->m, w.ex, w.a, bp->cap, st);
-    }
-  }
+  if (from_dense)  // stage 0: the HBM-bound extraction kernel alone
+    for (size_t i = 0; i < bp->workers.size(); ++i)
+      launch_extract_tiles<uint32_t>(dense[i], bp->m, bp->workers[i].ex, st);
   if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
+  if (from_dense)
+    for (auto& w : bp->workers) launch_extract_scan_begin<uint32_t>(bp->m, w.ex, w.a, bp->cap, st);
   // data path on `st`; the hash-memory side path of each worker forks onto
   // bp->side and joins at the end of the sync
   for (auto& w : bp->workers) {

@@ -115,12 +115,18 @@ __global__ void __launch_bounds__(1024) k_extract_scan(uint32_t* __restrict__ ti
   for (uint32_t b = 0; b < ntiles; b += blockDim.x * E) {
     const uint32_t t0 = b + threadIdx.x * E;
     uint32_t v[E];
+    if (t0 + E <= ntiles) {  // tile_cnt is 256-B aligned, t0 % 8 == 0
+      const uint4 a0 = reinterpret_cast<const uint4*>(tile_cnt + t0)[0];
+      const uint4 a1 = reinterpret_cast<const uint4*>(tile_cnt + t0)[1];
+      v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
+      v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = (t0 + e < ntiles) ? tile_cnt[t0 + e] : 0u;
+    }
     uint64_t local = 0;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      v[e] = (t0 + e < ntiles) ? tile_cnt[t0 + e] : 0u;
-      local += v[e];
-    }
+    for (int e = 0; e < E; ++e) local += v[e];
     uint64_t tot;
     uint64_t ex = carry + block_exclusive_sum(local, sscan, &tot);
 #pragma unroll
@@ -198,13 +204,19 @@ void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* o
 }
 
 template <typename K>
-void launch_extract_tiles_begin(const float* dense, uint64_t m, const ExtractWs<K>& ws,
-                                const HashArgs<K>& ha, uint64_t capacity, cudaStream_t stream) {
+void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws,
+                          cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
   k_extract_tiles<K><<<ntiles, kThreads, 0, stream>>>(dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
+  count_launch();
+}
+
+template <typename K>
+void launch_extract_scan_begin(uint64_t m, const ExtractWs<K>& ws, const HashArgs<K>& ha,
+                               uint64_t capacity, cudaStream_t stream) {
+  const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
   k_extract_scan<K, true><<<1, 1024, 0, stream>>>(ws.tile_cnt, ntiles, &ha.hdr->count, capacity,
                                                   &ha.hdr->status, ws.tile_base, ha);
-  count_launch();
   count_launch();
 }
 
@@ -228,8 +240,10 @@ void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx
 #define ZEN_INST(K)                                                                              \
   template void launch_extract<K>(const float*, uint64_t, const ExtractWs<K>&, K*, float*,      \
                                   uint64_t*, uint64_t, uint32_t*, cudaStream_t);                 \
-  template void launch_extract_tiles_begin<K>(const float*, uint64_t, const ExtractWs<K>&,     \
-                                              const HashArgs<K>&, uint64_t, cudaStream_t);       \
+  template void launch_extract_tiles<K>(const float*, uint64_t, const ExtractWs<K>&,           \
+                                        cudaStream_t);                                           \
+  template void launch_extract_scan_begin<K>(uint64_t, const ExtractWs<K>&, const HashArgs<K>&, \
+                                             uint64_t, cudaStream_t);                            \
   template void launch_extract_compact_place<K>(uint64_t, const ExtractWs<K>&, K*, float*,      \
                                                 uint64_t, const DevFamily&, HashHdr*,           \
                                                 unsigned long long*, bool, cudaStream_t);

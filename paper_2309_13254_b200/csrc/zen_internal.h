@@ -109,8 +109,11 @@ void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* o
 template <typename K>
 struct HashArgs;
 template <typename K>
-void launch_extract_tiles_begin(const float* dense, uint64_t m, const ExtractWs<K>& ws,
-                                const HashArgs<K>& ha, uint64_t capacity, cudaStream_t stream);
+void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws,
+                          cudaStream_t stream);
+template <typename K>
+void launch_extract_scan_begin(uint64_t m, const ExtractWs<K>& ws, const HashArgs<K>& ha,
+                               uint64_t capacity, cudaStream_t stream);
 template <typename K>
 void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx, float* out_val,
                                   uint64_t capacity, const DevFamily& fam, HashHdr* hdr,

@@ -59,3 +59,16 @@ def test_no_cpu_fallback_without_gpu():
     rc = lib.zen_ctx_create(0, ctypes.byref(h))
     assert rc == 7  # ZEN_E_CUDA
     assert b"no CPU fallback" in lib.zen_last_error_message()
+
+
+def test_compat_header_compiles():
+    """The C++ drop-in (include/zen_b200/compat.hpp) and its test build here."""
+    import shutil
+    import subprocess
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-Wall", "-Wextra",
+                        "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include",
+                        os.path.join(ROOT, "tests", "cpp", "compat_test.cpp")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]

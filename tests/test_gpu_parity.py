@@ -434,3 +434,16 @@ def test_bp_full_size_properties(zen, n, rows):
     led, counts, agg = bp.ledger()
     assert int(agg.sum()) == oi.numel()
     assert int(counts.sum()) == sum(int(torch.count_nonzero(x)) for x in dense)
+
+
+def test_cpp_compat_dropin(zen):
+    """The reference's own hashing/codec/schemes test cases through the C++
+    drop-in header (tests/cpp/compat_test.cpp, built by `make compat_test`)."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "build", "compat_test")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", ROOT, "compat_test"], check=True, capture_output=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:]
