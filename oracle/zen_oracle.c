@@ -4,7 +4,7 @@
  * Plain-C restatement of the reference Balanced-Parallelism path
  * (/root/reference/proj/include/zen/*.hpp).  Every function cites the
  * reference lines it follows.  It is pinned against the reference itself
- * (tests/golden/*, produced by oracle/make_golden.cpp compiled from the
+ * (tests/golden/*, produced by oracle/make_golden.py from oracle/_ref, the
  * reference headers) by tests/test_oracle_golden.py.
  */
 #include "zen_oracle.h"

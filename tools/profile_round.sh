@@ -1,0 +1,28 @@
+#!/usr/bin/env bash
+# One GPU-box pass that produces everything profiles/ and the round's bench
+# evidence need.  Run from the repo root under gpurun:
+#   gpurun --timeout 2400 -- 'bash tools/profile_round.sh rNN'
+# Order matters: each ncu pass runs only after the same command exited 0
+# without ncu.  Outputs land in gpurun_out/<tag>/.
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
+python -m pytest tests -m gpu -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/status"
+timeout 600 ./build/compat_test > "$OUT/compat_test.log" 2>&1; echo "compat rc=$?" >> "$OUT/status"
+timeout 900 python bench.py --impl reference > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"; echo "ref rc=$?" >> "$OUT/status"
+timeout 900 python bench.py --emulate 8 > "$OUT/bench.json" 2> "$OUT/bench.err"
+rc=$?; echo "bench rc=$rc" >> "$OUT/status"
+SHORT="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu"
+timeout 600 $SHORT > "$OUT/short.json" 2> "$OUT/short.err"
+rc2=$?; echo "short rc=$rc2" >> "$OUT/status"
+if [ $rc2 -eq 0 ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+      --log-file "$OUT/launches.csv" $SHORT > "$OUT/ncu_launches.log" 2>&1
+  echo "ncu launches rc=$?" >> "$OUT/status"
+  timeout 1500 ncu --set full --clock-control none --import-source on \
+      -k regex:'k_(extract_tiles|extract_compact|extract_scan|decode|bpre|agg_values|agg_union|agg_mark|scatter|part|part_scan|place|depth|serial_scan|serial_scatter|fallback|push_signal)' \
+      -s 60 -c 17 -o "$OUT/full" $SHORT > "$OUT/ncu_full.log" 2>&1
+  echo "ncu full rc=$?" >> "$OUT/status"
+fi
