@@ -287,28 +287,56 @@ def main():
     # correctness guard on the benchmarked configuration (cheap identity checks)
     cnt = bp.result_count()
     assert cnt >= z and cnt <= n * z, f"result size {cnt} out of range"
-    bp.stage_times()  # reset
-    bp.enable_timing(True)
     launches0 = zen.load().zen_kernel_launches()
     barrier()
     with ClockSampler(local_rank) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             bp.sync_dense([d_dense])
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         e1.record(stream)
         barrier()
     launches = zen.load().zen_kernel_launches() - launches0
     bp.wait()
     ms = e0.elapsed_time(e1) / args.steps
+    # stage breakdown: a second pass of the same K syncs replayed from the graph
+    # variant with CUDA-event nodes between the stages (the nodes cost a few us
+    # each, so the headline `value` above is timed without them)
+    bp.stage_times()  # reset
+    bp.enable_timing(True)
+    for _ in range(2):
+        bp.sync_dense([d_dense])
+    bp.wait()
+    bp.stage_times()
+    barrier()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.steps):
+        bp.sync_dense([d_dense])
+    s1.record(stream)
+    barrier()
+    bp.wait()
+    staged_ms = s0.elapsed_time(s1) / args.steps
     stage_ms, timed = bp.stage_times()
     bp.enable_timing(False)
     stage_ms = stage_ms / max(timed, 1)
+    # the roofline kernel alone: back-to-back launches, CUDA events on its stream
+    ext_kernel_ms = bp.time_extract(d_dense, iters=max(20, args.steps // 4))
+    per_rank = None
     if dist:
-        t = torch.tensor([ms] + list(stage_ms), device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, stage_ms = float(t[0]), t[1:].cpu().numpy()
+        t = torch.tensor([ms, host_ms, staged_ms] + list(stage_ms), device="cuda",
+                         dtype=torch.float64)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        allt = torch.stack(allt).cpu().numpy()
+        per_rank = [{"ms": round(float(r[0]), 4), "host_enqueue_ms": round(float(r[1]), 4),
+                     "stage_ms": [round(float(x), 4) for x in r[3:]]} for r in allt]
+        ms, host_ms, staged_ms = (float(allt[:, i].max()) for i in range(3))
+        stage_ms = allt[:, 3:].max(0)
     ledger, counts, agg = bp.ledger()
     union = int(bp.result_count())
 
@@ -350,7 +378,6 @@ def main():
         for _ in range(3):
             be.sync_dense(dd)
         be.wait()
-        be.enable_timing(True)
         torch.cuda.synchronize()
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
@@ -361,7 +388,12 @@ def main():
         a1.record(stream)
         torch.cuda.synchronize()
         be.wait()
+        be.enable_timing(True)  # stage breakdown from a second pass
+        for _ in range(ke):
+            be.sync_dense(dd)
+        be.wait()
         sms, kk = be.stage_times()
+        be.enable_timing(False)
         nzr = np.zeros(args.rows, bool)
         for w in range(ne):
             nzr[rows_e[w]] = True
@@ -380,7 +412,7 @@ def main():
 
     # roofline of the dominant kernel (extraction: streams the 256 MB dense gradient)
     peak, peak_src = measured_peaks()
-    ext_ms = float(stage_ms[0])
+    ext_ms = float(ext_kernel_ms)
     alg_bytes = 4 * m + 12 * z  # 4M + E*z, E = 12 B (u64 index + f32 value)
     achieved = alg_bytes / (ext_ms * 1e-3) / 1e9 if ext_ms > 0 else None
     traffic = ncu_traffic().get("k_extract")
@@ -389,7 +421,9 @@ def main():
                 "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
                 "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
                 "peak_source": peak_src,
-                "launch_ms": round(ext_ms, 5)}
+                "launch_ms": round(ext_ms, 5),
+                "timing": "k_extract_tiles alone, back-to-back launches, CUDA events on its stream "
+                          "(zen_bp_time_extract); in-sync stage time in stage_ms.extract"}
     hash_ms = float(stage_ms[1])
     hash_bytes = 24 * z  # 2*E*z
     total_nnz = n * z
@@ -401,6 +435,7 @@ def main():
         "config": config_dict(args, n, z),
         "throughput_mnnz_per_s": round(total_nnz / (ms * 1e-3) / 1e6, 1),
         "stage_ms": {nm: round(float(x), 5) for nm, x in zip(zen.STAGE_NAMES, stage_ms)},
+        "stage_pass_ms_per_step": round(staged_ms, 4),
         "hash_stage": {"mnnz_per_s": round(z / (hash_ms * 1e-3) / 1e6, 1) if hash_ms else None,
                        "algorithmic_bytes": hash_bytes,
                        "hbm_frac": round(hash_bytes / (hash_ms * 1e-3) / 1e9 / peak, 4) if hash_ms else None,
@@ -410,12 +445,15 @@ def main():
                      "note": "push wire: u32 index + f32 value (WireFormat::coo(32) layout); "
                              "pull: HashBitmap bits + f32 values; ledger bits use the reference "
                              "widths (64-bit COO)"},
+        "host_enqueue_ms_per_step": round(host_ms, 4),
         "union_nnz": union, "gpu_launches": int(launches),
         "kernels_per_sync": bp.kernels_per_sync(),
         "roofline": roofline,
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    if per_rank:
+        line["per_rank"] = per_rank
     if emu:
         line["emulated_local"] = emu
     if world == 1 and not args.no_cpu:

@@ -207,6 +207,10 @@ uint32_t zen_bp_kernels_per_sync(const zen_bp* bp);
 /* replay dense syncs from a captured CUDA graph (default on; needs a
  * non-legacy stream, see zen_ctx_set_stream) */
 zen_status zen_bp_use_graph(zen_bp* bp, int on);
+/* average duration (ms) of the extraction kernel alone over `iters`
+ * back-to-back launches on the context stream (roofline measurement; uses the
+ * synchroniser's workspace, so not concurrently with a sync) */
+zen_status zen_bp_time_extract(zen_bp* bp, const float* d_dense, uint32_t iters, double* ms);
 /* end to end from HOST buffers: H2D of the dense gradients (pinned host
  * memory recommended), the sync, D2H of the result. */
 zen_status zen_bp_sync_host(zen_bp* bp, const float* const* h_dense, uint64_t* h_idx,

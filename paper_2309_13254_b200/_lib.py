@@ -88,6 +88,7 @@ _SIGS = {
     "zen_bp_stage_times": (C.c_int, [vp, vp, P(u64)]),
     "zen_bp_kernels_per_sync": (u32, [vp]),
     "zen_bp_use_graph": (C.c_int, [vp, C.c_int]),
+    "zen_bp_time_extract": (C.c_int, [vp, vp, u32, P(C.c_double)]),
     "zen_bp_sync_host": (C.c_int, [vp, P(vp), vp, vp, u64, P(u64)]),
     "zen_bp_debug_part": (C.c_int, [vp, C.c_int, u32, u32, vp, vp, u64, P(u64)]),
 }

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -20,6 +21,34 @@
 namespace zen {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static bool pdl_env() {
+  static const bool on = [] {
+    const char* e = std::getenv("ZEN_PDL");  // ZEN_PDL=0: A/B measurement
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static int prio_range(bool least) {
+  static int lo = 0, hi = 0;
+  static const bool init = [] {
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least, hi = greatest
+    return true;
+  }();
+  (void)init;
+  return least ? lo : hi;
+}
+static thread_local bool t_pdl = true;
+static thread_local int t_prio = 1 << 30;  // "unset": greatest priority
+bool launch_pdl() { return t_pdl && pdl_env(); }
+int launch_priority() { return t_prio == (1 << 30) ? prio_range(false) : t_prio; }
+LaunchScope::LaunchScope(bool pdl, bool low_priority) : prev_pdl(t_pdl), prev_prio(t_prio) {
+  t_pdl = pdl;
+  t_prio = prio_range(low_priority);
+}
+LaunchScope::~LaunchScope() {
+  t_pdl = prev_pdl;
+  t_prio = prev_prio;
+}
 
 // extra small kernels (k_util.cu)
 void launch_dump_slots(const unsigned long long* slots, uint64_t cells, uint32_t epoch,
@@ -283,6 +312,8 @@ zen_status zen_to_sparse(zen_ctx* c, const float* d_dense, uint64_t m, uint64_t*
   CKR(mem.alloc(&ws.st_val, ntiles * kExtractTile, false));
   CKR(mem.alloc(&ws.tile_cnt, ntiles));
   CKR(mem.alloc(&ws.tile_base, ntiles));
+  ws.nblk = (std::min<uint64_t>(capacity, m) + 255) / 256;
+  CKR(mem.alloc(&ws.blk_tile, ws.nblk + 1));
   CKR(mem.alloc(&d_count, 1));
   CKR(mem.alloc(&err, 1));
   launch_extract<uint64_t>(d_dense, m, ws, d_idx, d_val, d_count, capacity, err, c->stream);
@@ -889,6 +920,8 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   CKR(mem.alloc(&w.ex.st_val, ext_tiles * kExtractTile, false));
   CKR(mem.alloc(&w.ex.tile_cnt, ext_tiles));
   CKR(mem.alloc(&w.ex.tile_base, ext_tiles));
+  w.ex.nblk = (std::min<uint64_t>(bp->cap, bp->m) + 255) / 256;
+  CKR(mem.alloc(&w.ex.blk_tile, w.ex.nblk + 1));
   zen_hash_family f;
   CKR(zen_hash_family_make_worker(bp->params.seed, w.id, n, k, &f));
   a.fam = fold(f);
@@ -1202,12 +1235,6 @@ zen_status zen_bp_connect(zen_bp* bp, const void* handles) {
 
 namespace {
 
-void record(zen_bp* bp, int stage) {
-  if (!bp->timing) return;
-  const uint64_t slot = bp->ev_head % kRing;
-  cudaEventRecord(bp->ev[slot * (ZEN_STAGES + 1) + stage], bp->ctx->stream);
-}
-
 // Enqueue one synchronisation.  `ev` (ZEN_STAGES + 1 events) brackets the
 // stages when non-null.
 zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cudaEvent_t* ev) {
@@ -1223,15 +1250,17 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   // bp->side and joins at the end of the sync
   for (auto& w : bp->workers) {
     if (from_dense) {
-      launch_extract_compact_place<uint32_t>(bp->m, w.ex, w.keys, w.vals, bp->cap, w.a.fam,
-                                             w.a.hdr, w.a.slots, /*place=*/false, st);
+      launch_extract_compact_part<uint32_t>(bp->m, w.ex, w.a, bp->n, st);
     } else {
       launch_hash_begin<uint32_t>(w.a, st);
     }
     CK(cudaEventRecord(bp->fork, st));
     CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
-    launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side);
-    launch_hash_critical<uint32_t>(w.a, bp->n, st);
+    {
+      LaunchScope low(/*pdl=*/false, /*low_priority=*/true);
+      launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side);
+    }
+    launch_hash_critical<uint32_t>(w.a, bp->n, /*part=*/!from_dense, st);
   }
   if (ev) CK(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
   for (auto& s : bp->servers) launch_aggregate(s.a, st);
@@ -1274,8 +1303,11 @@ zen_status bp_run(zen_bp* bp, bool from_dense, const float* const* dense) {
     CKR(bp_enqueue(bp, from_dense, dense, ring));
     bp->kernels_per_sync = uint32_t(g_launches.load() - before);
   } else {
+    // stage-event nodes only in the timing variant: an event node between two
+    // kernels breaks their programmatic edge (~6 us each on B200)
     std::vector<const void*> key(dense, dense + bp->workers.size());
     key.push_back((const void*)st);
+    key.push_back(bp->timing ? (const void*)1 : nullptr);
     if (!bp->gexec || key != bp->gkey) {
       bp_drop_graph(bp);
       if (bp->gev.empty()) {
@@ -1284,7 +1316,7 @@ zen_status bp_run(zen_bp* bp, bool from_dense, const float* const* dense) {
       }
       const uint64_t before = g_launches.load();
       CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      zen_status rc = bp_enqueue(bp, true, dense, bp->gev.data());
+      zen_status rc = bp_enqueue(bp, true, dense, bp->timing ? bp->gev.data() : nullptr);
       cudaGraph_t graph_def = nullptr;
       cudaError_t e = cudaStreamEndCapture(st, &graph_def);
       if (rc != ZEN_OK) {
@@ -1312,9 +1344,9 @@ zen_status bp_run(zen_bp* bp, bool from_dense, const float* const* dense) {
       bp->gdef = graph_def;
       bp->gkey = key;
     }
-    for (uint32_t i = 0; i <= ZEN_STAGES; ++i)  // retarget the stage events
-      CK(cudaGraphExecEventRecordNodeSetEvent(bp->gexec, bp->gev_nodes[i],
-                                              ring ? ring[i] : bp->gev[i]));
+    if (ring)
+      for (uint32_t i = 0; i <= ZEN_STAGES; ++i)  // retarget the stage events
+        CK(cudaGraphExecEventRecordNodeSetEvent(bp->gexec, bp->gev_nodes[i], ring[i]));
     CK(cudaGraphLaunch(bp->gexec, st));
     g_launches.fetch_add(bp->graph_kernels);
     bp->kernels_per_sync = bp->graph_kernels;
@@ -1549,6 +1581,28 @@ uint32_t zen_bp_kernels_per_sync(const zen_bp* bp) { return bp ? bp->kernels_per
 zen_status zen_bp_use_graph(zen_bp* bp, int on) {
   if (!bp) return fail(ZEN_E_INVALID, "null argument");
   bp->use_graph = on != 0;
+  return ZEN_OK;
+}
+
+zen_status zen_bp_time_extract(zen_bp* bp, const float* d_dense, uint32_t iters, double* ms) {
+  if (!bp || !d_dense || !ms || !iters) return fail(ZEN_E_INVALID, "null argument");
+  if (bp->workers.empty()) return fail(ZEN_E_INVALID, "no local worker");
+  DevGuard g(bp->ctx->device);
+  cudaStream_t st = bp->ctx->stream;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  launch_extract_tiles<uint32_t>(d_dense, bp->m, bp->workers[0].ex, st);  // warm-up
+  CK(cudaEventRecord(e0, st));
+  for (uint32_t i = 0; i < iters; ++i)
+    launch_extract_tiles<uint32_t>(d_dense, bp->m, bp->workers[0].ex, st);
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = double(t) / iters;
   return ZEN_OK;
 }
 

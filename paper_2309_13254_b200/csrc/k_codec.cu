@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256) k_tables_planes(uint64_t m, uint32_t n, u
                                                        uint32_t nplanes,
                                                        unsigned long long* planes,
                                                        uint32_t* chunk_cnt, uint64_t nwords) {
+  zen_dev::pdl_entry();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;  // multiple of 32
   for (uint64_t w0 = (uint64_t)blockIdx.x * blockDim.x; w0 < nwords; w0 += stride) {
     const uint64_t w = w0 + threadIdx.x;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) k_tables_planes(uint64_t m, uint32_t n, u
 // in-place exclusive scan over chunks, per server; totals[s] = |I_s|
 __global__ void __launch_bounds__(1024) k_tables_scan(uint32_t* cc, uint64_t nchunks, uint32_t n,
                                                       uint64_t* totals) {
+  zen_dev::pdl_entry();
   __shared__ uint32_t sscan[33];
   for (uint32_t s = 0; s < n; ++s) {
     uint64_t carry = 0;
@@ -104,6 +106,7 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
                                                     const unsigned long long* planes,
                                                     const uint32_t* cprefix, OwnWord* own,
                                                     uint32_t* sel, uint64_t nsel, uint64_t nwords) {
+  zen_dev::pdl_entry();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t w0 = (uint64_t)blockIdx.x * blockDim.x; w0 < nwords; w0 += stride) {
     const uint64_t w = w0 + threadIdx.x;
@@ -131,6 +134,7 @@ __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
 // Phase 1: every received entry sets its HashBitmap position (its rank in I_s,
 // zen/codec.hpp:146-158) in its worker's presence bitmap.
 __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
+  zen_dev::pdl_entry();
   __shared__ uint64_t pre[kMaxWorkers + 1];
   const uint32_t n = a.n;
   if (a.wait_push && threadIdx.x < n) {
@@ -200,6 +204,7 @@ __device__ __forceinline__ void store8u(uint32_t* p, const uint32_t (&v)[kWPT]) 
 // padded to 8 words); the last block turns the block totals into exclusive
 // prefixes and records U_s.
 __global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
+  zen_dev::pdl_entry();
   __shared__ uint32_t wsum[kMaxWorkers + 1][kAggThreads / 32];
   __shared__ uint32_t inw[kMaxWorkers + 1][kAggThreads];
   __shared__ uint32_t s_last;
@@ -282,6 +287,7 @@ constexpr int kValThreads = 128;
 
 template <int NMAX>
 __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
+  zen_dev::pdl_entry();
   __shared__ unsigned long long spw[kValThreads][NMAX];
   __shared__ uint32_t sbase[kValThreads][NMAX];
   const uint32_t n = a.n, lane = lane_id();
@@ -295,7 +301,10 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
     uint32_t b = 0;
     if (w < (int)n && valid) {
       v = a.pw[(uint64_t)w * a.nws + j];
-      if (v) b = a.blk[(uint64_t)w * a.nblk + pb] + a.pre[(uint64_t)w * a.nws + j];
+      if (v) {
+        b = a.blk[(uint64_t)w * a.nblk + pb] + a.pre[(uint64_t)w * a.nws + j];
+        a.pw[(uint64_t)w * a.nws + j] = 0ull;  // last reader: clean for the next sync
+      }
     }
     spw[threadIdx.x][w] = v;
     sbase[threadIdx.x][w] = b;
@@ -349,6 +358,7 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
 // boundary completes every NVLink store of the encode -- publishes U_s and
 // then the flag with release semantics at system scope.
 __global__ void k_agg_signal(AggArgs a) {
+  zen_dev::pdl_entry();
   __threadfence_system();
   const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
   const uint64_t u = *(volatile uint64_t*)a.agg_count;
@@ -371,6 +381,7 @@ __global__ void k_agg_signal(AggArgs a) {
 // block, 8 consecutive words per thread) + block totals; the last block turns
 // the totals into exclusive prefixes, per-server popcounts and |result|.
 __global__ void __launch_bounds__(256) k_bpre(DecodeArgs a) {
+  zen_dev::pdl_entry();
   __shared__ uint32_t sscan[33];
   __shared__ uint32_t s_last;
   const uint32_t n = a.n;
@@ -447,6 +458,7 @@ __device__ __forceinline__ uint64_t bitmap_prefix(const DecodeArgs& a, uint32_t 
 // mask); the warp then expands its set bits cooperatively.
 template <int NMAX>
 __global__ void __launch_bounds__(kDecodeTileWords) k_decode(DecodeArgs a, uint64_t nwords) {
+  zen_dev::pdl_entry();
   __shared__ unsigned long long spres[kDecodeTileWords][NMAX];
   __shared__ uint32_t svb[kDecodeTileWords][NMAX];
   __shared__ uint32_t sscan[33];
@@ -551,14 +563,14 @@ inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
 void launch_tables_planes(uint64_t m, uint32_t n, uint64_t pc, uint32_t nplanes,
                           unsigned long long* planes, uint32_t* chunk_cnt, cudaStream_t stream) {
   const uint64_t nwords = (m + 63) / 64;
-  k_tables_planes<<<grid_for(nwords, 256, 148 * 16), 256, 0, stream>>>(m, n, pc, nplanes, planes,
+  launch_k(k_tables_planes, grid_for(nwords, 256, 148 * 16), 256, 0, stream, m, n, pc, nplanes, planes,
                                                                         chunk_cnt, nwords);
   count_launch();
 }
 
 void launch_tables_scan(uint32_t* cc, uint64_t nchunks, uint32_t n, uint64_t* totals,
                         cudaStream_t stream) {
-  k_tables_scan<<<1, 1024, 0, stream>>>(cc, nchunks, n, totals);
+  launch_k(k_tables_scan, 1, 1024, 0, stream, cc, nchunks, n, totals);
   count_launch();
 }
 
@@ -566,30 +578,28 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
                        const unsigned long long* planes, const uint32_t* cprefix, OwnWord* own,
                        uint32_t* sel, uint64_t nsel, cudaStream_t stream) {
   const uint64_t nwords = (m + 63) / 64;
-  k_tables_own<<<grid_for(nwords, 256, 148 * 16), 256, 0, stream>>>(m, n, s, nplanes, planes,
+  launch_k(k_tables_own, grid_for(nwords, 256, 148 * 16), 256, 0, stream, m, n, s, nplanes, planes,
                                                                      cprefix, own, sel, nsel,
                                                                      nwords);
   count_launch();
 }
 
 void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
-  uint64_t cap_entries = 0;
-  (void)cap_entries;
-  cudaMemsetAsync(a.pw, 0, (size_t)a.n * a.nws * 8, stream);
-  k_agg_mark<<<148 * 8, kAggThreads, 0, stream>>>(a);
-  k_agg_union<<<a.nblk, kAggThreads, 0, stream>>>(a);
+  // a.pw is all-zero here: zeroed at allocation, re-zeroed by k_agg_values
+  launch_k(k_agg_mark, 148 * 8, kAggThreads, 0, stream, a);
+  launch_k(k_agg_union, a.nblk, kAggThreads, 0, stream, a);
   const unsigned g = (unsigned)((a.nw + kValThreads - 1) / kValThreads);
   if (a.n <= 2)
-    k_agg_values<2><<<g, kValThreads, 0, stream>>>(a);
+    launch_k(k_agg_values<2>, g, kValThreads, 0, stream, a);
   else if (a.n <= 4)
-    k_agg_values<4><<<g, kValThreads, 0, stream>>>(a);
+    launch_k(k_agg_values<4>, g, kValThreads, 0, stream, a);
   else if (a.n <= 8)
-    k_agg_values<8><<<g, kValThreads, 0, stream>>>(a);
+    launch_k(k_agg_values<8>, g, kValThreads, 0, stream, a);
   else
-    k_agg_values<16><<<g, kValThreads, 0, stream>>>(a);
+    launch_k(k_agg_values<16>, g, kValThreads, 0, stream, a);
   for (int i = 0; i < 3; ++i) count_launch();
   if (a.dst_hdr) {
-    k_agg_signal<<<1, 32, 0, stream>>>(a);
+    launch_k(k_agg_signal, 1, 32, 0, stream, a);
     count_launch();
   }
 }
@@ -597,16 +607,16 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
 void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {
   const uint64_t nwords = (a.m + 63) / 64;
   const uint32_t ntiles = (uint32_t)((nwords + kDecodeTileWords - 1) / kDecodeTileWords);
-  k_bpre<<<a.total_blocks ? a.total_blocks : 1, 256, 0, stream>>>(a);
+  launch_k(k_bpre, a.total_blocks ? a.total_blocks : 1, 256, 0, stream, a);
   constexpr unsigned T = kDecodeTileWords;
   if (a.n <= 2)
-    k_decode<2><<<ntiles, T, 0, stream>>>(a, nwords);
+    launch_k(k_decode<2>, ntiles, T, 0, stream, a, nwords);
   else if (a.n <= 4)
-    k_decode<4><<<ntiles, T, 0, stream>>>(a, nwords);
+    launch_k(k_decode<4>, ntiles, T, 0, stream, a, nwords);
   else if (a.n <= 8)
-    k_decode<8><<<ntiles, T, 0, stream>>>(a, nwords);
+    launch_k(k_decode<8>, ntiles, T, 0, stream, a, nwords);
   else
-    k_decode<16><<<ntiles, T, 0, stream>>>(a, nwords);
+    launch_k(k_decode<16>, ntiles, T, 0, stream, a, nwords);
   for (int i = 0; i < 2; ++i) count_launch();
 }
 

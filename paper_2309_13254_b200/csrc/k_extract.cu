@@ -36,6 +36,7 @@ template <typename K>
 __global__ void __launch_bounds__(kThreads, 4)
     k_extract_tiles(const float* __restrict__ dense, uint64_t m, K* __restrict__ st_idx,
                     float* __restrict__ st_val, uint32_t* __restrict__ tile_cnt) {
+  zen_dev::pdl_entry();
   __shared__ uint32_t s_warp_tot[kThreads / 32];
   const uint32_t tile = blockIdx.x;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -104,11 +105,17 @@ __global__ void __launch_bounds__(kThreads, 4)
   }
 }
 
+// Exclusive scan of the tile counts -> tile_base; and for every compaction
+// block b (output positions [256b, 256b+256)) the tile holding position 256b
+// (blk_tile[b]), so the compaction needs no binary search over all tiles.
 template <typename K, bool BEGIN>
 __global__ void __launch_bounds__(1024) k_extract_scan(uint32_t* __restrict__ tile_cnt,
                                                        uint32_t ntiles, uint64_t* d_count,
                                                        uint64_t capacity, uint32_t* err,
-                                                       uint64_t* tile_base, HashArgs<K> ha) {
+                                                       uint64_t* tile_base,
+                                                       uint32_t* __restrict__ blk_tile,
+                                                       uint64_t nblk, HashArgs<K> ha) {
+  zen_dev::pdl_entry();
   __shared__ uint64_t sscan[33];
   constexpr int E = 8;
   uint64_t carry = 0;
@@ -131,7 +138,13 @@ __global__ void __launch_bounds__(1024) k_extract_scan(uint32_t* __restrict__ ti
     uint64_t ex = carry + block_exclusive_sum(local, sscan, &tot);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      if (t0 + e < ntiles) tile_base[t0 + e] = ex;
+      if (t0 + e < ntiles) {
+        tile_base[t0 + e] = ex;
+        // blocks whose first position falls in this tile
+        const uint64_t end = ex + v[e];
+        for (uint64_t b = (ex + 255) / 256; b * 256 < end && b < nblk; ++b)
+          blk_tile[b] = t0 + e;
+      }
       ex += v[e];
     }
     carry += tot;
@@ -146,43 +159,82 @@ __global__ void __launch_bounds__(1024) k_extract_scan(uint32_t* __restrict__ ti
   }
 }
 
-// one thread per output position (balanced); optionally fuses the placement
-template <typename K, bool PLACE>
+// one thread per output position (balanced)
+template <typename K>
 __global__ void __launch_bounds__(256)
     k_extract_compact(const K* __restrict__ st_idx, const float* __restrict__ st_val,
                       const uint64_t* __restrict__ tile_base, uint32_t ntiles,
                       const uint64_t* d_count, K* __restrict__ out_idx,
-                      float* __restrict__ out_val, uint64_t capacity, DevFamily fam,
-                      HashHdr* hdr, unsigned long long* slots) {
-  __shared__ uint32_t s_range[2];
+                      float* __restrict__ out_val, uint64_t capacity,
+                      const uint32_t* __restrict__ blk_tile) {
+  zen_dev::pdl_entry();
   const uint64_t z = *d_count;
   const uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x;
   const uint64_t i = b0 + threadIdx.x;
-  if (b0 >= z || b0 >= capacity) return;
-  if (threadIdx.x < 2) {  // tiles of the block's first and last position
-    const uint64_t q = threadIdx.x == 0 ? b0 : min(min(z, capacity), b0 + blockDim.x) - 1;
-    uint32_t lo = 0, hi = ntiles;  // largest t with tile_base[t] <= q
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (tile_base[mid] <= q) lo = mid; else hi = mid;
-    }
-    s_range[threadIdx.x] = lo;
-  }
-  __syncthreads();
-  if (i >= z || i >= capacity) return;
-  uint32_t lo = s_range[0], hi = s_range[1] + 1;
+  const uint64_t zc = min(z, capacity);
+  if (i >= zc) return;
+  // tiles of the block's positions: [blk_tile[b], blk_tile[b+1]]
+  uint32_t lo = blk_tile[blockIdx.x];
+  uint32_t hi = (b0 + blockDim.x < zc) ? blk_tile[blockIdx.x + 1] + 1 : ntiles;
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
     if (tile_base[mid] <= i) lo = mid; else hi = mid;
   }
   const uint64_t src = (uint64_t)lo * kExtractTile + (i - tile_base[lo]);
-  const K x = st_idx[src];
-  out_idx[i] = x;
+  out_idx[i] = st_idx[src];
   out_val[i] = st_val[src];
-  if (PLACE) {
-    if (hdr->status & kErrCapacity) return;
-    place_key(fam, slots, (uint64_t)x + 1, hdr->r1, hdr->stride, epoch_word(hdr->epoch));
+}
+
+// BP pipeline: the compaction block of 256 output positions IS hash tile
+// `blockIdx.x`, so the data path's partition pass (k_hash.cu k_part) runs here
+// on the key just moved: h0 partition, its stable rank among the tile's
+// same-partition keys, and the per-(partition, tile) counts.
+template <typename K>
+__global__ void __launch_bounds__(256)
+    k_extract_compact_part(const K* __restrict__ st_idx, const float* __restrict__ st_val,
+                           const uint64_t* __restrict__ tile_base, uint32_t ntiles,
+                           const uint32_t* __restrict__ blk_tile, HashArgs<K> a) {
+  zen_dev::pdl_entry();
+  extern __shared__ uint32_t wc[];  // [8 warps][n] key counts -> cross-warp prefixes
+  const HashHdr* h = a.hdr;
+  if (h->status & kErrCapacity) return;
+  const uint32_t tile = blockIdx.x;
+  if (tile >= h->ntiles) return;
+  const uint64_t z = h->count;
+  const uint32_t n = a.fam.n, lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t b0 = (uint64_t)tile * kHashTile;
+  const uint64_t i = b0 + threadIdx.x;
+  const bool valid = i < z;
+  for (uint32_t q = threadIdx.x; q < 8 * n; q += blockDim.x) wc[q] = 0;
+  uint32_t p = 0xFFFFFFFFu;
+  if (valid) {
+    uint32_t lo = blk_tile[tile];
+    uint32_t hi = (b0 + kHashTile < z) ? blk_tile[tile + 1] + 1 : ntiles;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (tile_base[mid] <= i) lo = mid; else hi = mid;
+    }
+    const uint64_t src = (uint64_t)lo * kExtractTile + (i - tile_base[lo]);
+    const K x = st_idx[src];
+    const_cast<K*>(a.idx)[i] = x;  // the worker's compacted keys (HashArgs input)
+    const_cast<float*>(a.val)[i] = st_val[src];
+    p = part_of(a.fam, (uint64_t)x + 1);
   }
+  const uint32_t g = __match_any_sync(0xffffffffu, p);
+  const uint32_t wr = __popc(g & lanemask_lt());
+  if (valid && lane == (uint32_t)(__ffs(g) - 1)) wc[warp * n + p] = __popc(g);
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) {
+    uint32_t acc = 0;
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t t = wc[w * n + q];
+      wc[w * n + q] = acc;
+      acc += t;
+    }
+    a.tile_cnt[(uint64_t)q * a.tiles_cap + tile] = acc;
+  }
+  __syncthreads();
+  if (valid) a.pmeta[i] = p | ((wc[warp * n + p] + wr) << 16);
 }
 
 }  // namespace
@@ -194,12 +246,12 @@ void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* o
                     float* out_val, uint64_t* d_count, uint64_t capacity, uint32_t* d_status_bits,
                     cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  k_extract_tiles<K><<<ntiles, kThreads, 0, stream>>>(dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
-  k_extract_scan<K, false><<<1, 1024, 0, stream>>>(ws.tile_cnt, ntiles, d_count, capacity,
-                                                   d_status_bits, ws.tile_base, HashArgs<K>{});
-  k_extract_compact<K, false><<<blocks_for(std::min<uint64_t>(capacity, m)), 256, 0, stream>>>(
-      ws.st_idx, ws.st_val, ws.tile_base, ntiles, d_count, out_idx, out_val, capacity,
-      DevFamily{}, nullptr, nullptr);
+  launch_k(k_extract_tiles<K>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
+  launch_k(k_extract_scan<K, false>, 1, 1024, 0, stream, ws.tile_cnt, ntiles, d_count, capacity,
+           d_status_bits, ws.tile_base, ws.blk_tile, ws.nblk, HashArgs<K>{});
+  launch_k(k_extract_compact<K>, blocks_for(std::min<uint64_t>(capacity, m)), 256, 0, stream,
+           ws.st_idx, ws.st_val, ws.tile_base, ntiles, d_count, out_idx, out_val, capacity,
+           ws.blk_tile);
   for (int i = 0; i < 3; ++i) count_launch();
 }
 
@@ -207,7 +259,7 @@ template <typename K>
 void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws,
                           cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  k_extract_tiles<K><<<ntiles, kThreads, 0, stream>>>(dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
+  launch_k(k_extract_tiles<K>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
   count_launch();
 }
 
@@ -215,25 +267,18 @@ template <typename K>
 void launch_extract_scan_begin(uint64_t m, const ExtractWs<K>& ws, const HashArgs<K>& ha,
                                uint64_t capacity, cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  k_extract_scan<K, true><<<1, 1024, 0, stream>>>(ws.tile_cnt, ntiles, &ha.hdr->count, capacity,
-                                                  &ha.hdr->status, ws.tile_base, ha);
+  launch_k(k_extract_scan<K, true>, 1, 1024, 0, stream, ws.tile_cnt, ntiles, &ha.hdr->count,
+           capacity, &ha.hdr->status, ws.tile_base, ws.blk_tile, ws.nblk, ha);
   count_launch();
 }
 
 template <typename K>
-void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx, float* out_val,
-                                  uint64_t capacity, const DevFamily& fam, HashHdr* hdr,
-                                  unsigned long long* slots, bool place, cudaStream_t stream) {
+void launch_extract_compact_part(uint64_t m, const ExtractWs<K>& ws, const HashArgs<K>& a,
+                                 uint32_t n, cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  const unsigned g = blocks_for(std::min<uint64_t>(capacity, m));
-  if (place)
-    k_extract_compact<K, true><<<g, 256, 0, stream>>>(ws.st_idx, ws.st_val, ws.tile_base, ntiles,
-                                                      &hdr->count, out_idx, out_val, capacity,
-                                                      fam, hdr, slots);
-  else
-    k_extract_compact<K, false><<<g, 256, 0, stream>>>(ws.st_idx, ws.st_val, ws.tile_base,
-                                                       ntiles, &hdr->count, out_idx, out_val,
-                                                       capacity, fam, hdr, slots);
+  launch_k(k_extract_compact_part<K>, (unsigned)std::max<uint64_t>(a.tiles_cap, 1), 256,
+           8 * n * sizeof(uint32_t), stream, ws.st_idx, ws.st_val, ws.tile_base, ntiles,
+           ws.blk_tile, a);
   count_launch();
 }
 
@@ -244,9 +289,8 @@ void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx
                                         cudaStream_t);                                           \
   template void launch_extract_scan_begin<K>(uint64_t, const ExtractWs<K>&, const HashArgs<K>&, \
                                              uint64_t, cudaStream_t);                            \
-  template void launch_extract_compact_place<K>(uint64_t, const ExtractWs<K>&, K*, float*,      \
-                                                uint64_t, const DevFamily&, HashHdr*,           \
-                                                unsigned long long*, bool, cudaStream_t);
+  template void launch_extract_compact_part<K>(uint64_t, const ExtractWs<K>&, const HashArgs<K>&, \
+                                               uint32_t, cudaStream_t);
 ZEN_INST(uint32_t)
 ZEN_INST(uint64_t)
 #undef ZEN_INST

@@ -54,6 +54,7 @@ static_assert(kHashTile == kThreads, "one key per thread");
 
 template <typename K>
 __global__ void k_hash_begin(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   hash_begin_body(a);
 }
 
@@ -61,6 +62,7 @@ __global__ void k_hash_begin(HashArgs<K> a) {
 
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_part(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   extern __shared__ uint32_t sm[];
   const uint32_t n = a.fam.n;
   uint32_t* wc = sm;  // [kWarps][n] key counts -> cross-warp prefixes
@@ -119,6 +121,7 @@ __device__ __forceinline__ uint32_t block_scan_tiles(uint32_t* arr, uint32_t nti
 
 template <typename K>
 __global__ void __launch_bounds__(1024) k_part_scan(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   __shared__ uint32_t sscan[33];
   HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
@@ -130,6 +133,7 @@ __global__ void __launch_bounds__(1024) k_part_scan(HashArgs<K> a) {
 
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   extern __shared__ uint64_t soff[];  // [n] part offsets (contiguous mode)
   const uint32_t n = a.fam.n;
   HashHdr* h = a.hdr;
@@ -173,6 +177,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
 // every server's inbox header, then the flag (release, system scope).
 template <typename K>
 __global__ void k_push_signal(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   HashHdr* h = a.hdr;
   const uint32_t n = a.fam.n;
   fence_for(a.peer);
@@ -197,6 +202,7 @@ __global__ void k_push_signal(HashArgs<K> a) {
 
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_place(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   const HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
   const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
@@ -208,58 +214,63 @@ __global__ void __launch_bounds__(kThreads) k_place(HashArgs<K> a) {
 
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_depth(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   extern __shared__ uint32_t sm[];
   const uint32_t n = a.fam.n, k = a.fam.k;
   uint32_t* ws = sm;  // [kWarps][n] serial counts -> cross-warp prefixes
   const HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
-  const uint32_t tile = blockIdx.x;
-  if (tile >= h->ntiles) return;
   const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
   const uint64_t ew = epoch_word(h->epoch);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint32_t q = threadIdx.x; q < kWarps * n; q += kThreads) ws[q] = 0;
-  const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
-  const bool valid = i < z;
-  uint32_t p = kInvalid, depth = 0;
-  if (valid) {
-    const uint64_t key = (uint64_t)a.idx[i] + 1;
-    p = part_of(a.fam, key);
-    const uint64_t base = (uint64_t)p * stride;
-    for (uint32_t t = 0; t < k; ++t) {
-      const uint64_t c = slot_of(a.fam, key, t, r1);
-      if (a.slots[base + c] == (ew | key)) {
-        depth = t + 1;
-        if (a.slot_vals) a.slot_vals[base + c] = a.val[i];
-        break;
+  const uint32_t ntiles = h->ntiles;
+  // grid-stride over tiles: the side path keeps to a fraction of the SMs
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < kWarps * n; q += kThreads) ws[q] = 0;
+    const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
+    const bool valid = i < z;
+    uint32_t p = kInvalid, depth = 0;
+    if (valid) {
+      const uint64_t key = (uint64_t)a.idx[i] + 1;
+      p = part_of(a.fam, key);
+      const uint64_t base = (uint64_t)p * stride;
+      for (uint32_t t = 0; t < k; ++t) {
+        const uint64_t c = slot_of(a.fam, key, t, r1);
+        if (a.slots[base + c] == (ew | key)) {
+          depth = t + 1;
+          if (a.slot_vals) a.slot_vals[base + c] = a.val[i];
+          break;
+        }
       }
     }
-  }
-  __syncthreads();
-  const uint32_t ks = (valid && depth == 0) ? p : kInvalid;
-  const uint32_t gs = __match_any_sync(0xffffffffu, ks);
-  const uint32_t wsr = __popc(gs & lanemask_lt());
-  if (ks != kInvalid && lane == (uint32_t)(__ffs(gs) - 1)) ws[warp * n + p] = __popc(gs);
-  const uint32_t kd = valid ? (p * 32u + depth) : kInvalid;
-  const uint32_t gd = __match_any_sync(0xffffffffu, kd);
-  if (valid && lane == (uint32_t)(__ffs(gd) - 1))
-    atomicAdd(&a.stats[p * (k + 1) + depth], (uint32_t)__popc(gd));
-  __syncthreads();
-  for (uint32_t q = threadIdx.x; q < n; q += kThreads) {
-    uint32_t acc = 0;
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t t = ws[w * n + q];
-      ws[w * n + q] = acc;
-      acc += t;
+    __syncthreads();
+    const uint32_t ks = (valid && depth == 0) ? p : kInvalid;
+    const uint32_t gs = __match_any_sync(0xffffffffu, ks);
+    const uint32_t wsr = __popc(gs & lanemask_lt());
+    if (ks != kInvalid && lane == (uint32_t)(__ffs(gs) - 1)) ws[warp * n + p] = __popc(gs);
+    const uint32_t kd = valid ? (p * 32u + depth) : kInvalid;
+    const uint32_t gd = __match_any_sync(0xffffffffu, kd);
+    if (valid && lane == (uint32_t)(__ffs(gd) - 1))
+      atomicAdd(&a.stats[p * (k + 1) + depth], (uint32_t)__popc(gd));
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < n; q += kThreads) {
+      uint32_t acc = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t t = ws[w * n + q];
+        ws[w * n + q] = acc;
+        acc += t;
+      }
+      a.tile_scnt[(uint64_t)q * a.tiles_cap + tile] = acc;
     }
-    a.tile_scnt[(uint64_t)q * a.tiles_cap + tile] = acc;
+    __syncthreads();
+    if (valid) a.meta[i] = pack_meta(p, depth, 0, depth == 0 ? ws[warp * n + p] + wsr : 0u);
   }
-  __syncthreads();
-  if (valid) a.meta[i] = pack_meta(p, depth, 0, depth == 0 ? ws[warp * n + p] + wsr : 0u);
 }
 
 template <typename K>
 __global__ void __launch_bounds__(1024) k_serial_scan(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   __shared__ uint32_t sscan[33];
   HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
@@ -276,19 +287,22 @@ __global__ void __launch_bounds__(1024) k_serial_scan(HashArgs<K> a) {
 
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_serial_scatter(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
-  const uint32_t tile = blockIdx.x;
-  const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
-  if (tile >= h->ntiles || i >= h->count) return;
-  const uint32_t m = a.meta[i];
-  if (meta_depth(m) != 0) return;
-  const uint32_t p = meta_part(m);
-  const uint64_t spos = (uint64_t)a.tile_scnt[(uint64_t)p * a.tiles_cap + tile] + meta_srank(m);
-  if (spos < h->r2) {
-    const uint64_t s = (uint64_t)p * h->stride + h->r1 + spos;
-    a.slots[s] = epoch_word(h->epoch) | ((uint64_t)a.idx[i] + 1);
-    if (a.slot_vals) a.slot_vals[s] = a.val[i];
+  const uint64_t z = h->count;
+  for (uint64_t i = (uint64_t)blockIdx.x * kHashTile + threadIdx.x; i < z;
+       i += (uint64_t)gridDim.x * kHashTile) {
+    const uint32_t tile = (uint32_t)(i / kHashTile);
+    const uint32_t m = a.meta[i];
+    if (meta_depth(m) != 0) continue;
+    const uint32_t p = meta_part(m);
+    const uint64_t spos = (uint64_t)a.tile_scnt[(uint64_t)p * a.tiles_cap + tile] + meta_srank(m);
+    if (spos < h->r2) {
+      const uint64_t s = (uint64_t)p * h->stride + h->r1 + spos;
+      a.slots[s] = epoch_word(h->epoch) | ((uint64_t)a.idx[i] + 1);
+      if (a.slot_vals) a.slot_vals[s] = a.val[i];
+    }
   }
 }
 
@@ -297,6 +311,7 @@ __global__ void __launch_bounds__(kThreads) k_serial_scatter(HashArgs<K> a) {
 // folds the per-partition histograms into CollisionStats.
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
+  zen_dev::pdl_entry();
   __shared__ uint32_t list[kThreads];
   __shared__ uint32_t wcount[kWarps];
   __shared__ uint32_t s_last;
@@ -382,6 +397,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
 
 __global__ void k_partition_of(const uint64_t* __restrict__ idx, uint64_t count, uint64_t pc,
                                uint32_t n, uint32_t* __restrict__ out) {
+  zen_dev::pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
        i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = part_of_seed(pc, n, idx[i] + 1);
@@ -389,12 +405,14 @@ __global__ void k_partition_of(const uint64_t* __restrict__ idx, uint64_t count,
 
 __global__ void k_u64_to_u32(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
                              uint64_t n) {
+  zen_dev::pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = (uint32_t)in[i];
 }
 
 __global__ void k_fill_u64(unsigned long long* p, uint64_t n, uint64_t v) {
+  zen_dev::pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     p[i] = v;
@@ -410,19 +428,22 @@ inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
 
 template <typename K>
 void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream) {
-  k_hash_begin<K><<<1, 256, 0, stream>>>(a);
+  launch_k(k_hash_begin<K>, 1, 256, 0, stream, a);
   count_launch();
 }
 
 template <typename K>
-void launch_hash_critical(const HashArgs<K>& a, uint32_t n, cudaStream_t stream) {
+void launch_hash_critical(const HashArgs<K>& a, uint32_t n, bool part, cudaStream_t stream) {
   const unsigned tiles = (unsigned)std::max<uint64_t>(a.tiles_cap, 1);
-  k_part<K><<<tiles, kThreads, kWarps * n * sizeof(uint32_t), stream>>>(a);
-  k_part_scan<K><<<n, 1024, 0, stream>>>(a);
-  k_scatter<K><<<tiles, kThreads, a.dst_table ? 0 : n * sizeof(uint64_t), stream>>>(a);
-  for (int i = 0; i < 3; ++i) count_launch();
+  if (part) {  // else fused into the compaction (k_extract_compact_part)
+    launch_k(k_part<K>, tiles, kThreads, kWarps * n * sizeof(uint32_t), stream, a);
+    count_launch();
+  }
+  launch_k(k_part_scan<K>, n, 1024, 0, stream, a);
+  launch_k(k_scatter<K>, tiles, kThreads, a.dst_table ? 0 : n * sizeof(uint64_t), stream, a);
+  for (int i = 0; i < 2; ++i) count_launch();
   if (a.push_hdr) {
-    k_push_signal<K><<<1, 32, 0, stream>>>(a);
+    launch_k(k_push_signal<K>, 1, 32, 0, stream, a);
     count_launch();
   }
 }
@@ -430,21 +451,24 @@ void launch_hash_critical(const HashArgs<K>& a, uint32_t n, cudaStream_t stream)
 template <typename K>
 void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream) {
   const unsigned tiles = (unsigned)std::max<uint64_t>(a.tiles_cap, 1);
+  // grids capped at 2 CTAs per SM: the side path must not crowd out the
+  // critical path's kernels (it runs at the least priority, PDL off)
+  const unsigned side = std::min<unsigned>(tiles, 148 * 2);
   if (place) {
-    k_place<K><<<grid_for(a.cap, kThreads, 148 * 16), kThreads, 0, stream>>>(a);
+    launch_k(k_place<K>, grid_for(a.cap, kThreads, 148 * 2), kThreads, 0, stream, a);
     count_launch();
   }
-  k_depth<K><<<tiles, kThreads, kWarps * n * sizeof(uint32_t), stream>>>(a);
-  k_serial_scan<K><<<n, 1024, 0, stream>>>(a);
-  k_serial_scatter<K><<<tiles, kThreads, 0, stream>>>(a);
-  k_fallback<K><<<grid_for(n, 1, 148), kThreads, 0, stream>>>(a);
+  launch_k(k_depth<K>, side, kThreads, kWarps * n * sizeof(uint32_t), stream, a);
+  launch_k(k_serial_scan<K>, n, 1024, 0, stream, a);
+  launch_k(k_serial_scatter<K>, side, kThreads, 0, stream, a);
+  launch_k(k_fallback<K>, grid_for(n, 1, 148), kThreads, 0, stream, a);
   for (int i = 0; i < 4; ++i) count_launch();
 }
 
 template <typename K>
 void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
   launch_hash_begin<K>(a, stream);
-  launch_hash_critical<K>(a, n, stream);
+  launch_hash_critical<K>(a, n, true, stream);
   launch_hash_side<K>(a, n, true, stream);
   (void)k;
 }
@@ -452,7 +476,7 @@ void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stre
 #define ZEN_INST(K)                                                                         \
   template void launch_hash<K>(const HashArgs<K>&, uint32_t, uint32_t, cudaStream_t);       \
   template void launch_hash_begin<K>(const HashArgs<K>&, cudaStream_t);                     \
-  template void launch_hash_critical<K>(const HashArgs<K>&, uint32_t, cudaStream_t);        \
+  template void launch_hash_critical<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t);        \
   template void launch_hash_side<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t);
 ZEN_INST(uint32_t)
 ZEN_INST(uint64_t)
@@ -460,17 +484,17 @@ ZEN_INST(uint64_t)
 
 void launch_partition_of(const uint64_t* idx, uint64_t count, uint64_t pc, uint32_t n,
                          uint32_t* out, cudaStream_t stream) {
-  k_partition_of<<<grid_for(count, 256, 148 * 8), 256, 0, stream>>>(idx, count, pc, n, out);
+  launch_k(k_partition_of, grid_for(count, 256, 148 * 8), 256, 0, stream, idx, count, pc, n, out);
   count_launch();
 }
 
 void launch_u64_to_u32(const uint64_t* in, uint32_t* out, uint64_t n, cudaStream_t stream) {
-  k_u64_to_u32<<<grid_for(n, 256, 148 * 8), 256, 0, stream>>>(in, out, n);
+  launch_k(k_u64_to_u32, grid_for(n, 256, 148 * 8), 256, 0, stream, in, out, n);
   count_launch();
 }
 
 void launch_fill_u64(unsigned long long* p, uint64_t n, uint64_t v, cudaStream_t stream) {
-  k_fill_u64<<<grid_for(n, 256, 148 * 8), 256, 0, stream>>>(p, n, v);
+  launch_k(k_fill_u64, grid_for(n, 256, 148 * 8), 256, 0, stream, p, n, v);
   count_launch();
 }
 

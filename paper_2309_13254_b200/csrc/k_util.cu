@@ -13,6 +13,7 @@ using namespace zen_dev;
 __global__ void k_dump_slots(const unsigned long long* __restrict__ slots, uint64_t cells,
                              uint64_t ew, const float* __restrict__ vals,
                              uint64_t* __restrict__ out_slots, float* __restrict__ out_vals) {
+  zen_dev::pdl_entry();
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < cells;
        c += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned long long w = slots[c];
@@ -24,6 +25,7 @@ __global__ void k_dump_slots(const unsigned long long* __restrict__ slots, uint6
 
 __global__ void k_meta_depth(const uint32_t* __restrict__ meta, uint64_t count,
                              uint32_t* __restrict__ out) {
+  zen_dev::pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
        i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = meta_depth(meta[i]);
@@ -31,6 +33,7 @@ __global__ void k_meta_depth(const uint32_t* __restrict__ meta, uint64_t count,
 
 __global__ void k_universe_indices(const OwnWord* __restrict__ own, uint64_t nwords,
                                    uint64_t* __restrict__ out) {
+  zen_dev::pdl_entry();
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
        w += (uint64_t)gridDim.x * blockDim.x) {
     const OwnWord o = own[w];
@@ -46,6 +49,7 @@ __global__ void k_universe_indices(const OwnWord* __restrict__ own, uint64_t nwo
 
 __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
                              uint64_t n) {
+  zen_dev::pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = in[i];
@@ -55,6 +59,7 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restri
 // must be < M and owned by the server; the smallest offender is reported.
 __global__ void k_check_owned(const uint64_t* __restrict__ idx, uint64_t count, uint64_t m,
                               const OwnWord* __restrict__ own, HashHdr* hdr) {
+  zen_dev::pdl_entry();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t x = idx[i];
@@ -78,29 +83,29 @@ void launch_dump_slots(const unsigned long long* slots, uint64_t cells, uint32_t
                        const float* vals, uint64_t* out_slots, float* out_vals,
                        cudaStream_t stream) {
   const uint64_t ew = (uint64_t)(0xFFFFFFu - (epoch & 0xFFFFFFu)) << kKeyBits;
-  k_dump_slots<<<grid_for(cells), 256, 0, stream>>>(slots, cells, ew, vals, out_slots, out_vals);
+  launch_k(k_dump_slots, grid_for(cells), 256, 0, stream, slots, cells, ew, vals, out_slots, out_vals);
   count_launch();
 }
 
 void launch_meta_depth(const uint32_t* meta, uint64_t count, uint32_t* out, cudaStream_t stream) {
-  k_meta_depth<<<grid_for(count), 256, 0, stream>>>(meta, count, out);
+  launch_k(k_meta_depth, grid_for(count), 256, 0, stream, meta, count, out);
   count_launch();
 }
 
 void launch_universe_indices(const OwnWord* own, uint64_t nwords, uint64_t* out,
                              cudaStream_t stream) {
-  k_universe_indices<<<grid_for(nwords), 256, 0, stream>>>(own, nwords, out);
+  launch_k(k_universe_indices, grid_for(nwords), 256, 0, stream, own, nwords, out);
   count_launch();
 }
 
 void launch_check_owned(const uint64_t* idx, uint64_t count, uint64_t m, const OwnWord* own,
                         HashHdr* hdr, cudaStream_t stream) {
-  k_check_owned<<<grid_for(count), 256, 0, stream>>>(idx, count, m, own, hdr);
+  launch_k(k_check_owned, grid_for(count), 256, 0, stream, idx, count, m, own, hdr);
   count_launch();
 }
 
 void launch_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t stream) {
-  k_u32_to_u64<<<grid_for(n), 256, 0, stream>>>(in, out, n);
+  launch_k(k_u32_to_u64, grid_for(n), 256, 0, stream, in, out, n);
   count_launch();
 }
 

@@ -7,11 +7,27 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "zen_internal.h"
 
 namespace zen_dev {
+
+// ---- programmatic dependent launch (sm_90+) --------------------------------
+// Every kernel is launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// (launch_k below), so a kernel's CTAs become resident while its predecessor
+// drains and the launch latency between the ~20 dependent kernels of a sync
+// overlaps.  Correctness: pdl_entry() is the first statement of every kernel;
+// griddepcontrol.wait returns only once all prerequisite grids have completed
+// and their memory is visible, so no kernel touches global memory before its
+// predecessor is done.  launch_dependents lets the next grid start launching
+// as soon as every CTA of this grid is running.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 
 // ---- hash family: zen/hashing.hpp:18-39 -----------------------------------
 // mix64 is the splitmix64 finalizer; seeded_hash(x, s) = mix64(x + G*(s+1))
@@ -274,3 +290,31 @@ __device__ __forceinline__ f8 ld_stream_f8(const void* p) {
 }
 
 }  // namespace zen_dev
+
+namespace zen {
+// Launch policy of the calling host thread (capi.cpp): programmatic dependent
+// launch on/off and the CTA scheduling priority.  The BP side path (hash-memory
+// layout) launches with PDL off and the least priority so that it fills the
+// SMs the latency-bound critical path leaves idle instead of delaying it.
+bool launch_pdl();
+int launch_priority();
+
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = launch_pdl() ? 1 : 0;
+  at[1].id = cudaLaunchAttributePriority;
+  at[1].val.priority = launch_priority();
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+}  // namespace zen

@@ -99,6 +99,8 @@ struct ExtractWs {
   float* st_val;
   uint32_t* tile_cnt;
   uint64_t* tile_base;
+  uint32_t* blk_tile;  // [ceil(cap/256)+1]: tile holding output position 256*b
+  uint64_t nblk;       // compaction blocks the workspace was sized for
 };
 template <typename K>
 void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* out_idx,
@@ -114,10 +116,10 @@ void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws
 template <typename K>
 void launch_extract_scan_begin(uint64_t m, const ExtractWs<K>& ws, const HashArgs<K>& ha,
                                uint64_t capacity, cudaStream_t stream);
+// compaction fused with the data path's partition pass (replaces k_part)
 template <typename K>
-void launch_extract_compact_place(uint64_t m, const ExtractWs<K>& ws, K* out_idx, float* out_val,
-                                  uint64_t capacity, const DevFamily& fam, HashHdr* hdr,
-                                  unsigned long long* slots, bool place, cudaStream_t stream);
+void launch_extract_compact_part(uint64_t m, const ExtractWs<K>& ws, const HashArgs<K>& a,
+                                 uint32_t n, cudaStream_t stream);
 
 void launch_partition_of(const uint64_t* idx, uint64_t count, uint64_t pc, uint32_t n,
                          uint32_t* out, cudaStream_t stream);
@@ -166,7 +168,7 @@ void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stre
 template <typename K>
 void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream);
 template <typename K>
-void launch_hash_critical(const HashArgs<K>& a, uint32_t n, cudaStream_t stream);
+void launch_hash_critical(const HashArgs<K>& a, uint32_t n, bool part, cudaStream_t stream);
 template <typename K>
 void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream);
 
@@ -249,5 +251,13 @@ void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream);
 // small helpers
 void launch_u64_to_u32(const uint64_t* in, uint32_t* out, uint64_t n, cudaStream_t stream);
 void launch_fill_u64(unsigned long long* p, uint64_t n, uint64_t v, cudaStream_t stream);
+
+// RAII launch policy for the calling thread (see zen_common.cuh launch_k)
+struct LaunchScope {
+  LaunchScope(bool pdl, bool low_priority);
+  ~LaunchScope();
+  bool prev_pdl;
+  int prev_prio;
+};
 
 }  // namespace zen

@@ -813,6 +813,15 @@ class BPSynchronizer:
         """Replay dense syncs from a captured CUDA graph (needs a non-default stream)."""
         _check(_lib().zen_bp_use_graph(self.h, int(on)))
 
+    def time_extract(self, dense, iters: int = 50) -> float:
+        """Average ms of the extraction kernel alone (back-to-back launches on
+        the current stream) -- the roofline kernel's live launch duration."""
+        self.ctx.bind_stream()
+        ms = C.c_double()
+        _check(_lib().zen_bp_time_extract(self.h, C.c_void_p(dense.data_ptr()), iters,
+                                           C.byref(ms)))
+        return ms.value
+
     def kernels_per_sync(self) -> int:
         return int(_lib().zen_bp_kernels_per_sync(self.h))
 
