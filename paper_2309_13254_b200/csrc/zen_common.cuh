@@ -66,22 +66,53 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 // position of the (q+1)-th set bit of a 64-bit mask (q < popc(mask))
+// position of the q-th (0-based) set bit of mask (q < popc(mask)); branch-light
+// binary descent on popcounts (sm_100 has no native FNS; __fns is emulated)
 __device__ __forceinline__ uint32_t select64(uint64_t mask, uint32_t q) {
-  const uint32_t lo = (uint32_t)mask, hi = (uint32_t)(mask >> 32);
-  const uint32_t cl = __popc(lo);
-  if (q < cl) return __fns(lo, 0, (int)q + 1);
-  return 32 + __fns(hi, 0, (int)(q - cl) + 1);
-}
-// software pdep: deposit the low popc(mask) bits of src into mask's set bits,
-// iterating only over the set bits of src.
-__device__ __forceinline__ uint64_t deposit64(uint64_t src, uint64_t mask) {
-  uint64_t r = 0;
-  while (src) {
-    const uint32_t q = __ffsll((long long)src) - 1;
-    src &= src - 1;
-    r |= 1ull << select64(mask, q);
+  uint32_t pos = 0;
+  uint32_t c = __popc((uint32_t)mask);
+  uint32_t w = (uint32_t)mask;
+  if (q >= c) {
+    q -= c;
+    w = (uint32_t)(mask >> 32);
+    pos = 32;
   }
-  return r;
+  c = __popc(w & 0xFFFFu);
+  if (q >= c) { q -= c; w >>= 16; pos += 16; }
+  c = __popc(w & 0xFFu);
+  if (q >= c) { q -= c; w >>= 8; pos += 8; }
+  c = __popc(w & 0xFu);
+  if (q >= c) { q -= c; w >>= 4; pos += 4; }
+  c = __popc(w & 0x3u);
+  if (q >= c) { q -= c; w >>= 2; pos += 2; }
+  if (q >= (w & 1u)) pos += 1;
+  return pos;
+}
+// pdep: deposit the low popc(mask) bits of src into mask's set bits.  Full
+// slices (every owned bit present, e.g. whole embedding rows) take the fast
+// path; otherwise the uniform-cost "expand" of Hacker's Delight (7-5): six
+// parallel-suffix steps build the shift masks, six shifts move the bits.
+__device__ __forceinline__ uint64_t deposit64(uint64_t src, uint64_t mask) {
+  const uint32_t c = __popcll(mask);
+  if (src == (c == 64 ? ~0ull : ((1ull << c) - 1ull))) return mask;
+  uint64_t m = mask, mk = ~mask << 1, sh[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    uint64_t mp = mk ^ (mk << 1);
+    mp ^= mp << 2;
+    mp ^= mp << 4;
+    mp ^= mp << 8;
+    mp ^= mp << 16;
+    mp ^= mp << 32;
+    const uint64_t mv = mp & m;
+    sh[i] = mv;
+    m = (m ^ mv) | (mv >> (1 << i));
+    mk &= ~mp;
+  }
+  uint64_t x = src;
+#pragma unroll
+  for (int i = 5; i >= 0; --i) x = (x & ~sh[i]) | ((x << (1 << i)) & sh[i]);
+  return x & mask;
 }
 
 // ---- scans ------------------------------------------------------------------

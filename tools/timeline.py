@@ -31,24 +31,42 @@ def main():
     import bench
     import paper_2309_13254_b200 as zen
 
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:  # rank mode under torchrun: one worker per GPU
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        args.workers = world
     torch.cuda.set_stream(torch.cuda.Stream())
     n = args.workers
     per = int(np.ceil(args.density * args.rows))
     rows = bench.live_rows(args.rows, per, n, 0.5, 1.05, 1)
+    mine = [rank] if dist else list(range(n))
     dd = [torch.from_numpy(bench.dense_gradient(args.rows, args.width, rows[w], 1 + w)).cuda()
-          for w in range(n)]
+          for w in mine]
     m = args.rows * args.width
     z = per * args.width
-    bp = zen.BPSynchronizer(n, m, max_nnz=int(z * 1.25) + 4096, params=zen.HashParams(seed=1))
+    bp = zen.BPSynchronizer(n, m, max_nnz=int(z * 1.25) + 4096, params=zen.HashParams(seed=1),
+                            rank=rank if dist else None)
+    if dist:
+        bp.connect_process_group()
     for _ in range(10):
         bp.sync_dense(dd)
     bp.wait()
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
+    if dist:
+        dist.barrier()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(args.syncs):
             bp.sync_dense(dd)
         torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+        if args.out:
+            args.out = args.out.replace(".txt", f"_r{rank}.txt")
     tmp = tempfile.mktemp(suffix=".json")
     prof.export_chrome_trace(tmp)
     ev = json.load(open(tmp))["traceEvents"]
