@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
 // ------------------------------------------------------------- aggregate ----
 
 constexpr int kAggThreads = 256;
-constexpr int kWPT = kPrefixBlockWords / 256;  // consecutive words per thread (8)
+constexpr int kWPT = kPrefixBlockWords / 256;  // consecutive words per thread
 
 __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
   return a.in_hdr ? *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s] : (uint32_t)a.in_count[w];
@@ -194,13 +194,14 @@ __device__ __forceinline__ void store8(unsigned long long* p, const unsigned lon
   for (int i = 0; i < kWPT / 2; ++i) q[i] = make_ulonglong2(v[2 * i], v[2 * i + 1]);
 }
 __device__ __forceinline__ void store8u(uint32_t* p, const uint32_t (&v)[kWPT]) {
-  uint4* q = reinterpret_cast<uint4*>(p);  // 32 B, 32 B aligned
-  q[0] = make_uint4(v[0], v[1], v[2], v[3]);
-  q[1] = make_uint4(v[4], v[5], v[6], v[7]);
+  static_assert(kWPT % 2 == 0, "pairs of words per thread");
+  uint2* q = reinterpret_cast<uint2*>(p);  // 8 B aligned (kWPT even)
+#pragma unroll
+  for (int i = 0; i < kWPT / 2; ++i) q[i] = make_uint2(v[2 * i], v[2 * i + 1]);
 }
 
 // Phase 2: U = OR_w P_w -> every destination; block-local popcount prefixes of
-// U and each P_w (8 consecutive words per thread, 64-byte vector accesses; rows
+// U and each P_w (kWPT consecutive words per thread, vector accesses; rows
 // padded to 8 words); the last block turns the block totals into exclusive
 // prefixes and records U_s.
 __global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
@@ -451,77 +452,120 @@ __device__ __forceinline__ uint64_t bitmap_prefix(const DecodeArgs& a, uint32_t 
          a.bpre[s * a.words_stride + j] + (uint64_t)__popcll(a.bits[s][j] & lowmask64(o));
 }
 
-// One block per 256 global words.  The tile's first output position is the
-// number of set bits of all servers below the tile -- sum_s prefix_s(P_s(tile))
-// -- so no scan over tiles is needed.  Per word, each server's owned
-// positions are a contiguous bit range of its bitmap (deposited into the owner
-// mask); the warp then expands its set bits cooperatively.
+// One warp per 32-word chunk of the global index space (one word per lane),
+// warps fully independent.  Lane s first takes server s's slice of the chunk:
+// bits [cp_s, cpn_s) of its bitmap and the number of its set bits below them
+// (base_s, from the k_bpre prefixes).  A chunk whose slices are all empty
+// ends there (most chunks at embedding sparsity).  Otherwise, per word, each
+// server's owned positions are a contiguous bit range of its bitmap,
+// deposited into the owner mask; the value index of a word's first bit of
+// server s is base_s + (s's set bits in the chunk's earlier words), and its
+// first output position is sum_s base_s + (set bits of all servers in the
+// earlier words): both are warp scans, so no per-word prefix is read and no
+// block-wide scan is needed.  Servers go in groups of four, all loads of a
+// group issued before use, four counts packed per 64-bit scan.  Warps then
+// expand their set bits cooperatively (coalesced stores).
+constexpr int kDecGroup = 4;
+constexpr int kDecThreads = 128;
+
+__device__ __forceinline__ uint32_t field16(uint64_t v, int g) {
+  return (uint32_t)(v >> (16 * g)) & 0xFFFFu;
+}
+
 template <int NMAX>
-__global__ void __launch_bounds__(kDecodeTileWords) k_decode(DecodeArgs a, uint64_t nwords) {
+__global__ void __launch_bounds__(kDecThreads) k_decode(DecodeArgs a, uint64_t nwords) {
   zen_dev::pdl_entry();
-  __shared__ unsigned long long spres[kDecodeTileWords][NMAX];
-  __shared__ uint32_t svb[kDecodeTileWords][NMAX];
-  __shared__ uint32_t sscan[33];
-  __shared__ uint64_t s_tile_base;
-  const uint32_t n = a.n, lane = lane_id();
-  const uint32_t tile = blockIdx.x;
-  const uint64_t w = (uint64_t)tile * kDecodeTileWords + threadIdx.x;
+  __shared__ unsigned long long spres[kDecThreads][NMAX];
+  __shared__ uint32_t svb[kDecThreads][NMAX];
+  __shared__ unsigned long long spl[kDecThreads][4];
+  const uint32_t n = a.n, lane = lane_id(), np = a.nplanes;
+  const uint64_t w = (uint64_t)blockIdx.x * kDecThreads + threadIdx.x;
+  const uint64_t chunk = w >> 5;
+  const uint64_t nchunks = (nwords + 31) / 32;
+  if (chunk >= nchunks) return;  // warp-uniform
   const bool valid = w < nwords;
-  if (threadIdx.x < 32) {
-    uint64_t b = 0;
-    if (lane < n && a.bits[lane]) {
-      const uint64_t c0 = (uint64_t)tile * (kDecodeTileWords / 32);
-      b = bitmap_prefix(a, lane, a.cprefix[c0 * n + lane]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
-    if (lane == 0) s_tile_base = b;
+  // server `lane`'s slice of the chunk and its value base
+  uint64_t cp = 0, base = 0, end = 0;
+  if (lane < n && a.bits[lane]) {
+    cp = a.cprefix[chunk * n + lane];
+    const uint64_t cpn =
+        (chunk + 1 < nchunks) ? (uint64_t)a.cprefix[(chunk + 1) * n + lane] : a.bs[lane];
+    base = bitmap_prefix(a, lane, cp);
+    end = (cpn > cp) ? bitmap_prefix(a, lane, cpn) : base;
   }
+  if (!__any_sync(0xffffffffu, end > base)) return;
+  uint64_t ob = base;  // chunk's first output position = sum_s base_s
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ob += __shfl_xor_sync(0xffffffffu, ob, o);
   unsigned long long pl[4] = {0, 0, 0, 0};
   const uint64_t vmask = valid ? valid_mask(a.m, w) : 0ull;
   if (valid) {
 #pragma unroll
     for (uint32_t j = 0; j < 4; ++j)
-      if (j < a.nplanes) pl[j] = a.planes[w * a.nplanes + j];
+      if (j < np) pl[j] = a.planes[w * np + j];
   }
-  const uint64_t chunk = w >> 5;
+#pragma unroll
+  for (uint32_t j = 0; j < 4; ++j) spl[threadIdx.x][j] = pl[j];
   uint64_t G = 0;
 #pragma unroll
-  for (int s = 0; s < NMAX; ++s) {
-    unsigned long long pres = 0;
-    uint32_t vb = 0;
-    if (s < (int)n) {
-      const uint64_t ms = owner_mask4(pl, a.nplanes, (uint32_t)s, vmask);
-      const uint32_t c = __popcll(ms);
-      const uint32_t inc = warp_inclusive_sum(c);
-      const unsigned long long* bits = a.bits[s];
-      if (bits && c) {
-        const uint64_t P = (uint64_t)a.cprefix[chunk * n + s] + inc - c;
-        const uint64_t j = P >> 6;
-        const uint32_t o = (uint32_t)(P & 63);
-        const unsigned long long w0 = bits[j];
-        uint64_t xb = w0 >> o;
-        if (o + c > 64) xb |= (uint64_t)bits[j + 1] << (64 - o);
-        xb &= lowmask64(c);
-        if (xb) {
-          pres = (c == 64) ? xb : deposit64(xb, ms);
-          vb = a.bpre_blk[s * a.blk_stride + j / kPrefixBlockWords] +
-               a.bpre[s * a.words_stride + j] + (uint32_t)__popcll(w0 & lowmask64(o));
-          G |= pres;
-        }
+  for (int s0 = 0; s0 < NMAX; s0 += kDecGroup) {
+    uint64_t ms[kDecGroup];
+    uint32_t c[kDecGroup];
+    uint64_t packed = 0;
+#pragma unroll
+    for (int g = 0; g < kDecGroup; ++g) {
+      const uint32_t s = s0 + g;
+      ms[g] = (s < n) ? owner_mask4(pl, np, s, vmask) : 0ull;
+      c[g] = __popcll(ms[g]);
+      packed |= (uint64_t)c[g] << (16 * g);
+    }
+    const uint64_t incp = warp_inclusive_sum(packed);  // four 16-bit fields, no carries
+    uint64_t P[kDecGroup];
+    unsigned long long lo[kDecGroup], hi[kDecGroup];
+#pragma unroll
+    for (int g = 0; g < kDecGroup; ++g) {
+      const uint32_t s = s0 + g;
+      P[g] = __shfl_sync(0xffffffffu, cp, s & 31) + field16(incp, g) - c[g];
+      lo[g] = hi[g] = 0ull;
+      const unsigned long long* bits = (s < n) ? a.bits[s] : nullptr;
+      if (bits && c[g]) {
+        const uint64_t j = P[g] >> 6;
+        lo[g] = bits[j];
+        if ((P[g] & 63) + c[g] > 64) hi[g] = bits[j + 1];
       }
     }
-    spres[threadIdx.x][s] = pres;
-    svb[threadIdx.x][s] = vb;
+    uint64_t xb[kDecGroup];
+    uint64_t pk = 0;
+#pragma unroll
+    for (int g = 0; g < kDecGroup; ++g) {
+      const uint32_t o = (uint32_t)(P[g] & 63);
+      uint64_t x = lo[g] >> o;
+      if (o + c[g] > 64) x |= (uint64_t)hi[g] << (64 - o);
+      xb[g] = c[g] ? (x & lowmask64(c[g])) : 0ull;
+      pk |= (uint64_t)__popcll(xb[g]) << (16 * g);
+    }
+    const uint64_t incv = warp_inclusive_sum(pk);
+#pragma unroll
+    for (int g = 0; g < kDecGroup; ++g) {
+      const uint32_t s = s0 + g;
+      if (s >= NMAX) break;
+      const uint64_t bs_ = __shfl_sync(0xffffffffu, base, s & 31);
+      unsigned long long pres = 0;
+      if (xb[g]) {
+        pres = (c[g] == 64) ? xb[g] : deposit64(xb[g], ms[g]);
+        G |= pres;
+      }
+      spres[threadIdx.x][s] = pres;
+      svb[threadIdx.x][s] = (uint32_t)(bs_ + field16(incv, g) - field16(pk, g));
+    }
   }
+  __syncwarp();
   const uint32_t cnt = __popcll(G);
-  uint32_t tot;
-  const uint32_t bex = block_exclusive_sum(cnt, sscan, &tot);  // syncs: smem visible
   const uint32_t inc = warp_inclusive_sum(cnt);
   const uint32_t x = inc - cnt;
   const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
-  const uint64_t wbase = s_tile_base + __shfl_sync(0xffffffffu, bex - x, 0);
   const uint32_t row0 = threadIdx.x & ~31u;
+  const uint64_t wrow = (w & ~31ull);
   for (uint32_t k0 = 0; k0 < T; k0 += 32) {
     const uint32_t k = k0 + lane;
     uint32_t L = 0;
@@ -534,18 +578,15 @@ __global__ void __launch_bounds__(kDecodeTileWords) k_decode(DecodeArgs a, uint6
     const uint32_t xL = __shfl_sync(0xffffffffu, x, L);
     if (k < T) {
       const uint32_t bit = select64(GL, k - xL);
-      const uint64_t lm = lowmask64(bit);
-      float v = 0.0f;
+      uint32_t s = 0;  // owner of the bit, from the word's owner planes
 #pragma unroll
-      for (int s = 0; s < NMAX; ++s) {
-        if (s < (int)n) {
-          const unsigned long long p = spres[row0 + L][s];
-          if ((p >> bit) & 1ull) v = a.vals[s][svb[row0 + L][s] + __popcll(p & lm)];
-        }
-      }
-      const uint64_t pos = wbase + k;
+      for (uint32_t j = 0; j < 4; ++j)
+        if (j < np) s |= (uint32_t)((spl[row0 + L][j] >> bit) & 1ull) << j;
+      const unsigned long long p = spres[row0 + L][s];
+      const float v = a.vals[s][svb[row0 + L][s] + __popcll(p & lowmask64(bit))];
+      const uint64_t pos = ob + k;
       if (pos < a.out_cap) {
-        a.out_idx[pos] = ((uint64_t)tile * kDecodeTileWords + row0 + L) * 64 + bit;
+        a.out_idx[pos] = (wrow + L) * 64 + bit;
         a.out_val[pos] = v;
       }
     }
@@ -606,9 +647,9 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
 
 void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {
   const uint64_t nwords = (a.m + 63) / 64;
-  const uint32_t ntiles = (uint32_t)((nwords + kDecodeTileWords - 1) / kDecodeTileWords);
+  const uint32_t ntiles = (uint32_t)((nwords + kDecThreads - 1) / kDecThreads);
   launch_k(k_bpre, a.total_blocks ? a.total_blocks : 1, 256, 0, stream, a);
-  constexpr unsigned T = kDecodeTileWords;
+  constexpr unsigned T = kDecThreads;
   if (a.n <= 2)
     launch_k(k_decode<2>, ntiles, T, 0, stream, a, nwords);
   else if (a.n <= 4)
