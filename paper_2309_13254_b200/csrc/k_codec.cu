@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
 // ------------------------------------------------------------- aggregate ----
 
 constexpr int kAggThreads = 256;
-constexpr int kWPT = kPrefixBlockWords / 256;  // consecutive words per thread
+constexpr int kPrefixThreads = 1024;  // union / bpre blocks
+constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (2)
 
 __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
   return a.in_hdr ? *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s] : (uint32_t)a.in_count[w];
@@ -201,13 +202,14 @@ __device__ __forceinline__ void store8u(uint32_t* p, const uint32_t (&v)[kWPT]) 
 }
 
 // Phase 2: U = OR_w P_w -> every destination; block-local popcount prefixes of
-// U and each P_w (kWPT consecutive words per thread, vector accesses; rows
+// U and each P_w (1024 threads x kWPT consecutive words, vector accesses; rows
 // padded to 8 words); the last block turns the block totals into exclusive
 // prefixes and records U_s.
-__global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
+__global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
   zen_dev::pdl_entry();
-  __shared__ uint32_t wsum[kMaxWorkers + 1][kAggThreads / 32];
-  __shared__ uint32_t inw[kMaxWorkers + 1][kAggThreads];
+  constexpr int kW = kPrefixThreads / 32;
+  __shared__ uint32_t wsum[kMaxWorkers + 1][kW];
+  __shared__ uint32_t wtot[kMaxWorkers + 1];
   __shared__ uint32_t s_last;
   const uint32_t n = a.n, lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t j0 = (uint64_t)blockIdx.x * kPrefixBlockWords + (uint64_t)threadIdx.x * kWPT;
@@ -215,7 +217,10 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
   unsigned long long U[kWPT];
 #pragma unroll
   for (int i = 0; i < kWPT; ++i) U[i] = 0;
-  for (uint32_t x = 0; x <= n; ++x) {
+  uint32_t inw[kMaxWorkers + 1];  // in-warp exclusive prefix per bitmap
+#pragma unroll
+  for (uint32_t x = 0; x <= kMaxWorkers; ++x) {
+    if (x > n) break;
     unsigned long long v[kWPT];
     if (x < n) {
       if (live) load8(a.pw + (uint64_t)x * a.nws + j0, v);
@@ -233,29 +238,32 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
     for (int i = 0; i < kWPT; ++i) t += __popcll(v[i]);
     const uint32_t inc = warp_inclusive_sum(t);
     if (lane == 31) wsum[x][warp] = inc;
-    inw[x][threadIdx.x] = inc - t;
+    inw[x] = inc - t;
   }
   // the union bitmap (the HashBitmap: LSB-first = little-endian words)
   if (live)
     for (uint32_t d = 0; d < a.ndst; ++d) store8(a.dst_bits[d] + j0, U);
   __syncthreads();
-  for (uint32_t x = 0; x <= n; ++x) {
-    uint32_t wpre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kAggThreads / 32; ++w) {
-      const uint32_t v = wsum[x][w];
-      wpre += (w < (int)warp) ? v : 0u;
-      tot += v;
+  if (warp <= n) {  // warp x: exclusive prefix over the block's warps of bitmap x
+    const uint32_t v = wsum[warp][lane];
+    const uint32_t inc = warp_inclusive_sum(v);
+    wsum[warp][lane] = inc - v;
+    if (lane == 31) {
+      wtot[warp] = inc;
+      a.blk[(uint64_t)warp * a.nblk + blockIdx.x] = inc;
     }
-    if (threadIdx.x == 0) a.blk[(uint64_t)x * a.nblk + blockIdx.x] = tot;
-    if (!live) continue;
+  }
+  __syncthreads();
+#pragma unroll
+  for (uint32_t x = 0; x <= kMaxWorkers; ++x) {
+    if (x > n || !live) break;
     unsigned long long v[kWPT];
     if (x < n) load8(a.pw + (uint64_t)x * a.nws + j0, v);  // L1/L2 hit
     else
 #pragma unroll
       for (int i = 0; i < kWPT; ++i) v[i] = U[i];
     uint32_t pre[kWPT];
-    uint32_t run = wpre + inw[x][threadIdx.x];
+    uint32_t run = wsum[x][warp] + inw[x];
 #pragma unroll
     for (int i = 0; i < kWPT; ++i) {
       pre[i] = run;
@@ -272,12 +280,13 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_union(AggArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (uint32_t x = warp; x <= n; x += kAggThreads / 32) {
+  for (uint32_t x = warp; x <= n; x += kW) {
     const uint32_t total = warp_exscan_l2(a.blk + (uint64_t)x * a.nblk, a.nblk);
     if (x == n && lane == 0) *a.agg_count = total;
   }
   __syncthreads();
   if (threadIdx.x == 0) a.done[0] = 0;
+  (void)wtot;
 }
 
 // Phase 3: one thread per bitmap word stages its words in shared memory; the
@@ -381,7 +390,7 @@ __global__ void k_agg_signal(AggArgs a) {
 // Word popcount prefix of each server's bitmap: block-local (2048 words per
 // block, 8 consecutive words per thread) + block totals; the last block turns
 // the totals into exclusive prefixes, per-server popcounts and |result|.
-__global__ void __launch_bounds__(256) k_bpre(DecodeArgs a) {
+__global__ void __launch_bounds__(kPrefixThreads) k_bpre(DecodeArgs a) {
   zen_dev::pdl_entry();
   __shared__ uint32_t sscan[33];
   __shared__ uint32_t s_last;
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(256) k_bpre(DecodeArgs a) {
   __threadfence();
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   __shared__ uint64_t totals[kMaxWorkers];
-  for (uint32_t x = warp; x < n; x += 8) {
+  for (uint32_t x = warp; x < n; x += kPrefixThreads / 32) {
     const uint32_t nb = a.blk_start[x + 1] - a.blk_start[x];
     const uint32_t total = warp_exscan_l2(a.bpre_blk + x * a.blk_stride, nb);
     if (lane == 0) {
@@ -628,7 +637,7 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
 void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
   // a.pw is all-zero here: zeroed at allocation, re-zeroed by k_agg_values
   launch_k(k_agg_mark, 148 * 8, kAggThreads, 0, stream, a);
-  launch_k(k_agg_union, a.nblk, kAggThreads, 0, stream, a);
+  launch_k(k_agg_union, a.nblk, kPrefixThreads, 0, stream, a);
   const unsigned g = (unsigned)((a.nw + kValThreads - 1) / kValThreads);
   if (a.n <= 2)
     launch_k(k_agg_values<2>, g, kValThreads, 0, stream, a);
@@ -648,7 +657,7 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
 void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {
   const uint64_t nwords = (a.m + 63) / 64;
   const uint32_t ntiles = (uint32_t)((nwords + kDecThreads - 1) / kDecThreads);
-  launch_k(k_bpre, a.total_blocks ? a.total_blocks : 1, 256, 0, stream, a);
+  launch_k(k_bpre, a.total_blocks ? a.total_blocks : 1, kPrefixThreads, 0, stream, a);
   constexpr unsigned T = kDecThreads;
   if (a.n <= 2)
     launch_k(k_decode<2>, ntiles, T, 0, stream, a, nwords);
