@@ -1253,14 +1253,15 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
       launch_extract_compact_part<uint32_t>(bp->m, w.ex, w.a, bp->n, st);
     } else {
       launch_hash_begin<uint32_t>(w.a, st);
+      launch_hash_part<uint32_t>(w.a, bp->n, st);  // the side path reads its partitions
     }
     CK(cudaEventRecord(bp->fork, st));
     CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
     {
       LaunchScope low(/*pdl=*/false, /*low_priority=*/true);
-      launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side);
+      launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side, /*ctas_per_sm=*/2);
     }
-    launch_hash_critical<uint32_t>(w.a, bp->n, /*part=*/!from_dense, st);
+    launch_hash_critical<uint32_t>(w.a, bp->n, /*part=*/false, st);
   }
   if (ev) CK(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
   for (auto& s : bp->servers) launch_aggregate(s.a, st);

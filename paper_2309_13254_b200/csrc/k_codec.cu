@@ -125,8 +125,8 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
 // ------------------------------------------------------------- aggregate ----
 
 constexpr int kAggThreads = 256;
-constexpr int kPrefixThreads = 1024;  // union / bpre blocks
-constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (2)
+constexpr int kPrefixThreads = 512;  // union / bpre blocks
+constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (4)
 
 __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
   return a.in_hdr ? *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s] : (uint32_t)a.in_count[w];
@@ -154,14 +154,20 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
   }
   __syncthreads();
   const uint64_t total = pre[n];
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-       i += (uint64_t)gridDim.x * blockDim.x) {
+  const uint32_t lane = lane_id();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < total;
+       base += stride) {  // warp-uniform trip count: full-mask shuffles below
+    const uint64_t i = base + lane;
+    const bool in = i < total;
     uint32_t w = 0;
-    while (i >= pre[w + 1]) ++w;
-    const uint32_t key = a.in_idx[w][i - pre[w]];
-    const OwnWord ow = a.own[key >> 6];
-    const bool owned = (ow.mask >> (key & 63u)) & 1ull;
-    if (!owned) {
+    if (in)
+      while (i >= pre[w + 1]) ++w;
+    const uint64_t e = in ? i - pre[w] : 0;  // index inside worker w's part
+    const uint32_t key = in ? a.in_idx[w][e] : 0u;
+    const OwnWord ow = a.own[in ? key >> 6 : 0];
+    const bool owned = in && ((ow.mask >> (key & 63u)) & 1ull);
+    if (in && !owned) {
       atomicMin((unsigned long long*)&a.hdr->bad_index, (unsigned long long)key);
       atomicOr(&a.hdr->status, kErrOutside);
     }
@@ -169,11 +175,25 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
     // consecutive keys share bitmap words: one atomic per distinct word per warp
     unsigned long long* word = owned ? a.pw + (uint64_t)w * a.nws + (r >> 6) : nullptr;
     const uint64_t bit = owned ? 1ull << (r & 63u) : 0ull;
-    const uint32_t grp = __match_any_sync(__activemask(), (unsigned long long)word);
+    const uint32_t grp = __match_any_sync(0xffffffffu, (unsigned long long)word);
     const uint32_t lo = __reduce_or_sync(grp, (uint32_t)bit);
     const uint32_t hi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
-    if (owned && lane_id() == (uint32_t)(__ffs(grp) - 1))
+    if (owned && lane == (uint32_t)(__ffs(grp) - 1))
       atomicOr(word, ((unsigned long long)hi << 32) | lo);
+    // The part is ascending, so its entries in bitmap word j are consecutive:
+    // the first of them is at part index = worker w's popcount prefix at j,
+    // which the fold needs -- written here instead of scanned later.
+    const uint32_t jw = owned ? (r >> 6) : 0xFFFFFFFFu;
+    uint32_t prev_w = __shfl_up_sync(0xffffffffu, w, 1);
+    uint32_t prev_j = __shfl_up_sync(0xffffffffu, jw, 1);
+    if (in && owned && (lane == 0 || prev_w != w) && e > 0) {
+      const uint32_t pk = a.in_idx[w][e - 1];  // previous entry of the same part
+      const OwnWord po = a.own[pk >> 6];
+      prev_w = w;
+      prev_j = (po.prefix + (uint32_t)__popcll(po.mask & lowmask64(pk & 63u))) >> 6;
+    }
+    if (owned && (e == 0 || prev_w != w || prev_j != jw))
+      a.pre[(uint64_t)w * a.nws + jw] = (uint32_t)e;
   }
 }
 
@@ -201,15 +221,14 @@ __device__ __forceinline__ void store8u(uint32_t* p, const uint32_t (&v)[kWPT]) 
   for (int i = 0; i < kWPT / 2; ++i) q[i] = make_uint2(v[2 * i], v[2 * i + 1]);
 }
 
-// Phase 2: U = OR_w P_w -> every destination; block-local popcount prefixes of
-// U and each P_w (1024 threads x kWPT consecutive words, vector accesses; rows
-// padded to 8 words); the last block turns the block totals into exclusive
-// prefixes and records U_s.
+// Phase 2: U = OR_w P_w -> every destination, and the popcount prefix of U
+// (block-local per word + block totals; the last block turns the totals into
+// exclusive prefixes and records U_s).  Workers' own prefixes come from
+// k_agg_mark, so only U is scanned.
 __global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
   zen_dev::pdl_entry();
   constexpr int kW = kPrefixThreads / 32;
-  __shared__ uint32_t wsum[kMaxWorkers + 1][kW];
-  __shared__ uint32_t wtot[kMaxWorkers + 1];
+  __shared__ uint32_t wsum[kW];
   __shared__ uint32_t s_last;
   const uint32_t n = a.n, lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t j0 = (uint64_t)blockIdx.x * kPrefixBlockWords + (uint64_t)threadIdx.x * kWPT;
@@ -217,61 +236,40 @@ __global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
   unsigned long long U[kWPT];
 #pragma unroll
   for (int i = 0; i < kWPT; ++i) U[i] = 0;
-  uint32_t inw[kMaxWorkers + 1];  // in-warp exclusive prefix per bitmap
-#pragma unroll
-  for (uint32_t x = 0; x <= kMaxWorkers; ++x) {
-    if (x > n) break;
-    unsigned long long v[kWPT];
-    if (x < n) {
-      if (live) load8(a.pw + (uint64_t)x * a.nws + j0, v);
-      else
-#pragma unroll
-        for (int i = 0; i < kWPT; ++i) v[i] = 0;
+  if (live) {
+    for (uint32_t x = 0; x < n; ++x) {
+      unsigned long long v[kWPT];
+      load8(a.pw + (uint64_t)x * a.nws + j0, v);
 #pragma unroll
       for (int i = 0; i < kWPT; ++i) U[i] |= v[i];
-    } else {
-#pragma unroll
-      for (int i = 0; i < kWPT; ++i) v[i] = U[i];
     }
-    uint32_t t = 0;
-#pragma unroll
-    for (int i = 0; i < kWPT; ++i) t += __popcll(v[i]);
-    const uint32_t inc = warp_inclusive_sum(t);
-    if (lane == 31) wsum[x][warp] = inc;
-    inw[x] = inc - t;
-  }
-  // the union bitmap (the HashBitmap: LSB-first = little-endian words)
-  if (live)
+    // the union bitmap (the HashBitmap: LSB-first = little-endian words)
     for (uint32_t d = 0; d < a.ndst; ++d) store8(a.dst_bits[d] + j0, U);
+  }
+  uint32_t t = 0;
+#pragma unroll
+  for (int i = 0; i < kWPT; ++i) t += __popcll(U[i]);
+  const uint32_t inc = warp_inclusive_sum(t);
+  if (lane == 31) wsum[warp] = inc;
   __syncthreads();
-  if (warp <= n) {  // warp x: exclusive prefix over the block's warps of bitmap x
-    const uint32_t v = wsum[warp][lane];
-    const uint32_t inc = warp_inclusive_sum(v);
-    wsum[warp][lane] = inc - v;
-    if (lane == 31) {
-      wtot[warp] = inc;
-      a.blk[(uint64_t)warp * a.nblk + blockIdx.x] = inc;
-    }
+  if (warp == 0) {  // exclusive prefix over the block's warps
+    const uint32_t v = lane < (uint32_t)kW ? wsum[lane] : 0u;
+    const uint32_t wi = warp_inclusive_sum(v);
+    if (lane < (uint32_t)kW) wsum[lane] = wi - v;
+    if (lane == 31) a.blk[(uint64_t)n * a.nblk + blockIdx.x] = wi;
   }
   __syncthreads();
-#pragma unroll
-  for (uint32_t x = 0; x <= kMaxWorkers; ++x) {
-    if (x > n || !live) break;
-    unsigned long long v[kWPT];
-    if (x < n) load8(a.pw + (uint64_t)x * a.nws + j0, v);  // L1/L2 hit
-    else
-#pragma unroll
-      for (int i = 0; i < kWPT; ++i) v[i] = U[i];
+  if (live) {
     uint32_t pre[kWPT];
-    uint32_t run = wsum[x][warp] + inw[x];
+    uint32_t run = wsum[warp] + inc - t;
 #pragma unroll
     for (int i = 0; i < kWPT; ++i) {
       pre[i] = run;
-      run += __popcll(v[i]);
+      run += __popcll(U[i]);
     }
-    store8u(a.pre + (uint64_t)x * a.nws + j0, pre);
+    store8u(a.pre + (uint64_t)n * a.nws + j0, pre);
   }
-  // last block: exclusive prefix of the block totals (one warp per bitmap)
+  // last block: exclusive prefix of the block totals, |U_s|
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -280,13 +278,13 @@ __global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (uint32_t x = warp; x <= n; x += kW) {
-    const uint32_t total = warp_exscan_l2(a.blk + (uint64_t)x * a.nblk, a.nblk);
-    if (x == n && lane == 0) *a.agg_count = total;
+  if (warp == 0) {
+    const uint32_t total = warp_exscan_l2(a.blk + (uint64_t)n * a.nblk, a.nblk);
+    if (lane == 0) {
+      *a.agg_count = total;
+      a.done[0] = 0;
+    }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) a.done[0] = 0;
-  (void)wtot;
 }
 
 // Phase 3: one thread per bitmap word stages its words in shared memory; the
@@ -312,7 +310,7 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
     if (w < (int)n && valid) {
       v = a.pw[(uint64_t)w * a.nws + j];
       if (v) {
-        b = a.blk[(uint64_t)w * a.nblk + pb] + a.pre[(uint64_t)w * a.nws + j];
+        b = a.pre[(uint64_t)w * a.nws + j];  // part index of the word's first entry (k_agg_mark)
         a.pw[(uint64_t)w * a.nws + j] = 0ull;  // last reader: clean for the next sync
       }
     }
@@ -342,7 +340,7 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
     const unsigned long long UL = __shfl_sync(0xffffffffu, U, L);
     const uint32_t xL = __shfl_sync(0xffffffffu, x, L);
     if (k < T) {
-      const uint32_t bit = select64(UL, k - xL);
+      const uint32_t bit = (UL == ~0ull) ? k - xL : select64(UL, k - xL);
       const uint64_t lm = lowmask64(bit);
       float v = 0.0f;
       bool seen = false;
@@ -474,7 +472,6 @@ __device__ __forceinline__ uint64_t bitmap_prefix(const DecodeArgs& a, uint32_t 
 // block-wide scan is needed.  Servers go in groups of four, all loads of a
 // group issued before use, four counts packed per 64-bit scan.  Warps then
 // expand their set bits cooperatively (coalesced stores).
-constexpr int kDecGroup = 4;
 constexpr int kDecThreads = 128;
 
 __device__ __forceinline__ uint32_t field16(uint64_t v, int g) {
@@ -484,6 +481,7 @@ __device__ __forceinline__ uint32_t field16(uint64_t v, int g) {
 template <int NMAX>
 __global__ void __launch_bounds__(kDecThreads) k_decode(DecodeArgs a, uint64_t nwords) {
   zen_dev::pdl_entry();
+  constexpr int kDecGroup = NMAX < 4 ? NMAX : 4;  // servers per packed scan
   __shared__ unsigned long long spres[kDecThreads][NMAX];
   __shared__ uint32_t svb[kDecThreads][NMAX];
   __shared__ unsigned long long spl[kDecThreads][4];
@@ -586,7 +584,7 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecodeArgs a, uint64_t n
     const unsigned long long GL = __shfl_sync(0xffffffffu, G, L);
     const uint32_t xL = __shfl_sync(0xffffffffu, x, L);
     if (k < T) {
-      const uint32_t bit = select64(GL, k - xL);
+      const uint32_t bit = (GL == ~0ull) ? k - xL : select64(GL, k - xL);  // full rows: direct
       uint32_t s = 0;  // owner of the bit, from the word's owner planes
 #pragma unroll
       for (uint32_t j = 0; j < 4; ++j)

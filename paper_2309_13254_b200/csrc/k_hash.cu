@@ -207,9 +207,21 @@ __global__ void __launch_bounds__(kThreads) k_place(HashArgs<K> a) {
   if (h->status & kErrCapacity) return;
   const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
   const uint64_t ew = epoch_word(h->epoch);
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < z;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    place_key(a.fam, a.slots, (uint64_t)a.idx[i] + 1, r1, stride, ew);
+  constexpr int KPT = 4;  // claims in flight per thread
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < z; i0 += nthr * KPT) {
+    uint64_t key[KPT];
+    uint32_t part[KPT];
+    uint32_t nv = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const uint64_t i = i0 + (uint64_t)j * nthr;
+      key[j] = i < z ? (uint64_t)a.idx[i] + 1 : 0ull;
+      part[j] = i < z ? (a.pmeta[i] & 0xFFFFu) : 0u;  // h0 from the data path's pass
+      nv += i < z ? 1u : 0u;
+    }
+    place_keys<KPT>(a.fam, a.slots, key, part, nv, r1, stride, ew);
+  }
 }
 
 template <typename K>
@@ -233,16 +245,32 @@ __global__ void __launch_bounds__(kThreads) k_depth(HashArgs<K> a) {
     uint32_t p = kInvalid, depth = 0;
     if (valid) {
       const uint64_t key = (uint64_t)a.idx[i] + 1;
-      p = part_of(a.fam, key);
+      p = a.pmeta[i] & 0xFFFFu;  // h0 from the data path's partition pass
       const uint64_t base = (uint64_t)p * stride;
-      for (uint32_t t = 0; t < k; ++t) {
+      // the first four candidates are loaded together (k = 3 by default)
+      uint64_t c4[4];
+      unsigned long long s4[4];
+#pragma unroll
+      for (uint32_t t = 0; t < 4; ++t)
+        if (t < k) {
+          c4[t] = slot_of(a.fam, key, t, r1);
+          s4[t] = a.slots[base + c4[t]];
+        }
+      uint64_t hit = ~0ull;
+#pragma unroll
+      for (uint32_t t = 0; t < 4; ++t)
+        if (t < k && depth == 0 && s4[t] == (ew | key)) {
+          depth = t + 1;
+          hit = c4[t];
+        }
+      for (uint32_t t = 4; depth == 0 && t < k; ++t) {
         const uint64_t c = slot_of(a.fam, key, t, r1);
         if (a.slots[base + c] == (ew | key)) {
           depth = t + 1;
-          if (a.slot_vals) a.slot_vals[base + c] = a.val[i];
-          break;
+          hit = c;
         }
       }
+      if (depth && a.slot_vals) a.slot_vals[base + hit] = a.val[i];
     }
     __syncthreads();
     const uint32_t ks = (valid && depth == 0) ? p : kInvalid;
@@ -433,6 +461,13 @@ void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream) {
 }
 
 template <typename K>
+void launch_hash_part(const HashArgs<K>& a, uint32_t n, cudaStream_t stream) {
+  const unsigned tiles = (unsigned)std::max<uint64_t>(a.tiles_cap, 1);
+  launch_k(k_part<K>, tiles, kThreads, kWarps * n * sizeof(uint32_t), stream, a);
+  count_launch();
+}
+
+template <typename K>
 void launch_hash_critical(const HashArgs<K>& a, uint32_t n, bool part, cudaStream_t stream) {
   const unsigned tiles = (unsigned)std::max<uint64_t>(a.tiles_cap, 1);
   if (part) {  // else fused into the compaction (k_extract_compact_part)
@@ -449,13 +484,14 @@ void launch_hash_critical(const HashArgs<K>& a, uint32_t n, bool part, cudaStrea
 }
 
 template <typename K>
-void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream) {
+void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream,
+                      unsigned ctas_per_sm) {
   const unsigned tiles = (unsigned)std::max<uint64_t>(a.tiles_cap, 1);
-  // grids capped at 2 CTAs per SM: the side path must not crowd out the
-  // critical path's kernels (it runs at the least priority, PDL off)
-  const unsigned side = std::min<unsigned>(tiles, 148 * 2);
+  // concurrent with the critical path the grids are capped (2 CTAs per SM) so
+  // the side path does not crowd out the critical path's kernels
+  const unsigned side = std::min<unsigned>(tiles, 148 * ctas_per_sm);
   if (place) {
-    launch_k(k_place<K>, grid_for(a.cap, kThreads, 148 * 2), kThreads, 0, stream, a);
+    launch_k(k_place<K>, grid_for(a.cap, kThreads, 148 * ctas_per_sm), kThreads, 0, stream, a);
     count_launch();
   }
   launch_k(k_depth<K>, side, kThreads, kWarps * n * sizeof(uint32_t), stream, a);
@@ -469,15 +505,16 @@ template <typename K>
 void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
   launch_hash_begin<K>(a, stream);
   launch_hash_critical<K>(a, n, true, stream);
-  launch_hash_side<K>(a, n, true, stream);
+  launch_hash_side<K>(a, n, true, stream, 16);
   (void)k;
 }
 
 #define ZEN_INST(K)                                                                         \
   template void launch_hash<K>(const HashArgs<K>&, uint32_t, uint32_t, cudaStream_t);       \
   template void launch_hash_begin<K>(const HashArgs<K>&, cudaStream_t);                     \
+  template void launch_hash_part<K>(const HashArgs<K>&, uint32_t, cudaStream_t);            \
   template void launch_hash_critical<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t);        \
-  template void launch_hash_side<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t);
+  template void launch_hash_side<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t, unsigned);
 ZEN_INST(uint32_t)
 ZEN_INST(uint64_t)
 #undef ZEN_INST

@@ -43,16 +43,27 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
+// map_to_range for r < 2^32: (h * r) >> 64 = (h_hi * r + ((h_lo * r) >> 32)) >> 32
+// exactly -- two 32x32->64 multiplies instead of a full 64-bit mul-hi.
+__device__ __forceinline__ uint64_t map_to_range32(uint64_t h, uint32_t r) {
+  const uint64_t lo = (uint64_t)(uint32_t)h * r;
+  const uint64_t hi = (h >> 32) * (uint64_t)r;
+  return (hi + (lo >> 32)) >> 32;
+}
+__device__ __forceinline__ uint64_t map_to_range(uint64_t h, uint64_t r) {
+  return (r >> 32) ? __umul64hi(h, r) : map_to_range32(h, (uint32_t)r);
+}
+
 // key = index + 1 (zen/hashing.hpp:44-45, :73-76, :79-81)
 __device__ __forceinline__ uint32_t part_of(const zen::DevFamily& f, uint64_t key) {
-  return (uint32_t)__umul64hi(mix64(key + f.pc), (uint64_t)f.n);
+  return (uint32_t)map_to_range32(mix64(key + f.pc), f.n);
 }
 __device__ __forceinline__ uint64_t slot_of(const zen::DevFamily& f, uint64_t key, uint32_t t,
                                             uint64_t r1) {  // t is 0-based (round t+1)
-  return __umul64hi(mix64(key + f.sc[t]), r1);
+  return map_to_range(mix64(key + f.sc[t]), r1);
 }
 __device__ __forceinline__ uint32_t part_of_seed(uint64_t pc, uint32_t n, uint64_t key) {
-  return (uint32_t)__umul64hi(mix64(key + pc), (uint64_t)n);
+  return (uint32_t)map_to_range32(mix64(key + pc), n);
 }
 
 // ---- bit helpers ------------------------------------------------------------

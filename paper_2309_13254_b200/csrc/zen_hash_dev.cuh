@@ -39,6 +39,61 @@ __device__ __forceinline__ void place_key(const zen::DevFamily& fam, unsigned lo
   }
 }
 
+// KPT independent claims per thread, interleaved: every round issues the
+// pending atomicMin of each unfinished key before consuming any result, so a
+// thread keeps KPT L2 atomics in flight instead of one (same protocol and
+// outcome as place_key: the stable matching does not depend on the schedule).
+template <int KPT>
+__device__ __forceinline__ void place_keys(const zen::DevFamily& fam, unsigned long long* slots,
+                                           const uint64_t (&key)[KPT], const uint32_t (&part)[KPT],
+                                           uint32_t nvalid, uint64_t r1, uint64_t stride,
+                                           uint64_t ew) {
+  unsigned long long* base[KPT];
+  uint64_t cur[KPT];
+  uint32_t t[KPT];
+  bool act[KPT];
+  const uint32_t k = fam.k;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    act[j] = (uint32_t)j < nvalid;
+    cur[j] = key[j];
+    t[j] = 0;
+    base[j] = slots + (act[j] ? (uint64_t)part[j] * stride : 0ull);
+  }
+  bool any = nvalid > 0;
+  while (any) {
+    uint64_t c[KPT];
+    unsigned long long old[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      if (act[j]) {
+        c[j] = slot_of(fam, cur[j], t[j], r1);
+        old[j] = atomicMin(base[j] + c[j], (unsigned long long)(ew | cur[j]));
+      }
+    }
+    any = false;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      if (!act[j]) continue;
+      if (old[j] > (ew | zen::kKeyMask)) {  // empty or stale epoch: cur holds c
+        act[j] = false;
+        continue;
+      }
+      const uint64_t ok = old[j] & zen::kKeyMask;
+      if (ok > cur[j]) {  // displaced a larger key: it resumes after its first c
+        cur[j] = ok;
+        uint32_t f = 0;
+        while (f < k && slot_of(fam, ok, f, r1) != c[j]) ++f;
+        t[j] = f + 1;
+      } else {
+        ++t[j];
+      }
+      if (t[j] >= k) act[j] = false;  // ends serial
+      any |= act[j];
+    }
+  }
+}
+
 // meta word of a key after the post pass: partition (9 bits), depth (5),
 // stable rank in its 256-key tile among same-partition keys (8) and among
 // same-partition serial keys (8).

@@ -14,7 +14,7 @@ constexpr uint32_t kMaxWorkers = 16;    // n for the fused BP pipeline
 constexpr uint32_t kHashTile = 256;     // keys per hash tile (one per thread)
 constexpr uint32_t kExtractTile = 8192; // floats per extraction tile
 constexpr uint32_t kDecodeTileWords = 128;  // 64-index words per decode tile (= block size)
-constexpr uint32_t kPrefixBlockWords = 2048;  // bitmap words per popcount-prefix block (1024 threads x 2)
+constexpr uint32_t kPrefixBlockWords = 2048;  // bitmap words per popcount-prefix block (512 threads x 4)
                                               // (256 threads x 8 consecutive words)
 constexpr uint64_t kKeyBits = 40;       // slot word: [63:40] epoch, [39:0] index+1
 constexpr uint64_t kKeyMask = (1ull << kKeyBits) - 1ull;
@@ -168,9 +168,15 @@ void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stre
 template <typename K>
 void launch_hash_begin(const HashArgs<K>& a, cudaStream_t stream);
 template <typename K>
+void launch_hash_part(const HashArgs<K>& a, uint32_t n, cudaStream_t stream);
+// part: run k_part first (else the partition pass already ran: compaction or
+// launch_hash_part).  The side path reads k_part's partitions (pmeta).
+template <typename K>
 void launch_hash_critical(const HashArgs<K>& a, uint32_t n, bool part, cudaStream_t stream);
 template <typename K>
-void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream);
+void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream,
+                      unsigned ctas_per_sm);
+
 
 // universe tables (HashUniverseTable, zen/codec.hpp:47-72) as bit planes
 void launch_tables_planes(uint64_t m, uint32_t n, uint64_t pc, uint32_t nplanes,
