@@ -138,12 +138,6 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
   zen_dev::pdl_entry();
   __shared__ uint64_t pre[kMaxWorkers + 1];
   const uint32_t n = a.n;
-  if (a.wait_push && threadIdx.x < n) {
-    const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
-    if (!wait_flag(&a.in_hdr[threadIdx.x]->flag, iter, kPeerTimeoutNs))
-      atomicOr(&a.hdr->status, kErrTimeout);
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
     uint64_t acc = 0;
     for (uint32_t w = 0; w < n; ++w) {
@@ -383,6 +377,18 @@ __global__ void k_agg_signal(AggArgs a) {
     st_release_sys(&a.dst_hdr[d]->flag, (unsigned long long)iter);
 }
 
+// Rank mode: ONE warp waits for the n peers' flags (lane w polls flag w), so
+// the heavy kernels behind it (launched early by PDL) never poll: a grid of
+// CTAs spinning on the same lines with system-scope acquires slows the NVLink
+// stores they wait for.
+__global__ void k_wait_push(AggArgs a) {
+  zen_dev::pdl_entry();
+  const uint32_t w = threadIdx.x;
+  if (w >= a.n) return;
+  const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
+  if (!wait_flag(&a.in_hdr[w]->flag, iter, kPeerTimeoutNs)) atomicOr(&a.hdr->status, kErrTimeout);
+}
+
 // ---------------------------------------------------------------- decode ----
 
 // Word popcount prefix of each server's bitmap: block-local (2048 words per
@@ -393,13 +399,6 @@ __global__ void __launch_bounds__(kPrefixThreads) k_bpre(DecodeArgs a) {
   __shared__ uint32_t sscan[33];
   __shared__ uint32_t s_last;
   const uint32_t n = a.n;
-  if (a.wait_pull && threadIdx.x < n) {
-    const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
-    if (a.bits[threadIdx.x] &&
-        !wait_flag(&a.pull_hdr[threadIdx.x]->flag, iter, kPeerTimeoutNs))
-      atomicOr(&a.hdr->status, kErrTimeout);
-  }
-  __syncthreads();
   uint32_t s = 0;
   while (s + 1 < n && blockIdx.x >= a.blk_start[s + 1]) ++s;
   const uint32_t blk = blockIdx.x - a.blk_start[s];
@@ -448,6 +447,14 @@ __global__ void __launch_bounds__(kPrefixThreads) k_bpre(DecodeArgs a) {
     *a.out_count = u;
     *a.done = 0;
   }
+}
+
+__global__ void k_wait_pull(DecodeArgs a) {
+  zen_dev::pdl_entry();
+  const uint32_t s = threadIdx.x;
+  if (s >= a.n || !a.bits[s]) return;
+  const uint32_t iter = *(volatile uint32_t*)&a.hdr->iter;
+  if (!wait_flag(&a.pull_hdr[s]->flag, iter, kPeerTimeoutNs)) atomicOr(&a.hdr->status, kErrTimeout);
 }
 
 // popcount of server s's bitmap bits [0, P)
@@ -634,6 +641,10 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
 
 void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
   // a.pw is all-zero here: zeroed at allocation, re-zeroed by k_agg_values
+  if (a.wait_push) {
+    launch_k(k_wait_push, 1, 32, 0, stream, a);
+    count_launch();
+  }
   launch_k(k_agg_mark, 148 * 8, kAggThreads, 0, stream, a);
   launch_k(k_agg_union, a.nblk, kPrefixThreads, 0, stream, a);
   const unsigned g = (unsigned)((a.nw + kValThreads - 1) / kValThreads);
@@ -655,6 +666,10 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
 void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {
   const uint64_t nwords = (a.m + 63) / 64;
   const uint32_t ntiles = (uint32_t)((nwords + kDecThreads - 1) / kDecThreads);
+  if (a.wait_pull) {
+    launch_k(k_wait_pull, 1, 32, 0, stream, a);
+    count_launch();
+  }
   launch_k(k_bpre, a.total_blocks ? a.total_blocks : 1, kPrefixThreads, 0, stream, a);
   constexpr unsigned T = kDecThreads;
   if (a.n <= 2)
