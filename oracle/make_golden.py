@@ -231,11 +231,82 @@ def bp_cases(ro: RefOracle):
     return out
 
 
+def wire_cases(ro: RefOracle):
+    """Every WireKind (zen/codec.hpp:19-34) through the reference's encode,
+    write_framed and decode; .zspt bytes (zen/tensor.hpp:257-264)."""
+    rng = np.random.default_rng(1129)
+    out, meta = {}, []
+    # (kind, block_size, coo_bits, m, z, n, pseed, server)
+    specs = [(1, 256, 64, 5000, 60, 1, 0, 0), (1, 256, 32, 5000, 60, 1, 0, 0),
+             (1, 256, 64, 2**40, 33, 1, 0, 0), (1, 256, 64, 100, 0, 1, 0, 0),
+             (2, 256, 64, 5000, 60, 1, 0, 0), (2, 256, 64, 77, 13, 1, 0, 0),
+             (2, 256, 64, 64, 64, 1, 0, 0),
+             (3, 256, 64, 5000, 60, 1, 0, 0), (3, 7, 64, 5000, 300, 1, 0, 0),
+             (3, 1, 64, 999, 50, 1, 0, 0), (3, 100, 64, 1001, 1001, 1, 0, 0),
+             (4, 256, 64, 20000, 0, 4, 777, 1), (4, 256, 64, 20000, 0, 3, 12345, 2),
+             (4, 256, 64, 6400, 0, 1, 5, 0)]
+    for c, (kind, bs, cb, m, z, n, pseed, srv) in enumerate(specs):
+        if kind == 4:
+            cand = np.arange(m, dtype=np.uint64)
+            own = cand[ro.partition_of(cand, pseed, n) == srv]
+            idx = np.sort(rng.choice(own, min(own.size, 97), replace=False)).astype(np.uint64)
+        elif m > 2**32:
+            idx = np.sort(rng.choice(2**20, z, replace=False).astype(np.uint64) * 1000003 + 2**33)
+        else:
+            idx = np.sort(rng.choice(m, z, replace=False)).astype(np.uint64)
+        val = rng.integers(-16, 17, idx.size).astype(np.float32)
+        val[val == 0] = 0.5
+        if kind == 3 and idx.size > 3:
+            val[1] = 0.0  # explicit zeros are encoded but dropped by the decode
+        payload, info = ro.wire_encode(kind, m, idx, val, bs, cb, n, pseed, srv)
+        framed = ro.write_framed(kind, m, idx, val, bs, cb, n, pseed, srv)
+        di, dv = ro.wire_decode(kind, m, info["count"], payload, bs, cb, n, pseed, srv)
+        out[f"c{c}_idx"], out[f"c{c}_val"] = idx, val
+        out[f"c{c}_payload"], out[f"c{c}_framed"] = payload, framed
+        out[f"c{c}_didx"], out[f"c{c}_dval"] = di, dv
+        meta.append([kind, bs, cb, m, n, pseed, srv, info["count"], info["index_bits"],
+                     info["value_bits"]])
+    out["meta"] = np.array(meta, np.uint64)
+    # COO payload in arbitrary order: decode canonicalises (tensor.hpp:41, :72-84)
+    idx = rng.choice(4000, 50, replace=False).astype(np.uint64)
+    val = rng.integers(1, 9, 50).astype(np.float32)
+    out["unsorted_payload"] = np.concatenate([idx.view(np.uint8), val.view(np.uint8)])
+    out["unsorted_idx"], out["unsorted_val"] = ro.wire_decode(1, 4000, 50, out["unsorted_payload"])
+    m = 123456
+    idx = np.sort(rng.choice(m, 40, replace=False)).astype(np.uint64)
+    val = rng.standard_normal(40).astype(np.float32)
+    out["zspt_m"] = np.array([m], np.uint64)
+    out["zspt_idx"], out["zspt_val"] = idx, val
+    out["zspt_bytes"] = ro.write_sparse(m, idx, val)
+    return out
+
+
+def topk_cases(ro: RefOracle):
+    """zen::sparsify_topk (zen/workload.hpp:157-178): ties, zeros, signs."""
+    rng = np.random.default_rng(178)
+    out, cases = {}, []
+    dense = rng.standard_normal(20000).astype(np.float32)
+    dense[rng.choice(20000, 4000, replace=False)] = 0.0
+    dense[100:140] = 3.0          # a run of equal magnitudes: ties to the lower index
+    dense[200:220] = -3.0
+    dense[300] = -0.0
+    ints = rng.integers(-4, 5, 5000).astype(np.float32)  # many ties
+    for name, d in [("gauss", dense), ("ints", ints)]:
+        out[f"{name}_dense"] = d
+        for f in [1e-4, 0.001, 0.0021, 0.01, 0.05, 0.3, 0.9, 1.0]:
+            i, v = ro.sparsify_topk(d, f)
+            out[f"{name}_{f}_idx"], out[f"{name}_{f}_val"] = i, v
+            cases.append(f)
+    out["fractions"] = np.array(sorted(set(cases)), np.float64)
+    return out
+
+
 def main():
     ro = RefOracle()
     os.makedirs(OUT, exist_ok=True)
     for name, fn in [("hash_kat", hash_kat), ("hhash", hhash_cases), ("to_sparse", to_sparse_cases),
-                     ("codec", codec_cases), ("bp", bp_cases)]:
+                     ("codec", codec_cases), ("bp", bp_cases), ("wire", wire_cases),
+                     ("topk", topk_cases)]:
         data = fn(ro)
         path = os.path.join(OUT, name + ".npz")
         np.savez_compressed(path, **data)

@@ -56,6 +56,18 @@ class _ZoParams(C.Structure):
                 ("r2_ratio", C.c_double), ("lanes", C.c_uint32), ("seed", C.c_uint64)]
 
 
+class _ZoWire(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("block_size", C.c_uint32), ("coo_index_bits", C.c_uint32)]
+
+
+class _ZoMsg(C.Structure):
+    _fields_ = [("universe_size", C.c_uint64), ("count", C.c_uint64), ("index_bits", C.c_uint64),
+                ("value_bits", C.c_uint64), ("payload_len", C.c_uint64)]
+
+
+WIRE_KINDS = {"coo": 1, "bitmap": 2, "tensor_block": 3, "hash_bitmap": 4}
+
+
 @dataclass
 class HashResult:
     parts_idx: list
@@ -116,6 +128,20 @@ class COracle:
             f64p, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_uint32)]
         L.zo_bp_sizes.argtypes = [C.c_double, C.c_double, C.c_uint64, C.c_uint32,
                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.zo_wire_encode.argtypes = [C.POINTER(_ZoWire), C.c_void_p, C.c_uint32, C.c_uint64, u64p,
+                                     f32p, C.c_uint64, u8p, C.c_uint64, C.POINTER(_ZoMsg)]
+        L.zo_wire_decode.argtypes = [C.POINTER(_ZoWire), C.c_void_p, C.c_uint32,
+                                     C.POINTER(_ZoMsg), u8p, u64p, f32p, C.c_uint64,
+                                     C.POINTER(C.c_uint64)]
+        L.zo_frame_header.argtypes = [C.POINTER(_ZoWire), C.POINTER(_ZoMsg), u8p]
+        L.zo_frame_parse.argtypes = [u8p, C.c_uint64, C.POINTER(_ZoWire), C.POINTER(_ZoMsg)]
+        L.zo_sparse_file_size.restype = C.c_uint64
+        L.zo_sparse_file_size.argtypes = [C.c_uint64]
+        L.zo_write_sparse.argtypes = [C.c_uint64, u64p, f32p, C.c_uint64, u8p]
+        L.zo_read_sparse.argtypes = [u8p, C.c_uint64, C.POINTER(C.c_uint64), u64p, f32p,
+                                     C.c_uint64, C.POINTER(C.c_uint64)]
+        L.zo_sparsify_topk.restype = C.c_uint64
+        L.zo_sparsify_topk.argtypes = [f32p, C.c_uint64, C.c_double, u64p, f32p]
 
     # -- hash family -------------------------------------------------------
     def mix64(self, x):
@@ -236,6 +262,110 @@ class COracle:
                         (bal[0], bal[1]) if bv.value else None, counts.reshape(n, n), agg)
 
 
+def _wire_cap(kind, m, z, block_size):
+    k = WIRE_KINDS[kind] if isinstance(kind, str) else kind
+    if k == 1:
+        return 64 + 12 * z
+    if k == 3:
+        return 64 + (8 + 4 * block_size) * z
+    return 64 + (m + 7) // 8 + 4 * z
+
+
+def _wire(kind, block_size=256, coo_bits=64):
+    return _ZoWire(WIRE_KINDS[kind] if isinstance(kind, str) else kind, block_size, coo_bits)
+
+
+def _co_wire_encode(self, kind, m, idx, val, block_size=256, coo_bits=64, universe=None,
+                    server=0):
+    """zen::encode (zen/codec.hpp:213-278) -> (payload bytes, info dict)."""
+    idx, val = _u64(idx), _f32(val)
+    cap = _wire_cap(kind, m, idx.size, block_size)
+    buf = np.zeros(cap, np.uint8)
+    msg = _ZoMsg()
+    rc = self.lib.zo_wire_encode(C.byref(_wire(kind, block_size, coo_bits)),
+                                 universe.h if universe else None, server, m, idx, val, idx.size,
+                                 buf, cap, C.byref(msg))
+    if rc:
+        raise OracleError(rc, "wire encode")
+    return buf[:msg.payload_len].copy(), {"count": msg.count, "index_bits": msg.index_bits,
+                                          "value_bits": msg.value_bits}
+
+
+def _co_wire_decode(self, kind, m, count, payload, block_size=256, coo_bits=64, universe=None,
+                    server=0):
+    payload = np.ascontiguousarray(payload, np.uint8)
+    msg = _ZoMsg(m, count, 0, 0, payload.size)
+    cap = max(count, 1) * (block_size if WIRE_KINDS.get(kind, kind) == 3 else 1) + 1
+    idx = np.empty(cap, np.uint64)
+    val = np.empty(cap, np.float32)
+    oc = C.c_uint64()
+    rc = self.lib.zo_wire_decode(C.byref(_wire(kind, block_size, coo_bits)),
+                                 universe.h if universe else None, server, C.byref(msg), payload,
+                                 idx, val, cap, C.byref(oc))
+    if rc:
+        raise OracleError(rc, "wire decode")
+    return idx[:oc.value].copy(), val[:oc.value].copy()
+
+
+def _co_frame(self, kind, m, payload, info, block_size=256, coo_bits=64):
+    """write_framed (zen/codec.hpp:356-366): 33-byte header + payload."""
+    hdr = np.zeros(33, np.uint8)
+    msg = _ZoMsg(m, info["count"], info["index_bits"], info["value_bits"], len(payload))
+    self.lib.zo_frame_header(C.byref(_wire(kind, block_size, coo_bits)), C.byref(msg), hdr)
+    return np.concatenate([hdr, np.asarray(payload, np.uint8)])
+
+
+def _co_unframe(self, framed):
+    framed = np.ascontiguousarray(framed, np.uint8)
+    f, msg = _ZoWire(), _ZoMsg()
+    rc = self.lib.zo_frame_parse(framed, framed.size, C.byref(f), C.byref(msg))
+    if rc:
+        raise OracleError(rc, "frame")
+    return ({"kind": f.kind, "block_size": f.block_size, "coo_index_bits": f.coo_index_bits,
+             "universe_size": msg.universe_size, "count": msg.count,
+             "index_bits": msg.index_bits, "value_bits": msg.value_bits},
+            framed[33:33 + msg.payload_len].copy())
+
+
+def _co_write_sparse(self, m, idx, val):
+    idx, val = _u64(idx), _f32(val)
+    out = np.zeros(int(self.lib.zo_sparse_file_size(idx.size)), np.uint8)
+    self.lib.zo_write_sparse(m, idx, val, idx.size, out)
+    return out
+
+
+def _co_read_sparse(self, data):
+    data = np.ascontiguousarray(data, np.uint8)
+    cap = max(data.size // 12, 1)
+    idx = np.empty(cap, np.uint64)
+    val = np.empty(cap, np.float32)
+    m, c = C.c_uint64(), C.c_uint64()
+    rc = self.lib.zo_read_sparse(data, data.size, C.byref(m), idx, val, cap, C.byref(c))
+    if rc:
+        raise OracleError(rc, "read_sparse")
+    return m.value, idx[:c.value].copy(), val[:c.value].copy()
+
+
+def _co_sparsify_topk(self, dense, fraction):
+    dense = _f32(dense)
+    keep = min(dense.size, int(np.ceil(fraction * dense.size))) if 0 < fraction <= 1 else 1
+    idx = np.empty(max(keep, 1), np.uint64)
+    val = np.empty(max(keep, 1), np.float32)
+    c = self.lib.zo_sparsify_topk(dense, dense.size, fraction, idx, val)
+    if c == 2**64 - 1:
+        raise OracleError(1, "top-k fraction must be in (0,1]")
+    return idx[:c].copy(), val[:c].copy()
+
+
+COracle.wire_encode = _co_wire_encode
+COracle.wire_decode = _co_wire_decode
+COracle.frame = _co_frame
+COracle.unframe = _co_unframe
+COracle.write_sparse = _co_write_sparse
+COracle.read_sparse = _co_read_sparse
+COracle.sparsify_topk = _co_sparsify_topk
+
+
 class _Universe:
     def __init__(self, co, m, n, pseed):
         self.co, self.m, self.n, self.pseed = co, m, n, pseed
@@ -319,6 +449,19 @@ class RefOracle:
             C.POINTER(C.c_uint64), u64p, f64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.ref_aggregate.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p),
                                     C.POINTER(C.c_void_p), u64p, u64p, f32p, C.POINTER(C.c_uint64)]
+        L.ref_wire_encode.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
+                                      C.c_uint64, C.c_uint32, u64p, f32p, C.c_uint64, u8p,
+                                      C.c_uint64, u64p]
+        L.ref_wire_decode.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
+                                      C.c_uint64, C.c_uint32, C.c_uint64, u8p, C.c_uint64, u64p,
+                                      f32p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_write_framed.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
+                                       C.c_uint64, C.c_uint32, u64p, f32p, C.c_uint64, u8p,
+                                       C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_write_sparse.argtypes = [C.c_uint64, u64p, f32p, C.c_uint64, u8p, C.c_uint64,
+                                       C.POINTER(C.c_uint64)]
+        L.ref_sparsify_topk.argtypes = [f32p, C.c_uint64, C.c_double, u64p, f32p,
+                                        C.POINTER(C.c_uint64)]
         L.ref_bench_step.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), C.c_uint32,
                                      C.c_double, C.c_double, C.c_uint32, C.c_uint64, C.c_int, f64p,
                                      C.POINTER(C.c_uint64)]
@@ -466,6 +609,71 @@ class RefOracle:
         self._check(self.lib.ref_bench_step(n, m, dp, k, r1_multiplier, r2_ratio, lanes, seed,
                                             reps, t, C.byref(rn)), "bench_step")
         return {"to_sparse_ms": t[0], "sync_ms": t[1], "table_ms": t[2], "result_nnz": rn.value}
+
+
+def _ref_wire_encode(self, kind, m, idx, val, block_size=256, coo_bits=64, n=1, pseed=0,
+                     server=0):
+    idx, val = _u64(idx), _f32(val)
+    k = WIRE_KINDS[kind] if isinstance(kind, str) else kind
+    cap = _wire_cap(k, m, idx.size, block_size)
+    buf = np.zeros(cap, np.uint8)
+    info = np.zeros(4, np.uint64)
+    self._check(self.lib.ref_wire_encode(k, block_size, coo_bits, m, n, pseed, server, idx, val,
+                                         idx.size, buf, cap, info), "wire encode")
+    return buf[:int(info[3])].copy(), {"count": int(info[0]), "index_bits": int(info[1]),
+                                       "value_bits": int(info[2])}
+
+
+def _ref_wire_decode(self, kind, m, count, payload, block_size=256, coo_bits=64, n=1, pseed=0,
+                     server=0):
+    payload = np.ascontiguousarray(payload, np.uint8)
+    k = WIRE_KINDS[kind] if isinstance(kind, str) else kind
+    cap = max(count, 1) * (block_size if k == 3 else 1) + 1
+    idx = np.empty(cap, np.uint64)
+    val = np.empty(cap, np.float32)
+    oc = C.c_uint64()
+    self._check(self.lib.ref_wire_decode(k, block_size, coo_bits, m, n, pseed, server, count,
+                                         payload, payload.size, idx, val, cap, C.byref(oc)),
+                "wire decode")
+    return idx[:oc.value].copy(), val[:oc.value].copy()
+
+
+def _ref_write_framed(self, kind, m, idx, val, block_size=256, coo_bits=64, n=1, pseed=0,
+                      server=0):
+    idx, val = _u64(idx), _f32(val)
+    k = WIRE_KINDS[kind] if isinstance(kind, str) else kind
+    cap = 64 + _wire_cap(k, m, idx.size, block_size)
+    buf = np.zeros(cap, np.uint8)
+    ol = C.c_uint64()
+    self._check(self.lib.ref_write_framed(k, block_size, coo_bits, m, n, pseed, server, idx, val,
+                                          idx.size, buf, cap, C.byref(ol)), "write_framed")
+    return buf[:ol.value].copy()
+
+
+def _ref_write_sparse(self, m, idx, val):
+    idx, val = _u64(idx), _f32(val)
+    buf = np.zeros(24 + 12 * idx.size, np.uint8)
+    ol = C.c_uint64()
+    self._check(self.lib.ref_write_sparse(m, idx, val, idx.size, buf, buf.size, C.byref(ol)),
+                "write_sparse")
+    return buf[:ol.value].copy()
+
+
+def _ref_sparsify_topk(self, dense, fraction):
+    dense = _f32(dense)
+    idx = np.empty(max(dense.size, 1), np.uint64)
+    val = np.empty(max(dense.size, 1), np.float32)
+    oc = C.c_uint64()
+    self._check(self.lib.ref_sparsify_topk(dense, dense.size, fraction, idx, val, C.byref(oc)),
+                "sparsify_topk")
+    return idx[:oc.value].copy(), val[:oc.value].copy()
+
+
+RefOracle.wire_encode = _ref_wire_encode
+RefOracle.wire_decode = _ref_wire_decode
+RefOracle.write_framed = _ref_write_framed
+RefOracle.write_sparse = _ref_write_sparse
+RefOracle.sparsify_topk = _ref_sparsify_topk
 
 
 def c_oracle():

@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <sstream>
+#include <string>
 #include <vector>
 
 #include "zen/codec.hpp"
@@ -330,6 +332,101 @@ int ref_bench_step(uint32_t n, uint64_t m, const float* const* dense, uint32_t k
     }
     t[0] /= reps;
     t[1] /= reps;
+  });
+}
+
+// zen::encode for every WireKind (zen/codec.hpp:213-278).  kind: 1 coo,
+// 2 bitmap, 3 tensor block, 4 hash bitmap (n/pseed/s used for 4 only).
+// info: [count, index_bits, value_bits, payload_len]
+int ref_wire_encode(uint32_t kind, uint32_t block_size, uint32_t coo_bits, uint64_t m,
+                    uint32_t n, uint64_t pseed, uint32_t s, const uint64_t* idx, const float* val,
+                    uint64_t count, uint8_t* payload, uint64_t capacity, uint64_t* info) {
+  return guarded([&] {
+    zen::WireFormat fmt = kind == 1 ? zen::WireFormat::coo(coo_bits)
+                          : kind == 2 ? zen::WireFormat::bitmap()
+                          : kind == 3 ? zen::WireFormat::tensor_block(block_size)
+                                      : zen::WireFormat::hash_bitmap();
+    std::unique_ptr<zen::HashUniverseTable> table;
+    if (kind == 4) table.reset(new zen::HashUniverseTable(m, n, pseed));
+    auto msg = zen::encode(make_tensor(m, idx, val, count), fmt,
+                           table ? &table->universe(s) : nullptr);
+    if (msg.payload.size() > capacity) throw zen::Error("payload capacity");
+    std::memcpy(payload, msg.payload.data(), msg.payload.size());
+    info[0] = msg.count;
+    info[1] = msg.index_bits;
+    info[2] = msg.value_bits;
+    info[3] = msg.payload.size();
+  });
+}
+
+// zen::decode (zen/codec.hpp:282-347) of a payload with the given header fields
+int ref_wire_decode(uint32_t kind, uint32_t block_size, uint32_t coo_bits, uint64_t m,
+                    uint32_t n, uint64_t pseed, uint32_t s, uint64_t count, const uint8_t* payload,
+                    uint64_t payload_len, uint64_t* idx, float* val, uint64_t capacity,
+                    uint64_t* out_count) {
+  return guarded([&] {
+    zen::EncodedMessage msg;
+    msg.format = kind == 1 ? zen::WireFormat::coo(coo_bits)
+                 : kind == 2 ? zen::WireFormat::bitmap()
+                 : kind == 3 ? zen::WireFormat::tensor_block(block_size)
+                             : zen::WireFormat::hash_bitmap();
+    msg.universe_size = m;
+    msg.count = count;
+    msg.payload.assign(payload, payload + payload_len);
+    std::unique_ptr<zen::HashUniverseTable> table;
+    if (kind == 4) table.reset(new zen::HashUniverseTable(m, n, pseed));
+    auto t = zen::decode(msg, table ? &table->universe(s) : nullptr);
+    if (t.nnz() > capacity) throw zen::Error("output capacity");
+    std::copy(t.indices().begin(), t.indices().end(), idx);
+    std::copy(t.values().begin(), t.values().end(), val);
+    *out_count = t.nnz();
+  });
+}
+
+// zen::write_framed (zen/codec.hpp:356-366) of zen::encode's message -> bytes
+int ref_write_framed(uint32_t kind, uint32_t block_size, uint32_t coo_bits, uint64_t m,
+                     uint32_t n, uint64_t pseed, uint32_t s, const uint64_t* idx, const float* val,
+                     uint64_t count, uint8_t* out, uint64_t capacity, uint64_t* out_len) {
+  return guarded([&] {
+    zen::WireFormat fmt = kind == 1 ? zen::WireFormat::coo(coo_bits)
+                          : kind == 2 ? zen::WireFormat::bitmap()
+                          : kind == 3 ? zen::WireFormat::tensor_block(block_size)
+                                      : zen::WireFormat::hash_bitmap();
+    std::unique_ptr<zen::HashUniverseTable> table;
+    if (kind == 4) table.reset(new zen::HashUniverseTable(m, n, pseed));
+    auto msg = zen::encode(make_tensor(m, idx, val, count), fmt,
+                           table ? &table->universe(s) : nullptr);
+    std::ostringstream os;
+    zen::write_framed(os, msg);
+    const std::string b = os.str();
+    if (b.size() > capacity) throw zen::Error("frame capacity");
+    std::memcpy(out, b.data(), b.size());
+    *out_len = b.size();
+  });
+}
+
+// zen::write_sparse (zen/tensor.hpp:257-264) -> .zspt bytes
+int ref_write_sparse(uint64_t m, const uint64_t* idx, const float* val, uint64_t count,
+                     uint8_t* out, uint64_t capacity, uint64_t* out_len) {
+  return guarded([&] {
+    std::ostringstream os;
+    zen::write_sparse(os, make_tensor(m, idx, val, count));
+    const std::string b = os.str();
+    if (b.size() > capacity) throw zen::Error("capacity");
+    std::memcpy(out, b.data(), b.size());
+    *out_len = b.size();
+  });
+}
+
+// zen::sparsify_topk (zen/workload.hpp:157-178)
+int ref_sparsify_topk(const float* dense, uint64_t m, double fraction, uint64_t* idx, float* val,
+                      uint64_t* out_count) {
+  return guarded([&] {
+    zen::DenseTensor d(std::vector<float>(dense, dense + m));
+    auto t = zen::sparsify_topk(d, fraction);
+    std::copy(t.indices().begin(), t.indices().end(), idx);
+    std::copy(t.values().begin(), t.values().end(), val);
+    *out_count = t.nnz();
   });
 }
 

@@ -2,9 +2,9 @@
  * zen_oracle.c -- TEST INFRASTRUCTURE ONLY (see zen_oracle.h).
  *
  * Plain-C restatement of the reference Balanced-Parallelism path
- * (/root/reference/proj/include/zen/*.hpp).  Every function cites the
+ * (/root/reference/proj/include/zen/ headers).  Every function cites the
  * reference lines it follows.  It is pinned against the reference itself
- * (tests/golden/*, produced by oracle/make_golden.py from oracle/_ref, the
+ * (tests/golden/ fixtures, produced by oracle/make_golden.py from oracle/_ref, the
  * reference headers) by tests/test_oracle_golden.py.
  */
 #include "zen_oracle.h"
@@ -474,4 +474,291 @@ int zo_bp_sync(uint32_t n, uint64_t m, const uint64_t *const *idx, const float *
   free(pval);
   free(pcnt);
   return rc;
+}
+
+/* ---- wire formats: zen/codec.hpp ---------------------------------------- */
+
+static void put_le(uint8_t *p, uint64_t v, int bytes) {
+  for (int i = 0; i < bytes; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+static uint64_t get_le(const uint8_t *p, int bytes) {
+  uint64_t v = 0;
+  for (int i = 0; i < bytes; ++i) v |= (uint64_t)p[i] << (8 * i);
+  return v;
+}
+
+int zo_wire_encode(const zo_wire_format *f, const zo_universe *u, uint32_t server, uint64_t m,
+                   const uint64_t *idx, const float *val, uint64_t count, uint8_t *payload,
+                   uint64_t cap, zo_message *out) {
+  zo_message msg = {m, count, 0, 32 * count, 0};
+  switch (f->kind) {
+    case ZO_WIRE_COO: { /* codec.hpp:218-234: all indices, then all values */
+      const uint32_t ib = f->coo_index_bits;
+      if (ib != 32 && ib != 64) return ZO_E_INVALID;
+      msg.index_bits = (uint64_t)ib * count;
+      msg.payload_len = (ib / 8 + 4) * count;
+      if (msg.payload_len > cap) return ZO_E_INVALID;
+      for (uint64_t i = 0; i < count; ++i) {
+        if (ib == 32 && idx[i] > 0xffffffffULL) return ZO_E_INVALID;
+        put_le(payload + i * (ib / 8), idx[i], (int)(ib / 8));
+      }
+      memcpy(payload + (uint64_t)(ib / 8) * count, val, (size_t)count * 4);
+      break;
+    }
+    case ZO_WIRE_BITMAP: { /* codec.hpp:236-243: bitmap over [0, M), then values */
+      const uint64_t bytes = (m + 7) / 8;
+      msg.index_bits = m;
+      msg.payload_len = bytes + 4 * count;
+      if (msg.payload_len > cap) return ZO_E_INVALID;
+      memset(payload, 0, (size_t)bytes);
+      for (uint64_t i = 0; i < count; ++i) payload[idx[i] >> 3] |= (uint8_t)(1u << (idx[i] & 7));
+      memcpy(payload + bytes, val, (size_t)count * 4);
+      break;
+    }
+    case ZO_WIRE_TENSOR_BLOCK: { /* codec.hpp:244-262 + nonzero_blocks :167-178 */
+      const uint64_t b = f->block_size;
+      if (b < 1) return ZO_E_INVALID;
+      uint64_t nb = 0, values = 0, pos = 0, i = 0;
+      while (i < count) { /* sizes first */
+        const uint64_t id = idx[i] / b, begin = id * b;
+        const uint64_t len = (m - begin < b) ? m - begin : b;
+        while (i < count && idx[i] < begin + len) ++i;
+        ++nb;
+        values += len;
+      }
+      msg.count = nb;
+      msg.index_bits = 64 * nb;
+      msg.value_bits = 32 * values;
+      msg.payload_len = 8 * nb + 4 * values;
+      if (msg.payload_len > cap) return ZO_E_INVALID;
+      i = 0;
+      while (i < count) {
+        const uint64_t id = idx[i] / b, begin = id * b;
+        const uint64_t len = (m - begin < b) ? m - begin : b;
+        put_le(payload + pos, id, 8);
+        pos += 8;
+        for (uint64_t e = begin; e < begin + len; ++e) {
+          float v = 0.0f;
+          if (i < count && idx[i] == e) v = val[i++];
+          memcpy(payload + pos, &v, 4);
+          pos += 4;
+        }
+      }
+      break;
+    }
+    case ZO_WIRE_HASH_BITMAP: {
+      if (!u) return ZO_E_INVALID;
+      const uint64_t bytes = (u->sizes[server] + 7) / 8;
+      msg.payload_len = bytes + 4 * count;
+      if (msg.payload_len > cap) return ZO_E_INVALID;
+      const int rc = zo_hash_bitmap_encode(u, server, idx, val, count, payload, &msg.index_bits, NULL);
+      if (rc) return rc;
+      break;
+    }
+    default:
+      return ZO_E_INVALID;
+  }
+  if (out) *out = msg;
+  return ZO_OK;
+}
+
+/* SparseTensor(M, idx, val): sort when unsorted, then range/duplicate checks
+ * (tensor.hpp:36-46, canonicalize :72-84) */
+static int canonical(uint64_t m, uint64_t *idx, float *val, uint64_t n) {
+  int sorted = 1;
+  for (uint64_t i = 1; i < n && sorted; ++i) sorted = idx[i - 1] <= idx[i];
+  if (!sorted) {
+    zo_pair *p = (zo_pair *)malloc((size_t)(n ? n : 1) * sizeof(zo_pair));
+    for (uint64_t i = 0; i < n; ++i) p[i] = (zo_pair){idx[i], val[i]};
+    qsort(p, (size_t)n, sizeof(zo_pair), cmp_pair);
+    for (uint64_t i = 0; i < n; ++i) {
+      idx[i] = p[i].idx;
+      val[i] = p[i].val;
+    }
+    free(p);
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    if (idx[i] >= m) return ZO_E_INVALID;
+    if (i > 0 && idx[i] == idx[i - 1]) return ZO_E_INVALID;
+  }
+  return ZO_OK;
+}
+
+int zo_wire_decode(const zo_wire_format *f, const zo_universe *u, uint32_t server,
+                   const zo_message *msg, const uint8_t *payload, uint64_t *idx, float *val,
+                   uint64_t cap, uint64_t *out_count) {
+  const uint64_t m = msg->universe_size, count = msg->count, len = msg->payload_len;
+  uint64_t n = 0;
+  switch (f->kind) {
+    case ZO_WIRE_COO: { /* codec.hpp:285-296 */
+      const uint64_t ib = f->coo_index_bits / 8;
+      if (len != (ib + 4) * count) return ZO_E_MALFORMED;
+      if (count > cap) return ZO_E_INVALID;
+      for (uint64_t i = 0; i < count; ++i) idx[i] = get_le(payload + i * ib, (int)ib);
+      memcpy(val, payload + ib * count, (size_t)count * 4);
+      n = count;
+      break;
+    }
+    case ZO_WIRE_BITMAP: { /* codec.hpp:297-310 */
+      const uint64_t bytes = (m + 7) / 8;
+      if (len != bytes + 4 * count) return ZO_E_MALFORMED;
+      for (uint64_t b = 0; b < m; ++b)
+        if ((payload[b >> 3] >> (b & 7)) & 1u) {
+          if (n >= count || n >= cap) return ZO_E_MALFORMED;
+          idx[n++] = b;
+        }
+      if (n != count) return ZO_E_MALFORMED;
+      memcpy(val, payload + bytes, (size_t)count * 4);
+      break;
+    }
+    case ZO_WIRE_TENSOR_BLOCK: { /* codec.hpp:311-331 */
+      const uint64_t b = f->block_size;
+      uint64_t pos = 0;
+      for (uint64_t k = 0; k < count; ++k) {
+        if (pos + 8 > len) return ZO_E_MALFORMED; /* take_value: payload truncated */
+        const uint64_t id = get_le(payload + pos, 8);
+        pos += 8;
+        const uint64_t begin = id * b;
+        if (begin >= m) return ZO_E_MALFORMED;
+        const uint64_t blen = (m - begin < b) ? m - begin : b;
+        for (uint64_t e = 0; e < blen; ++e) {
+          if (pos + 4 > len) return ZO_E_MALFORMED;
+          float v;
+          memcpy(&v, payload + pos, 4);
+          pos += 4;
+          if (v != 0.0f) {
+            if (n >= cap) return ZO_E_INVALID;
+            idx[n] = begin + e;
+            val[n++] = v;
+          }
+        }
+      }
+      if (pos != len) return ZO_E_MALFORMED;
+      break;
+    }
+    case ZO_WIRE_HASH_BITMAP: {
+      if (!u) return ZO_E_INVALID;
+      if (count > cap) return ZO_E_INVALID;
+      const int rc = zo_hash_bitmap_decode(u, server, payload, len, count, idx, val);
+      if (rc) return rc;
+      n = count;
+      break;
+    }
+    default:
+      return ZO_E_MALFORMED;
+  }
+  const int rc = canonical(m, idx, val, n);
+  if (rc) return rc;
+  *out_count = n;
+  return ZO_OK;
+}
+
+void zo_frame_header(const zo_wire_format *f, const zo_message *msg, uint8_t out[33]) {
+  out[0] = (uint8_t)f->kind; /* codec.hpp:358-363 */
+  put_le(out + 1, f->block_size, 4);
+  put_le(out + 5, f->coo_index_bits, 4);
+  put_le(out + 9, msg->universe_size, 8);
+  put_le(out + 17, msg->count, 8);
+  put_le(out + 25, msg->index_bits + msg->value_bits, 8);
+}
+
+int zo_frame_parse(const uint8_t *h, uint64_t len, zo_wire_format *f, zo_message *msg) {
+  if (len < 33) return ZO_E_MALFORMED;
+  const uint8_t tag = h[0]; /* codec.hpp:368-410 */
+  if (tag < 1 || tag > 4) return ZO_E_MALFORMED;
+  f->kind = tag;
+  f->block_size = (uint32_t)get_le(h + 1, 4);
+  f->coo_index_bits = (uint32_t)get_le(h + 5, 4);
+  msg->universe_size = get_le(h + 9, 8);
+  msg->count = get_le(h + 17, 8);
+  const uint64_t bits = get_le(h + 25, 8), c = msg->count;
+  switch (tag) {
+    case ZO_WIRE_COO:
+      msg->index_bits = (uint64_t)f->coo_index_bits * c;
+      msg->value_bits = 32 * c;
+      msg->payload_len = (f->coo_index_bits / 8 + 4) * c;
+      break;
+    case ZO_WIRE_BITMAP:
+      msg->index_bits = msg->universe_size;
+      msg->value_bits = 32 * c;
+      msg->payload_len = (msg->universe_size + 7) / 8 + 4 * c;
+      break;
+    case ZO_WIRE_TENSOR_BLOCK:
+      msg->index_bits = 64 * c;
+      msg->value_bits = bits >= msg->index_bits ? bits - msg->index_bits : 0;
+      if (msg->value_bits % 32) return ZO_E_MALFORMED;
+      msg->payload_len = 8 * c + msg->value_bits / 8;
+      break;
+    default: /* hash bitmap */
+      msg->index_bits = bits >= 32 * c ? bits - 32 * c : 0;
+      msg->value_bits = 32 * c;
+      msg->payload_len = (msg->index_bits + 7) / 8 + 4 * c;
+      break;
+  }
+  if (msg->index_bits + msg->value_bits != bits) return ZO_E_MALFORMED;
+  if (len < 33 + msg->payload_len) return ZO_E_MALFORMED; /* payload truncated */
+  return ZO_OK;
+}
+
+/* ---- .zspt: zen/tensor.hpp:239-285 -------------------------------------- */
+
+uint64_t zo_sparse_file_size(uint64_t count) { return 24 + 12 * count; }
+
+void zo_write_sparse(uint64_t m, const uint64_t *idx, const float *val, uint64_t count,
+                     uint8_t *out) {
+  memcpy(out, "ZSPT", 4);
+  put_le(out + 4, 1, 4);
+  put_le(out + 8, m, 8);
+  put_le(out + 16, count, 8);
+  for (uint64_t i = 0; i < count; ++i) put_le(out + 24 + 8 * i, idx[i], 8);
+  memcpy(out + 24 + 8 * count, val, (size_t)count * 4);
+}
+
+int zo_read_sparse(const uint8_t *in, uint64_t len, uint64_t *m, uint64_t *idx, float *val,
+                   uint64_t cap, uint64_t *count) {
+  if (len < 8 || memcmp(in, "ZSPT", 4) != 0) return ZO_E_MALFORMED;
+  if (get_le(in + 4, 4) != 1) return ZO_E_MALFORMED;
+  if (len < 24) return ZO_E_MALFORMED;
+  *m = get_le(in + 8, 8);
+  const uint64_t c = get_le(in + 16, 8);
+  if (len < 24 + 12 * c) return ZO_E_MALFORMED;
+  if (c > cap) return ZO_E_INVALID;
+  for (uint64_t i = 0; i < c; ++i) idx[i] = get_le(in + 24 + 8 * i, 8);
+  memcpy(val, in + 24 + 8 * c, (size_t)c * 4);
+  *count = c;
+  if (*m == 0) return ZO_E_INVALID;
+  return canonical(*m, idx, val, c);
+}
+
+/* ---- sparsify_topk: zen/workload.hpp:157-178 ---------------------------- */
+
+static const float *g_topk_dense;
+static int cmp_topk(const void *a, const void *b) { /* |v| descending, index ascending */
+  const uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  const float mx = fabsf(g_topk_dense[x]), my = fabsf(g_topk_dense[y]);
+  if (mx != my) return mx > my ? -1 : 1;
+  return x < y ? -1 : x > y;
+}
+
+uint64_t zo_sparsify_topk(const float *dense, uint64_t m, double fraction, uint64_t *idx,
+                          float *val) {
+  if (!(fraction > 0.0 && fraction <= 1.0)) return UINT64_MAX;
+  uint64_t keep = (uint64_t)ceil(fraction * (double)m);
+  if (keep > m) keep = m;
+  uint64_t *order = (uint64_t *)malloc((size_t)(m ? m : 1) * sizeof(uint64_t));
+  for (uint64_t i = 0; i < m; ++i) order[i] = i;
+  g_topk_dense = dense;
+  qsort(order, (size_t)m, sizeof(uint64_t), cmp_topk);
+  zo_pair *p = (zo_pair *)malloc((size_t)(keep ? keep : 1) * sizeof(zo_pair));
+  uint64_t n = 0;
+  for (uint64_t i = 0; i < keep; ++i)
+    if (dense[order[i]] != 0.0f) p[n++] = (zo_pair){order[i], dense[order[i]]};
+  qsort(p, (size_t)n, sizeof(zo_pair), cmp_pair);
+  for (uint64_t i = 0; i < n; ++i) {
+    idx[i] = p[i].idx;
+    val[i] = p[i].val;
+  }
+  free(p);
+  free(order);
+  return n;
 }

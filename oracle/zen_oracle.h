@@ -2,7 +2,7 @@
  * zen_oracle.h -- TEST INFRASTRUCTURE ONLY.
  *
  * A plain-C CPU restatement of the reference (arXiv 2309.13254 "zensim",
- * /root/reference/proj/include/zen/*.hpp) Balanced-Parallelism hot path.
+ * /root/reference/proj/include/zen/ headers) Balanced-Parallelism hot path.
  * It is the parity checker for the sm_100a kernels: only tests/,
  * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
  * may load it.  The product library (paper_2309_13254_b200/lib/libzen_b200.so)
@@ -125,6 +125,43 @@ void zo_bp_sizes(double r1_multiplier, double r2_ratio, uint64_t nnz, uint32_t n
 
 /* zen/hashing.hpp:296-320 */
 double zo_imbalance_pull(const uint64_t *loads, uint32_t n, uint64_t union_size);
+
+/* ---- wire and file formats: zen/codec.hpp:19-34, 182-347, 352-410;
+ *      zen/tensor.hpp:239-303 ------------------------------------------- */
+enum { ZO_WIRE_COO = 1, ZO_WIRE_BITMAP = 2, ZO_WIRE_TENSOR_BLOCK = 3, ZO_WIRE_HASH_BITMAP = 4 };
+typedef struct zo_wire_format {
+  uint32_t kind, block_size, coo_index_bits;
+} zo_wire_format;
+typedef struct zo_message {
+  uint64_t universe_size, count, index_bits, value_bits, payload_len;
+} zo_message;
+
+/* encode (codec.hpp:213-278); u/server only for ZO_WIRE_HASH_BITMAP.  Input
+ * sorted unique < m.  Returns ZO_E_INVALID when cap is too small or a 32-bit
+ * COO index overflows, ZO_E_INDEX_OUTSIDE_UNIVERSE for foreign indices. */
+int zo_wire_encode(const zo_wire_format *f, const zo_universe *u, uint32_t server, uint64_t m,
+                   const uint64_t *idx, const float *val, uint64_t count, uint8_t *payload,
+                   uint64_t cap, zo_message *out);
+/* decode (codec.hpp:282-347) + the SparseTensor canonicalisation (sort when
+ * unsorted; duplicate / out-of-range -> ZO_E_INVALID, tensor.hpp:36-46). */
+int zo_wire_decode(const zo_wire_format *f, const zo_universe *u, uint32_t server,
+                   const zo_message *msg, const uint8_t *payload, uint64_t *idx, float *val,
+                   uint64_t cap, uint64_t *out_count);
+/* write_framed / read_framed header (codec.hpp:356-410): 33 bytes, LE. */
+enum { ZO_FRAME_HEADER = 33 };
+void zo_frame_header(const zo_wire_format *f, const zo_message *msg, uint8_t out[33]);
+int zo_frame_parse(const uint8_t *hdr, uint64_t len, zo_wire_format *f, zo_message *msg);
+/* .zspt (tensor.hpp:257-285): "ZSPT", u32 version 1, u64 M, u64 count, idx, val */
+uint64_t zo_sparse_file_size(uint64_t count);
+void zo_write_sparse(uint64_t m, const uint64_t *idx, const float *val, uint64_t count,
+                     uint8_t *out);
+int zo_read_sparse(const uint8_t *in, uint64_t len, uint64_t *m, uint64_t *idx, float *val,
+                   uint64_t cap, uint64_t *count);
+/* sparsify_topk (workload.hpp:157-178): the ceil(fraction*m) largest |v|, ties
+ * to the lower index, exact zeros dropped, ascending.  Returns the count or
+ * UINT64_MAX for a fraction outside (0, 1]. */
+uint64_t zo_sparsify_topk(const float *dense, uint64_t m, double fraction, uint64_t *idx,
+                          float *val);
 
 #ifdef __cplusplus
 }

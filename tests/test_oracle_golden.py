@@ -171,3 +171,62 @@ def test_oracle_matches_live_reference_random(co, ro):
         np.testing.assert_array_equal(a.idx, b.idx)
         np.testing.assert_array_equal(a.val, b.val)
         np.testing.assert_array_equal(a.ledger, b.ledger)
+
+
+def _wire_kw(meta_row):
+    kind, bs, cb, m, n, pseed, srv = (int(x) for x in meta_row[:7])
+    return kind, m, {"block_size": bs, "coo_bits": cb}, n, pseed, srv
+
+
+def test_wire_formats_golden(co):
+    """Every WireKind's payload bytes, bit accounting, framing and decode
+    (zen/codec.hpp:182-410) equal the reference's."""
+    g = load_golden("wire")
+    for c, row in enumerate(g["meta"]):
+        kind, m, kw, n, pseed, srv = _wire_kw(row)
+        u = co.universe(m, n, pseed) if kind == 4 else None
+        idx, val = g[f"c{c}_idx"], g[f"c{c}_val"]
+        payload, info = co.wire_encode(kind, m, idx, val, universe=u, server=srv, **kw)
+        assert np.array_equal(payload, g[f"c{c}_payload"]), c
+        assert [info["count"], info["index_bits"], info["value_bits"]] == [int(x) for x in row[7:]]
+        framed = co.frame(kind, m, payload, info, **kw)
+        assert np.array_equal(framed, g[f"c{c}_framed"]), c
+        hdr, body = co.unframe(framed)
+        assert np.array_equal(body, payload) and hdr["count"] == info["count"]
+        di, dv = co.wire_decode(kind, m, info["count"], payload, universe=u, server=srv, **kw)
+        assert np.array_equal(di, g[f"c{c}_didx"]) and np.array_equal(dv, g[f"c{c}_dval"]), c
+    di, dv = co.wire_decode(1, 4000, 50, g["unsorted_payload"])
+    assert np.array_equal(di, g["unsorted_idx"]) and np.array_equal(dv, g["unsorted_val"])
+
+
+def test_wire_malformed_and_sparse_file(co):
+    g = load_golden("wire")
+    m = int(g["zspt_m"][0])
+    raw = co.write_sparse(m, g["zspt_idx"], g["zspt_val"])
+    assert np.array_equal(raw, g["zspt_bytes"])
+    m2, i2, v2 = co.read_sparse(raw)
+    assert m2 == m and np.array_equal(i2, g["zspt_idx"]) and np.array_equal(v2, g["zspt_val"])
+    with pytest.raises(OracleError):
+        co.read_sparse(np.frombuffer(b"ZSPX" + raw.tobytes()[4:], np.uint8))
+    payload, info = co.wire_encode(1, 5000, g["c0_idx"], g["c0_val"])
+    with pytest.raises(OracleError):  # size mismatch (codec.hpp:287)
+        co.wire_decode(1, 5000, info["count"] + 1, payload)
+    dup = np.concatenate([np.array([5, 5], np.uint64).view(np.uint8),
+                          np.ones(2, np.float32).view(np.uint8)])
+    with pytest.raises(OracleError):  # duplicate index (tensor.hpp:44)
+        co.wire_decode(1, 5000, 2, dup)
+    framed = co.frame(1, 5000, payload, info)
+    with pytest.raises(OracleError):  # truncated frame
+        co.unframe(framed[:-1])
+
+
+def test_sparsify_topk_golden(co):
+    g = load_golden("topk")
+    for name in ["gauss", "ints"]:
+        d = g[f"{name}_dense"]
+        for f in g["fractions"]:
+            key = f"{name}_{f}_idx"
+            if key not in g:
+                continue
+            i, v = co.sparsify_topk(d, float(f))
+            assert np.array_equal(i, g[key]) and np.array_equal(v, g[f"{name}_{f}_val"]), (name, f)
