@@ -155,6 +155,50 @@ zen_status zen_hash_bitmap_decode(zen_universe* u, uint32_t server, const uint8_
                                   uint64_t payload_bytes, uint64_t count, uint64_t* d_idx,
                                   float* d_val);
 
+/* ---- wire formats: zen/codec.hpp:19-410 -------------------------------- */
+/* zen::WireKind (codec.hpp:19) */
+#define ZEN_WIRE_COO 1u
+#define ZEN_WIRE_BITMAP 2u
+#define ZEN_WIRE_TENSOR_BLOCK 3u
+#define ZEN_WIRE_HASH_BITMAP 4u
+#define ZEN_FRAME_HEADER_BYTES 33u /* write_framed header, codec.hpp:352-366 */
+/* zen::WireFormat (codec.hpp:21-35): block_size for TensorBlock, index width
+ * (32 or 64) for COO */
+typedef struct zen_wire_format {
+  uint32_t kind;
+  uint32_t block_size;
+  uint32_t coo_index_bits;
+} zen_wire_format;
+/* the header fields of zen::EncodedMessage (codec.hpp:101-111) */
+typedef struct zen_message_info {
+  uint64_t universe_size;
+  uint64_t count;        /* entries (Coo/Bitmap/HashBitmap) or non-zero blocks (TensorBlock) */
+  uint64_t index_bits;
+  uint64_t value_bits;
+  uint64_t payload_bytes;
+} zen_message_info;
+/* encode(t, fmt, universe), codec.hpp:213-278: device tensor (sorted unique
+ * u64 indices < universe) -> device payload bytes, byte-identical to the
+ * reference.  u/server only for ZEN_WIRE_HASH_BITMAP.  *out always carries the
+ * sizes; ZEN_E_CAPACITY when capacity < out->payload_bytes.  The plain Bitmap
+ * needs universe < 2^32. */
+zen_status zen_encode(zen_ctx* ctx, const zen_wire_format* fmt, zen_universe* u, uint32_t server,
+                      const uint64_t* d_idx, const float* d_val, uint64_t count, uint64_t universe,
+                      uint8_t* d_payload, uint64_t capacity, zen_message_info* out);
+/* decode(msg, universe), codec.hpp:282-347, plus the SparseTensor
+ * canonicalisation (sorted on return; duplicate / out-of-range indices ->
+ * ZEN_E_INVALID, tensor.hpp:36-46).  msg: universe_size, count, payload_bytes. */
+zen_status zen_decode(zen_ctx* ctx, const zen_wire_format* fmt, zen_universe* u, uint32_t server,
+                      const zen_message_info* msg, const uint8_t* d_payload, uint64_t* d_idx,
+                      float* d_val, uint64_t capacity, uint64_t* count);
+/* write_framed header (codec.hpp:356-366): out[ZEN_FRAME_HEADER_BYTES], host */
+zen_status zen_frame_header(const zen_wire_format* fmt, const zen_message_info* msg, uint8_t* out);
+/* read_framed header (codec.hpp:368-410): rebuilds the bit accounting and
+ * checks it; ZEN_E_MALFORMED on a bad tag / mismatch / fewer than header +
+ * payload bytes available */
+zen_status zen_frame_parse(const uint8_t* in, uint64_t available, zen_wire_format* fmt,
+                           zen_message_info* msg);
+
 /* ---- Balanced Parallelism: zen::run_balanced_parallelism -------------- */
 /* zen/schemes.hpp:341-417.  rank = ZEN_BP_LOCAL hosts all n workers/servers on
  * this context's GPU (exchange = local stores); otherwise this process is

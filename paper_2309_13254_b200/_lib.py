@@ -40,12 +40,29 @@ class CollisionStatsC(C.Structure):
                 ("k", C.c_uint32)]
 
 
+class WireFormatC(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("block_size", C.c_uint32), ("coo_index_bits", C.c_uint32)]
+
+
+class MessageInfoC(C.Structure):
+    _fields_ = [("universe_size", C.c_uint64), ("count", C.c_uint64), ("index_bits", C.c_uint64),
+                ("value_bits", C.c_uint64), ("payload_bytes", C.c_uint64)]
+
+
+FRAME_HEADER_BYTES = 33  # ZEN_FRAME_HEADER_BYTES
+
 vp = C.c_void_p
 u64 = C.c_uint64
 u32 = C.c_uint32
 P = C.POINTER
 
 _SIGS = {
+    "zen_encode": (C.c_int, [vp, P(WireFormatC), vp, u32, vp, vp, u64, u64, vp, u64,
+                             P(MessageInfoC)]),
+    "zen_decode": (C.c_int, [vp, P(WireFormatC), vp, u32, P(MessageInfoC), vp, vp, vp, u64,
+                             P(u64)]),
+    "zen_frame_header": (C.c_int, [P(WireFormatC), P(MessageInfoC), vp]),
+    "zen_frame_parse": (C.c_int, [vp, u64, P(WireFormatC), P(MessageInfoC)]),
     "zen_abi_version": (u32, []),
     "zen_status_string": (C.c_char_p, [C.c_int]),
     "zen_last_error_message": (C.c_char_p, []),

@@ -183,6 +183,7 @@ struct zen_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  zen_universe* ident = nullptr;  // identity universe of the plain Bitmap format (lazy)
 };
 
 extern "C" {
@@ -265,6 +266,7 @@ zen_status zen_ctx_create(int device, zen_ctx** out) {
 void zen_ctx_destroy(zen_ctx* c) {
   if (!c) return;
   DevGuard g(c->device);
+  if (c->ident) zen_universe_destroy(c->ident);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -739,6 +741,310 @@ zen_status zen_hash_bitmap_decode(zen_universe* u, uint32_t s, const uint8_t* d_
     CK(cudaMemcpyAsync(d_val, tmp_val, count * 4, cudaMemcpyDeviceToDevice, c->stream));
   }
   CK(cudaStreamSynchronize(c->stream));
+  return ZEN_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ wire formats ----
+// zen::encode / zen::decode for every WireKind and the frame header
+// (zen/codec.hpp:19-410).  Synchronous, like the reference's calls.
+
+namespace {
+
+zen_status wire_check_format(const zen_wire_format* f) {
+  if (!f) return fail(ZEN_E_INVALID, "null wire format");
+  if (f->kind < ZEN_WIRE_COO || f->kind > ZEN_WIRE_HASH_BITMAP)
+    return fail(ZEN_E_MALFORMED, "unknown wire format tag");
+  if (f->kind == ZEN_WIRE_COO && f->coo_index_bits != 32 && f->coo_index_bits != 64)
+    return fail(ZEN_E_INVALID, "COO index width must be 32 or 64");
+  if (f->kind == ZEN_WIRE_TENSOR_BLOCK && f->block_size < 1)
+    return fail(ZEN_E_INVALID, "tensor block size must be at least 1");
+  return ZEN_OK;
+}
+
+// the plain Bitmap is the HashBitmap over the one-server (identity) universe
+zen_status identity_universe(zen_ctx* c, uint64_t m, zen_universe** out) {
+  if (m >= 0xFFFFFFFFull) return fail(ZEN_E_INVALID, "bitmap universe must be below 2^32");
+  if (!c->ident || zen_universe_size(c->ident, 0) != m) {
+    if (c->ident) zen_universe_destroy(c->ident);
+    c->ident = nullptr;
+    CKR(zen_universe_create(c, m, 1, 0, &c->ident));
+  }
+  *out = c->ident;
+  return ZEN_OK;
+}
+
+zen_status wire_status(uint32_t st) {
+  if (st & kWireIdxOverflow) return fail(ZEN_E_INVALID, "index does not fit a 32-bit COO entry");
+  if (st & kWireMalformed) return fail(ZEN_E_MALFORMED, "tensor block payload malformed");
+  if (st & kWireRange) return fail(ZEN_E_INVALID, "sparse tensor index outside [0, M)");
+  if (st & kWireDup) return fail(ZEN_E_INVALID, "duplicate index in sparse tensor");
+  return ZEN_OK;
+}
+
+// input of an encode: a valid SparseTensor (sorted, unique, < M)
+zen_status wire_check_input(zen_ctx* c, const uint64_t* d_idx, uint64_t count, uint64_t m,
+                            uint32_t* st) {
+  if (!count) return ZEN_OK;
+  launch_check_canonical(d_idx, count, m, st, c->stream);
+  uint32_t h = 0;
+  CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h) return fail(ZEN_E_INVALID, "tensor indices not sorted/unique or >= M");
+  return ZEN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+zen_status zen_encode(zen_ctx* c, const zen_wire_format* f, zen_universe* u, uint32_t server,
+                      const uint64_t* d_idx, const float* d_val, uint64_t count, uint64_t m,
+                      uint8_t* d_payload, uint64_t capacity, zen_message_info* out) {
+  if (!c || !out) return fail(ZEN_E_INVALID, "null argument");
+  CKR(wire_check_format(f));
+  if (m == 0) return fail(ZEN_E_INVALID, "sparse tensor universe must be at least 1");
+  if (count && (!d_idx || !d_val)) return fail(ZEN_E_INVALID, "null tensor");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  DevMem mem;
+  uint32_t* st;
+  CKR(mem.alloc(&st, 1));
+  CKR(wire_check_input(c, d_idx, count, m, st));
+  zen_message_info info{m, count, 0, 32 * count, 0};
+  switch (f->kind) {
+    case ZEN_WIRE_COO: {
+      const int ib = int(f->coo_index_bits / 8);
+      info.index_bits = uint64_t(f->coo_index_bits) * count;
+      info.payload_bytes = uint64_t(ib + 4) * count;
+      *out = info;
+      if (info.payload_bytes > capacity) return fail(ZEN_E_CAPACITY, "payload capacity");
+      if (count && !d_payload) return fail(ZEN_E_INVALID, "null payload");
+      launch_coo_encode(d_idx, d_val, count, ib, d_payload, st, c->stream);
+      uint32_t h = 0;
+      CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      return wire_status(h);
+    }
+    case ZEN_WIRE_BITMAP:
+    case ZEN_WIRE_HASH_BITMAP: {
+      zen_universe* uu = u;
+      uint32_t s = server;
+      if (f->kind == ZEN_WIRE_BITMAP) {
+        CKR(identity_universe(c, m, &uu));
+        s = 0;
+      } else {
+        if (!uu) return fail(ZEN_E_INVALID, "hash bitmap requires a hash universe");
+        if (s >= uu->n) return fail(ZEN_E_INVALID, "bad universe/server");
+        if (uu->m != m) return fail(ZEN_E_UNIVERSE_MISMATCH, "tensor and universe sizes differ");
+      }
+      const uint64_t bs = uu->bs[s];
+      info.index_bits = bs;
+      info.payload_bytes = (bs + 7) / 8 + 4 * count;
+      *out = info;
+      if (info.payload_bytes > capacity) return fail(ZEN_E_CAPACITY, "payload capacity");
+      uint64_t ib = 0, pb = 0;
+      return zen_hash_bitmap_encode(uu, s, d_idx, d_val, count, d_payload, &ib, &pb);
+    }
+    default: {  // ZEN_WIRE_TENSOR_BLOCK
+      const uint64_t B = f->block_size;
+      uint64_t nb = 0, last = 0;
+      uint32_t *first = nullptr, *bpos = nullptr;
+      if (count) {
+        const size_t tb = wire_scan_bytes(count);
+        void* tmp;
+        CKR(mem.alloc(&first, count));
+        CKR(mem.alloc(&bpos, count));
+        CKR(mem.alloc((uint8_t**)&tmp, std::max<size_t>(tb, 1)));
+        launch_tb_blocks(d_idx, count, B, first, bpos, tmp, tb, c->stream);
+        uint32_t hb = 0;
+        CK(cudaMemcpyAsync(&hb, bpos + count - 1, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&last, d_idx + count - 1, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        nb = hb;
+      }
+      const uint64_t begin_last = (last / B) * B;
+      const uint64_t len_last = nb ? std::min<uint64_t>(B, m - begin_last) : 0;
+      const uint64_t values = nb ? (nb - 1) * B + len_last : 0;
+      info.count = nb;
+      info.index_bits = 64 * nb;
+      info.value_bits = 32 * values;
+      info.payload_bytes = 8 * nb + 4 * values;
+      *out = info;
+      if (info.payload_bytes > capacity) return fail(ZEN_E_CAPACITY, "payload capacity");
+      if (!count) return ZEN_OK;
+      CK(cudaMemsetAsync(d_payload, 0, info.payload_bytes, c->stream));
+      launch_tb_write(d_idx, d_val, count, B, first, bpos, d_payload, c->stream);
+      CK(cudaStreamSynchronize(c->stream));
+      return ZEN_OK;
+    }
+  }
+}
+
+zen_status zen_decode(zen_ctx* c, const zen_wire_format* f, zen_universe* u, uint32_t server,
+                      const zen_message_info* msg, const uint8_t* d_payload, uint64_t* d_idx,
+                      float* d_val, uint64_t capacity, uint64_t* count) {
+  if (!c || !msg || !count) return fail(ZEN_E_INVALID, "null argument");
+  CKR(wire_check_format(f));
+  const uint64_t m = msg->universe_size, n = msg->count, len = msg->payload_bytes;
+  if (m == 0) return fail(ZEN_E_INVALID, "sparse tensor universe must be at least 1");
+  if (len && !d_payload) return fail(ZEN_E_INVALID, "null payload");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  DevMem mem;
+  uint32_t* st;
+  CKR(mem.alloc(&st, 1));
+  uint64_t got = 0;
+  switch (f->kind) {
+    case ZEN_WIRE_COO: {
+      const int ib = int(f->coo_index_bits / 8);
+      if (len != uint64_t(ib + 4) * n) return fail(ZEN_E_MALFORMED, "COO payload size mismatch");
+      *count = n;
+      if (n > capacity) return fail(ZEN_E_CAPACITY, "output capacity");
+      launch_coo_decode(d_payload, n, ib, m, d_idx, d_val, st, c->stream);
+      got = n;
+      break;
+    }
+    case ZEN_WIRE_BITMAP:
+    case ZEN_WIRE_HASH_BITMAP: {
+      zen_universe* uu = u;
+      uint32_t s = server;
+      if (f->kind == ZEN_WIRE_BITMAP) {
+        CKR(identity_universe(c, m, &uu));
+        s = 0;
+      } else if (!uu) {
+        return fail(ZEN_E_INVALID, "hash bitmap requires the encoding universe");
+      }
+      *count = n;
+      if (n > capacity) return fail(ZEN_E_CAPACITY, "output capacity");
+      return zen_hash_bitmap_decode(uu, s, d_payload, len, n, d_idx, d_val);
+    }
+    default: {  // ZEN_WIRE_TENSOR_BLOCK
+      const uint64_t B = f->block_size;
+      const uint64_t slots = n * B;
+      uint64_t *off, *begin, *sidx, *dcount;
+      uint32_t* blen;
+      float* sval;
+      uint8_t* flag;
+      CKR(mem.alloc(&off, std::max<uint64_t>(n, 1)));
+      CKR(mem.alloc(&begin, std::max<uint64_t>(n, 1)));
+      CKR(mem.alloc(&blen, std::max<uint64_t>(n, 1)));
+      CKR(mem.alloc(&dcount, 1));
+      launch_tb_walk(d_payload, len, n, B, m, off, begin, blen, st, c->stream);
+      uint32_t h = 0;
+      CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (h) return wire_status(h);
+      if (slots) {
+        const size_t tb = wire_select_bytes(slots);
+        void* tmp;
+        uint64_t* oi;
+        float* ov;
+        CKR(mem.alloc(&sidx, slots));
+        CKR(mem.alloc(&sval, slots));
+        CKR(mem.alloc(&flag, slots));
+        CKR(mem.alloc(&oi, slots));
+        CKR(mem.alloc(&ov, slots));
+        CKR(mem.alloc((uint8_t**)&tmp, std::max<size_t>(tb, 1)));
+        launch_tb_expand_select(d_payload, n, B, off, begin, blen, sidx, sval, flag, oi, ov,
+                                dcount, tmp, tb, c->stream);
+        CK(cudaMemcpyAsync(&got, dcount, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        *count = got;
+        if (got > capacity) return fail(ZEN_E_CAPACITY, "output capacity");
+        if (got) {
+          CK(cudaMemcpyAsync(d_idx, oi, got * 8, cudaMemcpyDeviceToDevice, c->stream));
+          CK(cudaMemcpyAsync(d_val, ov, got * 4, cudaMemcpyDeviceToDevice, c->stream));
+        }
+      }
+      *count = got;
+      break;
+    }
+  }
+  // SparseTensor(M, idx, val): sort when unsorted, then range / duplicate checks
+  launch_check_canonical(d_idx, got, m, st, c->stream);
+  uint32_t h = 0;
+  CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h & kWireUnsorted) {
+    const size_t tb = wire_sort_bytes(got);
+    void* tmp;
+    uint64_t* ki;
+    float* vi;
+    CKR(mem.alloc(&ki, got));
+    CKR(mem.alloc(&vi, got));
+    CKR(mem.alloc((uint8_t**)&tmp, std::max<size_t>(tb, 1)));
+    CK(cudaMemcpyAsync(ki, d_idx, got * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(vi, d_val, got * 4, cudaMemcpyDeviceToDevice, c->stream));
+    launch_sort_pairs(ki, d_idx, vi, d_val, got, tmp, tb, c->stream);
+    CK(cudaMemsetAsync(st, 0, 4, c->stream));
+    launch_check_canonical(d_idx, got, m, st, c->stream);
+    CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return wire_status(h & ~kWireUnsorted);
+}
+
+zen_status zen_frame_header(const zen_wire_format* f, const zen_message_info* msg, uint8_t* out) {
+  if (!f || !msg || !out) return fail(ZEN_E_INVALID, "null argument");
+  auto put = [&](size_t at, uint64_t v, int nb) {
+    for (int b = 0; b < nb; ++b) out[at + b] = uint8_t(v >> (8 * b));
+  };
+  put(0, f->kind, 1);
+  put(1, f->block_size, 4);
+  put(5, f->coo_index_bits, 4);
+  put(9, msg->universe_size, 8);
+  put(17, msg->count, 8);
+  put(25, msg->index_bits + msg->value_bits, 8);
+  return ZEN_OK;
+}
+
+zen_status zen_frame_parse(const uint8_t* in, uint64_t available, zen_wire_format* f,
+                           zen_message_info* msg) {
+  if (!in || !f || !msg) return fail(ZEN_E_INVALID, "null argument");
+  if (available < ZEN_FRAME_HEADER_BYTES) return fail(ZEN_E_MALFORMED, "unexpected end of stream");
+  auto get = [&](size_t at, int nb) {
+    uint64_t v = 0;
+    for (int b = 0; b < nb; ++b) v |= uint64_t(in[at + b]) << (8 * b);
+    return v;
+  };
+  const uint64_t tag = get(0, 1);
+  if (tag < 1 || tag > 4) return fail(ZEN_E_MALFORMED, "unknown wire format tag");
+  f->kind = uint32_t(tag);
+  f->block_size = uint32_t(get(1, 4));
+  f->coo_index_bits = uint32_t(get(5, 4));
+  msg->universe_size = get(9, 8);
+  msg->count = get(17, 8);
+  const uint64_t bits = get(25, 8), c = msg->count;
+  switch (tag) {  // codec.hpp:380-405: accounting rebuilt from the format, then checked
+    case ZEN_WIRE_COO:
+      msg->index_bits = uint64_t(f->coo_index_bits) * c;
+      msg->value_bits = 32 * c;
+      msg->payload_bytes = (f->coo_index_bits / 8 + 4) * c;
+      break;
+    case ZEN_WIRE_BITMAP:
+      msg->index_bits = msg->universe_size;
+      msg->value_bits = 32 * c;
+      msg->payload_bytes = (msg->universe_size + 7) / 8 + 4 * c;
+      break;
+    case ZEN_WIRE_TENSOR_BLOCK:
+      msg->index_bits = 64 * c;
+      msg->value_bits = bits >= msg->index_bits ? bits - msg->index_bits : 0;
+      if (msg->value_bits % 32)
+        return fail(ZEN_E_MALFORMED, "tensor block value bits not 32-aligned");
+      msg->payload_bytes = 8 * c + msg->value_bits / 8;
+      break;
+    default:
+      msg->index_bits = bits >= 32 * c ? bits - 32 * c : 0;
+      msg->value_bits = 32 * c;
+      msg->payload_bytes = (msg->index_bits + 7) / 8 + 4 * c;
+      break;
+  }
+  if (msg->index_bits + msg->value_bits != bits)
+    return fail(ZEN_E_MALFORMED, "frame bit accounting mismatch");
+  if (available < ZEN_FRAME_HEADER_BYTES + msg->payload_bytes)
+    return fail(ZEN_E_MALFORMED, "frame payload truncated");
   return ZEN_OK;
 }
 

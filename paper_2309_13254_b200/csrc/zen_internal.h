@@ -258,6 +258,33 @@ void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream);
 void launch_u64_to_u32(const uint64_t* in, uint32_t* out, uint64_t n, cudaStream_t stream);
 void launch_fill_u64(unsigned long long* p, uint64_t n, uint64_t v, cudaStream_t stream);
 
+// wire formats (k_wire.cu)
+constexpr uint32_t kWireIdxOverflow = 1u, kWireUnsorted = 2u, kWireDup = 4u, kWireRange = 8u,
+                   kWireMalformed = 16u;
+void launch_coo_encode(const uint64_t* idx, const float* val, uint64_t count, int ib,
+                       uint8_t* payload, uint32_t* status, cudaStream_t s);
+void launch_coo_decode(const uint8_t* payload, uint64_t count, int ib, uint64_t m, uint64_t* idx,
+                       float* val, uint32_t* status, cudaStream_t s);
+void launch_check_canonical(const uint64_t* idx, uint64_t count, uint64_t m, uint32_t* status,
+                            cudaStream_t s);
+size_t wire_scan_bytes(uint64_t n);
+size_t wire_sort_bytes(uint64_t n);
+size_t wire_select_bytes(uint64_t n);
+void launch_tb_blocks(const uint64_t* idx, uint64_t count, uint64_t block, uint32_t* first,
+                      uint32_t* bpos, void* tmp, size_t tmp_bytes, cudaStream_t s);
+void launch_tb_write(const uint64_t* idx, const float* val, uint64_t count, uint64_t block,
+                     const uint32_t* first, const uint32_t* bpos, uint8_t* payload, cudaStream_t s);
+void launch_tb_walk(const uint8_t* payload, uint64_t len, uint64_t count, uint64_t block,
+                    uint64_t m, uint64_t* off, uint64_t* begin, uint32_t* blen, uint32_t* status,
+                    cudaStream_t s);
+void launch_tb_expand_select(const uint8_t* payload, uint64_t nb, uint64_t block,
+                             const uint64_t* off, const uint64_t* begin, const uint32_t* blen,
+                             uint64_t* sidx, float* sval, uint8_t* flag, uint64_t* out_idx,
+                             float* out_val, uint64_t* d_count, void* tmp, size_t tmp_bytes,
+                             cudaStream_t s);
+void launch_sort_pairs(const uint64_t* ki, uint64_t* ko, const float* vi, float* vo,
+                       uint64_t count, void* tmp, size_t tmp_bytes, cudaStream_t s);
+
 // RAII launch policy for the calling thread (see zen_common.cuh launch_k)
 struct LaunchScope {
   LaunchScope(bool pdl, bool low_priority);

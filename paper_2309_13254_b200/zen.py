@@ -415,14 +415,38 @@ def imbalance_pull(server_loads, union_size: int) -> float:
 
 # ------------------------------------------------- universe + hash bitmap ----
 
+_WIRE_KINDS = {"coo": 1, "bitmap": 2, "tensor_block": 3, "hash_bitmap": 4}
+
+
 @dataclass
 class WireFormat:
-    """zen::WireFormat (codec.hpp:20-35); only the HashBitmap row is on this path."""
-    kind: str = "hash_bitmap"
+    """zen::WireFormat (codec.hpp:20-35)."""
+    kind: str = "coo"
+    block_size: int = 256        # TensorBlock only
+    coo_index_bits: int = 64     # COO only: 64 (default) or 32
+
+    @staticmethod
+    def coo(index_bits: int = 64):
+        if index_bits not in (32, 64):
+            raise Error("COO index width must be 32 or 64")
+        return WireFormat("coo", 256, index_bits)
+
+    @staticmethod
+    def bitmap():
+        return WireFormat("bitmap")
+
+    @staticmethod
+    def tensor_block(block_size: int = 256):
+        if block_size < 1:
+            raise Error("tensor block size must be at least 1")
+        return WireFormat("tensor_block", block_size)
 
     @staticmethod
     def hash_bitmap():
         return WireFormat("hash_bitmap")
+
+    def _c(self):
+        return L.WireFormatC(_WIRE_KINDS[self.kind], self.block_size, self.coo_index_bits)
 
 
 @dataclass
@@ -502,43 +526,134 @@ def bp_universe_table(universe_size: int, servers: int, seed: int) -> HashUniver
     return HashUniverseTable(universe_size, servers, derive_seed(seed, 0))
 
 
-def encode(t: SparseTensor, fmt: WireFormat, universe: HashUniverse) -> EncodedMessage:
-    """zen::encode for WireKind::HashBitmap (codec.hpp:266-277)."""
-    if fmt.kind != "hash_bitmap":
-        raise Error("only the HashBitmap wire format is on the B200 path")
-    if universe is None:
-        raise Error("hash bitmap requires a hash universe")
+def encode(t: SparseTensor, fmt: WireFormat, universe: HashUniverse | None = None) -> EncodedMessage:
+    """zen::encode (codec.hpp:213-278) on the GPU, every WireKind; payload bytes
+    identical to the reference's."""
     torch = _torch()
-    tab = universe._table
-    s = universe.server_id
+    ctx = context()
     z = t.nnz()
-    nbytes = (tab.size(s) + 7) // 8 + 4 * z
     d_idx = _dev(t.indices().view(np.int64), torch.int64)
     d_val = _dev(t.values(), torch.float32)
-    out = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=d_idx.device)
-    bits, plen = C.c_uint64(), C.c_uint64()
-    _check(_lib().zen_hash_bitmap_encode(tab.h, s, _ptr(d_idx), _ptr(d_val), z, _ptr(out),
-                                         C.byref(bits), C.byref(plen)))
-    return EncodedMessage(fmt, t.universe(), z, int(bits.value), 32 * z,
-                          out[:plen.value].cpu().numpy())
+    uh, s = None, 0
+    if fmt.kind == "hash_bitmap":
+        if universe is None:
+            raise Error("hash bitmap requires a hash universe")
+        uh, s = universe._table.h, universe.server_id
+    info = L.MessageInfoC()
+    f = fmt._c()
+    rc = _lib().zen_encode(ctx.h, C.byref(f), uh, s, _ptr(d_idx), _ptr(d_val), z, t.universe(),
+                           None, 0, C.byref(info))
+    if rc not in (L.OK, L.E_CAPACITY):
+        _check(rc)
+    out = torch.empty(max(int(info.payload_bytes), 1), dtype=torch.uint8, device=d_idx.device)
+    _check(_lib().zen_encode(ctx.h, C.byref(f), uh, s, _ptr(d_idx), _ptr(d_val), z, t.universe(),
+                             _ptr(out), int(info.payload_bytes), C.byref(info)))
+    return EncodedMessage(fmt, t.universe(), int(info.count), int(info.index_bits),
+                          int(info.value_bits), out[:info.payload_bytes].cpu().numpy())
 
 
-def decode(msg: EncodedMessage, universe: HashUniverse) -> SparseTensor:
-    """zen::decode for WireKind::HashBitmap (codec.hpp:333-347)."""
-    if universe is None:
-        raise Error("hash bitmap requires the encoding universe")
+def decode(msg: EncodedMessage, universe: HashUniverse | None = None) -> SparseTensor:
+    """zen::decode (codec.hpp:282-347) on the GPU, every WireKind."""
     torch = _torch()
-    tab = universe._table
-    s = universe.server_id
+    ctx = context()
     payload = np.ascontiguousarray(msg.payload, dtype=np.uint8)
     d_p = _dev(payload, torch.uint8)
-    z = int(msg.count)
-    oi = torch.empty(max(z, 1), dtype=torch.int64, device=d_p.device)
-    ov = torch.empty(max(z, 1), dtype=torch.float32, device=d_p.device)
-    _check(_lib().zen_hash_bitmap_decode(tab.h, s, _ptr(d_p), payload.size, z, _ptr(oi),
-                                         _ptr(ov)))
+    uh, s = None, 0
+    if msg.format.kind == "hash_bitmap":
+        if universe is None:
+            raise Error("hash bitmap requires the encoding universe")
+        uh, s = universe._table.h, universe.server_id
+    cap = int(msg.count) * (msg.format.block_size if msg.format.kind == "tensor_block" else 1)
+    oi = torch.empty(max(cap, 1), dtype=torch.int64, device=d_p.device)
+    ov = torch.empty(max(cap, 1), dtype=torch.float32, device=d_p.device)
+    info = L.MessageInfoC(msg.universe_size, msg.count, msg.index_bits, msg.value_bits,
+                          payload.size)
+    got = C.c_uint64()
+    _check(_lib().zen_decode(ctx.h, C.byref(msg.format._c()), uh, s, C.byref(info), _ptr(d_p),
+                             _ptr(oi), _ptr(ov), cap, C.byref(got)))
+    z = got.value
     return SparseTensor(msg.universe_size, oi[:z].cpu().numpy().view(np.uint64),
                         ov[:z].cpu().numpy(), _trusted=True)
+
+
+def message_sizes(t: SparseTensor, fmt: WireFormat, universe: HashUniverse | None = None):
+    """zen::message_sizes (codec.hpp:182-211): (index_bits, value_bits)."""
+    m = encode(t, fmt, universe)
+    return m.index_bits, m.value_bits
+
+
+def write_framed(stream, msg: EncodedMessage):
+    """zen::write_framed (codec.hpp:356-366)."""
+    if msg.payload is None or (len(msg.payload) == 0 and msg.payload_bits() != 0):
+        raise Error("cannot frame a message without payload")
+    hdr = np.zeros(L.FRAME_HEADER_BYTES, np.uint8)
+    info = L.MessageInfoC(msg.universe_size, msg.count, msg.index_bits, msg.value_bits,
+                          len(msg.payload))
+    _check(_lib().zen_frame_header(C.byref(msg.format._c()), C.byref(info),
+                                   hdr.ctypes.data_as(C.c_void_p)))
+    stream.write(hdr.tobytes())
+    stream.write(np.ascontiguousarray(msg.payload, np.uint8).tobytes())
+
+
+def read_framed(stream) -> EncodedMessage:
+    """zen::read_framed (codec.hpp:368-410)."""
+    hdr = np.frombuffer(stream.read(L.FRAME_HEADER_BYTES), np.uint8).copy()
+    if hdr.size < L.FRAME_HEADER_BYTES:
+        raise MalformedPayload("unexpected end of stream")
+    f, info = L.WireFormatC(), L.MessageInfoC()
+    # header only (no payload bytes are read by the parse): available = max
+    _check(_lib().zen_frame_parse(hdr.ctypes.data_as(C.c_void_p), 2**64 - 1, C.byref(f),
+                                  C.byref(info)))
+    payload = np.frombuffer(stream.read(int(info.payload_bytes)), np.uint8).copy()
+    if payload.size < info.payload_bytes:
+        raise MalformedPayload("frame payload truncated")
+    kind = {v: k for k, v in _WIRE_KINDS.items()}[f.kind]
+    return EncodedMessage(WireFormat(kind, f.block_size, f.coo_index_bits), info.universe_size,
+                          info.count, info.index_bits, info.value_bits, payload)
+
+
+# .zspt (zen/tensor.hpp:239-303): "ZSPT", u32 version 1, u64 M, u64 count, u64
+# indices, f32 values -- host byte layout
+_SPARSE_MAGIC = b"ZSPT"
+
+
+def write_sparse(stream, t: SparseTensor):
+    """zen::write_sparse (tensor.hpp:257-264)."""
+    stream.write(_SPARSE_MAGIC)
+    stream.write(np.array([1], "<u4").tobytes())
+    stream.write(np.array([t.universe(), t.nnz()], "<u8").tobytes())
+    stream.write(t.indices().astype("<u8").tobytes())
+    stream.write(t.values().astype("<f4").tobytes())
+
+
+def read_sparse(stream) -> SparseTensor:
+    """zen::read_sparse (tensor.hpp:266-279)."""
+    if stream.read(4) != _SPARSE_MAGIC:
+        raise MalformedPayload("bad sparse tensor magic")
+    raw = stream.read(4)
+    if len(raw) < 4:
+        raise MalformedPayload("unexpected end of stream")
+    if np.frombuffer(raw, "<u4")[0] != 1:
+        raise MalformedPayload("unsupported sparse tensor version")
+    raw = stream.read(16)
+    if len(raw) < 16:
+        raise MalformedPayload("unexpected end of stream")
+    m, c = (int(x) for x in np.frombuffer(raw, "<u8"))
+    ib, vb = stream.read(8 * c), stream.read(4 * c)
+    if len(ib) < 8 * c or len(vb) < 4 * c:
+        raise MalformedPayload("unexpected end of stream")
+    return SparseTensor(m, np.frombuffer(ib, "<u8").astype(np.uint64),
+                        np.frombuffer(vb, "<f4").astype(np.float32))
+
+
+def write_sparse_file(path: str, t: SparseTensor):
+    with open(path, "wb") as f:
+        write_sparse(f, t)
+
+
+def read_sparse_file(path: str) -> SparseTensor:
+    with open(path, "rb") as f:
+        return read_sparse(f)
 
 
 # ------------------------------------------------------------- transport ----

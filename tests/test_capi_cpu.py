@@ -72,3 +72,39 @@ def test_compat_header_compiles():
                         os.path.join(ROOT, "tests", "cpp", "compat_test.cpp")],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_host_formats_without_gpu():
+    """Host-side byte layouts: the frame header through the C-ABI
+    (zen_frame_header / zen_frame_parse need no device) and the .zspt writer,
+    against the reference's bytes (tests/golden/wire.npz)."""
+    import io
+    import numpy as np
+    from conftest import load_golden
+    import paper_2309_13254_b200 as z
+    from paper_2309_13254_b200 import _lib as L
+    lib = z.load()
+    g = load_golden("wire")
+    for c, row in enumerate(g["meta"]):
+        kind, bs, cb, m = (int(x) for x in row[:4])
+        count, ib, vb = (int(x) for x in row[7:])
+        payload = g[f"c{c}_payload"]
+        f = L.WireFormatC(kind, bs, cb)
+        info = L.MessageInfoC(m, count, ib, vb, payload.size)
+        hdr = np.zeros(33, np.uint8)
+        assert lib.zen_frame_header(ctypes.byref(f), ctypes.byref(info),
+                                    hdr.ctypes.data_as(ctypes.c_void_p)) == 0
+        np.testing.assert_array_equal(hdr, g[f"c{c}_framed"][:33])
+        framed = g[f"c{c}_framed"]
+        f2, i2 = L.WireFormatC(), L.MessageInfoC()
+        assert lib.zen_frame_parse(framed.ctypes.data_as(ctypes.c_void_p), framed.size,
+                                   ctypes.byref(f2), ctypes.byref(i2)) == 0
+        assert (f2.kind, i2.count, i2.payload_bytes) == (kind, count, payload.size)
+        assert lib.zen_frame_parse(framed.ctypes.data_as(ctypes.c_void_p), framed.size - 1,
+                                   ctypes.byref(f2), ctypes.byref(i2)) == 4  # truncated
+    t = z.SparseTensor(int(g["zspt_m"][0]), g["zspt_idx"], g["zspt_val"])
+    buf = io.BytesIO()
+    z.write_sparse(buf, t)
+    np.testing.assert_array_equal(np.frombuffer(buf.getvalue(), np.uint8), g["zspt_bytes"])
+    buf.seek(0)
+    assert z.read_sparse(buf) == t
