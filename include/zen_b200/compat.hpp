@@ -16,7 +16,9 @@
 //   zen::collision_stats (hashing.hpp:259)      zen_b200::collision_stats
 //   zen::imbalance_push/pull (hashing.hpp:296)  zen_b200::imbalance_push/pull
 //   zen::HashUniverseTable (codec.hpp:47)       zen_b200::HashUniverseTable
-//   zen::encode/decode, HashBitmap (codec.hpp)  zen_b200::encode/decode
+//   zen::encode/decode, every WireKind,          zen_b200::encode/decode,
+//   message_sizes, write/read_framed (codec.hpp) message_sizes, write/read_framed
+//   zen::write/read_sparse[_file] (tensor.hpp)  zen_b200::write/read_sparse[_file]
 //   zen::SimNet / TrafficReport (simnet.hpp)    zen_b200::SimNet / TrafficReport
 //   zen::HashParams / SyncOutcome (schemes.hpp) zen_b200::HashParams / SyncOutcome
 //   zen::run_balanced_parallelism (schemes.hpp:341)  zen_b200::run_balanced_parallelism
@@ -31,6 +33,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <istream>
+#include <ostream>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -355,9 +360,20 @@ inline double imbalance_pull(const std::vector<uint64_t>& loads, uint64_t union_
 
 // ---- codec: zen/codec.hpp ---------------------------------------------------
 enum class WireKind : uint8_t { Coo = 1, Bitmap = 2, TensorBlock = 3, HashBitmap = 4 };
-struct WireFormat {
-  WireKind kind = WireKind::HashBitmap;
-  static WireFormat hash_bitmap() { return {WireKind::HashBitmap}; }
+struct WireFormat {  // codec.hpp:21-35
+  WireKind kind = WireKind::Coo;
+  uint32_t block_size = 256;
+  uint32_t coo_index_bits = 64;
+  static WireFormat coo(uint32_t index_bits = 64) {
+    if (index_bits != 32 && index_bits != 64) throw Error("COO index width must be 32 or 64");
+    return {WireKind::Coo, 256, index_bits};
+  }
+  static WireFormat bitmap() { return {WireKind::Bitmap, 256, 64}; }
+  static WireFormat tensor_block(uint32_t block_size = 256) {
+    if (block_size < 1) throw Error("tensor block size must be at least 1");
+    return {WireKind::TensorBlock, block_size, 64};
+  }
+  static WireFormat hash_bitmap() { return {WireKind::HashBitmap, 256, 64}; }
 };
 
 struct EncodedMessage {
@@ -418,38 +434,162 @@ inline HashUniverseTable bp_universe_table(uint64_t universe_size, uint32_t serv
   return HashUniverseTable(universe_size, servers, zen_derive_seed(seed, 0));
 }
 
-// encode(t, WireFormat::hash_bitmap(), &universe) -- codec.hpp:266-277
+namespace detail {
+inline zen_wire_format wire_c(const WireFormat& f) {
+  return zen_wire_format{uint32_t(f.kind), f.block_size, f.coo_index_bits};
+}
+inline zen_universe* universe_handle(const WireFormat& f, const HashUniverse* u,
+                                     uint32_t* server) {
+  if (f.kind != WireKind::HashBitmap) return nullptr;
+  *server = u->server_id;
+  return u->table->handle();
+}
+}  // namespace detail
+
+// encode(t, fmt, universe) -- codec.hpp:213-278, every WireKind, on the GPU
 inline EncodedMessage encode(const SparseTensor& t, const WireFormat& fmt,
-                             const HashUniverse* universe) {
-  if (fmt.kind != WireKind::HashBitmap) throw Error("only the HashBitmap format is on the path");
-  if (universe == nullptr) throw Error("hash bitmap requires a hash universe");
-  const auto* tab = universe->table;
-  const uint32_t s = universe->server_id;
-  const uint64_t bytes = (tab->size(s) + 7) / 8 + 4 * t.nnz();
+                             const HashUniverse* universe = nullptr) {
+  if (fmt.kind == WireKind::HashBitmap && universe == nullptr)
+    throw Error("hash bitmap requires a hash universe");
+  uint32_t s = 0;
+  zen_universe* u = detail::universe_handle(fmt, universe, &s);
+  const zen_wire_format f = detail::wire_c(fmt);
   detail::DBuf<uint64_t> di(t.indices());
   detail::DBuf<float> dv(t.values());
-  detail::DBuf<uint8_t> dp(bytes);
-  uint64_t bits = 0, plen = 0;
-  detail::check(zen_hash_bitmap_encode(tab->handle(), s, di.p, dv.p, t.nnz(), dp.p, &bits, &plen));
+  zen_message_info info{};
+  const zen_status rc = zen_encode(detail::ctx(), &f, u, s, di.p, dv.p, t.nnz(), t.universe(),
+                                   nullptr, 0, &info);
+  if (rc != ZEN_OK && rc != ZEN_E_CAPACITY) detail::check(rc);
+  detail::DBuf<uint8_t> dp(info.payload_bytes);
+  detail::check(zen_encode(detail::ctx(), &f, u, s, di.p, dv.p, t.nnz(), t.universe(), dp.p,
+                           info.payload_bytes, &info));
   EncodedMessage msg;
   msg.format = fmt;
   msg.universe_size = t.universe();
-  msg.count = t.nnz();
-  msg.index_bits = bits;
-  msg.value_bits = 32 * t.nnz();
-  msg.payload = dp.host(plen);
+  msg.count = info.count;
+  msg.index_bits = info.index_bits;
+  msg.value_bits = info.value_bits;
+  msg.payload = dp.host(info.payload_bytes);
   return msg;
 }
 
-// decode(msg, &universe) -- codec.hpp:333-347
-inline SparseTensor decode(const EncodedMessage& msg, const HashUniverse* universe) {
-  if (universe == nullptr) throw Error("hash bitmap requires the encoding universe");
+// message_sizes(t, fmt, universe) -- codec.hpp:92-96, 182-211
+struct MessageSizes {
+  uint64_t index_bits = 0;
+  uint64_t value_bits = 0;
+  uint64_t payload_bits() const { return index_bits + value_bits; }
+};
+inline MessageSizes message_sizes(const SparseTensor& t, const WireFormat& fmt,
+                                  const HashUniverse* universe = nullptr) {
+  const auto m = encode(t, fmt, universe);
+  return {m.index_bits, m.value_bits};
+}
+
+// decode(msg, universe) -- codec.hpp:282-347, every WireKind, on the GPU
+inline SparseTensor decode(const EncodedMessage& msg, const HashUniverse* universe = nullptr) {
+  if (msg.format.kind == WireKind::HashBitmap && universe == nullptr)
+    throw Error("hash bitmap requires the encoding universe");
+  uint32_t s = 0;
+  zen_universe* u = detail::universe_handle(msg.format, universe, &s);
+  const zen_wire_format f = detail::wire_c(msg.format);
+  const uint64_t cap =
+      msg.count * (msg.format.kind == WireKind::TensorBlock ? msg.format.block_size : 1);
   detail::DBuf<uint8_t> dp(msg.payload);
-  detail::DBuf<uint64_t> oi(msg.count);
-  detail::DBuf<float> ov(msg.count);
-  detail::check(zen_hash_bitmap_decode(universe->table->handle(), universe->server_id, dp.p,
-                                       msg.payload.size(), msg.count, oi.p, ov.p));
-  return SparseTensor(msg.universe_size, oi.host(msg.count), ov.host(msg.count));
+  detail::DBuf<uint64_t> oi(cap);
+  detail::DBuf<float> ov(cap);
+  zen_message_info info{msg.universe_size, msg.count, msg.index_bits, msg.value_bits,
+                        msg.payload.size()};
+  uint64_t got = 0;
+  detail::check(zen_decode(detail::ctx(), &f, u, s, &info, dp.p, oi.p, ov.p, cap, &got));
+  return SparseTensor(msg.universe_size, oi.host(got), ov.host(got));
+}
+
+// write_framed / read_framed -- codec.hpp:352-410
+inline void write_framed(std::ostream& os, const EncodedMessage& msg) {
+  if (msg.payload.empty() && msg.payload_bits() != 0)
+    throw Error("cannot frame a message without payload");
+  const zen_wire_format f = detail::wire_c(msg.format);
+  zen_message_info info{msg.universe_size, msg.count, msg.index_bits, msg.value_bits,
+                        msg.payload.size()};
+  uint8_t hdr[ZEN_FRAME_HEADER_BYTES];
+  detail::check(zen_frame_header(&f, &info, hdr));
+  os.write(reinterpret_cast<const char*>(hdr), sizeof hdr);
+  os.write(reinterpret_cast<const char*>(msg.payload.data()),
+           static_cast<std::streamsize>(msg.payload.size()));
+}
+
+inline EncodedMessage read_framed(std::istream& is) {
+  uint8_t hdr[ZEN_FRAME_HEADER_BYTES];
+  is.read(reinterpret_cast<char*>(hdr), sizeof hdr);
+  if (!is) throw MalformedPayload("unexpected end of stream");
+  zen_wire_format f{};
+  zen_message_info info{};
+  detail::check(zen_frame_parse(hdr, ~uint64_t(0), &f, &info));  // header only
+  EncodedMessage msg;
+  msg.format = WireFormat{WireKind(f.kind), f.block_size, f.coo_index_bits};
+  msg.universe_size = info.universe_size;
+  msg.count = info.count;
+  msg.index_bits = info.index_bits;
+  msg.value_bits = info.value_bits;
+  msg.payload.resize(info.payload_bytes);
+  is.read(reinterpret_cast<char*>(msg.payload.data()),
+          static_cast<std::streamsize>(msg.payload.size()));
+  if (!is) throw MalformedPayload("frame payload truncated");
+  return msg;
+}
+
+// .zspt -- tensor.hpp:239-303 (host byte layout, little-endian)
+namespace detail {
+template <typename T>
+inline void write_le(std::ostream& os, T v) {
+  unsigned char b[sizeof(T)];
+  std::memcpy(b, &v, sizeof(T));
+  os.write(reinterpret_cast<const char*>(b), sizeof(T));
+}
+template <typename T>
+inline T read_le(std::istream& is) {
+  unsigned char b[sizeof(T)];
+  is.read(reinterpret_cast<char*>(b), sizeof(T));
+  if (!is) throw MalformedPayload("unexpected end of stream");
+  T v;
+  std::memcpy(&v, b, sizeof(T));
+  return v;
+}
+}  // namespace detail
+
+inline void write_sparse(std::ostream& os, const SparseTensor& t) {
+  os.write("ZSPT", 4);
+  detail::write_le<uint32_t>(os, 1);
+  detail::write_le<uint64_t>(os, t.universe());
+  detail::write_le<uint64_t>(os, t.nnz());
+  for (uint64_t i : t.indices()) detail::write_le<uint64_t>(os, i);
+  for (float v : t.values()) detail::write_le<float>(os, v);
+}
+
+inline SparseTensor read_sparse(std::istream& is) {
+  char magic[4];
+  is.read(magic, 4);
+  if (!is || std::memcmp(magic, "ZSPT", 4) != 0) throw MalformedPayload("bad sparse tensor magic");
+  if (detail::read_le<uint32_t>(is) != 1) throw MalformedPayload("unsupported sparse tensor version");
+  const uint64_t m = detail::read_le<uint64_t>(is);
+  const uint64_t count = detail::read_le<uint64_t>(is);
+  std::vector<uint64_t> idx(count);
+  for (auto& i : idx) i = detail::read_le<uint64_t>(is);
+  std::vector<float> val(count);
+  for (auto& v : val) v = detail::read_le<float>(is);
+  return SparseTensor(m, std::move(idx), std::move(val));
+}
+
+inline void write_sparse_file(const std::string& path, const SparseTensor& t) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw Error("cannot open " + path + " for writing");
+  write_sparse(os, t);
+}
+
+inline SparseTensor read_sparse_file(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw Error("cannot open " + path);
+  return read_sparse(is);
 }
 
 // ---- transport ledger: zen/simnet.hpp ---------------------------------------

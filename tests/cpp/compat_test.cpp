@@ -8,6 +8,7 @@
 #include <map>
 #include <random>
 #include <set>
+#include <sstream>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -345,6 +346,113 @@ TEST(Tensor_ToSparseDropsSignedZeroKeepsNaN) {
   z::DenseTensor d({0.0f, -0.0f, 1.5f, NAN, 0.0f, -2.0f});
   auto t = z::to_sparse(d);
   EXPECT((t.indices() == std::vector<uint64_t>{2, 3, 5}));
+}
+
+// ---- codec_test.cpp / tensor_test.cpp: every wire format, framing, .zspt ----
+TEST(CooEncoding_SizesFollowTheWidth) {
+  std::mt19937_64 rng(1);
+  auto t = random_tensor(1000, 25, rng);
+  auto msg64 = z::encode(t, z::WireFormat::coo(64));
+  EXPECT(msg64.index_bits == 64u * 25 && msg64.value_bits == 32u * 25);
+  auto msg32 = z::encode(t, z::WireFormat::coo(32));
+  EXPECT(msg32.index_bits == 32u * 25);
+  EXPECT(z::decode(msg64) == t);
+  EXPECT(z::decode(msg32) == t);
+}
+
+TEST(BitmapEncoding_IndexCostIsTheUniverse) {
+  std::mt19937_64 rng(2);
+  auto t = random_tensor(500, 100, rng);
+  auto msg = z::encode(t, z::WireFormat::bitmap());
+  EXPECT(msg.index_bits == 500u && msg.value_bits == 3200u);
+  EXPECT(z::decode(msg) == t);
+}
+
+TEST(EmptyTensor_AllFormatsCarryZeroValueBits) {
+  z::SparseTensor t(64, {}, {});
+  for (auto fmt : {z::WireFormat::coo(), z::WireFormat::bitmap(), z::WireFormat::tensor_block(16)}) {
+    auto msg = z::encode(t, fmt);
+    EXPECT(msg.value_bits == 0u);
+    EXPECT(z::decode(msg) == t);
+  }
+}
+
+TEST(TensorBlockEncoding_ReconstructsShortLastAndCost) {
+  z::SparseTensor t(32, {3, 4, 17}, {1.0f, 2.0f, 3.0f});
+  auto msg = z::encode(t, z::WireFormat::tensor_block(8));
+  EXPECT(msg.index_bits == 2u * 64 && msg.value_bits == 2u * 8 * 32);
+  EXPECT(z::decode(msg) == t);
+  z::SparseTensor s(20, {19}, {5.0f});
+  auto m2 = z::encode(s, z::WireFormat::tensor_block(8));
+  EXPECT(m2.value_bits == 4u * 32);
+  EXPECT(z::decode(m2) == s);
+  std::vector<uint64_t> idx;
+  std::vector<float> val;
+  for (uint64_t b = 0; b < 8; ++b) {
+    idx.push_back(b * 256 + 7);
+    val.push_back(1.0f);
+  }
+  z::SparseTensor u(8 * 256, idx, val);
+  EXPECT(z::encode(u, z::WireFormat::tensor_block(256)).payload_bits() >
+         z::encode(u, z::WireFormat::coo()).payload_bits());
+}
+
+TEST(RoundTrip_RandomTensorsAcrossAllFormats) {
+  std::mt19937_64 rng(77);
+  for (int trial = 0; trial < 30; ++trial) {
+    const uint64_t m = 1 + rng() % 2000;
+    auto t = random_tensor(m, rng() % (m / 2 + 1), rng);
+    for (auto fmt : {z::WireFormat::coo(64), z::WireFormat::coo(32), z::WireFormat::bitmap(),
+                     z::WireFormat::tensor_block(1 + uint32_t(rng() % 300))}) {
+      auto msg = z::encode(t, fmt);
+      EXPECT(msg.payload_bits() == msg.index_bits + msg.value_bits);
+      EXPECT(z::decode(msg) == t);
+      auto sizes = z::message_sizes(t, fmt);
+      EXPECT(sizes.index_bits == msg.index_bits && sizes.value_bits == msg.value_bits);
+    }
+  }
+}
+
+TEST(Framing_RoundTripsAndRejectsTruncation) {
+  std::mt19937_64 rng(111);
+  for (int trial = 0; trial < 10; ++trial) {
+    const uint64_t m = 1 + rng() % 500;
+    auto t = random_tensor(m, rng() % (m / 2 + 1), rng);
+    for (auto fmt : {z::WireFormat::coo(64), z::WireFormat::coo(32), z::WireFormat::bitmap(),
+                     z::WireFormat::tensor_block(7)}) {
+      auto msg = z::encode(t, fmt);
+      std::stringstream ss;
+      z::write_framed(ss, msg);
+      auto back = z::read_framed(ss);
+      EXPECT(back.index_bits == msg.index_bits && back.value_bits == msg.value_bits);
+      EXPECT(back.payload == msg.payload);
+      EXPECT(z::decode(back) == t);
+    }
+  }
+  auto msg = z::encode(random_tensor(100, 10, rng), z::WireFormat::coo());
+  std::stringstream ss;
+  z::write_framed(ss, msg);
+  std::string bytes = ss.str();
+  bytes.resize(bytes.size() - 3);
+  std::stringstream truncated(bytes);
+  EXPECT_THROW(z::read_framed(truncated), z::MalformedPayload);
+}
+
+TEST(Decode_RejectsCorruptCounts) {
+  std::mt19937_64 rng(131);
+  auto msg = z::encode(random_tensor(64, 6, rng), z::WireFormat::bitmap());
+  msg.count += 1;
+  EXPECT_THROW(z::decode(msg), z::MalformedPayload);
+}
+
+TEST(Serialization_RoundTripsAndRejectsBadMagic) {
+  std::mt19937_64 rng(141);
+  auto t = random_tensor(5000, 40, rng);
+  std::stringstream ss;
+  z::write_sparse(ss, t);
+  EXPECT(z::read_sparse(ss) == t);
+  std::stringstream bad(std::string("ZSPX") + std::string(20, '\0'));
+  EXPECT_THROW(z::read_sparse(bad), z::MalformedPayload);
 }
 
 int main() {
