@@ -199,6 +199,15 @@ zen_status zen_frame_header(const zen_wire_format* fmt, const zen_message_info* 
 zen_status zen_frame_parse(const uint8_t* in, uint64_t available, zen_wire_format* fmt,
                            zen_message_info* msg);
 
+/* ---- top-k sparsification: zen::sparsify_topk ------------------------- */
+/* zen/workload.hpp:157-178: the ceil(fraction*m) largest-magnitude entries of
+ * a dense fp32 gradient (ties to the lower index), exact zeros dropped,
+ * ascending -- bit-exact with the reference.  m < 2^32; NaN magnitudes rank
+ * above +inf (the reference's order is undefined for NaN).  *count is set even
+ * when ZEN_E_CAPACITY is returned.  Workspace is cached in the context. */
+zen_status zen_sparsify_topk(zen_ctx* ctx, const float* d_dense, uint64_t m, double fraction,
+                             uint64_t* d_idx, float* d_val, uint64_t capacity, uint64_t* count);
+
 /* ---- Balanced Parallelism: zen::run_balanced_parallelism -------------- */
 /* zen/schemes.hpp:341-417.  rank = ZEN_BP_LOCAL hosts all n workers/servers on
  * this context's GPU (exchange = local stores); otherwise this process is

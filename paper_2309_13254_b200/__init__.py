@@ -13,5 +13,6 @@ from .zen import (  # noqa: F401
     UniverseMismatch, WireFormat, aggregate, bp_universe_table, collision_stats, context, decode,
     derive_seed, encode, hash_memory_layout, hierarchical_hash, imbalance_pull, imbalance_push,
     message_sizes, partition_of, read_framed, read_sparse, read_sparse_file,
-    run_balanced_parallelism, run_bp_with_retry, to_sparse, write_framed, write_sparse,
+    run_balanced_parallelism, run_bp_with_retry, sparsify_topk, to_sparse, write_framed,
+    write_sparse,
     write_sparse_file)

@@ -179,11 +179,26 @@ zen_status upload(T* d, const T* h, size_t count) {
 
 // ------------------------------------------------------------------ ctx ----
 
+// top-k sparsification workspace, kept per context and grown on demand (the
+// staging of the tile pass is 8 B per dense element)
+struct TopkWs {
+  DevMem mem;
+  uint64_t m = 0;
+  void* state = nullptr;
+  uint32_t* hist = nullptr;
+  uint32_t* cand = nullptr;
+  uint32_t cand_cap = 0;
+  ExtractWs<uint32_t> ex{};
+  uint32_t* tile_ties = nullptr;
+  uint64_t *tie_base = nullptr, *out_base = nullptr, *out_count = nullptr;
+};
+
 struct zen_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   zen_universe* ident = nullptr;  // identity universe of the plain Bitmap format (lazy)
+  std::unique_ptr<TopkWs> topk;
 };
 
 extern "C" {
@@ -1049,6 +1064,55 @@ zen_status zen_frame_parse(const uint8_t* in, uint64_t available, zen_wire_forma
 }
 
 }  // extern "C"
+
+// ----------------------------------------------------------------- top-k ----
+// zen::sparsify_topk (zen/workload.hpp:157-178), k_topk.cu
+
+extern "C" zen_status zen_sparsify_topk(zen_ctx* c, const float* d_dense, uint64_t m,
+                                        double fraction, uint64_t* d_idx, float* d_val,
+                                        uint64_t capacity, uint64_t* count) {
+  if (!c || !count) return fail(ZEN_E_INVALID, "null argument");
+  if (!(fraction > 0.0 && fraction <= 1.0)) return fail(ZEN_E_INVALID, "top-k fraction must be in (0,1]");
+  if (m == 0) return fail(ZEN_E_INVALID, "dense tensor must have at least one element");
+  if (m >= 0xFFFFFFFFull) return fail(ZEN_E_INVALID, "top-k universe must be below 2^32");
+  if (!d_dense) return fail(ZEN_E_INVALID, "null dense tensor");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  const uint64_t keep = std::min<uint64_t>(m, (uint64_t)std::ceil(fraction * double(m)));
+  const uint32_t ntiles = uint32_t((m + kExtractTile - 1) / kExtractTile);
+  if (!c->topk || c->topk->m < m) {
+    c->topk.reset(new TopkWs);
+    TopkWs& w = *c->topk;
+    w.m = m;
+    w.cand_cap = uint32_t(std::min<uint64_t>(m, 8ull << 20));
+    CKR(w.mem.alloc((uint8_t**)&w.state, topk_state_bytes()));
+    CKR(w.mem.alloc(&w.hist, 2048));
+    CKR(w.mem.alloc(&w.cand, w.cand_cap, false));
+    CKR(w.mem.alloc(&w.ex.st_idx, uint64_t(ntiles) * kExtractTile, false));
+    CKR(w.mem.alloc(&w.ex.st_val, uint64_t(ntiles) * kExtractTile, false));
+    CKR(w.mem.alloc(&w.ex.tile_cnt, ntiles));
+    CKR(w.mem.alloc(&w.tile_ties, ntiles));
+    CKR(w.mem.alloc(&w.tie_base, ntiles));
+    CKR(w.mem.alloc(&w.out_base, ntiles));
+    CKR(w.mem.alloc(&w.out_count, 1));
+  }
+  TopkWs& w = *c->topk;
+  cudaStream_t st = c->stream;
+  launch_topk_select(d_dense, m, keep, w.state, w.hist, w.cand, w.cand_cap, st);
+  launch_select_tiles(d_dense, m, w.ex,
+                      reinterpret_cast<const uint32_t*>(static_cast<char*>(w.state) +
+                                                        topk_threshold_offset()),
+                      st);
+  launch_topk_finish(w.ex, ntiles, w.state, w.tile_ties, w.tie_base, w.out_base, w.out_count,
+                     d_idx, d_val, capacity, st);
+  CK(cudaGetLastError());
+  uint64_t n = 0;
+  CK(cudaMemcpyAsync(&n, w.out_count, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *count = n;
+  if (n > capacity) return fail(ZEN_E_CAPACITY, "output capacity below the kept entries");
+  return ZEN_OK;
+}
 
 // --------------------------------------------------------------------- BP ----
 

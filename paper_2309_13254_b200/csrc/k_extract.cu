@@ -32,11 +32,30 @@ constexpr int kThreads = 256;
 constexpr int kIters = 4;  // 8-float units per lane
 constexpr int kUnit = 8;
 
-template <typename K>
+// element predicates of the tile pass: to_sparse keeps v != 0.0f
+// (-0.0 dropped, NaN kept; zen/tensor.hpp:94-104); the top-k selection keeps
+// non-zero magnitudes at or above a threshold key (k_topk.cu)
+struct NonZero {
+  __device__ __forceinline__ void init() {}
+  __device__ __forceinline__ bool operator()(float v) const { return v != 0.0f; }
+};
+struct MagnitudeAtLeast {
+  const uint32_t* key_ptr;  // threshold computed on the device (k_topk.cu)
+  uint32_t key;             // |v| as IEEE bits (sign cleared): monotone in |v|
+  __device__ __forceinline__ void init() { key = *key_ptr; }
+  __device__ __forceinline__ bool operator()(float v) const {
+    const uint32_t k = __float_as_uint(v) & 0x7fffffffu;
+    return k >= key && k != 0u;
+  }
+};
+
+template <typename K, typename Pred = NonZero>
 __global__ void __launch_bounds__(kThreads, 4)
     k_extract_tiles(const float* __restrict__ dense, uint64_t m, K* __restrict__ st_idx,
-                    float* __restrict__ st_val, uint32_t* __restrict__ tile_cnt) {
+                    float* __restrict__ st_val, uint32_t* __restrict__ tile_cnt,
+                    Pred pred = Pred()) {
   zen_dev::pdl_entry();
+  pred.init();
   __shared__ uint32_t s_warp_tot[kThreads / 32];
   const uint32_t tile = blockIdx.x;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -59,7 +78,7 @@ __global__ void __launch_bounds__(kThreads, 4)
 #pragma unroll
   for (int j = 0; j < kIters; ++j)
 #pragma unroll
-    for (int c = 0; c < kUnit; ++c) nzbits |= (uint32_t)(v[j].v[c] != 0.0f) << (kUnit * j + c);
+    for (int c = 0; c < kUnit; ++c) nzbits |= (uint32_t)pred(v[j].v[c]) << (kUnit * j + c);
   // in-warp offsets in ascending element order (iteration, lane, component)
   uint32_t off[kIters];
   uint32_t wrun = 0;
@@ -246,7 +265,8 @@ void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* o
                     float* out_val, uint64_t* d_count, uint64_t capacity, uint32_t* d_status_bits,
                     cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  launch_k(k_extract_tiles<K>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
+  launch_k(k_extract_tiles<K, NonZero>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx,
+           ws.st_val, ws.tile_cnt, NonZero());
   launch_k(k_extract_scan<K, false>, 1, 1024, 0, stream, ws.tile_cnt, ntiles, d_count, capacity,
            d_status_bits, ws.tile_base, ws.blk_tile, ws.nblk, HashArgs<K>{});
   launch_k(k_extract_compact<K>, blocks_for(std::min<uint64_t>(capacity, m)), 256, 0, stream,
@@ -259,7 +279,8 @@ template <typename K>
 void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws,
                           cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  launch_k(k_extract_tiles<K>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx, ws.st_val, ws.tile_cnt);
+  launch_k(k_extract_tiles<K, NonZero>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx,
+           ws.st_val, ws.tile_cnt, NonZero());
   count_launch();
 }
 
@@ -279,6 +300,15 @@ void launch_extract_compact_part(uint64_t m, const ExtractWs<K>& ws, const HashA
   launch_k(k_extract_compact_part<K>, (unsigned)std::max<uint64_t>(a.tiles_cap, 1), 256,
            8 * n * sizeof(uint32_t), stream, ws.st_idx, ws.st_val, ws.tile_base, ntiles,
            ws.blk_tile, a);
+  count_launch();
+}
+
+// top-k: stage the non-zero elements with |v| at or above the threshold key
+void launch_select_tiles(const float* dense, uint64_t m, const ExtractWs<uint32_t>& ws,
+                         const uint32_t* key, cudaStream_t stream) {
+  const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
+  launch_k(k_extract_tiles<uint32_t, MagnitudeAtLeast>, ntiles, kThreads, 0, stream, dense, m,
+           ws.st_idx, ws.st_val, ws.tile_cnt, MagnitudeAtLeast{key, 0u});
   count_launch();
 }
 

@@ -1,0 +1,363 @@
+// k_topk.cu -- zen::sparsify_topk (zen/workload.hpp:157-178) on sm_100a:
+// keep the ceil(fraction * M) largest-magnitude entries of a dense fp32
+// gradient, ties broken toward the lower index, exact zeros dropped, output
+// ascending.  Bit-exact with the reference's partial_sort order.
+//
+// The magnitude key is the IEEE bit pattern with the sign cleared, which is
+// monotone in |v| for every non-NaN value.  (The reference's comparator is not
+// a strict weak order on NaN; here NaN magnitudes rank above +inf.)
+//
+// Radix select in three digit levels, [31:21] [20:10] [9:0]:
+//   hist1   full pass over the dense input, 2048-bin histogram of the top digit
+//   select  one block: the digit of the k-th largest key, elements above it
+//   hist2   full pass: histogram of the middle digit among keys in that bucket,
+//           which are also appended to a candidate list (key + index)
+//   select, hist3 over the candidates only, select -> threshold key T and the
+//           number r of T-ties to keep (the r lowest-indexed ones)
+//   tiles   full pass (the extraction tile kernel with predicate |v| >= T,
+//           non-zero): candidates staged tile-locally in index order
+//   scan    one block: per tile, ties before it -> entries it keeps -> output base
+//   compact one block per tile: > T entries, plus ties while the global tie
+//           rank is below r, written in ascending index order.
+// Three HBM passes over the dense input in all; everything else touches the
+// candidates only.
+#include "zen_common.cuh"
+
+namespace zen {
+extern void count_launch();
+namespace {
+
+using namespace zen_dev;
+
+constexpr int kBins = 2048;
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+
+// Level-1 histogram: 32-byte streaming loads, warp-aggregated shared atomics
+// (equal keys -- e.g. the zeros of a sparse gradient -- cost one atomic per warp)
+__global__ void __launch_bounds__(kThreads) k_topk_hist1(const float* __restrict__ dense,
+                                                         uint64_t m, uint32_t* __restrict__ hist) {
+  zen_dev::pdl_entry();
+  __shared__ uint32_t sh[kBins];
+  for (int i = threadIdx.x; i < kBins; i += kThreads) sh[i] = 0;
+  __syncthreads();
+  const uint64_t nvec = m / 8;
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(dense) & 31u) == 0;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < (vec_ok ? nvec : 0);
+       base += stride) {  // warp-uniform trip count
+    const uint64_t u = base + threadIdx.x;
+    f8 v;
+    if (u < nvec) v = ld_stream_f8(dense + u * 8);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t bin = u < nvec ? mag_key(v.v[c]) >> 21 : 0xFFFFFFFFu;
+      const uint32_t grp = __match_any_sync(0xffffffffu, bin);
+      if (bin != 0xFFFFFFFFu && lane_id() == (uint32_t)(__ffs(grp) - 1))
+        atomicAdd(&sh[bin], (uint32_t)__popc(grp));
+    }
+  }
+  const uint64_t tail0 = vec_ok ? nvec * 8 : 0;
+  for (uint64_t i = tail0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < m; i += stride)
+    atomicAdd(&sh[mag_key(dense[i]) >> 21], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins; i += kThreads)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+struct TopkState {
+  uint32_t prefix;  // key bits fixed so far
+  uint32_t k;       // rank (1-based) still to find among keys matching the prefix
+  uint64_t above;   // keys strictly above the current bucket
+  uint32_t T;       // final threshold key
+  uint32_t r;       // ties of T to keep
+  uint32_t ncand;   // candidate list length (level 2)
+  uint32_t nsel;    // |output| before zero dropping is accounted (set by the scan)
+};
+
+// one block: the bucket of the k-th largest key among hist[0..kBins); the
+// histogram is cleared for the next level
+__global__ void __launch_bounds__(1024) k_topk_select(uint32_t* __restrict__ hist, int shift,
+                                                      int digit_bits, TopkState* st, int last) {
+  zen_dev::pdl_entry();
+  __shared__ uint32_t sscan[33];
+  __shared__ uint32_t s_bin, s_above;
+  constexpr int E = kBins / 1024;
+  const uint32_t k = st->k;
+  // suffix sums from the top bin down: thread t owns bins [kBins-1-E*t-E+1 .. kBins-1-E*t]
+  uint32_t c[E], local = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    c[e] = hist[kBins - 1 - (threadIdx.x * E + e)];
+    local += c[e];
+  }
+  uint32_t tot;
+  const uint32_t ex = block_exclusive_sum(local, sscan, &tot);
+  uint32_t run = ex;  // keys in bins above this thread's first bin
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t bin = kBins - 1 - (threadIdx.x * E + e);
+    if (run < k && run + c[e] >= k) {
+      s_bin = bin;
+      s_above = run;
+    }
+    run += c[e];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x == 0) {
+    const uint32_t bin = s_bin;
+    st->prefix |= bin << shift;
+    st->above += s_above;
+    st->k = k - s_above;
+    if (last) {
+      st->T = st->prefix;
+      st->r = st->k;  // ties of T that rank inside the top `keep`
+    }
+  }
+  (void)digit_bits;
+}
+
+// Level 2: full pass; keys whose top digit equals the chosen bucket feed the
+// middle-digit histogram and the candidate list
+__global__ void __launch_bounds__(kThreads) k_topk_hist2(const float* __restrict__ dense,
+                                                         uint64_t m, TopkState* st,
+                                                         uint32_t* __restrict__ hist,
+                                                         uint32_t* __restrict__ cand_key,
+                                                         uint32_t cand_cap) {
+  zen_dev::pdl_entry();
+  __shared__ uint32_t sh[kBins];
+  for (int i = threadIdx.x; i < kBins; i += kThreads) sh[i] = 0;
+  __syncthreads();
+  const uint32_t top = st->prefix >> 21;
+  const uint64_t nvec = m / 8;
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(dense) & 31u) == 0;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint32_t lane = lane_id();
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < (vec_ok ? nvec : 0);
+       base += stride) {
+    const uint64_t u = base + threadIdx.x;
+    f8 v;
+    if (u < nvec) v = ld_stream_f8(dense + u * 8);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t key = u < nvec ? mag_key(v.v[c]) : 0u;
+      const bool hit = u < nvec && (key >> 21) == top;
+      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+      if (!bal) continue;
+      uint32_t pos = 0;
+      if (lane == (uint32_t)(__ffs(bal) - 1)) pos = atomicAdd(&st->ncand, (uint32_t)__popc(bal));
+      pos = __shfl_sync(0xffffffffu, pos, __ffs(bal) - 1) + __popc(bal & lanemask_lt());
+      if (hit) {
+        if (pos < cand_cap) cand_key[pos] = key;
+        atomicAdd(&sh[(key >> 10) & (kBins - 1)], 1u);
+      }
+    }
+  }
+  const uint64_t tail0 = vec_ok ? nvec * 8 : 0;
+  for (uint64_t i = tail0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < m; i += stride) {
+    const uint32_t key = mag_key(dense[i]);
+    if ((key >> 21) == top) {
+      const uint32_t pos = atomicAdd(&st->ncand, 1u);
+      if (pos < cand_cap) cand_key[pos] = key;
+      atomicAdd(&sh[(key >> 10) & (kBins - 1)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins; i += kThreads)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// Level 3: over the candidate keys only (or, if the list overflowed its
+// capacity -- a pathological run of equal magnitudes -- over the dense input)
+__global__ void __launch_bounds__(kThreads) k_topk_hist3(const uint32_t* __restrict__ cand_key,
+                                                         uint32_t cand_cap,
+                                                         const float* __restrict__ dense,
+                                                         uint64_t m, const TopkState* st,
+                                                         uint32_t* __restrict__ hist) {
+  zen_dev::pdl_entry();
+  __shared__ uint32_t sh[kBins];
+  for (int i = threadIdx.x; i < kBins; i += kThreads) sh[i] = 0;
+  __syncthreads();
+  const uint32_t n = st->ncand, mid = st->prefix >> 10;
+  if (n <= cand_cap) {
+    for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
+      const uint32_t key = cand_key[i];
+      if ((key >> 10) == mid) atomicAdd(&sh[key & 1023u], 1u);
+    }
+  } else {
+    for (uint64_t i = blockIdx.x * (uint64_t)kThreads + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * kThreads) {
+      const uint32_t key = mag_key(dense[i]);
+      if ((key >> 10) == mid) atomicAdd(&sh[key & 1023u], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins; i += kThreads)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// ties (key == T) among each tile's staged candidates
+__global__ void __launch_bounds__(kThreads) k_topk_ties(const float* __restrict__ st_val,
+                                                        const uint32_t* __restrict__ tile_cnt,
+                                                        const TopkState* st,
+                                                        uint32_t* __restrict__ tile_ties) {
+  zen_dev::pdl_entry();
+  __shared__ uint32_t s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const uint32_t tile = blockIdx.x, n = tile_cnt[tile], T = st->T;
+  uint32_t c = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads)
+    c += mag_key(st_val[(uint64_t)tile * kExtractTile + i]) == T ? 1u : 0u;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if (lane_id() == 0 && c) atomicAdd(&s_cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_ties[tile] = s_cnt;
+}
+
+// one block over the tiles: ties before each tile -> the tile's kept entries
+// (all > T plus the ties whose global rank is below r) -> output base
+__global__ void __launch_bounds__(1024) k_topk_scan(const uint32_t* __restrict__ tile_cnt,
+                                                    const uint32_t* __restrict__ tile_ties,
+                                                    uint32_t ntiles, TopkState* st,
+                                                    uint64_t* __restrict__ tie_base,
+                                                    uint64_t* __restrict__ out_base,
+                                                    uint64_t* out_count) {
+  zen_dev::pdl_entry();
+  __shared__ uint64_t sscan[33];
+  const uint64_t r = st->T ? st->r : 0;  // T = 0: the ties are zeros, dropped
+  uint64_t tcarry = 0, ocarry = 0;
+  constexpr int E = 8;
+  for (uint32_t b = 0; b < ntiles; b += blockDim.x * E) {
+    const uint32_t t0 = b + threadIdx.x * E;
+    uint64_t ties[E], gt[E], lt = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const bool in = t0 + e < ntiles;
+      ties[e] = in ? tile_ties[t0 + e] : 0;
+      gt[e] = in ? tile_cnt[t0 + e] - ties[e] : 0;
+      lt += ties[e];
+    }
+    uint64_t tt;
+    uint64_t tex = tcarry + block_exclusive_sum(lt, sscan, &tt);
+    uint64_t keep[E], lk = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint64_t take = tex >= r ? 0 : (r - tex < ties[e] ? r - tex : ties[e]);
+      keep[e] = gt[e] + take;
+      if (t0 + e < ntiles) tie_base[t0 + e] = tex;
+      tex += ties[e];
+      lk += keep[e];
+    }
+    uint64_t kt;
+    uint64_t oex = ocarry + block_exclusive_sum(lk, sscan, &kt);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (t0 + e < ntiles) out_base[t0 + e] = oex;
+      oex += keep[e];
+    }
+    tcarry += tt;
+    ocarry += kt;
+  }
+  if (threadIdx.x == 0) *out_count = ocarry;
+}
+
+// one block per tile: stable selection of the staged candidates
+__global__ void __launch_bounds__(kThreads) k_topk_compact(
+    const uint32_t* __restrict__ st_idx, const float* __restrict__ st_val,
+    const uint32_t* __restrict__ tile_cnt, const uint64_t* __restrict__ tie_base,
+    const uint64_t* __restrict__ out_base, const TopkState* st, uint64_t* __restrict__ out_idx,
+    float* __restrict__ out_val, uint64_t cap) {
+  zen_dev::pdl_entry();
+  __shared__ uint32_t s_warp[2][kThreads / 32];
+  const uint32_t tile = blockIdx.x, n = tile_cnt[tile], T = st->T;
+  const uint64_t r = T ? st->r : 0;
+  uint64_t tb = tie_base[tile], ob = out_base[tile];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (uint32_t c0 = 0; c0 < n; c0 += kThreads) {
+    const uint32_t i = c0 + threadIdx.x;
+    const bool in = i < n;
+    const uint64_t src = (uint64_t)tile * kExtractTile + i;
+    const float v = in ? st_val[src] : 0.0f;
+    const uint32_t key = mag_key(v);
+    const bool tie = in && key == T;
+    // rank of this tie among the tile's ties so far (block scan of tie flags)
+    const uint32_t tbal = __ballot_sync(0xffffffffu, tie);
+    if (lane == 0) s_warp[0][warp] = __popc(tbal);
+    __syncthreads();
+    uint32_t tw = 0, ttot = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const uint32_t x = s_warp[0][w];
+      tw += w < (int)warp ? x : 0u;
+      ttot += x;
+    }
+    const uint64_t trank = tb + tw + __popc(tbal & lanemask_lt());
+    const bool keep = in && (key > T || (tie && trank < r));
+    const uint32_t kbal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_warp[1][warp] = __popc(kbal);
+    __syncthreads();
+    uint32_t kw = 0, ktot = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const uint32_t x = s_warp[1][w];
+      kw += w < (int)warp ? x : 0u;
+      ktot += x;
+    }
+    if (keep) {
+      const uint64_t pos = ob + kw + __popc(kbal & lanemask_lt());
+      if (pos < cap) {
+        out_idx[pos] = st_idx[src];
+        out_val[pos] = v;
+      }
+    }
+    tb += ttot;
+    ob += ktot;
+    __syncthreads();
+  }
+}
+
+inline unsigned pass_grid(uint64_t m) {
+  const uint64_t g = (m / 8 + kThreads - 1) / kThreads;
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, 148 * 8));
+}
+
+}  // namespace
+
+size_t topk_state_bytes() { return sizeof(TopkState); }
+size_t topk_threshold_offset() { return offsetof(TopkState, T); }
+
+// radix select of the threshold: state, histogram and candidates on `s`
+void launch_topk_select(const float* dense, uint64_t m, uint64_t keep, void* state_v,
+                        uint32_t* hist, uint32_t* cand_key, uint32_t cand_cap, cudaStream_t s) {
+  TopkState* st = static_cast<TopkState*>(state_v);
+  TopkState init{};
+  init.k = (uint32_t)keep;
+  cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(hist, 0, kBins * sizeof(uint32_t), s);
+  launch_k(k_topk_hist1, pass_grid(m), kThreads, 0, s, dense, m, hist);
+  launch_k(k_topk_select, 1, 1024, 0, s, hist, 21, 11, st, 0);
+  launch_k(k_topk_hist2, pass_grid(m), kThreads, 0, s, dense, m, st, hist, cand_key, cand_cap);
+  launch_k(k_topk_select, 1, 1024, 0, s, hist, 10, 11, st, 0);
+  launch_k(k_topk_hist3, 148 * 4, kThreads, 0, s, cand_key, cand_cap, dense, m, st, hist);
+  launch_k(k_topk_select, 1, 1024, 0, s, hist, 0, 10, st, 1);
+  for (int i = 0; i < 6; ++i) count_launch();
+}
+
+// after the tile pass staged the >= T candidates (launch_select_tiles)
+void launch_topk_finish(const ExtractWs<uint32_t>& ws, uint32_t ntiles, void* state_v,
+                        uint32_t* tile_ties, uint64_t* tie_base, uint64_t* out_base,
+                        uint64_t* out_count, uint64_t* out_idx, float* out_val, uint64_t cap,
+                        cudaStream_t s) {
+  TopkState* st = static_cast<TopkState*>(state_v);
+  launch_k(k_topk_ties, ntiles, kThreads, 0, s, ws.st_val, ws.tile_cnt, st, tile_ties);
+  launch_k(k_topk_scan, 1, 1024, 0, s, ws.tile_cnt, tile_ties, ntiles, st, tie_base, out_base,
+           out_count);
+  launch_k(k_topk_compact, ntiles, kThreads, 0, s, ws.st_idx, ws.st_val, ws.tile_cnt, tie_base,
+           out_base, st, out_idx, out_val, cap);
+  for (int i = 0; i < 3; ++i) count_launch();
+}
+
+}  // namespace zen

@@ -285,6 +285,18 @@ void launch_tb_expand_select(const uint8_t* payload, uint64_t nb, uint64_t block
 void launch_sort_pairs(const uint64_t* ki, uint64_t* ko, const float* vi, float* vo,
                        uint64_t count, void* tmp, size_t tmp_bytes, cudaStream_t s);
 
+// top-k sparsification (k_topk.cu + the tile pass of k_extract.cu)
+size_t topk_state_bytes();
+size_t topk_threshold_offset();
+void launch_topk_select(const float* dense, uint64_t m, uint64_t keep, void* state,
+                        uint32_t* hist, uint32_t* cand_key, uint32_t cand_cap, cudaStream_t s);
+void launch_select_tiles(const float* dense, uint64_t m, const ExtractWs<uint32_t>& ws,
+                         const uint32_t* key, cudaStream_t stream);
+void launch_topk_finish(const ExtractWs<uint32_t>& ws, uint32_t ntiles, void* state,
+                        uint32_t* tile_ties, uint64_t* tie_base, uint64_t* out_base,
+                        uint64_t* out_count, uint64_t* out_idx, float* out_val, uint64_t cap,
+                        cudaStream_t s);
+
 // RAII launch policy for the calling thread (see zen_common.cuh launch_k)
 struct LaunchScope {
   LaunchScope(bool pdl, bool low_priority);

@@ -576,6 +576,30 @@ def decode(msg: EncodedMessage, universe: HashUniverse | None = None) -> SparseT
                         ov[:z].cpu().numpy(), _trusted=True)
 
 
+def sparsify_topk(dense, fraction: float) -> SparseTensor:
+    """zen::sparsify_topk (workload.hpp:157-178) on the GPU: the
+    ceil(fraction*M) largest |v| (ties to the lower index), zeros dropped.
+    `dense`: DenseTensor, numpy array or CUDA tensor (fp32)."""
+    torch = _torch()
+    ctx = context()
+    if isinstance(dense, DenseTensor):
+        dense = dense.values
+    d = dense if (hasattr(dense, "is_cuda") and dense.is_cuda) else _dev(np.asarray(dense,
+                                                                               np.float32),
+                                                                    torch.float32)
+    d = d.reshape(-1).contiguous()
+    m = d.numel()
+    keep = min(m, math.ceil(fraction * m)) if 0 < fraction <= 1 else 1
+    oi = torch.empty(max(keep, 1), dtype=torch.int64, device=d.device)
+    ov = torch.empty(max(keep, 1), dtype=torch.float32, device=d.device)
+    got = C.c_uint64()
+    _check(_lib().zen_sparsify_topk(ctx.h, _ptr(d), m, float(fraction), _ptr(oi), _ptr(ov), keep,
+                                    C.byref(got)))
+    z = got.value
+    return SparseTensor(m, oi[:z].cpu().numpy().view(np.uint64), ov[:z].cpu().numpy(),
+                        _trusted=True)
+
+
 def message_sizes(t: SparseTensor, fmt: WireFormat, universe: HashUniverse | None = None):
     """zen::message_sizes (codec.hpp:182-211): (index_bits, value_bits)."""
     m = encode(t, fmt, universe)
