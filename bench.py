@@ -49,6 +49,8 @@ def parse():
                     help="extra: also time n emulated workers on one GPU (local mode)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the top-k / wire-format measurements (SURVEY §8f)")
     return ap.parse_args()
 
 
@@ -209,6 +211,98 @@ def cpu_reference_step(args, n, dense_list, budget_s=12.0):
                        f"universe table {res['table_ms']:.0f} ms excluded)"),
             "stages_ms": {"to_sparse": round(res["to_sparse_ms"], 3),
                           "sync": round(res["sync_ms"], 3), "table_once": round(res["table_ms"], 1)}}
+
+
+# ------------------------------------------------------------ extras (f1/f2) ----
+
+def measure_extras(args, zen, d_dense, peak, reps=10):
+    """The components either side of the sync: top-k
+    sparsification of the dense gradient (f2) and the COO / tensor-block wire
+    formats of its sparse form (f1), each a synchronous C-ABI call on
+    device-resident data, timed with CUDA events; the reference's CPU path on
+    a bounded sample beside it."""
+    import ctypes as C
+    import torch
+    lib = zen.load()
+    ctx = zen.context()
+    ctx.bind_stream()
+    stream = torch.cuda.current_stream()
+    m = d_dense.numel()
+    out = {}
+    frac = args.density
+    keep = min(m, int(np.ceil(frac * m)))
+    oi = torch.empty(keep, dtype=torch.int64, device="cuda")
+    ov = torch.empty(keep, dtype=torch.float32, device="cuda")
+    got = C.c_uint64()
+
+    def topk():
+        rc = lib.zen_sparsify_topk(ctx.h, C.c_void_p(d_dense.data_ptr()), m, frac,
+                                   C.c_void_p(oi.data_ptr()), C.c_void_p(ov.data_ptr()), keep,
+                                   C.byref(got))
+        assert rc == 0, lib.zen_last_error_message()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    t = timed(topk)
+    one_pass = 4 * m + 12 * got.value
+    out["sparsify_topk"] = {
+        "fraction": frac, "kept": int(got.value), "ms_per_call": round(t, 4),
+        "hbm_frac_of_one_pass": round(one_pass / (t * 1e-3) / 1e9 / peak, 4),
+        "note": "radix select: 3 HBM passes over the dense input; frac vs a single 4M-byte read"}
+    # the wire formats of the extracted sparse gradient
+    nz = torch.nonzero(d_dense).flatten()
+    vals = d_dense[nz].contiguous()
+    cnt = nz.numel()
+    for name, f in [("coo64", zen.WireFormat.coo()), ("tensor_block256", zen.WireFormat.tensor_block())]:
+        fc = f._c()
+        info = zen._lib.MessageInfoC()
+        lib.zen_encode(ctx.h, C.byref(fc), None, 0, C.c_void_p(nz.data_ptr()),
+                       C.c_void_p(vals.data_ptr()), cnt, m, None, 0, C.byref(info))
+        pay = torch.empty(max(int(info.payload_bytes), 1), dtype=torch.uint8, device="cuda")
+        di = torch.empty(cnt, dtype=torch.int64, device="cuda")
+        dv = torch.empty(cnt, dtype=torch.float32, device="cuda")
+        n2 = C.c_uint64()
+
+        def enc():
+            assert lib.zen_encode(ctx.h, C.byref(fc), None, 0, C.c_void_p(nz.data_ptr()),
+                                  C.c_void_p(vals.data_ptr()), cnt, m, C.c_void_p(pay.data_ptr()),
+                                  int(info.payload_bytes), C.byref(info)) == 0
+
+        def dec():
+            assert lib.zen_decode(ctx.h, C.byref(fc), None, 0, C.byref(info),
+                                  C.c_void_p(pay.data_ptr()), C.c_void_p(di.data_ptr()),
+                                  C.c_void_p(dv.data_ptr()), cnt, C.byref(n2)) == 0
+        te, td = timed(enc), timed(dec)
+        out[name] = {"entries": cnt, "payload_bytes": int(info.payload_bytes),
+                     "encode_ms": round(te, 4), "decode_ms": round(td, 4),
+                     "encode_GBps": round(info.payload_bytes / (te * 1e-3) / 1e9, 1),
+                     "decode_GBps": round(info.payload_bytes / (td * 1e-3) / 1e9, 1)}
+    # the reference's CPU sparsify_topk on a bounded sample (a 4M-element prefix)
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import ref_oracle
+        ro = ref_oracle()
+        if ro is not None:
+            sample = d_dense[: 1 << 22].cpu().numpy()
+            t0 = time.perf_counter()
+            ro.sparsify_topk(sample, frac)
+            dt = (time.perf_counter() - t0) * 1e3
+            out["sparsify_topk"]["cpu_reference"] = {
+                "ms": round(dt, 2), "cores": 1, "kind": "reference",
+                "sample": f"4,194,304-element prefix of the dense gradient (x{m / (1 << 22):.1f} "
+                          f"for the full tensor: ~{dt * m / (1 << 22):.0f} ms)"}
+    except Exception as e:  # the CPU sample is informational
+        out["sparsify_topk"]["cpu_reference"] = {"error": str(e)[:200]}
+    return out
 
 
 # --------------------------------------------------------------- our arm ----
@@ -456,6 +550,8 @@ def main():
         line["per_rank"] = per_rank
     if emu:
         line["emulated_local"] = emu
+    if world == 1 and not args.no_extras:
+        line["extras"] = measure_extras(args, zen, d_dense, peak)
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_reference_step(args, n, [host])
     print(json.dumps(line), flush=True)

@@ -193,13 +193,59 @@ struct TopkWs {
   uint64_t *tie_base = nullptr, *out_base = nullptr, *out_count = nullptr;
 };
 
+// grow-only device scratch of a context, carved up by one synchronous call at
+// a time (the API is externally synchronous per context, like the reference)
+struct Scratch {
+  char* base = nullptr;
+  size_t cap = 0;
+  ~Scratch() {
+    if (base) cudaFree(base);
+  }
+};
+struct Bump {
+  char* p = nullptr;
+  size_t used = 0;
+  template <typename T>
+  T* get(size_t n) {
+    T* r = reinterpret_cast<T*>(p + used);
+    used += align256(std::max<size_t>(n, 1) * sizeof(T));
+    return r;
+  }
+};
+inline size_t bump_bytes(std::initializer_list<size_t> sizes) {
+  size_t t = 0;
+  for (size_t b : sizes) t += align256(std::max<size_t>(b, 1));
+  return t;
+}
+
 struct zen_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   zen_universe* ident = nullptr;  // identity universe of the plain Bitmap format (lazy)
   std::unique_ptr<TopkWs> topk;
+  Scratch scratch;
 };
+
+namespace {
+zen_status ctx_scratch(zen_ctx* c, size_t bytes, Bump* out) {
+  if (c->scratch.cap < bytes) {
+    CK(cudaStreamSynchronize(c->stream));
+    const size_t want = std::max(bytes, c->scratch.cap * 2);
+    if (c->scratch.base) cudaFree(c->scratch.base);
+    c->scratch.base = nullptr;
+    c->scratch.cap = 0;
+    if (cudaMalloc(&c->scratch.base, want) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ZEN_E_OOM, "cudaMalloc (scratch) failed");
+    }
+    c->scratch.cap = want;
+  }
+  out->p = c->scratch.base;
+  out->used = 0;
+  return ZEN_OK;
+}
+}  // namespace
 
 extern "C" {
 
@@ -823,9 +869,12 @@ zen_status zen_encode(zen_ctx* c, const zen_wire_format* f, zen_universe* u, uin
   if (count && (!d_idx || !d_val)) return fail(ZEN_E_INVALID, "null tensor");
   DevGuard g(c->device);
   SetupStream setup_(c->stream);
-  DevMem mem;
-  uint32_t* st;
-  CKR(mem.alloc(&st, 1));
+  const bool tb = f->kind == ZEN_WIRE_TENSOR_BLOCK;
+  Bump sc;
+  CKR(ctx_scratch(c, bump_bytes({4, tb ? 4 * count : 0, tb ? 4 * count : 0,
+                                 tb ? wire_scan_bytes(count) : 0}), &sc));
+  uint32_t* st = sc.get<uint32_t>(1);
+  CK(cudaMemsetAsync(st, 0, 4, c->stream));
   CKR(wire_check_input(c, d_idx, count, m, st));
   zen_message_info info{m, count, 0, 32 * count, 0};
   switch (f->kind) {
@@ -867,12 +916,11 @@ zen_status zen_encode(zen_ctx* c, const zen_wire_format* f, zen_universe* u, uin
       uint64_t nb = 0, last = 0;
       uint32_t *first = nullptr, *bpos = nullptr;
       if (count) {
-        const size_t tb = wire_scan_bytes(count);
-        void* tmp;
-        CKR(mem.alloc(&first, count));
-        CKR(mem.alloc(&bpos, count));
-        CKR(mem.alloc((uint8_t**)&tmp, std::max<size_t>(tb, 1)));
-        launch_tb_blocks(d_idx, count, B, first, bpos, tmp, tb, c->stream);
+        const size_t tmp_bytes = wire_scan_bytes(count);
+        first = sc.get<uint32_t>(count);
+        bpos = sc.get<uint32_t>(count);
+        void* tmp = sc.get<uint8_t>(tmp_bytes);
+        launch_tb_blocks(d_idx, count, B, first, bpos, tmp, tmp_bytes, c->stream);
         uint32_t hb = 0;
         CK(cudaMemcpyAsync(&hb, bpos + count - 1, 4, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(&last, d_idx + count - 1, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -907,9 +955,15 @@ zen_status zen_decode(zen_ctx* c, const zen_wire_format* f, zen_universe* u, uin
   if (len && !d_payload) return fail(ZEN_E_INVALID, "null payload");
   DevGuard g(c->device);
   SetupStream setup_(c->stream);
-  DevMem mem;
-  uint32_t* st;
-  CKR(mem.alloc(&st, 1));
+  const uint64_t slots = f->kind == ZEN_WIRE_TENSOR_BLOCK ? n * f->block_size : 0;
+  const uint64_t maxout = f->kind == ZEN_WIRE_TENSOR_BLOCK ? slots : n;
+  Bump sc;
+  CKR(ctx_scratch(c, bump_bytes({4, 8, 8 * n, 8 * n, 4 * n, 8 * slots, 4 * slots, slots,
+                                 8 * slots, 4 * slots, wire_select_bytes(slots), 8 * maxout,
+                                 4 * maxout, wire_sort_bytes(maxout)}),
+                  &sc));
+  uint32_t* st = sc.get<uint32_t>(1);
+  CK(cudaMemsetAsync(st, 0, 4, c->stream));
   uint64_t got = 0;
   switch (f->kind) {
     case ZEN_WIRE_COO: {
@@ -937,31 +991,30 @@ zen_status zen_decode(zen_ctx* c, const zen_wire_format* f, zen_universe* u, uin
     }
     default: {  // ZEN_WIRE_TENSOR_BLOCK
       const uint64_t B = f->block_size;
-      const uint64_t slots = n * B;
-      uint64_t *off, *begin, *sidx, *dcount;
-      uint32_t* blen;
-      float* sval;
-      uint8_t* flag;
-      CKR(mem.alloc(&off, std::max<uint64_t>(n, 1)));
-      CKR(mem.alloc(&begin, std::max<uint64_t>(n, 1)));
-      CKR(mem.alloc(&blen, std::max<uint64_t>(n, 1)));
-      CKR(mem.alloc(&dcount, 1));
-      launch_tb_walk(d_payload, len, n, B, m, off, begin, blen, st, c->stream);
+      uint64_t* dcount = sc.get<uint64_t>(1);
+      uint64_t* off = sc.get<uint64_t>(n);
+      uint64_t* begin = sc.get<uint64_t>(n);
+      uint32_t* blen = sc.get<uint32_t>(n);
+      // parallel offsets for a regular payload; the sequential walk otherwise
+      launch_tb_offsets(d_payload, len, n, B, m, off, begin, blen, st, c->stream);
       uint32_t h = 0;
       CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
-      if (h) return wire_status(h);
+      if ((h & kWireIrregularLayout) || (n == 0 && len != 0)) {
+        CK(cudaMemsetAsync(st, 0, 4, c->stream));
+        launch_tb_walk(d_payload, len, n, B, m, off, begin, blen, st, c->stream);
+        CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (h) return wire_status(h);
+      }
       if (slots) {
+        uint64_t* sidx = sc.get<uint64_t>(slots);
+        float* sval = sc.get<float>(slots);
+        uint8_t* flag = sc.get<uint8_t>(slots);
+        uint64_t* oi = sc.get<uint64_t>(slots);
+        float* ov = sc.get<float>(slots);
         const size_t tb = wire_select_bytes(slots);
-        void* tmp;
-        uint64_t* oi;
-        float* ov;
-        CKR(mem.alloc(&sidx, slots));
-        CKR(mem.alloc(&sval, slots));
-        CKR(mem.alloc(&flag, slots));
-        CKR(mem.alloc(&oi, slots));
-        CKR(mem.alloc(&ov, slots));
-        CKR(mem.alloc((uint8_t**)&tmp, std::max<size_t>(tb, 1)));
+        void* tmp = sc.get<uint8_t>(tb);
         launch_tb_expand_select(d_payload, n, B, off, begin, blen, sidx, sval, flag, oi, ov,
                                 dcount, tmp, tb, c->stream);
         CK(cudaMemcpyAsync(&got, dcount, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -984,12 +1037,9 @@ zen_status zen_decode(zen_ctx* c, const zen_wire_format* f, zen_universe* u, uin
   CK(cudaStreamSynchronize(c->stream));
   if (h & kWireUnsorted) {
     const size_t tb = wire_sort_bytes(got);
-    void* tmp;
-    uint64_t* ki;
-    float* vi;
-    CKR(mem.alloc(&ki, got));
-    CKR(mem.alloc(&vi, got));
-    CKR(mem.alloc((uint8_t**)&tmp, std::max<size_t>(tb, 1)));
+    uint64_t* ki = sc.get<uint64_t>(got);
+    float* vi = sc.get<float>(got);
+    void* tmp = sc.get<uint8_t>(tb);
     CK(cudaMemcpyAsync(ki, d_idx, got * 8, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(vi, d_val, got * 4, cudaMemcpyDeviceToDevice, c->stream));
     launch_sort_pairs(ki, d_idx, vi, d_val, got, tmp, tb, c->stream);

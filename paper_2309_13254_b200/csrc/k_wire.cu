@@ -144,6 +144,40 @@ __global__ void k_tb_walk(const uint8_t* __restrict__ payload, uint64_t len, uin
   if (pos != len) atomicOr(status, kWireMalformed);
 }
 
+// TensorBlock decode, fast pass 1: every block of a well-formed, ascending
+// payload sits at b * (8 + 4 * block) -- only the universe's last block can
+// be shorter, and it is then the last one.  Anything else (including every
+// malformed payload) sets kWireIrregular and the host reruns the sequential
+// walk above, which reproduces the reference's reading exactly.
+constexpr uint32_t kWireIrregular = 32u;
+__global__ void k_tb_offsets(const uint8_t* __restrict__ payload, uint64_t len, uint64_t count,
+                             uint64_t block, uint64_t m, uint64_t* __restrict__ off,
+                             uint64_t* __restrict__ begin, uint32_t* __restrict__ blen,
+                             uint32_t* status) {
+  zen_dev::pdl_entry();
+  const uint64_t stride = 8 + 4 * block;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < count;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pos = b * stride;
+    if (pos + 8 > len) {
+      atomicOr(status, kWireIrregular);
+      continue;
+    }
+    const uint64_t bg = get_bytes(payload + pos, 8) * block;
+    if (bg >= m) {
+      atomicOr(status, kWireIrregular);
+      continue;
+    }
+    const uint64_t l = (m - bg < block) ? m - bg : block;
+    const uint64_t end = pos + 8 + 4 * l;
+    if ((l != block && b + 1 != count) || end > len || (b + 1 == count && end != len))
+      atomicOr(status, kWireIrregular);
+    off[b] = pos + 8;
+    begin[b] = bg;
+    blen[b] = (uint32_t)l;
+  }
+}
+
 // pass 2: every value slot -> (index, value, non-zero flag)
 __global__ void k_tb_expand(const uint8_t* __restrict__ payload, uint64_t nb, uint64_t block,
                             const uint64_t* __restrict__ off, const uint64_t* __restrict__ begin,
@@ -233,6 +267,15 @@ void launch_tb_walk(const uint8_t* payload, uint64_t len, uint64_t count, uint64
                     uint64_t m, uint64_t* off, uint64_t* begin, uint32_t* blen, uint32_t* status,
                     cudaStream_t s) {
   launch_k(k_tb_walk, 1, 32, 0, s, payload, len, count, block, m, off, begin, blen, status);
+  count_launch();
+}
+
+void launch_tb_offsets(const uint8_t* payload, uint64_t len, uint64_t count, uint64_t block,
+                       uint64_t m, uint64_t* off, uint64_t* begin, uint32_t* blen,
+                       uint32_t* status, cudaStream_t s) {
+  if (!count) return;
+  launch_k(k_tb_offsets, grid_for(count), 256, 0, s, payload, len, count, block, m, off, begin,
+           blen, status);
   count_launch();
 }
 

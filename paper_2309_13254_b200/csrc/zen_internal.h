@@ -277,6 +277,10 @@ void launch_tb_write(const uint64_t* idx, const float* val, uint64_t count, uint
 void launch_tb_walk(const uint8_t* payload, uint64_t len, uint64_t count, uint64_t block,
                     uint64_t m, uint64_t* off, uint64_t* begin, uint32_t* blen, uint32_t* status,
                     cudaStream_t s);
+constexpr uint32_t kWireIrregularLayout = 32u;  // k_tb_offsets: fall back to the walk
+void launch_tb_offsets(const uint8_t* payload, uint64_t len, uint64_t count, uint64_t block,
+                       uint64_t m, uint64_t* off, uint64_t* begin, uint32_t* blen,
+                       uint32_t* status, cudaStream_t s);
 void launch_tb_expand_select(const uint8_t* payload, uint64_t nb, uint64_t block,
                              const uint64_t* off, const uint64_t* begin, const uint32_t* blen,
                              uint64_t* sidx, float* sval, uint8_t* flag, uint64_t* out_idx,
