@@ -11,6 +11,7 @@ tracked evidence under profiles/<tag>/:
 and refresh profiles/ncu_traffic.json (DRAM bytes per launch of the
 roofline kernel, read by bench.py)."""
 import collections
+import re
 import csv
 import io
 import json
@@ -81,19 +82,23 @@ def main(tag):
     lines = []
     if os.path.exists(os.path.join(src, "launches.csv")):
         per = launch_table(os.path.join(src, "launches.csv"))
-        steady = {k: v for k, v in per.items() if not k.startswith("k_tables")}
-        nsync = min(len(v) for v in steady.values()) if steady else 0
+        extra = re.compile(r"k_topk|MagnitudeAtLeast|at_cuda_detail|at::|k_check_canonical|"
+                           r"k_coo_|k_tb_|CUB_|k_tables")
+        steady = {k: v for k, v in per.items() if not extra.search(k)}
+        counts = sorted(len(v) for v in steady.values())
+        nsync = counts[len(counts) // 2] if counts else 0
         step = sum(sum(v) / len(v) for v in steady.values())
         lines += [f"# Launch list ({tag}): ncu --metrics gpu__time_duration.sum --clock-control none",
                   "", "Cold-cache, serialised per-launch times (ncu replays each launch); "
                   "the SHARE of the sync is what compares with bench.py's live numbers.", "",
-                  f"syncs captured: {nsync}; sum of per-kernel means: {step:.1f} us "
+                  f"syncs captured: {nsync}; one sync = sum of per-kernel means: {step:.1f} us "
                   "(k_place/k_depth/k_serial_*/k_fallback run on the forked side stream, "
                   "overlapped with the data path in the live run)", "",
                   "| kernel | launches | mean us | share of sync |", "|---|---|---|---|"]
         for k, v in per.items():
             m = sum(v) / len(v)
-            share = f"{100 * m / step:.1f}%" if k in steady else "setup (once)"
+            share = (f"{100 * m / step:.1f}%" if k in steady else
+                     "setup (once)" if k.startswith("k_tables") else "not in the sync")
             lines.append(f"| {k} | {len(v)} | {m:.2f} | {share} |")
         open(os.path.join(dst, "launch_summary.md"), "w").write("\n".join(lines) + "\n")
     rep = os.path.join(src, "full.ncu-rep")

@@ -14,7 +14,7 @@ timeout 600 ./build/compat_test > "$OUT/compat_test.log" 2>&1; echo "compat rc=$
 timeout 900 python bench.py --impl reference > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"; echo "ref rc=$?" >> "$OUT/status"
 timeout 900 python bench.py --emulate 8 > "$OUT/bench.json" 2> "$OUT/bench.err"
 rc=$?; echo "bench rc=$rc" >> "$OUT/status"
-SHORT="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu"
+SHORT="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-extras"
 timeout 600 $SHORT > "$OUT/short.json" 2> "$OUT/short.err"
 rc2=$?; echo "short rc=$rc2" >> "$OUT/status"
 if [ $rc2 -eq 0 ]; then
