@@ -98,7 +98,7 @@ def main(tag):
         for k, v in per.items():
             m = sum(v) / len(v)
             share = (f"{100 * m / step:.1f}%" if k in steady else
-                     "setup (once)" if k.startswith("k_tables") else "not in the sync")
+                     "setup (once)" if "k_tables" in k else "not in the sync")
             lines.append(f"| {k} | {len(v)} | {m:.2f} | {share} |")
         open(os.path.join(dst, "launch_summary.md"), "w").write("\n".join(lines) + "\n")
     rep = os.path.join(src, "full.ncu-rep")
