@@ -115,11 +115,13 @@ EXPORTED = tuple(_SIGS)
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libzen_b200.so (raises if it was never built -- no fallback)."""
+def load(path: str | None = None):
+    """Load libzen_b200.so (raises if it was never built -- no fallback).
+    ZEN_B200_LIB selects another build of the same library (A/B timing)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("ZEN_B200_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} missing: build it with `make lib` (no CPU fallback exists)")
     lib = C.CDLL(path)

@@ -1366,6 +1366,9 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   a.in_idx = in_idx;
   a.in_val = in_val;
   a.in_hdr = in_hdr;
+  const uint32_t** in_load;
+  CKR(mem.alloc(&in_load, n));
+  a.in_load = in_load;
   a.in_count = nullptr;
   a.own = bp->uni->own[s.id];
   a.bs = bp->uni->bs[s.id];
@@ -1404,7 +1407,12 @@ zen_status bp_wire(zen_bp* bp) {
     CKR(upload(const_cast<uint32_t**>(w.a.dst_idx), di.data(), n));
     CKR(upload(const_cast<float**>(w.a.dst_val), dv.data(), n));
     CKR(upload(const_cast<PushHdr**>(w.a.push_hdr), ph.data(), n));
+    // local mode: the servers read the workers' counters directly, so there
+    // is no push header / signal kernel
+    if (bp->local) w.a.push_hdr = nullptr;
   }
+  std::vector<const uint32_t*> loads;
+  for (auto& w : bp->workers) loads.push_back(w.a.load);
   for (auto& s : bp->servers) {
     const Arena& A = bp->arena_of(s.id);
     const ArenaLayout& L = bp->layout_of(s.id);
@@ -1419,6 +1427,10 @@ zen_status bp_wire(zen_bp* bp) {
     CKR(upload(const_cast<const uint32_t**>(s.a.in_idx), ii.data(), n));
     CKR(upload(const_cast<const float**>(s.a.in_val), iv.data(), n));
     CKR(upload(const_cast<const PushHdr**>(s.a.in_hdr), ih.data(), n));
+    if (bp->local) {
+      CKR(upload(const_cast<const uint32_t**>(s.a.in_load), loads.data(), n));
+      s.a.in_hdr = nullptr;
+    }
     std::vector<unsigned long long*> db(s.a.ndst);
     std::vector<float*> dvv(s.a.ndst);
     std::vector<PullHdr*> dh(s.a.ndst);
@@ -1808,6 +1820,17 @@ zen_status bp_collect(zen_bp* bp) {
     bp->h_nnz[w] = ph[w].nnz;
     bp->h_agg[w] = pl[w].agg_count;
   }
+  if (bp->local) {  // no push headers in local mode: the workers' own counters
+    std::vector<uint32_t> ld(n);
+    for (size_t i = 0; i < bp->workers.size(); ++i) {
+      const uint32_t w = bp->workers[i].id;
+      CK(cudaMemcpy(ld.data(), bp->workers[i].a.load, n * 4, cudaMemcpyDeviceToHost));
+      const bool cap_ok = !(hh[i].status & kErrCapacity);
+      for (uint32_t s = 0; s < n; ++s) bp->h_counts[size_t(w) * n + s] = cap_ok ? ld[s] : 0;
+      bp->h_nnz[w] = hh[i].count;
+      ph[w].ovf_word = hh[i].ovf_word;
+    }
+  }
   if (bp->local)  // no pull headers in local mode: U_s from each server's counter
     for (auto& s : bp->servers) {
       CK(cudaMemcpy(&bp->h_agg[s.id], s.agg_count, 8, cudaMemcpyDeviceToHost));
@@ -2098,7 +2121,13 @@ extern "C" zen_status zen_bp_debug_part(zen_bp* bp, int what, uint32_t server, u
   if (!A.base || (!bp->local && server != bp->rank)) return fail(ZEN_E_INVALID, "server not local");
   const ArenaLayout& L = bp->layout_of(server);
   PushHdr ph{};
-  CK(cudaMemcpy(&ph, A.push_hdr(L) + worker, sizeof(ph), cudaMemcpyDeviceToHost));
+  if (bp->local) {
+    if (worker >= bp->workers.size()) return fail(ZEN_E_INVALID, "bad worker");
+    CK(cudaMemcpy(&ph.counts[server], bp->workers[worker].a.load + server, 4,
+                  cudaMemcpyDeviceToHost));
+  } else {
+    CK(cudaMemcpy(&ph, A.push_hdr(L) + worker, sizeof(ph), cudaMemcpyDeviceToHost));
+  }
   *count = ph.counts[server];
   const uint64_t c = std::min<uint64_t>(cap, ph.counts[server]);
   CK(cudaMemcpy(h_idx, A.inbox_idx(L) + size_t(worker) * bp->cap, c * 4, cudaMemcpyDeviceToHost));

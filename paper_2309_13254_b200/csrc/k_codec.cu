@@ -129,7 +129,9 @@ constexpr int kPrefixThreads = 512;  // union / bpre blocks
 constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (4)
 
 __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
-  return a.in_hdr ? *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s] : (uint32_t)a.in_count[w];
+  if (a.in_hdr) return *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s];  // peers (rank mode)
+  if (a.in_load) return a.in_load[w][a.s];  // local mode: the workers' own counters
+  return (uint32_t)a.in_count[w];
 }
 
 // Phase 1: every received entry sets its HashBitmap position (its rank in I_s,

@@ -203,7 +203,8 @@ struct AggArgs {
   const uint32_t* const* in_idx;  // [n] parts w -> s, worker order
   const float* const* in_val;
   const PushHdr* const* in_hdr;   // [n] headers (counts) or nullptr
-  const uint64_t* in_count;       // [n] counts when in_hdr == nullptr
+  const uint64_t* in_count;       // [n] counts when in_hdr == nullptr (standalone encode)
+  const uint32_t* const* in_load; // [n] local mode: worker w's partition loads (count = [s])
   const OwnWord* own;
   uint64_t bs;                    // |I_s|
   uint64_t nw;                    // ceil(bs / 64) (>= 1)
