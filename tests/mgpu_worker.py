@@ -25,8 +25,14 @@ def main():
     density = float(sys.argv[3]) if len(sys.argv) > 3 else 0.01
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ngpu = torch.cuda.device_count()
+    dev = local % ngpu
+    torch.cuda.set_device(dev)
+    if world <= ngpu:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:  # oversubscribed (several ranks per GPU, e.g. n = 8 on fewer GPUs):
+        # NCCL refuses duplicate GPUs; the handle exchange only needs gloo
+        dist.init_process_group("gloo")
     import bench
     import paper_2309_13254_b200 as zen
     from oracle import COracle
@@ -70,7 +76,7 @@ def main():
     if st.serial_writes != ref.serial_writes or st.placed_at_depth != ref.placed_at_depth:
         print(f"RANK {rank} collision stats mismatch", flush=True)
         ok = False
-    flag = torch.tensor([0 if ok else 1], device="cuda")
+    flag = torch.tensor([0 if ok else 1], device="cuda" if world <= ngpu else "cpu")
     dist.all_reduce(flag)
     if rank == 0:
         print("MGPU " + ("OK" if int(flag.item()) == 0 else "FAIL") + f" n={world} M={m}", flush=True)

@@ -64,3 +64,19 @@ def test_bp_multi_gpu_parity(shape):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MGPU OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_bp_rank_mode_eight_ranks_oversubscribed():
+    """n = 8 rank mode (the headline node count) with several ranks per GPU:
+    every rank is its own process mapping the others' arenas over CUDA IPC,
+    exactly as on 8 GPUs; the GPU time-slices the processes, so only
+    correctness is meaningful here."""
+    if _ngpus() < 1:
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
+           "--nproc-per-node=8", os.path.join(ROOT, "tests", "mgpu_worker.py"),
+           "20000", "64", "0.01"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MGPU OK n=8" in r.stdout
