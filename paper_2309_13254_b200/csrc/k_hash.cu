@@ -37,6 +37,7 @@
 //            sequentially (rare: ~3% serial vs r2 = 10% of r1).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "zen_common.cuh"
 #include "zen_hash_dev.cuh"
@@ -167,6 +168,66 @@ __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
   } else {
     a.out_idx[soff[p] + pos] = x;
     a.out_val[soff[p] + pos] = v;
+  }
+  if (pos == r1 + r2)
+    atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)x + 1) << 16) | p);
+}
+
+// Pipeline scatter (pointer-table destinations): the tile's keys are first
+// reordered in shared memory into their partitions' runs (block offset of p +
+// stable rank), so consecutive threads store consecutive positions of one
+// destination part -- full-line (NVLink) stores instead of ~n short segments
+// per warp.
+template <typename K>
+__global__ void __launch_bounds__(kThreads) k_scatter_runs(HashArgs<K> a) {
+  zen_dev::pdl_entry();
+  __shared__ K s_x[kHashTile];
+  __shared__ float s_v[kHashTile];
+  __shared__ uint16_t s_p[kHashTile];
+  __shared__ uint32_t s_boff[kMaxWorkers], s_base[kMaxWorkers];
+  const uint32_t n = a.fam.n;
+  HashHdr* h = a.hdr;
+  if (h->status & kErrCapacity) return;
+  const uint32_t tile = blockIdx.x, ntiles = h->ntiles;
+  if (tile >= ntiles) return;
+  const uint64_t z = h->count, r1 = h->r1, r2 = h->r2;
+  const uint64_t left = z - (uint64_t)tile * kHashTile;
+  const uint32_t keys = left < kHashTile ? (uint32_t)left : kHashTile;
+  if (threadIdx.x < 32) {  // per-partition counts of this tile -> block offsets
+    const uint32_t q = threadIdx.x;
+    uint32_t base = 0, cnt = 0;
+    if (q < n) {
+      base = a.tile_cnt[(uint64_t)q * a.tiles_cap + tile];
+      const uint32_t next =
+          tile + 1 < ntiles ? a.tile_cnt[(uint64_t)q * a.tiles_cap + tile + 1] : a.load[q];
+      cnt = next - base;
+    }
+    const uint32_t inc = warp_inclusive_sum(cnt);
+    if (q < n) {
+      s_boff[q] = inc - cnt;
+      s_base[q] = base;
+    }
+  }
+  __syncthreads();
+  const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
+  if (threadIdx.x < keys) {
+    const uint32_t pm = a.pmeta[i];
+    const uint32_t p = pm & 0xFFFFu;
+    const uint32_t slot = s_boff[p] + (pm >> 16);
+    s_x[slot] = a.idx[i];
+    s_v[slot] = a.val[i];
+    s_p[slot] = (uint16_t)p;
+  }
+  __syncthreads();
+  if (threadIdx.x >= keys) return;
+  const uint32_t t = threadIdx.x, p = s_p[t];
+  const uint64_t pos = (uint64_t)s_base[p] + (t - s_boff[p]);
+  const K x = s_x[t];
+  if (pos < a.dst_cap) {
+    a.dst_idx[p][pos] = x;
+    a.dst_val[p][pos] = s_v[t];
+  } else {
+    atomicOr(&h->status, kErrCapacity);
   }
   if (pos == r1 + r2)
     atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)x + 1) << 16) | p);
@@ -475,7 +536,11 @@ void launch_hash_critical(const HashArgs<K>& a, uint32_t n, bool part, cudaStrea
     count_launch();
   }
   launch_k(k_part_scan<K>, n, 1024, 0, stream, a);
-  launch_k(k_scatter<K>, tiles, kThreads, a.dst_table ? 0 : n * sizeof(uint64_t), stream, a);
+  if (a.dst_table && a.peer)  // NVLink destinations: full-line stores (measured -3 us at n=4;
+                             // local stores gain nothing from the reorder)
+    launch_k(k_scatter_runs<K>, tiles, kThreads, 0, stream, a);
+  else
+    launch_k(k_scatter<K>, tiles, kThreads, a.dst_table ? 0 : n * sizeof(uint64_t), stream, a);
   for (int i = 0; i < 2; ++i) count_launch();
   if (a.push_hdr) {
     launch_k(k_push_signal<K>, 1, 32, 0, stream, a);
