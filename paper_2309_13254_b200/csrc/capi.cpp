@@ -1691,7 +1691,12 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
     {
       LaunchScope low(/*pdl=*/false, /*low_priority=*/true);
-      launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side, /*ctas_per_sm=*/2);
+      // the side path's width follows the key capacity: at embedding-scale
+      // sparsity it stays narrow (the latency-bound critical path keeps the
+      // SMs), at millions of keys it needs the whole GPU not to become the tail
+      const unsigned side_ctas = (unsigned)std::min<uint64_t>(
+          6, std::max<uint64_t>(2, bp->cap >> 18));
+      launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side, side_ctas);
     }
     launch_hash_critical<uint32_t>(w.a, bp->n, /*part=*/false, st);
   }
