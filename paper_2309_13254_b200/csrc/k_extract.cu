@@ -204,56 +204,86 @@ __global__ void __launch_bounds__(256)
   out_val[i] = st_val[src];
 }
 
-// BP pipeline: the compaction block of 256 output positions IS hash tile
-// `blockIdx.x`, so the data path's partition pass (k_hash.cu k_part) runs here
-// on the key just moved: h0 partition, its stable rank among the tile's
-// same-partition keys, and the per-(partition, tile) counts.
+// BP pipeline: compaction fused with the data path's partition pass
+// (k_hash.cu k_part): each block handles kCompactTiles consecutive 256-key
+// hash tiles, one key per thread per tile, with every tile's loads issued
+// before any is used (the per-key work is a chain of dependent loads:
+// block->tile map, tile base, staged entry), then per tile: h0 partition,
+// the key's stable rank among the tile's same-partition keys and the
+// per-(partition, tile) counts.
+constexpr int kCompactTiles = 4;
+
 template <typename K>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
     k_extract_compact_part(const K* __restrict__ st_idx, const float* __restrict__ st_val,
                            const uint64_t* __restrict__ tile_base, uint32_t ntiles,
                            const uint32_t* __restrict__ blk_tile, HashArgs<K> a) {
   zen_dev::pdl_entry();
-  extern __shared__ uint32_t wc[];  // [8 warps][n] key counts -> cross-warp prefixes
+  extern __shared__ uint32_t wc[];  // [kCompactTiles][8 warps][n] counts -> prefixes
   const HashHdr* h = a.hdr;
   if (h->status & kErrCapacity) return;
-  const uint32_t tile = blockIdx.x;
-  if (tile >= h->ntiles) return;
   const uint64_t z = h->count;
+  const uint32_t tile0 = blockIdx.x * kCompactTiles;
+  if ((uint64_t)tile0 * kHashTile >= z) return;
   const uint32_t n = a.fam.n, lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint64_t b0 = (uint64_t)tile * kHashTile;
-  const uint64_t i = b0 + threadIdx.x;
-  const bool valid = i < z;
-  for (uint32_t q = threadIdx.x; q < 8 * n; q += blockDim.x) wc[q] = 0;
-  uint32_t p = 0xFFFFFFFFu;
-  if (valid) {
-    uint32_t lo = blk_tile[tile];
-    uint32_t hi = (b0 + kHashTile < z) ? blk_tile[tile + 1] + 1 : ntiles;
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (tile_base[mid] <= i) lo = mid; else hi = mid;
+  for (uint32_t q = threadIdx.x; q < kCompactTiles * 8 * n; q += blockDim.x) wc[q] = 0;
+  uint32_t p[kCompactTiles];
+  K x[kCompactTiles];
+  float v[kCompactTiles];
+  bool valid[kCompactTiles];
+#pragma unroll
+  for (int j = 0; j < kCompactTiles; ++j) {
+    const uint32_t tile = tile0 + j;
+    const uint64_t b0 = (uint64_t)tile * kHashTile;
+    const uint64_t i = b0 + threadIdx.x;
+    valid[j] = i < z;
+    p[j] = 0xFFFFFFFFu;
+    if (valid[j]) {
+      uint32_t lo = blk_tile[tile];
+      uint32_t hi = (b0 + kHashTile < z) ? blk_tile[tile + 1] + 1 : ntiles;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (tile_base[mid] <= i) lo = mid; else hi = mid;
+      }
+      const uint64_t src = (uint64_t)lo * kExtractTile + (i - tile_base[lo]);
+      x[j] = st_idx[src];
+      v[j] = st_val[src];
     }
-    const uint64_t src = (uint64_t)lo * kExtractTile + (i - tile_base[lo]);
-    const K x = st_idx[src];
-    const_cast<K*>(a.idx)[i] = x;  // the worker's compacted keys (HashArgs input)
-    const_cast<float*>(a.val)[i] = st_val[src];
-    p = part_of(a.fam, (uint64_t)x + 1);
   }
-  const uint32_t g = __match_any_sync(0xffffffffu, p);
-  const uint32_t wr = __popc(g & lanemask_lt());
-  if (valid && lane == (uint32_t)(__ffs(g) - 1)) wc[warp * n + p] = __popc(g);
+#pragma unroll
+  for (int j = 0; j < kCompactTiles; ++j) {
+    const uint64_t i = (uint64_t)(tile0 + j) * kHashTile + threadIdx.x;
+    if (valid[j]) {
+      const_cast<K*>(a.idx)[i] = x[j];  // the worker's compacted keys (HashArgs input)
+      const_cast<float*>(a.val)[i] = v[j];
+      p[j] = part_of(a.fam, (uint64_t)x[j] + 1);
+    }
+  }
+  __syncthreads();  // wc cleared
+  uint32_t wr[kCompactTiles];
+#pragma unroll
+  for (int j = 0; j < kCompactTiles; ++j) {
+    const uint32_t g = __match_any_sync(0xffffffffu, p[j]);
+    wr[j] = __popc(g & lanemask_lt());
+    if (valid[j] && lane == (uint32_t)(__ffs(g) - 1)) wc[(j * 8 + warp) * n + p[j]] = __popc(g);
+  }
   __syncthreads();
-  for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) {
+  for (uint32_t jq = threadIdx.x; jq < kCompactTiles * n; jq += blockDim.x) {
+    const uint32_t j = jq / n, q = jq - j * n, tile = tile0 + j;
     uint32_t acc = 0;
     for (int w = 0; w < 8; ++w) {
-      const uint32_t t = wc[w * n + q];
-      wc[w * n + q] = acc;
+      const uint32_t t = wc[(j * 8 + w) * n + q];
+      wc[(j * 8 + w) * n + q] = acc;
       acc += t;
     }
-    a.tile_cnt[(uint64_t)q * a.tiles_cap + tile] = acc;
+    if (tile < a.tiles_cap) a.tile_cnt[(uint64_t)q * a.tiles_cap + tile] = acc;
   }
   __syncthreads();
-  if (valid) a.pmeta[i] = p | ((wc[warp * n + p] + wr) << 16);
+#pragma unroll
+  for (int j = 0; j < kCompactTiles; ++j) {
+    const uint64_t i = (uint64_t)(tile0 + j) * kHashTile + threadIdx.x;
+    if (valid[j]) a.pmeta[i] = p[j] | ((wc[(j * 8 + warp) * n + p[j]] + wr[j]) << 16);
+  }
 }
 
 }  // namespace
@@ -297,9 +327,10 @@ template <typename K>
 void launch_extract_compact_part(uint64_t m, const ExtractWs<K>& ws, const HashArgs<K>& a,
                                  uint32_t n, cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
-  launch_k(k_extract_compact_part<K>, (unsigned)std::max<uint64_t>(a.tiles_cap, 1), 256,
-           8 * n * sizeof(uint32_t), stream, ws.st_idx, ws.st_val, ws.tile_base, ntiles,
-           ws.blk_tile, a);
+  const uint64_t blocks = (std::max<uint64_t>(a.tiles_cap, 1) + kCompactTiles - 1) / kCompactTiles;
+  launch_k(k_extract_compact_part<K>, (unsigned)blocks, 256,
+           kCompactTiles * 8 * n * sizeof(uint32_t), stream, ws.st_idx, ws.st_val, ws.tile_base,
+           ntiles, ws.blk_tile, a);
   count_launch();
 }
 
