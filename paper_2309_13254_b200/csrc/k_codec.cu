@@ -152,44 +152,57 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
   const uint64_t total = pre[n];
   const uint32_t lane = lane_id();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int R = 4;  // entries per thread per round, loads issued together
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < total;
-       base += stride) {  // warp-uniform trip count: full-mask shuffles below
-    const uint64_t i = base + lane;
-    const bool in = i < total;
-    uint32_t w = 0;
-    if (in)
-      while (i >= pre[w + 1]) ++w;
-    const uint64_t e = in ? i - pre[w] : 0;  // index inside worker w's part
-    const uint32_t key = in ? a.in_idx[w][e] : 0u;
-    const OwnWord ow = a.own[in ? key >> 6 : 0];
-    const bool owned = in && ((ow.mask >> (key & 63u)) & 1ull);
-    if (in && !owned) {
-      atomicMin((unsigned long long*)&a.hdr->bad_index, (unsigned long long)key);
-      atomicOr(&a.hdr->status, kErrOutside);
+       base += R * stride) {  // warp-uniform trip count: full-mask shuffles below
+    uint32_t w[R], key[R];
+    uint64_t e[R];
+    bool in[R];
+    OwnWord ow[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const uint64_t i = base + q * stride + lane;
+      in[q] = i < total;
+      w[q] = 0;
+      if (in[q])
+        while (i >= pre[w[q] + 1]) ++w[q];
+      e[q] = in[q] ? i - pre[w[q]] : 0;  // index inside worker w's part
+      key[q] = in[q] ? a.in_idx[w[q]][e[q]] : 0u;
     }
-    const uint32_t r = ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
-    // consecutive keys share bitmap words: one atomic per distinct word per warp
-    unsigned long long* word = owned ? a.pw + (uint64_t)w * a.nws + (r >> 6) : nullptr;
-    const uint64_t bit = owned ? 1ull << (r & 63u) : 0ull;
-    const uint32_t grp = __match_any_sync(0xffffffffu, (unsigned long long)word);
-    const uint32_t lo = __reduce_or_sync(grp, (uint32_t)bit);
-    const uint32_t hi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
-    if (owned && lane == (uint32_t)(__ffs(grp) - 1))
-      atomicOr(word, ((unsigned long long)hi << 32) | lo);
-    // The part is ascending, so its entries in bitmap word j are consecutive:
-    // the first of them is at part index = worker w's popcount prefix at j,
-    // which the fold needs -- written here instead of scanned later.
-    const uint32_t jw = owned ? (r >> 6) : 0xFFFFFFFFu;
-    uint32_t prev_w = __shfl_up_sync(0xffffffffu, w, 1);
-    uint32_t prev_j = __shfl_up_sync(0xffffffffu, jw, 1);
-    if (in && owned && (lane == 0 || prev_w != w) && e > 0) {
-      const uint32_t pk = a.in_idx[w][e - 1];  // previous entry of the same part
-      const OwnWord po = a.own[pk >> 6];
-      prev_w = w;
-      prev_j = (po.prefix + (uint32_t)__popcll(po.mask & lowmask64(pk & 63u))) >> 6;
+#pragma unroll
+    for (int q = 0; q < R; ++q) ow[q] = a.own[in[q] ? key[q] >> 6 : 0];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (base + q * stride >= total) break;  // warp-uniform
+      const bool owned = in[q] && ((ow[q].mask >> (key[q] & 63u)) & 1ull);
+      if (in[q] && !owned) {
+        atomicMin((unsigned long long*)&a.hdr->bad_index, (unsigned long long)key[q]);
+        atomicOr(&a.hdr->status, kErrOutside);
+      }
+      const uint32_t r = ow[q].prefix + (uint32_t)__popcll(ow[q].mask & lowmask64(key[q] & 63u));
+      // consecutive keys share bitmap words: one atomic per distinct word per warp
+      unsigned long long* word = owned ? a.pw + (uint64_t)w[q] * a.nws + (r >> 6) : nullptr;
+      const uint64_t bit = owned ? 1ull << (r & 63u) : 0ull;
+      const uint32_t grp = __match_any_sync(0xffffffffu, (unsigned long long)word);
+      const uint32_t lo = __reduce_or_sync(grp, (uint32_t)bit);
+      const uint32_t hi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
+      if (owned && lane == (uint32_t)(__ffs(grp) - 1))
+        atomicOr(word, ((unsigned long long)hi << 32) | lo);
+      // The part is ascending, so its entries in bitmap word j are consecutive:
+      // the first of them is at part index = worker w's popcount prefix at j,
+      // which the fold needs -- written here instead of scanned later.
+      const uint32_t jw = owned ? (r >> 6) : 0xFFFFFFFFu;
+      uint32_t prev_w = __shfl_up_sync(0xffffffffu, w[q], 1);
+      uint32_t prev_j = __shfl_up_sync(0xffffffffu, jw, 1);
+      if (in[q] && owned && (lane == 0 || prev_w != w[q]) && e[q] > 0) {
+        const uint32_t pk = a.in_idx[w[q]][e[q] - 1];  // previous entry of the same part
+        const OwnWord po = a.own[pk >> 6];
+        prev_w = w[q];
+        prev_j = (po.prefix + (uint32_t)__popcll(po.mask & lowmask64(pk & 63u))) >> 6;
+      }
+      if (owned && (e[q] == 0 || prev_w != w[q] || prev_j != jw))
+        a.pre[(uint64_t)w[q] * a.nws + jw] = (uint32_t)e[q];
     }
-    if (owned && (e == 0 || prev_w != w || prev_j != jw))
-      a.pre[(uint64_t)w * a.nws + jw] = (uint32_t)e;
   }
 }
 

@@ -132,6 +132,10 @@ __global__ void __launch_bounds__(1024) k_part_scan(HashArgs<K> a) {
   if (threadIdx.x == 0) a.load[p] = total;
 }
 
+// one key per thread per tile, kScatterTiles tiles per block, every load of
+// the block's tiles issued before the stores
+constexpr int kScatterTiles = 4;
+
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
   zen_dev::pdl_entry();
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
   HashHdr* h = a.hdr;
   const bool ok = !(h->status & kErrCapacity);
   const uint64_t z = h->count, r1 = h->r1, r2 = h->r2;
-  const uint32_t tile = blockIdx.x;
+  const uint32_t ntiles = h->ntiles, tile0 = blockIdx.x * kScatterTiles;
   if (!a.dst_table) {
     if (threadIdx.x == 0) {
       uint64_t off = 0;
@@ -151,26 +155,45 @@ __global__ void __launch_bounds__(kThreads) k_scatter(HashArgs<K> a) {
     }
     __syncthreads();
   }
-  const uint64_t i = (uint64_t)tile * kHashTile + threadIdx.x;
-  if (!ok || tile >= h->ntiles || i >= z) return;
-  const uint32_t pm = a.pmeta[i];
-  const uint32_t p = pm & 0xFFFFu;
-  const K x = a.idx[i];
-  const float v = a.val[i];
-  const uint64_t pos = (uint64_t)a.tile_cnt[(uint64_t)p * a.tiles_cap + tile] + (pm >> 16);
-  if (a.dst_table) {
-    if (pos < a.dst_cap) {
-      a.dst_idx[p][pos] = x;
-      a.dst_val[p][pos] = v;
-    } else {
-      atomicOr(&h->status, kErrCapacity);
+  if (!ok || tile0 >= ntiles) return;
+  uint32_t pm[kScatterTiles], p[kScatterTiles];
+  K x[kScatterTiles];
+  float v[kScatterTiles];
+  uint64_t pos[kScatterTiles];
+#pragma unroll
+  for (int j = 0; j < kScatterTiles; ++j) {
+    const uint64_t i = (uint64_t)(tile0 + j) * kHashTile + threadIdx.x;
+    pm[j] = 0;
+    if (tile0 + j < ntiles && i < z) {
+      pm[j] = a.pmeta[i] | 0x80000000u;  // bit 31: valid (ranks are < 2^15)
+      x[j] = a.idx[i];
+      v[j] = a.val[i];
     }
-  } else {
-    a.out_idx[soff[p] + pos] = x;
-    a.out_val[soff[p] + pos] = v;
   }
-  if (pos == r1 + r2)
-    atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)x + 1) << 16) | p);
+#pragma unroll
+  for (int j = 0; j < kScatterTiles; ++j) {
+    p[j] = pm[j] & 0xFFFFu;
+    pos[j] = (pm[j] >> 31) ? (uint64_t)a.tile_cnt[(uint64_t)p[j] * a.tiles_cap + tile0 + j] +
+                                 ((pm[j] >> 16) & 0x7FFFu)
+                           : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kScatterTiles; ++j) {
+    if (!(pm[j] >> 31)) continue;
+    if (a.dst_table) {
+      if (pos[j] < a.dst_cap) {
+        a.dst_idx[p[j]][pos[j]] = x[j];
+        a.dst_val[p[j]][pos[j]] = v[j];
+      } else {
+        atomicOr(&h->status, kErrCapacity);
+      }
+    } else {
+      a.out_idx[soff[p[j]] + pos[j]] = x[j];
+      a.out_val[soff[p[j]] + pos[j]] = v[j];
+    }
+    if (pos[j] == r1 + r2)
+      atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)x[j] + 1) << 16) | p[j]);
+  }
 }
 
 // Pipeline scatter (pointer-table destinations): the tile's keys are first
@@ -540,7 +563,8 @@ void launch_hash_critical(const HashArgs<K>& a, uint32_t n, bool part, cudaStrea
                              // local stores gain nothing from the reorder)
     launch_k(k_scatter_runs<K>, tiles, kThreads, 0, stream, a);
   else
-    launch_k(k_scatter<K>, tiles, kThreads, a.dst_table ? 0 : n * sizeof(uint64_t), stream, a);
+    launch_k(k_scatter<K>, (tiles + kScatterTiles - 1) / kScatterTiles, kThreads,
+             a.dst_table ? 0 : n * sizeof(uint64_t), stream, a);
   for (int i = 0; i < 2; ++i) count_launch();
   if (a.push_hdr) {
     launch_k(k_push_signal<K>, 1, 32, 0, stream, a);
