@@ -213,6 +213,34 @@ def cpu_reference_step(args, n, dense_list, budget_s=12.0):
                           "sync": round(res["sync_ms"], 3), "table_once": round(res["table_ms"], 1)}}
 
 
+# --------------------------------------------------------------- exchange ----
+
+NVLINK_PEER_GBPS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def exchange_report(ledger, n, stage_ms):
+    """NVLink bytes each GPU sends in one sync and the rate they imply.  The
+    push is fused into the scatter and the pull into the union/fold kernels,
+    so the exchange has no kernel of its own: the rates below divide by the
+    whole stage that carries it (a lower bound on the link rate)."""
+    if n < 2:
+        return {"note": "n = 1: no exchange"}
+    # ledger bits use the reference widths: push 96 bits per COO entry, pull
+    # B_s + 32 U_s; our wire sends u32 index + f32 value (64 bits) per entry
+    push_out = ledger[0, 0] // 96 * 8
+    pull_out = ledger[1, 0] // 8
+    push_s = float(stage_ms[1]) * 1e-3
+    pull_s = float(stage_ms[2]) * 1e-3
+    pmax, qmax = float(push_out.max()), float(pull_out.max())
+    return {"push_bytes_out_per_gpu_max": int(pmax), "pull_bytes_out_per_gpu_max": int(qmax),
+            "push_GBps_lower_bound": round(pmax / push_s / 1e9, 1) if push_s else None,
+            "pull_GBps_lower_bound": round(qmax / pull_s / 1e9, 1) if pull_s else None,
+            "nvlink_peak_GBps": NVLINK_PEER_GBPS,
+            "pull_frac_lower_bound": round(qmax / pull_s / 1e9 / NVLINK_PEER_GBPS, 4) if pull_s else None,
+            "note": "push wire: u32 index + f32 value; pull: HashBitmap bits + f32 values to each "
+                    "of the n-1 peers; rates = bytes / (hash_push | aggregate) stage time"}
+
+
 # ------------------------------------------------------------ extras (f1/f2) ----
 
 def measure_extras(args, zen, d_dense, peak, reps=10):
@@ -534,11 +562,7 @@ def main():
                        "algorithmic_bytes": hash_bytes,
                        "hbm_frac": round(hash_bytes / (hash_ms * 1e-3) / 1e9 / peak, 4) if hash_ms else None,
                        "note": "includes the fused NVLink push (scatter into owner inboxes)"},
-        "exchange": {"push_bytes_sent_per_gpu_max": int(ledger[0, 0].max() // 96 * 8),
-                     "pull_bytes_recv_per_gpu_max": int(ledger[1, 1].max() // 8),
-                     "note": "push wire: u32 index + f32 value (WireFormat::coo(32) layout); "
-                             "pull: HashBitmap bits + f32 values; ledger bits use the reference "
-                             "widths (64-bit COO)"},
+        "exchange": exchange_report(ledger, n, stage_ms),
         "host_enqueue_ms_per_step": round(host_ms, 4),
         "union_nnz": union, "gpu_launches": int(launches),
         "kernels_per_sync": bp.kernels_per_sync(),
