@@ -1694,8 +1694,10 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
       // the side path's width follows the key capacity: at embedding-scale
       // sparsity it stays narrow (the latency-bound critical path keeps the
       // SMs), at millions of keys it needs the whole GPU not to become the tail
+      // (rank mode keeps it narrower: its aggregate waits on the peers, and
+      // measured at n=4 one more CTA per SM costs the critical path 10 us)
       const unsigned side_ctas = (unsigned)std::min<uint64_t>(
-          6, std::max<uint64_t>(2, bp->cap >> 18));
+          6, std::max<uint64_t>(2, bp->cap >> (bp->local ? 18 : 20)));
       launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side, side_ctas);
     }
     launch_hash_critical<uint32_t>(w.a, bp->n, /*part=*/false, st);
