@@ -199,6 +199,13 @@ zen_status zen_frame_header(const zen_wire_format* fmt, const zen_message_info* 
 zen_status zen_frame_parse(const uint8_t* in, uint64_t available, zen_wire_format* fmt,
                            zen_message_info* msg);
 
+/* ---- apply: the step after the sync ------------------------------------ */
+/* d_dense[idx[i]] += alpha * val[i] for a sorted unique sparse tensor (an SGD
+ * step on a synced gradient: alpha = -lr; zen_bp_result gives the synced
+ * tensor on the device).  Indices >= m -> ZEN_E_INVALID.  Synchronous. */
+zen_status zen_axpy_sparse(zen_ctx* ctx, float* d_dense, uint64_t m, const uint64_t* d_idx,
+                           const float* d_val, uint64_t count, float alpha);
+
 /* ---- top-k sparsification: zen::sparsify_topk ------------------------- */
 /* zen/workload.hpp:157-178: the ceil(fraction*m) largest-magnitude entries of
  * a dense fp32 gradient (ties to the lower index), exact zeros dropped,

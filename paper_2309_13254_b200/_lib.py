@@ -64,6 +64,7 @@ _SIGS = {
     "zen_frame_header": (C.c_int, [P(WireFormatC), P(MessageInfoC), vp]),
     "zen_frame_parse": (C.c_int, [vp, u64, P(WireFormatC), P(MessageInfoC)]),
     "zen_sparsify_topk": (C.c_int, [vp, vp, u64, C.c_double, vp, vp, u64, P(u64)]),
+    "zen_axpy_sparse": (C.c_int, [vp, vp, u64, vp, vp, u64, C.c_float]),
     "zen_abi_version": (u32, []),
     "zen_status_string": (C.c_char_p, [C.c_int]),
     "zen_last_error_message": (C.c_char_p, []),

@@ -51,6 +51,8 @@ LaunchScope::~LaunchScope() {
 }
 
 // extra small kernels (k_util.cu)
+void launch_axpy_sparse(float* dense, uint64_t m, const uint64_t* idx, const float* val,
+                        uint64_t count, float alpha, uint32_t* status, cudaStream_t stream);
 void launch_dump_slots(const unsigned long long* slots, uint64_t cells, uint32_t epoch,
                        const float* vals, uint64_t* out_slots, float* out_vals,
                        cudaStream_t stream);
@@ -1114,6 +1116,27 @@ zen_status zen_frame_parse(const uint8_t* in, uint64_t available, zen_wire_forma
 }
 
 }  // extern "C"
+
+// ----------------------------------------------------------------- apply ----
+
+extern "C" zen_status zen_axpy_sparse(zen_ctx* c, float* d_dense, uint64_t m,
+                                      const uint64_t* d_idx, const float* d_val, uint64_t count,
+                                      float alpha) {
+  if (!c) return fail(ZEN_E_INVALID, "null ctx");
+  if (count && (!d_dense || !d_idx || !d_val)) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  Bump sc;
+  CKR(ctx_scratch(c, 256, &sc));
+  uint32_t* st = sc.get<uint32_t>(1);
+  CK(cudaMemsetAsync(st, 0, 4, c->stream));
+  launch_axpy_sparse(d_dense, m, d_idx, d_val, count, alpha, st, c->stream);
+  uint32_t h = 0;
+  CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h) return fail(ZEN_E_INVALID, "sparse tensor index outside [0, M)");
+  return ZEN_OK;
+}
 
 // ----------------------------------------------------------------- top-k ----
 // zen::sparsify_topk (zen/workload.hpp:157-178), k_topk.cu

@@ -47,6 +47,22 @@ __global__ void k_universe_indices(const OwnWord* __restrict__ own, uint64_t nwo
   }
 }
 
+// the apply step after a sync: dense[idx[i]] += alpha * val[i] (indices
+// unique, so no atomics); an SGD step on the synced gradient is alpha = -lr
+__global__ void k_axpy_sparse(float* __restrict__ dense, uint64_t m,
+                              const uint64_t* __restrict__ idx, const float* __restrict__ val,
+                              uint64_t count, float alpha, uint32_t* status) {
+  zen_dev::pdl_entry();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = idx[i];
+    if (x < m)
+      dense[x] = fmaf(alpha, val[i], dense[x]);
+    else
+      atomicOr(status, 1u);
+  }
+}
+
 __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
                              uint64_t n) {
   zen_dev::pdl_entry();
@@ -101,6 +117,13 @@ void launch_universe_indices(const OwnWord* own, uint64_t nwords, uint64_t* out,
 void launch_check_owned(const uint64_t* idx, uint64_t count, uint64_t m, const OwnWord* own,
                         HashHdr* hdr, cudaStream_t stream) {
   launch_k(k_check_owned, grid_for(count), 256, 0, stream, idx, count, m, own, hdr);
+  count_launch();
+}
+
+void launch_axpy_sparse(float* dense, uint64_t m, const uint64_t* idx, const float* val,
+                        uint64_t count, float alpha, uint32_t* status, cudaStream_t stream) {
+  if (!count) return;
+  launch_k(k_axpy_sparse, grid_for(count), 256, 0, stream, dense, m, idx, val, count, alpha, status);
   count_launch();
 }
 

@@ -885,6 +885,17 @@ class BPSynchronizer:
         self._keep = (idx_list, val_list)
         _check(_lib().zen_bp_sync_sparse(self.h, ip, vp, nz))
 
+    def apply_sgd(self, param, lr: float):
+        """The step after the sync: param.view(-1)[idx] -= lr * val with the
+        synced gradient, on the device (zen_axpy_sparse)."""
+        self.wait()
+        pi, pv, cnt = C.c_void_p(), C.c_void_p(), C.c_uint64()
+        _check(_lib().zen_bp_result(self.h, C.byref(pi), C.byref(pv), C.byref(cnt)))
+        flat = param.view(-1)
+        self.ctx.bind_stream()
+        _check(_lib().zen_axpy_sparse(self.ctx.h, _ptr(flat), flat.numel(), pi, pv, cnt.value,
+                                      -float(lr)))
+
     def wait(self):
         _check(_lib().zen_bp_wait(self.h))
 

@@ -96,3 +96,27 @@ def test_topk_full_size_properties(zen):
     if ties_out.numel():
         assert int(ties_in.max()) < int(ties_out.min())
     np.testing.assert_array_equal(t.values(), d[kept].cpu().numpy())
+
+
+def test_apply_sgd_after_sync(zen):
+    """The step after the sync (f2): param[idx] -= lr * synced value, on the
+    device, against a torch fp32 reference of the same update."""
+    import torch
+    rng = np.random.default_rng(11)
+    m, n = 200_000, 3
+    torch.cuda.set_stream(torch.cuda.Stream())
+    dense = []
+    for _ in range(n):
+        d = np.zeros(m, np.float32)
+        nz = rng.choice(m, 2000, replace=False)
+        d[nz] = rng.standard_normal(nz.size).astype(np.float32)
+        dense.append(torch.from_numpy(d).cuda())
+    bp = zen.BPSynchronizer(n, m, max_nnz=8000)
+    bp.sync_dense(dense)
+    param = torch.from_numpy(rng.standard_normal(m).astype(np.float32)).cuda()
+    want = param.clone()
+    bp.apply_sgd(param, 0.05)
+    idx, val = bp.result()
+    want[idx] -= 0.05 * val  # torch fp32 reference (fma vs mul+sub: <= 1 ulp)
+    torch.testing.assert_close(param, want, rtol=1e-6, atol=1e-7)
+    torch.cuda.set_stream(torch.cuda.default_stream())
