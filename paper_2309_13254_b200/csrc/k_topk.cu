@@ -53,9 +53,14 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist1(const float* __restrict
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const uint32_t bin = u < nvec ? mag_key(v.v[c]) >> 21 : 0xFFFFFFFFu;
-      const uint32_t grp = __match_any_sync(0xffffffffu, bin);
-      if (bin != 0xFFFFFFFFu && lane_id() == (uint32_t)(__ffs(grp) - 1))
-        atomicAdd(&sh[bin], (uint32_t)__popc(grp));
+      // a warp-uniform bin (the zeros of a sparse gradient) costs one atomic;
+      // spread values (dense layers) go straight to the shared histogram
+      const uint32_t b0 = __shfl_sync(0xffffffffu, bin, 0);
+      if (__all_sync(0xffffffffu, bin == b0)) {
+        if (lane_id() == 0 && b0 != 0xFFFFFFFFu) atomicAdd(&sh[b0], 32u);
+      } else if (bin != 0xFFFFFFFFu) {
+        atomicAdd(&sh[bin], 1u);
+      }
     }
   }
   const uint64_t tail0 = vec_ok ? nvec * 8 : 0;
