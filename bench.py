@@ -89,8 +89,9 @@ def dense_gradient(rows, width, live, seed):
 
 class ClockSampler:
     """SM clocks and throttle reasons sampled DURING the timed region
-    (B200_PROFILING.md clocks line).  NVML is polled in-process every ~2 ms so
-    a short timed region still yields many samples; nvidia-smi is the fallback."""
+    (B200_PROFILING.md clocks line).  NVML is opened up front and polled
+    in-process every ~2 ms (plus one synchronous sample at entry and exit), so
+    even a timed region of a few ms has samples; nvidia-smi is the fallback."""
 
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
@@ -100,54 +101,64 @@ class ClockSampler:
         self.source = None
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._bits = [nv.nvmlClocksEventReasonHwSlowdown,
+                          nv.nvmlClocksEventReasonHwThermalSlowdown,
+                          nv.nvmlClocksEventReasonSwThermalSlowdown,
+                          nv.nvmlClocksEventReasonSwPowerCap]
+            self._max = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._nv = nv
+            self.source = "nvml"
+        except Exception:
+            self.source = "nvidia-smi"
 
-    def _nvml(self):
-        import pynvml as nv
-        nv.nvmlInit()
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
-        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        self.source = "nvml"
-        while not self._stop.is_set():
-            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
-                                 {n for n, b in zip(self.NAMES, bits) if r & b}))
-            self._stop.wait(0.002)
+    def _sample_nvml(self):
+        nv = self._nv
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        self.samples.append((nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM), self._max,
+                             {n for n, b in zip(self.NAMES, self._bits) if r & b}))
 
-    def _smi(self):
-        self.source = "nvidia-smi"
+    def _sample_smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                f = [x.strip() for x in out.split(",")]
-                if len(f) == 6 and f[0].replace(".", "").isdigit():
-                    self.samples.append((float(f[0]), float(f[1]),
-                                         {n for n, v in zip(self.NAMES, f[2:]) if v.lower() == "active"}))
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=5).stdout.strip()
+            f = [x.strip() for x in out.split(",")]
+            if len(f) == 6 and f[0].replace(".", "").isdigit():
+                self.samples.append((float(f[0]), float(f[1]),
+                                     {n for n, v in zip(self.NAMES, f[2:]) if v.lower() == "active"}))
+        except Exception:
+            pass
+
+    def _sample(self):
+        try:
+            self._sample_nvml() if self._nv else self._sample_smi()
+        except Exception:
+            pass
 
     def __enter__(self):
+        self._sample()
+
         def run():
-            try:
-                self._nvml()
-            except Exception:
-                self._smi()
+            while not self._stop.is_set():
+                self._sample()
+                self._stop.wait(0.002 if self._nv else 0.2)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
-        time.sleep(0.01)  # first sample before the timed region starts
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         if self._t:
             self._t.join(timeout=6)
+        self._sample()
 
     def summary(self):
         if not self.samples:
