@@ -84,6 +84,7 @@ typedef struct zen_collision_stats {
 typedef struct zen_ctx zen_ctx;           /* one device + stream + scratch */
 typedef struct zen_universe zen_universe; /* zen::HashUniverseTable on device */
 typedef struct zen_bp zen_bp;             /* one BP synchroniser (rank or local) */
+typedef struct zen_hc zen_hc;             /* one Hierarchical Centralization rank */
 
 /* ---- library --------------------------------------------------------- */
 uint32_t zen_abi_version(void);
@@ -198,6 +199,43 @@ zen_status zen_frame_header(const zen_wire_format* fmt, const zen_message_info* 
  * payload bytes available */
 zen_status zen_frame_parse(const uint8_t* in, uint64_t available, zen_wire_format* fmt,
                            zen_message_info* msg);
+
+/* ---- merge_sum: zen/tensor.hpp:133-167 ---------------------------------- */
+/* union of two sorted unique-index tensors over `universe`, shared indices
+ * summed (fp32); the fold of every scheme (Hierarchical Centralization:
+ * zen/schemes.hpp:173-193).  *count is set even on ZEN_E_CAPACITY. */
+zen_status zen_merge_sum(zen_ctx* ctx, const uint64_t* a_idx, const float* a_val, uint64_t na,
+                         const uint64_t* b_idx, const float* b_val, uint64_t nb,
+                         uint64_t universe, uint64_t* d_idx, float* d_val, uint64_t capacity,
+                         uint64_t* count);
+/* per-range entry counts behind zen::skewness_ratio (zen/tensor.hpp:193-213):
+ * h_counts[p] = entries of the sorted tensor in [p*ceil(M/n), (p+1)*ceil(M/n)) */
+zen_status zen_range_counts(zen_ctx* ctx, const uint64_t* d_idx, uint64_t count,
+                            uint64_t universe, uint32_t partitions, uint64_t* h_counts);
+
+/* ---- Hierarchical Centralization: zen/schemes.hpp:173-193 -------------- */
+/* One process per GPU, n a power of two (zen::NonPowerOfTwo otherwise:
+ * ZEN_E_INVALID).  Stage s (s < log2 n) sends this rank's running aggregate to
+ * rank ^ 2^s as NVLink stores into that rank's CUDA-IPC arena and folds the
+ * partner's with merge_sum (zen/tensor.hpp:133-167).  Every rank ends with
+ * aggregate(inputs), bit-identical across ranks.  The ledger's sent bits at
+ * stage s are message_sizes(state_s, fmt) with |state_s| from
+ * zen_hc_stage_counts.  max_nnz bounds each rank's input. */
+zen_status zen_hc_create(zen_ctx* ctx, uint32_t n, uint32_t rank, uint64_t universe,
+                         uint64_t max_nnz, zen_hc** out);
+void zen_hc_destroy(zen_hc* hc);
+zen_status zen_hc_ipc_handle(zen_hc* hc, void* out); /* ZEN_IPC_HANDLE_BYTES */
+zen_status zen_hc_connect(zen_hc* hc, const void* handles); /* n handles, rank-major */
+/* asynchronous on the context stream; the dense form is graph-replayed */
+zen_status zen_hc_sync_dense(zen_hc* hc, const float* d_dense);
+zen_status zen_hc_sync_sparse(zen_hc* hc, const uint64_t* d_idx, const float* d_val,
+                              uint64_t count);
+zen_status zen_hc_wait(zen_hc* hc);
+zen_status zen_hc_result(zen_hc* hc, const uint64_t** d_idx, const float** d_val,
+                         uint64_t* count);
+zen_status zen_hc_copy_result(zen_hc* hc, uint64_t* d_idx, float* d_val, uint64_t capacity,
+                              uint64_t* count);
+zen_status zen_hc_stage_counts(zen_hc* hc, uint64_t* counts); /* log2(n) entries */
 
 /* ---- apply: the step after the sync ------------------------------------ */
 /* d_dense[idx[i]] += alpha * val[i] for a sorted unique sparse tensor (an SGD

@@ -301,12 +301,48 @@ def topk_cases(ro: RefOracle):
     return out
 
 
+def hc_cases(ro: RefOracle):
+    """zen::run_hier_centralization (zen/schemes.hpp:173-193) in every sized
+    format, zen::merge_sum (tensor.hpp:133-167), the tensor metrics
+    (tensor.hpp:111-213) and profile_sparsity + select_scheme
+    (costmodel.hpp:139-195), on the shapes schemes_test.cpp uses."""
+    out = {}
+    cases = [(2, 50, None), (4, 1000, (0.05, 1.0, 13)), (8, 100000, (0.002, 0.0, 23)),
+             (8, 100000, (0.002, 0.5, 23)), (8, 100000, (0.002, 1.0, 23)), (2, 2000, (0.03, 0.25, 5)),
+             (4, 2000, (0.01, 0.75, 6)), (16, 20000, (0.01, 0.4, 7))]
+    fmts = [("coo", 256, 64), ("coo", 256, 32), ("bitmap", 256, 64), ("tensor_block", 64, 64)]
+    for c, (n, m, spec) in enumerate(cases):
+        if spec is None:
+            ins = [(np.array([1], np.uint64), np.array([2], np.float32)),
+                   (np.array([2], np.uint64), np.array([3], np.float32))]
+        else:
+            ins = ro.generate(m, n, *spec)
+        out[f"c{c}_m"] = np.array([m, n], np.uint64)
+        for w, (i, v) in enumerate(ins):
+            out[f"c{c}_in{w}_idx"], out[f"c{c}_in{w}_val"] = i, v
+        for f, (kind, bs, cb) in enumerate(fmts):
+            i, v, led = ro.hier_centralization(m, ins, kind, bs, cb)
+            out[f"c{c}_f{f}_idx"], out[f"c{c}_f{f}_val"], out[f"c{c}_f{f}_ledger"] = i, v, led
+        i, v = ro.merge_sum(m, *ins[0], *ins[1])
+        out[f"c{c}_merge_idx"], out[f"c{c}_merge_val"] = i, v
+        if all(len(i) for i, _ in ins):
+            out[f"c{c}_metrics"] = np.array([ro.metric(0, m, ins[:2]), ro.metric(1, m, ins),
+                                             ro.metric(2, m, ins[:1], n)], np.float64)
+            d, g, sk, ch = ro.profile(m, [ins, list(reversed(ins))])
+            out[f"c{c}_profile"] = np.array([d, sk, ch] + [g.get(1 << j, np.nan)
+                                                           for j in range(5)], np.float64)
+    out["formats"] = np.array([[{"coo": 1, "bitmap": 2, "tensor_block": 3}[k], bs, cb]
+                               for k, bs, cb in fmts], np.uint32)
+    out["ncases"] = np.array([len(cases)], np.uint32)
+    return out
+
+
 def main():
     ro = RefOracle()
     os.makedirs(OUT, exist_ok=True)
     for name, fn in [("hash_kat", hash_kat), ("hhash", hhash_cases), ("to_sparse", to_sparse_cases),
                      ("codec", codec_cases), ("bp", bp_cases), ("wire", wire_cases),
-                     ("topk", topk_cases)]:
+                     ("topk", topk_cases), ("hc", hc_cases)]:
         data = fn(ro)
         path = os.path.join(OUT, name + ".npz")
         np.savez_compressed(path, **data)

@@ -29,6 +29,7 @@ u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 
 OK, INVALID, SERIAL_OVERFLOW, OUTSIDE, MALFORMED, EMPTY, MISMATCH = 0, 1, 2, 3, 4, 5, 6
+NON_POWER_OF_TWO, MISSING_PROFILE_ENTRY = 7, 8
 
 
 class OracleError(RuntimeError):
@@ -462,6 +463,18 @@ class RefOracle:
                                        C.POINTER(C.c_uint64)]
         L.ref_sparsify_topk.argtypes = [f32p, C.c_uint64, C.c_double, u64p, f32p,
                                         C.POINTER(C.c_uint64)]
+        vpp = C.POINTER(C.c_void_p)
+        L.ref_merge_sum.argtypes = [C.c_uint64, u64p, f32p, C.c_uint64, u64p, f32p, C.c_uint64,
+                                    u64p, f32p, C.POINTER(C.c_uint64)]
+        L.ref_tensor_metric.argtypes = [C.c_int, C.c_uint32, C.c_uint64, vpp, vpp, u64p,
+                                        C.c_uint32, C.POINTER(C.c_double)]
+        L.ref_profile.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, vpp, vpp, u64p,
+                                  C.POINTER(C.c_double), f64p, C.c_uint32, C.POINTER(C.c_double),
+                                  C.POINTER(C.c_int)]
+        L.ref_hier_centralization.argtypes = [
+            C.c_uint32, C.c_uint64, vpp, vpp, u64p, C.c_uint32, C.c_uint32, C.c_uint32, u64p,
+            f32p, C.POINTER(C.c_uint64), u64p, C.c_uint32, C.POINTER(C.c_uint32),
+            C.POINTER(C.c_int)]
         L.ref_bench_step.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), C.c_uint32,
                                      C.c_double, C.c_double, C.c_uint32, C.c_uint64, C.c_int, f64p,
                                      C.POINTER(C.c_uint64)]
@@ -668,6 +681,160 @@ def _ref_sparsify_topk(self, dense, fraction):
                 "sparsify_topk")
     return idx[:oc.value].copy(), val[:oc.value].copy()
 
+
+# ---- f3: merge_sum, metrics, profile / selector, Hierarchical Centralization ----
+
+def _ref_merge_sum(self, m, ia, va, ib, vb):
+    ia, va, ib, vb = _u64(ia), _f32(va), _u64(ib), _f32(vb)
+    oi = np.empty(max(ia.size + ib.size, 1), np.uint64)
+    ov = np.empty(max(ia.size + ib.size, 1), np.float32)
+    oc = C.c_uint64()
+    self._check(self.lib.ref_merge_sum(m, ia, va, ia.size, ib, vb, ib.size, oi, ov, C.byref(oc)),
+                "merge_sum")
+    return oi[:oc.value].copy(), ov[:oc.value].copy()
+
+
+def _ref_metric(self, what, m, inputs, partitions=1):
+    ins, nnz, ip, vp = self._ptrs(inputs)
+    out = C.c_double()
+    self._check(self.lib.ref_tensor_metric(what, len(inputs), m, ip, vp, nnz, partitions,
+                                           C.byref(out)), "metric")
+    return out.value
+
+
+def _ref_profile(self, m, rounds):
+    """profile_sparsity + select_scheme -> (d, {k: gamma}, skew, choice)."""
+    r, n = len(rounds), len(rounds[0])
+    flat = [t for rnd in rounds for t in rnd]
+    ins, nnz, ip, vp = self._ptrs(flat)
+    glen = max(n.bit_length(), 1)
+    gamma = np.zeros(glen, np.float64)
+    d, skew, ch = C.c_double(), C.c_double(), C.c_int()
+    self._check(self.lib.ref_profile(r, n, m, ip, vp, nnz, C.byref(d), gamma, glen,
+                                     C.byref(skew), C.byref(ch)), "profile")
+    g = {1 << j: float(gamma[j]) for j in range(glen) if not np.isnan(gamma[j])}
+    return d.value, g, skew.value, ch.value
+
+
+def _ref_hier_centralization(self, m, inputs, kind="coo", block_size=256, coo_bits=64):
+    """run_hier_centralization -> (idx, val, ledger[stages][4][n])."""
+    n = len(inputs)
+    ins, nnz, ip, vp = self._ptrs(inputs)
+    tot = int(nnz.sum())
+    oi = np.empty(max(tot, 1), np.uint64)
+    ov = np.empty(max(tot, 1), np.float32)
+    oc, ns, eq = C.c_uint64(), C.c_uint32(), C.c_int()
+    ledger = np.zeros(8 * 4 * n, np.uint64)
+    k = WIRE_KINDS[kind] if isinstance(kind, str) else kind
+    self._check(self.lib.ref_hier_centralization(n, m, ip, vp, nnz, k, block_size, coo_bits, oi,
+                                                 ov, C.byref(oc), ledger, 8, C.byref(ns),
+                                                 C.byref(eq)), "hier_centralization")
+    assert eq.value == 1
+    return (oi[:oc.value].copy(), ov[:oc.value].copy(),
+            ledger[:ns.value * 4 * n].reshape(ns.value, 4, n))
+
+
+RefOracle.merge_sum = _ref_merge_sum
+RefOracle.metric = _ref_metric
+RefOracle.profile = _ref_profile
+RefOracle.hier_centralization = _ref_hier_centralization
+
+
+def _pow2(v):
+    return v != 0 and (v & (v - 1)) == 0
+
+
+def _co_sizes(self, kind, m, idx, val, block_size=256, coo_bits=64):
+    """message_sizes (zen/codec.hpp:182-211) -> (index_bits, value_bits)."""
+    z = len(idx)
+    if kind == "coo":
+        return coo_bits * z, 32 * z
+    if kind == "bitmap":
+        return m, 32 * z
+    _, info = self.wire_encode(kind, m, idx, val, block_size, coo_bits)
+    return info["index_bits"], info["value_bits"]
+
+
+def _co_hier_centralization(self, m, inputs, kind="coo", block_size=256, coo_bits=64):
+    """Restatement of zen::run_hier_centralization (zen/schemes.hpp:173-193):
+    stage log2(bit) sends states[w] to w ^ bit, then every state becomes
+    merge_sum(states[w], states[w ^ bit]) (zo_merge_sum, tensor.hpp:133-167).
+    Returns (idx, val, ledger[stages][4][n]) like RefOracle."""
+    n = len(inputs)
+    if not _pow2(n):
+        raise OracleError(NON_POWER_OF_TWO, "node count must be a power of two")
+    states = [(_u64(i), _f32(v)) for i, v in inputs]
+    stages = []
+    bit = 1
+    while bit < n:
+        led = np.zeros((4, n), np.uint64)
+        for w in range(n):
+            ib, vb = _co_sizes(self, kind, m, *states[w], block_size, coo_bits)
+            to = w ^ bit
+            led[0, w] += ib + vb
+            led[1, to] += ib + vb
+            led[2, to] += ib
+            led[3, to] += vb
+        stages.append(led)
+        states = [self.merge_sum(*states[w], *states[w ^ bit]) for w in range(n)]
+        bit <<= 1
+    for i, v in states[1:]:
+        assert np.array_equal(i, states[0][0]) and np.array_equal(v.view(np.uint32),
+                                                                   states[0][1].view(np.uint32))
+    led = np.stack(stages) if stages else np.zeros((0, 4, n), np.uint64)
+    return states[0][0], states[0][1], led
+
+
+def _co_skewness(m, idx, partitions):
+    """zen::skewness_ratio (zen/tensor.hpp:192-213)."""
+    idx = _u64(idx)
+    rng = (m + partitions - 1) // partitions
+    best = 0.0
+    for p in range(partitions):
+        lo = p * rng
+        if lo >= m:
+            break
+        hi = min(m, lo + rng)
+        c = int(np.searchsorted(idx, np.uint64(hi)) - np.searchsorted(idx, np.uint64(lo)))
+        best = max(best, float(c) / float(hi - lo))
+    return best / (float(idx.size) / float(m))
+
+
+def _co_profile(self, m, rounds):
+    """Restatement of zen::profile_sparsity (zen/costmodel.hpp:151-195) and
+    select_scheme (:139-149) -> (d, {k: gamma}, skew, choice 0 BP / 1 HC)."""
+    n = len(rounds[0])
+    gsum, skew_sum, dsum, dcount = {}, 0.0, 0.0, 0
+    for rnd in rounds:
+        pds = 0.0
+        pi = pv = None
+        for i, (ti, tv) in enumerate(rnd):
+            d = float(len(ti)) / float(m)
+            dsum += d
+            dcount += 1
+            pi, pv = (_u64(ti), _f32(tv)) if i == 0 else self.merge_sum(pi, pv, ti, tv)
+            pds += d
+            k = i + 1
+            if _pow2(k):
+                gsum[k] = gsum.get(k, 0.0) + (float(pi.size) / float(m)) / (pds / float(k))
+            skew_sum += _co_skewness(m, ti, n)
+    gamma = {k: gsum[k] / float(len(rounds)) for k in sorted(gsum)}
+    gamma[1] = 1.0
+    choice = -1
+    if n in gamma:
+        bp = (float(n) - 1.0) / float(n) * (gamma[n] + 1.0) if n > 1 else 0.0
+        hc, k = 0.0, 1
+        while k < n:
+            hc += 1.0 if k == 1 else gamma[k]
+            k *= 2
+        choice = 0 if bp <= hc else 1
+    return dsum / float(dcount), gamma, skew_sum / float(len(rounds) * n), choice
+
+
+COracle.sizes = _co_sizes
+COracle.hier_centralization = _co_hier_centralization
+COracle.profile = _co_profile
+COracle.skewness = staticmethod(_co_skewness)
 
 RefOracle.wire_encode = _ref_wire_encode
 RefOracle.wire_decode = _ref_wire_decode

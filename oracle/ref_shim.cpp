@@ -10,12 +10,14 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <sstream>
 #include <string>
 #include <vector>
 
 #include "zen/codec.hpp"
+#include "zen/costmodel.hpp"
 #include "zen/errors.hpp"
 #include "zen/experiment.hpp"
 #include "zen/hashing.hpp"
@@ -26,7 +28,7 @@
 
 namespace {
 enum { ZR_OK = 0, ZR_INVALID = 1, ZR_OVERFLOW = 2, ZR_OUTSIDE = 3, ZR_MALFORMED = 4, ZR_EMPTY = 5,
-       ZR_MISMATCH = 6, ZR_OTHER = 9 };
+       ZR_MISMATCH = 6, ZR_NONPOW2 = 7, ZR_MISSING = 8, ZR_OTHER = 9 };
 
 thread_local int64_t g_last_partition = -1;
 thread_local char g_last_msg[512];
@@ -49,6 +51,12 @@ int guarded(F&& f) {
   } catch (const zen::EmptyTensor& e) {
     std::snprintf(g_last_msg, sizeof g_last_msg, "%s", e.what());
     return ZR_EMPTY;
+  } catch (const zen::NonPowerOfTwo& e) {
+    std::snprintf(g_last_msg, sizeof g_last_msg, "%s", e.what());
+    return ZR_NONPOW2;
+  } catch (const zen::MissingProfileEntry& e) {
+    std::snprintf(g_last_msg, sizeof g_last_msg, "%s", e.what());
+    return ZR_MISSING;
   } catch (const zen::UniverseMismatch& e) {
     std::snprintf(g_last_msg, sizeof g_last_msg, "%s", e.what());
     return ZR_MISMATCH;
@@ -427,6 +435,95 @@ int ref_sparsify_topk(const float* dense, uint64_t m, double fraction, uint64_t*
     std::copy(t.indices().begin(), t.indices().end(), idx);
     std::copy(t.values().begin(), t.values().end(), val);
     *out_count = t.nnz();
+  });
+}
+
+// zen::merge_sum (zen/tensor.hpp:133-167)
+int ref_merge_sum(uint64_t m, const uint64_t* ai, const float* av, uint64_t na, const uint64_t* bi,
+                  const float* bv, uint64_t nb, uint64_t* out_idx, float* out_val,
+                  uint64_t* out_count) {
+  return guarded([&] {
+    auto r = zen::merge_sum(make_tensor(m, ai, av, na), make_tensor(m, bi, bv, nb));
+    std::copy(r.indices().begin(), r.indices().end(), out_idx);
+    std::copy(r.values().begin(), r.values().end(), out_val);
+    *out_count = r.nnz();
+  });
+}
+
+// zen::overlap_ratio / densification_ratio / skewness_ratio (zen/tensor.hpp:111-213).
+// what: 0 overlap(t0, t1), 1 densification(all), 2 skewness(t0, partitions)
+int ref_tensor_metric(int what, uint32_t n, uint64_t m, const uint64_t* const* idx,
+                      const float* const* val, const uint64_t* nnz, uint32_t partitions,
+                      double* out) {
+  return guarded([&] {
+    std::vector<zen::SparseTensor> ts;
+    for (uint32_t w = 0; w < n; ++w) ts.push_back(make_tensor(m, idx[w], val[w], nnz[w]));
+    if (what == 0) *out = zen::overlap_ratio(ts.at(0), ts.at(1));
+    else if (what == 1) *out = zen::densification_ratio(ts);
+    else *out = zen::skewness_ratio(ts.at(0), partitions);
+  });
+}
+
+// zen::profile_sparsity over R rounds of n tensors (zen/costmodel.hpp:151-195)
+// and zen::select_scheme(profile, n) (:139-149).  gamma[j] = gamma at k = 2^j,
+// j <= log2(n) (NaN where absent); *choice: 0 BP, 1 HC, -1 when select throws.
+int ref_profile(uint32_t rounds, uint32_t n, uint64_t m, const uint64_t* const* idx,
+                const float* const* val, const uint64_t* nnz, double* d, double* gamma,
+                uint32_t gamma_len, double* skew, int* choice) {
+  return guarded([&] {
+    std::vector<std::vector<zen::SparseTensor>> rs(rounds);
+    for (uint32_t r = 0; r < rounds; ++r)
+      for (uint32_t w = 0; w < n; ++w)
+        rs[r].push_back(make_tensor(m, idx[r * n + w], val[r * n + w], nnz[r * n + w]));
+    auto p = zen::profile_sparsity(rs);
+    *d = p.d;
+    for (uint32_t j = 0; j < gamma_len; ++j) {
+      auto it = p.gamma.find(1ull << j);
+      gamma[j] = it == p.gamma.end() ? std::numeric_limits<double>::quiet_NaN() : it->second;
+    }
+    *skew = p.skew.at(n);
+    try {
+      *choice = zen::select_scheme(p, n) == zen::SchemeChoice::BalancedParallelism ? 0 : 1;
+    } catch (const zen::MissingProfileEntry&) {
+      *choice = -1;
+    }
+  });
+}
+
+// zen::run_hier_centralization (zen/schemes.hpp:173-193); wire kind as in
+// ref_wire_encode (1 coo, 2 bitmap, 3 tensor block).  ledger: [stages][4][n];
+// *stages = recorded stage count (<= max_stages).
+int ref_hier_centralization(uint32_t n, uint64_t m, const uint64_t* const* idx,
+                            const float* const* val, const uint64_t* nnz, uint32_t kind,
+                            uint32_t block_size, uint32_t coo_bits, uint64_t* out_idx,
+                            float* out_val, uint64_t* out_count, uint64_t* ledger,
+                            uint32_t max_stages, uint32_t* stages, int* all_equal) {
+  return guarded([&] {
+    std::vector<zen::SparseTensor> inputs;
+    for (uint32_t w = 0; w < n; ++w) inputs.push_back(make_tensor(m, idx[w], val[w], nnz[w]));
+    zen::WireFormat fmt = kind == 2   ? zen::WireFormat::bitmap()
+                          : kind == 3 ? zen::WireFormat::tensor_block(block_size)
+                                      : zen::WireFormat::coo(coo_bits);
+    zen::SimNet net(n, 1.0);
+    auto out = zen::run_hier_centralization(inputs, net, fmt);
+    const auto& r = out.results[0];
+    std::copy(r.indices().begin(), r.indices().end(), out_idx);
+    std::copy(r.values().begin(), r.values().end(), out_val);
+    *out_count = r.nnz();
+    int eq = 1;
+    for (const auto& x : out.results) eq = eq && (x == r);
+    *all_equal = eq;
+    const uint32_t ns = uint32_t(std::min<size_t>(max_stages, out.traffic.stages.size()));
+    *stages = ns;
+    for (uint32_t st = 0; st < ns; ++st) {
+      const auto& s = out.traffic.stages[st];
+      for (uint32_t node = 0; node < n; ++node) {
+        ledger[(st * 4 + 0) * n + node] = s.sent_bits[node];
+        ledger[(st * 4 + 1) * n + node] = s.recv_bits[node];
+        ledger[(st * 4 + 2) * n + node] = s.recv_index_bits[node];
+        ledger[(st * 4 + 3) * n + node] = s.recv_value_bits[node];
+      }
+    }
   });
 }
 

@@ -16,3 +16,9 @@ from .zen import (  # noqa: F401
     run_balanced_parallelism, run_bp_with_retry, sparsify_topk, to_sparse, write_framed,
     write_sparse,
     write_sparse_file)
+from .schemes import (  # noqa: F401
+    BALANCED_PARALLELISM, HIERARCHICAL_CENTRALIZATION, CostInputs, HCSynchronizer,
+    MissingProfileEntry, NonPowerOfTwo, SparsityProfile, densification_ratio, density,
+    merge_sum, overlap_ratio, profile_sparsity, run_hier_centralization, select_scheme,
+    skewness_ratio, t_allreduce_dense, t_bp, t_bp_coefficient, t_hc, t_hc_coefficient,
+    t_hierarchy_incremental_lb, t_ring_incremental, t_sparse_ps, t_sparse_ps_broadcast)

@@ -65,6 +65,18 @@ _SIGS = {
     "zen_frame_parse": (C.c_int, [vp, u64, P(WireFormatC), P(MessageInfoC)]),
     "zen_sparsify_topk": (C.c_int, [vp, vp, u64, C.c_double, vp, vp, u64, P(u64)]),
     "zen_axpy_sparse": (C.c_int, [vp, vp, u64, vp, vp, u64, C.c_float]),
+    "zen_merge_sum": (C.c_int, [vp, vp, vp, u64, vp, vp, u64, u64, vp, vp, u64, P(u64)]),
+    "zen_range_counts": (C.c_int, [vp, vp, u64, u64, u32, P(u64)]),
+    "zen_hc_create": (C.c_int, [vp, u32, u32, u64, u64, P(vp)]),
+    "zen_hc_destroy": (None, [vp]),
+    "zen_hc_ipc_handle": (C.c_int, [vp, vp]),
+    "zen_hc_connect": (C.c_int, [vp, vp]),
+    "zen_hc_sync_dense": (C.c_int, [vp, vp]),
+    "zen_hc_sync_sparse": (C.c_int, [vp, vp, vp, u64]),
+    "zen_hc_wait": (C.c_int, [vp]),
+    "zen_hc_result": (C.c_int, [vp, P(vp), P(vp), P(u64)]),
+    "zen_hc_copy_result": (C.c_int, [vp, vp, vp, u64, P(u64)]),
+    "zen_hc_stage_counts": (C.c_int, [vp, P(u64)]),
     "zen_abi_version": (u32, []),
     "zen_status_string": (C.c_char_p, [C.c_int]),
     "zen_last_error_message": (C.c_char_p, []),

@@ -1117,6 +1117,83 @@ zen_status zen_frame_parse(const uint8_t* in, uint64_t available, zen_wire_forma
 
 }  // extern "C"
 
+// ------------------------------------------------------------- merge_sum ----
+// zen::merge_sum (zen/tensor.hpp:133-167): the fold step of every scheme;
+// Hierarchical Centralization (zen/schemes.hpp:173-193) is one per stage.
+
+extern "C" zen_status zen_merge_sum(zen_ctx* c, const uint64_t* a_idx, const float* a_val,
+                                    uint64_t na, const uint64_t* b_idx, const float* b_val,
+                                    uint64_t nb, uint64_t universe, uint64_t* d_idx,
+                                    float* d_val, uint64_t capacity, uint64_t* count) {
+  if (!c || !count) return fail(ZEN_E_INVALID, "null argument");
+  if ((na && (!a_idx || !a_val)) || (nb && (!b_idx || !b_val)))
+    return fail(ZEN_E_INVALID, "null tensor");
+  if (na + nb >= (1ull << 31)) return fail(ZEN_E_INVALID, "merge above 2^31 entries");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  // one merge-path kernel (k_merge.cu); counts in device memory
+  const uint32_t tiles = hc_merge_tiles(na + nb);
+  Bump sc;
+  CKR(ctx_scratch(c, bump_bytes({32, sizeof(LookbackCtl), 8ull * tiles}), &sc));
+  uint64_t* st = sc.get<uint64_t>(4);  // [na, nb, out count, status]
+  LookbackCtl* ctl = sc.get<LookbackCtl>(1);
+  unsigned long long* lb = sc.get<unsigned long long>(tiles);
+  const uint64_t h_in[4] = {na, nb, 0, 0};
+  CK(cudaMemcpyAsync(st, h_in, 32, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(ctl, 0, sizeof(LookbackCtl), c->stream));
+  CK(cudaMemsetAsync(lb, 0, 8ull * tiles, c->stream));
+  // both inputs must be SparseTensors of the same universe (tensor.hpp:133-135)
+  uint32_t* err = (uint32_t*)(st + 3);
+  launch_check_canonical(a_idx, na, universe, err, c->stream);
+  launch_check_canonical(b_idx, nb, universe, err, c->stream);
+  HcMergeArgs m{};
+  m.a_idx = a_idx;
+  m.a_val = a_val;
+  m.a_cnt = st;
+  m.a_cap = na;
+  m.b_idx = b_idx;
+  m.b_val = b_val;
+  m.b_cnt = st + 1;
+  m.b_cap = nb;
+  m.o_idx = d_idx;
+  m.o_val = d_val;
+  m.o_cnt = st + 2;
+  m.o_cap = capacity;
+  m.lb_status = lb;
+  m.ctl = ctl;
+  m.err = err + 1;  // merge bits apart from the input check's
+  launch_hc_merge(m, tiles, c->stream);
+  uint64_t h[4];
+  CK(cudaMemcpyAsync(h, st, 32, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const uint32_t in_bits = uint32_t(h[3]), merge_bits = uint32_t(h[3] >> 32);
+  if (in_bits || (merge_bits & kErrOutside))
+    return fail(ZEN_E_INVALID, "tensor indices not sorted/unique or >= M");
+  *count = h[2];
+  if (h[2] > capacity) return fail(ZEN_E_CAPACITY, "output capacity");
+  return ZEN_OK;
+}
+
+// zen::skewness_ratio's per-range counts (zen/tensor.hpp:193-213): entries of
+// the sorted tensor in each of `partitions` contiguous ranges of ceil(M/n).
+extern "C" zen_status zen_range_counts(zen_ctx* c, const uint64_t* d_idx, uint64_t count,
+                                       uint64_t universe, uint32_t partitions,
+                                       uint64_t* h_counts) {
+  if (!c || !h_counts || (count && !d_idx)) return fail(ZEN_E_INVALID, "null argument");
+  if (!partitions || !universe) return fail(ZEN_E_INVALID, "partitions and universe must be >= 1");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  Bump sc;
+  CKR(ctx_scratch(c, bump_bytes({8ull * (partitions + 1)}), &sc));
+  uint64_t* bnd = sc.get<uint64_t>(partitions + 1);
+  launch_range_bounds(d_idx, count, universe, partitions, bnd, c->stream);
+  std::vector<uint64_t> h(partitions + 1);
+  CK(cudaMemcpyAsync(h.data(), bnd, 8ull * (partitions + 1), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (uint32_t p = 0; p < partitions; ++p) h_counts[p] = h[p + 1] - h[p];
+  return ZEN_OK;
+}
+
 // ----------------------------------------------------------------- apply ----
 
 extern "C" zen_status zen_axpy_sparse(zen_ctx* c, float* d_dense, uint64_t m,
@@ -2164,3 +2241,323 @@ extern "C" zen_status zen_bp_debug_part(zen_bp* bp, int what, uint32_t server, u
   CK(cudaMemcpy(h_val, A.inbox_val(L) + size_t(worker) * bp->cap, c * 4, cudaMemcpyDeviceToHost));
   return ZEN_OK;
 }
+
+// ============================================== Hierarchical Centralization ==
+// zen::run_hier_centralization (zen/schemes.hpp:173-193), one process per GPU:
+// recursive doubling, stage s exchanging with rank ^ 2^s over NVLink stores
+// into the partner's CUDA-IPC arena and folding with the merge-path merge_sum
+// (k_merge.cu).  Counts never leave the device; a dense sync is one graph.
+
+namespace {
+constexpr uint32_t kHcMaxStages = 8;  // n <= 256
+
+struct HcHdr {
+  unsigned long long epoch;
+  unsigned long long ready[kHcMaxStages];  // set by the stage-s partner's push
+  unsigned long long done[kHcMaxStages];   // set by the stage-s partner's merge
+  uint64_t cnt[2];                         // state ping-pong counts
+  uint64_t rcnt[kHcMaxStages];             // received counts
+  uint64_t stage_cnt[kHcMaxStages];        // |state| sent at stage s (ledger)
+  uint32_t err;                            // kErr* bits
+  uint32_t in_err;                         // kWire* bits of the input check
+};
+
+}  // namespace
+
+struct zen_hc {
+  zen_ctx* ctx = nullptr;
+  uint32_t n = 0, rank = 0, L = 0;
+  uint64_t m = 0, max_nnz = 0, cap = 0;
+  uint64_t stage_cap[kHcMaxStages] = {};
+  size_t off_buf[2][2] = {}, off_recv[kHcMaxStages][2] = {}, bytes = 0;
+  char* base = nullptr;
+  std::vector<char*> peer;  // arena base of every rank (own at `rank`)
+  bool connected = false;
+  DevMem mem;
+  ExtractWs<uint64_t> ex{};
+  unsigned long long* lb = nullptr;
+  LookbackCtl* ctl_merge = nullptr;
+  LookbackCtl* ctl_push = nullptr;
+  cudaGraph_t gdef = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const float* gdense = nullptr;
+  cudaStream_t gstream = nullptr;
+  uint32_t graph_kernels = 0;
+  uint64_t h_result = 0;
+  HcHdr* hdr(uint32_t r) const { return reinterpret_cast<HcHdr*>(peer[r]); }
+  uint64_t* idx(uint32_t r, size_t off) const { return reinterpret_cast<uint64_t*>(peer[r] + off); }
+  float* val(uint32_t r, size_t off) const { return reinterpret_cast<float*>(peer[r] + off); }
+};
+
+namespace {
+
+zen_status hc_enqueue(zen_hc* h, const float* dense, const uint64_t* in_idx, const float* in_val,
+                      uint64_t in_count) {
+  cudaStream_t st = h->ctx->stream;
+  HcHdr* me = h->hdr(h->rank);
+  launch_hc_begin(&me->epoch, st);
+  if (dense) {
+    launch_extract<uint64_t>(dense, h->m, h->ex, h->idx(h->rank, h->off_buf[0][0]),
+                             h->val(h->rank, h->off_buf[0][1]), &me->cnt[0], h->max_nnz, &me->err,
+                             st);
+  } else {
+    if (in_count) {
+      CK(cudaMemcpyAsync(h->idx(h->rank, h->off_buf[0][0]), in_idx, in_count * 8,
+                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(h->val(h->rank, h->off_buf[0][1]), in_val, in_count * 4,
+                         cudaMemcpyDeviceToDevice, st));
+    }
+    launch_check_canonical(in_idx, in_count, h->m, &me->in_err, st);
+    launch_set_u64(&me->cnt[0], in_count, st);
+  }
+  for (uint32_t s = 0; s < h->L; ++s) {
+    const uint32_t q = h->rank ^ (1u << s), in = s & 1, out = in ^ 1;
+    HcHdr* ph = h->hdr(q);
+    HcPushArgs p{};
+    p.src_idx = h->idx(h->rank, h->off_buf[in][0]);
+    p.src_val = h->val(h->rank, h->off_buf[in][1]);
+    p.src_cnt = &me->cnt[in];
+    p.dst_idx = h->idx(q, h->off_recv[s][0]);
+    p.dst_val = h->val(q, h->off_recv[s][1]);
+    p.dst_cnt = &ph->rcnt[s];
+    p.cap = h->stage_cap[s];
+    p.ready_flag = &ph->ready[s];
+    p.done_flag = &me->done[s];
+    p.epoch = &me->epoch;
+    p.ctl = h->ctl_push;
+    p.err = &me->err;
+    launch_hc_push(p, st);
+    HcMergeArgs a{};
+    a.a_idx = p.src_idx;
+    a.a_val = p.src_val;
+    a.a_cnt = p.src_cnt;
+    a.a_cap = h->stage_cap[s];
+    a.b_idx = h->idx(h->rank, h->off_recv[s][0]);
+    a.b_val = h->val(h->rank, h->off_recv[s][1]);
+    a.b_cnt = &me->rcnt[s];
+    a.b_cap = h->stage_cap[s];
+    a.o_idx = h->idx(h->rank, h->off_buf[out][0]);
+    a.o_val = h->val(h->rank, h->off_buf[out][1]);
+    a.o_cnt = &me->cnt[out];
+    a.o_cap = h->cap;
+    a.lb_status = h->lb;
+    a.ctl = h->ctl_merge;
+    a.err = &me->err;
+    a.wait_flag = &me->ready[s];
+    a.done_flag = &ph->done[s];
+    a.epoch = &me->epoch;
+    a.stage_cnt = &me->stage_cnt[s];
+    launch_hc_merge(a, hc_merge_tiles(2 * h->stage_cap[s]), st);
+  }
+  return ZEN_OK;
+}
+
+void hc_drop_graph(zen_hc* h) {
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gdef) cudaGraphDestroy(h->gdef);
+  h->gexec = nullptr;
+  h->gdef = nullptr;
+  h->gdense = nullptr;
+  h->gstream = nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+zen_status zen_hc_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t universe,
+                         uint64_t max_nnz, zen_hc** out) {
+  if (!c || !out) return fail(ZEN_E_INVALID, "null argument");
+  if (n == 0 || (n & (n - 1)) != 0) return fail(ZEN_E_INVALID, "node count must be a power of two");
+  if (n > (1u << kHcMaxStages)) return fail(ZEN_E_INVALID, "node count above 256");
+  if (rank >= n) return fail(ZEN_E_INVALID, "rank out of range");
+  if (universe == 0) return fail(ZEN_E_INVALID, "universe must be at least 1");
+  if (max_nnz == 0) return fail(ZEN_E_INVALID, "max_nnz must be at least 1");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  std::unique_ptr<zen_hc> h(new zen_hc);
+  h->ctx = c;
+  h->n = n;
+  h->rank = rank;
+  h->m = universe;
+  h->max_nnz = std::min(max_nnz, universe);
+  while ((1u << h->L) < n) ++h->L;
+  h->cap = std::min<uint64_t>(universe, uint64_t(n) * h->max_nnz);
+  size_t off = align256(sizeof(HcHdr));
+  for (int b = 0; b < 2; ++b) {
+    h->off_buf[b][0] = off;
+    off += align256(h->cap * 8);
+    h->off_buf[b][1] = off;
+    off += align256(h->cap * 4);
+  }
+  for (uint32_t s = 0; s < h->L; ++s) {
+    h->stage_cap[s] = std::min<uint64_t>(universe, (uint64_t(1) << s) * h->max_nnz);
+    h->off_recv[s][0] = off;
+    off += align256(h->stage_cap[s] * 8);
+    h->off_recv[s][1] = off;
+    off += align256(h->stage_cap[s] * 4);
+  }
+  h->bytes = off;
+  CK(cudaMalloc(&h->base, h->bytes));
+  CK(cudaMemsetAsync(h->base, 0, sizeof(HcHdr), c->stream));
+  h->peer.assign(n, nullptr);
+  h->peer[rank] = h->base;
+  h->connected = n == 1;
+  const uint64_t ntiles = (universe + kExtractTile - 1) / kExtractTile;
+  CKR(h->mem.alloc(&h->ex.st_idx, ntiles * kExtractTile, false));
+  CKR(h->mem.alloc(&h->ex.st_val, ntiles * kExtractTile, false));
+  CKR(h->mem.alloc(&h->ex.tile_cnt, ntiles));
+  CKR(h->mem.alloc(&h->ex.tile_base, ntiles));
+  h->ex.nblk = (h->max_nnz + 255) / 256;
+  CKR(h->mem.alloc(&h->ex.blk_tile, h->ex.nblk + 1));
+  uint64_t max_tiles = 1;
+  for (uint32_t s = 0; s < h->L; ++s)
+    max_tiles = std::max<uint64_t>(max_tiles, hc_merge_tiles(2 * h->stage_cap[s]));
+  CKR(h->mem.alloc(&h->lb, max_tiles));
+  CKR(h->mem.alloc(&h->ctl_merge, 1));
+  CKR(h->mem.alloc(&h->ctl_push, 1));
+  CK(cudaStreamSynchronize(c->stream));
+  *out = h.release();
+  return ZEN_OK;
+}
+
+void zen_hc_destroy(zen_hc* h) {
+  if (!h) return;
+  DevGuard g(h->ctx->device);
+  cudaDeviceSynchronize();
+  hc_drop_graph(h);
+  for (uint32_t r = 0; r < h->n; ++r)
+    if (r != h->rank && h->peer[r]) cudaIpcCloseMemHandle(h->peer[r]);
+  if (h->base) cudaFree(h->base);
+  delete h;
+}
+
+zen_status zen_hc_ipc_handle(zen_hc* h, void* out) {
+  if (!h || !out) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(h->ctx->device);
+  cudaIpcMemHandle_t ih;
+  CK(cudaIpcGetMemHandle(&ih, h->base));
+  std::memcpy(out, &ih, sizeof(ih));
+  return ZEN_OK;
+}
+
+zen_status zen_hc_connect(zen_hc* h, const void* handles) {
+  if (!h || !handles) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(h->ctx->device);
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  // only the log2(n) partners are ever touched
+  for (uint32_t s = 0; s < h->L; ++s) {
+    const uint32_t r = h->rank ^ (1u << s);
+    if (h->peer[r]) continue;
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ZEN_E_PEER, std::string("cudaIpcOpenMemHandle(rank ") + std::to_string(r) +
+                                  "): " + cudaGetErrorString(e));
+    }
+    h->peer[r] = static_cast<char*>(p);
+  }
+  h->connected = true;
+  hc_drop_graph(h);
+  return ZEN_OK;
+}
+
+zen_status zen_hc_sync_dense(zen_hc* h, const float* d_dense) {
+  if (!h || !d_dense) return fail(ZEN_E_INVALID, "null argument");
+  if (!h->connected) return fail(ZEN_E_INVALID, "zen_hc_connect has not been called");
+  DevGuard g(h->ctx->device);
+  cudaStream_t st = h->ctx->stream;
+  if (st == nullptr) {  // the legacy stream cannot be captured
+    CKR(hc_enqueue(h, d_dense, nullptr, nullptr, 0));
+    return ZEN_OK;
+  }
+  if (!h->gexec || h->gdense != d_dense || h->gstream != st) {
+    hc_drop_graph(h);
+    const uint64_t before = g_launches.load();
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    zen_status rc = hc_enqueue(h, d_dense, nullptr, nullptr, 0);
+    cudaGraph_t gd = nullptr;
+    cudaError_t e = cudaStreamEndCapture(st, &gd);
+    if (rc != ZEN_OK) {
+      if (gd) cudaGraphDestroy(gd);
+      return rc;
+    }
+    CK(e);
+    h->graph_kernels = uint32_t(g_launches.load() - before);
+    g_launches.fetch_sub(h->graph_kernels);
+    CK(cudaGraphInstantiate(&h->gexec, gd, 0));
+    h->gdef = gd;
+    h->gdense = d_dense;
+    h->gstream = st;
+  }
+  CK(cudaGraphLaunch(h->gexec, st));
+  g_launches.fetch_add(h->graph_kernels);
+  return ZEN_OK;
+}
+
+zen_status zen_hc_sync_sparse(zen_hc* h, const uint64_t* d_idx, const float* d_val,
+                              uint64_t count) {
+  if (!h) return fail(ZEN_E_INVALID, "null argument");
+  if (count && (!d_idx || !d_val)) return fail(ZEN_E_INVALID, "null tensor");
+  if (count > h->max_nnz) return fail(ZEN_E_CAPACITY, "input above max_nnz");
+  if (!h->connected) return fail(ZEN_E_INVALID, "zen_hc_connect has not been called");
+  DevGuard g(h->ctx->device);
+  return hc_enqueue(h, nullptr, d_idx, d_val, count);
+}
+
+zen_status zen_hc_wait(zen_hc* h) {
+  if (!h) return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(h->ctx->device);
+  HcHdr hh;
+  CK(cudaMemcpyAsync(&hh, h->base, sizeof(HcHdr), cudaMemcpyDeviceToHost, h->ctx->stream));
+  CK(cudaStreamSynchronize(h->ctx->stream));
+  if (hh.err || hh.in_err) {
+    const uint32_t e = hh.err, ie = hh.in_err;
+    uint32_t zero[2] = {0, 0};
+    CK(cudaMemcpy(&h->hdr(h->rank)->err, zero, 8, cudaMemcpyHostToDevice));
+    if (e & kErrTimeout) return fail(ZEN_E_TIMEOUT, "a hierarchy partner never signalled");
+    if (ie) return fail(ZEN_E_INVALID, "tensor indices not sorted/unique or >= M");
+    return fail(ZEN_E_CAPACITY, "non-zeros above max_nnz");
+  }
+  h->h_result = hh.cnt[h->L & 1];
+  return ZEN_OK;
+}
+
+zen_status zen_hc_result(zen_hc* h, const uint64_t** d_idx, const float** d_val,
+                         uint64_t* count) {
+  if (!h) return fail(ZEN_E_INVALID, "null argument");
+  CKR(zen_hc_wait(h));
+  const uint32_t b = h->L & 1;
+  if (d_idx) *d_idx = h->idx(h->rank, h->off_buf[b][0]);
+  if (d_val) *d_val = h->val(h->rank, h->off_buf[b][1]);
+  if (count) *count = h->h_result;
+  return ZEN_OK;
+}
+
+zen_status zen_hc_copy_result(zen_hc* h, uint64_t* d_idx, float* d_val, uint64_t capacity,
+                              uint64_t* count) {
+  if (!h || !count) return fail(ZEN_E_INVALID, "null argument");
+  const uint64_t* si;
+  const float* sv;
+  CKR(zen_hc_result(h, &si, &sv, count));
+  if (*count > capacity) return fail(ZEN_E_CAPACITY, "result buffer too small");
+  cudaStream_t st = h->ctx->stream;
+  if (*count) {
+    CK(cudaMemcpyAsync(d_idx, si, *count * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(d_val, sv, *count * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return ZEN_OK;
+}
+
+zen_status zen_hc_stage_counts(zen_hc* h, uint64_t* counts) {
+  if (!h || !counts) return fail(ZEN_E_INVALID, "null argument");
+  CKR(zen_hc_wait(h));
+  HcHdr hh;
+  CK(cudaMemcpy(&hh, h->base, sizeof(HcHdr), cudaMemcpyDeviceToHost));
+  for (uint32_t s = 0; s < h->L; ++s) counts[s] = hh.stage_cnt[s];
+  return ZEN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,294 @@
+// Hierarchical Centralization on B200: recursive
+// doubling (zen/schemes.hpp:173-193), one process per GPU.
+//
+// Stage s of rank r with partner q = r ^ 2^s:
+//   k_hc_push   my state -> q's receive buffer for stage s, as NVLink stores
+//               into q's CUDA-IPC arena.  The last block releases q.ready[s].
+//   k_hc_merge  merge_sum(my state, received state) -> my next state
+//               (zen/tensor.hpp:133-167).  Every block first acquires
+//               my.ready[s].  The last block releases q.done[s]: "your stage-s
+//               push was consumed", which q waits on before its next push into
+//               my receive buffer (one sync later).
+// Counts stay in device memory, so a whole sync is one CUDA graph with no host
+// round trip.
+//
+// The merge is a merge-path merge.  Each 2048-entry tile of the merged
+// sequence finds its split of the two sorted inputs by binary search, merges in
+// shared memory and folds each shared index into one entry.  A decoupled
+// look-back places the tile's unique entries.  On a tie the first input's entry
+// comes first, so a shared index sums to a + b, the reference's operand order.
+#include <cstdint>
+
+#include "zen_common.cuh"
+#include "zen_internal.h"
+
+namespace zen {
+
+extern void count_launch();
+
+namespace {
+
+using namespace zen_dev;
+
+constexpr uint32_t kMergeThreads = 256;
+constexpr uint32_t kMergeItems = 8;
+constexpr uint32_t kMergeTile = kMergeThreads * kMergeItems;  // merged positions per tile
+
+// number of A entries among the first d merged positions (A first on ties)
+template <typename KA, typename KB>
+__device__ __forceinline__ uint64_t merge_split(const KA& A, uint64_t na, const KB& B, uint64_t nb,
+                                                uint64_t d) {
+  uint64_t lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (A[mid] <= B[d - 1 - mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+struct SmemArr {  // indexable view of a shared-memory slice
+  const uint64_t* p;
+  __device__ __forceinline__ uint64_t operator[](uint64_t i) const { return p[i]; }
+};
+
+__global__ void __launch_bounds__(kMergeThreads) k_hc_merge(HcMergeArgs a) {
+  pdl_entry();
+  __shared__ uint64_t sk[kMergeTile];
+  __shared__ float sv[kMergeTile];
+  __shared__ uint64_t s_split[2];
+  __shared__ uint32_t s_tile, s_warp[kMergeThreads / 32];
+  __shared__ uint64_t s_excl;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t ep = a.epoch ? *(volatile const unsigned long long*)a.epoch : 0;
+  if (a.wait_flag && tid == 0 && !wait_flag(a.wait_flag, ep, kPeerTimeoutNs))
+    atomicOr(a.err, kErrTimeout);
+  const uint32_t tile = take_ticket(a.ctl, &s_tile);  // also orders the wait above
+  const uint32_t tag = *(volatile uint32_t*)&a.ctl->tag;
+  uint64_t na = *(volatile const uint64_t*)a.a_cnt, nb = *(volatile const uint64_t*)a.b_cnt;
+  if (na > a.a_cap || nb > a.b_cap) {
+    if (tid == 0) atomicOr(a.err, kErrCapacity);
+    na = na > a.a_cap ? a.a_cap : na;
+    nb = nb > a.b_cap ? a.b_cap : nb;
+  }
+  const uint64_t tot = na + nb;
+  const uint64_t lo = uint64_t(tile) * kMergeTile;
+  const bool live = lo < tot;
+  const uint64_t hi = live ? (tot - lo < kMergeTile ? tot : lo + kMergeTile) : lo;
+  if (tile == 0 && tid == 0 && a.stage_cnt) *a.stage_cnt = na;
+
+  // ---- tile split + staging ----
+  if (live && (tid == 0 || tid == 32))
+    s_split[tid >> 5] = merge_split(a.a_idx, na, a.b_idx, nb, tid == 0 ? lo : hi);
+  __syncthreads();
+  uint64_t a0 = live ? s_split[0] : 0, a1 = live ? s_split[1] : 0;
+  uint64_t b0 = lo - a0, b1 = hi - a1;
+  if (a1 < a0 || b1 < b0) {  // only unsorted input: skip the tile, report it
+    if (tid == 0) atomicOr(a.err, kErrOutside);
+    a1 = a0;
+    b1 = b0;
+  }
+  const uint32_t la = (uint32_t)(a1 - a0), lb = (uint32_t)(b1 - b0);
+  const uint32_t len = la + lb;
+  for (uint32_t x = tid; x < len; x += kMergeThreads) {
+    if (x < la) {
+      sk[x] = a.a_idx[a0 + x];
+      sv[x] = a.a_val[a0 + x];
+    } else {
+      sk[x] = a.b_idx[b0 + x - la];
+      sv[x] = a.b_val[b0 + x - la];
+    }
+  }
+  __syncthreads();
+
+  // ---- per-thread merge of up to 8 positions ----
+  uint64_t key[kMergeItems];
+  float val[kMergeItems];
+  bool keep[kMergeItems];
+  uint32_t u = 0;
+  const uint32_t d = tid * kMergeItems;
+  if (d < len) {
+    const SmemArr A{sk}, B{sk + la};
+    uint32_t i = (uint32_t)merge_split(A, la, B, lb, d), j = d - i;
+    // merged predecessor of local position d (the larger of the two last consumed)
+    bool has_prev;
+    uint64_t prev = 0;
+    if (d == 0) {
+      const bool pa = a0 > 0, pb = b0 > 0;
+      has_prev = pa || pb;
+      const uint64_t ka = pa ? a.a_idx[a0 - 1] : 0, kb = pb ? a.b_idx[b0 - 1] : 0;
+      prev = pa && pb ? (ka > kb ? ka : kb) : (pa ? ka : kb);
+    } else {
+      has_prev = true;
+      const uint64_t ka = i > 0 ? A[i - 1] : 0, kb = j > 0 ? B[j - 1] : 0;
+      prev = i > 0 && j > 0 ? (ka > kb ? ka : kb) : (i > 0 ? ka : kb);
+    }
+    const uint32_t cnt = len - d < kMergeItems ? len - d : kMergeItems;
+#pragma unroll
+    for (uint32_t k = 0; k < kMergeItems; ++k) {
+      if (k < cnt) {
+        const bool ta = i < la && (j >= lb || A[i] <= B[j]);
+        key[k] = ta ? A[i] : B[j];
+        val[k] = ta ? sv[i] : sv[la + j];
+        if (ta) ++i; else ++j;
+      }
+    }
+    // the merged entry after this thread's last one (next thread's or next tile's)
+    bool has_next = false;
+    uint64_t nkey = 0;
+    float nval = 0.f;
+    if (d + cnt < len) {
+      has_next = true;
+      const bool ta = i < la && (j >= lb || A[i] <= B[j]);
+      nkey = ta ? A[i] : B[j];
+      nval = ta ? sv[i] : sv[la + j];
+    } else if (hi < tot) {
+      has_next = true;
+      const bool ta = a1 < na && (b1 >= nb || a.a_idx[a1] <= a.b_idx[b1]);
+      nkey = ta ? a.a_idx[a1] : a.b_idx[b1];
+      nval = ta ? a.a_val[a1] : a.b_val[b1];
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kMergeItems; ++k) {
+      keep[k] = false;
+      if (k < cnt) {
+        const bool dup = k == 0 ? (has_prev && prev == key[0]) : key[k - 1] == key[k];
+        keep[k] = !dup;
+        if (!dup) {
+          // a shared index is (A entry, B entry), adjacent: fold b into a
+          if (k + 1 < cnt) {
+            if (key[k + 1] == key[k]) val[k] = val[k] + val[k + 1];
+          } else if (has_next && nkey == key[k]) {
+            val[k] = val[k] + nval;
+          }
+          ++u;
+        }
+      }
+    }
+  }
+
+  // ---- block scan of the unique counts ----
+  const uint32_t lane = tid & 31, warp = tid >> 5;
+  uint32_t incl = u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();  // also: every thread is done reading sk/sv
+  uint32_t wbase = 0, agg = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < kMergeThreads / 32; ++w) {
+    const uint32_t t = s_warp[w];
+    if (w < warp) wbase += t;
+    agg += t;
+  }
+  uint32_t pos = wbase + incl - u;
+  if (d < len) {
+#pragma unroll
+    for (uint32_t k = 0; k < kMergeItems; ++k)
+      if (keep[k]) {
+        sk[pos] = key[k];
+        sv[pos] = val[k];
+        ++pos;
+      }
+  }
+  if (warp == 0) {
+    const uint64_t ex = lookback_warp(a.lb_status, tile, tag, agg);
+    if (lane == 0) s_excl = ex;
+  }
+  __syncthreads();
+  const uint64_t excl = s_excl;
+  for (uint32_t x = tid; x < agg; x += kMergeThreads) {
+    const uint64_t o = excl + x;
+    if (o < a.o_cap) {
+      a.o_idx[o] = sk[x];
+      a.o_val[o] = sv[x];
+    }
+  }
+  if (tid == 0) {
+    const uint64_t total = excl + agg;
+    if ((live && hi == tot) || (tot == 0 && tile == 0)) {
+      if (total > a.o_cap) atomicOr(a.err, kErrCapacity);
+      *a.o_cnt = total;  // the true size; readers clamp to their capacity
+    }
+  }
+  if (finish_tile(a.ctl, gridDim.x, /*sys=*/a.done_flag != nullptr) && a.done_flag && tid == 0) {
+    __threadfence_system();
+    st_release_sys(a.done_flag, ep);
+  }
+}
+
+// my state -> the partner's receive buffer (peer stores); the last block
+// publishes the count and releases the partner's ready flag.
+__global__ void __launch_bounds__(256) k_hc_push(HcPushArgs a) {
+  pdl_entry();
+  const uint32_t tid = threadIdx.x;
+  const uint64_t ep = *(volatile const unsigned long long*)a.epoch;
+  // the partner consumed what this rank pushed into the same buffer last sync
+  if (tid == 0 && ep > 1 && !wait_flag(a.done_flag, ep - 1, kPeerTimeoutNs))
+    atomicOr(a.err, kErrTimeout);
+  __syncthreads();
+  uint64_t n = *(volatile const uint64_t*)a.src_cnt;
+  if (n > a.cap) {
+    if (tid == 0 && blockIdx.x == 0) atomicOr(a.err, kErrCapacity);
+    n = a.cap;
+  }
+  const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + tid, stride = uint64_t(gridDim.x) * blockDim.x;
+  // buffers are 256-byte aligned: 16-byte vectors, then the tails
+  const uint64_t n2 = n >> 1, n4 = n >> 2;
+  const ulonglong2* si = reinterpret_cast<const ulonglong2*>(a.src_idx);
+  ulonglong2* di = reinterpret_cast<ulonglong2*>(a.dst_idx);
+  for (uint64_t x = g; x < n2; x += stride) di[x] = si[x];
+  const float4* sv = reinterpret_cast<const float4*>(a.src_val);
+  float4* dv = reinterpret_cast<float4*>(a.dst_val);
+  for (uint64_t x = g; x < n4; x += stride) dv[x] = sv[x];
+  if (blockIdx.x == 0) {
+    if (tid == 0 && (n & 1)) a.dst_idx[n - 1] = a.src_idx[n - 1];
+    if (tid < (n & 3)) a.dst_val[(n4 << 2) + tid] = a.src_val[(n4 << 2) + tid];
+    if (tid == 0) *a.dst_cnt = n;
+  }
+  if (finish_tile(a.ctl, gridDim.x, /*sys=*/true) && tid == 0) {
+    __threadfence_system();
+    st_release_sys(a.ready_flag, ep);
+  }
+}
+
+__global__ void k_hc_begin(unsigned long long* epoch) {
+  pdl_entry();
+  if (threadIdx.x == 0) *epoch = *epoch + 1;
+}
+
+__global__ void k_set_u64(uint64_t* p, uint64_t v) {
+  pdl_entry();
+  if (threadIdx.x == 0) *p = v;
+}
+
+}  // namespace
+
+uint32_t hc_merge_tiles(uint64_t max_entries) {
+  return (uint32_t)((max_entries + kMergeTile - 1) / kMergeTile) + 1;
+}
+
+void launch_hc_merge(const HcMergeArgs& a, uint32_t tiles, cudaStream_t stream) {
+  launch_k(k_hc_merge, tiles, kMergeThreads, 0, stream, a);
+  count_launch();
+}
+
+void launch_hc_push(const HcPushArgs& a, cudaStream_t stream) {
+  launch_k(k_hc_push, 148 * 2, 256, 0, stream, a);
+  count_launch();
+}
+
+void launch_hc_begin(unsigned long long* epoch, cudaStream_t stream) {
+  launch_k(k_hc_begin, 1, 32, 0, stream, epoch);
+  count_launch();
+}
+
+void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t stream) {
+  launch_k(k_set_u64, 1, 32, 0, stream, p, v);
+  count_launch();
+}
+
+}  // namespace zen

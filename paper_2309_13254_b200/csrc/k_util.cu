@@ -127,6 +127,27 @@ void launch_axpy_sparse(float* dense, uint64_t m, const uint64_t* idx, const flo
   count_launch();
 }
 
+__global__ void k_range_bounds(const uint64_t* __restrict__ idx, uint64_t count, uint64_t m,
+                               uint32_t parts, uint64_t* __restrict__ bnd) {
+  pdl_entry();
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > parts) return;
+  const uint64_t range = (m + parts - 1) / parts;
+  const uint64_t key = p == parts ? m : (uint64_t(p) * range < m ? uint64_t(p) * range : m);
+  uint64_t lo = 0, hi = count;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (idx[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  bnd[p] = lo;
+}
+
+void launch_range_bounds(const uint64_t* idx, uint64_t count, uint64_t m, uint32_t parts,
+                         uint64_t* bnd, cudaStream_t stream) {
+  launch_k(k_range_bounds, (parts + 256) / 256, 256, 0, stream, idx, count, m, parts, bnd);
+  count_launch();
+}
+
 void launch_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t stream) {
   launch_k(k_u32_to_u64, grid_for(n), 256, 0, stream, in, out, n);
   count_launch();

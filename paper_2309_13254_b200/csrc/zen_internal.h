@@ -302,6 +302,52 @@ void launch_topk_finish(const ExtractWs<uint32_t>& ws, uint32_t ntiles, void* st
                         uint64_t* out_count, uint64_t* out_idx, float* out_val, uint64_t cap,
                         cudaStream_t s);
 
+// Hierarchical Centralization + merge_sum (k_merge.cu)
+struct HcMergeArgs {
+  const uint64_t* a_idx;  // first input (this rank's state), sorted unique
+  const float* a_val;
+  const uint64_t* a_cnt;
+  uint64_t a_cap;
+  const uint64_t* b_idx;  // second input (the partner's state, received locally)
+  const float* b_val;
+  const uint64_t* b_cnt;
+  uint64_t b_cap;
+  uint64_t* o_idx;  // merge_sum(a, b); *o_cnt = the true size, writes clamp at o_cap
+  float* o_val;
+  uint64_t* o_cnt;
+  uint64_t o_cap;
+  unsigned long long* lb_status;  // look-back words, one per tile
+  LookbackCtl* ctl;
+  uint32_t* err;                        // kErr* bits (kErrOutside: unsorted input)
+  const unsigned long long* wait_flag;  // local ready flag (nullptr: none)
+  unsigned long long* done_flag;        // the partner's done flag (nullptr: none)
+  const unsigned long long* epoch;      // local sync counter (nullptr: 0)
+  uint64_t* stage_cnt;                  // receives |a| (the ledger), may be null
+};
+struct HcPushArgs {
+  const uint64_t* src_idx;
+  const float* src_val;
+  const uint64_t* src_cnt;
+  uint64_t* dst_idx;  // the partner's receive buffer (peer memory)
+  float* dst_val;
+  uint64_t* dst_cnt;
+  uint64_t cap;
+  unsigned long long* ready_flag;       // the partner's ready flag
+  const unsigned long long* done_flag;  // local: the partner consumed the last push
+  const unsigned long long* epoch;
+  LookbackCtl* ctl;
+  uint32_t* err;
+};
+uint32_t hc_merge_tiles(uint64_t max_entries);
+void launch_hc_merge(const HcMergeArgs& a, uint32_t tiles, cudaStream_t stream);
+void launch_hc_push(const HcPushArgs& a, cudaStream_t stream);
+void launch_hc_begin(unsigned long long* epoch, cudaStream_t stream);
+void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t stream);
+
+// bnd[p] = lower_bound(idx, min(M, p*ceil(M/parts))), p in [0, parts] (k_util.cu)
+void launch_range_bounds(const uint64_t* idx, uint64_t count, uint64_t m, uint32_t parts,
+                         uint64_t* bnd, cudaStream_t stream);
+
 // RAII launch policy for the calling thread (see zen_common.cuh launch_k)
 struct LaunchScope {
   LaunchScope(bool pdl, bool low_priority);

@@ -1,0 +1,478 @@
+"""Hierarchical Centralization, the sparsity profile and the scheme selector
+ on the GPU.
+
+Theorem 1 of the paper has two optima: Balanced Parallelism (zen.py, the hot
+path) and Hierarchical Centralization, recursive doubling that merges at every
+stage.  The selector picks between them from a measured sparsity profile.
+
+Reference interface -> here:
+  zen::merge_sum                      (tensor.hpp:133-167)  merge_sum (zen_merge_sum: CUB merge + reduce-by-key)
+  zen::density / overlap_ratio        (tensor.hpp:106-130)  density / overlap_ratio
+  zen::densification_ratio            (tensor.hpp:178-189)  densification_ratio
+  zen::skewness_ratio                 (tensor.hpp:193-213)  skewness_ratio (zen_range_counts)
+  zen::SparsityProfile                (tensor.hpp:216-240)  SparsityProfile
+  zen::profile_sparsity               (costmodel.hpp:153-195) profile_sparsity
+  zen::CostInputs, t_* formulas       (costmodel.hpp:15-135) CostInputs, t_bp, t_hc, ...
+  zen::select_scheme                  (costmodel.hpp:139-150) select_scheme
+  zen::run_hier_centralization        (schemes.hpp:173-193) run_hier_centralization (one GPU)
+  -- one process per GPU --                                  HCSynchronizer (NCCL P2P + zen_merge_sum)
+
+Every fold is zen_merge_sum.  Its merge may put a shared index's two entries
+in either order.  fp32 addition of two operands is commutative, so each value
+equals the reference's a + b bit for bit.  The same argument makes all n HC
+results identical, exactly as in the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from .zen import (Error, EmptyTensor, SimNet, SparseTensor, SyncOutcome, UniverseMismatch,
+                  WireFormat, _check, _check_inputs, _lib, _ptr, _torch, context)
+
+
+class NonPowerOfTwo(Error):
+    """zen::NonPowerOfTwo (errors.hpp:42-46)."""
+
+    def __init__(self, msg: str = "node count must be a power of two"):
+        super().__init__(msg)
+
+
+class MissingProfileEntry(Error):
+    """zen::MissingProfileEntry (errors.hpp)."""
+
+
+def _pow2(v: int) -> bool:
+    return v != 0 and (v & (v - 1)) == 0
+
+
+# ------------------------------------------------------------- merge_sum ----
+
+def _merge_dev(ai, av, bi, bv, m: int):
+    """Device merge_sum of two canonical (int64 idx, f32 val) tensor pairs."""
+    torch = _torch()
+    dev = ai.device if ai.numel() else bi.device
+    cap = ai.numel() + bi.numel()
+    oi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    ov = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+    got = C.c_uint64()
+    ctx = context(dev.index)
+    _check(_lib().zen_merge_sum(ctx.h, _ptr(ai), _ptr(av), ai.numel(), _ptr(bi), _ptr(bv),
+                                bi.numel(), m, _ptr(oi), _ptr(ov), cap, C.byref(got)))
+    return oi[:got.value], ov[:got.value]
+
+
+def _to_dev(t: SparseTensor):
+    torch = _torch()
+    return (torch.from_numpy(t.indices().view(np.int64)).cuda(),
+            torch.from_numpy(t.values()).cuda())
+
+
+def _to_host(m: int, i, v) -> SparseTensor:
+    return SparseTensor(m, i.cpu().numpy().view(np.uint64), v.cpu().numpy(), _trusted=True)
+
+
+def merge_sum(a: SparseTensor, b: SparseTensor) -> SparseTensor:
+    """zen::merge_sum (tensor.hpp:133-167): union, shared indices summed."""
+    if a.universe() != b.universe():
+        raise UniverseMismatch("tensors have different universe sizes")
+    i, v = _merge_dev(*_to_dev(a), *_to_dev(b), a.universe())
+    return _to_host(a.universe(), i, v)
+
+
+# --------------------------------------------------------------- metrics ----
+
+def density(t: SparseTensor) -> float:
+    """zen::density (tensor.hpp:106-108)."""
+    return float(t.nnz()) / float(t.universe())
+
+
+def overlap_ratio(a: SparseTensor, b: SparseTensor) -> float:
+    """zen::overlap_ratio (tensor.hpp:111-130): |I_a ∩ I_b| / min(|I_a|, |I_b|);
+    the intersection is na + nb - |union| from the device merge."""
+    if a.universe() != b.universe():
+        raise UniverseMismatch("tensors have different universe sizes")
+    if a.empty() or b.empty():
+        raise EmptyTensor("overlap ratio undefined for empty tensors")
+    u, _ = _merge_dev(*_to_dev(a), *_to_dev(b), a.universe())
+    common = a.nnz() + b.nnz() - u.numel()
+    return float(common) / float(min(a.nnz(), b.nnz()))
+
+
+def _union_count(tensors) -> int:
+    i, v = _to_dev(tensors[0])
+    for t in tensors[1:]:
+        if t.universe() != tensors[0].universe():
+            raise UniverseMismatch("tensors have different universe sizes")
+        i, v = _merge_dev(i, v, *_to_dev(t), t.universe())
+    return i.numel()
+
+
+def densification_ratio(tensors) -> float:
+    """zen::densification_ratio (tensor.hpp:178-189): density(aggregate) / mean density."""
+    if not tensors:
+        raise Error("densification ratio requires at least one tensor")
+    mean_d = 0.0
+    for t in tensors:
+        if t.empty():
+            raise EmptyTensor("densification ratio undefined with an empty tensor")
+        mean_d += density(t)
+    mean_d /= float(len(tensors))
+    return (float(_union_count(tensors)) / float(tensors[0].universe())) / mean_d
+
+
+def _range_counts_dev(i, m: int, partitions: int) -> np.ndarray:
+    out = (C.c_uint64 * partitions)()
+    ctx = context(i.device.index)
+    _check(_lib().zen_range_counts(ctx.h, _ptr(i), i.numel(), m, partitions, out))
+    return np.frombuffer(out, dtype=np.uint64).copy()
+
+
+def skewness_ratio(t: SparseTensor, partitions: int) -> float:
+    """zen::skewness_ratio (tensor.hpp:193-213): max density over ceil(M/n)
+    ranges / whole density; range counts from zen_range_counts."""
+    if partitions == 0:
+        raise Error("skewness ratio requires at least one partition")
+    if t.empty():
+        raise EmptyTensor("skewness ratio undefined for an empty tensor")
+    i, _ = _to_dev(t)
+    return _skew_from_counts(_range_counts_dev(i, t.universe(), partitions), t.universe(),
+                             partitions, t.nnz())
+
+
+def _skew_from_counts(counts, m: int, partitions: int, nnz: int) -> float:
+    rng = (m + partitions - 1) // partitions
+    best = 0.0
+    for p in range(partitions):
+        lo = p * rng
+        if lo >= m:
+            break
+        hi = min(m, lo + rng)
+        best = max(best, float(int(counts[p])) / float(hi - lo))
+    return best / (float(nnz) / float(m))
+
+
+@dataclass
+class SparsityProfile:
+    """zen::SparsityProfile (tensor.hpp:216-240)."""
+    d: float = 0.0
+    gamma: dict = field(default_factory=dict)
+    skew: dict = field(default_factory=dict)
+
+    def validate(self):
+        if not (0.0 < self.d <= 1.0):
+            raise Error("profile density must be in (0,1]")
+        if self.gamma.get(1) != 1.0:
+            raise Error("profile gamma[1] must equal 1")
+        prev = 0.0
+        for k in sorted(self.gamma):
+            g = self.gamma[k]
+            if g < prev - 1e-9:
+                raise Error("profile gamma must be non-decreasing in k")
+            if g > float(k) + 1e-9:
+                raise Error("profile gamma[k] must not exceed k")
+            if self.d * g > 1.0 + 1e-9:
+                raise Error("profile d*gamma[k] must not exceed 1")
+            prev = g
+        for s in self.skew.values():
+            if s < 1.0 - 1e-9:
+                raise Error("profile skew must be at least 1")
+
+    def to_json(self) -> dict:  # costmodel.hpp profile_to_json
+        return {"d": self.d, "gamma": {str(k): v for k, v in sorted(self.gamma.items())},
+                "skew": {str(k): v for k, v in sorted(self.skew.items())}}
+
+
+def profile_sparsity(rounds) -> SparsityProfile:
+    """zen::profile_sparsity (costmodel.hpp:153-195): mean density, the
+    densification ladder gamma[k] for power-of-two k, and the skew at n
+    partitions, averaged over rounds.  The prefix unions are device merges; the
+    double arithmetic follows the reference's order term for term."""
+    if not rounds:
+        raise Error("profiling requires at least one round")
+    n = len(rounds[0])
+    if n == 0:
+        raise Error("profiling requires at least one tensor per round")
+    gamma_sums: dict = {}
+    skew_sum = density_sum = 0.0
+    density_count = 0
+    for rnd in rounds:
+        if len(rnd) != n:
+            raise Error("profiling rounds must have matching node counts")
+        prefix_density_sum = 0.0
+        pi = pv = None
+        for i, t in enumerate(rnd):
+            if t.empty():
+                raise EmptyTensor("profiling requires non-empty tensors")
+            density_sum += density(t)
+            density_count += 1
+            ti, tv = _to_dev(t)
+            if i == 0:
+                pi, pv = ti, tv
+            else:
+                if t.universe() != rnd[0].universe():
+                    raise UniverseMismatch("tensors have different universe sizes")
+                pi, pv = _merge_dev(pi, pv, ti, tv, t.universe())
+            prefix_density_sum += density(t)
+            k = i + 1
+            if _pow2(k):
+                dp = float(pi.numel()) / float(t.universe())
+                gamma_sums[k] = gamma_sums.get(k, 0.0) + dp / (prefix_density_sum / float(k))
+            skew_sum += _skew_from_counts(_range_counts_dev(ti, t.universe(), n), t.universe(),
+                                          n, t.nnz())
+    prof = SparsityProfile()
+    prof.d = density_sum / float(density_count)
+    for k in sorted(gamma_sums):
+        prof.gamma[k] = gamma_sums[k] / float(len(rounds))
+    prof.gamma[1] = 1.0
+    prof.skew[n] = skew_sum / float(len(rounds) * n)
+    return prof
+
+
+# ------------------------------------------------------------ cost model ----
+
+@dataclass
+class CostInputs:
+    """zen::CostInputs (costmodel.hpp:15-27); element units (one fp32 = 1)."""
+    n: int = 1
+    universe: float = 0.0
+    d: float = 0.0
+    b: float = 1.0
+    gamma: dict = field(default_factory=dict)
+    skew: float = 1.0
+    broadcast_rounds: float = 1.0
+
+
+def _gamma_at(c: CostInputs, k: int) -> float:
+    if k == 1:
+        return 1.0
+    if k not in c.gamma:
+        raise MissingProfileEntry(f"densification ratio for k={k} missing from profile")
+    return c.gamma[k]
+
+
+def t_bp_coefficient(n: int, gamma_n: float) -> float:
+    """(n-1)/n * (gamma_n + 1), costmodel.hpp:53-58."""
+    if n <= 1:
+        return 0.0
+    return (float(n) - 1.0) / float(n) * (gamma_n + 1.0)
+
+
+def t_hc_coefficient(n: int, gamma: dict) -> float:
+    """sum over log n stages of gamma at 2^(i-1), costmodel.hpp:62-77."""
+    if not _pow2(n):
+        raise NonPowerOfTwo("hierarchy requires a power-of-two n")
+    s, k = 0.0, 1
+    while k < n:
+        if k == 1:
+            s += 1.0
+        else:
+            if k not in gamma:
+                raise MissingProfileEntry(f"densification ratio for k={k} missing from profile")
+            s += gamma[k]
+        k *= 2
+    return s
+
+
+def t_bp(c: CostInputs) -> float:
+    if c.n <= 1:
+        return 0.0
+    return t_bp_coefficient(c.n, _gamma_at(c, c.n)) * 2.0 * c.universe * c.d / c.b
+
+
+def t_hc(c: CostInputs) -> float:
+    return t_hc_coefficient(c.n, c.gamma) * 2.0 * c.universe * c.d / c.b
+
+
+def t_sparse_ps(c: CostInputs) -> float:
+    if c.n <= 1:
+        return 0.0
+    g = _gamma_at(c, c.n)
+    return 2.0 * (float(c.n) - 1.0) * (1.0 + g) * c.skew * c.d * c.universe / float(c.n) / c.b
+
+
+def t_sparse_ps_broadcast(c: CostInputs) -> float:
+    if c.n <= 1:
+        return 0.0
+    g = _gamma_at(c, c.n)
+    push = 2.0 * (float(c.n) - 1.0) * c.skew * c.d * c.universe / float(c.n) / c.b
+    return push + 2.0 * c.broadcast_rounds * g * c.d * c.universe / c.b
+
+
+def t_ring_incremental(c: CostInputs) -> float:
+    if c.n <= 1:
+        return 0.0
+    s = sum(_gamma_at(c, k) for k in range(1, c.n))
+    return 2.0 * s * c.d * c.universe / float(c.n) / c.b
+
+
+def t_hierarchy_incremental_lb(c: CostInputs) -> float:
+    if c.n <= 1:
+        return 0.0
+    return 2.0 * (float(c.n) - 1.0) * c.d * c.universe / float(c.n) / c.b
+
+
+def t_allreduce_dense(c: CostInputs) -> float:
+    if c.n <= 1:
+        return 0.0
+    return 2.0 * (float(c.n) - 1.0) / float(c.n) * c.universe / c.b
+
+
+BALANCED_PARALLELISM = "balanced-parallelism"
+HIERARCHICAL_CENTRALIZATION = "hierarchical-centralization"
+
+
+def select_scheme(profile: SparsityProfile, n: int) -> str:
+    """zen::select_scheme (costmodel.hpp:139-150): the cheaper optimum by
+    coefficient; ties go to Balanced Parallelism."""
+    if n not in profile.gamma:
+        raise MissingProfileEntry(f"densification ratio for k={n} missing from profile")
+    bp = t_bp_coefficient(n, profile.gamma[n])
+    hc = t_hc_coefficient(n, profile.gamma)
+    return BALANCED_PARALLELISM if bp <= hc else HIERARCHICAL_CENTRALIZATION
+
+
+# ------------------------------------------- Hierarchical Centralization ----
+
+def _sizes_dev(i, v, m: int, fmt: WireFormat):
+    """message_sizes (codec.hpp:182-211) of a device tensor: closed forms for
+    COO / Bitmap, the device encoder's size pass for TensorBlock."""
+    z = i.numel()
+    if fmt.kind == "coo":
+        return fmt.coo_index_bits * z, 32 * z
+    if fmt.kind == "bitmap":
+        return m, 32 * z
+    if fmt.kind == "hash_bitmap":
+        raise Error("hash bitmap requires a hash universe")
+    info = L.MessageInfoC()
+    f = fmt._c()
+    rc = _lib().zen_encode(context(i.device.index).h, C.byref(f), None, 0, _ptr(i), _ptr(v), z, m,
+                           None, 0, C.byref(info))
+    if rc not in (L.OK, L.E_CAPACITY):
+        _check(rc)
+    return int(info.index_bits), int(info.value_bits)
+
+
+class _Sized:
+    """An accounting-only EncodedMessage (schemes.hpp:78-88, sized_message)."""
+
+    def __init__(self, index_bits: int, value_bits: int):
+        self.index_bits, self.value_bits = index_bits, value_bits
+
+    def payload_bits(self) -> int:
+        return self.index_bits + self.value_bits
+
+
+def run_hier_centralization(inputs, net: SimNet, fmt: WireFormat | None = None) -> SyncOutcome:
+    """zen::run_hier_centralization (schemes.hpp:173-193) with all n nodes on
+    the current GPU.  Stage log2(bit): every node sends its state to w ^ bit
+    (ledger from the exact wire sizes), then states[w] = merge_sum(states[w],
+    states[w ^ bit]) on the device."""
+    fmt = fmt or WireFormat.coo()
+    _check_inputs(inputs, net)
+    n = len(inputs)
+    if not _pow2(n):
+        raise NonPowerOfTwo()
+    m = inputs[0].universe()
+    states = [_to_dev(t) for t in inputs]
+    bit = 1
+    while bit < n:
+        stage = bit.bit_length() - 1
+        for w in range(n):
+            net.send(stage, w, w ^ bit, _Sized(*_sizes_dev(*states[w], m, fmt)))
+        states = [_merge_dev(*states[w], *states[w ^ bit], m) for w in range(n)]
+        bit <<= 1
+    results = [_to_host(m, i, v) for i, v in states]
+    return SyncOutcome(results, net.finalize(), None)
+
+
+class HCSynchronizer:
+    """Hierarchical Centralization with one process per GPU (zen_hc_*): stage s
+    pushes this rank's running aggregate into rank ^ 2^s's CUDA-IPC arena as
+    NVLink stores and folds the received one with the merge-path merge_sum.
+    Counts stay on the device; sync_dense replays one CUDA graph.  Every rank
+    ends with aggregate(inputs), bit for bit."""
+
+    def __init__(self, n: int, universe: int, rank: int, max_nnz: int,
+                 fmt: WireFormat | None = None, device: int | None = None):
+        if not _pow2(n):
+            raise NonPowerOfTwo()
+        if fmt is not None and fmt.kind not in ("coo", "bitmap"):
+            raise Error("rank-mode hierarchy ledger supports COO and bitmap formats")
+        self.n, self.m, self.rank, self.max_nnz = n, universe, rank, max_nnz
+        self.fmt = fmt or WireFormat.coo()
+        self.ctx = context(device)
+        self.h = C.c_void_p()
+        _check(_lib().zen_hc_create(self.ctx.h, n, rank, universe, max_nnz, C.byref(self.h)))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                _lib().zen_hc_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_ubyte * L.ZEN_IPC_HANDLE_BYTES)()
+        _check(_lib().zen_hc_ipc_handle(self.h, buf))
+        return bytes(buf)
+
+    def connect(self, handles: list):
+        blob = b"".join(handles)
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _check(_lib().zen_hc_connect(self.h, buf))
+
+    def connect_process_group(self, group=None):
+        """Exchange CUDA IPC handles over torch.distributed (plumbing only)."""
+        import torch.distributed as dist
+        handles = [None] * self.n
+        dist.all_gather_object(handles, self.ipc_handle(), group=group)
+        self.connect(handles)
+
+    def sync_dense(self, dense):
+        """Asynchronous on the current stream: to_sparse + log2(n) stages."""
+        d = dense.contiguous().view(-1)
+        if d.numel() != self.m:
+            raise Error("dense gradient size differs from the universe")
+        self.ctx.bind_stream()
+        _check(_lib().zen_hc_sync_dense(self.h, _ptr(d)))
+
+    def sync_sparse(self, idx, val):
+        """idx (int64, sorted unique < M) / val (f32) on this rank's GPU."""
+        i, v = idx.contiguous(), val.contiguous()
+        self.ctx.bind_stream()
+        _check(_lib().zen_hc_sync_sparse(self.h, _ptr(i), _ptr(v), i.numel()))
+
+    def wait(self):
+        _check(_lib().zen_hc_wait(self.h))
+
+    def result(self):
+        """(int64 indices, f32 values) CUDA tensors of the aggregate, ascending."""
+        torch = _torch()
+        c = C.c_uint64()
+        _check(_lib().zen_hc_result(self.h, None, None, C.byref(c)))
+        z = c.value
+        dev = torch.device("cuda", self.ctx.device)
+        oi = torch.empty(max(z, 1), dtype=torch.int64, device=dev)
+        ov = torch.empty(max(z, 1), dtype=torch.float32, device=dev)
+        _check(_lib().zen_hc_copy_result(self.h, _ptr(oi), _ptr(ov), max(z, 1), C.byref(c)))
+        return oi[:z], ov[:z]
+
+    def stage_bits(self):
+        """[(index_bits, value_bits)] this rank sent per stage (the SimNet
+        ledger row of run_hier_centralization, schemes.hpp:183-185)."""
+        ns = self.n.bit_length() - 1
+        out = (C.c_uint64 * max(ns, 1))()
+        _check(_lib().zen_hc_stage_counts(self.h, out))
+        res = []
+        for s in range(ns):
+            z = int(out[s])
+            res.append((self.fmt.coo_index_bits * z, 32 * z) if self.fmt.kind == "coo"
+                       else (self.m, 32 * z))
+        return res
+

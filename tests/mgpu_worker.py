@@ -76,6 +76,30 @@ def main():
     if st.serial_writes != ref.serial_writes or st.placed_at_depth != ref.placed_at_depth:
         print(f"RANK {rank} collision stats mismatch", flush=True)
         ok = False
+    # Hierarchical Centralization (f3) over the same inputs: NVLink pushes into
+    # the partners' IPC arenas + merge-path merge_sum, graph-replayed
+    if world & (world - 1) == 0:
+        hc = zen.HCSynchronizer(world, m, rank, max_nnz=per * width + 1024)
+        hc.connect_process_group()
+        wi, wv, led = co.hier_centralization(m, [co.to_sparse(d) for d in dense])
+        for it in range(3):
+            hc.sync_dense(mine)
+            hi, hv = hc.result()
+            good = np.array_equal(hi.cpu().numpy().view(np.uint64), wi) and np.array_equal(
+                hv.cpu().numpy().view(np.uint32), wv.view(np.uint32))
+            sent = [ib + vb for ib, vb in hc.stage_bits()]
+            good = good and sent == [int(led[s, 0, rank]) for s in range(led.shape[0])]
+            if not good:
+                print(f"RANK {rank} HC iter {it} MISMATCH {hi.numel()} vs {wi.size}", flush=True)
+                ok = False
+        si, sv = co.to_sparse(dense[rank])
+        hc.sync_sparse(torch.from_numpy(si.view(np.int64)).cuda(), torch.from_numpy(sv).cuda())
+        hi, hv = hc.result()
+        if not (np.array_equal(hi.cpu().numpy().view(np.uint64), wi)
+                and np.array_equal(hv.cpu().numpy().view(np.uint32), wv.view(np.uint32))):
+            print(f"RANK {rank} HC sparse MISMATCH", flush=True)
+            ok = False
+        del hc
     flag = torch.tensor([0 if ok else 1], device="cuda" if world <= ngpu else "cpu")
     dist.all_reduce(flag)
     if rank == 0:

@@ -230,3 +230,67 @@ def test_sparsify_topk_golden(co):
                 continue
             i, v = co.sparsify_topk(d, float(f))
             assert np.array_equal(i, g[key]) and np.array_equal(v, g[f"{name}_{f}_val"]), (name, f)
+
+
+# ---- f3: Hierarchical Centralization, merge_sum, metrics, profile / selector ----
+
+KIND_NAMES = {1: "coo", 2: "bitmap", 3: "tensor_block"}
+
+
+def hc_case(g, c):
+    m, n = (int(x) for x in g[f"c{c}_m"])
+    ins = [(g[f"c{c}_in{w}_idx"], g[f"c{c}_in{w}_val"]) for w in range(n)]
+    return m, n, ins
+
+
+def test_hier_centralization_golden(co):
+    """The restatement of run_hier_centralization + its SimNet ledger against
+    the reference's outputs, every sized wire format."""
+    g = load_golden("hc")
+    for c in range(int(g["ncases"][0])):
+        m, n, ins = hc_case(g, c)
+        for f, (k, bs, cb) in enumerate(g["formats"]):
+            i, v, led = co.hier_centralization(m, ins, KIND_NAMES[int(k)], int(bs), int(cb))
+            np.testing.assert_array_equal(i, g[f"c{c}_f{f}_idx"], err_msg=f"case {c} fmt {f}")
+            np.testing.assert_array_equal(v.view(np.uint32), g[f"c{c}_f{f}_val"].view(np.uint32))
+            np.testing.assert_array_equal(led, g[f"c{c}_f{f}_ledger"])
+        i, v = co.merge_sum(*ins[0], *ins[1])
+        np.testing.assert_array_equal(i, g[f"c{c}_merge_idx"])
+        np.testing.assert_array_equal(v.view(np.uint32), g[f"c{c}_merge_val"].view(np.uint32))
+
+
+def test_profile_and_selector_golden(co):
+    g = load_golden("hc")
+    seen = 0
+    for c in range(int(g["ncases"][0])):
+        if f"c{c}_profile" not in g:
+            continue
+        m, n, ins = hc_case(g, c)
+        d, gamma, skew, choice = co.profile(m, [ins, list(reversed(ins))])
+        want = g[f"c{c}_profile"]
+        assert (d, skew, choice) == (want[0], want[1], int(want[2]))
+        for j in range(5):
+            assert gamma.get(1 << j, np.nan) == want[3 + j] or np.isnan(want[3 + j])
+        assert co.skewness(m, ins[0][0], n) == g[f"c{c}_metrics"][2]
+        seen += 1
+    assert seen >= 5
+
+
+def test_hier_centralization_rejects_non_power_of_two(co):
+    ins = [(np.array([w], np.uint64), np.ones(1, np.float32)) for w in range(6)]
+    with pytest.raises(OracleError):
+        co.hier_centralization(100, ins)
+
+
+def test_hier_centralization_restatement_vs_reference(co, ro):
+    rng = np.random.default_rng(17)
+    for trial in range(12):
+        n = 1 << int(rng.integers(1, 4))
+        ins = ro.generate(2000, n, 0.01 + 0.01 * int(rng.integers(0, 5)),
+                          0.25 * int(rng.integers(0, 4)), int(rng.integers(1, 1 << 30)))
+        for kind in ["coo", "bitmap", "tensor_block"]:
+            a = co.hier_centralization(2000, ins, kind, 32)
+            b = ro.hier_centralization(2000, ins, kind, 32)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
+            assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
+        assert co.profile(2000, [ins]) == ro.profile(2000, [ins])
