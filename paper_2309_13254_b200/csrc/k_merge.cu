@@ -47,6 +47,34 @@ __device__ __forceinline__ uint64_t merge_split(const KA& A, uint64_t na, const 
   return lo;
 }
 
+// the same split found by one warp: 32 probes per round trip (a 33-ary
+// search) instead of one, so a split over millions of entries costs ~5
+// dependent loads.  All lanes call; all get the result.  Always returns a
+// value in the search range, even for unsorted input.
+template <typename KA, typename KB>
+__device__ __forceinline__ uint64_t merge_split_warp(const KA& A, uint64_t na, const KB& B,
+                                                     uint64_t nb, uint64_t d) {
+  const uint32_t lane = lane_id();
+  uint64_t lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+  while (hi > lo) {
+    const uint64_t span = hi - lo;
+    if (span <= 32) {
+      bool p = false;
+      if (lane < span) {
+        const uint64_t i = lo + lane;
+        p = A[i] <= B[d - 1 - i];
+      }
+      return lo + __popc(__ballot_sync(0xffffffffu, p));
+    }
+    const uint64_t i = lo + span * (lane + 1) / 33;  // strictly increasing in [lo, hi)
+    const uint32_t k = __popc(__ballot_sync(0xffffffffu, A[i] <= B[d - 1 - i]));
+    const uint64_t nlo = k ? lo + span * k / 33 + 1 : lo;
+    hi = k < 32 ? lo + span * (k + 1) / 33 : hi;
+    lo = nlo;
+  }
+  return lo;
+}
+
 struct SmemArr {  // indexable view of a shared-memory slice
   const uint64_t* p;
   __device__ __forceinline__ uint64_t operator[](uint64_t i) const { return p[i]; }
@@ -78,8 +106,10 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_merge(HcMergeArgs a) {
   if (tile == 0 && tid == 0 && a.stage_cnt) *a.stage_cnt = na;
 
   // ---- tile split + staging ----
-  if (live && (tid == 0 || tid == 32))
-    s_split[tid >> 5] = merge_split(a.a_idx, na, a.b_idx, nb, tid == 0 ? lo : hi);
+  if (live && tid < 64) {
+    const uint64_t sp = merge_split_warp(a.a_idx, na, a.b_idx, nb, tid < 32 ? lo : hi);
+    if ((tid & 31) == 0) s_split[tid >> 5] = sp;
+  }
   __syncthreads();
   uint64_t a0 = live ? s_split[0] : 0, a1 = live ? s_split[1] : 0;
   uint64_t b0 = lo - a0, b1 = hi - a1;
@@ -237,13 +267,30 @@ __global__ void __launch_bounds__(256) k_hc_push(HcPushArgs a) {
   }
   const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + tid, stride = uint64_t(gridDim.x) * blockDim.x;
   // buffers are 256-byte aligned: 16-byte vectors, then the tails
+  // four independent 16-byte loads in flight per thread, then their stores
   const uint64_t n2 = n >> 1, n4 = n >> 2;
   const ulonglong2* si = reinterpret_cast<const ulonglong2*>(a.src_idx);
   ulonglong2* di = reinterpret_cast<ulonglong2*>(a.dst_idx);
-  for (uint64_t x = g; x < n2; x += stride) di[x] = si[x];
+  for (uint64_t x = g; x < n2; x += 4 * stride) {
+    ulonglong2 t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (x + u * stride < n2) t[u] = si[x + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (x + u * stride < n2) di[x + u * stride] = t[u];
+  }
   const float4* sv = reinterpret_cast<const float4*>(a.src_val);
   float4* dv = reinterpret_cast<float4*>(a.dst_val);
-  for (uint64_t x = g; x < n4; x += stride) dv[x] = sv[x];
+  for (uint64_t x = g; x < n4; x += 4 * stride) {
+    float4 t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (x + u * stride < n4) t[u] = sv[x + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (x + u * stride < n4) dv[x + u * stride] = t[u];
+  }
   if (blockIdx.x == 0) {
     if (tid == 0 && (n & 1)) a.dst_idx[n - 1] = a.src_idx[n - 1];
     if (tid < (n & 3)) a.dst_val[(n4 << 2) + tid] = a.src_val[(n4 << 2) + tid];

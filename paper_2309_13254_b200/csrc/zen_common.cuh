@@ -201,18 +201,19 @@ __device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned l
 
 // Called by every thread of warp 0 of the tile's block after the block knows
 // its aggregate; returns the exclusive prefix of the tile (same on all lanes).
+// The flag and the value share one 64-bit word and nothing else is published
+// with them, so the stores need no fence (a fence.sc here costs microseconds
+// per tile).
 __device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, uint32_t tile,
                                                   uint32_t tag, uint64_t aggregate) {
   const uint32_t lane = lane_id();
   if (tile == 0) {
     if (lane == 0) {
-      __threadfence();
       st_relaxed_gpu(status, lb_pack(tag, LB_FLAG_PRE, aggregate));
     }
     return 0;
   }
   if (lane == 0) {
-    __threadfence();
     st_relaxed_gpu(status + tile, lb_pack(tag, LB_FLAG_AGG, aggregate));
   }
   uint64_t exclusive = 0;
@@ -222,10 +223,12 @@ __device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, ui
     const int64_t t = base - (int64_t)lane;
     uint64_t w = 0, flag = 0, val = 0;
     if (t >= 0) {
-      do {
+      while (true) {
         w = ld_relaxed_gpu(status + t);
         flag = ((w >> 40) == tagbits) ? ((w >> 38) & 3ull) : 0ull;
-      } while (flag == 0);
+        if (flag) break;
+        __nanosleep(32);
+      }
       val = w & LB_VAL_MASK;
     } else {
       flag = LB_FLAG_PRE;  // virtual predecessor of tile 0
@@ -243,7 +246,6 @@ __device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, ui
     base -= 32;
   }
   if (lane == 0) {
-    __threadfence();
     st_relaxed_gpu(status + tile, lb_pack(tag, LB_FLAG_PRE, exclusive + aggregate));
   }
   return exclusive;

@@ -49,17 +49,26 @@ def main():
     stream = torch.cuda.current_stream()
     out = {"config": f"{rows}x{width}, {args.density:.1%} rows, omega {args.omega}", "n_gpus": world}
 
-    def timed(fn):
+    def timed(fn, after=None):
+        """device time of fn's enqueue (events on the stream), then `after`
+        (the host-side wait / error check) outside the timed region"""
         for _ in range(3):
             fn()
+            if after:
+                after()
         torch.cuda.synchronize()
         ts = []
         for _ in range(args.steps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
             a.record(stream)
             fn()
             b.record(stream)
             b.synchronize()
+            if after:
+                after()
             ts.append(a.elapsed_time(b))
         t = float(np.median(ts))
         if world > 1:
@@ -72,18 +81,12 @@ def main():
         bp = zen.BPSynchronizer(world, m, max_nnz=per * width + 4096, rank=rank)
         bp.connect_process_group()
 
-        def bp_step():
-            bp.sync_dense([mine])
-            bp.wait()
-        out["bp_ms"] = timed(bp_step)
+        out["bp_ms"] = timed(lambda: bp.sync_dense([mine]), bp.wait)
         if world & (world - 1) == 0:
             hc = zen.HCSynchronizer(world, m, rank, max_nnz=per * width + 4096)
             hc.connect_process_group()
 
-            def hc_step():
-                hc.sync_dense(mine)
-                hc.wait()
-            out["hc_ms"] = timed(hc_step)
+            out["hc_ms"] = timed(lambda: hc.sync_dense(mine), hc.wait)
             hi, hv = hc.result()
             bi, bv = bp.result()
             out["hc_equals_bp"] = bool(torch.equal(hi, bi) and torch.equal(hv.view(torch.int32),

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--density", type=float, default=0.01)
     ap.add_argument("--syncs", type=int, default=3)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--scheme", default="bp", choices=["bp", "hc"],
+                    help="hc: Hierarchical Centralization (rank mode, torchrun)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -48,20 +50,31 @@ def main():
           for w in mine]
     m = args.rows * args.width
     z = per * args.width
-    bp = zen.BPSynchronizer(n, m, max_nnz=int(z * 1.25) + 4096, params=zen.HashParams(seed=1),
-                            rank=rank if dist else None)
-    if dist:
-        bp.connect_process_group()
+    if args.scheme == "hc":
+        hc = zen.HCSynchronizer(n, m, rank, max_nnz=int(z * 1.25) + 4096)
+        hc.connect_process_group() if dist else hc.connect([hc.ipc_handle()])
+
+        def run():
+            hc.sync_dense(dd[0])
+        first, last = "k_hc_begin", None
+    else:
+        bp = zen.BPSynchronizer(n, m, max_nnz=int(z * 1.25) + 4096, params=zen.HashParams(seed=1),
+                                rank=rank if dist else None)
+        if dist:
+            bp.connect_process_group()
+
+        def run():
+            bp.sync_dense(dd)
+        first, last = "k_extract_tiles", "k_decode"
     for _ in range(10):
-        bp.sync_dense(dd)
-    bp.wait()
+        run()
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
     if dist:
         dist.barrier()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(args.syncs):
-            bp.sync_dense(dd)
+            run()
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -75,7 +88,7 @@ def main():
     # split into syncs at each extraction kernel
     syncs, cur = [], []
     for e in ks:
-        if "k_extract_tiles" in e["name"] and cur and any("k_decode" in x["name"] for x in cur):
+        if first in e["name"] and cur and (last is None or any(last in x["name"] for x in cur)):
             syncs.append(cur)
             cur = []
         cur.append(e)
