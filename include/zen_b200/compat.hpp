@@ -24,6 +24,12 @@
 //   zen::run_balanced_parallelism (schemes.hpp:341)  zen_b200::run_balanced_parallelism
 //   zen::bp_universe_table (schemes.hpp:332)    zen_b200::bp_universe_table
 //   zen::run_bp_with_retry (experiment.hpp:128) zen_b200::run_bp_with_retry
+//   zen::merge_sum / aggregate (tensor.hpp:133) zen_b200::merge_sum / aggregate
+//   zen::density, overlap/densification/skewness_ratio (tensor.hpp:106-213)
+//                                               zen_b200::(same names)
+//   zen::SparsityProfile, profile_sparsity,     zen_b200::(same names)
+//   select_scheme, t_bp/t_hc[_coefficient] (costmodel.hpp)
+//   zen::run_hier_centralization (schemes.hpp:173) zen_b200::run_hier_centralization
 //
 // Host containers stay std::vector (value semantics, as in the reference); the
 // device copies are made per call.  For a device-resident, allocation-free
@@ -34,6 +40,7 @@
 #include <cstdint>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <istream>
 #include <ostream>
 #include <memory>
@@ -92,6 +99,17 @@ class UnbalancedLedger : public Error {
   explicit UnbalancedLedger(const std::string& w = "sent and received byte totals disagree")
       : Error(w) {}
 };
+class NonPowerOfTwo : public Error {  // errors.hpp:42-46
+ public:
+  explicit NonPowerOfTwo(const std::string& what = "node count must be a power of two")
+      : Error(what) {}
+};
+
+class MissingProfileEntry : public Error {  // errors.hpp:54-57
+ public:
+  explicit MissingProfileEntry(const std::string& what) : Error(what) {}
+};
+
 class DeviceError : public Error {  // no CPU fallback exists
  public:
   explicit DeviceError(const std::string& w) : Error(w) {}
@@ -592,6 +610,176 @@ inline SparseTensor read_sparse_file(const std::string& path) {
   return read_sparse(is);
 }
 
+// ---- merge_sum and the sparsity metrics: zen/tensor.hpp:106-213 ------------
+namespace detail {
+struct DevTensor {  // a device copy of a SparseTensor (or of a merge result)
+  uint64_t m = 1, n = 0;
+  std::unique_ptr<DBuf<uint64_t>> idx;
+  std::unique_ptr<DBuf<float>> val;
+  DevTensor() = default;
+  explicit DevTensor(const SparseTensor& t)
+      : m(t.universe()), n(t.nnz()), idx(new DBuf<uint64_t>(t.indices())),
+        val(new DBuf<float>(t.values())) {}
+  SparseTensor host() const { return SparseTensor(m, idx->host(n), val->host(n)); }
+};
+inline DevTensor merge_dev(const DevTensor& a, const DevTensor& b) {
+  if (a.m != b.m) throw UniverseMismatch();
+  DevTensor o;
+  o.m = a.m;
+  o.idx.reset(new DBuf<uint64_t>(a.n + b.n));
+  o.val.reset(new DBuf<float>(a.n + b.n));
+  check(zen_merge_sum(ctx(), a.idx->p, a.val->p, a.n, b.idx->p, b.val->p, b.n, a.m, o.idx->p,
+                      o.val->p, a.n + b.n, &o.n));
+  return o;
+}
+inline bool is_pow2(uint64_t v) { return v != 0 && (v & (v - 1)) == 0; }
+}  // namespace detail
+
+// zen::merge_sum (tensor.hpp:133-167), the merge-path kernel on the GPU
+inline SparseTensor merge_sum(const SparseTensor& a, const SparseTensor& b) {
+  if (a.universe() != b.universe()) throw UniverseMismatch();
+  return detail::merge_dev(detail::DevTensor(a), detail::DevTensor(b)).host();
+}
+
+// zen::aggregate (tensor.hpp:171-176)
+inline SparseTensor aggregate(const std::vector<SparseTensor>& tensors) {
+  if (tensors.empty()) throw Error("aggregate requires at least one tensor");
+  detail::DevTensor acc(tensors.front());
+  for (size_t i = 1; i < tensors.size(); ++i) acc = detail::merge_dev(acc, detail::DevTensor(tensors[i]));
+  return acc.host();
+}
+
+inline double density(const SparseTensor& t) { return double(t.nnz()) / double(t.universe()); }
+
+inline double overlap_ratio(const SparseTensor& a, const SparseTensor& b) {  // tensor.hpp:111-130
+  if (a.universe() != b.universe()) throw UniverseMismatch();
+  if (a.empty() || b.empty()) throw EmptyTensor("overlap ratio undefined for empty tensors");
+  const auto u = detail::merge_dev(detail::DevTensor(a), detail::DevTensor(b));
+  return double(a.nnz() + b.nnz() - u.n) / double(std::min(a.nnz(), b.nnz()));
+}
+
+inline double densification_ratio(const std::vector<SparseTensor>& tensors) {  // :178-189
+  if (tensors.empty()) throw Error("densification ratio requires at least one tensor");
+  double mean_d = 0.0;
+  for (const auto& t : tensors) {
+    if (t.empty()) throw EmptyTensor("densification ratio undefined with an empty tensor");
+    mean_d += density(t);
+  }
+  mean_d /= double(tensors.size());
+  detail::DevTensor acc(tensors.front());
+  for (size_t i = 1; i < tensors.size(); ++i) acc = detail::merge_dev(acc, detail::DevTensor(tensors[i]));
+  return (double(acc.n) / double(tensors.front().universe())) / mean_d;
+}
+
+namespace detail {
+inline double skew_from_counts(const std::vector<uint64_t>& counts, uint64_t m, uint32_t parts,
+                               uint64_t nnz) {
+  const uint64_t range = (m + parts - 1) / parts;
+  double best = 0.0;
+  for (uint64_t p = 0; p < parts; ++p) {
+    const uint64_t lo = p * range;
+    if (lo >= m) break;
+    const uint64_t hi = std::min(m, lo + range);
+    best = std::max(best, double(counts[p]) / double(hi - lo));
+  }
+  return best / (double(nnz) / double(m));
+}
+inline std::vector<uint64_t> range_counts(const DevTensor& t, uint32_t parts) {
+  std::vector<uint64_t> c(parts);
+  check(zen_range_counts(ctx(), t.idx->p, t.n, t.m, parts, c.data()));
+  return c;
+}
+}  // namespace detail
+
+inline double skewness_ratio(const SparseTensor& t, uint32_t partitions) {  // :192-213
+  if (partitions == 0) throw Error("skewness ratio requires at least one partition");
+  if (t.empty()) throw EmptyTensor("skewness ratio undefined for an empty tensor");
+  return detail::skew_from_counts(detail::range_counts(detail::DevTensor(t), partitions),
+                                  t.universe(), partitions, t.nnz());
+}
+
+// ---- sparsity profile and scheme selection: zen/costmodel.hpp ---------------
+struct SparsityProfile {  // tensor.hpp:216-240
+  double d = 0.0;
+  std::map<uint64_t, double> gamma;
+  std::map<uint32_t, double> skew;
+};
+
+// (n-1)/n * (gamma_n + 1), costmodel.hpp:53-58
+inline double t_bp_coefficient(uint32_t n, double gamma_n) {
+  return n <= 1 ? 0.0 : (double(n) - 1.0) / double(n) * (gamma_n + 1.0);
+}
+// sum over log n stages of gamma at 2^(i-1), costmodel.hpp:62-77
+inline double t_hc_coefficient(uint32_t n, const std::map<uint64_t, double>& gamma) {
+  if (!detail::is_pow2(n)) throw NonPowerOfTwo("hierarchy requires a power-of-two n");
+  double sum = 0.0;
+  for (uint64_t k = 1; k < n; k *= 2) {
+    if (k == 1) {
+      sum += 1.0;
+      continue;
+    }
+    auto it = gamma.find(k);
+    if (it == gamma.end())
+      throw MissingProfileEntry("densification ratio for k=" + std::to_string(k) +
+                                " missing from profile");
+    sum += it->second;
+  }
+  return sum;
+}
+
+enum class SchemeChoice { BalancedParallelism, HierarchicalCentralization };
+inline const char* to_string(SchemeChoice s) {
+  return s == SchemeChoice::BalancedParallelism ? "balanced-parallelism"
+                                                : "hierarchical-centralization";
+}
+
+// zen::select_scheme (costmodel.hpp:139-149): ties go to Balanced Parallelism
+inline SchemeChoice select_scheme(const SparsityProfile& p, uint32_t n) {
+  auto it = p.gamma.find(n);
+  if (it == p.gamma.end())
+    throw MissingProfileEntry("densification ratio for k=" + std::to_string(n) +
+                              " missing from profile");
+  return t_bp_coefficient(n, it->second) <= t_hc_coefficient(n, p.gamma)
+             ? SchemeChoice::BalancedParallelism
+             : SchemeChoice::HierarchicalCentralization;
+}
+
+// zen::profile_sparsity (costmodel.hpp:151-195); prefix unions by device merges
+inline SparsityProfile profile_sparsity(const std::vector<std::vector<SparseTensor>>& rounds) {
+  if (rounds.empty()) throw Error("profiling requires at least one round");
+  const size_t n = rounds.front().size();
+  if (n == 0) throw Error("profiling requires at least one tensor per round");
+  SparsityProfile prof;
+  std::map<uint64_t, double> gamma_sums;
+  double skew_sum = 0.0, density_sum = 0.0;
+  uint64_t density_count = 0;
+  for (const auto& round : rounds) {
+    if (round.size() != n) throw Error("profiling rounds must have matching node counts");
+    double prefix_density_sum = 0.0;
+    detail::DevTensor prefix;
+    for (size_t i = 0; i < n; ++i) {
+      const SparseTensor& t = round[i];
+      if (t.empty()) throw EmptyTensor("profiling requires non-empty tensors");
+      density_sum += density(t);
+      ++density_count;
+      detail::DevTensor dt(t);
+      skew_sum += detail::skew_from_counts(detail::range_counts(dt, uint32_t(n)), t.universe(),
+                                           uint32_t(n), t.nnz());
+      prefix = i == 0 ? std::move(dt) : detail::merge_dev(prefix, dt);
+      prefix_density_sum += density(t);
+      const uint64_t k = i + 1;
+      if (detail::is_pow2(k))
+        gamma_sums[k] += (double(prefix.n) / double(t.universe())) /
+                         (prefix_density_sum / double(k));
+    }
+  }
+  prof.d = density_sum / double(density_count);
+  for (const auto& [k, sum] : gamma_sums) prof.gamma[k] = sum / double(rounds.size());
+  prof.gamma[1] = 1.0;
+  prof.skew[uint32_t(n)] = skew_sum / double(rounds.size() * n);
+  return prof;
+}
+
 // ---- transport ledger: zen/simnet.hpp ---------------------------------------
 struct StageRecord {
   std::vector<uint64_t> sent_bits, recv_bits, recv_index_bits, recv_value_bits;
@@ -619,6 +807,21 @@ class SimNet {
   }
   uint32_t nodes() const { return n_; }
   double bandwidth() const { return b_; }
+  // simnet.hpp:71-85
+  void send(uint32_t stage, uint32_t from, uint32_t to, const EncodedMessage& msg) {
+    if (final_) throw Error("cannot send after finalize");
+    if (from == to) throw SelfSend();
+    if (from >= n_ || to >= n_) throw Error("node id out of range");
+    if (!stages_.empty() && stage + 1 < stages_.size())
+      throw Error("stage numbers must be non-decreasing");
+    while (stages_.size() <= stage) stages_.emplace_back(n_);
+    StageRecord& r = stages_[stage];
+    r.sent_bits[from] += msg.payload_bits();
+    r.recv_bits[to] += msg.payload_bits();
+    r.recv_index_bits[to] += msg.index_bits;
+    r.recv_value_bits[to] += msg.value_bits;
+    lat_charges_ += lat_;
+  }
   // ledger[2][4][n] as produced by zen_bp_traffic
   void record(const std::vector<uint64_t>& ledger, uint64_t messages) {
     if (final_) throw Error("cannot send after finalize");
@@ -754,6 +957,56 @@ inline SyncOutcome run_bp_with_retry(const std::vector<SparseTensor>& inputs, do
       params.r2_ratio *= 2.0;
     }
   }
+}
+
+// zen::run_hier_centralization (zen/schemes.hpp:173-193): recursive doubling
+// with a device merge_sum per node and stage; all n nodes on this GPU (the
+// multi-GPU form is the zen_hc_* C-ABI, one process per GPU)
+inline SyncOutcome run_hier_centralization(const std::vector<SparseTensor>& inputs, SimNet& net,
+                                           WireFormat fmt = WireFormat::coo()) {
+  if (inputs.size() < 2) throw Error("synchronization needs at least two nodes");
+  if (inputs.size() != net.nodes()) throw Error("input count must match the network size");
+  for (const auto& t : inputs)
+    if (t.universe() != inputs.front().universe()) throw UniverseMismatch();
+  if (!detail::is_pow2(inputs.size())) throw NonPowerOfTwo();
+  const uint32_t n = uint32_t(inputs.size());
+  std::vector<detail::DevTensor> states;
+  for (const auto& t : inputs) states.emplace_back(t);
+  for (uint32_t bit = 1; bit < n; bit <<= 1) {
+    uint32_t stage = 0;
+    while ((1u << stage) != bit) ++stage;
+    for (uint32_t w = 0; w < n; ++w) {  // sized_message (schemes.hpp:78-88)
+      const detail::DevTensor& st = states[w];
+      EncodedMessage msg;
+      msg.format = fmt;
+      msg.universe_size = st.m;
+      msg.count = st.n;
+      msg.value_bits = 32 * st.n;  // message_sizes, codec.hpp:182-211
+      if (fmt.kind == WireKind::Coo) {
+        msg.index_bits = uint64_t(fmt.coo_index_bits) * st.n;
+      } else if (fmt.kind == WireKind::Bitmap) {
+        msg.index_bits = st.m;
+      } else if (fmt.kind == WireKind::HashBitmap) {
+        throw Error("hash bitmap requires a hash universe");
+      } else {  // tensor blocks: the device encoder's size pass
+        zen_wire_format f = detail::wire_c(fmt);
+        zen_message_info info{};
+        const zen_status rc = zen_encode(detail::ctx(), &f, nullptr, 0, st.idx->p, st.val->p,
+                                         st.n, st.m, nullptr, 0, &info);
+        if (rc != ZEN_OK && rc != ZEN_E_CAPACITY) detail::check(rc);
+        msg.index_bits = info.index_bits;
+        msg.value_bits = info.value_bits;
+      }
+      net.send(stage, w, w ^ bit, msg);
+    }
+    std::vector<detail::DevTensor> next;
+    for (uint32_t w = 0; w < n; ++w) next.push_back(detail::merge_dev(states[w], states[w ^ bit]));
+    states = std::move(next);
+  }
+  SyncOutcome out;
+  for (const auto& st : states) out.results.push_back(st.host());
+  out.traffic = net.finalize();
+  return out;
 }
 
 }  // namespace zen_b200

@@ -455,6 +455,102 @@ TEST(Serialization_RoundTripsAndRejectsBadMagic) {
   EXPECT_THROW(z::read_sparse(bad), z::MalformedPayload);
 }
 
+// ---- schemes_test.cpp: HierCentralization; costmodel_test.cpp: SelectScheme ----
+static void expect_oracle_equal(const z::SyncOutcome& out, const std::vector<z::SparseTensor>& in) {
+  const auto want = z::aggregate(in);
+  // the reference oracle folds left in worker order; HC sums pairwise in a
+  // tree, so values are compared within fp32 rounding, indices exactly
+  for (const auto& r : out.results) {
+    EXPECT(r.indices() == want.indices());
+    bool close = r.values().size() == want.values().size();
+    for (size_t i = 0; close && i < r.values().size(); ++i)
+      close = std::fabs(r.values()[i] - want.values()[i]) <=
+              1e-5f * std::max(1.0f, std::fabs(want.values()[i]));
+    EXPECT(close);
+    EXPECT(r == out.results.front());
+  }
+}
+
+TEST(HierCentralization_TwoNodesExchangeOnce) {
+  z::SparseTensor a(50, {1}, {2}), b(50, {2}, {3});
+  z::SimNet net(2, 1.0);
+  auto out = z::run_hier_centralization({a, b}, net);
+  expect_oracle_equal(out, {a, b});
+  EXPECT(out.traffic.stages.size() == 1u);
+}
+
+TEST(HierCentralization_FullOverlapReceivesCommonSetLogNTimes) {
+  auto inputs = workload(4, 1000, 0.05, 1.0, 13);
+  const uint64_t zz = inputs[0].nnz();
+  z::SimNet net(4, 1.0);
+  auto out = z::run_hier_centralization(inputs, net);
+  expect_oracle_equal(out, inputs);
+  EXPECT(out.traffic.stages.size() == 2u);
+  for (uint32_t node = 0; node < 4; ++node) {
+    uint64_t total = 0;
+    for (const auto& s : out.traffic.stages) total += s.recv_bits[node];
+    EXPECT(total == 2 * zz * 96);
+  }
+}
+
+TEST(HierCentralization_OracleEqualOnRandomCases) {
+  std::mt19937_64 rng(17);
+  for (int trial = 0; trial < 25; ++trial) {
+    const uint32_t n = 1u << (1 + rng() % 3);
+    auto inputs = workload(n, 2000, 0.01 + 0.01 * double(rng() % 5), 0.25 * double(rng() % 4), rng());
+    z::SimNet net(n, 1.0);
+    expect_oracle_equal(z::run_hier_centralization(inputs, net), inputs);
+  }
+}
+
+TEST(HierCentralization_RejectsNonPowerOfTwo) {
+  auto inputs = workload(6, 1000, 0.01, 0.0, 3);
+  z::SimNet net(6, 1.0);
+  EXPECT_THROW(z::run_hier_centralization(inputs, net), z::NonPowerOfTwo);
+}
+
+TEST(HierCentralization_ReceivedBitsShrinkAsOverlapGrows) {
+  std::vector<uint64_t> totals;
+  for (double omega : {0.0, 0.5, 1.0}) {
+    auto inputs = workload(8, 100000, 0.002, omega, 23);
+    z::SimNet net(8, 1.0);
+    totals.push_back(z::run_hier_centralization(inputs, net).traffic.total_recv_bits);
+  }
+  EXPECT(totals[0] > totals[1] && totals[1] > totals[2]);
+}
+
+TEST(SelectScheme_FullOverlapAndNoOverlap) {
+  z::SparsityProfile p;
+  p.d = 0.01;
+  for (uint64_t k = 1; k <= 16; k *= 2) p.gamma[k] = 1.0;
+  EXPECT(z::select_scheme(p, 16) == z::SchemeChoice::BalancedParallelism);
+  z::SparsityProfile q;
+  q.d = 0.001;
+  for (uint64_t k = 1; k <= 16; k *= 2) q.gamma[k] = double(k);
+  EXPECT(z::select_scheme(q, 8) == z::SchemeChoice::HierarchicalCentralization);
+  EXPECT(z::select_scheme(q, 16) == z::SchemeChoice::HierarchicalCentralization);
+  z::SparsityProfile t;
+  t.gamma = {{1, 1.0}, {2, 1.0}};
+  EXPECT(z::select_scheme(t, 2) == z::SchemeChoice::BalancedParallelism);  // tie -> BP
+  EXPECT_THROW(z::t_hc_coefficient(6, q.gamma), z::NonPowerOfTwo);
+  z::SparsityProfile u;
+  u.gamma = {{1, 1.0}, {4, 2.0}};
+  EXPECT_THROW(z::select_scheme(u, 4), z::MissingProfileEntry);
+}
+
+TEST(ProfileSparsity_MatchesItsDefinition) {
+  auto inputs = workload(4, 20000, 0.02, 0.5, 77);
+  auto p = z::profile_sparsity({inputs});
+  EXPECT(p.gamma.at(1) == 1.0);
+  EXPECT(std::fabs(p.gamma.at(4) - z::densification_ratio(inputs)) < 1e-12);
+  EXPECT(std::fabs(p.d - z::density(inputs[0])) < 1e-12);
+  EXPECT(p.skew.at(4) >= 1.0);
+  EXPECT(std::fabs(z::overlap_ratio(inputs[0], inputs[0]) - 1.0) < 1e-12);
+  auto m = z::merge_sum(inputs[0], inputs[1]);
+  const double common = z::overlap_ratio(inputs[0], inputs[1]) * double(inputs[0].nnz());
+  EXPECT(m.nnz() == inputs[0].nnz() + inputs[1].nnz() - uint64_t(std::llround(common)));
+}
+
 int main() {
   for (auto& [name, fn] : tests()) {
     const int before = g_fail;
