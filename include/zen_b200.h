@@ -213,6 +213,15 @@ zen_status zen_merge_sum(zen_ctx* ctx, const uint64_t* a_idx, const float* a_val
 zen_status zen_range_counts(zen_ctx* ctx, const uint64_t* d_idx, uint64_t count,
                             uint64_t universe, uint32_t partitions, uint64_t* h_counts);
 
+/* ---- OmniReduce-like block framing: zen/schemes.hpp:227-295 ------------ */
+/* non-zero blocks of block_size positions counted from `origin` (sorted input) */
+zen_status zen_count_blocks(zen_ctx* ctx, const uint64_t* d_idx, uint64_t count, uint64_t origin,
+                            uint64_t block_size, uint64_t* blocks);
+/* drop entries whose value is exactly zero, order kept (the block decode) */
+zen_status zen_compact_nonzero(zen_ctx* ctx, const uint64_t* d_idx, const float* d_val,
+                               uint64_t count, uint64_t* d_out_idx, float* d_out_val,
+                               uint64_t* out_count);
+
 /* ---- Hierarchical Centralization: zen/schemes.hpp:173-193 -------------- */
 /* One process per GPU, n a power of two (zen::NonPowerOfTwo otherwise:
  * ZEN_E_INVALID).  Stage s (s < log2 n) sends this rank's running aggregate to

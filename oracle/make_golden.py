@@ -337,12 +337,54 @@ def hc_cases(ro: RefOracle):
     return out
 
 
+SCHEME_RUNS = [  # name, communication override, wire kind override, block size
+    ("agsparse", None, None, 256), ("agsparse", "ring", None, 256),
+    ("agsparse", "hierarchy", "tensor_block", 64), ("sparcml", None, None, 256),
+    ("sparcml", None, "coo32", 256), ("ring-centralization", None, None, 256),
+    ("ring-centralization", None, "bitmap", 256), ("omnireduce", None, None, 256),
+    ("omnireduce", None, "tensor_block", 64), ("omnireduce", None, "tensor_block", 1000)]
+
+
+def scheme_cases(ro: RefOracle):
+    """zen::run_scheme over the baseline schemes (zen/schemes.hpp:119-328,
+    420-465): every node's result, the SimNet ledger and the balance, on
+    shapes from schemes_test.cpp (overlaps 0..1, n = 2..16, a value that
+    cancels to exact zero for the OmniReduce block decode)."""
+    out = {}
+    cases = [(4, 2000, 0.03, 0.5, 3), (8, 5000, 0.01, 0.0, 4), (2, 777, 0.05, 1.0, 5),
+             (4, 100000, 0.002, 0.25, 6), (16, 20000, 0.005, 0.4, 7)]
+    for c, (n, m, d, om, seed) in enumerate(cases):
+        ins = ro.generate(m, n, d, om, seed)
+        if c == 0:  # a shared index whose values cancel: dropped by the block decode
+            i0, v0 = ins[0]
+            i1, v1 = ins[1]
+            common = np.intersect1d(i0, i1)[:1]
+            if common.size:
+                v1 = v1.copy()
+                v1[np.searchsorted(i1, common)] = -v0[np.searchsorted(i0, common)]
+                ins[1] = (i1, v1)
+        out[f"c{c}_m"] = np.array([m, n], np.uint64)
+        for w, (i, v) in enumerate(ins):
+            out[f"c{c}_in{w}_idx"], out[f"c{c}_in{w}_val"] = i, v
+        for r, (name, comm, kind, bs) in enumerate(SCHEME_RUNS):
+            k, cb = (("coo", 32) if kind == "coo32" else (kind, 64))
+            res, led, bal = ro.run_scheme(name, m, ins, comm, k, bs, cb)
+            for w, (i, v) in enumerate(res):
+                out[f"c{c}_r{r}_w{w}_idx"], out[f"c{c}_r{r}_w{w}_val"] = i, v
+            out[f"c{c}_r{r}_ledger"] = led
+            if bal is not None:
+                out[f"c{c}_r{r}_balance"] = np.array(bal, np.float64)
+    out["ncases"] = np.array([len(cases)], np.uint32)
+    return out
+
+
 def main():
     ro = RefOracle()
     os.makedirs(OUT, exist_ok=True)
     for name, fn in [("hash_kat", hash_kat), ("hhash", hhash_cases), ("to_sparse", to_sparse_cases),
                      ("codec", codec_cases), ("bp", bp_cases), ("wire", wire_cases),
-                     ("topk", topk_cases), ("hc", hc_cases)]:
+                     ("topk", topk_cases), ("hc", hc_cases),
+                     ("schemes", scheme_cases)]:
         data = fn(ro)
         path = os.path.join(OUT, name + ".npz")
         np.savez_compressed(path, **data)

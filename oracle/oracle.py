@@ -475,6 +475,10 @@ class RefOracle:
             C.c_uint32, C.c_uint64, vpp, vpp, u64p, C.c_uint32, C.c_uint32, C.c_uint32, u64p,
             f32p, C.POINTER(C.c_uint64), u64p, C.c_uint32, C.POINTER(C.c_uint32),
             C.POINTER(C.c_int)]
+        L.ref_run_scheme.argtypes = [
+            C.c_char_p, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, vpp,
+            vpp, u64p, C.c_uint64, u64p, f32p, u64p, u64p, C.c_uint32, C.POINTER(C.c_uint32),
+            f64p, C.POINTER(C.c_int)]
         L.ref_bench_step.argtypes = [C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p), C.c_uint32,
                                      C.c_double, C.c_double, C.c_uint32, C.c_uint64, C.c_int, f64p,
                                      C.POINTER(C.c_uint64)]
@@ -734,6 +738,32 @@ def _ref_hier_centralization(self, m, inputs, kind="coo", block_size=256, coo_bi
             ledger[:ns.value * 4 * n].reshape(ns.value, 4, n))
 
 
+COMM = {"ring": 0, "hierarchy": 1, "point-to-point": 2}
+
+
+def _ref_run_scheme(self, name, m, inputs, comm=None, kind=None, block_size=256, coo_bits=64):
+    """run_scheme(scheme_config_from_name(name)) -> (results [(idx, val)] per
+    node, ledger [stages][4][n], balance (push, pull) or None)."""
+    n = len(inputs)
+    ins, nnz, ip, vp = self._ptrs(inputs)
+    cap = max(int(nnz.sum()), 1)
+    oi = np.zeros(n * cap, np.uint64)
+    ov = np.zeros(n * cap, np.float32)
+    oc = np.zeros(n, np.uint64)
+    ledger = np.zeros(16 * 4 * n, np.uint64)
+    ns, bv = C.c_uint32(), C.c_int()
+    bal = np.zeros(2, np.float64)
+    k = 0 if kind is None else (WIRE_KINDS[kind] if isinstance(kind, str) else kind)
+    self._check(self.lib.ref_run_scheme(name.encode(), -1 if comm is None else COMM[comm], k,
+                                        block_size, coo_bits, n, m, ip, vp, nnz, cap, oi, ov, oc,
+                                        ledger, 16, C.byref(ns), bal, C.byref(bv)), "run_scheme")
+    res = [(oi[w * cap:w * cap + int(oc[w])].copy(), ov[w * cap:w * cap + int(oc[w])].copy())
+           for w in range(n)]
+    return res, ledger[:ns.value * 4 * n].reshape(ns.value, 4, n), \
+        ((bal[0], bal[1]) if bv.value else None)
+
+
+RefOracle.run_scheme = _ref_run_scheme
 RefOracle.merge_sum = _ref_merge_sum
 RefOracle.metric = _ref_metric
 RefOracle.profile = _ref_profile
@@ -831,6 +861,113 @@ def _co_profile(self, m, rounds):
     return dsum / float(dcount), gamma, skew_sum / float(len(rounds) * n), choice
 
 
+def _co_fold(self, parts):
+    i, v = _u64(parts[0][0]), _f32(parts[0][1])
+    for pi, pv in parts[1:]:
+        i, v = self.merge_sum(i, v, pi, pv)
+    return i, v
+
+
+def _co_run_scheme(self, name, m, inputs, comm=None, kind=None, block_size=256, coo_bits=64):
+    """Restatement of run_scheme (zen/schemes.hpp:420-442) for the centralized
+    schemes and the OmniReduce-like one (BP has its own oracle): same return
+    shape as RefOracle.run_scheme."""
+    n = len(inputs)
+    ins = [(_u64(i), _f32(v)) for i, v in inputs]
+    kind = kind or ("tensor_block" if name == "omnireduce" else "coo")
+    if name == "omnireduce":
+        block_size = block_size if kind == "tensor_block" else 256
+    stages = {}
+
+    def send(stage, frm, to, ib, vb):
+        led = stages.setdefault(stage, np.zeros((4, n), np.uint64))
+        led[0, frm] += ib + vb
+        led[1, to] += ib + vb
+        led[2, to] += ib
+        led[3, to] += vb
+
+    def sz(t):
+        return _co_sizes(self, kind, m, t[0], t[1], block_size, coo_bits)
+
+    balance = None
+    if name == "agsparse":  # schemes.hpp:119-168
+        comm = comm or "point-to-point"
+        if comm == "point-to-point":
+            for w in range(n):
+                for to in range(n):
+                    if to != w:
+                        send(0, w, to, *sz(ins[w]))
+        elif comm == "ring":
+            if not _pow2(n):
+                raise OracleError(NON_POWER_OF_TWO)
+            for st in range(n - 1):
+                for w in range(n):
+                    send(st, w, (w + 1) % n, *sz(ins[(w + n - st) % n]))
+        else:
+            if not _pow2(n):
+                raise OracleError(NON_POWER_OF_TWO)
+            hold = [[w] for w in range(n)]
+            bit = 1
+            while bit < n:
+                prev = [list(h) for h in hold]
+                for w in range(n):
+                    for o in prev[w]:
+                        send(bit.bit_length() - 1, w, w ^ bit, *sz(ins[o]))
+                    hold[w] += prev[w ^ bit]
+                bit <<= 1
+        r = _co_fold(self, ins)
+        results = [r] * n
+    elif name == "sparcml":
+        i, v, led = _co_hier_centralization(self, m, ins, kind, block_size, coo_bits)
+        return [(i, v)] * n, led, None
+    elif name == "ring-centralization":  # schemes.hpp:194-215
+        if not _pow2(n):
+            raise OracleError(NON_POWER_OF_TWO)
+        tok = list(ins)
+        for st in range(n - 1):
+            for w in range(n):
+                send(st, w, (w + 1) % n, *sz(tok[w]))
+            tok = [self.merge_sum(*tok[(w + n - 1) % n], *ins[w]) for w in range(n)]
+        results = tok
+    elif name == "omnireduce":  # schemes.hpp:219-328
+        rng = (m + n - 1) // n
+        sl = [[(i[(i // rng) == p], v[(i // rng) == p]) for p in range(n)] for i, v in ins]
+
+        def blocks(t, p):
+            lo, hi = p * rng, min(m, p * rng + rng)
+            b = np.unique((t[0] - np.uint64(lo)) // np.uint64(block_size)) if len(t[0]) else []
+            vb = sum(32 * min(block_size, hi - (lo + int(x) * block_size)) for x in b)
+            return 64 * len(b), vb
+        for w in range(n):
+            for p in range(n):
+                if p != w and len(sl[w][p][0]):
+                    send(0, w, p, *blocks(sl[w][p], p))
+        agg = [_co_fold(self, [sl[w][p] for w in range(n)]) for p in range(n)]
+        for p in range(n):
+            if len(agg[p][0]):
+                ib, vb = blocks(agg[p], p)
+                for w in range(n):
+                    if w != p:
+                        send(1, p, w, ib, vb)
+        ai = np.concatenate([a[0] for a in agg])
+        av = np.concatenate([a[1] for a in agg])
+        keep = av != 0.0
+        results = [(ai[keep], av[keep])] * n
+        if all(len(i) for i, _ in ins):
+            push = max(float(n) * float(len(sl[w][p][0])) / float(len(ins[w][0]))
+                       for w in range(n) for p in range(n))
+            loads = [len(a[0]) for a in agg]
+            pull = max(float(n) * float(x) / float(sum(loads)) for x in loads)
+            balance = (push, pull)
+    else:
+        raise OracleError(INVALID, "scheme not restated: " + name)
+    ns = max(stages) + 1 if stages else 0
+    led = np.stack([stages.get(s, np.zeros((4, n), np.uint64)) for s in range(ns)]) \
+        if ns else np.zeros((0, 4, n), np.uint64)
+    return results, led, balance
+
+
+COracle.run_scheme = _co_run_scheme
 COracle.sizes = _co_sizes
 COracle.hier_centralization = _co_hier_centralization
 COracle.profile = _co_profile

@@ -28,7 +28,7 @@
 
 namespace {
 enum { ZR_OK = 0, ZR_INVALID = 1, ZR_OVERFLOW = 2, ZR_OUTSIDE = 3, ZR_MALFORMED = 4, ZR_EMPTY = 5,
-       ZR_MISMATCH = 6, ZR_NONPOW2 = 7, ZR_MISSING = 8, ZR_OTHER = 9 };
+       ZR_MISMATCH = 6, ZR_NONPOW2 = 7, ZR_MISSING = 8, ZR_OTHER = 9, ZR_UNSUPPORTED = 10 };
 
 thread_local int64_t g_last_partition = -1;
 thread_local char g_last_msg[512];
@@ -54,6 +54,9 @@ int guarded(F&& f) {
   } catch (const zen::NonPowerOfTwo& e) {
     std::snprintf(g_last_msg, sizeof g_last_msg, "%s", e.what());
     return ZR_NONPOW2;
+  } catch (const zen::UnsupportedCombination& e) {
+    std::snprintf(g_last_msg, sizeof g_last_msg, "%s", e.what());
+    return ZR_UNSUPPORTED;
   } catch (const zen::MissingProfileEntry& e) {
     std::snprintf(g_last_msg, sizeof g_last_msg, "%s", e.what());
     return ZR_MISSING;
@@ -523,6 +526,54 @@ int ref_hier_centralization(uint32_t n, uint64_t m, const uint64_t* const* idx,
         ledger[(st * 4 + 2) * n + node] = s.recv_index_bits[node];
         ledger[(st * 4 + 3) * n + node] = s.recv_value_bits[node];
       }
+    }
+  });
+}
+
+// zen::run_scheme (zen/schemes.hpp:420-442) on scheme_config_from_name(name),
+// optionally overriding the communication pattern (0 ring, 1 hierarchy, 2
+// point-to-point; -1 keep) and the wire format (kind 0 keeps it).  Every
+// node's result goes out (n * cap entries), with the ledger [stages][4][n]
+// and the balance when the scheme measures one.
+int ref_run_scheme(const char* name, int comm, uint32_t kind, uint32_t block_size,
+                   uint32_t coo_bits, uint32_t n, uint64_t m, const uint64_t* const* idx,
+                   const float* const* val, const uint64_t* nnz, uint64_t cap, uint64_t* out_idx,
+                   float* out_val, uint64_t* out_counts, uint64_t* ledger, uint32_t max_stages,
+                   uint32_t* stages, double* balance, int* balance_valid) {
+  return guarded([&] {
+    std::vector<zen::SparseTensor> inputs;
+    for (uint32_t w = 0; w < n; ++w) inputs.push_back(make_tensor(m, idx[w], val[w], nnz[w]));
+    zen::SchemeConfig cfg = zen::scheme_config_from_name(name);
+    if (comm == 0) cfg.communication = zen::CommPattern::Ring;
+    if (comm == 1) cfg.communication = zen::CommPattern::Hierarchy;
+    if (comm == 2) cfg.communication = zen::CommPattern::PointToPoint;
+    if (kind == 1) cfg.format = zen::WireFormat::coo(coo_bits);
+    if (kind == 2) cfg.format = zen::WireFormat::bitmap();
+    if (kind == 3) cfg.format = zen::WireFormat::tensor_block(block_size);
+    zen::SimNet net(n, 1.0);
+    auto out = zen::run_scheme(cfg, inputs, net);
+    for (uint32_t w = 0; w < n; ++w) {
+      const auto& r = out.results[w];
+      if (r.nnz() > cap) throw zen::Error("result capacity");
+      std::copy(r.indices().begin(), r.indices().end(), out_idx + size_t(w) * cap);
+      std::copy(r.values().begin(), r.values().end(), out_val + size_t(w) * cap);
+      out_counts[w] = r.nnz();
+    }
+    const uint32_t ns = uint32_t(std::min<size_t>(max_stages, out.traffic.stages.size()));
+    *stages = ns;
+    for (uint32_t st = 0; st < ns; ++st) {
+      const auto& s = out.traffic.stages[st];
+      for (uint32_t node = 0; node < n; ++node) {
+        ledger[(st * 4 + 0) * n + node] = s.sent_bits[node];
+        ledger[(st * 4 + 1) * n + node] = s.recv_bits[node];
+        ledger[(st * 4 + 2) * n + node] = s.recv_index_bits[node];
+        ledger[(st * 4 + 3) * n + node] = s.recv_value_bits[node];
+      }
+    }
+    *balance_valid = out.balance.has_value();
+    if (out.balance) {
+      balance[0] = out.balance->push_imbalance;
+      balance[1] = out.balance->pull_imbalance;
     }
   });
 }

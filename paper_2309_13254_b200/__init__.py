@@ -20,5 +20,7 @@ from .schemes import (  # noqa: F401
     BALANCED_PARALLELISM, HIERARCHICAL_CENTRALIZATION, CostInputs, HCSynchronizer,
     MissingProfileEntry, NonPowerOfTwo, SparsityProfile, densification_ratio, density,
     merge_sum, overlap_ratio, profile_sparsity, run_hier_centralization, select_scheme,
-    skewness_ratio, t_allreduce_dense, t_bp, t_bp_coefficient, t_hc, t_hc_coefficient,
+    skewness_ratio, t_allreduce_dense, KNOWN_SCHEME_NAMES, Aggregation, BalancePattern,
+    CommPattern, PartitionPattern, SchemeConfig, UnsupportedCombination, run_agsparse,
+    run_omnireduce_like, run_ring_centralization, run_scheme, scheme_config_from_name, t_bp, t_bp_coefficient, t_hc, t_hc_coefficient,
     t_hierarchy_incremental_lb, t_ring_incremental, t_sparse_ps, t_sparse_ps_broadcast)

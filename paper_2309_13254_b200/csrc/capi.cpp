@@ -1174,6 +1174,48 @@ extern "C" zen_status zen_merge_sum(zen_ctx* c, const uint64_t* a_idx, const flo
   return ZEN_OK;
 }
 
+// Non-zero blocks of `block_size` positions counted from `origin` in a sorted
+// tensor: the block framing of run_omnireduce_like (zen/schemes.hpp:227-244).
+extern "C" zen_status zen_count_blocks(zen_ctx* c, const uint64_t* d_idx, uint64_t count,
+                                       uint64_t origin, uint64_t block_size, uint64_t* blocks) {
+  if (!c || !blocks || (count && !d_idx)) return fail(ZEN_E_INVALID, "null argument");
+  if (block_size == 0) return fail(ZEN_E_INVALID, "block size must be at least 1");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  Bump sc;
+  CKR(ctx_scratch(c, bump_bytes({8}), &sc));
+  unsigned long long* d = sc.get<unsigned long long>(1);
+  CK(cudaMemsetAsync(d, 0, 8, c->stream));
+  launch_count_blocks(d_idx, count, origin, block_size, d, c->stream);
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *blocks = h;
+  return ZEN_OK;
+}
+
+// Drops the entries whose value is exactly zero (+0.0 or -0.0), keeping order:
+// the block decoding of run_omnireduce_like (zen/schemes.hpp:289-295).
+extern "C" zen_status zen_compact_nonzero(zen_ctx* c, const uint64_t* d_idx, const float* d_val,
+                                          uint64_t count, uint64_t* d_out_idx, float* d_out_val,
+                                          uint64_t* out_count) {
+  if (!c || !out_count || (count && (!d_idx || !d_val || !d_out_idx || !d_out_val)))
+    return fail(ZEN_E_INVALID, "null argument");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  const size_t tb = wire_select_bytes(count);
+  Bump sc;
+  CKR(ctx_scratch(c, bump_bytes({8, count, tb}), &sc));
+  uint64_t* d = sc.get<uint64_t>(1);
+  uint8_t* flag = sc.get<uint8_t>(count);
+  void* tmp = sc.get<uint8_t>(tb);
+  CK(cudaMemsetAsync(d, 0, 8, c->stream));
+  launch_compact_nonzero(d_idx, d_val, count, flag, d_out_idx, d_out_val, d, tmp, tb, c->stream);
+  CK(cudaMemcpyAsync(out_count, d, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return ZEN_OK;
+}
+
 // zen::skewness_ratio's per-range counts (zen/tensor.hpp:193-213): entries of
 // the sorted tensor in each of `partitions` contiguous ranges of ceil(M/n).
 extern "C" zen_status zen_range_counts(zen_ctx* c, const uint64_t* d_idx, uint64_t count,

@@ -303,3 +303,49 @@ void launch_sort_pairs(const uint64_t* ki, uint64_t* ko, const float* vi, float*
 }
 
 }  // namespace zen
+
+// ---- OmniReduce-like range blocks (zen/schemes.hpp:227-244) -----------------
+namespace zen {
+namespace {
+// 1 where a sorted entry opens a new block of `block` positions counted from
+// `origin`; a single counter gathers them (tiny key sets)
+__global__ void k_count_blocks(const uint64_t* __restrict__ idx, uint64_t count, uint64_t origin,
+                               uint64_t block, unsigned long long* out) {
+  zen_dev::pdl_entry();
+  uint32_t c = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    c += (i == 0 || (idx[i] - origin) / block != (idx[i - 1] - origin) / block) ? 1u : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+__global__ void k_nonzero_flags(const float* __restrict__ val, uint64_t count, uint8_t* flag) {
+  zen_dev::pdl_entry();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    flag[i] = val[i] != 0.0f ? 1 : 0;
+}
+}  // namespace
+
+void launch_count_blocks(const uint64_t* idx, uint64_t count, uint64_t origin, uint64_t block,
+                         unsigned long long* out, cudaStream_t s) {
+  if (!count) return;
+  launch_k(k_count_blocks, (unsigned)std::min<uint64_t>(grid_for(count), 148 * 8), 256, 0, s, idx,
+           count, origin, block, out);
+  count_launch();
+}
+
+void launch_compact_nonzero(const uint64_t* idx, const float* val, uint64_t count, uint8_t* flag,
+                            uint64_t* out_idx, float* out_val, uint64_t* d_count, void* tmp,
+                            size_t tmp_bytes, cudaStream_t s) {
+  if (!count) return;
+  launch_k(k_nonzero_flags, grid_for(count), 256, 0, s, val, count, flag);
+  count_launch();
+  cub::DeviceSelect::Flagged(tmp, tmp_bytes, idx, flag, out_idx, d_count, (int64_t)count, s);
+  cub::DeviceSelect::Flagged(tmp, tmp_bytes, val, flag, out_val, d_count, (int64_t)count, s);
+  count_launch();
+  count_launch();
+}
+}  // namespace zen

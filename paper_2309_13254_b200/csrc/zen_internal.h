@@ -344,6 +344,13 @@ void launch_hc_push(const HcPushArgs& a, cudaStream_t stream);
 void launch_hc_begin(unsigned long long* epoch, cudaStream_t stream);
 void launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t stream);
 
+// OmniReduce-like helpers (k_wire.cu)
+void launch_count_blocks(const uint64_t* idx, uint64_t count, uint64_t origin, uint64_t block,
+                         unsigned long long* out, cudaStream_t s);
+void launch_compact_nonzero(const uint64_t* idx, const float* val, uint64_t count, uint8_t* flag,
+                            uint64_t* out_idx, float* out_val, uint64_t* d_count, void* tmp,
+                            size_t tmp_bytes, cudaStream_t s);
+
 // bnd[p] = lower_bound(idx, min(M, p*ceil(M/parts))), p in [0, parts] (k_util.cu)
 void launch_range_bounds(const uint64_t* idx, uint64_t count, uint64_t m, uint32_t parts,
                          uint64_t* bnd, cudaStream_t stream);

@@ -476,3 +476,241 @@ class HCSynchronizer:
                        else (self.m, 32 * z))
         return res
 
+
+
+# ----------------------------------------------- the design space (f4) ----
+# zen/schemes.hpp:21-41, 119-168, 194-328, 418-470: the baseline schemes the
+# paper compares against, with all n nodes on the current GPU.  Each keeps the
+# reference's SimNet ledger message for message and its results bit for bit;
+# every fold is the device merge_sum.
+
+class UnsupportedCombination(Error):
+    """zen::UnsupportedCombination (errors.hpp:48-52)."""
+
+
+class CommPattern:
+    Ring, Hierarchy, PointToPoint = "ring", "hierarchy", "point-to-point"
+
+
+class Aggregation:
+    Incremental, OneShot = "incremental", "one-shot"
+
+
+class PartitionPattern:
+    Centralization, Parallelism = "centralization", "parallelism"
+
+
+class BalancePattern:
+    Balanced, Imbalanced, NotApplicable = "balanced", "imbalanced", "not-applicable"
+
+
+@dataclass
+class SchemeConfig:
+    """zen::SchemeConfig (schemes.hpp:27-41)."""
+    communication: str = CommPattern.PointToPoint
+    aggregation: str = Aggregation.OneShot
+    partition: str = PartitionPattern.Centralization
+    balance: str = BalancePattern.NotApplicable
+    format: WireFormat = field(default_factory=WireFormat.coo)
+
+    def validate(self):
+        centralized = self.partition == PartitionPattern.Centralization
+        if centralized != (self.balance == BalancePattern.NotApplicable):
+            raise UnsupportedCombination(
+                "the balance dimension applies exactly when the partition pattern is Parallelism")
+
+
+def _fold_dev(states, m):
+    """aggregate (tensor.hpp:171-176): left fold in the given order."""
+    i, v = states[0]
+    for t in states[1:]:
+        i, v = _merge_dev(i, v, *t, m)
+    return i, v
+
+
+def run_agsparse(inputs, net: SimNet, pattern: str = CommPattern.PointToPoint,
+                 fmt: WireFormat | None = None) -> SyncOutcome:
+    """zen::run_agsparse (schemes.hpp:119-168): all-gather of whole tensors
+    (point-to-point, ring or hierarchy ledger), then one aggregate."""
+    fmt = fmt or WireFormat.coo()
+    _check_inputs(inputs, net)
+    n, m = len(inputs), inputs[0].universe()
+    states = [_to_dev(t) for t in inputs]
+    sizes = [_Sized(*_sizes_dev(*s, m, fmt)) for s in states]
+    if pattern == CommPattern.PointToPoint:
+        for w in range(n):
+            for to in range(n):
+                if to != w:
+                    net.send(0, w, to, sizes[w])
+    elif pattern == CommPattern.Ring:
+        if not _pow2(n):
+            raise NonPowerOfTwo()
+        for s in range(n - 1):
+            for w in range(n):
+                net.send(s, w, (w + 1) % n, sizes[(w + n - s) % n])
+    elif pattern == CommPattern.Hierarchy:
+        if not _pow2(n):
+            raise NonPowerOfTwo()
+        holdings = [[w] for w in range(n)]
+        bit = 1
+        while bit < n:
+            stage = bit.bit_length() - 1
+            prev = [list(h) for h in holdings]
+            for w in range(n):
+                for origin in prev[w]:
+                    net.send(stage, w, w ^ bit, sizes[origin])
+                holdings[w] += prev[w ^ bit]
+            bit <<= 1
+    else:
+        raise Error(f"unknown communication pattern {pattern}")
+    result = _to_host(m, *_fold_dev(states, m))
+    return SyncOutcome([result] * n, net.finalize(), None)
+
+
+def run_ring_centralization(inputs, net: SimNet, fmt: WireFormat | None = None) -> SyncOutcome:
+    """zen::run_ring_centralization (schemes.hpp:194-215): n-1 stages, each node
+    forwards its running token to the next; token'[w] = merge_sum(token[w-1],
+    input[w])."""
+    fmt = fmt or WireFormat.coo()
+    _check_inputs(inputs, net)
+    n, m = len(inputs), inputs[0].universe()
+    if not _pow2(n):
+        raise NonPowerOfTwo()
+    ins = [_to_dev(t) for t in inputs]
+    tokens = list(ins)
+    for s in range(n - 1):
+        for w in range(n):
+            net.send(s, w, (w + 1) % n, _Sized(*_sizes_dev(*tokens[w], m, fmt)))
+        tokens = [_merge_dev(*tokens[(w + n - 1) % n], *ins[w], m) for w in range(n)]
+    return SyncOutcome([_to_host(m, i, v) for i, v in tokens], net.finalize(), None)
+
+
+def _range_slices(i, v, m, n):
+    """Slices of a sorted device tensor by the contiguous ranges ceil(M/n)
+    (schemes.hpp:240-252): zen_range_counts gives the boundaries."""
+    counts = _range_counts_dev(i, m, n)
+    out, at = [], 0
+    for p in range(n):
+        c = int(counts[p])
+        out.append((i[at:at + c], v[at:at + c]))
+        at += c
+    return out
+
+
+def _block_sizes(i, m, n, p, block_size):
+    """block_sizes (schemes.hpp:255-270): 64 index bits per non-zero block,
+    32 value bits per position of each (the range's last block may be short)."""
+    rng = (m + n - 1) // n
+    lo = p * rng
+    hi = min(m, lo + rng)
+    z = i.numel()
+    if z == 0:
+        return 0, 0
+    nb = C.c_uint64()
+    _check(_lib().zen_count_blocks(context(i.device.index).h, _ptr(i), z, lo, block_size,
+                                   C.byref(nb)))
+    blocks = nb.value
+    value = 32 * block_size * blocks
+    last = (int(i[-1].item()) - lo) // block_size  # only the block holding hi-1 can be short
+    if lo + last * block_size + block_size > hi:
+        value -= 32 * (lo + last * block_size + block_size - hi)
+    return 64 * blocks, value
+
+
+class _TbMsg(_Sized):
+    pass
+
+
+def run_omnireduce_like(inputs, net: SimNet, block_size: int = 256) -> SyncOutcome:
+    """zen::run_omnireduce_like (schemes.hpp:219-328): contiguous ranges, block
+    transport to the range owner, per-range aggregate in worker order, block
+    broadcast back, exact zeros dropped by the block decode."""
+    from .zen import BalanceDetails, PartitionedSparseTensor, imbalance_pull, imbalance_push
+    _check_inputs(inputs, net)
+    if block_size < 1:
+        raise Error("block size must be at least 1")
+    torch = _torch()
+    n, m = len(inputs), inputs[0].universe()
+    slices = [_range_slices(*_to_dev(t), m, n) for t in inputs]
+    for w in range(n):
+        for p in range(n):
+            if p == w or slices[w][p][0].numel() == 0:
+                continue
+            net.send(0, w, p, _TbMsg(*_block_sizes(slices[w][p][0], m, n, p, block_size)))
+    aggregated = [_fold_dev([slices[w][p] for w in range(n)], m) for p in range(n)]
+    for p in range(n):
+        if aggregated[p][0].numel() == 0:
+            continue
+        sz = _TbMsg(*_block_sizes(aggregated[p][0], m, n, p, block_size))
+        for w in range(n):
+            if w != p:
+                net.send(1, p, w, sz)
+    ai = torch.cat([a[0] for a in aggregated])
+    av = torch.cat([a[1] for a in aggregated])
+    oi = torch.empty(max(ai.numel(), 1), dtype=torch.int64, device=ai.device)
+    ov = torch.empty(max(ai.numel(), 1), dtype=torch.float32, device=ai.device)
+    got = C.c_uint64()
+    _check(_lib().zen_compact_nonzero(context(ai.device.index).h, _ptr(ai), _ptr(av), ai.numel(),
+                                      _ptr(oi), _ptr(ov), C.byref(got)))
+    result = _to_host(m, oi[:got.value], ov[:got.value])
+    balance = None
+    if all(not t.empty() for t in inputs):
+        parted = [PartitionedSparseTensor([_SizeOnly(s[0].numel()) for s in slices[w]])
+                  for w in range(n)]
+        loads = [a[0].numel() for a in aggregated]
+        balance = BalanceDetails(imbalance_push(parted), imbalance_pull(loads, sum(loads)))
+    return SyncOutcome([result] * n, net.finalize(), balance)
+
+
+class _SizeOnly:
+    def __init__(self, z):
+        self._z = z
+
+    def nnz(self):
+        return self._z
+
+
+def run_scheme(cfg: SchemeConfig, inputs, net: SimNet, params=None) -> SyncOutcome:
+    """zen::run_scheme (schemes.hpp:420-442)."""
+    from .zen import run_balanced_parallelism
+    cfg.validate()
+    if cfg.partition == PartitionPattern.Centralization:
+        if cfg.aggregation == Aggregation.OneShot:
+            return run_agsparse(inputs, net, cfg.communication, cfg.format)
+        if cfg.communication == CommPattern.Hierarchy:
+            return run_hier_centralization(inputs, net, cfg.format)
+        if cfg.communication == CommPattern.Ring:
+            return run_ring_centralization(inputs, net, cfg.format)
+        raise UnsupportedCombination("point-to-point incremental centralization is not implemented")
+    if cfg.communication == CommPattern.PointToPoint:
+        if (cfg.aggregation == Aggregation.OneShot and cfg.balance == BalancePattern.Imbalanced
+                and cfg.format.kind == "tensor_block"):
+            return run_omnireduce_like(inputs, net, cfg.format.block_size)
+        if cfg.aggregation == Aggregation.Incremental and cfg.balance == BalancePattern.Balanced:
+            return run_balanced_parallelism(inputs, net, params)
+    raise UnsupportedCombination("no implemented scheme matches this configuration")
+
+
+KNOWN_SCHEME_NAMES = ["agsparse", "sparcml", "ring-centralization", "omnireduce",
+                      "balanced-parallelism"]
+
+
+def scheme_config_from_name(name: str) -> SchemeConfig:
+    """zen::scheme_config_from_name (schemes.hpp:445-465)."""
+    C_, P_ = PartitionPattern.Centralization, PartitionPattern.Parallelism
+    if name == "agsparse":
+        return SchemeConfig(CommPattern.PointToPoint, Aggregation.OneShot, C_,
+                            BalancePattern.NotApplicable, WireFormat.coo())
+    if name == "sparcml":
+        return SchemeConfig(CommPattern.Hierarchy, Aggregation.Incremental, C_,
+                            BalancePattern.NotApplicable, WireFormat.coo())
+    if name == "ring-centralization":
+        return SchemeConfig(CommPattern.Ring, Aggregation.Incremental, C_,
+                            BalancePattern.NotApplicable, WireFormat.coo())
+    if name == "omnireduce":
+        return SchemeConfig(CommPattern.PointToPoint, Aggregation.OneShot, P_,
+                            BalancePattern.Imbalanced, WireFormat.tensor_block())
+    if name == "balanced-parallelism":
+        return SchemeConfig(CommPattern.PointToPoint, Aggregation.Incremental, P_,
+                            BalancePattern.Balanced, WireFormat.hash_bitmap())
+    raise UnsupportedCombination("unknown scheme name: " + name)

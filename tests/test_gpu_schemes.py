@@ -171,3 +171,68 @@ def test_hc_rank_api_single_rank(zen):
         hc.sync_sparse(torch.tensor([5, 3], device="cuda"), torch.ones(2, device="cuda"))
         hc.wait()
     torch.cuda.set_stream(torch.cuda.default_stream())
+
+
+# ---- f4: the baseline schemes on the GPU (run_scheme) ----
+
+def _scheme_cfg(zen, name, comm, kind, bs):
+    cfg = zen.scheme_config_from_name(name)
+    if comm is not None:
+        cfg.communication = comm
+    if kind == "coo32":
+        cfg.format = zen.WireFormat.coo(32)
+    elif kind == "bitmap":
+        cfg.format = zen.WireFormat.bitmap()
+    elif kind == "tensor_block":
+        cfg.format = zen.WireFormat.tensor_block(bs)
+    return cfg
+
+
+def test_baseline_schemes_golden(zen):
+    """run_scheme for AGsparse (3 patterns), SparCML, ring centralization and
+    OmniReduce-like against the reference's own outputs: every node's result
+    (fp32 bits), the SimNet ledger and the balance."""
+    from make_golden import SCHEME_RUNS
+    g = load_golden("schemes")
+    for c in range(int(g["ncases"][0])):
+        m, n = (int(x) for x in g[f"c{c}_m"])
+        ins = [zen.SparseTensor(m, g[f"c{c}_in{w}_idx"], g[f"c{c}_in{w}_val"]) for w in range(n)]
+        for r, (name, comm, kind, bs) in enumerate(SCHEME_RUNS):
+            out = zen.run_scheme(_scheme_cfg(zen, name, comm, kind, bs), ins, zen.SimNet(n, 1.0))
+            for w in range(n):
+                want = zen.SparseTensor(m, g[f"c{c}_r{r}_w{w}_idx"], g[f"c{c}_r{r}_w{w}_val"])
+                assert out.results[w] == want, f"case {c} {name} {comm} {kind} node {w}"
+            np.testing.assert_array_equal(_ledger(out.traffic, n), g[f"c{c}_r{r}_ledger"])
+            key = f"c{c}_r{r}_balance"
+            assert (out.balance is None) == (key not in g)
+            if out.balance is not None:
+                assert (out.balance.push_imbalance, out.balance.pull_imbalance) == tuple(g[key])
+
+
+def test_scheme_dispatch_and_errors(zen):
+    m = 1000
+    ins = [zen.SparseTensor(m, [w, 500 + w], [1.0, 2.0]) for w in range(4)]
+    assert set(zen.KNOWN_SCHEME_NAMES) == {"agsparse", "sparcml", "ring-centralization",
+                                           "omnireduce", "balanced-parallelism"}
+    bp = zen.run_scheme(zen.scheme_config_from_name("balanced-parallelism"), ins,
+                        zen.SimNet(4, 1.0))
+    ag = zen.run_scheme(zen.scheme_config_from_name("agsparse"), ins, zen.SimNet(4, 1.0))
+    assert bp.results[0] == ag.results[0]
+    with pytest.raises(zen.UnsupportedCombination):
+        zen.scheme_config_from_name("nope")
+    bad = zen.scheme_config_from_name("agsparse")
+    bad.balance = zen.BalancePattern.Balanced
+    with pytest.raises(zen.UnsupportedCombination):
+        zen.run_scheme(bad, ins, zen.SimNet(4, 1.0))
+    p2p_inc = zen.scheme_config_from_name("sparcml")
+    p2p_inc.communication = zen.CommPattern.PointToPoint
+    with pytest.raises(zen.UnsupportedCombination):
+        zen.run_scheme(p2p_inc, ins, zen.SimNet(4, 1.0))
+    three = [zen.SparseTensor(m, [w], [1.0]) for w in range(3)]
+    for name in ["ring-centralization", "sparcml"]:
+        with pytest.raises(zen.NonPowerOfTwo):
+            zen.run_scheme(zen.scheme_config_from_name(name), three, zen.SimNet(3, 1.0))
+    om = zen.run_omnireduce_like(three, zen.SimNet(3, 1.0), 16)  # any n
+    assert om.results[0].nnz() == 3
+    with pytest.raises(zen.Error):
+        zen.run_omnireduce_like(three, zen.SimNet(3, 1.0), 0)

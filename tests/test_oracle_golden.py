@@ -294,3 +294,28 @@ def test_hier_centralization_restatement_vs_reference(co, ro):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
             assert np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
         assert co.profile(2000, [ins]) == ro.profile(2000, [ins])
+
+
+# ---- f4: the baseline schemes (run_scheme) ----
+
+def test_baseline_schemes_golden(co):
+    """The restatement of run_agsparse / run_ring_centralization /
+    run_omnireduce_like / sparcml against the reference's outputs: every
+    node's result, the ledger and the balance."""
+    from make_golden import SCHEME_RUNS
+    g = load_golden("schemes")
+    for c in range(int(g["ncases"][0])):
+        m, n = (int(x) for x in g[f"c{c}_m"])
+        ins = [(g[f"c{c}_in{w}_idx"], g[f"c{c}_in{w}_val"]) for w in range(n)]
+        for r, (name, comm, kind, bs) in enumerate(SCHEME_RUNS):
+            k, cb = (("coo", 32) if kind == "coo32" else (kind, 64))
+            res, led, bal = co.run_scheme(name, m, ins, comm, k, bs, cb)
+            for w, (i, v) in enumerate(res):
+                np.testing.assert_array_equal(i, g[f"c{c}_r{r}_w{w}_idx"], err_msg=f"{c} {name}")
+                np.testing.assert_array_equal(v.view(np.uint32),
+                                              g[f"c{c}_r{r}_w{w}_val"].view(np.uint32))
+            np.testing.assert_array_equal(led, g[f"c{c}_r{r}_ledger"], err_msg=f"{c} {name}")
+            key = f"c{c}_r{r}_balance"
+            assert (bal is None) == (key not in g)
+            if bal is not None:
+                assert tuple(bal) == tuple(g[key])
