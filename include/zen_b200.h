@@ -232,6 +232,18 @@ zen_status zen_compact_nonzero(zen_ctx* ctx, const uint64_t* d_idx, const float*
  * zen_hc_stage_counts.  max_nnz bounds each rank's input. */
 zen_status zen_hc_create(zen_ctx* ctx, uint32_t n, uint32_t rank, uint64_t universe,
                          uint64_t max_nnz, zen_hc** out);
+/* the same machinery for the centralized baselines (§8f row f4):
+ *   ZEN_SCHEME_HC        run_hier_centralization, zen/schemes.hpp:173-193
+ *   ZEN_SCHEME_RING      run_ring_centralization, zen/schemes.hpp:194-215
+ *                        (stage s: token -> rank+1; token' = merge(recv, input))
+ *   ZEN_SCHEME_AGSPARSE  run_agsparse point-to-point, zen/schemes.hpp:119-168
+ *                        (input -> every peer; aggregate in worker order; any n) */
+#define ZEN_SCHEME_HC 0u
+#define ZEN_SCHEME_RING 1u
+#define ZEN_SCHEME_AGSPARSE 2u
+zen_status zen_hc_create_scheme(zen_ctx* ctx, uint32_t scheme, uint32_t n, uint32_t rank,
+                                uint64_t universe, uint64_t max_nnz, zen_hc** out);
+uint32_t zen_hc_pushes(const zen_hc* hc); /* pushes per sync (entries of zen_hc_stage_counts) */
 void zen_hc_destroy(zen_hc* hc);
 zen_status zen_hc_ipc_handle(zen_hc* hc, void* out); /* ZEN_IPC_HANDLE_BYTES */
 zen_status zen_hc_connect(zen_hc* hc, const void* handles); /* n handles, rank-major */
@@ -244,7 +256,9 @@ zen_status zen_hc_result(zen_hc* hc, const uint64_t** d_idx, const float** d_val
                          uint64_t* count);
 zen_status zen_hc_copy_result(zen_hc* hc, uint64_t* d_idx, float* d_val, uint64_t capacity,
                               uint64_t* count);
-zen_status zen_hc_stage_counts(zen_hc* hc, uint64_t* counts); /* log2(n) entries */
+/* entries this rank sent per push, in plan order (HC / ring: one per stage;
+ * AGsparse: one per peer) -- the SimNet ledger's sent side */
+zen_status zen_hc_stage_counts(zen_hc* hc, uint64_t* counts);
 
 /* ---- apply: the step after the sync ------------------------------------ */
 /* d_dense[idx[i]] += alpha * val[i] for a sorted unique sparse tensor (an SGD

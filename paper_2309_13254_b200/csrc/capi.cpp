@@ -2284,36 +2284,64 @@ extern "C" zen_status zen_bp_debug_part(zen_bp* bp, int what, uint32_t server, u
   return ZEN_OK;
 }
 
-// ============================================== Hierarchical Centralization ==
-// zen::run_hier_centralization (zen/schemes.hpp:173-193), one process per GPU:
-// recursive doubling, stage s exchanging with rank ^ 2^s over NVLink stores
-// into the partner's CUDA-IPC arena and folding with the merge-path merge_sum
-// (k_merge.cu).  Counts never leave the device; a dense sync is one graph.
+// ======================================== centralized schemes, rank mode ==
+// One process per GPU, NVLink stores into the peers' CUDA-IPC arenas, every
+// fold the merge-path merge_sum (k_merge.cu); counts never leave the device,
+// so a dense sync is one CUDA graph.
+//   ZEN_SCHEME_HC       run_hier_centralization (zen/schemes.hpp:173-193):
+//                       stage s: state -> rank^2^s, state' = merge(state, recv)
+//   ZEN_SCHEME_RING     run_ring_centralization (zen/schemes.hpp:194-215):
+//                       stage s: token -> rank+1, token' = merge(recv, input)
+//   ZEN_SCHEME_AGSPARSE run_agsparse, point-to-point (zen/schemes.hpp:119-168):
+//                       input -> every peer, then aggregate in worker order
 
 namespace {
-constexpr uint32_t kHcMaxStages = 8;  // n <= 256
+constexpr uint32_t kHcMaxRanks = 256;
 
 struct HcHdr {
   unsigned long long epoch;
-  unsigned long long ready[kHcMaxStages];  // set by the stage-s partner's push
-  unsigned long long done[kHcMaxStages];   // set by the stage-s partner's merge
-  uint64_t cnt[2];                         // state ping-pong counts
-  uint64_t rcnt[kHcMaxStages];             // received counts
-  uint64_t stage_cnt[kHcMaxStages];        // |state| sent at stage s (ledger)
-  uint32_t err;                            // kErr* bits
-  uint32_t in_err;                         // kWire* bits of the input check
+  unsigned long long ready[kHcMaxRanks];  // receive slot j was filled (epoch)
+  unsigned long long done[kHcMaxRanks];   // the push this rank made to peer j was consumed
+  uint64_t cnt[3];                        // [input, state 0, state 1] counts
+  uint64_t rcnt[kHcMaxRanks];             // receive slot counts
+  uint64_t sent[kHcMaxRanks];             // entries of this rank's i-th push (ledger)
+  uint32_t err;                           // kErr* bits
+  uint32_t in_err;                        // kWire* bits of the input check
 };
 
+constexpr int kBufIn = 0, kBufSt0 = 1, kBufSt1 = 2, kBufRecv = 3;  // + slot
+
+struct HcPush {
+  int src;
+  uint32_t dst, slot;
+  uint64_t cap;
+};
+struct HcMerge {
+  int a, b, out;
+  int wait[2];       // receive slots to acquire (-1: none)
+  int done_rank[2];  // senders whose pushes this merge consumes (-1: none) ...
+  int done_idx[2];   // ... and the index of that push in the sender's plan
+  uint64_t a_cap, b_cap;
+};
+struct HcStage {
+  std::vector<HcPush> push;
+  std::vector<HcMerge> merge;
+};
 }  // namespace
 
 struct zen_hc {
   zen_ctx* ctx = nullptr;
-  uint32_t n = 0, rank = 0, L = 0;
+  uint32_t scheme = ZEN_SCHEME_HC;
+  uint32_t n = 0, rank = 0;
   uint64_t m = 0, max_nnz = 0, cap = 0;
-  uint64_t stage_cap[kHcMaxStages] = {};
-  size_t off_buf[2][2] = {}, off_recv[kHcMaxStages][2] = {}, bytes = 0;
+  std::vector<HcStage> plan;
+  int result_buf = kBufSt0;
+  uint32_t nslots = 0;
+  std::vector<size_t> off_idx, off_val;  // per buffer id
+  std::vector<uint64_t> buf_cap;
+  size_t bytes = 0;
   char* base = nullptr;
-  std::vector<char*> peer;  // arena base of every rank (own at `rank`)
+  std::vector<char*> peer;  // arena base per rank (own at `rank`)
   bool connected = false;
   DevMem mem;
   ExtractWs<uint64_t> ex{};
@@ -2325,72 +2353,163 @@ struct zen_hc {
   const float* gdense = nullptr;
   cudaStream_t gstream = nullptr;
   uint32_t graph_kernels = 0;
+  uint32_t npush = 0;
   uint64_t h_result = 0;
   HcHdr* hdr(uint32_t r) const { return reinterpret_cast<HcHdr*>(peer[r]); }
-  uint64_t* idx(uint32_t r, size_t off) const { return reinterpret_cast<uint64_t*>(peer[r] + off); }
-  float* val(uint32_t r, size_t off) const { return reinterpret_cast<float*>(peer[r] + off); }
+  uint32_t nslots_used() const { return uint32_t(buf_cap.size()) - kBufRecv; }
+  uint64_t* idx(uint32_t r, int b) const { return reinterpret_cast<uint64_t*>(peer[r] + off_idx[b]); }
+  float* val(uint32_t r, int b) const { return reinterpret_cast<float*>(peer[r] + off_val[b]); }
+  uint64_t* cntp(uint32_t r, int b) const {
+    return b < kBufRecv ? &hdr(r)->cnt[b] : &hdr(r)->rcnt[b - kBufRecv];
+  }
 };
 
 namespace {
 
+// The per-rank plan of a scheme: pushes and folds per stage, and the buffers.
+// A sender's push i waits until the receiver released done[i] for the
+// previous sync; the receiver releases it after the fold that consumed it.
+void hc_plan(zen_hc* h) {
+  const uint32_t n = h->n, r = h->rank;
+  const uint64_t z = h->max_nnz, M = h->m;
+  auto capk = [&](uint64_t k) { return std::min<uint64_t>(M, k * z); };
+  h->buf_cap = {capk(1), h->cap, h->cap};
+  auto merge = [](int a, int b, int out, uint64_t ac, uint64_t bc) {
+    return HcMerge{a, b, out, {-1, -1}, {-1, -1}, {0, 0}, ac, bc};
+  };
+  if (h->scheme == ZEN_SCHEME_HC) {
+    uint32_t L = 0;
+    while ((1u << L) < n) ++L;
+    int cur = kBufIn;
+    for (uint32_t s = 0; s < L; ++s) {
+      const uint32_t q = r ^ (1u << s);
+      const int out = (s & 1) ? kBufSt1 : kBufSt0;
+      HcStage st;
+      st.push.push_back({cur, q, s, capk(1ull << s)});
+      HcMerge mg = merge(cur, kBufRecv + int(s), out, capk(1ull << s), capk(1ull << s));
+      mg.wait[0] = int(s);
+      mg.done_rank[0] = int(q);
+      mg.done_idx[0] = int(s);  // q's s-th push
+      st.merge.push_back(mg);
+      h->plan.push_back(st);
+      h->buf_cap.push_back(capk(1ull << s));
+      cur = out;
+    }
+    h->result_buf = cur;
+  } else if (h->scheme == ZEN_SCHEME_RING) {
+    int tok = kBufIn;
+    for (uint32_t s = 0; s + 1 < n; ++s) {
+      const uint32_t next = (r + 1) % n, prev = (r + n - 1) % n;
+      const int out = (s & 1) ? kBufSt1 : kBufSt0;
+      HcStage st;
+      st.push.push_back({tok, next, s, capk(s + 1)});
+      // token'[w] = merge_sum(token[w-1], input[w]): the received token first
+      HcMerge mg = merge(kBufRecv + int(s), kBufIn, out, capk(s + 1), capk(1));
+      mg.wait[0] = int(s);
+      mg.done_rank[0] = int(prev);
+      mg.done_idx[0] = int(s);
+      st.merge.push_back(mg);
+      h->plan.push_back(st);
+      h->buf_cap.push_back(capk(s + 1));
+      tok = out;
+    }
+    h->result_buf = tok;
+  } else {  // AGsparse point-to-point: slot j holds worker j's input
+    HcStage st;
+    for (uint32_t q = 0; q < n; ++q)
+      if (q != r) st.push.push_back({kBufIn, q, r, capk(1)});
+    auto in_of = [&](uint32_t w) { return w == r ? kBufIn : kBufRecv + int(w); };
+    auto push_idx = [&](uint32_t sender) { return int(r < sender ? r : r - 1); };
+    int acc = in_of(0);
+    for (uint32_t w = 1; w < n; ++w) {
+      const int out = (w & 1) ? kBufSt0 : kBufSt1;
+      HcMerge mg = merge(acc, in_of(w), out, capk(w), capk(1));
+      int k = 0;
+      if (w == 1 && r != 0) {  // worker 0's input arrives too
+        mg.wait[k] = 0;
+        mg.done_rank[k] = 0;
+        mg.done_idx[k++] = push_idx(0);
+      }
+      if (w != r) {
+        mg.wait[k] = int(w);
+        mg.done_rank[k] = int(w);
+        mg.done_idx[k++] = push_idx(w);
+      }
+      st.merge.push_back(mg);
+      acc = out;
+    }
+    h->plan.push_back(st);
+    // every rank's arena must have the same layout: peers address it with
+    // their own offsets (this rank's own slot stays unused)
+    for (uint32_t j = 0; j < n; ++j) h->buf_cap.push_back(capk(1));
+    h->result_buf = acc;
+  }
+}
+
 zen_status hc_enqueue(zen_hc* h, const float* dense, const uint64_t* in_idx, const float* in_val,
                       uint64_t in_count) {
   cudaStream_t st = h->ctx->stream;
-  HcHdr* me = h->hdr(h->rank);
+  const uint32_t r = h->rank;
+  HcHdr* me = h->hdr(r);
   launch_hc_begin(&me->epoch, st);
   if (dense) {
-    launch_extract<uint64_t>(dense, h->m, h->ex, h->idx(h->rank, h->off_buf[0][0]),
-                             h->val(h->rank, h->off_buf[0][1]), &me->cnt[0], h->max_nnz, &me->err,
-                             st);
+    launch_extract<uint64_t>(dense, h->m, h->ex, h->idx(r, kBufIn), h->val(r, kBufIn),
+                             &me->cnt[kBufIn], h->max_nnz, &me->err, st);
   } else {
     if (in_count) {
-      CK(cudaMemcpyAsync(h->idx(h->rank, h->off_buf[0][0]), in_idx, in_count * 8,
-                         cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(h->val(h->rank, h->off_buf[0][1]), in_val, in_count * 4,
-                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(h->idx(r, kBufIn), in_idx, in_count * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(h->val(r, kBufIn), in_val, in_count * 4, cudaMemcpyDeviceToDevice, st));
     }
     launch_check_canonical(in_idx, in_count, h->m, &me->in_err, st);
-    launch_set_u64(&me->cnt[0], in_count, st);
+    launch_set_u64(&me->cnt[kBufIn], in_count, st);
   }
-  for (uint32_t s = 0; s < h->L; ++s) {
-    const uint32_t q = h->rank ^ (1u << s), in = s & 1, out = in ^ 1;
-    HcHdr* ph = h->hdr(q);
-    HcPushArgs p{};
-    p.src_idx = h->idx(h->rank, h->off_buf[in][0]);
-    p.src_val = h->val(h->rank, h->off_buf[in][1]);
-    p.src_cnt = &me->cnt[in];
-    p.dst_idx = h->idx(q, h->off_recv[s][0]);
-    p.dst_val = h->val(q, h->off_recv[s][1]);
-    p.dst_cnt = &ph->rcnt[s];
-    p.cap = h->stage_cap[s];
-    p.ready_flag = &ph->ready[s];
-    p.done_flag = &me->done[s];
-    p.epoch = &me->epoch;
-    p.ctl = h->ctl_push;
-    p.err = &me->err;
-    launch_hc_push(p, st);
-    HcMergeArgs a{};
-    a.a_idx = p.src_idx;
-    a.a_val = p.src_val;
-    a.a_cnt = p.src_cnt;
-    a.a_cap = h->stage_cap[s];
-    a.b_idx = h->idx(h->rank, h->off_recv[s][0]);
-    a.b_val = h->val(h->rank, h->off_recv[s][1]);
-    a.b_cnt = &me->rcnt[s];
-    a.b_cap = h->stage_cap[s];
-    a.o_idx = h->idx(h->rank, h->off_buf[out][0]);
-    a.o_val = h->val(h->rank, h->off_buf[out][1]);
-    a.o_cnt = &me->cnt[out];
-    a.o_cap = h->cap;
-    a.lb_status = h->lb;
-    a.ctl = h->ctl_merge;
-    a.err = &me->err;
-    a.wait_flag = &me->ready[s];
-    a.done_flag = &ph->done[s];
-    a.epoch = &me->epoch;
-    a.stage_cnt = &me->stage_cnt[s];
-    launch_hc_merge(a, hc_merge_tiles(2 * h->stage_cap[s]), st);
+  uint32_t pi = 0;
+  for (const HcStage& stg : h->plan) {
+    for (const HcPush& p : stg.push) {
+      HcPushArgs a{};
+      a.src_idx = h->idx(r, p.src);
+      a.src_val = h->val(r, p.src);
+      a.src_cnt = h->cntp(r, p.src);
+      a.dst_idx = h->idx(p.dst, kBufRecv + int(p.slot));
+      a.dst_val = h->val(p.dst, kBufRecv + int(p.slot));
+      a.dst_cnt = &h->hdr(p.dst)->rcnt[p.slot];
+      a.cap = p.cap;
+      a.ready_flag = &h->hdr(p.dst)->ready[p.slot];
+      a.done_flag = &me->done[pi];
+      a.epoch = &me->epoch;
+      a.ctl = h->ctl_push;
+      a.err = &me->err;
+      a.sent_cnt = &me->sent[pi++];
+      launch_hc_push(a, st);
+    }
+    for (const HcMerge& mg : stg.merge) {
+      HcMergeArgs a{};
+      a.a_idx = h->idx(r, mg.a);
+      a.a_val = h->val(r, mg.a);
+      a.a_cnt = h->cntp(r, mg.a);
+      a.a_cap = mg.a_cap;
+      a.b_idx = h->idx(r, mg.b);
+      a.b_val = h->val(r, mg.b);
+      a.b_cnt = h->cntp(r, mg.b);
+      a.b_cap = mg.b_cap;
+      a.o_idx = h->idx(r, mg.out);
+      a.o_val = h->val(r, mg.out);
+      a.o_cnt = h->cntp(r, mg.out);
+      a.o_cap = h->cap;
+      a.lb_status = h->lb;
+      a.ctl = h->ctl_merge;
+      a.err = &me->err;
+      a.wait_flag = mg.wait[0] >= 0 ? &me->ready[mg.wait[0]] : nullptr;
+      a.wait_flag2 = mg.wait[1] >= 0 ? &me->ready[mg.wait[1]] : nullptr;
+      a.done_flag = mg.done_rank[0] >= 0
+                        ? &h->hdr(uint32_t(mg.done_rank[0]))->done[mg.done_idx[0]] : nullptr;
+      a.done_flag2 = mg.done_rank[1] >= 0
+                         ? &h->hdr(uint32_t(mg.done_rank[1]))->done[mg.done_idx[1]] : nullptr;
+      a.epoch = &me->epoch;
+      launch_hc_merge(a, hc_merge_tiles(mg.a_cap + mg.b_cap), st);
+    }
   }
+  h->npush = pi;
   return ZEN_OK;
 }
 
@@ -2407,11 +2526,14 @@ void hc_drop_graph(zen_hc* h) {
 
 extern "C" {
 
-zen_status zen_hc_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t universe,
-                         uint64_t max_nnz, zen_hc** out) {
+zen_status zen_hc_create_scheme(zen_ctx* c, uint32_t scheme, uint32_t n, uint32_t rank,
+                                uint64_t universe, uint64_t max_nnz, zen_hc** out) {
   if (!c || !out) return fail(ZEN_E_INVALID, "null argument");
-  if (n == 0 || (n & (n - 1)) != 0) return fail(ZEN_E_INVALID, "node count must be a power of two");
-  if (n > (1u << kHcMaxStages)) return fail(ZEN_E_INVALID, "node count above 256");
+  if (scheme > ZEN_SCHEME_AGSPARSE) return fail(ZEN_E_INVALID, "unknown scheme");
+  const bool pow2 = n != 0 && (n & (n - 1)) == 0;
+  if (n == 0 || (scheme != ZEN_SCHEME_AGSPARSE && !pow2))
+    return fail(ZEN_E_INVALID, "node count must be a power of two");
+  if (n > kHcMaxRanks) return fail(ZEN_E_INVALID, "node count above 256");
   if (rank >= n) return fail(ZEN_E_INVALID, "rank out of range");
   if (universe == 0) return fail(ZEN_E_INVALID, "universe must be at least 1");
   if (max_nnz == 0) return fail(ZEN_E_INVALID, "max_nnz must be at least 1");
@@ -2419,25 +2541,21 @@ zen_status zen_hc_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
   SetupStream setup_(c->stream);
   std::unique_ptr<zen_hc> h(new zen_hc);
   h->ctx = c;
+  h->scheme = scheme;
   h->n = n;
   h->rank = rank;
   h->m = universe;
   h->max_nnz = std::min(max_nnz, universe);
-  while ((1u << h->L) < n) ++h->L;
   h->cap = std::min<uint64_t>(universe, uint64_t(n) * h->max_nnz);
+  hc_plan(h.get());
   size_t off = align256(sizeof(HcHdr));
-  for (int b = 0; b < 2; ++b) {
-    h->off_buf[b][0] = off;
-    off += align256(h->cap * 8);
-    h->off_buf[b][1] = off;
-    off += align256(h->cap * 4);
-  }
-  for (uint32_t s = 0; s < h->L; ++s) {
-    h->stage_cap[s] = std::min<uint64_t>(universe, (uint64_t(1) << s) * h->max_nnz);
-    h->off_recv[s][0] = off;
-    off += align256(h->stage_cap[s] * 8);
-    h->off_recv[s][1] = off;
-    off += align256(h->stage_cap[s] * 4);
+  h->off_idx.resize(h->buf_cap.size());
+  h->off_val.resize(h->buf_cap.size());
+  for (size_t b = 0; b < h->buf_cap.size(); ++b) {
+    h->off_idx[b] = off;
+    off += align256(h->buf_cap[b] * 8);
+    h->off_val[b] = off;
+    off += align256(h->buf_cap[b] * 4);
   }
   h->bytes = off;
   CK(cudaMalloc(&h->base, h->bytes));
@@ -2453,14 +2571,20 @@ zen_status zen_hc_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
   h->ex.nblk = (h->max_nnz + 255) / 256;
   CKR(h->mem.alloc(&h->ex.blk_tile, h->ex.nblk + 1));
   uint64_t max_tiles = 1;
-  for (uint32_t s = 0; s < h->L; ++s)
-    max_tiles = std::max<uint64_t>(max_tiles, hc_merge_tiles(2 * h->stage_cap[s]));
+  for (const auto& stg : h->plan)
+    for (const auto& mg : stg.merge)
+      max_tiles = std::max<uint64_t>(max_tiles, hc_merge_tiles(mg.a_cap + mg.b_cap));
   CKR(h->mem.alloc(&h->lb, max_tiles));
   CKR(h->mem.alloc(&h->ctl_merge, 1));
   CKR(h->mem.alloc(&h->ctl_push, 1));
   CK(cudaStreamSynchronize(c->stream));
   *out = h.release();
   return ZEN_OK;
+}
+
+zen_status zen_hc_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t universe,
+                         uint64_t max_nnz, zen_hc** out) {
+  return zen_hc_create_scheme(c, ZEN_SCHEME_HC, n, rank, universe, max_nnz, out);
 }
 
 void zen_hc_destroy(zen_hc* h) {
@@ -2487,9 +2611,14 @@ zen_status zen_hc_connect(zen_hc* h, const void* handles) {
   if (!h || !handles) return fail(ZEN_E_INVALID, "null argument");
   DevGuard g(h->ctx->device);
   const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
-  // only the log2(n) partners are ever touched
-  for (uint32_t s = 0; s < h->L; ++s) {
-    const uint32_t r = h->rank ^ (1u << s);
+  std::vector<uint32_t> need;  // only the ranks the plan touches
+  for (const auto& stg : h->plan) {
+    for (const auto& p : stg.push) need.push_back(p.dst);
+    for (const auto& mg : stg.merge)
+      for (int k = 0; k < 2; ++k)
+        if (mg.done_rank[k] >= 0) need.push_back(uint32_t(mg.done_rank[k]));
+  }
+  for (uint32_t r : need) {
     if (h->peer[r]) continue;
     void* p = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess);
@@ -2558,11 +2687,16 @@ zen_status zen_hc_wait(zen_hc* h) {
     const uint32_t e = hh.err, ie = hh.in_err;
     uint32_t zero[2] = {0, 0};
     CK(cudaMemcpy(&h->hdr(h->rank)->err, zero, 8, cudaMemcpyHostToDevice));
-    if (e & kErrTimeout) return fail(ZEN_E_TIMEOUT, "a hierarchy partner never signalled");
+    if (e & kErrTimeout) return fail(ZEN_E_TIMEOUT, "a scheme partner never signalled");
     if (ie) return fail(ZEN_E_INVALID, "tensor indices not sorted/unique or >= M");
-    return fail(ZEN_E_CAPACITY, "non-zeros above max_nnz");
+    if (e & kErrOutside) return fail(ZEN_E_INVALID, "a fold saw unsorted input (err bits " + std::to_string(e) + ")");
+    std::string c = "non-zeros above capacity (counts: input " + std::to_string(hh.cnt[0]) +
+                    ", states " + std::to_string(hh.cnt[1]) + "/" + std::to_string(hh.cnt[2]) +
+                    ", received";
+    for (uint32_t j = 0; j < h->nslots_used(); ++j) c += " " + std::to_string(hh.rcnt[j]);
+    return fail(ZEN_E_CAPACITY, c + "; max_nnz " + std::to_string(h->max_nnz) + ")");
   }
-  h->h_result = hh.cnt[h->L & 1];
+  h->h_result = h->result_buf < kBufRecv ? hh.cnt[h->result_buf] : 0;
   return ZEN_OK;
 }
 
@@ -2570,9 +2704,8 @@ zen_status zen_hc_result(zen_hc* h, const uint64_t** d_idx, const float** d_val,
                          uint64_t* count) {
   if (!h) return fail(ZEN_E_INVALID, "null argument");
   CKR(zen_hc_wait(h));
-  const uint32_t b = h->L & 1;
-  if (d_idx) *d_idx = h->idx(h->rank, h->off_buf[b][0]);
-  if (d_val) *d_val = h->val(h->rank, h->off_buf[b][1]);
+  if (d_idx) *d_idx = h->idx(h->rank, h->result_buf);
+  if (d_val) *d_val = h->val(h->rank, h->result_buf);
   if (count) *count = h->h_result;
   return ZEN_OK;
 }
@@ -2598,8 +2731,17 @@ zen_status zen_hc_stage_counts(zen_hc* h, uint64_t* counts) {
   CKR(zen_hc_wait(h));
   HcHdr hh;
   CK(cudaMemcpy(&hh, h->base, sizeof(HcHdr), cudaMemcpyDeviceToHost));
-  for (uint32_t s = 0; s < h->L; ++s) counts[s] = hh.stage_cnt[s];
+  uint32_t i = 0;
+  for (const auto& stg : h->plan)
+    for (size_t k = 0; k < stg.push.size(); ++k, ++i) counts[i] = hh.sent[i];
   return ZEN_OK;
+}
+
+uint32_t zen_hc_pushes(const zen_hc* h) {
+  uint32_t c = 0;
+  if (h)
+    for (const auto& stg : h->plan) c += uint32_t(stg.push.size());
+  return c;
 }
 
 }  // extern "C"

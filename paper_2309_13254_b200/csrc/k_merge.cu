@@ -89,8 +89,10 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_merge(HcMergeArgs a) {
   __shared__ uint64_t s_excl;
   const uint32_t tid = threadIdx.x;
   const uint64_t ep = a.epoch ? *(volatile const unsigned long long*)a.epoch : 0;
-  if (a.wait_flag && tid == 0 && !wait_flag(a.wait_flag, ep, kPeerTimeoutNs))
-    atomicOr(a.err, kErrTimeout);
+  if (tid == 0) {
+    if (a.wait_flag && !wait_flag(a.wait_flag, ep, kPeerTimeoutNs)) atomicOr(a.err, kErrTimeout);
+    if (a.wait_flag2 && !wait_flag(a.wait_flag2, ep, kPeerTimeoutNs)) atomicOr(a.err, kErrTimeout);
+  }
   const uint32_t tile = take_ticket(a.ctl, &s_tile);  // also orders the wait above
   const uint32_t tag = *(volatile uint32_t*)&a.ctl->tag;
   uint64_t na = *(volatile const uint64_t*)a.a_cnt, nb = *(volatile const uint64_t*)a.b_cnt;
@@ -244,9 +246,10 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_merge(HcMergeArgs a) {
       *a.o_cnt = total;  // the true size; readers clamp to their capacity
     }
   }
-  if (finish_tile(a.ctl, gridDim.x, /*sys=*/a.done_flag != nullptr) && a.done_flag && tid == 0) {
-    __threadfence_system();
-    st_release_sys(a.done_flag, ep);
+  if (finish_tile(a.ctl, gridDim.x, /*sys=*/a.done_flag != nullptr) && tid == 0) {
+    if (a.done_flag || a.done_flag2) __threadfence_system();
+    if (a.done_flag) st_release_sys(a.done_flag, ep);
+    if (a.done_flag2) st_release_sys(a.done_flag2, ep);
   }
 }
 
@@ -294,7 +297,10 @@ __global__ void __launch_bounds__(256) k_hc_push(HcPushArgs a) {
   if (blockIdx.x == 0) {
     if (tid == 0 && (n & 1)) a.dst_idx[n - 1] = a.src_idx[n - 1];
     if (tid < (n & 3)) a.dst_val[(n4 << 2) + tid] = a.src_val[(n4 << 2) + tid];
-    if (tid == 0) *a.dst_cnt = n;
+    if (tid == 0) {
+      *a.dst_cnt = n;
+      if (a.sent_cnt) *a.sent_cnt = n;
+    }
   }
   if (finish_tile(a.ctl, gridDim.x, /*sys=*/true) && tid == 0) {
     __threadfence_system();

@@ -319,10 +319,12 @@ struct HcMergeArgs {
   unsigned long long* lb_status;  // look-back words, one per tile
   LookbackCtl* ctl;
   uint32_t* err;                        // kErr* bits (kErrOutside: unsorted input)
-  const unsigned long long* wait_flag;  // local ready flag (nullptr: none)
-  unsigned long long* done_flag;        // the partner's done flag (nullptr: none)
-  const unsigned long long* epoch;      // local sync counter (nullptr: 0)
-  uint64_t* stage_cnt;                  // receives |a| (the ledger), may be null
+  const unsigned long long* wait_flag;   // local ready flags to acquire (nullptr: none)
+  const unsigned long long* wait_flag2;
+  unsigned long long* done_flag;         // senders' done flags to release (nullptr: none)
+  unsigned long long* done_flag2;
+  const unsigned long long* epoch;       // local sync counter (nullptr: 0)
+  uint64_t* stage_cnt;                   // receives |a| (the ledger), may be null
 };
 struct HcPushArgs {
   const uint64_t* src_idx;
@@ -337,6 +339,7 @@ struct HcPushArgs {
   const unsigned long long* epoch;
   LookbackCtl* ctl;
   uint32_t* err;
+  uint64_t* sent_cnt;  // receives the pushed count (the ledger)
 };
 uint32_t hc_merge_tiles(uint64_t max_entries);
 void launch_hc_merge(const HcMergeArgs& a, uint32_t tiles, cudaStream_t stream);

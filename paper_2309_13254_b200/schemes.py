@@ -396,17 +396,27 @@ class HCSynchronizer:
     Counts stay on the device; sync_dense replays one CUDA graph.  Every rank
     ends with aggregate(inputs), bit for bit."""
 
+    SCHEMES = {"hc": 0, "ring": 1, "agsparse": 2}
+
     def __init__(self, n: int, universe: int, rank: int, max_nnz: int,
-                 fmt: WireFormat | None = None, device: int | None = None):
-        if not _pow2(n):
+                 fmt: WireFormat | None = None, device: int | None = None,
+                 scheme: str = "hc"):
+        """scheme: "hc" (run_hier_centralization), "ring"
+        (run_ring_centralization) or "agsparse" (run_agsparse point-to-point,
+        any n) -- the same NVLink push + device fold machinery."""
+        if scheme not in self.SCHEMES:
+            raise Error(f"unknown scheme {scheme}")
+        if scheme != "agsparse" and not _pow2(n):
             raise NonPowerOfTwo()
         if fmt is not None and fmt.kind not in ("coo", "bitmap"):
-            raise Error("rank-mode hierarchy ledger supports COO and bitmap formats")
+            raise Error("rank-mode ledger supports COO and bitmap formats")
         self.n, self.m, self.rank, self.max_nnz = n, universe, rank, max_nnz
+        self.scheme = scheme
         self.fmt = fmt or WireFormat.coo()
         self.ctx = context(device)
         self.h = C.c_void_p()
-        _check(_lib().zen_hc_create(self.ctx.h, n, rank, universe, max_nnz, C.byref(self.h)))
+        _check(_lib().zen_hc_create_scheme(self.ctx.h, self.SCHEMES[scheme], n, rank, universe,
+                                           max_nnz, C.byref(self.h)))
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -464,9 +474,10 @@ class HCSynchronizer:
         return oi[:z], ov[:z]
 
     def stage_bits(self):
-        """[(index_bits, value_bits)] this rank sent per stage (the SimNet
-        ledger row of run_hier_centralization, schemes.hpp:183-185)."""
-        ns = self.n.bit_length() - 1
+        """[(index_bits, value_bits)] this rank sent per push, in plan order
+        (HC / ring: one per stage; AGsparse: one per peer) -- its row of the
+        scheme's SimNet ledger."""
+        ns = _lib().zen_hc_pushes(self.h)
         out = (C.c_uint64 * max(ns, 1))()
         _check(_lib().zen_hc_stage_counts(self.h, out))
         res = []

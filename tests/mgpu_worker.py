@@ -100,6 +100,27 @@ def main():
             print(f"RANK {rank} HC sparse MISMATCH", flush=True)
             ok = False
         del hc
+    # the centralized baselines in rank mode (f4): ring centralization and
+    # AGsparse point-to-point, same push + fold machinery
+    sparse_in = [co.to_sparse(d) for d in dense]
+    for scheme, name in [("ring", "ring-centralization"), ("agsparse", "agsparse")]:
+        if scheme == "ring" and world & (world - 1):
+            continue
+        sy = zen.HCSynchronizer(world, m, rank, max_nnz=per * width + 1024, scheme=scheme)
+        sy.connect_process_group()
+        res, led, _ = co.run_scheme(name, m, sparse_in)
+        for it in range(2):
+            sy.sync_dense(mine)
+            gi, gv = sy.result()
+            good = np.array_equal(gi.cpu().numpy().view(np.uint64), res[rank][0]) and \
+                np.array_equal(gv.cpu().numpy().view(np.uint32), res[rank][1].view(np.uint32))
+            sent = sum(ib + vb for ib, vb in sy.stage_bits())
+            good = good and sent == int(led[:, 0, rank].sum())
+            if not good:
+                print(f"RANK {rank} {scheme} iter {it} MISMATCH {gi.numel()} vs {res[rank][0].size}",
+                      flush=True)
+                ok = False
+        del sy
     flag = torch.tensor([0 if ok else 1], device="cuda" if world <= ngpu else "cpu")
     dist.all_reduce(flag)
     if rank == 0:

@@ -92,6 +92,16 @@ def main():
             out["hc_equals_bp"] = bool(torch.equal(hi, bi) and torch.equal(hv.view(torch.int32),
                                                                            bv.view(torch.int32)))
             out["hc_sent_bits_rank0"] = [ib + vb for ib, vb in hc.stage_bits()]
+        for scheme in ["ring", "agsparse"]:
+            if scheme == "ring" and world & (world - 1):
+                continue
+            sy = zen.HCSynchronizer(world, m, rank, max_nnz=per * width + 4096, scheme=scheme)
+            sy.connect_process_group()
+            out[f"{scheme}_ms"] = timed(lambda: sy.sync_dense(mine), sy.wait)
+            si, sv = sy.result()
+            bi, bv = bp.result()
+            out[f"{scheme}_equals_bp_indices"] = bool(torch.equal(si, bi))
+            del sy
     # merge throughput + profile on rank 0's device
     sp = [zen.to_sparse(torch.from_numpy(bench.dense_gradient(rows, width, live[w], 3 + w)).cuda())
           for w in range(n)]
