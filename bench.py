@@ -254,6 +254,62 @@ def exchange_report(ledger, n, stage_ms):
 
 # ------------------------------------------------------------ extras (f1/f2) ----
 
+def compare_schemes(args, zen, d_dense, m, z, n, rank, stream, barrier, dist):
+    """BP vs the centralized schemes on this run's gradients, one process per
+    GPU: device time of K syncs (CUDA events, max over ranks); result
+    indices checked equal to BP's on every rank."""
+    import torch
+    from paper_2309_13254_b200 import schemes as sch
+    out = {}
+    k = max(5, min(args.steps, 20))
+    counts = None
+    for name in ["hc", "ring", "agsparse"]:
+        if name != "agsparse" and n & (n - 1):
+            continue
+        sy = sch.HCSynchronizer(n, m, rank, max_nnz=int(z * 1.25) + 4096, scheme=name)
+        sy.connect_process_group()
+        for _ in range(3):
+            sy.sync_dense(d_dense)
+        sy.wait()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(k):
+            sy.sync_dense(d_dense)
+        a1.record(stream)
+        barrier()
+        sy.wait()
+        t = torch.tensor([a0.elapsed_time(a1) / k], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        si, _ = sy.result()
+        entry = {"ms": round(float(t[0]), 4), "result_nnz": int(si.numel())}
+        if name == "hc":
+            counts = sy.stage_bits()  # (index, value) bits sent per stage
+        out[name] = entry
+        del sy
+    # densification ladder from rank 0's HC: state s covers ranks [0, 2^s)
+    if counts is not None:
+        nnz = torch.tensor([float(z)], device="cuda", dtype=torch.float64)
+        alln = [torch.zeros_like(nnz) for _ in range(n)]
+        dist.all_gather(alln, nnz)
+        d = [float(x[0]) / float(m) for x in alln]
+        union = [c[1] // 32 for c in counts] + [out["hc"]["result_nnz"]]  # |U_1|, |U_2|, ..
+        gamma = {1: 1.0}
+        kk = 2
+        for u in union[1:]:
+            gamma[kk] = (float(u) / float(m)) / (sum(d[:kk]) / float(kk))
+            kk *= 2
+        g = torch.tensor([gamma[kk] for kk in sorted(gamma)], device="cuda", dtype=torch.float64)
+        dist.broadcast(g, 0)
+        gamma = {kk: float(x) for kk, x in zip(sorted(gamma), g.cpu().numpy())}
+        prof = sch.SparsityProfile(sum(d) / n, gamma, {})
+        out["gamma"] = {str(kk): round(v, 4) for kk, v in gamma.items()}
+        out["select_scheme"] = sch.select_scheme(prof, n)
+        out["t_bp_coefficient"] = round(sch.t_bp_coefficient(n, gamma[n]), 4)
+        out["t_hc_coefficient"] = round(sch.t_hc_coefficient(n, gamma), 4)
+    return out
+
+
 def measure_extras(args, zen, d_dense, peak, reps=10):
     """The components either side of the sync: top-k
     sparsification of the dense gradient (f2) and the COO / tensor-block wire
@@ -500,6 +556,14 @@ def main():
                "d2h_bytes_per_step": 12 * got * n,
                "path": "zen_bp_sync_host (C-ABI): pinned host dense -> device -> host result"}
 
+    # the paper's comparison at N > 1: the same
+    # gradients through Hierarchical Centralization, ring centralization and
+    # AGsparse in rank mode, and select_scheme's choice from the measured
+    # densification ladder (rank 0's HC stage counts are the prefix unions)
+    schemes = None
+    if dist and not args.no_extras:
+        schemes = compare_schemes(args, zen, d_dense, m, z, n, rank, stream, barrier, dist)
+
     # extra: n workers emulated on one GPU (local mode), e.g. the 8-worker headline
     emu = None
     if args.emulate and rank == 0 and world == 1:
@@ -587,6 +651,9 @@ def main():
         line["emulated_local"] = emu
     if world == 1 and not args.no_extras:
         line["extras"] = measure_extras(args, zen, d_dense, peak)
+    if schemes is not None:
+        line["schemes"] = dict(schemes, bp_ms=round(ms, 4),
+                               note="rank mode, same gradients; CUDA events, max over ranks")
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_reference_step(args, n, [host])
     print(json.dumps(line), flush=True)
