@@ -30,6 +30,9 @@
 //   zen::SparsityProfile, profile_sparsity,     zen_b200::(same names)
 //   select_scheme, t_bp/t_hc[_coefficient] (costmodel.hpp)
 //   zen::run_hier_centralization (schemes.hpp:173) zen_b200::run_hier_centralization
+//   zen::run_agsparse / run_ring_centralization / run_omnireduce_like,
+//   SchemeConfig, run_scheme, scheme_config_from_name (schemes.hpp:21-470)
+//                                               zen_b200::(same names)
 //
 // Host containers stay std::vector (value semantics, as in the reference); the
 // device copies are made per call.  For a device-resident, allocation-free
@@ -102,6 +105,12 @@ class UnbalancedLedger : public Error {
 class NonPowerOfTwo : public Error {  // errors.hpp:42-46
  public:
   explicit NonPowerOfTwo(const std::string& what = "node count must be a power of two")
+      : Error(what) {}
+};
+
+class UnsupportedCombination : public Error {  // errors.hpp:48-52
+ public:
+  explicit UnsupportedCombination(const std::string& what = "unsupported scheme configuration")
       : Error(what) {}
 };
 
@@ -1007,6 +1016,265 @@ inline SyncOutcome run_hier_centralization(const std::vector<SparseTensor>& inpu
   for (const auto& st : states) out.results.push_back(st.host());
   out.traffic = net.finalize();
   return out;
+}
+
+// ---- the design space: zen/schemes.hpp:21-41, 119-168, 194-328, 418-470 -----
+enum class CommPattern { Ring, Hierarchy, PointToPoint };
+enum class Aggregation { Incremental, OneShot };
+enum class PartitionPattern { Centralization, Parallelism };
+enum class BalancePattern { Balanced, Imbalanced, NotApplicable };
+
+struct SchemeConfig {
+  CommPattern communication = CommPattern::PointToPoint;
+  Aggregation aggregation = Aggregation::OneShot;
+  PartitionPattern partition = PartitionPattern::Centralization;
+  BalancePattern balance = BalancePattern::NotApplicable;
+  WireFormat format = WireFormat::coo();
+  void validate() const {
+    const bool centralized = partition == PartitionPattern::Centralization;
+    if (centralized != (balance == BalancePattern::NotApplicable))
+      throw UnsupportedCombination(
+          "the balance dimension applies exactly when the partition pattern is Parallelism");
+  }
+};
+
+struct RunParams {
+  HashParams hash;
+};
+
+namespace detail {
+inline void check_scheme_inputs(const std::vector<SparseTensor>& inputs, const SimNet& net) {
+  if (inputs.size() < 2) throw Error("synchronization needs at least two nodes");
+  if (inputs.size() != net.nodes()) throw Error("input count must match the network size");
+  for (const auto& t : inputs)
+    if (t.universe() != inputs.front().universe()) throw UniverseMismatch();
+}
+// message_sizes of a device tensor (codec.hpp:182-211)
+inline EncodedMessage sized(const DevTensor& t, const WireFormat& fmt) {
+  EncodedMessage msg;
+  msg.format = fmt;
+  msg.universe_size = t.m;
+  msg.count = t.n;
+  msg.value_bits = 32 * t.n;
+  if (fmt.kind == WireKind::Coo) {
+    msg.index_bits = uint64_t(fmt.coo_index_bits) * t.n;
+  } else if (fmt.kind == WireKind::Bitmap) {
+    msg.index_bits = t.m;
+  } else if (fmt.kind == WireKind::HashBitmap) {
+    throw Error("hash bitmap requires a hash universe");
+  } else {
+    zen_wire_format f = wire_c(fmt);
+    zen_message_info info{};
+    const zen_status rc =
+        zen_encode(ctx(), &f, nullptr, 0, t.idx->p, t.val->p, t.n, t.m, nullptr, 0, &info);
+    if (rc != ZEN_OK && rc != ZEN_E_CAPACITY) check(rc);
+    msg.count = info.count;
+    msg.index_bits = info.index_bits;
+    msg.value_bits = info.value_bits;
+  }
+  return msg;
+}
+inline DevTensor fold(const std::vector<const DevTensor*>& parts) {
+  DevTensor acc = merge_dev(*parts[0], DevTensor(SparseTensor(parts[0]->m, {}, {})));
+  for (size_t i = 1; i < parts.size(); ++i) acc = merge_dev(acc, *parts[i]);
+  return acc;
+}
+inline DevTensor slice(const DevTensor& t, uint64_t at, uint64_t count) {
+  DevTensor s;
+  s.m = t.m;
+  s.n = count;
+  s.idx.reset(new DBuf<uint64_t>(count));
+  s.val.reset(new DBuf<float>(count));
+  if (count) {
+    cudaMemcpy(s.idx->p, t.idx->p + at, count * 8, cudaMemcpyDeviceToDevice);
+    cudaMemcpy(s.val->p, t.val->p + at, count * 4, cudaMemcpyDeviceToDevice);
+  }
+  return s;
+}
+}  // namespace detail
+
+// zen::run_agsparse (schemes.hpp:119-168)
+inline SyncOutcome run_agsparse(const std::vector<SparseTensor>& inputs, SimNet& net,
+                                CommPattern pattern = CommPattern::PointToPoint,
+                                WireFormat fmt = WireFormat::coo()) {
+  detail::check_scheme_inputs(inputs, net);
+  const uint32_t n = uint32_t(inputs.size());
+  std::vector<detail::DevTensor> ins;
+  for (const auto& t : inputs) ins.emplace_back(t);
+  std::vector<EncodedMessage> msg;
+  for (const auto& t : ins) msg.push_back(detail::sized(t, fmt));
+  if (pattern == CommPattern::PointToPoint) {
+    for (uint32_t w = 0; w < n; ++w)
+      for (uint32_t to = 0; to < n; ++to)
+        if (to != w) net.send(0, w, to, msg[w]);
+  } else if (pattern == CommPattern::Ring) {
+    if (!detail::is_pow2(n)) throw NonPowerOfTwo();
+    for (uint32_t s = 0; s + 1 < n; ++s)
+      for (uint32_t w = 0; w < n; ++w) net.send(s, w, (w + 1) % n, msg[(w + n - s) % n]);
+  } else {
+    if (!detail::is_pow2(n)) throw NonPowerOfTwo();
+    std::vector<std::vector<uint32_t>> hold(n);
+    for (uint32_t w = 0; w < n; ++w) hold[w] = {w};
+    for (uint32_t bit = 1, stage = 0; bit < n; bit <<= 1, ++stage) {
+      auto prev = hold;
+      for (uint32_t w = 0; w < n; ++w) {
+        for (uint32_t id : prev[w]) net.send(stage, w, w ^ bit, msg[id]);
+        hold[w].insert(hold[w].end(), prev[w ^ bit].begin(), prev[w ^ bit].end());
+      }
+    }
+  }
+  std::vector<const detail::DevTensor*> ps;
+  for (const auto& t : ins) ps.push_back(&t);
+  SyncOutcome out;
+  out.results.assign(n, detail::fold(ps).host());
+  out.traffic = net.finalize();
+  return out;
+}
+
+// zen::run_ring_centralization (schemes.hpp:194-215)
+inline SyncOutcome run_ring_centralization(const std::vector<SparseTensor>& inputs, SimNet& net,
+                                           WireFormat fmt = WireFormat::coo()) {
+  detail::check_scheme_inputs(inputs, net);
+  if (!detail::is_pow2(inputs.size())) throw NonPowerOfTwo();
+  const uint32_t n = uint32_t(inputs.size());
+  std::vector<detail::DevTensor> ins, tok;
+  for (const auto& t : inputs) ins.emplace_back(t);
+  for (const auto& t : inputs) tok.emplace_back(t);
+  for (uint32_t s = 0; s + 1 < n; ++s) {
+    for (uint32_t w = 0; w < n; ++w) net.send(s, w, (w + 1) % n, detail::sized(tok[w], fmt));
+    std::vector<detail::DevTensor> next;
+    for (uint32_t w = 0; w < n; ++w) next.push_back(detail::merge_dev(tok[(w + n - 1) % n], ins[w]));
+    tok = std::move(next);
+  }
+  SyncOutcome out;
+  for (const auto& t : tok) out.results.push_back(t.host());
+  out.traffic = net.finalize();
+  return out;
+}
+
+// zen::run_omnireduce_like (schemes.hpp:219-328)
+inline SyncOutcome run_omnireduce_like(const std::vector<SparseTensor>& inputs, SimNet& net,
+                                       uint32_t block_size = 256) {
+  detail::check_scheme_inputs(inputs, net);
+  if (block_size < 1) throw Error("block size must be at least 1");
+  const uint32_t n = uint32_t(inputs.size());
+  const uint64_t m = inputs.front().universe(), range = (m + n - 1) / n;
+  std::vector<std::vector<detail::DevTensor>> sl(n);
+  for (uint32_t w = 0; w < n; ++w) {
+    detail::DevTensor t(inputs[w]);
+    const auto cnt = detail::range_counts(t, n);
+    uint64_t at = 0;
+    for (uint32_t p = 0; p < n; ++p) {
+      sl[w].push_back(detail::slice(t, at, cnt[p]));
+      at += cnt[p];
+    }
+  }
+  auto blocks = [&](const detail::DevTensor& t, uint32_t p) {
+    EncodedMessage msg;
+    msg.format = WireFormat::tensor_block(block_size);
+    msg.universe_size = m;
+    if (!t.n) return msg;
+    const uint64_t lo = uint64_t(p) * range, hi = std::min(m, lo + range);
+    uint64_t nb = 0, last = 0;
+    detail::check(zen_count_blocks(detail::ctx(), t.idx->p, t.n, lo, block_size, &nb));
+    cudaMemcpy(&last, t.idx->p + t.n - 1, 8, cudaMemcpyDeviceToHost);
+    const uint64_t lb = (last - lo) / block_size, end = lo + (lb + 1) * block_size;
+    msg.count = nb;
+    msg.index_bits = 64 * nb;
+    msg.value_bits = 32 * block_size * nb - (end > hi ? 32 * (end - hi) : 0);
+    return msg;
+  };
+  for (uint32_t w = 0; w < n; ++w)
+    for (uint32_t p = 0; p < n; ++p)
+      if (p != w && sl[w][p].n) net.send(0, w, p, blocks(sl[w][p], p));
+  std::vector<detail::DevTensor> agg;
+  for (uint32_t p = 0; p < n; ++p) {
+    std::vector<const detail::DevTensor*> ps;
+    for (uint32_t w = 0; w < n; ++w) ps.push_back(&sl[w][p]);
+    agg.push_back(detail::fold(ps));
+  }
+  for (uint32_t p = 0; p < n; ++p) {
+    if (!agg[p].n) continue;
+    const EncodedMessage msg = blocks(agg[p], p);
+    for (uint32_t w = 0; w < n; ++w)
+      if (w != p) net.send(1, p, w, msg);
+  }
+  uint64_t total = 0;
+  for (const auto& a : agg) total += a.n;
+  detail::DBuf<uint64_t> ci(total);
+  detail::DBuf<float> cv(total);
+  uint64_t at = 0;
+  for (const auto& a : agg) {
+    if (a.n) {
+      cudaMemcpy(ci.p + at, a.idx->p, a.n * 8, cudaMemcpyDeviceToDevice);
+      cudaMemcpy(cv.p + at, a.val->p, a.n * 4, cudaMemcpyDeviceToDevice);
+    }
+    at += a.n;
+  }
+  detail::DBuf<uint64_t> oi(total);
+  detail::DBuf<float> ov(total);
+  uint64_t kept = 0;
+  detail::check(zen_compact_nonzero(detail::ctx(), ci.p, cv.p, total, oi.p, ov.p, &kept));
+  SyncOutcome out;
+  out.results.assign(n, SparseTensor(m, oi.host(kept), ov.host(kept)));
+  bool loaded = true;
+  for (const auto& t : inputs) loaded = loaded && !t.empty();
+  if (loaded) {  // imbalance_push / imbalance_pull (hashing.hpp:296-320)
+    BalanceDetails b;
+    double worst = 0.0;
+    for (uint32_t w = 0; w < n; ++w)
+      for (uint32_t p = 0; p < n; ++p)
+        worst = std::max(worst, double(n) * double(sl[w][p].n) / double(inputs[w].nnz()));
+    b.push_imbalance = worst;
+    worst = 0.0;
+    for (const auto& a : agg) worst = std::max(worst, double(n) * double(a.n) / double(total));
+    b.pull_imbalance = worst;
+    out.balance = b;
+  }
+  out.traffic = net.finalize();
+  return out;
+}
+
+// zen::run_scheme (schemes.hpp:420-442)
+inline SyncOutcome run_scheme(const SchemeConfig& cfg, const std::vector<SparseTensor>& inputs,
+                              SimNet& net, const RunParams& params = {}) {
+  cfg.validate();
+  if (cfg.partition == PartitionPattern::Centralization) {
+    if (cfg.aggregation == Aggregation::OneShot)
+      return run_agsparse(inputs, net, cfg.communication, cfg.format);
+    if (cfg.communication == CommPattern::Hierarchy)
+      return run_hier_centralization(inputs, net, cfg.format);
+    if (cfg.communication == CommPattern::Ring)
+      return run_ring_centralization(inputs, net, cfg.format);
+    throw UnsupportedCombination("point-to-point incremental centralization is not implemented");
+  }
+  if (cfg.communication == CommPattern::PointToPoint) {
+    if (cfg.aggregation == Aggregation::OneShot && cfg.balance == BalancePattern::Imbalanced &&
+        cfg.format.kind == WireKind::TensorBlock)
+      return run_omnireduce_like(inputs, net, cfg.format.block_size);
+    if (cfg.aggregation == Aggregation::Incremental && cfg.balance == BalancePattern::Balanced)
+      return run_balanced_parallelism(inputs, net, params.hash);
+  }
+  throw UnsupportedCombination("no implemented scheme matches this configuration");
+}
+
+// zen::scheme_config_from_name / known_scheme_names (schemes.hpp:445-470)
+inline SchemeConfig scheme_config_from_name(const std::string& name) {
+  using C = CommPattern;
+  using A = Aggregation;
+  using P = PartitionPattern;
+  using B = BalancePattern;
+  if (name == "agsparse") return {C::PointToPoint, A::OneShot, P::Centralization, B::NotApplicable, WireFormat::coo()};
+  if (name == "sparcml") return {C::Hierarchy, A::Incremental, P::Centralization, B::NotApplicable, WireFormat::coo()};
+  if (name == "ring-centralization") return {C::Ring, A::Incremental, P::Centralization, B::NotApplicable, WireFormat::coo()};
+  if (name == "omnireduce") return {C::PointToPoint, A::OneShot, P::Parallelism, B::Imbalanced, WireFormat::tensor_block()};
+  if (name == "balanced-parallelism") return {C::PointToPoint, A::Incremental, P::Parallelism, B::Balanced, WireFormat::hash_bitmap()};
+  throw UnsupportedCombination("unknown scheme name: " + name);
+}
+inline const std::vector<std::string>& known_scheme_names() {
+  static const std::vector<std::string> names = {"agsparse", "sparcml", "ring-centralization",
+                                                 "omnireduce", "balanced-parallelism"};
+  return names;
 }
 
 }  // namespace zen_b200

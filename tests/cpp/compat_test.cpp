@@ -551,6 +551,130 @@ TEST(ProfileSparsity_MatchesItsDefinition) {
   EXPECT(m.nnz() == inputs[0].nnz() + inputs[1].nnz() - uint64_t(std::llround(common)));
 }
 
+// ---- schemes_test.cpp: AgSparse, RingCentralization, OmniReduce, RunScheme ----
+static void expect_exact(const z::SyncOutcome& out, const std::vector<z::SparseTensor>& in) {
+  const auto want = z::aggregate(in);  // integer-valued workloads: every order sums exactly
+  EXPECT(out.results.size() == in.size());
+  for (const auto& r : out.results) EXPECT(r == want);
+}
+
+TEST(AgSparse_TwoDisjointNodesReceiveEachOthersPayload) {
+  z::SparseTensor a(100, {1, 2, 3}, {1, 1, 1}), b(100, {10, 11}, {2, 2});
+  z::SimNet net(2, 1.0);
+  auto out = z::run_agsparse({a, b}, net);
+  expect_exact(out, {a, b});
+  EXPECT(out.traffic.stages[0].recv_bits[0] == 2u * 96);
+  EXPECT(out.traffic.stages[0].recv_bits[1] == 3u * 96);
+}
+
+TEST(AgSparse_AllPatternsMoveTheSameBitsAndAgree) {
+  auto inputs = workload(8, 5000, 0.01, 0.3, 7);
+  std::vector<uint64_t> totals;
+  for (auto pat : {z::CommPattern::PointToPoint, z::CommPattern::Ring, z::CommPattern::Hierarchy}) {
+    z::SimNet net(8, 1.0);
+    auto out = z::run_agsparse(inputs, net, pat);
+    expect_exact(out, inputs);
+    totals.push_back(out.traffic.total_recv_bits);
+  }
+  EXPECT(totals[0] == totals[1] && totals[0] == totals[2]);
+}
+
+TEST(AgSparse_ReceivedBitsGrowLinearlyInN) {
+  std::vector<double> per_node;
+  for (uint32_t n : {4u, 8u, 16u}) {
+    auto inputs = workload(n, 100000, 0.005, 0.5, 11);
+    z::SimNet net(n, 1.0);
+    per_node.push_back(double(z::run_agsparse(inputs, net).traffic.total_recv_bits) / n);
+  }
+  EXPECT(std::fabs(per_node[1] / per_node[0] - 7.0 / 3.0) < 0.01);
+  EXPECT(std::fabs(per_node[2] / per_node[1] - 15.0 / 7.0) < 0.01);
+}
+
+TEST(RingCentralization_FullOverlapReceivesCommonSetNMinusOneTimes) {
+  auto inputs = workload(4, 1000, 0.05, 1.0, 29);
+  const uint64_t zz = inputs[0].nnz();
+  z::SimNet net(4, 1.0);
+  auto out = z::run_ring_centralization(inputs, net);
+  expect_exact(out, inputs);
+  EXPECT(out.traffic.stages.size() == 3u);
+  for (uint32_t node = 0; node < 4; ++node) {
+    uint64_t total = 0;
+    for (const auto& st : out.traffic.stages) total += st.recv_bits[node];
+    EXPECT(total == 3 * zz * 96);
+  }
+}
+
+TEST(RingCentralization_StageDensityFollowsTheWindow) {
+  std::vector<z::SparseTensor> inputs;
+  for (uint64_t i = 0; i < 4; ++i) inputs.push_back(z::SparseTensor(100, {i * 10, i * 10 + 1}, {1, 1}));
+  z::SimNet net(4, 1.0);
+  auto out = z::run_ring_centralization(inputs, net);
+  expect_exact(out, inputs);
+  for (uint32_t st = 0; st < 3; ++st) EXPECT(out.traffic.stages[st].recv_bits[0] == (st + 1) * 2 * 96);
+}
+
+TEST(OmniReduce_UniformInputsStayBalanced) {
+  auto inputs = workload(8, 100000, 0.01, 0.0, 31);
+  z::SimNet net(8, 1.0);
+  auto out = z::run_omnireduce_like(inputs, net, 64);
+  expect_exact(out, inputs);
+  EXPECT(out.balance.has_value() && out.balance->push_imbalance < 1.3);
+}
+
+TEST(OmniReduce_OracleEqualOnRandomCases) {
+  std::mt19937_64 rng(41);
+  for (int trial = 0; trial < 25; ++trial) {
+    const uint32_t n = 2 + rng() % 7;
+    auto inputs = workload(n, 3000, 0.02, 0.25 * double(rng() % 4), rng());
+    z::SimNet net(n, 1.0);
+    expect_exact(z::run_omnireduce_like(inputs, net, uint32_t(1 + rng() % 100)), inputs);
+  }
+}
+
+TEST(RunScheme_DispatchAndRejections) {
+  auto inputs = workload(4, 2000, 0.02, 0.5, 59);
+  for (const auto& name : z::known_scheme_names()) {
+    z::SimNet net(4, 1.0);
+    expect_exact(z::run_scheme(z::scheme_config_from_name(name), inputs, net), inputs);
+  }
+  z::SimNet na(4, 1.0), nb(4, 1.0);
+  auto direct = z::run_agsparse(inputs, na);
+  auto via = z::run_scheme(z::scheme_config_from_name("agsparse"), inputs, nb);
+  EXPECT(direct.traffic.total_recv_bits == via.traffic.total_recv_bits);
+  EXPECT(direct.results[0] == via.results[0]);
+  z::SchemeConfig cfg;
+  cfg.balance = z::BalancePattern::Balanced;
+  z::SimNet n1(4, 1.0);
+  EXPECT_THROW(z::run_scheme(cfg, inputs, n1), z::UnsupportedCombination);
+  z::SchemeConfig c2;
+  c2.communication = z::CommPattern::Ring;
+  c2.aggregation = z::Aggregation::Incremental;
+  c2.partition = z::PartitionPattern::Parallelism;
+  c2.balance = z::BalancePattern::Imbalanced;
+  z::SimNet n2(4, 1.0);
+  EXPECT_THROW(z::run_scheme(c2, inputs, n2), z::UnsupportedCombination);
+  EXPECT_THROW(z::scheme_config_from_name("nope"), z::UnsupportedCombination);
+}
+
+TEST(EdgeCases_EmptyInputsSynchronizeToEmptyEveryScheme) {
+  std::vector<z::SparseTensor> inputs(4, z::SparseTensor(1000, {}, {}));
+  for (const auto& name : z::known_scheme_names()) {
+    z::SimNet net(4, 1.0);
+    auto out = z::run_scheme(z::scheme_config_from_name(name), inputs, net);
+    for (const auto& r : out.results) EXPECT(r.nnz() == 0u);
+    EXPECT(!out.balance.has_value());
+  }
+}
+
+TEST(Uniformity_AllNodesAgreeForEveryScheme) {
+  auto inputs = workload(8, 20000, 0.01, 0.3, 79);
+  for (const auto& name : z::known_scheme_names()) {
+    z::SimNet net(8, 1.0);
+    auto out = z::run_scheme(z::scheme_config_from_name(name), inputs, net);
+    for (size_t i = 1; i < out.results.size(); ++i) EXPECT(out.results[i] == out.results[0]);
+  }
+}
+
 int main() {
   for (auto& [name, fn] : tests()) {
     const int before = g_fail;
