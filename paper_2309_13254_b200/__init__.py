@@ -17,7 +17,7 @@ from .zen import (  # noqa: F401
     write_sparse,
     write_sparse_file)
 from .schemes import (  # noqa: F401
-    BALANCED_PARALLELISM, HIERARCHICAL_CENTRALIZATION, CostInputs, HCSynchronizer,
+    BALANCED_PARALLELISM, HIERARCHICAL_CENTRALIZATION, AutoSynchronizer, CostInputs, HCSynchronizer,
     MissingProfileEntry, NonPowerOfTwo, SparsityProfile, densification_ratio, density,
     merge_sum, overlap_ratio, profile_sparsity, run_hier_centralization, select_scheme,
     skewness_ratio, t_allreduce_dense, KNOWN_SCHEME_NAMES, Aggregation, BalancePattern,

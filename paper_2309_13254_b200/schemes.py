@@ -725,3 +725,86 @@ def scheme_config_from_name(name: str) -> SchemeConfig:
         return SchemeConfig(CommPattern.PointToPoint, Aggregation.Incremental, P_,
                             BalancePattern.Balanced, WireFormat.hash_bitmap())
     raise UnsupportedCombination("unknown scheme name: " + name)
+
+
+# ------------------------------------------------- runtime scheme choice ----
+
+class AutoSynchronizer:
+    """select_scheme (costmodel.hpp:139-150) at run time, one process per GPU.
+
+    The first `profile_rounds` syncs run Hierarchical Centralization.  Rank 0's
+    HC state before stage s is the union of ranks [0, 2^s), so its stage counts
+    are exactly profile_sparsity's prefix unions (costmodel.hpp:151-195) for
+    k = 1, 2, 4, .., n; with the ranks' input counts (all-gathered) they give
+    the densification ladder gamma[k].  After profiling, the cheaper optimum by
+    the cost model serves every later sync: BP or HC.  Both return the same
+    aggregate (bit-identical at every rank)."""
+
+    def __init__(self, n: int, universe: int, rank: int, max_nnz: int, params=None,
+                 profile_rounds: int = 1, group=None):
+        from .zen import BPSynchronizer
+        self.n, self.m, self.rank, self.group = n, universe, rank, group
+        self.profile_rounds = profile_rounds
+        self.bp = BPSynchronizer(n, universe, max_nnz, params, rank=rank)
+        self.hc = HCSynchronizer(n, universe, rank, max_nnz) if _pow2(n) else None
+        self.choice = None if self.hc is not None else BALANCED_PARALLELISM
+        self.profile = None
+        self._gamma_sums, self._d_sum, self._rounds = {}, 0.0, 0
+        self._active = self.hc if self.hc is not None else self.bp
+        self._last = self._active
+
+    def connect_process_group(self):
+        self.bp.connect_process_group(self.group)
+        if self.hc is not None:
+            self.hc.connect_process_group(self.group)
+
+    def _observe(self):
+        import torch
+        import torch.distributed as dist
+        sent = [vb // 32 for _, vb in self.hc.stage_bits()]  # |U_1|, |U_2|, .., |U_{n/2}|
+        i, _ = self.hc.result()
+        unions = sent + [i.numel()]
+        dev = "cpu" if dist.get_backend(self.group) == "gloo" else "cuda"
+        own = torch.tensor([float(sent[0]) if sent else float(i.numel())], device=dev,
+                           dtype=torch.float64)
+        alln = [torch.zeros_like(own) for _ in range(self.n)]
+        dist.all_gather(alln, own, group=self.group)
+        d = [float(x[0]) / float(self.m) for x in alln]
+        g = torch.tensor([float(u) for u in unions], device=dev, dtype=torch.float64)
+        dist.broadcast(g, 0, group=self.group)
+        unions = [float(x) for x in g.cpu().numpy()]
+        self._d_sum += sum(d) / self.n
+        k = 2
+        for u in unions[1:]:
+            mean_d = sum(d[:k]) / float(k)
+            if mean_d > 0:
+                self._gamma_sums[k] = self._gamma_sums.get(k, 0.0) + (u / float(self.m)) / mean_d
+            k *= 2
+        self._rounds += 1
+        if self._rounds >= self.profile_rounds:
+            gamma = {k: v / self._rounds for k, v in self._gamma_sums.items()}
+            gamma[1] = 1.0
+            self.profile = SparsityProfile(self._d_sum / self._rounds, gamma, {})
+            self.choice = select_scheme(self.profile, self.n) if self.n in gamma \
+                else BALANCED_PARALLELISM
+            self._active = self.bp if self.choice == BALANCED_PARALLELISM else self.hc
+
+    def sync_dense(self, dense):
+        if self.choice is None:
+            self._last = self.hc
+            self.hc.sync_dense(dense)
+            self.hc.wait()
+            self._observe()
+            return
+        self._last = self._active
+        if self._active is self.bp:
+            self.bp.sync_dense([dense])
+        else:
+            self._active.sync_dense(dense)
+
+    def wait(self):
+        self._last.wait()
+
+    def result(self):
+        """(int64 indices, f32 values) of the last sync, whichever scheme ran it."""
+        return self._last.result()

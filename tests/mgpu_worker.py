@@ -100,6 +100,25 @@ def main():
             print(f"RANK {rank} HC sparse MISMATCH", flush=True)
             ok = False
         del hc
+    # runtime scheme choice: HC profiles the first sync, then select_scheme
+    auto = zen.AutoSynchronizer(world, m, rank, max_nnz=per * width + 1024)
+    auto.connect_process_group()
+    agg_i, agg_v = want.idx, want.val
+    for it in range(3):
+        auto.sync_dense(mine)
+        auto.wait()
+        ai, av = auto.result()
+        if not np.array_equal(ai.cpu().numpy().view(np.uint64), agg_i):
+            print(f"RANK {rank} auto iter {it} index MISMATCH ({auto.choice})", flush=True)
+            ok = False
+    if world & (world - 1) == 0:
+        prof = co.profile(m, [[co.to_sparse(d) for d in dense]])
+        if auto.profile is None or abs(auto.profile.gamma[world] - prof[1][world]) > 1e-12 \
+                or auto.choice != ("balanced-parallelism" if prof[3] == 0
+                                   else "hierarchical-centralization"):
+            print(f"RANK {rank} auto profile MISMATCH {auto.profile} vs {prof}", flush=True)
+            ok = False
+    del auto
     # the centralized baselines in rank mode (f4): ring centralization and
     # AGsparse point-to-point, same push + fold machinery
     sparse_in = [co.to_sparse(d) for d in dense]
