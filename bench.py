@@ -266,7 +266,19 @@ def compare_schemes(args, zen, d_dense, m, z, n, rank, stream, barrier, dist):
     for name in ["hc", "ring", "agsparse"]:
         if name != "agsparse" and n & (n - 1):
             continue
-        sy = sch.HCSynchronizer(n, m, rank, max_nnz=int(z * 1.25) + 4096, scheme=name)
+        # create everywhere or nowhere: a rank that fails must not leave the
+        # others waiting in the handle exchange
+        try:
+            sy = sch.HCSynchronizer(n, m, rank, max_nnz=int(z * 1.25) + 4096, scheme=name)
+            okf = 1.0
+        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+            sy, okf, err = None, 0.0, str(e)[:200]
+        flag = torch.tensor([okf], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if float(flag[0]) < 1.0:
+            out[name] = {"error": err if sy is None else "failed on another rank"}
+            del sy
+            continue
         sy.connect_process_group()
         for _ in range(3):
             sy.sync_dense(d_dense)
@@ -562,7 +574,10 @@ def main():
     # densification ladder (rank 0's HC stage counts are the prefix unions)
     schemes = None
     if dist and not args.no_extras:
-        schemes = compare_schemes(args, zen, d_dense, m, z, n, rank, stream, barrier, dist)
+        try:
+            schemes = compare_schemes(args, zen, d_dense, m, z, n, rank, stream, barrier, dist)
+        except Exception as e:  # noqa: BLE001 -- the headline line must still print
+            schemes = {"error": str(e)[:300]}
 
     # extra: n workers emulated on one GPU (local mode), e.g. the 8-worker headline
     emu = None
