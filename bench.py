@@ -255,16 +255,16 @@ def exchange_report(ledger, n, stage_ms):
 # ------------------------------------------------------------ extras (f1/f2) ----
 
 def compare_schemes(args, zen, d_dense, m, z, n, rank, stream, barrier, dist):
-    """BP vs the centralized schemes on this run's gradients, one process per
-    GPU: device time of K syncs (CUDA events, max over ranks); result
+    """BP vs HC, ring centralization, AGsparse and OmniReduce-like on this
+    run's gradients, one process per GPU: device time of K syncs (CUDA events, max over ranks); result
     indices checked equal to BP's on every rank."""
     import torch
     from paper_2309_13254_b200 import schemes as sch
     out = {}
     k = max(5, min(args.steps, 20))
     counts = None
-    for name in ["hc", "ring", "agsparse"]:
-        if name != "agsparse" and n & (n - 1):
+    for name in ["hc", "ring", "agsparse", "omnireduce"]:
+        if name in ("hc", "ring") and n & (n - 1):
             continue
         # create everywhere or nowhere: a rank that fails must not leave the
         # others waiting in the handle exchange

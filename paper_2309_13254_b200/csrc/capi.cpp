@@ -2300,11 +2300,12 @@ constexpr uint32_t kHcMaxRanks = 256;
 
 struct HcHdr {
   unsigned long long epoch;
-  unsigned long long ready[kHcMaxRanks];  // receive slot j was filled (epoch)
-  unsigned long long done[kHcMaxRanks];   // the push this rank made to peer j was consumed
+  unsigned long long ready[2 * kHcMaxRanks];  // receive slot j was filled (epoch)
+  unsigned long long done[2 * kHcMaxRanks];  // this rank's push i was consumed
   uint64_t cnt[3];                        // [input, state 0, state 1] counts
-  uint64_t rcnt[kHcMaxRanks];             // receive slot counts
-  uint64_t sent[kHcMaxRanks];             // entries of this rank's i-th push (ledger)
+  uint64_t rcnt[2 * kHcMaxRanks];         // receive slot counts
+  uint64_t sent[2 * kHcMaxRanks];         // entries of this rank's i-th push (ledger)
+  uint64_t bnd[kHcMaxRanks + 1];          // OmniReduce: range bounds of the input
   uint32_t err;                           // kErr* bits
   uint32_t in_err;                        // kWire* bits of the input check
 };
@@ -2315,6 +2316,7 @@ struct HcPush {
   int src;
   uint32_t dst, slot;
   uint64_t cap;
+  int src_bnd = -1;  // OmniReduce: the source is input range [bnd[i], bnd[i+1])
 };
 struct HcMerge {
   int a, b, out;
@@ -2322,10 +2324,13 @@ struct HcMerge {
   int done_rank[2];  // senders whose pushes this merge consumes (-1: none) ...
   int done_idx[2];   // ... and the index of that push in the sender's plan
   uint64_t a_cap, b_cap;
+  int a_bnd = -1, b_bnd = -1;  // OmniReduce: an operand is input range i
 };
 struct HcStage {
+  bool bounds = false;  // OmniReduce: range bounds of the input first
   std::vector<HcPush> push;
   std::vector<HcMerge> merge;
+  int concat_out = -1;  // OmniReduce: concat (zeros dropped) of the ranges into this buffer
 };
 }  // namespace
 
@@ -2355,6 +2360,13 @@ struct zen_hc {
   uint32_t graph_kernels = 0;
   uint32_t npush = 0;
   uint64_t h_result = 0;
+  int omni_acc = -1;  // OmniReduce: the buffer holding this rank's range aggregate
+  // OmniReduce concat tables (device), built at connect
+  const uint64_t** c_idx = nullptr;
+  const float** c_val = nullptr;
+  const uint64_t** c_cnt = nullptr;
+  const unsigned long long** c_wait = nullptr;
+  unsigned long long** c_done = nullptr;
   HcHdr* hdr(uint32_t r) const { return reinterpret_cast<HcHdr*>(peer[r]); }
   uint32_t nslots_used() const { return uint32_t(buf_cap.size()) - kBufRecv; }
   uint64_t* idx(uint32_t r, int b) const { return reinterpret_cast<uint64_t*>(peer[r] + off_idx[b]); }
@@ -2375,7 +2387,7 @@ void hc_plan(zen_hc* h) {
   auto capk = [&](uint64_t k) { return std::min<uint64_t>(M, k * z); };
   h->buf_cap = {capk(1), h->cap, h->cap};
   auto merge = [](int a, int b, int out, uint64_t ac, uint64_t bc) {
-    return HcMerge{a, b, out, {-1, -1}, {-1, -1}, {0, 0}, ac, bc};
+    return HcMerge{a, b, out, {-1, -1}, {-1, -1}, {0, 0}, ac, bc, -1, -1};
   };
   if (h->scheme == ZEN_SCHEME_HC) {
     uint32_t L = 0;
@@ -2414,6 +2426,64 @@ void hc_plan(zen_hc* h) {
       tok = out;
     }
     h->result_buf = tok;
+  } else if (h->scheme == ZEN_SCHEME_OMNIREDUCE) {
+    // run_omnireduce_like (zen/schemes.hpp:219-328): range p = [p*R, (p+1)*R),
+    // R = ceil(M/n).  Stage 0: slice p of the input -> owner p (slot = sender);
+    // the owner folds the n slices in worker order.  Stage 1: the owner's
+    // aggregate -> every peer (slot n + owner); every rank concatenates the
+    // n ranges and drops exact zeros (the block decode).
+    const uint64_t R = (M + n - 1) / n;
+    auto rcap = [&](uint32_t p) {
+      const uint64_t lo = uint64_t(p) * R, hi = std::min(M, lo + R);
+      return std::min<uint64_t>(hi > lo ? hi - lo : 0, uint64_t(n) * z);
+    };
+    auto idx0 = [&](uint32_t sender) { return int(r < sender ? r : r - 1); };  // stage-0 push index
+    HcStage s0;
+    s0.bounds = true;
+    for (uint32_t q = 0; q < n; ++q)
+      if (q != r) {
+        HcPush p{kBufIn, q, r, capk(1)};
+        p.src_bnd = int(q);
+        s0.push.push_back(p);
+      }
+    auto slice = [&](uint32_t w, int* buf, int* bnd) {
+      *buf = w == r ? kBufIn : kBufRecv + int(w);
+      *bnd = w == r ? int(r) : -1;
+    };
+    int acc, acc_bnd;
+    slice(0, &acc, &acc_bnd);
+    for (uint32_t w = 1; w < n; ++w) {
+      const int out = (w & 1) ? kBufSt0 : kBufSt1;
+      int b, b_bnd;
+      slice(w, &b, &b_bnd);
+      HcMerge mg = merge(acc, b, out, capk(w), capk(1));
+      mg.a_bnd = acc_bnd;
+      mg.b_bnd = b_bnd;
+      int k = 0;
+      if (w == 1 && r != 0) {
+        mg.wait[k] = 0;
+        mg.done_rank[k] = 0;
+        mg.done_idx[k++] = idx0(0);
+      }
+      if (w != r) {
+        mg.wait[k] = int(w);
+        mg.done_rank[k] = int(w);
+        mg.done_idx[k++] = idx0(w);
+      }
+      s0.merge.push_back(mg);
+      acc = out;
+      acc_bnd = -1;
+    }
+    h->plan.push_back(s0);
+    HcStage s1;
+    for (uint32_t q = 0; q < n; ++q)
+      if (q != r) s1.push.push_back({acc, q, n + r, rcap(r)});
+    s1.concat_out = acc == kBufSt0 ? kBufSt1 : kBufSt0;
+    h->plan.push_back(s1);
+    for (uint32_t j = 0; j < n; ++j) h->buf_cap.push_back(capk(1));  // slices
+    for (uint32_t p = 0; p < n; ++p) h->buf_cap.push_back(rcap(p));  // owners' ranges
+    h->omni_acc = acc;
+    h->result_buf = s1.concat_out;
   } else {  // AGsparse point-to-point: slot j holds worker j's input
     HcStage st;
     for (uint32_t q = 0; q < n; ++q)
@@ -2465,6 +2535,7 @@ zen_status hc_enqueue(zen_hc* h, const float* dense, const uint64_t* in_idx, con
   }
   uint32_t pi = 0;
   for (const HcStage& stg : h->plan) {
+    if (stg.bounds) launch_hc_bounds(h->idx(r, kBufIn), &me->cnt[kBufIn], h->m, h->n, me->bnd, st);
     for (const HcPush& p : stg.push) {
       HcPushArgs a{};
       a.src_idx = h->idx(r, p.src);
@@ -2480,6 +2551,7 @@ zen_status hc_enqueue(zen_hc* h, const float* dense, const uint64_t* in_idx, con
       a.ctl = h->ctl_push;
       a.err = &me->err;
       a.sent_cnt = &me->sent[pi++];
+      a.src_bnd = p.src_bnd >= 0 ? &me->bnd[p.src_bnd] : nullptr;
       launch_hc_push(a, st);
     }
     for (const HcMerge& mg : stg.merge) {
@@ -2506,7 +2578,28 @@ zen_status hc_enqueue(zen_hc* h, const float* dense, const uint64_t* in_idx, con
       a.done_flag2 = mg.done_rank[1] >= 0
                          ? &h->hdr(uint32_t(mg.done_rank[1]))->done[mg.done_idx[1]] : nullptr;
       a.epoch = &me->epoch;
+      a.a_bnd = mg.a_bnd >= 0 ? &me->bnd[mg.a_bnd] : nullptr;
+      a.b_bnd = mg.b_bnd >= 0 ? &me->bnd[mg.b_bnd] : nullptr;
       launch_hc_merge(a, hc_merge_tiles(mg.a_cap + mg.b_cap), st);
+    }
+    if (stg.concat_out >= 0) {
+      HcConcatArgs c{};
+      c.seg_idx = h->c_idx;
+      c.seg_val = h->c_val;
+      c.seg_cnt = h->c_cnt;
+      c.wait = h->c_wait;
+      c.done = h->c_done;
+      c.n = h->n;
+      c.seg_cap = h->cap;
+      c.o_idx = h->idx(r, stg.concat_out);
+      c.o_val = h->val(r, stg.concat_out);
+      c.o_cnt = h->cntp(r, stg.concat_out);
+      c.o_cap = h->cap;
+      c.lb_status = h->lb;
+      c.ctl = h->ctl_merge;
+      c.err = &me->err;
+      c.epoch = &me->epoch;
+      launch_hc_concat(c, hc_merge_tiles(h->cap), st);
     }
   }
   h->npush = pi;
@@ -2529,9 +2622,11 @@ extern "C" {
 zen_status zen_hc_create_scheme(zen_ctx* c, uint32_t scheme, uint32_t n, uint32_t rank,
                                 uint64_t universe, uint64_t max_nnz, zen_hc** out) {
   if (!c || !out) return fail(ZEN_E_INVALID, "null argument");
-  if (scheme > ZEN_SCHEME_AGSPARSE) return fail(ZEN_E_INVALID, "unknown scheme");
+  if (scheme > ZEN_SCHEME_OMNIREDUCE) return fail(ZEN_E_INVALID, "unknown scheme");
   const bool pow2 = n != 0 && (n & (n - 1)) == 0;
-  if (n == 0 || (scheme != ZEN_SCHEME_AGSPARSE && !pow2))
+  if (scheme == ZEN_SCHEME_OMNIREDUCE && n < 2)
+    return fail(ZEN_E_INVALID, "synchronization needs at least two nodes");
+  if (n == 0 || ((scheme == ZEN_SCHEME_HC || scheme == ZEN_SCHEME_RING) && !pow2))
     return fail(ZEN_E_INVALID, "node count must be a power of two");
   if (n > kHcMaxRanks) return fail(ZEN_E_INVALID, "node count above 256");
   if (rank >= n) return fail(ZEN_E_INVALID, "rank out of range");
@@ -2570,7 +2665,7 @@ zen_status zen_hc_create_scheme(zen_ctx* c, uint32_t scheme, uint32_t n, uint32_
   CKR(h->mem.alloc(&h->ex.tile_base, ntiles));
   h->ex.nblk = (h->max_nnz + 255) / 256;
   CKR(h->mem.alloc(&h->ex.blk_tile, h->ex.nblk + 1));
-  uint64_t max_tiles = 1;
+  uint64_t max_tiles = hc_merge_tiles(h->cap);  // (the OmniReduce concat)
   for (const auto& stg : h->plan)
     for (const auto& mg : stg.merge)
       max_tiles = std::max<uint64_t>(max_tiles, hc_merge_tiles(mg.a_cap + mg.b_cap));
@@ -2628,6 +2723,44 @@ zen_status zen_hc_connect(zen_hc* h, const void* handles) {
                                   "): " + cudaGetErrorString(e));
     }
     h->peer[r] = static_cast<char*>(p);
+  }
+  if (h->scheme == ZEN_SCHEME_OMNIREDUCE) {  // the concat's segment and flag tables
+    const uint32_t n = h->n, r = h->rank;
+    std::vector<const uint64_t*> ci(n), cc(n);
+    std::vector<const float*> cv(n);
+    std::vector<const unsigned long long*> cw(n);
+    std::vector<unsigned long long*> cd(n);
+    for (uint32_t p = 0; p < n; ++p) {
+      if (!h->peer[p]) {
+        void* q = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&q, hs[p], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          return fail(ZEN_E_PEER, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        }
+        h->peer[p] = static_cast<char*>(q);
+      }
+      const int b = p == r ? h->omni_acc : kBufRecv + int(n + p);
+      ci[p] = h->idx(r, b);
+      cv[p] = h->val(r, b);
+      cc[p] = h->cntp(r, b);
+      cw[p] = p == r ? nullptr : &h->hdr(r)->ready[n + p];
+      // owner p's stage-1 push to this rank: index (n-1) + position of r among p's peers
+      cd[p] = p == r ? nullptr : &h->hdr(p)->done[(n - 1) + (r < p ? r : r - 1)];
+    }
+    if (!h->c_idx) {
+      CKR(h->mem.alloc(&h->c_idx, n));
+      CKR(h->mem.alloc(&h->c_val, n));
+      CKR(h->mem.alloc(&h->c_cnt, n));
+      CKR(h->mem.alloc(&h->c_wait, n));
+      CKR(h->mem.alloc(&h->c_done, n));
+    }
+    SetupStream setup_(h->ctx->stream);
+    CKR(upload(h->c_idx, ci.data(), n));
+    CKR(upload(h->c_val, cv.data(), n));
+    CKR(upload(h->c_cnt, cc.data(), n));
+    CKR(upload(h->c_wait, cw.data(), n));
+    CKR(upload(h->c_done, cd.data(), n));
   }
   h->connected = true;
   hc_drop_graph(h);

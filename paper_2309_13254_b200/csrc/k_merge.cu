@@ -96,6 +96,18 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_merge(HcMergeArgs a) {
   const uint32_t tile = take_ticket(a.ctl, &s_tile);  // also orders the wait above
   const uint32_t tag = *(volatile uint32_t*)&a.ctl->tag;
   uint64_t na = *(volatile const uint64_t*)a.a_cnt, nb = *(volatile const uint64_t*)a.b_cnt;
+  if (a.a_bnd) {  // a sub-range of the buffer (an OmniReduce range slice)
+    const uint64_t b0 = a.a_bnd[0], b1 = a.a_bnd[1];
+    a.a_idx += b0;
+    a.a_val += b0;
+    na = b1 > b0 ? b1 - b0 : 0;
+  }
+  if (a.b_bnd) {
+    const uint64_t b0 = a.b_bnd[0], b1 = a.b_bnd[1];
+    a.b_idx += b0;
+    a.b_val += b0;
+    nb = b1 > b0 ? b1 - b0 : 0;
+  }
   if (na > a.a_cap || nb > a.b_cap) {
     if (tid == 0) atomicOr(a.err, kErrCapacity);
     na = na > a.a_cap ? a.a_cap : na;
@@ -264,11 +276,33 @@ __global__ void __launch_bounds__(256) k_hc_push(HcPushArgs a) {
     atomicOr(a.err, kErrTimeout);
   __syncthreads();
   uint64_t n = *(volatile const uint64_t*)a.src_cnt;
+  uint64_t off = 0;
+  if (a.src_bnd) {  // a sub-range of the source buffer
+    off = a.src_bnd[0];
+    n = a.src_bnd[1] > off ? a.src_bnd[1] - off : 0;
+    a.src_idx += off;
+    a.src_val += off;
+  }
   if (n > a.cap) {
     if (tid == 0 && blockIdx.x == 0) atomicOr(a.err, kErrCapacity);
     n = a.cap;
   }
   const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + tid, stride = uint64_t(gridDim.x) * blockDim.x;
+  if (off & 3) {  // a misaligned slice: element copies (still coalesced)
+    for (uint64_t x = g; x < n; x += stride) {
+      a.dst_idx[x] = a.src_idx[x];
+      a.dst_val[x] = a.src_val[x];
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      *a.dst_cnt = n;
+      if (a.sent_cnt) *a.sent_cnt = n;
+    }
+    if (finish_tile(a.ctl, gridDim.x, /*sys=*/true) && tid == 0) {
+      __threadfence_system();
+      st_release_sys(a.ready_flag, ep);
+    }
+    return;
+  }
   // buffers are 256-byte aligned: 16-byte vectors, then the tails
   // four independent 16-byte loads in flight per thread, then their stores
   const uint64_t n2 = n >> 1, n4 = n >> 2;
@@ -308,6 +342,116 @@ __global__ void __launch_bounds__(256) k_hc_push(HcPushArgs a) {
   }
 }
 
+// n disjoint ascending segments -> one tensor with exact zeros dropped; tiles
+// of the concatenated position space, a block scan of the kept entries and a
+// decoupled look-back for their output positions.
+constexpr uint32_t kConcatMaxSeg = 256;
+
+__global__ void __launch_bounds__(kMergeThreads) k_hc_concat(HcConcatArgs a) {
+  pdl_entry();
+  __shared__ uint64_t s_pre[kConcatMaxSeg + 1];
+  __shared__ uint32_t s_tile, s_warp[kMergeThreads / 32];
+  __shared__ uint64_t s_excl;
+  const uint32_t tid = threadIdx.x, n = a.n;
+  const uint64_t ep = *(volatile const unsigned long long*)a.epoch;
+  if (tid < n && a.wait[tid] && !wait_flag(a.wait[tid], ep, kPeerTimeoutNs))
+    atomicOr(a.err, kErrTimeout);
+  const uint32_t tile = take_ticket(a.ctl, &s_tile);
+  const uint32_t tag = *(volatile uint32_t*)&a.ctl->tag;
+  if (tid == 0) {
+    uint64_t run = 0;
+    for (uint32_t p = 0; p < n; ++p) {
+      s_pre[p] = run;
+      uint64_t c = *(volatile const uint64_t*)a.seg_cnt[p];
+      if (c > a.seg_cap) {
+        atomicOr(a.err, kErrCapacity);
+        c = a.seg_cap;
+      }
+      run += c;
+    }
+    s_pre[n] = run;
+  }
+  __syncthreads();
+  const uint64_t tot = s_pre[n];
+  uint32_t keep = 0;
+  uint64_t key[kMergeItems];
+  float val[kMergeItems];
+  const uint64_t base = uint64_t(tile) * kMergeTile + uint64_t(tid) * kMergeItems;
+#pragma unroll
+  for (uint32_t k = 0; k < kMergeItems; ++k) {
+    const uint64_t x = base + k;
+    val[k] = 0.f;
+    if (x < tot) {
+      uint32_t lo = 0, hi = n;  // segment: last p with s_pre[p] <= x
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_pre[mid] <= x) lo = mid; else hi = mid;
+      }
+      key[k] = a.seg_idx[lo][x - s_pre[lo]];
+      val[k] = a.seg_val[lo][x - s_pre[lo]];
+      if (val[k] != 0.0f) keep |= 1u << k;
+    }
+  }
+  const uint32_t u = __popc(keep), lane = tid & 31, warp = tid >> 5;
+  uint32_t incl = u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  uint32_t wbase = 0, agg = 0;
+#pragma unroll
+  for (uint32_t w = 0; w < kMergeThreads / 32; ++w) {
+    const uint32_t t = s_warp[w];
+    if (w < warp) wbase += t;
+    agg += t;
+  }
+  if (warp == 0) {
+    const uint64_t ex = lookback_warp(a.lb_status, tile, tag, agg);
+    if (lane == 0) s_excl = ex;
+  }
+  __syncthreads();
+  uint64_t pos = s_excl + wbase + incl - u;
+#pragma unroll
+  for (uint32_t k = 0; k < kMergeItems; ++k)
+    if ((keep >> k) & 1u) {
+      if (pos < a.o_cap) {
+        a.o_idx[pos] = key[k];
+        a.o_val[pos] = val[k];
+      }
+      ++pos;
+    }
+  if (tid == 0 && (base < tot || tile == 0) &&
+      (uint64_t(tile + 1) * kMergeTile >= tot)) {  // the tile holding the last position
+    const uint64_t total = s_excl + agg;
+    if (total > a.o_cap) atomicOr(a.err, kErrCapacity);
+    *a.o_cnt = total;
+  }
+  if (finish_tile(a.ctl, gridDim.x, /*sys=*/true)) {
+    if (tid == 0) __threadfence_system();
+    __syncthreads();
+    if (tid < n && a.done[tid]) st_release_sys(a.done[tid], ep);
+  }
+}
+
+__global__ void k_hc_bounds(const uint64_t* __restrict__ idx, const uint64_t* count, uint64_t m,
+                            uint32_t parts, uint64_t* __restrict__ bnd) {
+  pdl_entry();
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > parts) return;
+  const uint64_t c = *(volatile const uint64_t*)count;
+  const uint64_t range = (m + parts - 1) / parts;
+  const uint64_t key = p == parts ? m : (uint64_t(p) * range < m ? uint64_t(p) * range : m);
+  uint64_t lo = 0, hi = c;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (idx[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  bnd[p] = lo;
+}
+
 __global__ void k_hc_begin(unsigned long long* epoch) {
   pdl_entry();
   if (threadIdx.x == 0) *epoch = *epoch + 1;
@@ -331,6 +475,17 @@ void launch_hc_merge(const HcMergeArgs& a, uint32_t tiles, cudaStream_t stream) 
 
 void launch_hc_push(const HcPushArgs& a, cudaStream_t stream) {
   launch_k(k_hc_push, 148 * 2, 256, 0, stream, a);
+  count_launch();
+}
+
+void launch_hc_concat(const HcConcatArgs& a, uint32_t tiles, cudaStream_t stream) {
+  launch_k(k_hc_concat, tiles, kMergeThreads, 0, stream, a);
+  count_launch();
+}
+
+void launch_hc_bounds(const uint64_t* idx, const uint64_t* count, uint64_t m, uint32_t parts,
+                      uint64_t* bnd, cudaStream_t stream) {
+  launch_k(k_hc_bounds, (parts + 256) / 256, 256, 0, stream, idx, count, m, parts, bnd);
   count_launch();
 }
 

@@ -325,6 +325,8 @@ struct HcMergeArgs {
   unsigned long long* done_flag2;
   const unsigned long long* epoch;       // local sync counter (nullptr: 0)
   uint64_t* stage_cnt;                   // receives |a| (the ledger), may be null
+  const uint64_t* a_bnd;                 // optional [begin, end) of a / b inside their
+  const uint64_t* b_bnd;                 // buffers (device words; count = end - begin)
 };
 struct HcPushArgs {
   const uint64_t* src_idx;
@@ -340,7 +342,31 @@ struct HcPushArgs {
   LookbackCtl* ctl;
   uint32_t* err;
   uint64_t* sent_cnt;  // receives the pushed count (the ledger)
+  const uint64_t* src_bnd;  // optional [begin, end) of the source (device words)
 };
+// n sorted, index-disjoint, ascending segments -> one tensor, exact zeros
+// dropped (the block decode of run_omnireduce_like, zen/schemes.hpp:289-295)
+struct HcConcatArgs {
+  const uint64_t* const* seg_idx;  // [n] device pointer tables
+  const float* const* seg_val;
+  const uint64_t* const* seg_cnt;
+  const unsigned long long* const* wait;  // [n] ready flags to acquire (null entries: none)
+  unsigned long long* const* done;        // [n] senders' done flags to release (null: none)
+  uint32_t n;
+  uint64_t seg_cap;
+  uint64_t* o_idx;
+  float* o_val;
+  uint64_t* o_cnt;
+  uint64_t o_cap;
+  unsigned long long* lb_status;
+  LookbackCtl* ctl;
+  uint32_t* err;
+  const unsigned long long* epoch;
+};
+void launch_hc_concat(const HcConcatArgs& a, uint32_t tiles, cudaStream_t stream);
+// bnd[p] = lower_bound(idx[0, *count), min(M, p*ceil(M/parts))), p in [0, parts]
+void launch_hc_bounds(const uint64_t* idx, const uint64_t* count, uint64_t m, uint32_t parts,
+                      uint64_t* bnd, cudaStream_t stream);
 uint32_t hc_merge_tiles(uint64_t max_entries);
 void launch_hc_merge(const HcMergeArgs& a, uint32_t tiles, cudaStream_t stream);
 void launch_hc_push(const HcPushArgs& a, cudaStream_t stream);

@@ -396,17 +396,18 @@ class HCSynchronizer:
     Counts stay on the device; sync_dense replays one CUDA graph.  Every rank
     ends with aggregate(inputs), bit for bit."""
 
-    SCHEMES = {"hc": 0, "ring": 1, "agsparse": 2}
+    SCHEMES = {"hc": 0, "ring": 1, "agsparse": 2, "omnireduce": 3}
 
     def __init__(self, n: int, universe: int, rank: int, max_nnz: int,
                  fmt: WireFormat | None = None, device: int | None = None,
                  scheme: str = "hc"):
         """scheme: "hc" (run_hier_centralization), "ring"
-        (run_ring_centralization) or "agsparse" (run_agsparse point-to-point,
-        any n) -- the same NVLink push + device fold machinery."""
+        (run_ring_centralization), "agsparse" (run_agsparse point-to-point,
+        any n) or "omnireduce" (run_omnireduce_like, any n >= 2) -- the same
+        NVLink push + device fold machinery."""
         if scheme not in self.SCHEMES:
             raise Error(f"unknown scheme {scheme}")
-        if scheme != "agsparse" and not _pow2(n):
+        if scheme in ("hc", "ring") and not _pow2(n):
             raise NonPowerOfTwo()
         if fmt is not None and fmt.kind not in ("coo", "bitmap"):
             raise Error("rank-mode ledger supports COO and bitmap formats")
@@ -472,6 +473,14 @@ class HCSynchronizer:
         ov = torch.empty(max(z, 1), dtype=torch.float32, device=dev)
         _check(_lib().zen_hc_copy_result(self.h, _ptr(oi), _ptr(ov), max(z, 1), C.byref(c)))
         return oi[:z], ov[:z]
+
+    def sent_counts(self):
+        """Entries this rank sent per push, in plan order (OmniReduce: the n-1
+        range slices, then its range aggregate to each of the n-1 peers)."""
+        ns = _lib().zen_hc_pushes(self.h)
+        out = (C.c_uint64 * max(ns, 1))()
+        _check(_lib().zen_hc_stage_counts(self.h, out))
+        return [int(out[i]) for i in range(ns)]
 
     def stage_bits(self):
         """[(index_bits, value_bits)] this rank sent per push, in plan order

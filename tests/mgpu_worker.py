@@ -122,6 +122,25 @@ def main():
     # the centralized baselines in rank mode (f4): ring centralization and
     # AGsparse point-to-point, same push + fold machinery
     sparse_in = [co.to_sparse(d) for d in dense]
+    # OmniReduce-like in rank mode: results per rank, and the sent entries
+    om = zen.HCSynchronizer(world, m, rank, max_nnz=per * width + 1024, scheme="omnireduce")
+    om.connect_process_group()
+    res, led, _ = co.run_scheme("omnireduce", m, sparse_in_all := [co.to_sparse(d) for d in dense])
+    rng = (m + world - 1) // world
+    mi = sparse_in_all[rank][0]
+    slices = [int(np.count_nonzero((mi // rng) == q)) for q in range(world) if q != rank]
+    for it in range(2):
+        om.sync_dense(mine)
+        gi, gv = om.result()
+        good = np.array_equal(gi.cpu().numpy().view(np.uint64), res[rank][0]) and \
+            np.array_equal(gv.cpu().numpy().view(np.uint32), res[rank][1].view(np.uint32))
+        sc = om.sent_counts()
+        good = good and sc[:world - 1] == slices and len(set(sc[world - 1:])) == 1
+        if not good:
+            print(f"RANK {rank} omnireduce iter {it} MISMATCH {gi.numel()} vs {res[rank][0].size} "
+                  f"{sc} {slices}", flush=True)
+            ok = False
+    del om
     for scheme, name in [("ring", "ring-centralization"), ("agsparse", "agsparse")]:
         if scheme == "ring" and world & (world - 1):
             continue

@@ -92,7 +92,7 @@ def main():
             out["hc_equals_bp"] = bool(torch.equal(hi, bi) and torch.equal(hv.view(torch.int32),
                                                                            bv.view(torch.int32)))
             out["hc_sent_bits_rank0"] = [ib + vb for ib, vb in hc.stage_bits()]
-        for scheme in ["ring", "agsparse"]:
+        for scheme in ["ring", "agsparse", "omnireduce"]:
             if scheme == "ring" and world & (world - 1):
                 continue
             sy = zen.HCSynchronizer(world, m, rank, max_nnz=per * width + 4096, scheme=scheme)
