@@ -489,10 +489,12 @@ def main():
     cnt = bp.result_count()
     assert cnt >= z and cnt <= n * z, f"result size {cnt} out of range"
     launches0 = zen.load().zen_kernel_launches()
-    barrier()
     with ClockSampler(local_rank) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        # the barrier right before the first event: the sampler's start-up
+        # (NVML calls) must not skew the ranks' start times
+        barrier()
         e0.record(stream)
         h0 = time.perf_counter()
         for _ in range(args.steps):
