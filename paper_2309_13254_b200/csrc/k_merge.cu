@@ -18,6 +18,7 @@
 // look-back places the tile's unique entries.  On a tie the first input's entry
 // comes first, so a shared index sums to a + b, the reference's operand order.
 #include <cstdint>
+#include <cstdlib>
 
 #include "zen_common.cuh"
 #include "zen_internal.h"
@@ -85,15 +86,18 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_merge(HcMergeArgs a) {
   __shared__ uint64_t sk[kMergeTile];
   __shared__ float sv[kMergeTile];
   __shared__ uint64_t s_split[2];
-  __shared__ uint32_t s_tile, s_warp[kMergeThreads / 32];
-  __shared__ uint64_t s_excl;
+  __shared__ uint32_t s_warp[kMergeThreads / 32];
+  __shared__ unsigned long long s_red[32];
   const uint32_t tid = threadIdx.x;
   const uint64_t ep = a.epoch ? *(volatile const unsigned long long*)a.epoch : 0;
   if (tid == 0) {
     if (a.wait_flag && !wait_flag(a.wait_flag, ep, kPeerTimeoutNs)) atomicOr(a.err, kErrTimeout);
     if (a.wait_flag2 && !wait_flag(a.wait_flag2, ep, kPeerTimeoutNs)) atomicOr(a.err, kErrTimeout);
   }
-  const uint32_t tile = take_ticket(a.ctl, &s_tile);  // also orders the wait above
+  // tiles in launch order (single-pass scans rely on in-order block dispatch);
+  // the barrier orders the flag acquire above before any input read
+  __syncthreads();
+  const uint32_t tile = blockIdx.x;
   const uint32_t tag = *(volatile uint32_t*)&a.ctl->tag;
   uint64_t na = *(volatile const uint64_t*)a.a_cnt, nb = *(volatile const uint64_t*)a.b_cnt;
   if (a.a_bnd) {  // a sub-range of the buffer (an OmniReduce range slice)
@@ -238,12 +242,10 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_merge(HcMergeArgs a) {
         ++pos;
       }
   }
-  if (warp == 0) {
-    const uint64_t ex = lookback_warp(a.lb_status, tile, tag, agg);
-    if (lane == 0) s_excl = ex;
-  }
-  __syncthreads();
-  const uint64_t excl = s_excl;
+  // block-wide look-back: the grid is one wave, so a warp-wide walk would go
+  // back window by window through every tile in flight
+  const uint64_t excl = lookback_block(a.lb_status, tile, tag, agg, s_red);
+  __syncthreads();  // the staged entries in sk/sv (tile 0 returns without a barrier)
   for (uint32_t x = tid; x < agg; x += kMergeThreads) {
     const uint64_t o = excl + x;
     if (o < a.o_cap) {
@@ -258,7 +260,15 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_merge(HcMergeArgs a) {
       *a.o_cnt = total;  // the true size; readers clamp to their capacity
     }
   }
-  if (finish_tile(a.ctl, gridDim.x, /*sys=*/a.done_flag != nullptr) && tid == 0) {
+  // the last tile's prefix needed every tile's aggregate, which each tile
+  // publishes after its last read of the inputs and of the tag: the tag can
+  // advance and the senders can reuse their buffers
+  const bool last = blockIdx.x == gridDim.x - 1;
+  if (last && tid == 0) {
+    const uint32_t t = (tag + 1u) & 0xFFFFFFu;
+    a.ctl->tag = t ? t : 1u;
+  }
+  if (last && tid == 0) {
     if (a.done_flag || a.done_flag2) __threadfence_system();
     if (a.done_flag) st_release_sys(a.done_flag, ep);
     if (a.done_flag2) st_release_sys(a.done_flag2, ep);
@@ -350,13 +360,14 @@ constexpr uint32_t kConcatMaxSeg = 256;
 __global__ void __launch_bounds__(kMergeThreads) k_hc_concat(HcConcatArgs a) {
   pdl_entry();
   __shared__ uint64_t s_pre[kConcatMaxSeg + 1];
-  __shared__ uint32_t s_tile, s_warp[kMergeThreads / 32];
-  __shared__ uint64_t s_excl;
+  __shared__ uint32_t s_warp[kMergeThreads / 32];
+  __shared__ unsigned long long s_red[32];
   const uint32_t tid = threadIdx.x, n = a.n;
   const uint64_t ep = *(volatile const unsigned long long*)a.epoch;
   if (tid < n && a.wait[tid] && !wait_flag(a.wait[tid], ep, kPeerTimeoutNs))
     atomicOr(a.err, kErrTimeout);
-  const uint32_t tile = take_ticket(a.ctl, &s_tile);
+  __syncthreads();  // orders the flag acquires above before any segment read
+  const uint32_t tile = blockIdx.x;
   const uint32_t tag = *(volatile uint32_t*)&a.ctl->tag;
   if (tid == 0) {
     uint64_t run = 0;
@@ -408,12 +419,8 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_concat(HcConcatArgs a) {
     if (w < warp) wbase += t;
     agg += t;
   }
-  if (warp == 0) {
-    const uint64_t ex = lookback_warp(a.lb_status, tile, tag, agg);
-    if (lane == 0) s_excl = ex;
-  }
-  __syncthreads();
-  uint64_t pos = s_excl + wbase + incl - u;
+  const uint64_t excl = lookback_block(a.lb_status, tile, tag, agg, s_red);
+  uint64_t pos = excl + wbase + incl - u;
 #pragma unroll
   for (uint32_t k = 0; k < kMergeItems; ++k)
     if ((keep >> k) & 1u) {
@@ -425,12 +432,17 @@ __global__ void __launch_bounds__(kMergeThreads) k_hc_concat(HcConcatArgs a) {
     }
   if (tid == 0 && (base < tot || tile == 0) &&
       (uint64_t(tile + 1) * kMergeTile >= tot)) {  // the tile holding the last position
-    const uint64_t total = s_excl + agg;
+    const uint64_t total = excl + agg;
     if (total > a.o_cap) atomicOr(a.err, kErrCapacity);
     *a.o_cnt = total;
   }
-  if (finish_tile(a.ctl, gridDim.x, /*sys=*/true)) {
-    if (tid == 0) __threadfence_system();
+  // the last tile: every tile has read its segments and the tag (as k_hc_merge)
+  if (blockIdx.x == gridDim.x - 1) {
+    if (tid == 0) {
+      const uint32_t t = (tag + 1u) & 0xFFFFFFu;
+      a.ctl->tag = t ? t : 1u;
+      __threadfence_system();
+    }
     __syncthreads();
     if (tid < n && a.done[tid]) st_release_sys(a.done[tid], ep);
   }

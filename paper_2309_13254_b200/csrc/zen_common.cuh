@@ -251,6 +251,57 @@ __device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, ui
   return exclusive;
 }
 
+// Block-wide decoupled look-back: the block's threads inspect blockDim.x
+// predecessors per round trip (the warp form: 32), for grids whose tiles are
+// all in flight at once, where a tile deep in the wave would otherwise walk
+// back window by window.  Every thread calls it after the block knows its
+// aggregate; returns the exclusive prefix on every thread.  s_red: >= 32 words.
+__device__ __forceinline__ uint64_t lookback_block(unsigned long long* status, uint32_t tile,
+                                                   uint32_t tag, uint64_t aggregate,
+                                                   unsigned long long* s_red) {
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tile == 0) {
+    if (tid == 0) st_relaxed_gpu(status, lb_pack(tag, LB_FLAG_PRE, aggregate));
+    return 0;
+  }
+  if (tid == 0) st_relaxed_gpu(status + tile, lb_pack(tag, LB_FLAG_AGG, aggregate));
+  const uint64_t tagbits = (uint64_t)(tag & 0xFFFFFFu);
+  uint64_t exclusive = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (true) {
+    const int64_t t = base - (int64_t)tid;  // thread i looks i tiles further back
+    uint64_t flag = LB_FLAG_PRE, val = 0;   // t < 0: the virtual predecessor of tile 0
+    if (t >= 0) {
+      while (true) {
+        const uint64_t w = ld_relaxed_gpu(status + t);
+        flag = ((w >> 40) == tagbits) ? ((w >> 38) & 3ull) : 0ull;
+        if (flag) {
+          val = w & LB_VAL_MASK;
+          break;
+        }
+        __nanosleep(32);
+      }
+    }
+    const uint32_t pm = __ballot_sync(0xffffffffu, flag == LB_FLAG_PRE);
+    if (lane == 0) s_red[warp] = pm ? (uint64_t)(warp * 32 + __ffs(pm) - 1) : ~0ull;
+    __syncthreads();
+    uint64_t stop = ~0ull;
+    for (uint32_t w = 0; w < nw; ++w) stop = s_red[w] < stop ? s_red[w] : stop;
+    uint64_t c = (stop != ~0ull && tid > stop) ? 0 : val;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __syncthreads();
+    if (lane == 0) s_red[warp] = c;
+    __syncthreads();
+    for (uint32_t w = 0; w < nw; ++w) exclusive += s_red[w];
+    __syncthreads();
+    if (stop != ~0ull) break;
+    base -= (int64_t)blockDim.x;
+  }
+  if (tid == 0) st_relaxed_gpu(status + tile, lb_pack(tag, LB_FLAG_PRE, exclusive + aggregate));
+  return exclusive;
+}
+
 // Dynamic tile ticket; ensures tiles start in order so look-back progresses.
 __device__ __forceinline__ uint32_t take_ticket(zen::LookbackCtl* ctl, uint32_t* smem_slot) {
   if (threadIdx.x == 0) *smem_slot = atomicAdd(&ctl->ticket, 1u);
