@@ -750,8 +750,17 @@ class AutoSynchronizer:
     aggregate (bit-identical at every rank)."""
 
     def __init__(self, n: int, universe: int, rank: int, max_nnz: int, params=None,
-                 profile_rounds: int = 1, group=None):
+                 profile_rounds: int = 1, group=None, policy: str = "cost-model"):
+        """policy "cost-model": select_scheme on the profiled ladder (the
+        reference's rule).  policy "measured": after profiling, time a few
+        syncs of each scheme on the device (CUDA events, max over ranks) and
+        keep the faster -- the traffic model ignores per-stage latency, which
+        on NVLink can decide (at N=4 the model ties BP and HC)."""
         from .zen import BPSynchronizer
+        if policy not in ("cost-model", "measured"):
+            raise Error(f"unknown policy {policy}")
+        self.policy = policy
+        self.measured_ms = None
         self.n, self.m, self.rank, self.group = n, universe, rank, group
         self.profile_rounds = profile_rounds
         self.bp = BPSynchronizer(n, universe, max_nnz, params, rank=rank)
@@ -798,12 +807,39 @@ class AutoSynchronizer:
                 else BALANCED_PARALLELISM
             self._active = self.bp if self.choice == BALANCED_PARALLELISM else self.hc
 
+    def _measure(self, dense, reps: int = 5):
+        import torch
+        import torch.distributed as dist
+        stream = torch.cuda.current_stream()
+        t = {}
+        for name, run in [(BALANCED_PARALLELISM, lambda: self.bp.sync_dense([dense])),
+                          (HIERARCHICAL_CENTRALIZATION, lambda: self.hc.sync_dense(dense))]:
+            run()
+            (self.bp if name == BALANCED_PARALLELISM else self.hc).wait()
+            dist.barrier(group=self.group)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                run()
+            e1.record(stream)
+            (self.bp if name == BALANCED_PARALLELISM else self.hc).wait()
+            x = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64,
+                             device="cpu" if dist.get_backend(self.group) == "gloo" else "cuda")
+            dist.all_reduce(x, op=dist.ReduceOp.MAX, group=self.group)
+            t[name] = float(x.item())
+        self.measured_ms = t
+        self.choice = min(t, key=t.get)
+        self._active = self.bp if self.choice == BALANCED_PARALLELISM else self.hc
+
     def sync_dense(self, dense):
         if self.choice is None:
             self._last = self.hc
             self.hc.sync_dense(dense)
             self.hc.wait()
             self._observe()
+            if self.choice is not None and self.policy == "measured":
+                self._measure(dense)  # both ran this input: either holds its result
+                self._last = self._active
             return
         self._last = self._active
         if self._active is self.bp:

@@ -119,6 +119,20 @@ def main():
             print(f"RANK {rank} auto profile MISMATCH {auto.profile} vs {prof}", flush=True)
             ok = False
     del auto
+    # the measured policy: both schemes timed on the device, the faster kept
+    auto = zen.AutoSynchronizer(world, m, rank, max_nnz=per * width + 1024, policy="measured")
+    auto.connect_process_group()
+    for it in range(2):
+        auto.sync_dense(mine)
+        auto.wait()
+        ai, _ = auto.result()
+        if not np.array_equal(ai.cpu().numpy().view(np.uint64), want.idx):
+            print(f"RANK {rank} auto(measured) iter {it} index MISMATCH", flush=True)
+            ok = False
+    if world & (world - 1) == 0 and (auto.measured_ms is None or auto.choice not in auto.measured_ms):
+        print(f"RANK {rank} auto(measured) no choice {auto.measured_ms}", flush=True)
+        ok = False
+    del auto
     # the centralized baselines in rank mode (f4): ring centralization and
     # AGsparse point-to-point, same push + fold machinery
     sparse_in = [co.to_sparse(d) for d in dense]
