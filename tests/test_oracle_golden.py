@@ -319,3 +319,25 @@ def test_baseline_schemes_golden(co):
             assert (bal is None) == (key not in g)
             if bal is not None:
                 assert tuple(bal) == tuple(g[key])
+
+
+def test_baseline_schemes_restatement_vs_reference(co, ro):
+    """The f4 restatement against the compiled reference on fresh random cases
+    (any n for AGsparse / OmniReduce; powers of two for the ring)."""
+    rng = np.random.default_rng(41)
+    for trial in range(8):
+        n = int(rng.integers(2, 9))
+        m = int(rng.integers(500, 5000))
+        ins = ro.generate(m, n, 0.01 + 0.01 * int(rng.integers(0, 4)),
+                          0.25 * int(rng.integers(0, 4)), int(rng.integers(1, 1 << 30)))
+        runs = [("agsparse", None, None, 256), ("omnireduce", None, "tensor_block",
+                                                  int(rng.integers(1, 100)))]
+        if n & (n - 1) == 0:
+            runs += [("ring-centralization", None, None, 256), ("agsparse", "hierarchy", None, 256)]
+        for name, comm, kind, bs in runs:
+            a = ro.run_scheme(name, m, ins, comm, kind, bs)
+            b = co.run_scheme(name, m, ins, comm, kind, bs)
+            for (ai, av), (bi, bv) in zip(a[0], b[0]):
+                assert np.array_equal(ai, bi) and np.array_equal(av.view(np.uint32),
+                                                                 bv.view(np.uint32))
+            assert np.array_equal(a[1], b[1]) and a[2] == b[2], (trial, name)
