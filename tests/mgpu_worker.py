@@ -173,6 +173,36 @@ def main():
                       flush=True)
                 ok = False
         del sy
+    # edge cases through sync_sparse: an empty rank, all empty, and values
+    # that cancel across ranks (OmniReduce's block decode drops exact zeros)
+    rng = np.random.default_rng(99)
+    mm = 5000
+    base_idx = np.sort(rng.choice(mm, 40, replace=False)).astype(np.uint64)
+    cases = {
+        "one_empty": [(np.zeros(0, np.uint64), np.zeros(0, np.float32)) if w == 0 else
+                      (np.sort(rng.choice(mm, 30, replace=False)).astype(np.uint64),
+                       rng.integers(1, 9, 30).astype(np.float32)) for w in range(world)],
+        "all_empty": [(np.zeros(0, np.uint64), np.zeros(0, np.float32)) for _ in range(world)],
+        "cancel": [(base_idx, np.full(40, 1.0 if w % 2 == 0 else -1.0, np.float32))
+                   for w in range(world)],
+    }
+    for cname, ins in cases.items():
+        for scheme, name in [("hc", "sparcml"), ("ring", "ring-centralization"),
+                             ("agsparse", "agsparse"), ("omnireduce", "omnireduce")]:
+            if scheme in ("hc", "ring") and world & (world - 1):
+                continue
+            sy = zen.HCSynchronizer(world, mm, rank, max_nnz=64, scheme=scheme)
+            sy.connect_process_group()
+            res, _, _ = co.run_scheme(name, mm, ins)
+            i, v = ins[rank]
+            sy.sync_sparse(torch.from_numpy(i.view(np.int64)).cuda(), torch.from_numpy(v).cuda())
+            gi, gv = sy.result()
+            if not (np.array_equal(gi.cpu().numpy().view(np.uint64), res[rank][0]) and
+                    np.array_equal(gv.cpu().numpy().view(np.uint32), res[rank][1].view(np.uint32))):
+                print(f"RANK {rank} {scheme} {cname} MISMATCH {gi.numel()} vs {res[rank][0].size}",
+                      flush=True)
+                ok = False
+            del sy
     flag = torch.tensor([0 if ok else 1], device="cuda" if world <= ngpu else "cpu")
     dist.all_reduce(flag)
     if rank == 0:
