@@ -637,10 +637,6 @@ def _block_sizes(i, m, n, p, block_size):
     return 64 * blocks, value
 
 
-class _TbMsg(_Sized):
-    pass
-
-
 def run_omnireduce_like(inputs, net: SimNet, block_size: int = 256) -> SyncOutcome:
     """zen::run_omnireduce_like (schemes.hpp:219-328): contiguous ranges, block
     transport to the range owner, per-range aggregate in worker order, block
@@ -656,12 +652,12 @@ def run_omnireduce_like(inputs, net: SimNet, block_size: int = 256) -> SyncOutco
         for p in range(n):
             if p == w or slices[w][p][0].numel() == 0:
                 continue
-            net.send(0, w, p, _TbMsg(*_block_sizes(slices[w][p][0], m, n, p, block_size)))
+            net.send(0, w, p, _Sized(*_block_sizes(slices[w][p][0], m, n, p, block_size)))
     aggregated = [_fold_dev([slices[w][p] for w in range(n)], m) for p in range(n)]
     for p in range(n):
         if aggregated[p][0].numel() == 0:
             continue
-        sz = _TbMsg(*_block_sizes(aggregated[p][0], m, n, p, block_size))
+        sz = _Sized(*_block_sizes(aggregated[p][0], m, n, p, block_size))
         for w in range(n):
             if w != p:
                 net.send(1, p, w, sz)
