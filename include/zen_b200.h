@@ -244,6 +244,10 @@ zen_status zen_hc_create(zen_ctx* ctx, uint32_t n, uint32_t rank, uint64_t unive
 #define ZEN_SCHEME_OMNIREDUCE 3u /* run_omnireduce_like, zen/schemes.hpp:219-328 (n >= 2):
                                     ranges -> owners, fold, owners' ranges -> all,
                                     concat with exact zeros dropped */
+#define ZEN_SCHEME_AGSPARSE_RING 4u /* run_agsparse, CommPattern::Ring (zen/schemes.hpp:132-142):
+                                       stage s forwards the input of rank - s to rank + 1 */
+#define ZEN_SCHEME_AGSPARSE_HIER 5u /* run_agsparse, CommPattern::Hierarchy (:143-160):
+                                       stage s sends every held input to rank ^ 2^s */
 zen_status zen_hc_create_scheme(zen_ctx* ctx, uint32_t scheme, uint32_t n, uint32_t rank,
                                 uint64_t universe, uint64_t max_nnz, zen_hc** out);
 uint32_t zen_hc_pushes(const zen_hc* hc); /* pushes per sync (entries of zen_hc_stage_counts) */

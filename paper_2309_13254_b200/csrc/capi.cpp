@@ -4,6 +4,7 @@
 // gradient data is touched only by the sm_100a kernels in k_*.cu.  There is no
 // CPU fallback: a missing or non-sm_100 device is an error.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -2316,7 +2317,8 @@ struct HcPush {
   int src;
   uint32_t dst, slot;
   uint64_t cap;
-  int src_bnd = -1;  // OmniReduce: the source is input range [bnd[i], bnd[i+1])
+  int src_bnd = -1;   // OmniReduce: the source is input range [bnd[i], bnd[i+1])
+  int src_wait = -1;  // AGsparse forwarding: the source slot's ready flag to acquire
 };
 struct HcMerge {
   int a, b, out;
@@ -2484,12 +2486,49 @@ void hc_plan(zen_hc* h) {
     for (uint32_t p = 0; p < n; ++p) h->buf_cap.push_back(rcap(p));  // owners' ranges
     h->omni_acc = acc;
     h->result_buf = s1.concat_out;
-  } else {  // AGsparse point-to-point: slot j holds worker j's input
-    HcStage st;
-    for (uint32_t q = 0; q < n; ++q)
-      if (q != r) st.push.push_back({kBufIn, q, r, capk(1)});
+  } else {  // AGsparse (zen/schemes.hpp:119-168): slot j holds worker j's input
+    // pushes of one rank, in order: (stage, destination, origin), per pattern
+    const uint32_t pattern = h->scheme;
+    auto pushes_of = [&](uint32_t q) {
+      std::vector<std::array<uint32_t, 3>> v;
+      if (pattern == ZEN_SCHEME_AGSPARSE) {  // point-to-point: one stage
+        for (uint32_t d = 0; d < n; ++d)
+          if (d != q) v.push_back({0u, d, q});
+      } else if (pattern == ZEN_SCHEME_AGSPARSE_RING) {  // stage s forwards origin q - s
+        for (uint32_t st = 0; st + 1 < n; ++st) v.push_back({st, (q + 1) % n, (q + n - st) % n});
+      } else {  // hierarchy: stage s sends every held origin to q ^ 2^s
+        std::vector<uint32_t> hold{q};
+        for (uint32_t bit = 1, st = 0; bit < n; bit <<= 1, ++st) {
+          for (uint32_t o : hold) v.push_back({st, q ^ bit, o});
+          // the partner held the same-size aligned group: origins of its group
+          const uint32_t base = (q ^ bit) & ~(bit - 1);
+          for (uint32_t o = base; o < base + bit; ++o) hold.push_back(o);
+        }
+      }
+      return v;
+    };
+    // who delivered origin o to this rank, and as which of its pushes
+    std::vector<int> from(n, -1), from_idx(n, -1);
+    for (uint32_t q = 0; q < n; ++q) {
+      if (q == r) continue;
+      const auto v = pushes_of(q);
+      for (size_t i = 0; i < v.size(); ++i)
+        if (v[i][1] == r) {
+          from[v[i][2]] = int(q);
+          from_idx[v[i][2]] = int(i);
+        }
+    }
     auto in_of = [&](uint32_t w) { return w == r ? kBufIn : kBufRecv + int(w); };
-    auto push_idx = [&](uint32_t sender) { return int(r < sender ? r : r - 1); };
+    const auto mine = pushes_of(r);
+    uint32_t nst = 0;
+    for (const auto& e : mine) nst = std::max(nst, e[0] + 1);
+    h->plan.assign(std::max(nst, 1u), HcStage{});
+    for (const auto& e : mine) {
+      HcPush p{in_of(e[2]), e[1], e[2], capk(1)};
+      p.src_wait = e[2] == r ? -1 : int(e[2]);  // a forwarded origin must have arrived
+      h->plan[e[0]].push.push_back(p);
+    }
+    HcStage& last = h->plan.back();
     int acc = in_of(0);
     for (uint32_t w = 1; w < n; ++w) {
       const int out = (w & 1) ? kBufSt0 : kBufSt1;
@@ -2497,18 +2536,17 @@ void hc_plan(zen_hc* h) {
       int k = 0;
       if (w == 1 && r != 0) {  // worker 0's input arrives too
         mg.wait[k] = 0;
-        mg.done_rank[k] = 0;
-        mg.done_idx[k++] = push_idx(0);
+        mg.done_rank[k] = from[0];
+        mg.done_idx[k++] = from_idx[0];
       }
       if (w != r) {
         mg.wait[k] = int(w);
-        mg.done_rank[k] = int(w);
-        mg.done_idx[k++] = push_idx(w);
+        mg.done_rank[k] = from[w];
+        mg.done_idx[k++] = from_idx[w];
       }
-      st.merge.push_back(mg);
+      last.merge.push_back(mg);
       acc = out;
     }
-    h->plan.push_back(st);
     // every rank's arena must have the same layout: peers address it with
     // their own offsets (this rank's own slot stays unused)
     for (uint32_t j = 0; j < n; ++j) h->buf_cap.push_back(capk(1));
@@ -2552,6 +2590,7 @@ zen_status hc_enqueue(zen_hc* h, const float* dense, const uint64_t* in_idx, con
       a.err = &me->err;
       a.sent_cnt = &me->sent[pi++];
       a.src_bnd = p.src_bnd >= 0 ? &me->bnd[p.src_bnd] : nullptr;
+      a.src_wait = p.src_wait >= 0 ? &me->ready[p.src_wait] : nullptr;
       launch_hc_push(a, st);
     }
     for (const HcMerge& mg : stg.merge) {
@@ -2622,11 +2661,13 @@ extern "C" {
 zen_status zen_hc_create_scheme(zen_ctx* c, uint32_t scheme, uint32_t n, uint32_t rank,
                                 uint64_t universe, uint64_t max_nnz, zen_hc** out) {
   if (!c || !out) return fail(ZEN_E_INVALID, "null argument");
-  if (scheme > ZEN_SCHEME_OMNIREDUCE) return fail(ZEN_E_INVALID, "unknown scheme");
+  if (scheme > ZEN_SCHEME_AGSPARSE_HIER) return fail(ZEN_E_INVALID, "unknown scheme");
   const bool pow2 = n != 0 && (n & (n - 1)) == 0;
   if (scheme == ZEN_SCHEME_OMNIREDUCE && n < 2)
     return fail(ZEN_E_INVALID, "synchronization needs at least two nodes");
-  if (n == 0 || ((scheme == ZEN_SCHEME_HC || scheme == ZEN_SCHEME_RING) && !pow2))
+  if (n == 0 || ((scheme == ZEN_SCHEME_HC || scheme == ZEN_SCHEME_RING ||
+                  scheme == ZEN_SCHEME_AGSPARSE_RING || scheme == ZEN_SCHEME_AGSPARSE_HIER) &&
+                 !pow2))
     return fail(ZEN_E_INVALID, "node count must be a power of two");
   if (n > kHcMaxRanks) return fail(ZEN_E_INVALID, "node count above 256");
   if (rank >= n) return fail(ZEN_E_INVALID, "rank out of range");

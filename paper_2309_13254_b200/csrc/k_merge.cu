@@ -284,6 +284,9 @@ __global__ void __launch_bounds__(256) k_hc_push(HcPushArgs a) {
   // the partner consumed what this rank pushed into the same buffer last sync
   if (tid == 0 && ep > 1 && !wait_flag(a.done_flag, ep - 1, kPeerTimeoutNs))
     atomicOr(a.err, kErrTimeout);
+  // a forwarded tensor: it must have arrived in this rank's slot
+  if (tid == 0 && a.src_wait && !wait_flag(a.src_wait, ep, kPeerTimeoutNs))
+    atomicOr(a.err, kErrTimeout);
   __syncthreads();
   uint64_t n = *(volatile const uint64_t*)a.src_cnt;
   uint64_t off = 0;

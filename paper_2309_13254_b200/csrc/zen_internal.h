@@ -343,6 +343,7 @@ struct HcPushArgs {
   uint32_t* err;
   uint64_t* sent_cnt;  // receives the pushed count (the ledger)
   const uint64_t* src_bnd;  // optional [begin, end) of the source (device words)
+  const unsigned long long* src_wait;  // optional local ready flag of the source (forwarding)
 };
 // n sorted, index-disjoint, ascending segments -> one tensor, exact zeros
 // dropped (the block decode of run_omnireduce_like, zen/schemes.hpp:289-295)

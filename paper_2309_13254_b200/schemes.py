@@ -396,18 +396,21 @@ class HCSynchronizer:
     Counts stay on the device; sync_dense replays one CUDA graph.  Every rank
     ends with aggregate(inputs), bit for bit."""
 
-    SCHEMES = {"hc": 0, "ring": 1, "agsparse": 2, "omnireduce": 3}
+    SCHEMES = {"hc": 0, "ring": 1, "agsparse": 2, "omnireduce": 3, "agsparse-ring": 4,
+               "agsparse-hierarchy": 5}
 
     def __init__(self, n: int, universe: int, rank: int, max_nnz: int,
                  fmt: WireFormat | None = None, device: int | None = None,
                  scheme: str = "hc"):
         """scheme: "hc" (run_hier_centralization), "ring"
         (run_ring_centralization), "agsparse" (run_agsparse point-to-point,
-        any n) or "omnireduce" (run_omnireduce_like, any n >= 2) -- the same
-        NVLink push + device fold machinery."""
+        any n), "agsparse-ring" / "agsparse-hierarchy" (run_agsparse with the
+        ring / hierarchy forwarding patterns) or "omnireduce"
+        (run_omnireduce_like, any n >= 2) -- the same NVLink push + device
+        fold machinery."""
         if scheme not in self.SCHEMES:
             raise Error(f"unknown scheme {scheme}")
-        if scheme in ("hc", "ring") and not _pow2(n):
+        if scheme in ("hc", "ring", "agsparse-ring", "agsparse-hierarchy") and not _pow2(n):
             raise NonPowerOfTwo()
         if fmt is not None and fmt.kind not in ("coo", "bitmap"):
             raise Error("rank-mode ledger supports COO and bitmap formats")

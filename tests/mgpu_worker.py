@@ -155,12 +155,14 @@ def main():
                   f"{sc} {slices}", flush=True)
             ok = False
     del om
-    for scheme, name in [("ring", "ring-centralization"), ("agsparse", "agsparse")]:
-        if scheme == "ring" and world & (world - 1):
+    for scheme, name, comm in [("ring", "ring-centralization", None), ("agsparse", "agsparse", None),
+                               ("agsparse-ring", "agsparse", "ring"),
+                               ("agsparse-hierarchy", "agsparse", "hierarchy")]:
+        if scheme != "agsparse" and world & (world - 1):
             continue
         sy = zen.HCSynchronizer(world, m, rank, max_nnz=per * width + 1024, scheme=scheme)
         sy.connect_process_group()
-        res, led, _ = co.run_scheme(name, m, sparse_in)
+        res, led, _ = co.run_scheme(name, m, sparse_in, comm)
         for it in range(2):
             sy.sync_dense(mine)
             gi, gv = sy.result()
@@ -187,13 +189,15 @@ def main():
                    for w in range(world)],
     }
     for cname, ins in cases.items():
-        for scheme, name in [("hc", "sparcml"), ("ring", "ring-centralization"),
-                             ("agsparse", "agsparse"), ("omnireduce", "omnireduce")]:
-            if scheme in ("hc", "ring") and world & (world - 1):
+        for scheme, name, comm in [("hc", "sparcml", None), ("ring", "ring-centralization", None),
+                                   ("agsparse", "agsparse", None),
+                                   ("agsparse-hierarchy", "agsparse", "hierarchy"),
+                                   ("omnireduce", "omnireduce", None)]:
+            if scheme in ("hc", "ring", "agsparse-hierarchy") and world & (world - 1):
                 continue
             sy = zen.HCSynchronizer(world, mm, rank, max_nnz=64, scheme=scheme)
             sy.connect_process_group()
-            res, _, _ = co.run_scheme(name, mm, ins)
+            res, _, _ = co.run_scheme(name, mm, ins, comm)
             i, v = ins[rank]
             sy.sync_sparse(torch.from_numpy(i.view(np.int64)).cuda(), torch.from_numpy(v).cuda())
             gi, gv = sy.result()
