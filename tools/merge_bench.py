@@ -48,11 +48,12 @@ def main():
             for _ in range(10):
                 schemes._merge_dev(a, av, b, bv, m)
             torch.cuda.synchronize()
+        import re
         ks = {}
         for e in prof.events():
             if e.device_type.name == "CUDA":
-                nm = e.name.split("(")[0].replace("(anonymous namespace)::", "")
-                nm = nm.split("::")[-1] if "::" in nm else nm
+                mm = re.search(r"(k_\w+)", e.name)
+                nm = mm.group(1) if mm else e.name.split("(")[0].strip()
                 ks.setdefault(nm, []).append(e.device_time_total)
         out["kernel_us"] = {k: round(sum(v) / len(v), 2) for k, v in ks.items()}
         u = schemes._merge_dev(a, av, b, bv, m)[0].numel()
