@@ -1135,10 +1135,11 @@ extern "C" zen_status zen_merge_sum(zen_ctx* c, const uint64_t* a_idx, const flo
   // one merge-path kernel (k_merge.cu); counts in device memory
   const uint32_t tiles = hc_merge_tiles(na + nb);
   Bump sc;
-  CKR(ctx_scratch(c, bump_bytes({32, sizeof(LookbackCtl), 8ull * tiles}), &sc));
+  CKR(ctx_scratch(c, bump_bytes({32, sizeof(LookbackCtl), 8ull * tiles, 8ull * (tiles + 2)}), &sc));
   uint64_t* st = sc.get<uint64_t>(4);  // [na, nb, out count, status]
   LookbackCtl* ctl = sc.get<LookbackCtl>(1);
   unsigned long long* lb = sc.get<unsigned long long>(tiles);
+  uint64_t* splits = sc.get<uint64_t>(tiles + 2);
   const uint64_t h_in[4] = {na, nb, 0, 0};
   CK(cudaMemcpyAsync(st, h_in, 32, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(ctl, 0, sizeof(LookbackCtl), c->stream));
@@ -1163,6 +1164,7 @@ extern "C" zen_status zen_merge_sum(zen_ctx* c, const uint64_t* a_idx, const flo
   m.lb_status = lb;
   m.ctl = ctl;
   m.err = err + 1;  // merge bits apart from the input check's
+  m.splits = splits;
   launch_hc_merge(m, tiles, c->stream);
   uint64_t h[4];
   CK(cudaMemcpyAsync(h, st, 32, cudaMemcpyDeviceToHost, c->stream));
@@ -2353,6 +2355,7 @@ struct zen_hc {
   DevMem mem;
   ExtractWs<uint64_t> ex{};
   unsigned long long* lb = nullptr;
+  uint64_t* splits = nullptr;
   LookbackCtl* ctl_merge = nullptr;
   LookbackCtl* ctl_push = nullptr;
   cudaGraph_t gdef = nullptr;
@@ -2619,6 +2622,7 @@ zen_status hc_enqueue(zen_hc* h, const float* dense, const uint64_t* in_idx, con
       a.epoch = &me->epoch;
       a.a_bnd = mg.a_bnd >= 0 ? &me->bnd[mg.a_bnd] : nullptr;
       a.b_bnd = mg.b_bnd >= 0 ? &me->bnd[mg.b_bnd] : nullptr;
+      a.splits = h->splits;
       launch_hc_merge(a, hc_merge_tiles(mg.a_cap + mg.b_cap), st);
     }
     if (stg.concat_out >= 0) {
@@ -2711,6 +2715,7 @@ zen_status zen_hc_create_scheme(zen_ctx* c, uint32_t scheme, uint32_t n, uint32_
     for (const auto& mg : stg.merge)
       max_tiles = std::max<uint64_t>(max_tiles, hc_merge_tiles(mg.a_cap + mg.b_cap));
   CKR(h->mem.alloc(&h->lb, max_tiles));
+  CKR(h->mem.alloc(&h->splits, max_tiles + 2));
   CKR(h->mem.alloc(&h->ctl_merge, 1));
   CKR(h->mem.alloc(&h->ctl_push, 1));
   CK(cudaStreamSynchronize(c->stream));

@@ -327,6 +327,8 @@ struct HcMergeArgs {
   uint64_t* stage_cnt;                   // receives |a| (the ledger), may be null
   const uint64_t* a_bnd;                 // optional [begin, end) of a / b inside their
   const uint64_t* b_bnd;                 // buffers (device words; count = end - begin)
+  uint64_t* splits;                      // optional [tiles + 1]: the tiles' merge-path splits,
+                                         // computed by a one-wave pre-pass (k_hc_splits)
 };
 struct HcPushArgs {
   const uint64_t* src_idx;
