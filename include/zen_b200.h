@@ -251,6 +251,9 @@ zen_status zen_hc_create(zen_ctx* ctx, uint32_t n, uint32_t rank, uint64_t unive
 zen_status zen_hc_create_scheme(zen_ctx* ctx, uint32_t scheme, uint32_t n, uint32_t rank,
                                 uint64_t universe, uint64_t max_nnz, zen_hc** out);
 uint32_t zen_hc_pushes(const zen_hc* hc); /* pushes per sync (entries of zen_hc_stage_counts) */
+/* this rank's input entries and result entries of the last sync (the
+ * OmniReduce balance, zen/schemes.hpp:297-313, is built from these + the pushes) */
+zen_status zen_hc_counts(zen_hc* hc, uint64_t* input_count, uint64_t* result_count);
 void zen_hc_destroy(zen_hc* hc);
 zen_status zen_hc_ipc_handle(zen_hc* hc, void* out); /* ZEN_IPC_HANDLE_BYTES */
 zen_status zen_hc_connect(zen_hc* hc, const void* handles); /* n handles, rank-major */

@@ -72,6 +72,7 @@ _SIGS = {
     "zen_hc_create": (C.c_int, [vp, u32, u32, u64, u64, P(vp)]),
     "zen_hc_create_scheme": (C.c_int, [vp, u32, u32, u32, u64, u64, P(vp)]),
     "zen_hc_pushes": (u32, [vp]),
+    "zen_hc_counts": (C.c_int, [vp, P(u64), P(u64)]),
     "zen_hc_destroy": (None, [vp]),
     "zen_hc_ipc_handle": (C.c_int, [vp, vp]),
     "zen_hc_connect": (C.c_int, [vp, vp]),

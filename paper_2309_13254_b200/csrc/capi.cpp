@@ -2916,6 +2916,16 @@ zen_status zen_hc_stage_counts(zen_hc* h, uint64_t* counts) {
   return ZEN_OK;
 }
 
+zen_status zen_hc_counts(zen_hc* h, uint64_t* input_count, uint64_t* result_count) {
+  if (!h) return fail(ZEN_E_INVALID, "null argument");
+  CKR(zen_hc_wait(h));
+  HcHdr hh;
+  CK(cudaMemcpy(&hh, h->base, sizeof(HcHdr), cudaMemcpyDeviceToHost));
+  if (input_count) *input_count = hh.cnt[kBufIn];
+  if (result_count) *result_count = h->h_result;
+  return ZEN_OK;
+}
+
 uint32_t zen_hc_pushes(const zen_hc* h) {
   uint32_t c = 0;
   if (h)

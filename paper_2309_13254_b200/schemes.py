@@ -485,6 +485,38 @@ class HCSynchronizer:
         _check(_lib().zen_hc_stage_counts(self.h, out))
         return [int(out[i]) for i in range(ns)]
 
+    def balance(self, group=None):
+        """OmniReduce-like only: BalanceDetails(push, pull) of the last sync as
+        run_omnireduce_like reports them (schemes.hpp:297-313): push = max over
+        workers w and ranges p of n*|slice_wp|/|I_w|, pull = max over owners
+        of n*|range aggregate|/union; None when some input is empty.  Collective
+        over the ranks (all-gathers the counts)."""
+        import torch
+        import torch.distributed as dist
+        from .zen import BalanceDetails
+        if self.scheme != "omnireduce":
+            raise Error("balance is reported by the OmniReduce-like scheme")
+        n, r = self.n, self.rank
+        inp, res = C.c_uint64(), C.c_uint64()
+        _check(_lib().zen_hc_counts(self.h, C.byref(inp), C.byref(res)))
+        sc = self.sent_counts()
+        slices = sc[:n - 1]
+        own = inp.value - sum(slices)
+        row = slices[:r] + [own] + slices[r:]  # slice p of this rank's input, p = 0..n-1
+        agg = sc[n - 1] if n > 1 else own  # |aggregate of this rank's range|
+        dev = "cpu" if dist.get_backend(group) == "gloo" else "cuda"
+        t = torch.tensor([float(inp.value), float(agg)] + [float(x) for x in row],
+                         dtype=torch.float64, device=dev)
+        allt = [torch.zeros_like(t) for _ in range(n)]
+        dist.all_gather(allt, t, group=group)
+        rows = [x.cpu().numpy() for x in allt]
+        if any(x[0] == 0 for x in rows):
+            return None
+        push = max(float(n) * float(x[2 + p]) / float(x[0]) for x in rows for p in range(n))
+        loads = [float(x[1]) for x in rows]
+        pull = max(float(n) * ld / float(sum(loads)) for ld in loads)
+        return BalanceDetails(push, pull)
+
     def stage_bits(self):
         """[(index_bits, value_bits)] this rank sent per push, in plan order
         (HC / ring: one per stage; AGsparse: one per peer) -- its row of the

@@ -150,6 +150,10 @@ def main():
             np.array_equal(gv.cpu().numpy().view(np.uint32), res[rank][1].view(np.uint32))
         sc = om.sent_counts()
         good = good and sc[:world - 1] == slices and len(set(sc[world - 1:])) == 1
+        bal = om.balance(None if world <= ngpu else None)
+        _, _, wbal = co.run_scheme("omnireduce", m, sparse_in_all)
+        good = good and bal is not None and wbal is not None and \
+            (bal.push_imbalance, bal.pull_imbalance) == tuple(wbal)
         if not good:
             print(f"RANK {rank} omnireduce iter {it} MISMATCH {gi.numel()} vs {res[rank][0].size} "
                   f"{sc} {slices}", flush=True)
