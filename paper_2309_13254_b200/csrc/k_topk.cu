@@ -132,16 +132,35 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist2(const float* __restrict
                                                          uint32_t* __restrict__ cand_key,
                                                          uint32_t cand_cap) {
   zen_dev::pdl_entry();
+  // candidates are staged per block in shared memory and flushed with ONE
+  // global reservation per flush: with a dense layer the threshold bucket is
+  // hit in most warps of every pass, and a global counter per warp serialises
+  constexpr uint32_t kStage = 2 * kThreads * 8;
   __shared__ uint32_t sh[kBins];
+  __shared__ uint32_t sbuf[kStage];
+  __shared__ uint32_t s_n, s_base;
   for (int i = threadIdx.x; i < kBins; i += kThreads) sh[i] = 0;
+  if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
   const uint32_t top = st->prefix >> 21;
   const uint64_t nvec = m / 8;
   const bool vec_ok = (reinterpret_cast<uintptr_t>(dense) & 31u) == 0;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   const uint32_t lane = lane_id();
+  auto flush = [&]() {  // block-wide: move the staged keys to the global list
+    __syncthreads();
+    const uint32_t cnt = s_n;
+    if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&st->ncand, cnt);
+    __syncthreads();
+    const uint32_t b = s_base;
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads)
+      if (b + i < cand_cap) cand_key[b + i] = sbuf[i];
+    __syncthreads();
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+  };
   for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < (vec_ok ? nvec : 0);
-       base += stride) {
+       base += stride) {  // block-uniform trip count
     const uint64_t u = base + threadIdx.x;
     f8 v;
     if (u < nvec) v = ld_stream_f8(dense + u * 8);
@@ -152,14 +171,19 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist2(const float* __restrict
       const uint32_t bal = __ballot_sync(0xffffffffu, hit);
       if (!bal) continue;
       uint32_t pos = 0;
-      if (lane == (uint32_t)(__ffs(bal) - 1)) pos = atomicAdd(&st->ncand, (uint32_t)__popc(bal));
+      if (lane == (uint32_t)(__ffs(bal) - 1)) pos = atomicAdd(&s_n, (uint32_t)__popc(bal));
       pos = __shfl_sync(0xffffffffu, pos, __ffs(bal) - 1) + __popc(bal & lanemask_lt());
       if (hit) {
-        if (pos < cand_cap) cand_key[pos] = key;
+        sbuf[pos] = key;  // pos < kStage: flushed whenever half full
         atomicAdd(&sh[(key >> 10) & (kBins - 1)], 1u);
       }
     }
+    __syncthreads();
+    const uint32_t staged = s_n;
+    __syncthreads();  // every thread has read s_n before any adds to it again
+    if (staged > kStage / 2) flush();  // block-uniform
   }
+  flush();
   const uint64_t tail0 = vec_ok ? nvec * 8 : 0;
   for (uint64_t i = tail0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < m; i += stride) {
     const uint32_t key = mag_key(dense[i]);
