@@ -364,7 +364,7 @@ def measure_extras(args, zen, d_dense, peak, reps=10):
     out["sparsify_topk"] = {
         "fraction": frac, "kept": int(got.value), "ms_per_call": round(t, 4),
         "hbm_frac_of_one_pass": round(one_pass / (t * 1e-3) / 1e9 / peak, 4),
-        "note": "radix select: 3 HBM passes over the dense input; frac vs a single 4M-byte read"}
+        "note": "radix select: 2 HBM passes over the dense input (histogram, bucket-floor tile pass); frac vs a single 4M-byte read"}
     # the wire formats of the extracted sparse gradient
     nz = torch.nonzero(d_dense).flatten()
     vals = d_dense[nz].contiguous()

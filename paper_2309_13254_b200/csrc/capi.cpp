@@ -189,8 +189,6 @@ struct TopkWs {
   uint64_t m = 0;
   void* state = nullptr;
   uint32_t* hist = nullptr;
-  uint32_t* cand = nullptr;
-  uint32_t cand_cap = 0;
   ExtractWs<uint32_t> ex{};
   uint32_t* tile_ties = nullptr;
   uint64_t *tie_base = nullptr, *out_base = nullptr, *out_count = nullptr;
@@ -1279,10 +1277,8 @@ extern "C" zen_status zen_sparsify_topk(zen_ctx* c, const float* d_dense, uint64
     c->topk.reset(new TopkWs);
     TopkWs& w = *c->topk;
     w.m = m;
-    w.cand_cap = uint32_t(std::min<uint64_t>(m, 8ull << 20));
     CKR(w.mem.alloc((uint8_t**)&w.state, topk_state_bytes()));
     CKR(w.mem.alloc(&w.hist, 2048));
-    CKR(w.mem.alloc(&w.cand, w.cand_cap, false));
     CKR(w.mem.alloc(&w.ex.st_idx, uint64_t(ntiles) * kExtractTile, false));
     CKR(w.mem.alloc(&w.ex.st_val, uint64_t(ntiles) * kExtractTile, false));
     CKR(w.mem.alloc(&w.ex.tile_cnt, ntiles));
@@ -1293,12 +1289,12 @@ extern "C" zen_status zen_sparsify_topk(zen_ctx* c, const float* d_dense, uint64
   }
   TopkWs& w = *c->topk;
   cudaStream_t st = c->stream;
-  launch_topk_select(d_dense, m, keep, w.state, w.hist, w.cand, w.cand_cap, st);
+  launch_topk_select(d_dense, m, keep, w.state, w.hist, st);
   launch_select_tiles(d_dense, m, w.ex,
                       reinterpret_cast<const uint32_t*>(static_cast<char*>(w.state) +
                                                         topk_threshold_offset()),
                       st);
-  launch_topk_finish(w.ex, ntiles, w.state, w.tile_ties, w.tie_base, w.out_base, w.out_count,
+  launch_topk_finish(w.ex, ntiles, w.state, w.hist, w.tile_ties, w.tie_base, w.out_base, w.out_count,
                      d_idx, d_val, capacity, st);
   CK(cudaGetLastError());
   uint64_t n = 0;

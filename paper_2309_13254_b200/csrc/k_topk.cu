@@ -9,18 +9,20 @@
 //
 // Radix select in three digit levels, [31:21] [20:10] [9:0]:
 //   hist1   full pass over the dense input, 2048-bin histogram of the top digit
-//   select  one block: the digit of the k-th largest key, elements above it
-//   hist2   full pass: histogram of the middle digit among keys in that bucket,
-//           which are also appended to a candidate list (key + index)
-//   select, hist3 over the candidates only, select -> threshold key T and the
-//           number r of T-ties to keep (the r lowest-indexed ones)
-//   tiles   full pass (the extraction tile kernel with predicate |v| >= T,
-//           non-zero): candidates staged tile-locally in index order
-//   scan    one block: per tile, ties before it -> entries it keeps -> output base
+//   select  one block: the digit of the k-th largest key; the bucket's lower
+//           bound becomes the staging threshold
+//   tiles   full pass (the extraction tile kernel with predicate
+//           |v| >= bucket floor, non-zero): every kept entry plus the rest of
+//           the threshold bucket staged tile-locally in index order
+//   hist2/3 over the staged entries only (a warp per tile), each followed by a
+//           select -> threshold key T and the number r of T-ties to keep (the
+//           r lowest-indexed ones)
+//   ties, scan  one block: per tile, ties before it -> entries it keeps -> base
 //   compact one block per tile: > T entries, plus ties while the global tie
 //           rank is below r, written in ascending index order.
-// Three HBM passes over the dense input in all; everything else touches the
-// candidates only.
+// Two HBM passes over the dense input in all (an earlier version collected
+// the bucket with a second full pass before the tile pass: three); everything
+// else touches the staged entries only.
 #include "zen_common.cuh"
 
 namespace zen {
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(1024) k_topk_select(uint32_t* __restrict__ his
   __shared__ uint32_t s_bin, s_above;
   constexpr int E = kBins / 1024;
   const uint32_t k = st->k;
+  if (threadIdx.x == 0) s_bin = 0xFFFFFFFFu;  // ordered by the scan's barriers
   // suffix sums from the top bin down: thread t owns bins [kBins-1-E*t-E+1 .. kBins-1-E*t]
   uint32_t c[E], local = 0;
 #pragma unroll
@@ -112,114 +115,39 @@ __global__ void __launch_bounds__(1024) k_topk_select(uint32_t* __restrict__ his
   __syncthreads();
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
   if (threadIdx.x == 0) {
-    const uint32_t bin = s_bin;
+    // levels 2 and 3 count staged (non-zero) keys only: a rank beyond them
+    // lies among the zeros of bucket 0, so the digit is 0 and T ends at 0
+    // (every non-zero kept)
+    const bool found = s_bin != 0xFFFFFFFFu;
+    const uint32_t bin = found ? s_bin : 0u, above = found ? s_above : tot;
     st->prefix |= bin << shift;
-    st->above += s_above;
-    st->k = k - s_above;
-    if (last) {
-      st->T = st->prefix;
-      st->r = st->k;  // ties of T that rank inside the top `keep`
-    }
+    st->above += above;
+    st->k = k - above;
+    st->T = st->prefix;  // level 1: the staging floor; last level: the threshold
+    if (last) st->r = st->k;  // ties of T that rank inside the top `keep`
   }
   (void)digit_bits;
 }
 
-// Level 2: full pass; keys whose top digit equals the chosen bucket feed the
-// middle-digit histogram and the candidate list
-__global__ void __launch_bounds__(kThreads) k_topk_hist2(const float* __restrict__ dense,
-                                                         uint64_t m, TopkState* st,
-                                                         uint32_t* __restrict__ hist,
-                                                         uint32_t* __restrict__ cand_key,
-                                                         uint32_t cand_cap) {
-  zen_dev::pdl_entry();
-  // candidates are staged per block in shared memory and flushed with ONE
-  // global reservation per flush: with a dense layer the threshold bucket is
-  // hit in most warps of every pass, and a global counter per warp serialises
-  constexpr uint32_t kStage = 2 * kThreads * 8;
-  __shared__ uint32_t sh[kBins];
-  __shared__ uint32_t sbuf[kStage];
-  __shared__ uint32_t s_n, s_base;
-  for (int i = threadIdx.x; i < kBins; i += kThreads) sh[i] = 0;
-  if (threadIdx.x == 0) s_n = 0;
-  __syncthreads();
-  const uint32_t top = st->prefix >> 21;
-  const uint64_t nvec = m / 8;
-  const bool vec_ok = (reinterpret_cast<uintptr_t>(dense) & 31u) == 0;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  const uint32_t lane = lane_id();
-  auto flush = [&]() {  // block-wide: move the staged keys to the global list
-    __syncthreads();
-    const uint32_t cnt = s_n;
-    if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&st->ncand, cnt);
-    __syncthreads();
-    const uint32_t b = s_base;
-    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads)
-      if (b + i < cand_cap) cand_key[b + i] = sbuf[i];
-    __syncthreads();
-    if (threadIdx.x == 0) s_n = 0;
-    __syncthreads();
-  };
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < (vec_ok ? nvec : 0);
-       base += stride) {  // block-uniform trip count
-    const uint64_t u = base + threadIdx.x;
-    f8 v;
-    if (u < nvec) v = ld_stream_f8(dense + u * 8);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t key = u < nvec ? mag_key(v.v[c]) : 0u;
-      const bool hit = u < nvec && (key >> 21) == top;
-      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-      if (!bal) continue;
-      uint32_t pos = 0;
-      if (lane == (uint32_t)(__ffs(bal) - 1)) pos = atomicAdd(&s_n, (uint32_t)__popc(bal));
-      pos = __shfl_sync(0xffffffffu, pos, __ffs(bal) - 1) + __popc(bal & lanemask_lt());
-      if (hit) {
-        sbuf[pos] = key;  // pos < kStage: flushed whenever half full
-        atomicAdd(&sh[(key >> 10) & (kBins - 1)], 1u);
-      }
-    }
-    __syncthreads();
-    const uint32_t staged = s_n;
-    __syncthreads();  // every thread has read s_n before any adds to it again
-    if (staged > kStage / 2) flush();  // block-uniform
-  }
-  flush();
-  const uint64_t tail0 = vec_ok ? nvec * 8 : 0;
-  for (uint64_t i = tail0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < m; i += stride) {
-    const uint32_t key = mag_key(dense[i]);
-    if ((key >> 21) == top) {
-      const uint32_t pos = atomicAdd(&st->ncand, 1u);
-      if (pos < cand_cap) cand_key[pos] = key;
-      atomicAdd(&sh[(key >> 10) & (kBins - 1)], 1u);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kBins; i += kThreads)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
-
-// Level 3: over the candidate keys only (or, if the list overflowed its
-// capacity -- a pathological run of equal magnitudes -- over the dense input)
-__global__ void __launch_bounds__(kThreads) k_topk_hist3(const uint32_t* __restrict__ cand_key,
-                                                         uint32_t cand_cap,
-                                                         const float* __restrict__ dense,
-                                                         uint64_t m, const TopkState* st,
-                                                         uint32_t* __restrict__ hist) {
+// Levels 2 and 3 over the tile-staged entries (a warp per tile): keys whose
+// higher digits equal the prefix so far feed the next digit's histogram
+__global__ void __launch_bounds__(kThreads) k_topk_hist_staged(
+    const float* __restrict__ st_val, const uint32_t* __restrict__ tile_cnt, uint32_t ntiles,
+    const TopkState* st, uint32_t* __restrict__ hist, int shift) {
   zen_dev::pdl_entry();
   __shared__ uint32_t sh[kBins];
   for (int i = threadIdx.x; i < kBins; i += kThreads) sh[i] = 0;
   __syncthreads();
-  const uint32_t n = st->ncand, mid = st->prefix >> 10;
-  if (n <= cand_cap) {
-    for (uint32_t i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
-      const uint32_t key = cand_key[i];
-      if ((key >> 10) == mid) atomicAdd(&sh[key & 1023u], 1u);
-    }
-  } else {
-    for (uint64_t i = blockIdx.x * (uint64_t)kThreads + threadIdx.x; i < m;
-         i += (uint64_t)gridDim.x * kThreads) {
-      const uint32_t key = mag_key(dense[i]);
-      if ((key >> 10) == mid) atomicAdd(&sh[key & 1023u], 1u);
+  const int hi = shift + 11;  // bits above the digit being histogrammed
+  const uint32_t want = st->prefix >> hi, lane = lane_id();
+  const uint32_t nwarps = gridDim.x * (kThreads / 32);
+  for (uint32_t tile = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); tile < ntiles;
+       tile += nwarps) {
+    const uint32_t n = tile_cnt[tile];
+    const float* v = st_val + (uint64_t)tile * kExtractTile;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t key = mag_key(v[i]);
+      if ((key >> hi) == want) atomicAdd(&sh[(key >> shift) & (kBins - 1)], 1u);
     }
   }
   __syncthreads();
@@ -358,9 +286,9 @@ inline unsigned pass_grid(uint64_t m) {
 size_t topk_state_bytes() { return sizeof(TopkState); }
 size_t topk_threshold_offset() { return offsetof(TopkState, T); }
 
-// radix select of the threshold: state, histogram and candidates on `s`
+// level 1 of the radix select: state, histogram, staging floor on `s`
 void launch_topk_select(const float* dense, uint64_t m, uint64_t keep, void* state_v,
-                        uint32_t* hist, uint32_t* cand_key, uint32_t cand_cap, cudaStream_t s) {
+                        uint32_t* hist, cudaStream_t s) {
   TopkState* st = static_cast<TopkState*>(state_v);
   TopkState init{};
   init.k = (uint32_t)keep;
@@ -368,25 +296,28 @@ void launch_topk_select(const float* dense, uint64_t m, uint64_t keep, void* sta
   cudaMemsetAsync(hist, 0, kBins * sizeof(uint32_t), s);
   launch_k(k_topk_hist1, pass_grid(m), kThreads, 0, s, dense, m, hist);
   launch_k(k_topk_select, 1, 1024, 0, s, hist, 21, 11, st, 0);
-  launch_k(k_topk_hist2, pass_grid(m), kThreads, 0, s, dense, m, st, hist, cand_key, cand_cap);
-  launch_k(k_topk_select, 1, 1024, 0, s, hist, 10, 11, st, 0);
-  launch_k(k_topk_hist3, 148 * 4, kThreads, 0, s, cand_key, cand_cap, dense, m, st, hist);
-  launch_k(k_topk_select, 1, 1024, 0, s, hist, 0, 10, st, 1);
-  for (int i = 0; i < 6; ++i) count_launch();
+  for (int i = 0; i < 2; ++i) count_launch();
 }
 
 // after the tile pass staged the >= T candidates (launch_select_tiles)
 void launch_topk_finish(const ExtractWs<uint32_t>& ws, uint32_t ntiles, void* state_v,
-                        uint32_t* tile_ties, uint64_t* tie_base, uint64_t* out_base,
+                        uint32_t* hist, uint32_t* tile_ties, uint64_t* tie_base, uint64_t* out_base,
                         uint64_t* out_count, uint64_t* out_idx, float* out_val, uint64_t cap,
                         cudaStream_t s) {
   TopkState* st = static_cast<TopkState*>(state_v);
+  const unsigned hgrid = std::max(1u, std::min(148u * 8, (ntiles + 7) / 8));
+  launch_k(k_topk_hist_staged, hgrid, kThreads, 0, s, ws.st_val, ws.tile_cnt, ntiles, st, hist,
+           10);
+  launch_k(k_topk_select, 1, 1024, 0, s, hist, 10, 11, st, 0);
+  launch_k(k_topk_hist_staged, hgrid, kThreads, 0, s, ws.st_val, ws.tile_cnt, ntiles, st, hist,
+           0);
+  launch_k(k_topk_select, 1, 1024, 0, s, hist, 0, 10, st, 1);
   launch_k(k_topk_ties, ntiles, kThreads, 0, s, ws.st_val, ws.tile_cnt, st, tile_ties);
   launch_k(k_topk_scan, 1, 1024, 0, s, ws.tile_cnt, tile_ties, ntiles, st, tie_base, out_base,
            out_count);
   launch_k(k_topk_compact, ntiles, kThreads, 0, s, ws.st_idx, ws.st_val, ws.tile_cnt, tie_base,
            out_base, st, out_idx, out_val, cap);
-  for (int i = 0; i < 3; ++i) count_launch();
+  for (int i = 0; i < 7; ++i) count_launch();
 }
 
 }  // namespace zen

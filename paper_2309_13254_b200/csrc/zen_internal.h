@@ -294,11 +294,11 @@ void launch_sort_pairs(const uint64_t* ki, uint64_t* ko, const float* vi, float*
 size_t topk_state_bytes();
 size_t topk_threshold_offset();
 void launch_topk_select(const float* dense, uint64_t m, uint64_t keep, void* state,
-                        uint32_t* hist, uint32_t* cand_key, uint32_t cand_cap, cudaStream_t s);
+                        uint32_t* hist, cudaStream_t s);
 void launch_select_tiles(const float* dense, uint64_t m, const ExtractWs<uint32_t>& ws,
                          const uint32_t* key, cudaStream_t stream);
 void launch_topk_finish(const ExtractWs<uint32_t>& ws, uint32_t ntiles, void* state,
-                        uint32_t* tile_ties, uint64_t* tie_base, uint64_t* out_base,
+                        uint32_t* hist, uint32_t* tile_ties, uint64_t* tie_base, uint64_t* out_base,
                         uint64_t* out_count, uint64_t* out_idx, float* out_val, uint64_t cap,
                         cudaStream_t s);
 

@@ -69,6 +69,27 @@ def test_topk_edges(zen):
             zen.sparsify_topk(d, bad)
 
 
+def test_topk_staging_edges(zen, co):
+    """The tile pass stages the whole threshold bucket (top 11 key bits) and the
+    lower digits are selected among the staged entries: a rank that falls
+    among the zeros of bucket 0 (next to non-zero denormals), every entry in
+    one bucket, and equal magnitudes everywhere."""
+    rng = np.random.default_rng(23)
+    m = 70_001
+    den = np.zeros(m, np.float32)
+    nz = rng.choice(m, 300, replace=False)
+    den[nz] = (rng.integers(1, 1 << 20, nz.size).astype(np.uint32)).view(np.float32)
+    den[nz[:50]] *= -1
+    one_bucket = (1.0 + 0.2 * rng.random(m)).astype(np.float32) * rng.choice([-1, 1], m)
+    equal = np.full(m, 0.5, np.float32) * rng.choice([-1, 1], m).astype(np.float32)
+    for name, d in [("denormals", den), ("one_bucket", one_bucket), ("equal", equal)]:
+        for f in [1.0 / m, 0.002, 0.01, 0.5, 1.0]:
+            t = zen.sparsify_topk(d, f)
+            wi, wv = co.sparsify_topk(d, f)
+            np.testing.assert_array_equal(t.indices(), wi, err_msg=f"{name} {f}")
+            np.testing.assert_array_equal(t.values().view(np.uint32), wv.view(np.uint32))
+
+
 def test_topk_full_size_properties(zen):
     """64M-element embedding gradient (1M x 64, 1% rows live, Gaussian values),
     keep 0.5%: the kept set is exactly {|v| > T} plus the lowest-indexed
