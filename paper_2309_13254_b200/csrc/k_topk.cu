@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist_staged(
   __shared__ uint32_t sh[kBins];
   for (int i = threadIdx.x; i < kBins; i += kThreads) sh[i] = 0;
   __syncthreads();
-  const int hi = shift + 11;  // bits above the digit being histogrammed
-  const uint32_t want = st->prefix >> hi, lane = lane_id();
+  const int hi = shift == 0 ? 10 : 21;  // bits above the digit: [31:21] or [31:10]
+  const uint32_t want = st->prefix >> hi, lane = lane_id(), mask = (1u << (hi - shift)) - 1;
   const uint32_t nwarps = gridDim.x * (kThreads / 32);
   for (uint32_t tile = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); tile < ntiles;
        tile += nwarps) {
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist_staged(
     const float* v = st_val + (uint64_t)tile * kExtractTile;
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t key = mag_key(v[i]);
-      if ((key >> hi) == want) atomicAdd(&sh[(key >> shift) & (kBins - 1)], 1u);
+      if ((key >> hi) == want) atomicAdd(&sh[(key >> shift) & mask], 1u);
     }
   }
   __syncthreads();

@@ -80,7 +80,7 @@ def test_topk_staging_edges(zen, co):
     nz = rng.choice(m, 300, replace=False)
     den[nz] = (rng.integers(1, 1 << 20, nz.size).astype(np.uint32)).view(np.float32)
     den[nz[:50]] *= -1
-    one_bucket = (1.0 + 0.2 * rng.random(m)).astype(np.float32) * rng.choice([-1, 1], m)
+    one_bucket = ((1.0 + 0.2 * rng.random(m)) * rng.choice([-1, 1], m)).astype(np.float32)
     equal = np.full(m, 0.5, np.float32) * rng.choice([-1, 1], m).astype(np.float32)
     for name, d in [("denormals", den), ("one_bucket", one_bucket), ("equal", equal)]:
         for f in [1.0 / m, 0.002, 0.01, 0.5, 1.0]:
