@@ -1282,7 +1282,7 @@ extern "C" zen_status zen_sparsify_topk(zen_ctx* c, const float* d_dense, uint64
     CKR(w.mem.alloc(&w.ex.st_idx, uint64_t(ntiles) * kExtractTile, false));
     CKR(w.mem.alloc(&w.ex.st_val, uint64_t(ntiles) * kExtractTile, false));
     CKR(w.mem.alloc(&w.ex.tile_cnt, ntiles));
-    CKR(w.mem.alloc(&w.tile_ties, ntiles));
+    CKR(w.mem.alloc(&w.tile_ties, 2ull * ntiles));  // ties, then entries above T
     CKR(w.mem.alloc(&w.tie_base, ntiles));
     CKR(w.mem.alloc(&w.out_base, ntiles));
     CKR(w.mem.alloc(&w.out_count, 1));

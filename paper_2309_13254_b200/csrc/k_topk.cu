@@ -38,7 +38,7 @@ __device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v)
 
 // Level-1 histogram: 32-byte streaming loads, warp-aggregated shared atomics
 // (equal keys -- e.g. the zeros of a sparse gradient -- cost one atomic per warp)
-__global__ void __launch_bounds__(kThreads) k_topk_hist1(const float* __restrict__ dense,
+__global__ void __launch_bounds__(kThreads, 4) k_topk_hist1(const float* __restrict__ dense,
                                                          uint64_t m, uint32_t* __restrict__ hist) {
   zen_dev::pdl_entry();
   __shared__ uint32_t sh[kBins];
@@ -47,21 +47,31 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist1(const float* __restrict
   const uint64_t nvec = m / 8;
   const bool vec_ok = (reinterpret_cast<uintptr_t>(dense) & 31u) == 0;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads; base < (vec_ok ? nvec : 0);
-       base += stride) {  // warp-uniform trip count
-    const uint64_t u = base + threadIdx.x;
-    f8 v;
-    if (u < nvec) v = ld_stream_f8(dense + u * 8);
+  // kU independent 32-byte loads in flight per thread before any binning
+  // (one load per iteration left the pass at ~55% of HBM bandwidth)
+  constexpr int kU = 4;
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads * kU; base < (vec_ok ? nvec : 0);
+       base += stride * kU) {  // warp-uniform trip count
+    f8 v[kU];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t bin = u < nvec ? mag_key(v.v[c]) >> 21 : 0xFFFFFFFFu;
-      // a warp-uniform bin (the zeros of a sparse gradient) costs one atomic;
-      // spread values (dense layers) go straight to the shared histogram
-      const uint32_t b0 = __shfl_sync(0xffffffffu, bin, 0);
-      if (__all_sync(0xffffffffu, bin == b0)) {
-        if (lane_id() == 0 && b0 != 0xFFFFFFFFu) atomicAdd(&sh[b0], 32u);
-      } else if (bin != 0xFFFFFFFFu) {
-        atomicAdd(&sh[bin], 1u);
+    for (int j = 0; j < kU; ++j) {
+      const uint64_t u = base + (uint64_t)j * kThreads + threadIdx.x;
+      if (u < nvec) v[j] = ld_stream_f8(dense + u * 8);
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const uint64_t u = base + (uint64_t)j * kThreads + threadIdx.x;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t bin = u < nvec ? mag_key(v[j].v[c]) >> 21 : 0xFFFFFFFFu;
+        // a warp-uniform bin (the zeros of a sparse gradient) costs one atomic;
+        // spread values (dense layers) go straight to the shared histogram
+        const uint32_t b0 = __shfl_sync(0xffffffffu, bin, 0);
+        if (__all_sync(0xffffffffu, bin == b0)) {
+          if (lane_id() == 0 && b0 != 0xFFFFFFFFu) atomicAdd(&sh[b0], 32u);
+        } else if (bin != 0xFFFFFFFFu) {
+          atomicAdd(&sh[bin], 1u);
+        }
       }
     }
   }
@@ -155,23 +165,30 @@ __global__ void __launch_bounds__(kThreads) k_topk_hist_staged(
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-// ties (key == T) among each tile's staged candidates
+// per tile: ties (key == T) and entries above T among the staged candidates
+// (the staged set also holds the threshold bucket's entries below T);
+// tile_ties[0, ntiles) = ties, tile_ties[ntiles, 2 ntiles) = above
 __global__ void __launch_bounds__(kThreads) k_topk_ties(const float* __restrict__ st_val,
                                                         const uint32_t* __restrict__ tile_cnt,
-                                                        const TopkState* st,
+                                                        uint32_t ntiles, const TopkState* st,
                                                         uint32_t* __restrict__ tile_ties) {
   zen_dev::pdl_entry();
-  __shared__ uint32_t s_cnt;
-  if (threadIdx.x == 0) s_cnt = 0;
-  __syncthreads();
-  const uint32_t tile = blockIdx.x, n = tile_cnt[tile], T = st->T;
-  uint32_t c = 0;
-  for (uint32_t i = threadIdx.x; i < n; i += kThreads)
-    c += mag_key(st_val[(uint64_t)tile * kExtractTile + i]) == T ? 1u : 0u;
+  // a warp per tile: a tile stages ~1-2% of its 8192 elements
+  const uint32_t tile = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (tile >= ntiles) return;
+  const uint32_t n = tile_cnt[tile], T = st->T;
+  uint32_t c = 0, g = 0;
+  for (uint32_t i = lane_id(); i < n; i += 32) {
+    const uint32_t key = mag_key(st_val[(uint64_t)tile * kExtractTile + i]);
+    c += key == T ? 1u : 0u;
+    g += key > T ? 1u : 0u;
+  }
   c = __reduce_add_sync(0xffffffffu, c);
-  if (lane_id() == 0 && c) atomicAdd(&s_cnt, c);
-  __syncthreads();
-  if (threadIdx.x == 0) tile_ties[tile] = s_cnt;
+  g = __reduce_add_sync(0xffffffffu, g);
+  if (lane_id() == 0) {
+    tile_ties[tile] = c;
+    tile_ties[ntiles + tile] = g;
+  }
 }
 
 // one block over the tiles: ties before each tile -> the tile's kept entries
@@ -194,7 +211,7 @@ __global__ void __launch_bounds__(1024) k_topk_scan(const uint32_t* __restrict__
     for (int e = 0; e < E; ++e) {
       const bool in = t0 + e < ntiles;
       ties[e] = in ? tile_ties[t0 + e] : 0;
-      gt[e] = in ? tile_cnt[t0 + e] - ties[e] : 0;
+      gt[e] = in ? tile_ties[ntiles + t0 + e] : 0;
       lt += ties[e];
     }
     uint64_t tt;
@@ -276,9 +293,9 @@ __global__ void __launch_bounds__(kThreads) k_topk_compact(
   }
 }
 
-inline unsigned pass_grid(uint64_t m) {
+inline unsigned pass_grid(uint64_t m) {  // hist1: 4 resident CTAs per SM (55 registers)
   const uint64_t g = (m / 8 + kThreads - 1) / kThreads;
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, 148 * 8));
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, 148 * 4));
 }
 
 }  // namespace
@@ -312,7 +329,7 @@ void launch_topk_finish(const ExtractWs<uint32_t>& ws, uint32_t ntiles, void* st
   launch_k(k_topk_hist_staged, hgrid, kThreads, 0, s, ws.st_val, ws.tile_cnt, ntiles, st, hist,
            0);
   launch_k(k_topk_select, 1, 1024, 0, s, hist, 0, 10, st, 1);
-  launch_k(k_topk_ties, ntiles, kThreads, 0, s, ws.st_val, ws.tile_cnt, st, tile_ties);
+  launch_k(k_topk_ties, (ntiles + 7) / 8, kThreads, 0, s, ws.st_val, ws.tile_cnt, ntiles, st, tile_ties);
   launch_k(k_topk_scan, 1, 1024, 0, s, ws.tile_cnt, tile_ties, ntiles, st, tie_base, out_base,
            out_count);
   launch_k(k_topk_compact, ntiles, kThreads, 0, s, ws.st_idx, ws.st_val, ws.tile_cnt, tie_base,
