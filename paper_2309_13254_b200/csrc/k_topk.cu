@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_hist1(const float* __restr
   // kU independent 32-byte loads in flight per thread before any binning
   // (one load per iteration left the pass at ~55% of HBM bandwidth)
   constexpr int kU = 4;
+  uint32_t run_bin = 0, run_cnt = 0;  // warp-uniform
   for (uint64_t base = (uint64_t)blockIdx.x * kThreads * kU; base < (vec_ok ? nvec : 0);
        base += stride * kU) {  // warp-uniform trip count
     f8 v[kU];
@@ -61,20 +62,46 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_hist1(const float* __restr
 #pragma unroll
     for (int j = 0; j < kU; ++j) {
       const uint64_t u = base + (uint64_t)j * kThreads + threadIdx.x;
+      // fast path: all 8 x 32 keys of this warp-wide load in one bin (a run of
+      // zeros) -- one vote instead of eight
+      const uint32_t f0 = mag_key(v[j].v[0]) >> 21;
+      bool same = u < nvec;
+#pragma unroll
+      for (int c = 1; c < 8; ++c) same &= (mag_key(v[j].v[c]) >> 21) == f0;
+      const uint32_t w0 = __shfl_sync(0xffffffffu, f0, 0);
+      if (__all_sync(0xffffffffu, same && f0 == w0)) {
+        if (w0 == run_bin) {
+          run_cnt += 256;
+        } else {
+          if (lane_id() == 0 && run_cnt) atomicAdd(&sh[run_bin], run_cnt);
+          run_bin = w0;
+          run_cnt = 256;
+        }
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const uint32_t bin = u < nvec ? mag_key(v[j].v[c]) >> 21 : 0xFFFFFFFFu;
-        // a warp-uniform bin (the zeros of a sparse gradient) costs one atomic;
-        // spread values (dense layers) go straight to the shared histogram
+        // a warp-uniform bin costs no atomic at all; spread values (dense
+        // layers) go straight to the shared histogram
         const uint32_t b0 = __shfl_sync(0xffffffffu, bin, 0);
         if (__all_sync(0xffffffffu, bin == b0)) {
-          if (lane_id() == 0 && b0 != 0xFFFFFFFFu) atomicAdd(&sh[b0], 32u);
+          // runs of one bin accumulate in a (warp-uniform) register: every
+          // warp of the SM hitting sh[0] with an atomic serialises
+          if (b0 == run_bin) {
+            run_cnt += 32;
+          } else if (b0 != 0xFFFFFFFFu) {
+            if (lane_id() == 0 && run_cnt) atomicAdd(&sh[run_bin], run_cnt);
+            run_bin = b0;
+            run_cnt = 32;
+          }
         } else if (bin != 0xFFFFFFFFu) {
           atomicAdd(&sh[bin], 1u);
         }
       }
     }
   }
+  if (lane_id() == 0 && run_cnt) atomicAdd(&sh[run_bin], run_cnt);
   const uint64_t tail0 = vec_ok ? nvec * 8 : 0;
   for (uint64_t i = tail0 + (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < m; i += stride)
     atomicAdd(&sh[mag_key(dense[i]) >> 21], 1u);
