@@ -17,8 +17,9 @@
 //   hist2/3 over the staged entries only (a warp per tile), each followed by a
 //           select -> threshold key T and the number r of T-ties to keep (the
 //           r lowest-indexed ones)
-//   ties, scan  one block: per tile, ties before it -> entries it keeps -> base
-//   compact one block per tile: > T entries, plus ties while the global tie
+//   ties    a warp per tile: the tile's T-ties and entries above T
+//   scan    one block: per tile, ties before it -> entries it keeps -> base
+//   compact a warp per tile: > T entries, plus ties while the global tie
 //           rank is below r, written in ascending index order.
 // Two HBM passes over the dense input in all (an earlier version collected
 // the bucket with a second full pass before the tile pass: three); everything
@@ -37,7 +38,6 @@ constexpr int kThreads = 256;
 __device__ __forceinline__ uint32_t mag_key(float v) { return __float_as_uint(v) & 0x7fffffffu; }
 
 // Level-1 histogram: 32-byte streaming loads, warp-aggregated shared atomics
-// (equal keys -- e.g. the zeros of a sparse gradient -- cost one atomic per warp)
 __global__ void __launch_bounds__(kThreads, 4) k_topk_hist1(const float* __restrict__ dense,
                                                          uint64_t m, uint32_t* __restrict__ hist) {
   zen_dev::pdl_entry();
@@ -82,8 +82,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_hist1(const float* __restr
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const uint32_t bin = u < nvec ? mag_key(v[j].v[c]) >> 21 : 0xFFFFFFFFu;
-        // a warp-uniform bin costs no atomic at all; spread values (dense
-        // layers) go straight to the shared histogram
+        // a warp-uniform bin costs no atomic at all
         const uint32_t b0 = __shfl_sync(0xffffffffu, bin, 0);
         if (__all_sync(0xffffffffu, bin == b0)) {
           // runs of one bin accumulate in a (warp-uniform) register: every
@@ -96,6 +95,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_hist1(const float* __restr
             run_cnt = 32;
           }
         } else if (bin != 0xFFFFFFFFu) {
+          // spread values go straight to the shared histogram (aggregating
+          // them with __match_any_sync was 3.7x slower on a Gaussian layer)
           atomicAdd(&sh[bin], 1u);
         }
       }
@@ -116,7 +117,7 @@ struct TopkState {
   uint64_t above;   // keys strictly above the current bucket
   uint32_t T;       // final threshold key
   uint32_t r;       // ties of T to keep
-  uint32_t ncand;   // candidate list length (level 2)
+  uint32_t ncand;   // unused (the level-2 candidate list of the three-pass version)
   uint32_t nsel;    // |output| before zero dropping is accounted (set by the scan)
 };
 
@@ -265,58 +266,39 @@ __global__ void __launch_bounds__(1024) k_topk_scan(const uint32_t* __restrict__
   if (threadIdx.x == 0) *out_count = ocarry;
 }
 
-// one block per tile: stable selection of the staged candidates
+// a warp per tile: stable selection of the staged candidates (a tile stages
+// ~1-2% of its 8192 elements, so a block per tile idled most of its lanes)
 __global__ void __launch_bounds__(kThreads) k_topk_compact(
     const uint32_t* __restrict__ st_idx, const float* __restrict__ st_val,
-    const uint32_t* __restrict__ tile_cnt, const uint64_t* __restrict__ tie_base,
+    const uint32_t* __restrict__ tile_cnt, uint32_t ntiles, const uint64_t* __restrict__ tie_base,
     const uint64_t* __restrict__ out_base, const TopkState* st, uint64_t* __restrict__ out_idx,
     float* __restrict__ out_val, uint64_t cap) {
   zen_dev::pdl_entry();
-  __shared__ uint32_t s_warp[2][kThreads / 32];
-  const uint32_t tile = blockIdx.x, n = tile_cnt[tile], T = st->T;
+  const uint32_t tile = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (tile >= ntiles) return;
+  const uint32_t n = tile_cnt[tile], T = st->T;
   const uint64_t r = T ? st->r : 0;
   uint64_t tb = tie_base[tile], ob = out_base[tile];
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  for (uint32_t c0 = 0; c0 < n; c0 += kThreads) {
-    const uint32_t i = c0 + threadIdx.x;
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t c0 = 0; c0 < n; c0 += 32) {  // warp-uniform trip count
+    const uint32_t i = c0 + lane_id();
     const bool in = i < n;
     const uint64_t src = (uint64_t)tile * kExtractTile + i;
     const float v = in ? st_val[src] : 0.0f;
     const uint32_t key = mag_key(v);
     const bool tie = in && key == T;
-    // rank of this tie among the tile's ties so far (block scan of tie flags)
     const uint32_t tbal = __ballot_sync(0xffffffffu, tie);
-    if (lane == 0) s_warp[0][warp] = __popc(tbal);
-    __syncthreads();
-    uint32_t tw = 0, ttot = 0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) {
-      const uint32_t x = s_warp[0][w];
-      tw += w < (int)warp ? x : 0u;
-      ttot += x;
-    }
-    const uint64_t trank = tb + tw + __popc(tbal & lanemask_lt());
-    const bool keep = in && (key > T || (tie && trank < r));
+    const bool keep = in && (key > T || (tie && tb + __popc(tbal & lt) < r));
     const uint32_t kbal = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_warp[1][warp] = __popc(kbal);
-    __syncthreads();
-    uint32_t kw = 0, ktot = 0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) {
-      const uint32_t x = s_warp[1][w];
-      kw += w < (int)warp ? x : 0u;
-      ktot += x;
-    }
     if (keep) {
-      const uint64_t pos = ob + kw + __popc(kbal & lanemask_lt());
+      const uint64_t pos = ob + __popc(kbal & lt);
       if (pos < cap) {
         out_idx[pos] = st_idx[src];
         out_val[pos] = v;
       }
     }
-    tb += ttot;
-    ob += ktot;
-    __syncthreads();
+    tb += __popc(tbal);
+    ob += __popc(kbal);
   }
 }
 
@@ -359,8 +341,8 @@ void launch_topk_finish(const ExtractWs<uint32_t>& ws, uint32_t ntiles, void* st
   launch_k(k_topk_ties, (ntiles + 7) / 8, kThreads, 0, s, ws.st_val, ws.tile_cnt, ntiles, st, tile_ties);
   launch_k(k_topk_scan, 1, 1024, 0, s, ws.tile_cnt, tile_ties, ntiles, st, tie_base, out_base,
            out_count);
-  launch_k(k_topk_compact, ntiles, kThreads, 0, s, ws.st_idx, ws.st_val, ws.tile_cnt, tie_base,
-           out_base, st, out_idx, out_val, cap);
+  launch_k(k_topk_compact, (ntiles + 7) / 8, kThreads, 0, s, ws.st_idx, ws.st_val, ws.tile_cnt,
+           ntiles, tie_base, out_base, st, out_idx, out_val, cap);
   for (int i = 0; i < 7; ++i) count_launch();
 }
 
