@@ -53,13 +53,31 @@ __global__ void k_axpy_sparse(float* __restrict__ dense, uint64_t m,
                               const uint64_t* __restrict__ idx, const float* __restrict__ val,
                               uint64_t count, float alpha, uint32_t* status) {
   zen_dev::pdl_entry();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t x = idx[i];
-    if (x < m)
-      dense[x] = fmaf(alpha, val[i], dense[x]);
-    else
-      atomicOr(status, 1u);
+  // R entries per thread per round with every load issued before the
+  // read-modify-writes: one index -> parameter latency chain per round, not
+  // per entry
+  constexpr int R = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; base < count;
+       base += R * stride) {
+    uint64_t x[R];
+    float v[R], d[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const uint64_t i = base + q * stride;
+      x[q] = i < count ? idx[i] : ~0ull;
+      v[q] = i < count ? val[i] : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) d[q] = x[q] < m ? dense[x[q]] : 0.0f;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (base + q * stride >= count) break;
+      if (x[q] < m)
+        dense[x[q]] = fmaf(alpha, v[q], d[q]);
+      else
+        atomicOr(status, 1u);
+    }
   }
 }
 

@@ -141,3 +141,28 @@ def test_apply_sgd_after_sync(zen):
     want[idx] -= 0.05 * val  # torch fp32 reference (fma vs mul+sub: <= 1 ulp)
     torch.testing.assert_close(param, want, rtol=1e-6, atol=1e-7)
     torch.cuda.set_stream(torch.cuda.default_stream())
+
+
+def test_axpy_sparse_many_rounds_and_range_error(zen):
+    """zen_axpy_sparse over more entries than one round of the grid (4 per
+    thread): param[idx] += alpha * val against torch fp32; an index >= M is
+    reported as ZEN_E_INVALID."""
+    import ctypes as C
+    import torch
+    lib, ctx = zen.load(), zen.context()
+    m, cnt = 4_000_000, 2_500_001
+    g = torch.Generator(device="cuda").manual_seed(3)
+    idx = torch.randperm(m, device="cuda", generator=g)[:cnt].sort().values
+    val = torch.randn(cnt, device="cuda", generator=g)
+    param = torch.randn(m, device="cuda", generator=g)
+    want = param.clone()
+    want[idx] = torch.addcmul(want[idx], val, torch.full_like(val, -0.5))
+    ctx.bind_stream()
+    assert lib.zen_axpy_sparse(ctx.h, C.c_void_p(param.data_ptr()), m, C.c_void_p(idx.data_ptr()),
+                               C.c_void_p(val.data_ptr()), cnt, C.c_float(-0.5)) == 0
+    torch.cuda.synchronize()
+    torch.testing.assert_close(param, want, rtol=1e-6, atol=1e-7)
+    bad = idx.clone()
+    bad[-1] = m
+    assert lib.zen_axpy_sparse(ctx.h, C.c_void_p(param.data_ptr()), m, C.c_void_p(bad.data_ptr()),
+                               C.c_void_p(val.data_ptr()), cnt, C.c_float(-0.5)) != 0
