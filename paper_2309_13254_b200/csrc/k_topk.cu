@@ -79,26 +79,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_topk_hist1(const float* __restr
         }
         continue;
       }
+      // otherwise straight to the shared histogram: a per-element warp vote
+      // here left a dense layer's pass instruction-bound (67% issue-active)
+      if (same) {  // this lane's 8 keys share a bin (e.g. zeros next to a live row)
+        atomicAdd(&sh[f0], 8u);
+      } else if (u < nvec) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t bin = u < nvec ? mag_key(v[j].v[c]) >> 21 : 0xFFFFFFFFu;
-        // a warp-uniform bin costs no atomic at all
-        const uint32_t b0 = __shfl_sync(0xffffffffu, bin, 0);
-        if (__all_sync(0xffffffffu, bin == b0)) {
-          // runs of one bin accumulate in a (warp-uniform) register: every
-          // warp of the SM hitting sh[0] with an atomic serialises
-          if (b0 == run_bin) {
-            run_cnt += 32;
-          } else if (b0 != 0xFFFFFFFFu) {
-            if (lane_id() == 0 && run_cnt) atomicAdd(&sh[run_bin], run_cnt);
-            run_bin = b0;
-            run_cnt = 32;
-          }
-        } else if (bin != 0xFFFFFFFFu) {
-          // spread values go straight to the shared histogram (aggregating
-          // them with __match_any_sync was 3.7x slower on a Gaussian layer)
-          atomicAdd(&sh[bin], 1u);
-        }
+        for (int c = 0; c < 8; ++c) atomicAdd(&sh[mag_key(v[j].v[c]) >> 21], 1u);
       }
     }
   }
