@@ -217,40 +217,37 @@ __global__ void __launch_bounds__(1024) k_topk_scan(const uint32_t* __restrict__
   zen_dev::pdl_entry();
   __shared__ uint64_t sscan[33];
   const uint64_t r = st->T ? st->r : 0;  // T = 0: the ties are zeros, dropped
-  uint64_t tcarry = 0, ocarry = 0;
+  // one scan of packed (ties << 32 | above-T) counts (both totals stay below
+  // m < 2^32): the first r ties in index order are kept, so a tile's output
+  // base is above_before + min(r, ties_before)
+  uint64_t carry = 0;
   constexpr int E = 8;
   for (uint32_t b = 0; b < ntiles; b += blockDim.x * E) {
     const uint32_t t0 = b + threadIdx.x * E;
-    uint64_t ties[E], gt[E], lt = 0;
+    uint64_t pk[E], lsum = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const bool in = t0 + e < ntiles;
-      ties[e] = in ? tile_ties[t0 + e] : 0;
-      gt[e] = in ? tile_ties[ntiles + t0 + e] : 0;
-      lt += ties[e];
+      pk[e] = in ? ((uint64_t)tile_ties[t0 + e] << 32 | tile_ties[ntiles + t0 + e]) : 0;
+      lsum += pk[e];
     }
-    uint64_t tt;
-    uint64_t tex = tcarry + block_exclusive_sum(lt, sscan, &tt);
-    uint64_t keep[E], lk = 0;
+    uint64_t tot;
+    uint64_t ex = carry + block_exclusive_sum(lsum, sscan, &tot);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const uint64_t take = tex >= r ? 0 : (r - tex < ties[e] ? r - tex : ties[e]);
-      keep[e] = gt[e] + take;
-      if (t0 + e < ntiles) tie_base[t0 + e] = tex;
-      tex += ties[e];
-      lk += keep[e];
+      if (t0 + e < ntiles) {
+        const uint64_t tb = ex >> 32;
+        tie_base[t0 + e] = tb;
+        out_base[t0 + e] = (ex & 0xffffffffull) + (tb < r ? tb : r);
+      }
+      ex += pk[e];
     }
-    uint64_t kt;
-    uint64_t oex = ocarry + block_exclusive_sum(lk, sscan, &kt);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      if (t0 + e < ntiles) out_base[t0 + e] = oex;
-      oex += keep[e];
-    }
-    tcarry += tt;
-    ocarry += kt;
+    carry += tot;
   }
-  if (threadIdx.x == 0) *out_count = ocarry;
+  if (threadIdx.x == 0) {
+    const uint64_t tb = carry >> 32;
+    *out_count = (carry & 0xffffffffull) + (tb < r ? tb : r);
+  }
 }
 
 // a warp per tile: stable selection of the staged candidates (a tile stages
