@@ -27,6 +27,22 @@ $(COMPAT_TEST): tests/cpp/compat_test.cpp include/zen_b200/compat.hpp include/ze
 	g++ -O2 -std=c++17 -Wall -Wextra -Iinclude -I$(CUDA_HOME)/include -o $@ $< \
 	    -L$(dir $(LIB)) -lzen_b200 -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))' -L$(CUDA_HOME)/lib64 -lcudart
 
+# The reference's OWN unit suites, compiled unmodified against the drop-in:
+# tests/cpp/zen_shim maps each "zen/<name>.hpp" include to compat.hpp with
+# `namespace zen = zen_b200;`, tests/cpp/gtest_shim stands in for GTest (not
+# installed).  Built only where the reference exists (this container); the
+# binaries travel to the GPU box in build/ and run there (tests/test_gpu_parity.py).
+REF_TESTS ?= /root/reference/proj/tests
+REF_SUITES := hashing
+REF_BINS := $(patsubst %,build/ref_%_test,$(REF_SUITES))
+ref_tests: $(if $(wildcard $(REF_TESTS)),$(REF_BINS),)
+build/ref_%_test: $(REF_TESTS)/%_test.cpp include/zen_b200/compat.hpp include/zen_b200.h \
+                  tests/cpp/gtest_shim/gtest/gtest.h $(LIB)
+	@mkdir -p build
+	g++ -O2 -std=c++20 -w -Itests/cpp/gtest_shim -Itests/cpp/zen_shim -Iinclude \
+	    -I$(CUDA_HOME)/include -o $@ $< -L$(dir $(LIB)) -lzen_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))' -L$(CUDA_HOME)/lib64 -lcudart
+
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
@@ -46,4 +62,4 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle clean compat_test
+.PHONY: all lib oracle clean compat_test ref_tests

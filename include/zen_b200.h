@@ -97,11 +97,27 @@ uint64_t zen_kernel_launches(void);     /* kernels this process launched through
 /* ---- hash family (host math) ------------------------------------------ */
 /* detail::derive_seed, zen/hashing.hpp:37-39 */
 uint64_t zen_derive_seed(uint64_t master, uint64_t stream);
+/* detail::mix64 / seeded_hash / map_to_range, zen/hashing.hpp:18-34: the
+ * scalar functions behind HashFamily::partition_of / slot_of and the
+ * standalone partition_of (:73-88).  One hash per call: host arithmetic (the
+ * batched device path is zen_partition_of below). */
+uint64_t zen_mix64(uint64_t x);
+uint64_t zen_seeded_hash(uint64_t x, uint64_t seed);
+uint64_t zen_map_to_range(uint64_t h, uint64_t range);
 /* HashFamily::make, zen/hashing.hpp:51-60 */
 zen_status zen_hash_family_make(uint64_t seed, uint32_t n, uint32_t k, zen_hash_family* out);
 /* HashFamily::make_worker, zen/hashing.hpp:64-69 */
 zen_status zen_hash_family_make_worker(uint64_t shared_seed, uint32_t worker, uint32_t n,
                                        uint32_t k, zen_hash_family* out);
+
+/* Test knob for the lock-free priority claim (the hash-memory placement of
+ * zen_hierarchical_hash on this thread): grid / block size of the claim kernel
+ * and a permutation i -> (i * perm_mul + perm_add) mod count of the order in
+ * which keys claim (used only when gcd(perm_mul, count) = 1).  The layout must
+ * not change (the outcome is schedule invariant).  Zeros
+ * restore the defaults. */
+zen_status zen_debug_hash_schedule(uint32_t grid, uint32_t threads, uint64_t perm_mul,
+                                   uint64_t perm_add);
 
 /* ---- device context ---------------------------------------------------- */
 zen_status zen_ctx_create(int device, zen_ctx** out);
@@ -273,7 +289,9 @@ zen_status zen_hc_stage_counts(zen_hc* hc, uint64_t* counts);
 /* ---- apply: the step after the sync ------------------------------------ */
 /* d_dense[idx[i]] += alpha * val[i] for a sorted unique sparse tensor (an SGD
  * step on a synced gradient: alpha = -lr; zen_bp_result gives the synced
- * tensor on the device).  Indices >= m -> ZEN_E_INVALID.  Synchronous. */
+ * tensor on the device).  The indices are validated first (ascending, unique,
+ * < m, as a SparseTensor guarantees); an invalid tensor -> ZEN_E_INVALID with
+ * d_dense untouched.  Synchronous. */
 zen_status zen_axpy_sparse(zen_ctx* ctx, float* d_dense, uint64_t m, const uint64_t* d_idx,
                            const float* d_val, uint64_t count, float alpha);
 

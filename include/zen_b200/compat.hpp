@@ -125,6 +125,14 @@ class DeviceError : public Error {  // no CPU fallback exists
 };
 
 namespace detail {
+// zen/hashing.hpp:18-39
+inline uint64_t mix64(uint64_t x) { return zen_mix64(x); }
+inline uint64_t seeded_hash(uint64_t x, uint64_t seed) { return zen_seeded_hash(x, seed); }
+inline uint64_t map_to_range(uint64_t h, uint64_t range) { return zen_map_to_range(h, range); }
+inline uint64_t derive_seed(uint64_t master, uint64_t stream) {
+  return zen_derive_seed(master, stream);
+}
+
 inline void check(zen_status s) {
   if (s == ZEN_OK) return;
   const std::string msg = zen_last_error_message();
@@ -292,6 +300,13 @@ struct HashFamily {
     return from(f);
   }
   uint32_t depth() const { return uint32_t(slot_seeds.size()); }
+  // zen/hashing.hpp:73-81 (round is 1-based)
+  uint32_t partition_of(uint64_t index) const {
+    return uint32_t(zen_map_to_range(zen_seeded_hash(index + 1, partition_seed), partitions));
+  }
+  uint64_t slot_of(uint64_t index, uint32_t round, uint64_t r1) const {
+    return zen_map_to_range(zen_seeded_hash(index + 1, slot_seeds.at(round - 1)), r1);
+  }
   zen_hash_family c() const {
     zen_hash_family f{};
     f.partition_seed = partition_seed;
@@ -311,7 +326,11 @@ struct HashFamily {
   }
 };
 
-// zen::partition_of (hashing.hpp:85-88), batched on the GPU
+// zen::partition_of (hashing.hpp:85-88): one index (host math) ...
+inline uint32_t partition_of(uint64_t index, uint64_t partition_seed, uint32_t n) {
+  return uint32_t(zen_map_to_range(zen_seeded_hash(index + 1, partition_seed), n));
+}
+// ... or a batch, on the GPU
 inline std::vector<uint32_t> partition_of(const std::vector<uint64_t>& idx, uint64_t pseed,
                                           uint32_t n) {
   detail::DBuf<uint64_t> d(idx);
@@ -362,6 +381,32 @@ inline PartitionedSparseTensor hierarchical_hash(const SparseTensor& t, uint32_t
 inline CollisionStats collision_stats(const SparseTensor& t, uint32_t n, const HashFamily& family,
                                       uint64_t r1, uint64_t r2) {
   return detail::run_hierarchical_hash(t, n, family, r1, r2, 1).second;
+}
+
+// zen::strawman_hash (hashing.hpp:266-291): the paper's single-hash,
+// last-writer-wins strawman, kept as a baseline only (it loses data by
+// design).  Host arithmetic: the winner of a cell is the largest index that
+// maps to it, because the reference writes the cells in ascending index order.
+inline std::pair<PartitionedSparseTensor, uint64_t> strawman_hash(const SparseTensor& t,
+                                                                  uint32_t n, uint64_t r,
+                                                                  uint64_t seed) {
+  if (n == 0 || r == 0) throw Error("strawman hash needs n >= 1 and r >= 1");
+  const uint64_t cells = uint64_t(n) * r;
+  const uint64_t hs = zen_derive_seed(seed, 77);
+  std::vector<int64_t> owner(cells, -1);
+  const auto& idx = t.indices();
+  for (size_t i = 0; i < idx.size(); ++i)
+    owner[zen_map_to_range(zen_seeded_hash(idx[i] + 1, hs), cells)] = int64_t(i);
+  PartitionedSparseTensor out;
+  uint64_t kept = 0;
+  for (uint32_t p = 0; p < n; ++p) {
+    std::vector<std::pair<uint64_t, float>> cell;
+    for (uint64_t c = uint64_t(p) * r; c < uint64_t(p + 1) * r; ++c)
+      if (owner[c] >= 0) cell.emplace_back(idx[size_t(owner[c])], t.values()[size_t(owner[c])]);
+    kept += cell.size();
+    out.parts.push_back(SparseTensor::from_pairs(t.universe(), std::move(cell)));
+  }
+  return {std::move(out), t.nnz() - kept};
 }
 
 inline double imbalance_push(const std::vector<PartitionedSparseTensor>& per_worker) {

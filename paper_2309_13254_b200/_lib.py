@@ -89,6 +89,10 @@ _SIGS = {
     "zen_last_error_index": (u64, []),
     "zen_kernel_launches": (u64, []),
     "zen_derive_seed": (u64, [u64, u64]),
+    "zen_debug_hash_schedule": (C.c_int, [u32, u32, u64, u64]),
+    "zen_mix64": (u64, [u64]),
+    "zen_seeded_hash": (u64, [u64, u64]),
+    "zen_map_to_range": (u64, [u64, u64]),
     "zen_hash_family_make": (C.c_int, [u64, u32, u32, P(HashFamilyC)]),
     "zen_hash_family_make_worker": (C.c_int, [u64, u32, u32, u32, P(HashFamilyC)]),
     "zen_ctx_create": (C.c_int, [C.c_int, P(vp)]),

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <numeric>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -275,6 +276,11 @@ uint64_t zen_last_error_index(void) { return t_index; }
 uint64_t zen_kernel_launches(void) { return g_launches.load(); }
 
 uint64_t zen_derive_seed(uint64_t master, uint64_t stream) { return h_derive(master, stream); }
+uint64_t zen_mix64(uint64_t x) { return h_mix64(x); }
+uint64_t zen_seeded_hash(uint64_t x, uint64_t seed) { return h_mix64(x + kG * (seed + 1)); }
+uint64_t zen_map_to_range(uint64_t h, uint64_t range) {
+  return uint64_t((static_cast<unsigned __int128>(h) * range) >> 64);
+}
 
 zen_status zen_hash_family_make(uint64_t seed, uint32_t n, uint32_t k, zen_hash_family* out) {
   // HashFamily::make, zen/hashing.hpp:51-60
@@ -388,6 +394,22 @@ zen_status zen_to_sparse(zen_ctx* c, const float* d_dense, uint64_t m, uint64_t*
   return ZEN_OK;
 }
 
+namespace {
+struct HashSchedule {
+  uint32_t grid = 0, threads = 0;
+  uint64_t mul = 0, add = 0;
+};
+thread_local HashSchedule t_sched;
+}  // namespace
+
+zen_status zen_debug_hash_schedule(uint32_t grid, uint32_t threads, uint64_t perm_mul,
+                                   uint64_t perm_add) {
+  if (threads && (threads % 32 || threads > 1024))
+    return fail(ZEN_E_INVALID, "threads must be a multiple of 32, <= 1024");
+  t_sched = HashSchedule{grid, threads, perm_mul, perm_add};
+  return ZEN_OK;
+}
+
 zen_status zen_hierarchical_hash(zen_ctx* c, const uint64_t* d_idx, const float* d_val,
                                  uint64_t count, uint64_t universe, const zen_hash_family* fam,
                                  uint64_t r1, uint64_t r2, uint64_t* d_out_idx, float* d_out_val,
@@ -436,6 +458,12 @@ zen_status zen_hierarchical_hash(zen_ctx* c, const uint64_t* d_idx, const float*
   a.cap = cap;
   a.tiles_cap = ntiles;
   a.stride_cap = stride;
+  a.place_grid = t_sched.grid;
+  a.place_threads = t_sched.threads;
+  if (t_sched.mul && count && std::gcd(t_sched.mul % count, count) == 1) {
+    a.perm_mul = t_sched.mul % count;  // a bijection of [0, count)
+    a.perm_add = t_sched.add % count;
+  }
   HashHdr h{};
   h.count = count;
   h.r1 = r1;
@@ -1250,6 +1278,10 @@ extern "C" zen_status zen_axpy_sparse(zen_ctx* c, float* d_dense, uint64_t m,
   CKR(ctx_scratch(c, 256, &sc));
   uint32_t* st = sc.get<uint32_t>(1);
   CK(cudaMemsetAsync(st, 0, 4, c->stream));
+  // validate first (ascending, unique, < M: the SparseTensor invariant), so an
+  // invalid tensor leaves the parameters untouched and no update is lost to a
+  // duplicate index
+  CKR(wire_check_input(c, d_idx, count, m, st));
   launch_axpy_sparse(d_dense, m, d_idx, d_val, count, alpha, st, c->stream);
   uint32_t h = 0;
   CK(cudaMemcpyAsync(&h, st, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1411,6 +1443,7 @@ struct zen_bp {
   uint32_t kernels_per_sync = 0;
   // e2e staging
   std::vector<float*> dense_dev;
+  uint32_t* chk = nullptr;  // status word of the sparse-input validation
   // hash-memory side path stream + fork/join events
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -1483,9 +1516,20 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   CKR(mem.alloc(&w.ex.tile_base, ext_tiles));
   w.ex.nblk = (std::min<uint64_t>(bp->cap, bp->m) + 255) / 256;
   CKR(mem.alloc(&w.ex.blk_tile, w.ex.nblk + 1));
+  // dense data path: per-(partition, tile) counts + chunk / super-chunk sums
+  PushCounts& x = a.xc;
+  x.ntiles = (uint32_t)ext_tiles;
+  x.nchunk = (uint32_t)((ext_tiles + 31) / 32);
+  x.nsup = (uint32_t)((ext_tiles + 1023) / 1024);
+  x.n = n;
+  CKR(mem.alloc(&x.tcnt, size_t(n) * x.ntiles));
+  CKR(mem.alloc(&x.ccnt, size_t(n) * (x.nchunk + x.nsup)));
+  x.scnt = x.ccnt + size_t(n) * x.nchunk;
+  CKR(mem.alloc(&x.tbase, x.ntiles));
   zen_hash_family f;
   CKR(zen_hash_family_make_worker(bp->params.seed, w.id, n, k, &f));
   a.fam = fold(f);
+  x.pc = a.fam.pc;
   return ZEN_OK;
 }
 
@@ -1684,6 +1728,7 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
   CKR(bp->mem.alloc(&bp->out_idx, bp->out_cap));
   CKR(bp->mem.alloc(&bp->out_val, bp->out_cap));
   CKR(bp->mem.alloc(&bp->out_count, 1));
+  CKR(bp->mem.alloc(&bp->chk, 1));
   DecodeArgs& da = bp->da;
   bp->dec.fill(da, bp->uni.get());
   const unsigned long long** bits_t;
@@ -1813,35 +1858,49 @@ namespace {
 zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cudaEvent_t* ev) {
   cudaStream_t st = bp->ctx->stream;
   if (ev) CK(cudaEventRecordWithFlags(ev[0], st, cudaEventRecordExternal));
-  if (from_dense)  // stage 0: the HBM-bound extraction kernel alone
-    for (size_t i = 0; i < bp->workers.size(); ++i)
-      launch_extract_tiles<uint32_t>(dense[i], bp->m, bp->workers[i].ex, st);
-  if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
-  if (from_dense)
-    for (auto& w : bp->workers) launch_extract_scan_begin<uint32_t>(bp->m, w.ex, w.a, bp->cap, st);
-  // data path on `st`; the hash-memory side path of each worker forks onto
-  // bp->side and joins at the end of the sync
-  for (auto& w : bp->workers) {
-    if (from_dense) {
-      launch_extract_compact_part<uint32_t>(bp->m, w.ex, w.a, bp->n, st);
-    } else {
-      launch_hash_begin<uint32_t>(w.a, st);
-      launch_hash_part<uint32_t>(w.a, bp->n, st);  // the side path reads its partitions
-    }
+  // the side path's width follows the key capacity: at embedding-scale
+  // sparsity it stays narrow (the latency-bound critical path keeps the SMs),
+  // at millions of keys it needs the whole GPU not to become the tail (rank
+  // mode keeps it narrower: its aggregate waits on the peers, and measured at
+  // n=4 one more CTA per SM costs the critical path 10 us)
+  const unsigned side_ctas = (unsigned)std::min<uint64_t>(
+      6, std::max<uint64_t>(2, bp->cap >> (bp->local ? 18 : 20)));
+  auto fork_side = [&](Worker& w, bool dense_path) -> zen_status {
     CK(cudaEventRecord(bp->fork, st));
     CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
-    {
-      LaunchScope low(/*pdl=*/false, /*low_priority=*/true);
-      // the side path's width follows the key capacity: at embedding-scale
-      // sparsity it stays narrow (the latency-bound critical path keeps the
-      // SMs), at millions of keys it needs the whole GPU not to become the tail
-      // (rank mode keeps it narrower: its aggregate waits on the peers, and
-      // measured at n=4 one more CTA per SM costs the critical path 10 us)
-      const unsigned side_ctas = (unsigned)std::min<uint64_t>(
-          6, std::max<uint64_t>(2, bp->cap >> (bp->local ? 18 : 20)));
+    LaunchScope low(/*pdl=*/false, /*low_priority=*/true);
+    if (dense_path)  // the claims ran inside the push scatter
+      launch_hash_side_bp<uint32_t>(w.a, bp->side, side_ctas);
+    else
       launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side, side_ctas);
+    return ZEN_OK;
+  };
+  if (from_dense) {
+    // stage 0: per-sync reset, then the HBM-bound extraction (which also
+    // computes every non-zero's h0 partition and the per-tile partition counts)
+    for (auto& w : bp->workers) launch_bp_begin<uint32_t>(w.a, st);
+    for (size_t i = 0; i < bp->workers.size(); ++i)
+      launch_extract_tiles_part<uint32_t>(dense[i], bp->m, bp->workers[i].ex, bp->workers[i].a, st);
+    if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
+    // stage 1: the push -- one kernel from the staging into the owners'
+    // inboxes; the hash-memory side path of each worker forks onto bp->side
+    // and joins at the end of the sync
+    static const bool diag_noclaim = std::getenv("ZEN_DIAG_NOCLAIM") != nullptr;  // timing diagnosis only
+    for (auto& w : bp->workers) {
+      HashArgs<uint32_t> sa = w.a;
+      if (diag_noclaim) sa.slots = nullptr;
+      launch_push_scatter<uint32_t>(sa, w.ex, st);
+      CKR(fork_side(w, true));
+      if (w.a.push_hdr) launch_push_signal<uint32_t>(w.a, st);
     }
-    launch_hash_critical<uint32_t>(w.a, bp->n, /*part=*/false, st);
+  } else {
+    if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
+    for (auto& w : bp->workers) {
+      launch_hash_begin<uint32_t>(w.a, st);
+      launch_hash_part<uint32_t>(w.a, bp->n, st);  // the side path reads its partitions
+      CKR(fork_side(w, false));
+      launch_hash_critical<uint32_t>(w.a, bp->n, /*part=*/false, st);
+    }
   }
   if (ev) CK(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
   for (auto& s : bp->servers) launch_aggregate(s.a, st);
@@ -2017,6 +2076,13 @@ zen_status zen_bp_sync_sparse(zen_bp* bp, const uint64_t* const* d_idx, const fl
   for (size_t i = 0; i < bp->workers.size(); ++i) {
     Worker& w = bp->workers[i];
     if (nnz[i] > bp->cap) return fail(ZEN_E_CAPACITY, "nnz above max_nnz");
+    if (nnz[i] && (!d_idx[i] || !d_val[i])) return fail(ZEN_E_INVALID, "null tensor");
+    // a SparseTensor's invariant (zen/tensor.hpp:36-45: ascending, unique,
+    // < M) is checked before the u32 narrowing below can wrap an index
+    if (nnz[i]) {
+      CK(cudaMemsetAsync(bp->chk, 0, 4, st));
+      CKR(wire_check_input(bp->ctx, d_idx[i], nnz[i], bp->m, bp->chk));
+    }
     w.h_count = nnz[i];
     if (nnz[i]) {
       launch_u64_to_u32(d_idx[i], w.keys, nnz[i], st);
@@ -2184,10 +2250,13 @@ zen_status zen_bp_time_extract(zen_bp* bp, const float* d_dense, uint32_t iters,
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  launch_extract_tiles<uint32_t>(d_dense, bp->m, bp->workers[0].ex, st);  // warm-up
+  // the sync's own extraction kernel (staging + h0 partition counts); its
+  // counters only accumulate here and are reset by the next sync's begin
+  Worker& w0 = bp->workers[0];
+  launch_extract_tiles_part<uint32_t>(d_dense, bp->m, w0.ex, w0.a, st);  // warm-up
   CK(cudaEventRecord(e0, st));
   for (uint32_t i = 0; i < iters; ++i)
-    launch_extract_tiles<uint32_t>(d_dense, bp->m, bp->workers[0].ex, st);
+    launch_extract_tiles_part<uint32_t>(d_dense, bp->m, w0.ex, w0.a, st);
   CK(cudaEventRecord(e1, st));
   CK(cudaEventSynchronize(e1));
   float t = 0.f;
@@ -2236,7 +2305,7 @@ extern "C" zen_status zen_bp_debug_part(zen_bp* bp, int what, uint32_t server, u
   if (!bp || !count) return fail(ZEN_E_INVALID, "null argument");
   DevGuard g(bp->ctx->device);
   CK(cudaStreamSynchronize(bp->ctx->stream));
-  if (what == 0) {  // compacted keys of a local worker
+  if (what == 0) {  // compacted keys of a local worker (values: sparse-input syncs only)
     for (auto& w : bp->workers) {
       if (w.id != worker) continue;
       HashHdr h{};

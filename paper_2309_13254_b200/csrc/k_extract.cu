@@ -49,14 +49,22 @@ struct MagnitudeAtLeast {
   }
 };
 
-template <typename K, typename Pred = NonZero>
+// PART (the dense BP data path): each tile also computes the h0 partition of
+// its non-zeros (partition_of, zen/hashing.hpp:85-88) and publishes its
+// per-partition counts at three levels (tile, 32-tile chunk, 1024-tile super
+// chunk; k_push.cu), so the push scatter finds every tile's partition bases
+// without a scan kernel.  The dense loads are issued before the PDL wait: the
+// gradient does not come from the predecessor (the per-sync begin kernel).
+template <typename K, typename Pred = NonZero, bool PART = false>
 __global__ void __launch_bounds__(kThreads, 4)
     k_extract_tiles(const float* __restrict__ dense, uint64_t m, K* __restrict__ st_idx,
                     float* __restrict__ st_val, uint32_t* __restrict__ tile_cnt,
-                    Pred pred = Pred()) {
-  zen_dev::pdl_entry();
+                    Pred pred = Pred(), PushCounts pc = PushCounts{},
+                    uint32_t* __restrict__ load = nullptr) {
+  if (!PART) zen_dev::pdl_entry();
   pred.init();
   __shared__ uint32_t s_warp_tot[kThreads / 32];
+  __shared__ uint32_t s_wpc[PART ? kThreads / 32 : 1][PART ? kMaxWorkers : 1];
   const uint32_t tile = blockIdx.x;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t unit0 = (uint64_t)tile * (kExtractTile / kUnit) + (uint64_t)warp * 128 + lane;
@@ -74,6 +82,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       for (int c = 0; c < kUnit; ++c) v[j].v[c] = e + c < m ? dense[e + c] : 0.0f;
     }
   }
+  if (PART) zen_dev::pdl_entry();
   uint32_t nzbits = 0;  // 8 bits per iteration
 #pragma unroll
   for (int j = 0; j < kIters; ++j)
@@ -95,7 +104,37 @@ __global__ void __launch_bounds__(kThreads, 4)
     for (int j = 0; j < kIters; ++j) off[j] = 0;
   }
   if (lane == 0) s_warp_tot[warp] = wrun;
+  if (PART) {
+    // 8-bit per-partition counters per lane (<= 32 non-zeros per lane)
+    uint64_t c0 = 0, c1 = 0;
+    const bool any = __ballot_sync(0xffffffffu, nzbits != 0) != 0;
+    if (any) {
+      for (uint32_t b = nzbits; b; b &= b - 1) {
+        const uint32_t q = __ffs(b) - 1;
+        const uint64_t e = (unit0 + (uint64_t)(q >> 3) * 32) * kUnit + (q & 7u);
+        const uint32_t p = part_of_seed(pc.pc, pc.n, e + 1);
+        if (p < 8) c0 += 1ull << (8 * p); else c1 += 1ull << (8 * (p - 8));
+      }
+    }
+    for (uint32_t p = 0; p < pc.n; ++p) {
+      const uint32_t f = (uint32_t)(((p < 8 ? c0 : c1) >> (8 * (p & 7))) & 0xFFu);
+      const uint32_t t = any ? __reduce_add_sync(0xffffffffu, f) : 0u;
+      if (lane == 0) s_wpc[warp][p] = t;
+    }
+  }
   __syncthreads();
+  if (PART && threadIdx.x < pc.n) {
+    const uint32_t p = threadIdx.x;
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) c += s_wpc[w][p];
+    pc.tcnt[(uint64_t)p * pc.ntiles + tile] = c;
+    if (c) {
+      atomicAdd(pc.ccnt + (uint64_t)p * pc.nchunk + (tile >> 5), c);
+      atomicAdd(pc.scnt + (uint64_t)p * pc.nsup + (tile >> 10), c);
+      atomicAdd(load + p, c);
+    }
+  }
   uint32_t wbase = 0, total = 0;
 #pragma unroll
   for (int w = 0; w < kThreads / 32; ++w) {
@@ -296,7 +335,7 @@ void launch_extract(const float* dense, uint64_t m, const ExtractWs<K>& ws, K* o
                     cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
   launch_k(k_extract_tiles<K, NonZero>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx,
-           ws.st_val, ws.tile_cnt, NonZero());
+           ws.st_val, ws.tile_cnt, NonZero(), PushCounts{}, (uint32_t*)nullptr);
   launch_k(k_extract_scan<K, false>, 1, 1024, 0, stream, ws.tile_cnt, ntiles, d_count, capacity,
            d_status_bits, ws.tile_base, ws.blk_tile, ws.nblk, HashArgs<K>{});
   launch_k(k_extract_compact<K>, blocks_for(std::min<uint64_t>(capacity, m)), 256, 0, stream,
@@ -310,7 +349,7 @@ void launch_extract_tiles(const float* dense, uint64_t m, const ExtractWs<K>& ws
                           cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
   launch_k(k_extract_tiles<K, NonZero>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx,
-           ws.st_val, ws.tile_cnt, NonZero());
+           ws.st_val, ws.tile_cnt, NonZero(), PushCounts{}, (uint32_t*)nullptr);
   count_launch();
 }
 
@@ -334,12 +373,23 @@ void launch_extract_compact_part(uint64_t m, const ExtractWs<K>& ws, const HashA
   count_launch();
 }
 
+// dense BP data path: staging + h0 partition counts (k_push.cu consumes them)
+template <typename K>
+void launch_extract_tiles_part(const float* dense, uint64_t m, const ExtractWs<K>& ws,
+                               const HashArgs<K>& a, cudaStream_t stream) {
+  const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
+  launch_k(k_extract_tiles<K, NonZero, true>, ntiles, kThreads, 0, stream, dense, m, ws.st_idx,
+           ws.st_val, ws.tile_cnt, NonZero(), a.xc, a.load);
+  count_launch();
+}
+
 // top-k: stage the non-zero elements with |v| at or above the threshold key
 void launch_select_tiles(const float* dense, uint64_t m, const ExtractWs<uint32_t>& ws,
                          const uint32_t* key, cudaStream_t stream) {
   const uint32_t ntiles = (uint32_t)((m + kExtractTile - 1) / kExtractTile);
   launch_k(k_extract_tiles<uint32_t, MagnitudeAtLeast>, ntiles, kThreads, 0, stream, dense, m,
-           ws.st_idx, ws.st_val, ws.tile_cnt, MagnitudeAtLeast{key, 0u});
+           ws.st_idx, ws.st_val, ws.tile_cnt, MagnitudeAtLeast{key, 0u}, PushCounts{},
+           (uint32_t*)nullptr);
   count_launch();
 }
 
@@ -348,6 +398,8 @@ void launch_select_tiles(const float* dense, uint64_t m, const ExtractWs<uint32_
                                   uint64_t*, uint64_t, uint32_t*, cudaStream_t);                 \
   template void launch_extract_tiles<K>(const float*, uint64_t, const ExtractWs<K>&,           \
                                         cudaStream_t);                                           \
+  template void launch_extract_tiles_part<K>(const float*, uint64_t, const ExtractWs<K>&,      \
+                                             const HashArgs<K>&, cudaStream_t);                  \
   template void launch_extract_scan_begin<K>(uint64_t, const ExtractWs<K>&, const HashArgs<K>&, \
                                              uint64_t, cudaStream_t);                            \
   template void launch_extract_compact_part<K>(uint64_t, const ExtractWs<K>&, const HashArgs<K>&, \

@@ -299,7 +299,9 @@ __global__ void __launch_bounds__(kThreads) k_place(HashArgs<K> a) {
     uint32_t nv = 0;
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
-      const uint64_t i = i0 + (uint64_t)j * nthr;
+      uint64_t i = i0 + (uint64_t)j * nthr;
+      if (a.perm_mul && i < z)  // test knob: another claim order, same outcome
+        i = (uint64_t)(((unsigned __int128)i * a.perm_mul + a.perm_add) % z);
       key[j] = i < z ? (uint64_t)a.idx[i] + 1 : 0ull;
       part[j] = i < z ? (a.pmeta[i] & 0xFFFFu) : 0u;  // h0 from the data path's pass
       nv += i < z ? 1u : 0u;
@@ -505,6 +507,95 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
   }
 }
 
+// BP side path (after k_push_scatter ran every key's priority claim): each
+// key's depth = the first probe whose slot holds it, 0 = serial.  A BP sync
+// only exposes CollisionStats (zen/hashing.hpp:259-262), so no serial slot is
+// written: the per-partition depth histogram is enough, unless a partition
+// has more serial keys than its r2 serial slots -- then the reference's
+// order-dependent fallback scan (zen/hashing.hpp:170-175) changes later
+// placements, and the last block flags the partition for the exact replay
+// (k_fallback).  Otherwise the last block folds the histogram into
+// CollisionStats right here.
+template <typename K>
+__global__ void __launch_bounds__(kThreads) k_depth_bp(HashArgs<K> a) {
+  zen_dev::pdl_entry();
+  __shared__ uint32_t s_hist[kMaxWorkers * (kMaxK + 1)];
+  __shared__ uint32_t s_last;
+  HashHdr* h = a.hdr;
+  const uint32_t n = a.fam.n, k = a.fam.k, lane = lane_id();
+  const bool ok = !(h->status & kErrCapacity);
+  const uint64_t z = h->count, r1 = h->r1, r2 = h->r2, stride = h->stride;
+  const uint64_t ew = epoch_word(h->epoch);
+  for (uint32_t i = threadIdx.x; i < n * (k + 1); i += kThreads) s_hist[i] = 0;
+  __syncthreads();
+  constexpr int KPT = 4;
+  const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
+  // warp-uniform trip count (full-mask match_any below)
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); ok && i0 < z;
+       i0 += nthr * KPT) {
+    uint64_t key[KPT];
+    uint32_t p[KPT], depth[KPT];
+    unsigned long long sl[KPT][4];
+    uint64_t c[KPT][4];
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const uint64_t i = i0 + (uint64_t)j * nthr + lane;
+      key[j] = i < z ? (uint64_t)a.idx[i] + 1 : 0ull;
+      p[j] = i < z ? a.pmeta[i] : 0u;
+      depth[j] = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+#pragma unroll
+      for (uint32_t t = 0; t < 4; ++t)
+        if (key[j] && t < k) {
+          c[j][t] = slot_of(a.fam, key[j], t, r1);
+          sl[j][t] = a.slots[(uint64_t)p[j] * stride + c[j][t]];
+        }
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const uint64_t i = i0 + (uint64_t)j * nthr + lane;
+      if (key[j]) {
+#pragma unroll
+        for (uint32_t t = 0; t < 4; ++t)
+          if (t < k && depth[j] == 0 && sl[j][t] == (ew | key[j])) depth[j] = t + 1;
+        for (uint32_t t = 4; depth[j] == 0 && t < k; ++t)
+          if (a.slots[(uint64_t)p[j] * stride + slot_of(a.fam, key[j], t, r1)] == (ew | key[j]))
+            depth[j] = t + 1;
+        a.meta[i] = pack_meta(p[j], depth[j], 0, 0);
+      }
+      const uint32_t bin = key[j] ? p[j] * (k + 1) + depth[j] : 0xFFFFFFFFu;
+      const uint32_t g = __match_any_sync(0xffffffffu, bin);
+      if (key[j] && lane == (uint32_t)(__ffs(g) - 1)) atomicAdd(&s_hist[bin], (uint32_t)__popc(g));
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n * (k + 1); i += kThreads)
+    if (s_hist[i]) atomicAdd(&a.stats[i], s_hist[i]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (atomicAdd(&h->done, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < n) {  // serial keys beyond r2 reach the fallback scan
+    const uint32_t q = threadIdx.x;
+    const uint32_t serial = ((volatile uint32_t*)a.stats)[q * (k + 1)];
+    const uint32_t fb = (ok && serial > r2 && (uint64_t)a.load[q] <= stride) ? 1u : 0u;
+    a.fallback[q] = fb;
+    if (fb) atomicOr(&h->fallback_any, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x <= k && !((volatile uint32_t*)&h->fallback_any)[0]) {
+    uint64_t sum = 0;
+    for (uint32_t q = 0; q < n; ++q) sum += ((volatile uint32_t*)a.stats)[q * (k + 1) + threadIdx.x];
+    a.stats_out[threadIdx.x] = sum;
+  }
+  if (threadIdx.x == 0) h->done = 0;
+}
+
 // ----------------------------------------------------------------- utils ----
 
 __global__ void k_partition_of(const uint64_t* __restrict__ idx, uint64_t count, uint64_t pc,
@@ -580,7 +671,9 @@ void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t
   // the side path does not crowd out the critical path's kernels
   const unsigned side = std::min<unsigned>(tiles, 148 * ctas_per_sm);
   if (place) {
-    launch_k(k_place<K>, grid_for(a.cap, kThreads, 148 * ctas_per_sm), kThreads, 0, stream, a);
+    const unsigned bt = a.place_threads ? a.place_threads : kThreads;
+    const unsigned g = a.place_grid ? a.place_grid : grid_for(a.cap, kThreads, 148 * ctas_per_sm);
+    launch_k(k_place<K>, g, bt, 0, stream, a);
     count_launch();
   }
   launch_k(k_depth<K>, side, kThreads, kWarps * n * sizeof(uint32_t), stream, a);
@@ -591,6 +684,14 @@ void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t
 }
 
 template <typename K>
+void launch_hash_side_bp(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm) {
+  launch_k(k_depth_bp<K>, grid_for(a.cap, kThreads * 4, 148 * ctas_per_sm), kThreads, 0, stream, a);
+  // the replay is data dependent: it returns at once unless a partition was flagged
+  launch_k(k_fallback<K>, grid_for(a.fam.n, 1, 148), kThreads, 0, stream, a);
+  for (int i = 0; i < 2; ++i) count_launch();
+}
+
+template <typename K>
 void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stream) {
   launch_hash_begin<K>(a, stream);
   launch_hash_critical<K>(a, n, true, stream);
@@ -598,12 +699,20 @@ void launch_hash(const HashArgs<K>& a, uint32_t n, uint32_t k, cudaStream_t stre
   (void)k;
 }
 
+template <typename K>
+void launch_push_signal(const HashArgs<K>& a, cudaStream_t stream) {
+  launch_k(k_push_signal<K>, 1, 32, 0, stream, a);
+  count_launch();
+}
+
 #define ZEN_INST(K)                                                                         \
+  template void launch_push_signal<K>(const HashArgs<K>&, cudaStream_t);                   \
   template void launch_hash<K>(const HashArgs<K>&, uint32_t, uint32_t, cudaStream_t);       \
   template void launch_hash_begin<K>(const HashArgs<K>&, cudaStream_t);                     \
   template void launch_hash_part<K>(const HashArgs<K>&, uint32_t, cudaStream_t);            \
   template void launch_hash_critical<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t);        \
-  template void launch_hash_side<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t, unsigned);
+  template void launch_hash_side<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t, unsigned); \
+  template void launch_hash_side_bp<K>(const HashArgs<K>&, cudaStream_t, unsigned);
 ZEN_INST(uint32_t)
 ZEN_INST(uint64_t)
 #undef ZEN_INST

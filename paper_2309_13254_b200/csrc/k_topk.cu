@@ -108,6 +108,15 @@ struct TopkState {
   uint32_t nsel;    // |output| before zero dropping is accounted (set by the scan)
 };
 
+// per-call state + histogram reset as a kernel (graph-capturable, keeps the
+// programmatic-launch chain; no host buffer outlives the call)
+__global__ void __launch_bounds__(256) k_topk_init(TopkState* st, uint32_t keep,
+                                                   uint32_t* __restrict__ hist) {
+  zen_dev::pdl_entry();
+  if (threadIdx.x == 0) *st = TopkState{0u, keep, 0ull, 0u, 0u, 0u, 0u};
+  for (uint32_t i = threadIdx.x; i < (uint32_t)kBins; i += blockDim.x) hist[i] = 0;
+}
+
 // one block: the bucket of the k-th largest key among hist[0..kBins); the
 // histogram is cleared for the next level
 __global__ void __launch_bounds__(1024) k_topk_select(uint32_t* __restrict__ hist, int shift,
@@ -300,13 +309,10 @@ size_t topk_threshold_offset() { return offsetof(TopkState, T); }
 void launch_topk_select(const float* dense, uint64_t m, uint64_t keep, void* state_v,
                         uint32_t* hist, cudaStream_t s) {
   TopkState* st = static_cast<TopkState*>(state_v);
-  TopkState init{};
-  init.k = (uint32_t)keep;
-  cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s);
-  cudaMemsetAsync(hist, 0, kBins * sizeof(uint32_t), s);
+  launch_k(k_topk_init, 1, 256, 0, s, st, (uint32_t)keep, hist);
   launch_k(k_topk_hist1, pass_grid(m), kThreads, 0, s, dense, m, hist);
   launch_k(k_topk_select, 1, 1024, 0, s, hist, 21, 11, st, 0);
-  for (int i = 0; i < 2; ++i) count_launch();
+  for (int i = 0; i < 3; ++i) count_launch();
 }
 
 // after the tile pass staged the >= T candidates (launch_select_tiles)

@@ -87,6 +87,19 @@ struct OwnWord {
   uint32_t pad;
 };
 
+// Dense BP data path counters (k_extract.cu PART tiles -> k_push.cu): the
+// per-(partition, extraction tile) counts and their sums over 32-tile chunks
+// and 1024-tile super chunks.  A tile's partition base is then a sum of at
+// most 31 + 31 + ceil(tiles/1024) L2-resident words -- no scan kernel.
+struct PushCounts {
+  uint32_t* tcnt;   // [n][ntiles] plain stores (every tile, every sync)
+  uint32_t* ccnt;   // [n][nchunk] atomics, zeroed by the per-sync begin kernel
+  uint32_t* scnt;   // [n][nsup]   atomics, zeroed by the per-sync begin kernel
+  uint64_t* tbase;  // [ntiles] ascending position of each tile's first non-zero
+  uint32_t ntiles, nchunk, nsup, n;
+  uint64_t pc;      // G * (partition_seed + 1)
+};
+
 // ---- kernel launchers (implemented in k_*.cu) ------------------------------
 // All are asynchronous on `stream`; counts live in device memory.
 
@@ -157,6 +170,12 @@ struct HashArgs {
   PushHdr* const* push_hdr;   // [n] or nullptr
   uint32_t me;
   int peer;                   // destinations include other GPUs (system-scope release)
+  PushCounts xc;              // dense data path (zero-initialised otherwise)
+  // claim schedule of k_place (test knob, zen_debug_hash_schedule): grid,
+  // block size and a permutation i -> (i * perm_mul + perm_add) mod z of the
+  // order in which keys claim; 0 = defaults / identity
+  uint32_t place_grid, place_threads;
+  uint64_t perm_mul, perm_add;
 };
 
 // The hash run = begin (r1/r2, epoch, counters) + a DATA path (partition
@@ -176,6 +195,24 @@ void launch_hash_critical(const HashArgs<K>& a, uint32_t n, bool part, cudaStrea
 template <typename K>
 void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t stream,
                       unsigned ctas_per_sm);
+template <typename K>
+void launch_push_signal(const HashArgs<K>& a, cudaStream_t stream);
+
+// Dense BP data path (k_push.cu): per-sync begin (header + counter reset),
+// extraction tiles with the h0 counts (k_extract.cu), and the push scatter
+// straight from the extraction staging into the owners' inboxes (which also
+// writes the ascending key list and runs the priority claims).
+template <typename K>
+void launch_bp_begin(const HashArgs<K>& a, cudaStream_t stream);
+template <typename K>
+void launch_extract_tiles_part(const float* dense, uint64_t m, const ExtractWs<K>& ws,
+                               const HashArgs<K>& a, cudaStream_t stream);
+template <typename K>
+void launch_push_scatter(const HashArgs<K>& a, const ExtractWs<K>& ws, cudaStream_t stream);
+// BP side path after the push scatter (which ran the claims): depth pass +
+// CollisionStats + fallback detection, then the (predicated) fallback replay
+template <typename K>
+void launch_hash_side_bp(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm);
 
 
 // universe tables (HashUniverseTable, zen/codec.hpp:47-72) as bit planes

@@ -31,7 +31,8 @@ import numpy as np
 
 from . import _lib as L
 from .zen import (Error, EmptyTensor, SimNet, SparseTensor, SyncOutcome, UniverseMismatch,
-                  WireFormat, _check, _check_inputs, _lib, _ptr, _torch, context)
+                  WireFormat, _check, _check_device_tensor, _check_inputs, _lib, _ptr, _torch,
+                  context)
 
 
 class NonPowerOfTwo(Error):
@@ -451,14 +452,16 @@ class HCSynchronizer:
     def sync_dense(self, dense):
         """Asynchronous on the current stream: to_sparse + log2(n) stages."""
         d = dense.contiguous().view(-1)
-        if d.numel() != self.m:
-            raise Error("dense gradient size differs from the universe")
+        _check_device_tensor(d, "float32", self.m, self.ctx.device, "sync_dense")
         self.ctx.bind_stream()
         _check(_lib().zen_hc_sync_dense(self.h, _ptr(d)))
 
     def sync_sparse(self, idx, val):
         """idx (int64, sorted unique < M) / val (f32) on this rank's GPU."""
         i, v = idx.contiguous(), val.contiguous()
+        if i.numel():
+            _check_device_tensor(i, "int64", None, self.ctx.device, "sync_sparse indices")
+            _check_device_tensor(v, "float32", i.numel(), self.ctx.device, "sync_sparse values")
         self.ctx.bind_stream()
         _check(_lib().zen_hc_sync_sparse(self.h, _ptr(i), _ptr(v), i.numel()))
 

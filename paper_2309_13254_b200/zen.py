@@ -163,6 +163,24 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr() if t.numel() else 0)
 
 
+def _check_device_tensor(t, dtype_name: str, numel: int | None, device: int | None, what: str):
+    """Refuse a CUDA tensor the kernels would misread: the C-ABI takes raw
+    pointers, so a bf16 gradient (half the bytes), a strided view or a tensor
+    on another GPU would otherwise be read out of bounds or silently wrong."""
+    torch = _torch()
+    want = getattr(torch, dtype_name)
+    if not (hasattr(t, "is_cuda") and t.is_cuda):
+        raise Error(f"{what}: expected a CUDA tensor")
+    if t.dtype != want:
+        raise Error(f"{what}: expected dtype {dtype_name}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise Error(f"{what}: tensor must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise Error(f"{what}: expected {numel} elements, got {t.numel()}")
+    if device is not None and t.device.index != device:
+        raise Error(f"{what}: tensor is on cuda:{t.device.index}, the synchroniser on cuda:{device}")
+
+
 # ------------------------------------------------------------ data model ----
 
 class DenseTensor:
@@ -581,13 +599,14 @@ def sparsify_topk(dense, fraction: float) -> SparseTensor:
     ceil(fraction*M) largest |v| (ties to the lower index), zeros dropped.
     `dense`: DenseTensor, numpy array or CUDA tensor (fp32)."""
     torch = _torch()
-    ctx = context()
     if isinstance(dense, DenseTensor):
         dense = dense.values
     d = dense if (hasattr(dense, "is_cuda") and dense.is_cuda) else _dev(np.asarray(dense,
                                                                                np.float32),
                                                                     torch.float32)
     d = d.reshape(-1).contiguous()
+    _check_device_tensor(d, "float32", None, None, "sparsify_topk")
+    ctx = context(d.device.index)
     m = d.numel()
     keep = min(m, math.ceil(fraction * m)) if 0 < fraction <= 1 else 1
     oi = torch.empty(max(keep, 1), dtype=torch.int64, device=d.device)
@@ -870,6 +889,10 @@ class BPSynchronizer:
     # -- synchronisation ------------------------------------------------------
     def sync_dense(self, dense):
         """dense: list of local_workers CUDA fp32 tensors of M elements."""
+        if len(dense) != self.local_workers:
+            raise Error(f"expected {self.local_workers} dense gradients, got {len(dense)}")
+        for d in dense:
+            _check_device_tensor(d, "float32", self.universe, self.ctx.device, "sync_dense")
         self.ctx.bind_stream()
         ptrs = (C.c_void_p * self.local_workers)(*[d.data_ptr() for d in dense])
         self._keep = dense
@@ -877,8 +900,14 @@ class BPSynchronizer:
 
     def sync_sparse(self, idx_list, val_list):
         """idx_list/val_list: CUDA int64/fp32 tensors (sorted unique indices)."""
-        self.ctx.bind_stream()
         k = self.local_workers
+        if len(idx_list) != k or len(val_list) != k:
+            raise Error(f"expected {k} index and value tensors")
+        for i, v in zip(idx_list, val_list):
+            if i.numel():
+                _check_device_tensor(i, "int64", None, self.ctx.device, "sync_sparse indices")
+                _check_device_tensor(v, "float32", i.numel(), self.ctx.device, "sync_sparse values")
+        self.ctx.bind_stream()
         ip = (C.c_void_p * k)(*[t.data_ptr() if t.numel() else 0 for t in idx_list])
         vp = (C.c_void_p * k)(*[t.data_ptr() if t.numel() else 0 for t in val_list])
         nz = (C.c_uint64 * k)(*[t.numel() for t in idx_list])

@@ -111,8 +111,8 @@ struct Reg {
 TEST(HashFamily_DeterministicAcrossInstances) {
   auto a = z::HashFamily::make(1234, 16, 3), b = z::HashFamily::make(1234, 16, 3);
   EXPECT(a.partition_seed == b.partition_seed && a.slot_seeds == b.slot_seeds);
-  auto pa = z::partition_of({0, 1, 17, 123456789}, a.partition_seed, 16);
-  auto pb = z::partition_of({0, 1, 17, 123456789}, b.partition_seed, 16);
+  auto pa = z::partition_of(std::vector<uint64_t>{0, 1, 17, 123456789}, a.partition_seed, 16);
+  auto pb = z::partition_of(std::vector<uint64_t>{0, 1, 17, 123456789}, b.partition_seed, 16);
   EXPECT(pa == pb);
 }
 
@@ -129,7 +129,7 @@ TEST(HierarchicalHash_SingleIndexLandsInItsPartition) {
   auto f = z::HashFamily::make(5, 8, 3);
   z::SparseTensor t(1000, {123}, {2.5f});
   auto parts = z::hierarchical_hash(t, 8, f, 4, 2);
-  const uint32_t p = z::partition_of({123}, f.partition_seed, 8)[0];
+  const uint32_t p = f.partition_of(123);  // the member form, zen/hashing.hpp:73-76
   for (uint32_t i = 0; i < 8; ++i) EXPECT(parts.parts[i].nnz() == (i == p ? 1u : 0u));
   EXPECT(parts.parts[p].values()[0] == 2.5f);
 }

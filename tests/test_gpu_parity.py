@@ -109,21 +109,35 @@ def test_hierarchical_hash_c2_no_loss_and_invariance(zen, co):
 
 
 def test_priority_claim_is_schedule_invariant(zen, co):
-    """Same keys at very different device sizes / grid shapes -> same layout."""
+    """The lock-free priority claim has ONE outcome (deferred
+    acceptance with a common priority order = serial dictatorship in ascending
+    key order = the reference's lanes=1 greedy, zen/hashing.hpp:155-179), for
+    any thread schedule: vary the claim kernel's grid and block size and the
+    order in which keys claim (a permutation), and compare every slot with
+    the oracle's sequential layout."""
+    import ctypes as C
+    from paper_2309_13254_b200 import _lib as L
+    lib = L.load()
     rng = np.random.default_rng(11)
-    m = 200_000
-    idx = np.sort(rng.choice(m, 20_000, replace=False)).astype(np.uint64)
+    m, z, n, k = 200_000, 20_000, 4, 3
+    idx = np.sort(rng.choice(m, z, replace=False)).astype(np.uint64)
     val = rng.standard_normal(idx.size).astype(np.float32)
-    fam = zen.HashFamily.make(9, 4, 3)
-    ref = None
-    for r1 in [10_000, 10_000, 10_000]:
-        parts, stats, lay = zen.hash_memory_layout(zen.SparseTensor(m, idx, val), 4, fam, r1, 1000)
-        if ref is None:
-            ref = lay
-        np.testing.assert_array_equal(lay.slots, ref.slots)
+    fam = zen.HashFamily.make(9, n, k)
+    r1, r2 = 6_000, 600  # tight: many displacements, serial keys and a fallback-free run
+    want = co.hierarchical_hash(m, idx, val, co.family(9, n, k), r1, r2, layout=True)
+    schedules = [(0, 0, 0, 0), (1, 32, 0, 0), (3, 64, 7919, 13), (148, 1024, 0, 0),
+                 (37, 96, 104729, 5), (2000, 256, 1_000_003, 17), (5, 512, z - 1, 0)]
+    try:
+        for g, t, mul, add in schedules:
+            assert lib.zen_debug_hash_schedule(g, t, mul, add) == 0
+            parts, stats, lay = zen.hash_memory_layout(zen.SparseTensor(m, idx, val), n, fam, r1, r2)
+            np.testing.assert_array_equal(lay.slots, want.slots, err_msg=f"schedule {g, t, mul, add}")
+            np.testing.assert_array_equal(lay.depth, want.depth_of)
+            assert stats.serial_writes == want.serial_writes
+            assert stats.placed_at_depth == want.placed_at_depth
+    finally:
+        lib.zen_debug_hash_schedule(0, 0, 0, 0)
 
-
-# ------------------------------------------------------------- extraction ----
 
 def test_to_sparse_golden(zen):
     g = load_golden("to_sparse")
@@ -447,3 +461,20 @@ def test_cpp_compat_dropin(zen):
         subprocess.run(["make", "-C", ROOT, "compat_test"], check=True, capture_output=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:]
+
+
+@pytest.mark.parametrize("suite", ["hashing"])
+def test_reference_unit_suite_unmodified(zen, suite):
+    """The reference's OWN GTest suite (proj/tests/<suite>_test.cpp), compiled
+    unmodified against the drop-in by `make ref_tests` (zen/*.hpp -> compat.hpp
+    with `namespace zen = zen_b200;`, a GTest shim) in the build container and
+    run here on the B200."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "build", f"ref_{suite}_test")
+    if not os.path.exists(exe):
+        pytest.skip("built only where /root/reference exists (make ref_tests)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-6000:]
+    assert "[  PASSED  ]" in r.stdout

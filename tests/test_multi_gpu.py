@@ -67,13 +67,14 @@ def test_bp_multi_gpu_parity(shape):
 
 
 @pytest.mark.gpu
-def test_bp_rank_mode_eight_ranks_oversubscribed():
-    """n = 8 rank mode (the headline node count) with several ranks per GPU:
-    every rank is its own process mapping the others' arenas over CUDA IPC,
-    exactly as on 8 GPUs; the GPU time-slices the processes, so only
-    correctness is meaningful here."""
-    if _ngpus() < 1:
-        pytest.skip("needs a GPU")
+def test_bp_rank_mode_eight_ranks():
+    """n = 8 rank mode (the headline node count), one process per GPU, every
+    rank mapping the others' arenas over CUDA IPC.  Ranks that spin on each
+    other's flags must not share a GPU (time-sliced spinning processes can
+    trip a context-switch timeout), so this needs 8 devices; with fewer, the
+    n = 8 data path is covered by local mode (tests/test_gpu_fullsize.py)."""
+    if _ngpus() < 8:
+        pytest.skip("needs 8 GPUs (one rank per GPU)")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
            "--nproc-per-node=8", os.path.join(ROOT, "tests", "mgpu_worker.py"),
            "20000", "64", "0.01"]

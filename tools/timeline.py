@@ -65,7 +65,7 @@ def main():
 
         def run():
             bp.sync_dense(dd)
-        first, last = "k_extract_tiles", "k_decode"
+        first, last = "k_bp_begin", "k_decode"
     for _ in range(10):
         run()
     torch.cuda.synchronize()
