@@ -78,6 +78,41 @@ def live_rows(rows, per_worker, n, omega, zipf, seed):
     return out
 
 
+def element_workload(m, n, density, omega, seed, hot_fraction=0.125, hot_mass=0.125,
+                     workers=None):
+    """Element-granular inputs with the reference generator's spec
+    (zen::generate, zen/workload.hpp:22-30, 56-154): ceil(d*M) distinct
+    indices per worker, a shared core of ceil(omega*d*M), the rest drawn per
+    worker from a two-tier distribution (hot_mass of the draws in the first
+    hot_fraction*M indices), integer values in [1, 16].  numpy streams, so the
+    same spec, not the same bits as libstdc++'s mt19937_64 (the parity tests
+    use the reference's own generator through oracle/_ref)."""
+    z = int(np.ceil(density * m))
+    hot = min(m, max(1, int(round(hot_fraction * m))))
+    rng = np.random.default_rng(seed)
+
+    def draw(k, used, r):
+        out = np.empty(0, np.int64)
+        while out.size < k:
+            want = k - out.size
+            nh = r.binomial(want, hot_mass if hot < m else 1.0)
+            c = np.concatenate([r.integers(0, hot, nh), r.integers(hot, m, want - nh)]) \
+                if hot < m else r.integers(0, hot, want)
+            c = np.setdiff1d(np.unique(c), used, assume_unique=False)
+            c = np.setdiff1d(c, out)
+            out = np.concatenate([out, r.permutation(c)[:want]])
+        return out
+
+    core = draw(min(z, int(np.ceil(omega * density * m))), np.empty(0, np.int64), rng)
+    res = {}
+    for w in (range(n) if workers is None else workers):
+        r = np.random.default_rng([seed, 0x10000 + w])
+        rest = draw(z - core.size, core, r)
+        idx = np.sort(np.concatenate([core, rest])).astype(np.uint64)
+        res[w] = (idx, r.integers(1, 17, idx.size).astype(np.float32))
+    return res
+
+
 def dense_gradient(rows, width, live, seed):
     r = np.random.default_rng(seed)
     g = np.zeros((rows, width), np.float32)
@@ -618,6 +653,51 @@ def main():
                "union": union, "union_ok": bool(union == int(nzr.sum()) * args.width)}
         del be, dd
 
+    # the same sync on element-granular gradients (the reference generator's
+    # spec, zen/workload.hpp:123-154): one non-zero per position instead of
+    # whole 64-float rows, the harder case for the bitmap fold and decode
+    elem = None
+    if not args.no_extras:
+        ei, evv = element_workload(m, n, args.density, args.omega, args.seed + 17,
+                                   workers=[rank])[rank]
+        ed = torch.zeros(m, dtype=torch.float32, device="cuda")
+        ed[torch.from_numpy(ei.view(np.int64)).cuda()] = torch.from_numpy(evv).cuda()
+        be = zen.BPSynchronizer(n, m, max_nnz=int(ei.size * 1.25) + 4096, params=params,
+                                rank=None if n == 1 else rank)
+        if n > 1:
+            be.connect_process_group()
+        for _ in range(max(3, args.warmup)):
+            be.sync_dense([ed])
+        be.wait()
+        barrier()
+        x0 = torch.cuda.Event(enable_timing=True)
+        x1 = torch.cuda.Event(enable_timing=True)
+        kx = max(5, args.steps // 2)
+        x0.record(stream)
+        for _ in range(kx):
+            be.sync_dense([ed])
+        x1.record(stream)
+        barrier()
+        be.wait()
+        ems = x0.elapsed_time(x1) / kx
+        be.enable_timing(True)
+        for _ in range(kx):
+            be.sync_dense([ed])
+        be.wait()
+        esm, ek = be.stage_times()
+        be.enable_timing(False)
+        if dist:
+            t = torch.tensor([ems] + list(esm / max(ek, 1)), device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems, esm, ek = float(t[0]), t[1:].cpu().numpy(), 1
+        elem = {"workload": f"element-granular {m} positions, {args.density:.2%} density, "
+                            f"omega={args.omega}, two-tier (1/8 hot, 1/8 mass)",
+                "nnz_per_worker": int(ei.size), "ms_per_sync": round(ems, 4),
+                "union_nnz": int(be.result_count()),
+                "stage_ms": {nm: round(float(x) / max(ek, 1), 5)
+                             for nm, x in zip(zen.STAGE_NAMES, esm)}}
+        del be, ed
+
     if rank != 0:
         if dist:
             dist.barrier()
@@ -666,6 +746,8 @@ def main():
         line["per_rank"] = per_rank
     if emu:
         line["emulated_local"] = emu
+    if elem:
+        line["element_granular"] = elem
     if world == 1 and not args.no_extras:
         line["extras"] = measure_extras(args, zen, d_dense, peak)
     if schemes is not None:

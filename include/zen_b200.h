@@ -113,7 +113,8 @@ zen_status zen_hash_family_make_worker(uint64_t shared_seed, uint32_t worker, ui
 /* Test knob for the lock-free priority claim (the hash-memory placement of
  * zen_hierarchical_hash on this thread): grid / block size of the claim kernel
  * and a permutation i -> (i * perm_mul + perm_add) mod count of the order in
- * which keys claim (used only when gcd(perm_mul, count) = 1).  The layout must
+ * which keys claim (used only when gcd(perm_mul, count) = 1; threads: a
+ * multiple of 32, at most 256).  The layout must
  * not change (the outcome is schedule invariant).  Zeros
  * restore the defaults. */
 zen_status zen_debug_hash_schedule(uint32_t grid, uint32_t threads, uint64_t perm_mul,

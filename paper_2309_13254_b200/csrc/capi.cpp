@@ -404,8 +404,8 @@ thread_local HashSchedule t_sched;
 
 zen_status zen_debug_hash_schedule(uint32_t grid, uint32_t threads, uint64_t perm_mul,
                                    uint64_t perm_add) {
-  if (threads && (threads % 32 || threads > 1024))
-    return fail(ZEN_E_INVALID, "threads must be a multiple of 32, <= 1024");
+  if (threads && (threads % 32 || threads > 256))
+    return fail(ZEN_E_INVALID, "threads must be a multiple of 32, <= 256");
   t_sched = HashSchedule{grid, threads, perm_mul, perm_add};
   return ZEN_OK;
 }
@@ -1345,12 +1345,13 @@ namespace {
 // can compute each other's sub-pointers from the base alone).
 struct ArenaLayout {
   size_t inbox_idx = 0, inbox_val = 0, push_hdr = 0, pull_hdr = 0;
-  std::vector<size_t> pull_bits, pull_vals;
+  std::vector<size_t> pull_bits, pull_vals, pull_cbase;
   size_t bytes = 0;
 };
 
 ArenaLayout make_layout(uint32_t n, uint64_t cap, const std::vector<uint64_t>& nw,
-                        const std::vector<uint64_t>& valcap, bool with_pull) {
+                        const std::vector<uint64_t>& valcap, bool with_pull,
+                        uint64_t nchunks) {
   ArenaLayout L;
   size_t off = 0;
   L.inbox_idx = off;
@@ -1363,7 +1364,12 @@ ArenaLayout make_layout(uint32_t n, uint64_t cap, const std::vector<uint64_t>& n
   off += align256(n * sizeof(PullHdr));
   L.pull_bits.assign(n, 0);
   L.pull_vals.assign(n, 0);
+  L.pull_cbase.assign(n, 0);
   if (with_pull) {
+    for (uint32_t s = 0; s < n; ++s) {  // per-chunk value bases (k_agg_values -> k_decode)
+      L.pull_cbase[s] = off;
+      off += align256((nchunks + 1) * 4);
+    }
     for (uint32_t s = 0; s < n; ++s) {
       L.pull_bits[s] = off;
       off += align256(std::max<uint64_t>(nw[s], 1) * 8);
@@ -1388,6 +1394,9 @@ struct Arena {
     return (unsigned long long*)(base + L.pull_bits[s]);
   }
   float* vals(const ArenaLayout& L, uint32_t s) const { return (float*)(base + L.pull_vals[s]); }
+  uint32_t* cbase(const ArenaLayout& L, uint32_t s) const {
+    return (uint32_t*)(base + L.pull_cbase[s]);
+  }
 };
 
 struct Worker {
@@ -1396,7 +1405,6 @@ struct Worker {
   float* vals = nullptr;
   HashArgs<uint32_t> a{};
   ExtractWs<uint32_t> ex{};
-  uint32_t epoch_runs = 0;
   uint64_t h_count = 0;  // staging for sparse inputs (stable address)
 };
 
@@ -1473,8 +1481,9 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   a.idx = w.keys;
   a.val = w.vals;
   CKR(mem.alloc(&a.hdr, 1));
+  // u32 slot words (vacant = ~0), kept vacant between syncs by the depth pass
   CKR(mem.alloc(&a.slots, size_t(n) * bp->stride_cap, false));
-  CK(cudaMemsetAsync(a.slots, 0xFF, size_t(n) * bp->stride_cap * 8, t_setup));
+  CK(cudaMemsetAsync(a.slots, 0xFF, size_t(n) * bp->stride_cap * sizeof(*a.slots), t_setup));
   a.slot_vals = nullptr;
   CKR(mem.alloc(&a.meta, cap));
   CKR(mem.alloc(&a.pmeta, cap));
@@ -1525,7 +1534,8 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   CKR(mem.alloc(&x.tcnt, size_t(n) * x.ntiles));
   CKR(mem.alloc(&x.ccnt, size_t(n) * (x.nchunk + x.nsup)));
   x.scnt = x.ccnt + size_t(n) * x.nchunk;
-  CKR(mem.alloc(&x.tbase, x.ntiles));
+  x.st_idx = w.ex.st_idx;
+  x.scatter_grid = push_scatter_grid<uint32_t>(!bp->local, x.ntiles);
   zen_hash_family f;
   CKR(zen_hash_family_make_worker(bp->params.seed, w.id, n, k, &f));
   a.fam = fold(f);
@@ -1565,8 +1575,13 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   CKR(mem.alloc(&db, a.ndst));
   CKR(mem.alloc(&dv, a.ndst));
   CKR(mem.alloc(&dh, a.ndst));
+  uint32_t** dc;
+  CKR(mem.alloc(&dc, a.ndst));
   a.dst_bits = db;
   a.dst_vals = dv;
+  a.dst_cbase = dc;
+  a.cprefix = bp->uni->cprefix;
+  a.nchunks = bp->uni->nchunks;
   a.dst_hdr = bp->local ? nullptr : dh;
   a.val_cap = bp->valcap[s.id];
   a.agg_count = s.agg_count;
@@ -1619,15 +1634,20 @@ zen_status bp_wire(zen_bp* bp) {
     std::vector<unsigned long long*> db(s.a.ndst);
     std::vector<float*> dvv(s.a.ndst);
     std::vector<PullHdr*> dh(s.a.ndst);
+    std::vector<uint32_t*> dcb(s.a.ndst);
     for (uint32_t d = 0; d < s.a.ndst; ++d) {
       const uint32_t r = bp->local ? 0 : d;  // local: one shared pull inbox (arena 0)
       const Arena& R = bp->arena_of(r);
       db[d] = R.bits(bp->L, s.id);
       dvv[d] = R.vals(bp->L, s.id);
       dh[d] = R.pull_hdr(bp->L) + s.id;
+      dcb[d] = R.cbase(bp->L, s.id);
     }
+    // this server's own (local) copy of U, read back for the chunk bases
+    s.a.own_bits = db[bp->local ? 0 : s.id];
     CKR(upload(const_cast<unsigned long long**>(s.a.dst_bits), db.data(), s.a.ndst));
     CKR(upload(const_cast<float**>(s.a.dst_vals), dvv.data(), s.a.ndst));
+    CKR(upload(const_cast<uint32_t**>(s.a.dst_cbase), dcb.data(), s.a.ndst));
     if (s.a.dst_hdr) CKR(upload(const_cast<PullHdr**>(s.a.dst_hdr), dh.data(), s.a.ndst));
   }
   // receiver: this node's pull inbox (local: arena 0)
@@ -1635,11 +1655,14 @@ zen_status bp_wire(zen_bp* bp) {
   std::vector<const unsigned long long*> hb(n);
   std::vector<const float*> hv(n);
   std::vector<const PullHdr*> hh(n);
+  std::vector<const uint32_t*> hc(n);
   for (uint32_t s = 0; s < n; ++s) {
     hb[s] = R.bits(bp->L, s);
     hv[s] = R.vals(bp->L, s);
     hh[s] = R.pull_hdr(bp->L) + s;
+    hc[s] = R.cbase(bp->L, s);
   }
+  CKR(upload(const_cast<const uint32_t**>(bp->da.cbase), hc.data(), n));
   CKR(upload(const_cast<const unsigned long long**>(bp->da.bits), hb.data(), n));
   CKR(upload(const_cast<const float**>(bp->da.vals), hv.data(), n));
   CKR(upload(const_cast<const PullHdr**>(bp->da.pull_hdr), hh.data(), n));
@@ -1694,8 +1717,8 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
     bp->nw[s] = (bp->uni->bs[s] + 63) / 64;
     bp->valcap[s] = std::min<uint64_t>(bp->uni->bs[s], uint64_t(n) * bp->cap);
   }
-  bp->L = make_layout(n, bp->cap, bp->nw, bp->valcap, true);
-  bp->L0 = make_layout(n, bp->cap, bp->nw, bp->valcap, false);
+  bp->L = make_layout(n, bp->cap, bp->nw, bp->valcap, true, bp->uni->nchunks);
+  bp->L0 = make_layout(n, bp->cap, bp->nw, bp->valcap, false, bp->uni->nchunks);
   CK(cudaStreamCreateWithFlags(&bp->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&bp->fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&bp->join, cudaEventDisableTiming));
@@ -1734,9 +1757,12 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
   const unsigned long long** bits_t;
   const float** vals_t;
   const PullHdr** ph_t;
+  const uint32_t** cb_t;
   CKR(bp->mem.alloc(&bits_t, n));
   CKR(bp->mem.alloc(&vals_t, n));
   CKR(bp->mem.alloc(&ph_t, n));
+  CKR(bp->mem.alloc(&cb_t, n));
+  da.cbase = cb_t;
   da.bits = bits_t;
   da.vals = vals_t;
   da.pull_hdr = ph_t;
@@ -1792,14 +1818,11 @@ zen_status zen_bp_set_params(zen_bp* bp, const zen_hash_params* p) {
   const uint64_t sc = stride_cap_for(*p, bp->cap, bp->n);
   for (auto& w : bp->workers) {
     if (sc > bp->stride_cap) {
-      unsigned long long* slots;
+      SlotOf<uint32_t>* slots;
       CKR(bp->mem.alloc(&slots, size_t(bp->n) * sc, false));
-      CK(cudaMemsetAsync(slots, 0xFF, size_t(bp->n) * sc * 8, t_setup));
+      CK(cudaMemsetAsync(slots, 0xFF, size_t(bp->n) * sc * sizeof(*slots), t_setup));
       w.a.slots = slots;
       w.a.stride_cap = sc;
-      uint32_t zero = 0;
-      CKR(upload(&w.a.hdr->epoch, &zero, 1));
-      w.epoch_runs = 0;
     }
     CKR(upload(&w.a.hdr->r1_mult, &p->r1_multiplier, 1));
     CKR(upload(&w.a.hdr->r2_ratio, &p->r2_ratio, 1));
@@ -1869,10 +1892,15 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     CK(cudaEventRecord(bp->fork, st));
     CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
     LaunchScope low(/*pdl=*/false, /*low_priority=*/true);
-    if (dense_path)  // the claims ran inside the push scatter
-      launch_hash_side_bp<uint32_t>(w.a, bp->side, side_ctas);
-    else
-      launch_hash_side<uint32_t>(w.a, bp->n, /*place=*/true, bp->side, side_ctas);
+    // claims (dense: straight from the extraction staging) + table-scan depth
+    // pass (CollisionStats) + the data-dependent fallback replay
+    HashArgs<uint32_t> sa = w.a;
+    if (dense_path) {
+      launch_place_tiles<uint32_t>(sa, bp->side, side_ctas);
+    } else {
+      sa.xc.st_idx = nullptr;  // the ascending key list, not the staging
+    }
+    launch_hash_side_bp<uint32_t>(sa, bp->side, side_ctas, /*place=*/!dense_path);
     return ZEN_OK;
   };
   if (from_dense) {
@@ -1885,11 +1913,8 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     // stage 1: the push -- one kernel from the staging into the owners'
     // inboxes; the hash-memory side path of each worker forks onto bp->side
     // and joins at the end of the sync
-    static const bool diag_noclaim = std::getenv("ZEN_DIAG_NOCLAIM") != nullptr;  // timing diagnosis only
     for (auto& w : bp->workers) {
-      HashArgs<uint32_t> sa = w.a;
-      if (diag_noclaim) sa.slots = nullptr;
-      launch_push_scatter<uint32_t>(sa, w.ex, st);
+      launch_push_scatter<uint32_t>(w.a, w.ex, st);
       CKR(fork_side(w, true));
       if (w.a.push_hdr) launch_push_signal<uint32_t>(w.a, st);
     }
@@ -1898,8 +1923,8 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     for (auto& w : bp->workers) {
       launch_hash_begin<uint32_t>(w.a, st);
       launch_hash_part<uint32_t>(w.a, bp->n, st);  // the side path reads its partitions
-      CKR(fork_side(w, false));
       launch_hash_critical<uint32_t>(w.a, bp->n, /*part=*/false, st);
+      CKR(fork_side(w, false));  // after the loads (k_part_scan) the depth pass reads
     }
   }
   if (ev) CK(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
@@ -1928,13 +1953,7 @@ zen_status bp_run(zen_bp* bp, bool from_dense, const float* const* dense) {
   bp->collected = false;
   if (bp->timing && bp->ev_head - bp->ev_tail >= (uint64_t)kRing)
     return fail(ZEN_E_INVALID, "timing ring full: call zen_bp_stage_times");
-  for (auto& w : bp->workers) {
-    if (++w.epoch_runs >= 0xFFFFF0u) {  // epoch wrap: refill the hash memory once
-      launch_fill_u64(w.a.slots, size_t(bp->n) * w.a.stride_cap, ~0ull, st);
-      CK(cudaMemsetAsync(&w.a.hdr->epoch, 0, 4, st));
-      w.epoch_runs = 1;
-    }
-  }
+  // (the BP hash memory is epoch-free: the depth pass leaves it vacant)
   cudaEvent_t* ring = bp->timing ? &bp->ev[(bp->ev_head % kRing) * (ZEN_STAGES + 1)] : nullptr;
   // CUDA-graph replay of the whole dense sync (not capturable on the legacy stream)
   const bool graph = bp->use_graph && from_dense && st != nullptr;

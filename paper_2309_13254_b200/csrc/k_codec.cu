@@ -309,6 +309,24 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
   __shared__ uint32_t sbase[kValThreads][NMAX];
   const uint32_t n = a.n, lane = lane_id();
   const uint64_t j = (uint64_t)blockIdx.x * kValThreads + threadIdx.x;
+  if (a.dst_cbase) {
+    // the receivers' value bases per global chunk: U's popcount below the
+    // chunk's first position P in I_s = block prefix + word prefix + the
+    // word's low bits (this server's prefixes of U, final since k_agg_union)
+    const uint64_t nth = (uint64_t)gridDim.x * kValThreads;
+    for (uint64_t c = j; c <= a.nchunks; c += nth) {
+      const uint64_t P = c < a.nchunks ? (uint64_t)a.cprefix[c * n + a.s] : a.bs;
+      const uint64_t w = P >> 6;
+      uint32_t b;
+      if (w >= a.nw) {
+        b = (uint32_t)*a.agg_count;
+      } else {
+        b = a.blk[(uint64_t)n * a.nblk + w / kPrefixBlockWords] + a.pre[(uint64_t)n * a.nws + w] +
+            (uint32_t)__popcll(a.own_bits[w] & lowmask64((uint32_t)(P & 63)));
+      }
+      for (uint32_t d = 0; d < a.ndst; ++d) a.dst_cbase[d][c] = b;
+    }
+  }
   const bool valid = j < a.nw;
   const uint32_t pb = (uint32_t)(j / kPrefixBlockWords);
   unsigned long long U = 0;
@@ -517,10 +535,20 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecodeArgs a, uint64_t n
   uint64_t cp = 0, base = 0, end = 0;
   if (lane < n && a.bits[lane]) {
     cp = a.cprefix[chunk * n + lane];
-    const uint64_t cpn =
-        (chunk + 1 < nchunks) ? (uint64_t)a.cprefix[(chunk + 1) * n + lane] : a.bs[lane];
-    base = bitmap_prefix(a, lane, cp);
-    end = (cpn > cp) ? bitmap_prefix(a, lane, cpn) : base;
+    if (a.cbase) {  // BP: the server sent its value base for every global chunk
+      base = a.cbase[lane][chunk];
+      end = a.cbase[lane][chunk + 1];
+    } else {
+      const uint64_t cpn =
+          (chunk + 1 < nchunks) ? (uint64_t)a.cprefix[(chunk + 1) * n + lane] : a.bs[lane];
+      base = bitmap_prefix(a, lane, cp);
+      end = (cpn > cp) ? bitmap_prefix(a, lane, cpn) : base;
+    }
+  }
+  if (a.cbase && w == 0 && lane == 0) {  // |result| = sum_s U_s (k_bpre's job otherwise)
+    uint64_t u = 0;
+    for (uint32_t s = 0; s < n; ++s) u += a.bits[s] ? a.cbase[s][nchunks] : 0u;
+    *a.out_count = u;
   }
   if (!__any_sync(0xffffffffu, end > base)) return;
   uint64_t ob = base;  // chunk's first output position = sum_s base_s
@@ -685,7 +713,10 @@ void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {
     launch_k(k_wait_pull, 1, 32, 0, stream, a);
     count_launch();
   }
-  launch_k(k_bpre, a.total_blocks ? a.total_blocks : 1, kPrefixThreads, 0, stream, a);
+  if (!a.cbase) {
+    launch_k(k_bpre, a.total_blocks ? a.total_blocks : 1, kPrefixThreads, 0, stream, a);
+    count_launch();
+  }
   constexpr unsigned T = kDecThreads;
   if (a.n <= 2)
     launch_k(k_decode<2>, ntiles, T, 0, stream, a, nwords);
@@ -695,7 +726,7 @@ void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {
     launch_k(k_decode<8>, ntiles, T, 0, stream, a, nwords);
   else
     launch_k(k_decode<16>, ntiles, T, 0, stream, a, nwords);
-  for (int i = 0; i < 2; ++i) count_launch();
+  count_launch();
 }
 
 }  // namespace zen

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kThreads) k_depth(HashArgs<K> a) {
       const uint64_t base = (uint64_t)p * stride;
       // the first four candidates are loaded together (k = 3 by default)
       uint64_t c4[4];
-      unsigned long long s4[4];
+      SlotOf<K> s4[4];
 #pragma unroll
       for (uint32_t t = 0; t < 4; ++t)
         if (t < k) {
@@ -345,13 +345,13 @@ __global__ void __launch_bounds__(kThreads) k_depth(HashArgs<K> a) {
       uint64_t hit = ~0ull;
 #pragma unroll
       for (uint32_t t = 0; t < 4; ++t)
-        if (t < k && depth == 0 && s4[t] == (ew | key)) {
+        if (t < k && depth == 0 && s4[t] == Slot<SlotOf<K>>::make(ew, key)) {
           depth = t + 1;
           hit = c4[t];
         }
       for (uint32_t t = 4; depth == 0 && t < k; ++t) {
         const uint64_t c = slot_of(a.fam, key, t, r1);
-        if (a.slots[base + c] == (ew | key)) {
+        if (a.slots[base + c] == Slot<SlotOf<K>>::make(ew, key)) {
           depth = t + 1;
           hit = c;
         }
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kThreads) k_serial_scatter(HashArgs<K> a) {
     const uint64_t spos = (uint64_t)a.tile_scnt[(uint64_t)p * a.tiles_cap + tile] + meta_srank(m);
     if (spos < h->r2) {
       const uint64_t s = (uint64_t)p * h->stride + h->r1 + spos;
-      a.slots[s] = epoch_word(h->epoch) | ((uint64_t)a.idx[i] + 1);
+      a.slots[s] = Slot<SlotOf<K>>::make(epoch_word(h->epoch), (uint64_t)a.idx[i] + 1);
       if (a.slot_vals) a.slot_vals[s] = a.val[i];
     }
   }
@@ -422,72 +422,130 @@ __global__ void __launch_bounds__(kThreads) k_serial_scatter(HashArgs<K> a) {
 
 // Sequential replay of partitions that reached the fallback scan, exactly as
 // place_index (zen/hashing.hpp:155-179) in ascending key order; the last block
-// folds the per-partition histograms into CollisionStats.
+// folds the per-partition histograms into CollisionStats.  One block per
+// flagged partition: the block scans the keys in ascending order 256 at a
+// time (a ballot collects the partition's keys) and one thread places them in
+// order.  Slots only ever fill during the replay, so the smallest vacant
+// parallel slot (the fallback scan's answer) never moves backwards: the scan
+// resumes from the previous answer instead of from slot 0, and the whole
+// replay costs O(keys + r1) instead of O(keys * r1).  The keys come from the
+// ascending list (standalone / sparse syncs) or straight from the extraction
+// staging, tile by tile (dense syncs).
+template <typename K>
+__device__ __forceinline__ void fallback_place(const HashArgs<K>& a, SlotOf<K>* base, uint64_t key,
+                                               uint64_t r1, uint64_t stride, uint64_t ew,
+                                               uint64_t& cursor, uint64_t& fbp, uint32_t& depth,
+                                               int64_t& slot) {
+  using S = Slot<SlotOf<K>>;
+  const uint32_t k = a.fam.k;
+  depth = 0;
+  slot = -1;
+  for (uint32_t t0 = 0; t0 < k && slot < 0; t0 += 4) {  // four probes in flight
+    uint64_t c[4];
+    SlotOf<K> w[4];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q)
+      if (t0 + q < k) {
+        c[q] = slot_of(a.fam, key, t0 + q, r1);
+        w[q] = base[c[q]];
+      }
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q)
+      if (slot < 0 && t0 + q < k && S::vacant(w[q], ew)) {
+        slot = (int64_t)c[q];
+        depth = t0 + q + 1;
+      }
+  }
+  if (slot < 0) {
+    const uint64_t q = cursor++;
+    if (q < stride) {
+      slot = (int64_t)q;
+    } else {
+      while (fbp < r1 && !S::vacant(base[fbp], ew)) ++fbp;
+      if (fbp < r1) slot = (int64_t)fbp;
+    }
+  }
+  if (slot >= 0) base[slot] = S::make(ew, key);
+}
+
 template <typename K>
 __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
   zen_dev::pdl_entry();
-  __shared__ uint32_t list[kThreads];
+  __shared__ K list[kThreads];
+  __shared__ uint32_t lpos[kThreads];
   __shared__ uint32_t wcount[kWarps];
-  __shared__ uint32_t s_last;
+  __shared__ uint32_t s_last, s_T;
   __shared__ uint32_t fstat[kMaxK + 1];
   HashHdr* h = a.hdr;
-  const uint32_t n = a.fam.n, k = a.fam.k;
+  const uint32_t n = a.fam.n, k = a.fam.k, lane = lane_id(), warp = threadIdx.x >> 5;
   const bool ok = !(h->status & kErrCapacity) && h->ovf_word == ~0ull && h->fallback_any;
+  const K* st = static_cast<const K*>(a.xc.st_idx);
   for (uint32_t p = blockIdx.x; ok && p < n; p += gridDim.x) {
     if (!a.fallback[p]) continue;
     const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
     const uint64_t ew = epoch_word(h->epoch);
-    unsigned long long* base = a.slots + (uint64_t)p * stride;
-    for (uint64_t q = threadIdx.x; q < stride; q += kThreads) base[q] = ~0ull;
+    using S = Slot<SlotOf<K>>;
+    SlotOf<K>* base = a.slots + (uint64_t)p * stride;
+    for (uint64_t q = threadIdx.x; q < stride; q += kThreads) base[q] = S::kVacant;
     if (threadIdx.x <= k) fstat[threadIdx.x] = 0;
     __syncthreads();
-    uint64_t cursor = r1;
-    for (uint64_t c0 = 0; c0 < z; c0 += kThreads) {
-      const uint64_t i = c0 + threadIdx.x;
-      const bool mine = i < z && meta_part(a.meta[i]) == p;
+    uint64_t cursor = r1, fbp = 0;
+    // one chunk of up to 256 ascending keys: collect partition p's, place in order
+    auto chunk = [&](bool valid, K key, uint64_t pos) {
+      const bool mine = valid && part_of(a.fam, (uint64_t)key + 1) == p;
       const uint32_t bal = __ballot_sync(0xffffffffu, mine);
-      if (lane_id() == 0) wcount[threadIdx.x >> 5] = __popc(bal);
+      if (lane == 0) wcount[warp] = __popc(bal);
       __syncthreads();
       uint32_t before = 0, total = 0;
       for (int w = 0; w < kWarps; ++w) {
-        if (w < (int)(threadIdx.x >> 5)) before += wcount[w];
+        if (w < (int)warp) before += wcount[w];
         total += wcount[w];
       }
-      if (mine) list[before + __popc(bal & lanemask_lt())] = (uint32_t)(i - c0);
+      if (mine) {
+        list[before + __popc(bal & lanemask_lt())] = key;
+        lpos[before + __popc(bal & lanemask_lt())] = (uint32_t)pos;
+      }
       __syncthreads();
       if (threadIdx.x == 0) {
         for (uint32_t e = 0; e < total; ++e) {
-          const uint64_t ii = c0 + list[e];
-          const uint64_t key = (uint64_t)a.idx[ii] + 1;
-          uint32_t depth = 0;
-          int64_t slot = -1;
-          for (uint32_t t = 0; t < k && slot < 0; ++t) {
-            const uint64_t c = slot_of(a.fam, key, t, r1);
-            if (base[c] > (ew | kKeyMask)) {
-              slot = (int64_t)c;
-              depth = t + 1;
-            }
+          uint32_t depth;
+          int64_t slot;
+          fallback_place(a, base, (uint64_t)list[e] + 1, r1, stride, ew, cursor, fbp, depth, slot);
+          if (!st) {  // the layout dump's depths and slot values
+            a.meta[lpos[e]] = pack_meta(p, depth, 0, 0);
+            if (slot >= 0 && a.slot_vals) a.slot_vals[(uint64_t)p * stride + slot] = a.val[lpos[e]];
           }
-          if (slot < 0) {
-            const uint64_t q = cursor++;
-            if (q < stride) {
-              slot = (int64_t)q;
-            } else {
-              for (uint64_t s = 0; s < r1 && slot < 0; ++s)
-                if (base[s] > (ew | kKeyMask)) slot = (int64_t)s;
-            }
-          }
-          if (slot >= 0) {
-            base[slot] = ew | key;
-            if (a.slot_vals) a.slot_vals[(uint64_t)p * stride + slot] = a.val[ii];
-          }
-          a.meta[ii] = pack_meta(p, depth, 0, 0);
           fstat[depth] += 1;
         }
       }
       __syncthreads();
+    };
+    if (st) {  // dense sync: the staging, tile by tile in ascending order
+      const PushCounts& x = a.xc;
+      for (uint32_t t = 0; t < x.ntiles; ++t) {
+        if (threadIdx.x < 32) {
+          uint32_t c = lane < n ? x.tcnt[(uint64_t)lane * x.ntiles + t] : 0u;
+          c = __reduce_add_sync(0xffffffffu, c);
+          if (lane == 0) s_T = c;
+        }
+        __syncthreads();
+        const uint32_t T = s_T;
+        for (uint32_t c0 = 0; c0 < T; c0 += kThreads) {
+          const uint32_t j = c0 + threadIdx.x;
+          chunk(j < T, j < T ? st[(uint64_t)t * kExtractTile + j] : (K)0, 0);
+        }
+        __syncthreads();  // s_T reuse
+      }
+    } else {
+      for (uint64_t c0 = 0; c0 < z; c0 += kThreads) {
+        const uint64_t i = c0 + threadIdx.x;
+        chunk(i < z, i < z ? a.idx[i] : (K)0, i);
+      }
     }
     if (threadIdx.x <= k) a.fb_stats[p * (k + 1) + threadIdx.x] = fstat[threadIdx.x];
+    __syncthreads();
+    if (sizeof(SlotOf<K>) == 4)  // epoch-free words (BP): leave the partition vacant
+      for (uint64_t q = threadIdx.x; q < stride; q += kThreads) base[q] = S::kVacant;
     __syncthreads();
   }
   __syncthreads();
@@ -507,66 +565,63 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
   }
 }
 
-// BP side path (after k_push_scatter ran every key's priority claim): each
-// key's depth = the first probe whose slot holds it, 0 = serial.  A BP sync
-// only exposes CollisionStats (zen/hashing.hpp:259-262), so no serial slot is
-// written: the per-partition depth histogram is enough, unless a partition
-// has more serial keys than its r2 serial slots -- then the reference's
-// order-dependent fallback scan (zen/hashing.hpp:170-175) changes later
-// placements, and the last block flags the partition for the exact replay
-// (k_fallback).  Otherwise the last block folds the histogram into
-// CollisionStats right here.
+// BP side path, after the claims (k_place): the depth histogram from the
+// TABLE instead of the keys.  Every parallel slot held in this epoch holds
+// exactly one key, whose depth is the first probe t with slot_of(key, t) ==
+// the slot -- a hash recomputation, not a random load -- and a key holding no
+// slot is serial, so serial_p = load_p - (slots held in p).  One coalesced
+// pass over the n*r1 parallel slots replaces k probes per key.  A BP sync
+// exposes only CollisionStats (zen/hashing.hpp:259-262), so no serial slot is
+// written; when a partition has more serial keys than its r2 serial slots,
+// the reference's order-dependent fallback scan (zen/hashing.hpp:170-175)
+// changes later placements and the last block flags the partition for the
+// exact replay (k_fallback).  Otherwise the last block folds CollisionStats.
 template <typename K>
-__global__ void __launch_bounds__(kThreads) k_depth_bp(HashArgs<K> a) {
+__global__ void __launch_bounds__(kThreads) k_depth_scan(HashArgs<K> a) {
   zen_dev::pdl_entry();
   __shared__ uint32_t s_hist[kMaxWorkers * (kMaxK + 1)];
   __shared__ uint32_t s_last;
   HashHdr* h = a.hdr;
   const uint32_t n = a.fam.n, k = a.fam.k, lane = lane_id();
   const bool ok = !(h->status & kErrCapacity);
-  const uint64_t z = h->count, r1 = h->r1, r2 = h->r2, stride = h->stride;
+  const uint64_t r1 = h->r1, r2 = h->r2, stride = h->stride;
   const uint64_t ew = epoch_word(h->epoch);
   for (uint32_t i = threadIdx.x; i < n * (k + 1); i += kThreads) s_hist[i] = 0;
   __syncthreads();
-  constexpr int KPT = 4;
+  // grid.y = partition: the parallel region [p*stride, p*stride + r1)
+  const uint32_t p = blockIdx.y;
+  using W = SlotOf<K>;
+  using S = Slot<W>;
+  W* region = a.slots + (uint64_t)p * stride;
   const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
-  // warp-uniform trip count (full-mask match_any below)
-  for (uint64_t i0 = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); ok && i0 < z;
-       i0 += nthr * KPT) {
-    uint64_t key[KPT];
-    uint32_t p[KPT], depth[KPT];
-    unsigned long long sl[KPT][4];
-    uint64_t c[KPT][4];
+  constexpr int R = 4;  // slots per thread per round, loads issued together
+  for (uint64_t c0 = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); ok && c0 < r1;
+       c0 += nthr * R) {  // warp-uniform trip count (full-mask match_any below)
+    W w[R];
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const uint64_t i = i0 + (uint64_t)j * nthr + lane;
-      key[j] = i < z ? (uint64_t)a.idx[i] + 1 : 0ull;
-      p[j] = i < z ? a.pmeta[i] : 0u;
-      depth[j] = 0;
+    for (int j = 0; j < R; ++j) {
+      const uint64_t c = c0 + (uint64_t)j * nthr + lane;
+      w[j] = c < r1 ? region[c] : S::kVacant;
+    }
+    if (sizeof(W) == 4) {  // epoch-free words: vacate what was read for the next sync
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const uint64_t c = c0 + (uint64_t)j * nthr + lane;
+        if (!S::vacant(w[j], ew)) region[c] = S::kVacant;
+      }
     }
 #pragma unroll
-    for (int j = 0; j < KPT; ++j)
-#pragma unroll
-      for (uint32_t t = 0; t < 4; ++t)
-        if (key[j] && t < k) {
-          c[j][t] = slot_of(a.fam, key[j], t, r1);
-          sl[j][t] = a.slots[(uint64_t)p[j] * stride + c[j][t]];
-        }
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const uint64_t i = i0 + (uint64_t)j * nthr + lane;
-      if (key[j]) {
-#pragma unroll
-        for (uint32_t t = 0; t < 4; ++t)
-          if (t < k && depth[j] == 0 && sl[j][t] == (ew | key[j])) depth[j] = t + 1;
-        for (uint32_t t = 4; depth[j] == 0 && t < k; ++t)
-          if (a.slots[(uint64_t)p[j] * stride + slot_of(a.fam, key[j], t, r1)] == (ew | key[j]))
-            depth[j] = t + 1;
-        a.meta[i] = pack_meta(p[j], depth[j], 0, 0);
+    for (int j = 0; j < R; ++j) {
+      const uint64_t c = c0 + (uint64_t)j * nthr + lane;
+      uint32_t d = 0;
+      if (!S::vacant(w[j], ew)) {  // held in this sync (c < r1 implied)
+        const uint64_t key = S::key(w[j]);
+        uint32_t t = 0;
+        while (t + 1 < k && slot_of(a.fam, key, t, r1) != c) ++t;
+        d = t + 1;
       }
-      const uint32_t bin = key[j] ? p[j] * (k + 1) + depth[j] : 0xFFFFFFFFu;
-      const uint32_t g = __match_any_sync(0xffffffffu, bin);
-      if (key[j] && lane == (uint32_t)(__ffs(g) - 1)) atomicAdd(&s_hist[bin], (uint32_t)__popc(g));
+      const uint32_t g = __match_any_sync(0xffffffffu, d);
+      if (d && lane == (uint32_t)(__ffs(g) - 1)) atomicAdd(&s_hist[p * (k + 1) + d], (uint32_t)__popc(g));
     }
   }
   __syncthreads();
@@ -575,14 +630,18 @@ __global__ void __launch_bounds__(kThreads) k_depth_bp(HashArgs<K> a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    s_last = (atomicAdd(&h->done, 1u) == gridDim.x - 1) ? 1u : 0u;
+    s_last = (atomicAdd(&h->done, 1u) == gridDim.x * gridDim.y - 1) ? 1u : 0u;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x < n) {  // serial keys beyond r2 reach the fallback scan
+  if (threadIdx.x < n) {  // serial = keys of p holding no slot
     const uint32_t q = threadIdx.x;
-    const uint32_t serial = ((volatile uint32_t*)a.stats)[q * (k + 1)];
+    volatile uint32_t* st = a.stats + q * (k + 1);
+    uint32_t held = 0;
+    for (uint32_t d = 1; d <= k; ++d) held += st[d];
+    const uint32_t serial = a.load[q] - held;
+    st[0] = serial;
     const uint32_t fb = (ok && serial > r2 && (uint64_t)a.load[q] <= stride) ? 1u : 0u;
     a.fallback[q] = fb;
     if (fb) atomicOr(&h->fallback_any, 1u);
@@ -684,8 +743,14 @@ void launch_hash_side(const HashArgs<K>& a, uint32_t n, bool place, cudaStream_t
 }
 
 template <typename K>
-void launch_hash_side_bp(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm) {
-  launch_k(k_depth_bp<K>, grid_for(a.cap, kThreads * 4, 148 * ctas_per_sm), kThreads, 0, stream, a);
+void launch_hash_side_bp(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm,
+                         bool place) {
+  if (place) {  // sparse syncs: claims over the ascending key list (dense: k_place_tiles)
+    launch_k(k_place<K>, grid_for(a.cap, kThreads * 4, 148 * ctas_per_sm), kThreads, 0, stream, a);
+    count_launch();
+  }
+  const unsigned gx = std::max(1u, grid_for(a.stride_cap, kThreads * 4, 148 * ctas_per_sm) / a.fam.n);
+  launch_k(k_depth_scan<K>, dim3(gx, a.fam.n), kThreads, 0, stream, a);
   // the replay is data dependent: it returns at once unless a partition was flagged
   launch_k(k_fallback<K>, grid_for(a.fam.n, 1, 148), kThreads, 0, stream, a);
   for (int i = 0; i < 2; ++i) count_launch();
@@ -712,7 +777,7 @@ void launch_push_signal(const HashArgs<K>& a, cudaStream_t stream) {
   template void launch_hash_part<K>(const HashArgs<K>&, uint32_t, cudaStream_t);            \
   template void launch_hash_critical<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t);        \
   template void launch_hash_side<K>(const HashArgs<K>&, uint32_t, bool, cudaStream_t, unsigned); \
-  template void launch_hash_side_bp<K>(const HashArgs<K>&, cudaStream_t, unsigned);
+  template void launch_hash_side_bp<K>(const HashArgs<K>&, cudaStream_t, unsigned, bool);
 ZEN_INST(uint32_t)
 ZEN_INST(uint64_t)
 #undef ZEN_INST

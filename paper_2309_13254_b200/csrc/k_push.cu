@@ -21,10 +21,9 @@
 //                   (zen/hashing.hpp:176-177), the global minimum of which is
 //                   the reference's SerialOverflow witness.
 //
-// The same kernel writes the ascending key list with each key's partition and
-// runs the hash-memory placement (the lock-free priority claim, k_hash.cu) of
-// the keys it holds in registers, so only the depth pass (k_depth_bp:
-// CollisionStats, fallback detection) is left for the side stream.  Before it:
+// The same kernel writes the ascending key list with each key's partition, from
+// which the hash-memory placement (the lock-free priority claim + the depth
+// pass, k_hash.cu) runs on the side stream, off the critical path.  Before it:
 // k_bp_begin (first kernel of a sync: header + counter reset, its latency
 // hidden under the extraction's first loads).
 #include "zen_common.cuh"
@@ -58,6 +57,8 @@ __global__ void __launch_bounds__(256) k_bp_begin(HashArgs<K> a) {
       h->fb_done = 0;
       h->fallback_any = 0;
       h->bad_index = ~0ull;
+      h->work[0] = 0;
+      h->work[1] = 0;
     }
     for (uint32_t i = threadIdx.x; i < n * (k + 1); i += blockDim.x) {
       a.stats[i] = 0;
@@ -75,22 +76,55 @@ __global__ void __launch_bounds__(256) k_bp_begin(HashArgs<K> a) {
     x.ccnt[i] = 0;
 }
 
-template <typename K>
+// Tile-group prologue shared by the scatter and the claims: the entries of
+// the group's kPushTiles extraction tiles (their staging windows back to
+// back) and the exclusive prefix over the tiles.
+__device__ __forceinline__ uint32_t group_prefix(const PushCounts& x, uint32_t n, uint32_t t0,
+                                                 uint32_t* s_tpre) {
+  const uint32_t lane = lane_id();
+  uint32_t c = 0;
+  const uint32_t t = t0 + lane;
+  if (lane < (uint32_t)kPushTiles && t < x.ntiles)
+    for (uint32_t p = 0; p < n; ++p) c += x.tcnt[(uint64_t)p * x.ntiles + t];
+  const uint32_t inc = warp_inclusive_sum(c);
+  if (lane < (uint32_t)kPushTiles) s_tpre[lane + 1] = inc;
+  if (lane == 0) s_tpre[0] = 0;
+  return __shfl_sync(0xffffffffu, inc, kPushTiles - 1);
+}
+
+// staging address of group entry e (its tile: s_tpre[i] <= e < s_tpre[i + 1])
+__device__ __forceinline__ uint64_t group_src(const uint32_t* s_tpre, uint32_t t0, uint32_t e) {
+  uint32_t i = 0;
+#pragma unroll
+  for (int q = 1; q < kPushTiles; ++q) i += (s_tpre[q] <= e) ? 1u : 0u;
+  return (uint64_t)(t0 + i) * kExtractTile + (e - s_tpre[i]);
+}
+
+// Persistent blocks take tile groups from a counter (balanced however skewed
+// the rows are).  REORDER (peer destinations): each round's entries are
+// regrouped in shared memory into per-partition runs, so consecutive threads
+// store consecutive positions of one part -- full-line NVLink stores.  Local
+// destinations skip the regrouping: a warp's entries of one partition land on
+// consecutive positions and L2 merges the partial sectors, so a round needs a
+// single block barrier, and the next round's staging loads are issued before
+// the current round's stores.
+template <typename K, bool REORDER>
 __global__ void __launch_bounds__(kPushThreads)
     k_push_scatter(HashArgs<K> a, const K* __restrict__ st_idx, const float* __restrict__ st_val) {
   zen_dev::pdl_entry();
   __shared__ uint64_t s_base[kMaxWorkers];
   __shared__ uint32_t s_run[kMaxWorkers], s_tot[kMaxWorkers];
   __shared__ uint32_t s_off[kMaxWorkers];
-  __shared__ uint32_t s_tpre[kPushTiles + 1];  // entry prefix over the block's tiles
+  __shared__ uint32_t s_tpre[kPushTiles + 1];
   __shared__ uint32_t s_pre[kPushPer * kPushWarps][kMaxWorkers];  // [sub-round j, warp][p]
-  __shared__ K s_x[kPushRound];
-  __shared__ float s_v[kPushRound];
-  __shared__ uint8_t s_p[kPushRound];
+  __shared__ uint32_t s_wh[2][kPushWarps][kMaxWorkers];  // per-warp partition counts (2 rounds)
+  __shared__ K s_x[REORDER ? kPushRound : 1];
+  __shared__ float s_v[REORDER ? kPushRound : 1];
+  __shared__ uint8_t s_p[REORDER ? kPushRound : 1];
   __shared__ uint64_t s_z;
+  __shared__ uint32_t s_group;
   const PushCounts& x = a.xc;
   const uint32_t n = a.fam.n, lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t t0 = blockIdx.x * kPushTiles;
   HashHdr* h = a.hdr;
   if (warp == 0) {
     const uint64_t l = lane < n ? (uint64_t)a.load[lane] : 0ull;
@@ -98,15 +132,6 @@ __global__ void __launch_bounds__(kPushThreads)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
     if (lane == 0) s_z = z;
-    if (lane < n) s_run[lane] = 0;
-  } else if (warp == 1) {  // entries per tile of this block
-    uint32_t c = 0;
-    const uint32_t t = t0 + lane;
-    if (lane < (uint32_t)kPushTiles && t < x.ntiles)
-      for (uint32_t p = 0; p < n; ++p) c += x.tcnt[(uint64_t)p * x.ntiles + t];
-    const uint32_t inc = warp_inclusive_sum(c);
-    if (lane < (uint32_t)kPushTiles) s_tpre[lane + 1] = inc;
-    if (lane == 0) s_tpre[0] = 0;
   }
   __syncthreads();
   // z and the worker's sizes r1, r2 (zen/schemes.hpp:363-367), the same in every block
@@ -124,122 +149,229 @@ __global__ void __launch_bounds__(kPushThreads)
     h->ntiles = (uint32_t)((z + kHashTile - 1) / kHashTile);
     if (bad) atomicOr(&h->status, kErrCapacity);
   }
-  const uint32_t T = s_tpre[kPushTiles];
-  if (bad || T == 0) return;
-  // partition bases of the block's first tile: three levels of counts, lane-parallel
-  {
-    const uint32_t sup = t0 >> 10, c_lo = sup << 5, c_hi = t0 >> 5, t_lo = c_hi << 5;
-    for (uint32_t p = warp; p < n; p += kPushWarps) {
-      const uint32_t* sc = x.scnt + (uint64_t)p * x.nsup;
-      uint64_t acc = 0;
-      if (c_lo + lane < c_hi) acc += x.ccnt[(uint64_t)p * x.nchunk + c_lo + lane];
-      if (t_lo + lane < t0) acc += x.tcnt[(uint64_t)p * x.ntiles + t_lo + lane];
-      for (uint32_t i = lane; i < sup; i += 32) acc += sc[i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) s_base[p] = acc;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < (uint32_t)kPushTiles && t0 + threadIdx.x < x.ntiles) {
-    uint64_t b = 0;
-    for (uint32_t p = 0; p < n; ++p) b += s_base[p];
-    x.tbase[t0 + threadIdx.x] = b + s_tpre[threadIdx.x];  // the side path's compaction offsets
-  }
+  if (bad) return;
   const uint64_t lim = r1 + r2;
-  uint64_t bstart = 0;  // the block's first ascending position (its first tile's tbase)
-  for (uint32_t p = 0; p < n; ++p) bstart += s_base[p];
-  const uint64_t ew = epoch_word(h->epoch);
-  K* keys = const_cast<K*>(a.idx);
-  for (uint32_t r0 = 0; r0 < T; r0 += kPushRound) {
-    for (uint32_t i = threadIdx.x; i < kPushPer * kPushWarps * kMaxWorkers; i += kPushThreads)
-      (&s_pre[0][0])[i] = 0;
-    K xv[kPushPer];
-    float vv[kPushPer];
-    uint32_t pv[kPushPer], rk[kPushPer];
-#pragma unroll
-    for (int j = 0; j < kPushPer; ++j) {
-      const uint32_t e = r0 + j * kPushThreads + threadIdx.x;
-      if (e < T) {
-        uint32_t i = 0;  // the entry's tile: s_tpre[i] <= e < s_tpre[i + 1]
-#pragma unroll
-        for (int q = 1; q < kPushTiles; ++q) i += (s_tpre[q] <= e) ? 1u : 0u;
-        const uint64_t src = (uint64_t)(t0 + i) * kExtractTile + (e - s_tpre[i]);
-        xv[j] = st_idx[src];
-        vv[j] = st_val[src];
-      }
-    }
-    __syncthreads();  // s_pre cleared
-#pragma unroll
-    for (int j = 0; j < kPushPer; ++j) {
-      const uint32_t e = r0 + j * kPushThreads + threadIdx.x;
-      pv[j] = e < T ? part_of(a.fam, (uint64_t)xv[j] + 1) : 0xFFFFFFFFu;
-      if (e < T) {  // the ascending key list + partitions the side path's depth pass reads
-        keys[bstart + e] = xv[j];
-        a.pmeta[bstart + e] = pv[j];
-      }
-      const uint32_t g = __match_any_sync(0xffffffffu, pv[j]);
-      rk[j] = __popc(g & lanemask_lt());
-      if (e < T && lane == (uint32_t)(__ffs(g) - 1)) s_pre[j * kPushWarps + warp][pv[j]] = __popc(g);
-    }
+  const uint32_t ngroups = (x.ntiles + kPushTiles - 1) / kPushTiles;
+  for (;;) {
+    if (threadIdx.x == 0) s_group = atomicAdd(&h->work[0], 1u);
+    if (warp == 0 && lane < n) s_run[lane] = 0;
     __syncthreads();
-    // per partition: exclusive scan over the round's (sub-round, warp) rows, in
-    // ascending entry order
-    for (uint32_t p = warp; p < n; p += kPushWarps) {
-      const uint32_t v = s_pre[lane][p];
-      const uint32_t inc = warp_inclusive_sum(v);
-      s_pre[lane][p] = inc - v;
-      if (lane == 31) s_tot[p] = inc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t v = lane < n ? s_tot[lane] : 0u;
-      const uint32_t inc = warp_inclusive_sum(v);
-      if (lane < n) s_off[lane] = inc - v;
-    }
-    __syncthreads();
+    const uint32_t g = s_group;
+    if (g >= ngroups) break;
+    const uint32_t t0 = g * kPushTiles;
+    uint32_t T = 0;
+    if (warp == 1) T = group_prefix(x, n, t0, s_tpre);
+    // partition bases of the group's first tile: three levels of counts, lane-parallel
+    {
+      const uint32_t sup = t0 >> 10, c_lo = sup << 5, c_hi = t0 >> 5, t_lo = c_hi << 5;
+      for (uint32_t p = warp; p < n; p += kPushWarps) {
+        const uint32_t* sc = x.scnt + (uint64_t)p * x.nsup;
+        uint64_t acc = 0;
+        if (c_lo + lane < c_hi) acc += x.ccnt[(uint64_t)p * x.nchunk + c_lo + lane];
+        if (t_lo + lane < t0) acc += x.tcnt[(uint64_t)p * x.ntiles + t_lo + lane];
+        for (uint32_t i = lane; i < sup; i += 32) acc += sc[i];
 #pragma unroll
-    for (int j = 0; j < kPushPer; ++j) {
-      const uint32_t e = r0 + j * kPushThreads + threadIdx.x;
-      if (e < T) {
-        const uint32_t p = pv[j];
-        const uint32_t slot = s_off[p] + s_pre[j * kPushWarps + warp][p] + rk[j];
-        s_x[slot] = xv[j];
-        s_v[slot] = vv[j];
-        s_p[slot] = (uint8_t)p;
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) s_base[p] = acc;
       }
     }
     __syncthreads();
-    const uint32_t cnt = min(T - r0, (uint32_t)kPushRound);
-    for (uint32_t sl = threadIdx.x; sl < cnt; sl += kPushThreads) {
-      const uint32_t p = s_p[sl];
-      const uint64_t pos = s_base[p] + s_run[p] + (sl - s_off[p]);
-      const K key = s_x[sl];
-      if (pos < a.dst_cap) {
-        a.dst_idx[p][pos] = key;
-        a.dst_val[p][pos] = s_v[sl];
-      } else {
-        atomicOr(&h->status, kErrCapacity);
-      }
-      if (pos == lim)
-        atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)key + 1) << 16) | p);
-    }
-    // hierarchical hash placement of this round's keys: the lock-free priority
-    // claim (k_hash.cu, zen_hash_dev.cuh place_keys) -- every key of the sync
-    // has claimed once this kernel ends, which the depth pass needs
-    if (a.slots) {
-      uint64_t kk[kPushPer];
-      uint32_t nv = 0;
+    T = s_tpre[kPushTiles];
+    if (!REORDER) {
+      // lane p < n keeps partition p's running offset; rounds are pipelined
+      uint32_t run = 0;
+      const uint64_t mybase = lane < n ? s_base[lane] : 0ull;
+      uint32_t parity = 0;
+      K xn[kPushPer];
+      float vn[kPushPer];
 #pragma unroll
       for (int j = 0; j < kPushPer; ++j) {
-        const bool v = r0 + j * kPushThreads + threadIdx.x < T;  // valid j form a prefix
-        kk[j] = v ? (uint64_t)xv[j] + 1 : 0ull;
-        nv += v ? 1u : 0u;
+        const uint32_t e = warp * (32 * kPushPer) + j * 32 + lane;
+        if (e < T) {
+          const uint64_t src = group_src(s_tpre, t0, e);
+          xn[j] = st_idx[src];
+          vn[j] = st_val[src];
+        }
       }
-      place_keys<kPushPer>(a.fam, a.slots, kk, pv, nv, r1, lim, ew);
+      for (uint32_t r0 = 0; r0 < T; r0 += kPushRound, parity ^= 1u) {
+        K xv[kPushPer];
+        float vv[kPushPer];
+        uint32_t pv[kPushPer], rk[kPushPer];
+#pragma unroll
+        for (int j = 0; j < kPushPer; ++j) {
+          xv[j] = xn[j];
+          vv[j] = vn[j];
+          const uint32_t e = r0 + warp * (32 * kPushPer) + j * 32 + lane;
+          pv[j] = e < T ? part_of(a.fam, (uint64_t)xv[j] + 1) : 0xFFFFFFFFu;
+          const uint32_t en = e + kPushRound;  // next round's entry
+          if (en < T) {
+            const uint64_t src = group_src(s_tpre, t0, en);
+            xn[j] = st_idx[src];
+            vn[j] = st_val[src];
+          }
+        }
+        // per-warp stable ranks: a warp's entries are (j, lane)-ascending; the
+        // leader of each partition group keeps the warp's running count
+        uint32_t* wh = s_wh[parity][warp];
+        if (lane < kMaxWorkers) wh[lane] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kPushPer; ++j) {
+          const uint32_t gm = __match_any_sync(0xffffffffu, pv[j]);
+          const uint32_t leader = __ffs(gm) - 1;
+          uint32_t before = 0;
+          if (pv[j] != 0xFFFFFFFFu && lane == leader) {
+            before = wh[pv[j]];
+            wh[pv[j]] = before + __popc(gm);
+          }
+          rk[j] = __shfl_sync(0xffffffffu, before, leader) + __popc(gm & lanemask_lt());
+          __syncwarp();
+        }
+        __syncthreads();
+        // lane p < n: this warp's offset in partition p and the round's total
+        uint32_t woff = 0, tot = 0;
+        if (lane < n) {
+#pragma unroll
+          for (int w = 0; w < kPushWarps; ++w) {
+            const uint32_t c = s_wh[parity][w][lane];
+            woff += (w < (int)warp) ? c : 0u;
+            tot += c;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kPushPer; ++j) {
+          const uint32_t p = pv[j];
+          const uint64_t b = __shfl_sync(0xffffffffu, mybase + run + woff, p < kMaxWorkers ? p : 0u);
+          if (p != 0xFFFFFFFFu) {
+            const uint64_t pos = b + rk[j];
+            if (pos < a.dst_cap) {
+              a.dst_idx[p][pos] = xv[j];
+              a.dst_val[p][pos] = vv[j];
+            } else {
+              atomicOr(&h->status, kErrCapacity);
+            }
+            if (pos == lim)
+              atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)xv[j] + 1) << 16) | p);
+          }
+        }
+        run += tot;
+      }
+      continue;  // the loop head's barrier orders the next group's shared writes
     }
+    for (uint32_t r0 = 0; r0 < T; r0 += kPushRound) {
+      K xv[kPushPer];
+      float vv[kPushPer];
+      uint32_t pv[kPushPer], rk[kPushPer];
+#pragma unroll
+      for (int j = 0; j < kPushPer; ++j) {
+        const uint32_t e = r0 + j * kPushThreads + threadIdx.x;
+        pv[j] = 0xFFFFFFFFu;
+        if (e < T) {
+          const uint64_t src = group_src(s_tpre, t0, e);
+          xv[j] = st_idx[src];
+          vv[j] = st_val[src];
+          pv[j] = part_of(a.fam, (uint64_t)xv[j] + 1);
+        }
+      }
+      for (uint32_t i = threadIdx.x; i < kPushPer * kPushWarps * kMaxWorkers; i += kPushThreads)
+        (&s_pre[0][0])[i] = 0;
+      __syncthreads();  // s_pre cleared
+#pragma unroll
+      for (int j = 0; j < kPushPer; ++j) {
+        const uint32_t e = r0 + j * kPushThreads + threadIdx.x;
+        const uint32_t gm = __match_any_sync(0xffffffffu, pv[j]);
+        rk[j] = __popc(gm & lanemask_lt());
+        if (e < T && lane == (uint32_t)(__ffs(gm) - 1)) s_pre[j * kPushWarps + warp][pv[j]] = __popc(gm);
+      }
+      __syncthreads();
+      // per partition: exclusive scan over the round's (sub-round, warp) rows, in
+      // ascending entry order
+      for (uint32_t p = warp; p < n; p += kPushWarps) {
+        const uint32_t v = s_pre[lane][p];
+        const uint32_t inc = warp_inclusive_sum(v);
+        s_pre[lane][p] = inc - v;
+        if (lane == 31) s_tot[p] = inc;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t v = lane < n ? s_tot[lane] : 0u;
+        const uint32_t inc = warp_inclusive_sum(v);
+        if (lane < n) s_off[lane] = inc - v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kPushPer; ++j) {
+        const uint32_t e = r0 + j * kPushThreads + threadIdx.x;
+        if (e < T) {
+          const uint32_t p = pv[j];
+          const uint32_t slot = s_off[p] + s_pre[j * kPushWarps + warp][p] + rk[j];
+          s_x[slot] = xv[j];
+          s_v[slot] = vv[j];
+          s_p[slot] = (uint8_t)p;
+        }
+      }
+      __syncthreads();
+      const uint32_t cnt = min(T - r0, (uint32_t)kPushRound);
+      for (uint32_t sl = threadIdx.x; sl < cnt; sl += kPushThreads) {
+        const uint32_t p = s_p[sl];
+        const uint64_t pos = s_base[p] + s_run[p] + (sl - s_off[p]);
+        const K key = s_x[sl];
+        if (pos < a.dst_cap) {
+          a.dst_idx[p][pos] = key;
+          a.dst_val[p][pos] = s_v[sl];
+        } else {
+          atomicOr(&h->status, kErrCapacity);
+        }
+        if (pos == lim)
+          atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)key + 1) << 16) | p);
+      }
+      __syncthreads();
+      if (threadIdx.x < n) s_run[threadIdx.x] += s_tot[threadIdx.x];
+    }
+  }
+}
+
+// Side path, the hash-memory placement of the dense data path: the lock-free
+// priority claim (zen_hash_dev.cuh place_keys) of every
+// staged key, read straight from the extraction staging -- the claims' outcome
+// does not depend on the order keys claim in, so no ascending key list is
+// built.  Persistent blocks take tile groups from a counter.
+template <typename K>
+__global__ void __launch_bounds__(kPushThreads) k_place_tiles(HashArgs<K> a) {
+  zen_dev::pdl_entry();
+  __shared__ uint32_t s_tpre[kPushTiles + 1];
+  __shared__ uint32_t s_group;
+  const PushCounts& x = a.xc;
+  HashHdr* h = a.hdr;
+  if (h->status & kErrCapacity) return;
+  const K* st = static_cast<const K*>(x.st_idx);
+  const uint32_t n = a.fam.n, warp = threadIdx.x >> 5;
+  const uint64_t r1 = h->r1, stride = h->stride;
+  const uint64_t ew = epoch_word(h->epoch);
+  const uint32_t ngroups = (x.ntiles + kPushTiles - 1) / kPushTiles;
+  constexpr int KPT = 4;
+  for (;;) {
+    if (threadIdx.x == 0) s_group = atomicAdd(&h->work[1], 1u);
     __syncthreads();
-    if (threadIdx.x < n) s_run[threadIdx.x] += s_tot[threadIdx.x];
+    const uint32_t g = s_group;
+    if (g >= ngroups) break;
+    const uint32_t t0 = g * kPushTiles;
+    if (warp == 0) group_prefix(x, n, t0, s_tpre);
+    __syncthreads();
+    const uint32_t T = s_tpre[kPushTiles];
+    for (uint32_t e0 = threadIdx.x; e0 < T; e0 += kPushThreads * KPT) {
+      uint64_t key[KPT];
+      uint32_t part[KPT], nv = 0;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const uint32_t e = e0 + j * kPushThreads;  // valid entries form a prefix in j
+        key[j] = e < T ? (uint64_t)st[group_src(s_tpre, t0, e)] + 1 : 0ull;
+        part[j] = e < T ? part_of(a.fam, key[j]) : 0u;
+        nv += e < T ? 1u : 0u;
+      }
+      place_keys<KPT>(a.fam, a.slots, key, part, nv, r1, stride, ew);
+    }
+    __syncthreads();  // s_tpre / s_group reuse
   }
 }
 
@@ -255,15 +387,37 @@ void launch_bp_begin(const HashArgs<K>& a, cudaStream_t stream) {
 
 template <typename K>
 void launch_push_scatter(const HashArgs<K>& a, const ExtractWs<K>& ws, cudaStream_t stream) {
-  launch_k(k_push_scatter<K>, (a.xc.ntiles + kPushTiles - 1) / kPushTiles, kPushThreads, 0, stream,
-           a, (const K*)ws.st_idx,
-           (const float*)ws.st_val);
+  launch_k(a.peer ? k_push_scatter<K, true> : k_push_scatter<K, false>, a.xc.scatter_grid,
+           kPushThreads, 0, stream, a, (const K*)ws.st_idx, (const float*)ws.st_val);
   count_launch();
+}
+
+template <typename K>
+void launch_place_tiles(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm) {
+  const unsigned groups = (a.xc.ntiles + kPushTiles - 1) / kPushTiles;
+  launch_k(k_place_tiles<K>, std::max(1u, std::min(groups, 148u * ctas_per_sm)), kPushThreads, 0,
+           stream, a);
+  count_launch();
+}
+
+// resident blocks of the persistent scatter (the whole grid in one wave)
+template <typename K>
+unsigned push_scatter_grid(bool peer, uint32_t ntiles) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, peer ? k_push_scatter<K, true> : k_push_scatter<K, false>, kPushThreads, 0);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned groups = (ntiles + kPushTiles - 1) / kPushTiles;
+  return std::max(1u, std::min(groups, (unsigned)(std::max(per_sm, 1) * sms)));
 }
 
 #define ZEN_INST(K)                                                                          \
   template void launch_bp_begin<K>(const HashArgs<K>&, cudaStream_t);                        \
-  template void launch_push_scatter<K>(const HashArgs<K>&, const ExtractWs<K>&, cudaStream_t);
+  template void launch_push_scatter<K>(const HashArgs<K>&, const ExtractWs<K>&, cudaStream_t); \
+  template void launch_place_tiles<K>(const HashArgs<K>&, cudaStream_t, unsigned);            \
+  template unsigned push_scatter_grid<K>(bool, uint32_t);
 ZEN_INST(uint32_t)
 #undef ZEN_INST
 

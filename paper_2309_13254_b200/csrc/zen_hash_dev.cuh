@@ -11,22 +11,48 @@ __device__ __forceinline__ uint64_t epoch_word(uint32_t epoch) {
   return (uint64_t)(0xFFFFFFu - (epoch & 0xFFFFFFu)) << zen::kKeyBits;
 }
 
+// Slot word codecs (zen::SlotOf<K>).  u64 (standalone hash, indices < 2^40):
+// [63:40] = 0xFFFFFF - epoch, [39:0] = index+1, so stale epochs lose every
+// atomicMin and the memory is never cleared.  u32 (the BP pipeline, M < 2^32
+// - 1): the word is index+1, 0xFFFFFFFF = vacant -- half the bytes, so the
+// hash memory stays L2-resident twice as long; the depth pass clears the
+// words it read, which keeps the memory vacant between syncs.
+template <typename W>
+struct Slot;
+template <>
+struct Slot<unsigned long long> {
+  static constexpr unsigned long long kVacant = ~0ull;
+  __device__ __forceinline__ static unsigned long long make(uint64_t ew, uint64_t key) { return ew | key; }
+  __device__ __forceinline__ static bool vacant(unsigned long long w, uint64_t ew) {
+    return w > (ew | zen::kKeyMask);  // empty or an older epoch
+  }
+  __device__ __forceinline__ static uint64_t key(unsigned long long w) { return w & zen::kKeyMask; }
+};
+template <>
+struct Slot<unsigned int> {
+  static constexpr unsigned int kVacant = 0xFFFFFFFFu;
+  __device__ __forceinline__ static unsigned int make(uint64_t, uint64_t key) { return (unsigned int)key; }
+  __device__ __forceinline__ static bool vacant(unsigned int w, uint64_t) { return w == kVacant; }
+  __device__ __forceinline__ static uint64_t key(unsigned int w) { return w; }
+};
+
 // Priority claim of one key (deferred acceptance, smallest key wins):
 // reproduces place_index's parallel-region layout of the lanes=1 run
 // (zen/hashing.hpp:155-163) for any thread schedule.
-__device__ __forceinline__ void place_key(const zen::DevFamily& fam, unsigned long long* slots,
-                                          uint64_t key, uint64_t r1, uint64_t stride,
-                                          uint64_t ew) {
+template <typename W>
+__device__ __forceinline__ void place_key(const zen::DevFamily& fam, W* slots, uint64_t key,
+                                          uint64_t r1, uint64_t stride, uint64_t ew) {
+  using S = Slot<W>;
   const uint32_t p = part_of(fam, key);
-  unsigned long long* base = slots + (uint64_t)p * stride;
+  W* base = slots + (uint64_t)p * stride;
   uint64_t cur = key;
   uint32_t t = 0;
   const uint32_t k = fam.k;
   while (true) {
     const uint64_t c = slot_of(fam, cur, t, r1);
-    const unsigned long long old = atomicMin(base + c, (unsigned long long)(ew | cur));
-    if (old > (ew | zen::kKeyMask)) break;  // empty or stale epoch: cur now holds c
-    const uint64_t ok = old & zen::kKeyMask;
+    const W old = atomicMin(base + c, S::make(ew, cur));
+    if (S::vacant(old, ew)) break;  // empty or stale epoch: cur now holds c
+    const uint64_t ok = S::key(old);
     if (ok > cur) {  // cur displaced a larger key: it resumes after its first c
       cur = ok;
       uint32_t f = 0;
@@ -43,12 +69,13 @@ __device__ __forceinline__ void place_key(const zen::DevFamily& fam, unsigned lo
 // pending atomicMin of each unfinished key before consuming any result, so a
 // thread keeps KPT L2 atomics in flight instead of one (same protocol and
 // outcome as place_key: the stable matching does not depend on the schedule).
-template <int KPT>
-__device__ __forceinline__ void place_keys(const zen::DevFamily& fam, unsigned long long* slots,
+template <int KPT, typename W>
+__device__ __forceinline__ void place_keys(const zen::DevFamily& fam, W* slots,
                                            const uint64_t (&key)[KPT], const uint32_t (&part)[KPT],
                                            uint32_t nvalid, uint64_t r1, uint64_t stride,
                                            uint64_t ew) {
-  unsigned long long* base[KPT];
+  using S = Slot<W>;
+  W* base[KPT];
   uint64_t cur[KPT];
   uint32_t t[KPT];
   bool act[KPT];
@@ -63,23 +90,23 @@ __device__ __forceinline__ void place_keys(const zen::DevFamily& fam, unsigned l
   bool any = nvalid > 0;
   while (any) {
     uint64_t c[KPT];
-    unsigned long long old[KPT];
+    W old[KPT];
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       if (act[j]) {
         c[j] = slot_of(fam, cur[j], t[j], r1);
-        old[j] = atomicMin(base[j] + c[j], (unsigned long long)(ew | cur[j]));
+        old[j] = atomicMin(base[j] + c[j], S::make(ew, cur[j]));
       }
     }
     any = false;
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       if (!act[j]) continue;
-      if (old[j] > (ew | zen::kKeyMask)) {  // empty or stale epoch: cur holds c
+      if (S::vacant(old[j], ew)) {  // empty or stale epoch: cur holds c
         act[j] = false;
         continue;
       }
-      const uint64_t ok = old[j] & zen::kKeyMask;
+      const uint64_t ok = S::key(old[j]);
       if (ok > cur[j]) {  // displaced a larger key: it resumes after its first c
         cur[j] = ok;
         uint32_t f = 0;

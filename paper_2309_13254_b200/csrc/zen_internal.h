@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace zen {
@@ -53,6 +54,7 @@ struct HashHdr {
   uint32_t fb_done;      // fallback blocks finished
   double r1_mult, r2_ratio;
   uint64_t bad_index;    // IndexOutsideUniverse witness (min), ~0 = none
+  uint32_t work[2];      // dynamic tile-group counters (push scatter, claims), reset per sync
 };
 
 constexpr uint32_t kErrTimeout = 1u, kErrOutside = 2u, kErrCapacity = 4u;
@@ -95,9 +97,10 @@ struct PushCounts {
   uint32_t* tcnt;   // [n][ntiles] plain stores (every tile, every sync)
   uint32_t* ccnt;   // [n][nchunk] atomics, zeroed by the per-sync begin kernel
   uint32_t* scnt;   // [n][nsup]   atomics, zeroed by the per-sync begin kernel
-  uint64_t* tbase;  // [ntiles] ascending position of each tile's first non-zero
   uint32_t ntiles, nchunk, nsup, n;
   uint64_t pc;      // G * (partition_seed + 1)
+  const void* st_idx;  // the extraction staging (K keys): the side path reads it in place
+  uint32_t scatter_grid, place_grid;  // persistent grids (resident blocks)
 };
 
 // ---- kernel launchers (implemented in k_*.cu) ------------------------------
@@ -137,13 +140,18 @@ void launch_extract_compact_part(uint64_t m, const ExtractWs<K>& ws, const HashA
 void launch_partition_of(const uint64_t* idx, uint64_t count, uint64_t pc, uint32_t n,
                          uint32_t* out, cudaStream_t stream);
 
+// hash-memory slot word per key width (zen_hash_dev.cuh Slot<>): u64 with an
+// epoch field for the standalone hash, u32 (vacant = ~0) for the BP pipeline
+template <typename K>
+using SlotOf = typename std::conditional<sizeof(K) == 4, unsigned int, unsigned long long>::type;
+
 template <typename K>
 struct HashArgs {
   const K* idx;
   const float* val;
   DevFamily fam;
   HashHdr* hdr;
-  unsigned long long* slots;  // n * stride_cap words
+  SlotOf<K>* slots;           // n * stride_cap words
   float* slot_vals;           // optional (layout dump)
   uint32_t* meta;             // [cap] side path: packed p | depth | serial rank (zen_hash_dev.cuh)
   uint32_t* pmeta;            // [cap] data path: p | (rank in tile among same-p keys) << 16
@@ -201,7 +209,7 @@ void launch_push_signal(const HashArgs<K>& a, cudaStream_t stream);
 // Dense BP data path (k_push.cu): per-sync begin (header + counter reset),
 // extraction tiles with the h0 counts (k_extract.cu), and the push scatter
 // straight from the extraction staging into the owners' inboxes (which also
-// writes the ascending key list and runs the priority claims).
+// writes the ascending key list the side path's placement reads).
 template <typename K>
 void launch_bp_begin(const HashArgs<K>& a, cudaStream_t stream);
 template <typename K>
@@ -209,10 +217,18 @@ void launch_extract_tiles_part(const float* dense, uint64_t m, const ExtractWs<K
                                const HashArgs<K>& a, cudaStream_t stream);
 template <typename K>
 void launch_push_scatter(const HashArgs<K>& a, const ExtractWs<K>& ws, cudaStream_t stream);
-// BP side path after the push scatter (which ran the claims): depth pass +
-// CollisionStats + fallback detection, then the (predicated) fallback replay
+// BP side path after the push scatter: the priority claims, the table-scan
+// depth pass (CollisionStats + fallback detection), then the (data-dependent)
+// fallback replay
 template <typename K>
-void launch_hash_side_bp(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm);
+void launch_hash_side_bp(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm,
+                         bool place);
+// the claims of a dense sync, straight from the extraction staging (k_push.cu)
+template <typename K>
+void launch_place_tiles(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm);
+// resident blocks of the persistent push scatter
+template <typename K>
+unsigned push_scatter_grid(bool peer, uint32_t ntiles);
 
 
 // universe tables (HashUniverseTable, zen/codec.hpp:47-72) as bit planes
@@ -260,6 +276,13 @@ struct AggArgs {
   HashHdr* hdr;                   // iteration / error bits / bad index
   int wait_push;                  // wait for in_hdr[w]->flag >= hdr->iter
   int peer;                       // destinations include other GPUs (system-scope release)
+  // BP pull: per 32-word chunk of the GLOBAL index space, the number of U_s
+  // bits before the chunk's first position in I_s -- the receivers' decode
+  // reads its value bases here instead of re-scanning every pulled bitmap
+  const uint32_t* cprefix;        // universe chunk prefixes [nchunks * n] (null: off)
+  uint64_t nchunks;               // ceil(M / 2048)
+  const unsigned long long* own_bits;  // this server's local copy of U (a dst_bits entry)
+  uint32_t* const* dst_cbase;     // [ndst] -> (nchunks + 1) u32 per receiver
 };
 void launch_aggregate(const AggArgs& a, cudaStream_t stream);
 
@@ -289,6 +312,8 @@ struct DecodeArgs {
   HashHdr* hdr;
   int wait_pull;
   uint32_t* popc_total;                    // [n] per-server popcount (malformed check)
+  const uint32_t* const* cbase;            // [n] pulled per-chunk value bases (BP), or null:
+                                           // the prefixes come from k_bpre
 };
 void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream);
 

@@ -52,11 +52,12 @@ def _dense_on_device(m, idx, val):
     return g
 
 
-def _check_full(zen, co, ro, m, pairs, seed=1, check_stats=True):
+def _check_full(zen, co, ro, m, pairs, seed=1, check_stats=True, r2_ratio=0.1):
     n = len(pairs)
     lanes = os.cpu_count() or 1
     zmax = max(i.size for i, _ in pairs)
-    bp = zen.BPSynchronizer(n, m, max_nnz=zmax + 4096, params=zen.HashParams(seed=seed))
+    bp = zen.BPSynchronizer(n, m, max_nnz=zmax + 4096,
+                            params=zen.HashParams(seed=seed, r2_ratio=r2_ratio))
     dense = [_dense_on_device(m, i, v) for i, v in pairs]
     side = torch.cuda.Stream()
     for it in range(2):  # eager capture, then CUDA-graph replay
@@ -72,7 +73,7 @@ def _check_full(zen, co, ro, m, pairs, seed=1, check_stats=True):
     del dense, oi, ov, bp
     torch.cuda.empty_cache()
 
-    want = ro.bp_sync(m, pairs, seed=seed, lanes=lanes)
+    want = ro.bp_sync(m, pairs, seed=seed, lanes=lanes, r2_ratio=r2_ratio)
     np.testing.assert_array_equal(got_i, want.idx)
     np.testing.assert_array_equal(got_v.view(np.uint32), want.val.view(np.uint32))
     np.testing.assert_array_equal(led, want.ledger)
@@ -86,7 +87,7 @@ def _check_full(zen, co, ro, m, pairs, seed=1, check_stats=True):
     assert int(agg.sum()) == want.idx.size
     if check_stats:
         for w, (i, v) in enumerate(pairs):
-            r1, r2 = co.bp_sizes(2.0, 0.1, i.size, n)
+            r1, r2 = co.bp_sizes(2.0, r2_ratio, i.size, n)
             ws = ro.hierarchical_hash(m, i, v, seed, n, 3, r1, r2, worker=w, lanes=lanes)
             assert stats[w].serial_writes == ws.serial_writes, f"worker {w}"
             assert stats[w].placed_at_depth == ws.placed_at_depth, f"worker {w}"
@@ -120,3 +121,14 @@ def test_c3_rows_n8(zen, co, ro):
         pytest.skip("C3 with 8 emulated workers needs ~110 GB of device memory")
     rows, d = 800_000, 1024
     _check_full(zen, co, ro, rows * d, _rows_inputs(rows, d, 0.01, 8, seed=3), seed=3)
+
+
+def test_c4_tight_r2_fallback_n8(zen, co, ro):
+    """r2 = 1 % of r1: every partition has more serial keys than serial slots,
+    so the reference's order-dependent fallback scan (zen/hashing.hpp:170-175)
+    places the rest -- the exact replay path -- at the headline size."""
+    import time
+    rows, d = 1_000_000, 64
+    t = time.time()
+    _check_full(zen, co, ro, rows * d, _rows_inputs(rows, d, 0.01, 8), r2_ratio=0.01)
+    print(f"tight-r2 sync + reference check: {time.time() - t:.1f} s")

@@ -125,8 +125,8 @@ def test_priority_claim_is_schedule_invariant(zen, co):
     fam = zen.HashFamily.make(9, n, k)
     r1, r2 = 6_000, 600  # tight: many displacements, serial keys and a fallback-free run
     want = co.hierarchical_hash(m, idx, val, co.family(9, n, k), r1, r2, layout=True)
-    schedules = [(0, 0, 0, 0), (1, 32, 0, 0), (3, 64, 7919, 13), (148, 1024, 0, 0),
-                 (37, 96, 104729, 5), (2000, 256, 1_000_003, 17), (5, 512, z - 1, 0)]
+    schedules = [(0, 0, 0, 0), (1, 32, 0, 0), (3, 64, 7919, 13), (148, 256, 0, 0),
+                 (37, 96, 104729, 5), (2000, 256, 1_000_003, 17), (5, 160, z - 1, 0)]
     try:
         for g, t, mul, add in schedules:
             assert lib.zen_debug_hash_schedule(g, t, mul, add) == 0

@@ -1,5 +1,6 @@
-mkdir -p gpurun_out/r06e
-python tools/timeline.py --syncs 2 --out gpurun_out/r06e/tl_1pct.txt > /dev/null 2>&1
-ZEN_DIAG_NOCLAIM=1 python tools/timeline.py --syncs 2 --out gpurun_out/r06e/tl_1pct_noclaim.txt > /dev/null 2>&1
-ZEN_DIAG_NOCLAIM=1 python tools/timeline.py --syncs 2 --density 0.1 --out gpurun_out/r06e/tl_10pct_noclaim.txt > /dev/null 2>&1
-python tools/timeline.py --syncs 1 > gpurun_out/r06e/plain.log 2>&1 && ncu --set full --cache-control none --clock-control none --import-source on -k regex:"k_push_scatter|k_depth_bp|k_agg_mark|k_decode" -s 8 -c 4 -o gpurun_out/r06e/prof python tools/timeline.py --syncs 1 > gpurun_out/r06e/ncu.log 2>&1
+# r06 diagnosis: GPU suite + warm timelines (CUPTI) at 1 % and 10 % + a short bench
+mkdir -p gpurun_out/$1
+timeout 1200 python -m pytest tests -m gpu -x -q --durations=8 > gpurun_out/$1/pytest.log 2>&1; echo rc=$? >> gpurun_out/$1/pytest.log
+python tools/timeline.py --syncs 2 --out gpurun_out/$1/tl_1pct.txt > /dev/null 2>&1
+python tools/timeline.py --syncs 2 --density 0.1 --out gpurun_out/$1/tl_10pct.txt > /dev/null 2>&1
+timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu --no-extras > gpurun_out/$1/bench.json 2> gpurun_out/$1/bench.err
