@@ -33,13 +33,14 @@ $(COMPAT_TEST): tests/cpp/compat_test.cpp include/zen_b200/compat.hpp include/ze
 # installed).  Built only where the reference exists (this container); the
 # binaries travel to the GPU box in build/ and run there (tests/test_gpu_parity.py).
 REF_TESTS ?= /root/reference/proj/tests
-REF_SUITES := hashing
+REF_SUITES := hashing tensor simnet
+JSON_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
 REF_BINS := $(patsubst %,build/ref_%_test,$(REF_SUITES))
 ref_tests: $(if $(wildcard $(REF_TESTS)),$(REF_BINS),)
 build/ref_%_test: $(REF_TESTS)/%_test.cpp include/zen_b200/compat.hpp include/zen_b200.h \
                   tests/cpp/gtest_shim/gtest/gtest.h $(LIB)
 	@mkdir -p build
-	g++ -O2 -std=c++20 -w -Itests/cpp/gtest_shim -Itests/cpp/zen_shim -Iinclude \
+	g++ -O2 -std=c++20 -w -Itests/cpp/gtest_shim -Itests/cpp/zen_shim -Iinclude -I$(JSON_DIR) \
 	    -I$(CUDA_HOME)/include -o $@ $< -L$(dir $(LIB)) -lzen_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))' -L$(CUDA_HOME)/lib64 -lcudart
 

@@ -757,6 +757,22 @@ struct SparsityProfile {  // tensor.hpp:216-240
   double d = 0.0;
   std::map<uint64_t, double> gamma;
   std::map<uint32_t, double> skew;
+  // the profile's invariants (tensor.hpp:221-238): d in (0,1], gamma[1] = 1,
+  // gamma non-decreasing with gamma[k] <= k and d*gamma[k] <= 1, skew >= 1
+  void validate() const {
+    if (!(d > 0.0 && d <= 1.0)) throw Error("profile density must be in (0,1]");
+    auto one = gamma.find(1);
+    if (one == gamma.end() || one->second != 1.0) throw Error("profile gamma[1] must equal 1");
+    double last = 0.0;
+    for (const auto& kv : gamma) {
+      if (kv.second < last - 1e-9) throw Error("profile gamma must be non-decreasing in k");
+      if (kv.second > double(kv.first) + 1e-9) throw Error("profile gamma[k] must not exceed k");
+      if (d * kv.second > 1.0 + 1e-9) throw Error("profile d*gamma[k] must not exceed 1");
+      last = kv.second;
+    }
+    for (const auto& kv : skew)
+      if (kv.second < 1.0 - 1e-9) throw Error("profile skewness must be at least 1");
+  }
 };
 
 // (n-1)/n * (gamma_n + 1), costmodel.hpp:53-58
@@ -848,7 +864,37 @@ struct TrafficReport {
   std::vector<StageRecord> stages;
   uint64_t total_sent_bits = 0, total_recv_bits = 0, total_index_bits = 0, total_value_bits = 0;
   double simulated_time = 0.0;
+#ifdef NLOHMANN_JSON_VERSION_MAJOR
+  // the reference's report document (simnet.hpp:37-55), when nlohmann/json is
+  // included before this header (as the reference's own headers do)
+  nlohmann::json to_json() const {
+    nlohmann::json j;
+    j["n"] = nodes;
+    j["b"] = bandwidth;
+    j["stages"] = nlohmann::json::array();
+    for (const auto& st : stages)
+      j["stages"].push_back({{"time", st.stage_time}, {"sent_bits", st.sent_bits},
+                             {"recv_bits", st.recv_bits}, {"recv_index_bits", st.recv_index_bits},
+                             {"recv_value_bits", st.recv_value_bits}});
+    j["totals"] = {{"sent_bits", total_sent_bits}, {"recv_bits", total_recv_bits},
+                   {"index_bits", total_index_bits}, {"value_bits", total_value_bits}};
+    j["simulated_time"] = simulated_time;
+    return j;
+  }
+#endif
 };
+
+// value-payload time in COO-equivalent fp32 element units (simnet.hpp:125-134):
+// per stage the largest received value payload, two elements per value
+inline double value_payload_time_coo_equivalent(const TrafficReport& r) {
+  double elems = 0.0;
+  for (const auto& st : r.stages) {
+    uint64_t mx = 0;
+    for (uint64_t v : st.recv_value_bits) mx = std::max(mx, v);
+    elems += double(mx) / 32.0 * 2.0;
+  }
+  return elems / (r.bandwidth / 32.0);
+}
 
 // The reference's accounting network.  On B200 the bytes really move over
 // NVLink; this keeps the deterministic bit ledger (stage time = max recv / b).

@@ -11,7 +11,8 @@ from .zen import (  # noqa: F401
     HashUniverseTable, IndexOutsideUniverse, MalformedPayload, PartitionedSparseTensor,
     PeerTimeout, SerialOverflow, SimNet, SparseTensor, SyncOutcome, TrafficReport,
     UniverseMismatch, WireFormat, aggregate, bp_universe_table, collision_stats, context, decode,
-    derive_seed, encode, hash_memory_layout, hierarchical_hash, imbalance_pull, imbalance_push,
+    derive_seed, encode, exchange_ipc_handles, hash_memory_layout, hierarchical_hash,
+    imbalance_pull, imbalance_push,
     message_sizes, partition_of, read_framed, read_sparse, read_sparse_file,
     run_balanced_parallelism, run_bp_with_retry, sparsify_topk, to_sparse, write_framed,
     write_sparse,
@@ -24,3 +25,4 @@ from .schemes import (  # noqa: F401
     CommPattern, PartitionPattern, SchemeConfig, UnsupportedCombination, run_agsparse,
     run_omnireduce_like, run_ring_centralization, run_scheme, scheme_config_from_name, t_bp, t_bp_coefficient, t_hc, t_hc_coefficient,
     t_hierarchy_incremental_lb, t_ring_incremental, t_sparse_ps, t_sparse_ps_broadcast)
+from .buckets import Bucket, MixedBucketSync, allreduce_dense_time_bits  # noqa: F401,E402

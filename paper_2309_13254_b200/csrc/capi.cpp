@@ -1535,7 +1535,7 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   CKR(mem.alloc(&x.ccnt, size_t(n) * (x.nchunk + x.nsup)));
   x.scnt = x.ccnt + size_t(n) * x.nchunk;
   x.st_idx = w.ex.st_idx;
-  x.scatter_grid = push_scatter_grid<uint32_t>(!bp->local, x.ntiles);
+  x.scatter_grid = push_scatter_grid<uint32_t>(!bp->local && n > 4, x.ntiles);  // push_reorder
   zen_hash_family f;
   CKR(zen_hash_family_make_worker(bp->params.seed, w.id, n, k, &f));
   a.fam = fold(f);
@@ -1914,9 +1914,8 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     // inboxes; the hash-memory side path of each worker forks onto bp->side
     // and joins at the end of the sync
     for (auto& w : bp->workers) {
-      launch_push_scatter<uint32_t>(w.a, w.ex, st);
+      launch_push_scatter<uint32_t>(w.a, w.ex, st);  // + the push signal (rank mode)
       CKR(fork_side(w, true));
-      if (w.a.push_hdr) launch_push_signal<uint32_t>(w.a, st);
     }
   } else {
     if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));

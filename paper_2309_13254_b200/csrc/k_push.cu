@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) k_bp_begin(HashArgs<K> a) {
       h->bad_index = ~0ull;
       h->work[0] = 0;
       h->work[1] = 0;
+      h->work[2] = 0;
     }
     for (uint32_t i = threadIdx.x; i < n * (k + 1); i += blockDim.x) {
       a.stats[i] = 0;
@@ -149,10 +150,9 @@ __global__ void __launch_bounds__(kPushThreads)
     h->ntiles = (uint32_t)((z + kHashTile - 1) / kHashTile);
     if (bad) atomicOr(&h->status, kErrCapacity);
   }
-  if (bad) return;
   const uint64_t lim = r1 + r2;
   const uint32_t ngroups = (x.ntiles + kPushTiles - 1) / kPushTiles;
-  for (;;) {
+  for (; !bad;) {
     if (threadIdx.x == 0) s_group = atomicAdd(&h->work[0], 1u);
     if (warp == 0 && lane < n) s_run[lane] = 0;
     __syncthreads();
@@ -329,6 +329,36 @@ __global__ void __launch_bounds__(kPushThreads)
       if (threadIdx.x < n) s_run[threadIdx.x] += s_tot[threadIdx.x];
     }
   }
+  // rank mode: the push signal (k_hash.cu k_push_signal) from the last block
+  // to finish -- every block fences its NVLink stores (system scope) before it
+  // counts itself done, so the count row and the release of the flag follow
+  // every part store of this worker
+  if (a.push_hdr) {
+    __shared__ uint32_t s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_for(a.peer);
+      s_last = (atomicAdd(&h->work[2], 1u) == gridDim.x - 1) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (s_last) {
+      fence_for(a.peer);
+      const bool cap_ok = !(*(volatile uint32_t*)&h->status & kErrCapacity);
+      const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
+      const uint32_t st = *(volatile uint32_t*)&h->status;
+      for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
+        PushHdr* ph = a.push_hdr[s];
+        ph->nnz = z;
+        ph->ovf_word = ovf;
+        ph->status = st;
+        for (uint32_t q = 0; q < n; ++q) ph->counts[q] = cap_ok ? a.load[q] : 0u;
+      }
+      __syncthreads();
+      fence_for(a.peer);
+      for (uint32_t s = threadIdx.x; s < n; s += blockDim.x)
+        st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
+    }
+  }
 }
 
 // Side path, the hash-memory placement of the dense data path: the lock-free
@@ -385,9 +415,14 @@ void launch_bp_begin(const HashArgs<K>& a, cudaStream_t stream) {
   count_launch();
 }
 
+// peer destinations at n > 4: a warp's entries scatter over many parts, so
+// regroup them into full-line NVLink stores; otherwise store in place
+inline bool push_reorder(bool peer, uint32_t n) { return peer && n > 4; }
+
 template <typename K>
 void launch_push_scatter(const HashArgs<K>& a, const ExtractWs<K>& ws, cudaStream_t stream) {
-  launch_k(a.peer ? k_push_scatter<K, true> : k_push_scatter<K, false>, a.xc.scatter_grid,
+  launch_k(push_reorder(a.peer, a.fam.n) ? k_push_scatter<K, true> : k_push_scatter<K, false>,
+           a.xc.scatter_grid,
            kPushThreads, 0, stream, a, (const K*)ws.st_idx, (const float*)ws.st_val);
   count_launch();
 }
@@ -406,6 +441,7 @@ unsigned push_scatter_grid(bool peer, uint32_t ntiles) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &per_sm, peer ? k_push_scatter<K, true> : k_push_scatter<K, false>, kPushThreads, 0);
+  // (the REORDER variant needs more shared memory: its occupancy bounds both)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -54,7 +54,7 @@ struct HashHdr {
   uint32_t fb_done;      // fallback blocks finished
   double r1_mult, r2_ratio;
   uint64_t bad_index;    // IndexOutsideUniverse witness (min), ~0 = none
-  uint32_t work[2];      // dynamic tile-group counters (push scatter, claims), reset per sync
+  uint32_t work[3];      // push-scatter groups, claim groups, push-scatter blocks done (per sync)
 };
 
 constexpr uint32_t kErrTimeout = 1u, kErrOutside = 2u, kErrCapacity = 4u;

@@ -839,6 +839,21 @@ class SyncOutcome:
     balance: BalanceDetails | None = None
 
 
+def exchange_ipc_handles(handle: bytes, n: int, group=None) -> list:
+    """All-gather one receive-arena handle per rank over torch.distributed
+    (gloo or NCCL: plumbing only, the data path never uses it), rank-major,
+    checked against the job size the synchroniser was created with."""
+    import torch.distributed as dist
+    if len(handle) != L.ZEN_IPC_HANDLE_BYTES:
+        raise Error(f"IPC handle must be {L.ZEN_IPC_HANDLE_BYTES} bytes, got {len(handle)}")
+    world = dist.get_world_size(group)
+    if world != n:
+        raise Error(f"process group has {world} ranks, the synchroniser {n} workers")
+    handles = [None] * n
+    dist.all_gather_object(handles, bytes(handle), group=group)
+    return handles
+
+
 class BPSynchronizer:
     """A device-resident BP synchroniser (zen_bp).  rank=None hosts all n
     workers on this GPU (exchange = local stores); rank=r is worker+server r of
@@ -881,10 +896,7 @@ class BPSynchronizer:
 
     def connect_process_group(self, group=None):
         """Exchange CUDA IPC handles over torch.distributed (plumbing only)."""
-        import torch.distributed as dist
-        handles = [None] * self.n
-        dist.all_gather_object(handles, self.ipc_handle(), group=group)
-        self.connect(handles)
+        self.connect(exchange_ipc_handles(self.ipc_handle(), self.n, group))
 
     # -- synchronisation ------------------------------------------------------
     def sync_dense(self, dense):

@@ -211,6 +211,34 @@ def main():
                       flush=True)
                 ok = False
             del sy
+    # mixed buckets (f2): the embedding through BP, a dense layer top-k'd on
+    # the device then BP, the rest all-reduced over NCCL, one MixedBucketSync
+    if world <= ngpu:
+        lay_all = [np.random.default_rng(900 + r).standard_normal(50_000).astype(np.float32)
+                   for r in range(world)]
+        den_all = [np.random.default_rng(700 + r).integers(-8, 9, 20_000).astype(np.float32)
+                   for r in range(world)]
+        g = [mine, torch.from_numpy(lay_all[rank]).cuda(), torch.from_numpy(den_all[rank]).cuda()]
+        mb = zen.MixedBucketSync([("sparse", m), ("topk", 50_000, 0.02), ("dense", 20_000)],
+                                 n=world, rank=rank)
+        mb.step(g)
+        i0, v0 = mb.result(0)
+        if not (np.array_equal(i0.cpu().numpy().view(np.uint64), want.idx) and
+                np.array_equal(v0.cpu().numpy().view(np.uint32), want.val.view(np.uint32))):
+            print(f"RANK {rank} mixed sparse bucket MISMATCH", flush=True)
+            ok = False
+        tk = [co.sparsify_topk(x, 0.02) for x in lay_all]
+        wt = co.bp_sync(50_000, tk)
+        i1, v1 = mb.result(1)
+        if not (np.array_equal(i1.cpu().numpy().view(np.uint64), wt.idx) and
+                np.array_equal(v1.cpu().numpy().view(np.uint32), wt.val.view(np.uint32))):
+            print(f"RANK {rank} mixed top-k bucket MISMATCH", flush=True)
+            ok = False
+        torch.cuda.synchronize()
+        if not np.array_equal(g[2].cpu().numpy(), np.sum(den_all, axis=0)):  # integers: exact
+            print(f"RANK {rank} mixed dense bucket MISMATCH", flush=True)
+            ok = False
+        del mb
     flag = torch.tensor([0 if ok else 1], device="cuda" if world <= ngpu else "cpu")
     dist.all_reduce(flag)
     if rank == 0:

@@ -463,7 +463,7 @@ def test_cpp_compat_dropin(zen):
     assert r.returncode == 0, r.stdout[-4000:]
 
 
-@pytest.mark.parametrize("suite", ["hashing"])
+@pytest.mark.parametrize("suite", ["hashing", "tensor", "simnet"])
 def test_reference_unit_suite_unmodified(zen, suite):
     """The reference's OWN GTest suite (proj/tests/<suite>_test.cpp), compiled
     unmodified against the drop-in by `make ref_tests` (zen/*.hpp -> compat.hpp

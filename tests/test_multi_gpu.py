@@ -15,32 +15,63 @@ import pytest
 from conftest import ROOT
 
 
-def _gloo_exchange(rank, world, port, q):
+def _gloo_rank(rank, world, port, q):
+    """One rank of the CPU (gloo) job: the library's own handle exchange
+    (zen.exchange_ipc_handles, what BPSynchronizer.connect_process_group
+    runs) and the C-ABI's rank-plumbing argument checks, which need no GPU."""
+    import ctypes as C
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    handle = bytes([rank]) * 64  # stands in for a cudaIpcMemHandle_t
-    handles = [None] * world
-    dist.all_gather_object(handles, handle)
-    blob = b"".join(handles)
-    q.put((rank, len(blob), blob[::64]))
+    import paper_2309_13254_b200 as zen
+    from paper_2309_13254_b200 import _lib as L
+    lib = L.load()
+    out = {}
+    handle = bytes([rank + 1]) * L.ZEN_IPC_HANDLE_BYTES  # stands in for a cudaIpcMemHandle_t
+    hs = zen.exchange_ipc_handles(handle, world)
+    out["order"] = [h[0] for h in hs]
+    out["sizes"] = [len(h) for h in hs]
+    try:  # a job-size mismatch is refused before any exchange
+        zen.exchange_ipc_handles(handle, world + 1)
+        out["mismatch"] = "accepted"
+    except zen.Error:
+        out["mismatch"] = "refused"
+    try:
+        zen.exchange_ipc_handles(handle[:-1], world)
+        out["short"] = "accepted"
+    except zen.Error:
+        out["short"] = "refused"
+    blob = b"".join(hs)
+    buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+    out["connect_null"] = lib.zen_bp_connect(None, buf)
+    out["handle_null"] = lib.zen_bp_ipc_handle(None, buf)
+    out["hc_connect_null"] = lib.zen_hc_connect(None, buf)
+    q.put((rank, out))
+    dist.barrier()
     dist.destroy_process_group()
 
 
-def test_ipc_handle_exchange_gloo_world2():
+def test_rank_plumbing_gloo_world2():
     import multiprocessing as mp
+    from paper_2309_13254_b200 import _lib as L
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29500 + os.getpid() % 1000
-    ps = [ctx.Process(target=_gloo_exchange, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_gloo_rank, args=(r, 2, port, q)) for r in range(2)]
     for p in ps:
         p.start()
-    out = sorted(q.get(timeout=120) for _ in ps)
+    out = dict(q.get(timeout=180) for _ in ps)
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # every rank sees the handles rank-major, n * ZEN_IPC_HANDLE_BYTES bytes
-    assert out == [(0, 128, bytes([0, 1])), (1, 128, bytes([0, 1]))]
+    for r in range(2):
+        o = out[r]
+        assert o["order"] == [1, 2]  # rank-major on every rank
+        assert o["sizes"] == [L.ZEN_IPC_HANDLE_BYTES] * 2
+        assert o["mismatch"] == "refused" and o["short"] == "refused"
+        assert o["connect_null"] == L.E_INVALID
+        assert o["handle_null"] == L.E_INVALID
+        assert o["hc_connect_null"] == L.E_INVALID
 
 
 def _ngpus():
