@@ -33,16 +33,23 @@ $(COMPAT_TEST): tests/cpp/compat_test.cpp include/zen_b200/compat.hpp include/ze
 # installed).  Built only where the reference exists (this container); the
 # binaries travel to the GPU box in build/ and run there (tests/test_gpu_parity.py).
 REF_TESTS ?= /root/reference/proj/tests
-REF_SUITES := hashing tensor simnet
+REF_SUITES := hashing tensor codec simnet workload costmodel schemes
 JSON_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
-REF_BINS := $(patsubst %,build/ref_%_test,$(REF_SUITES))
+REF_DATA := /root/repo/tests/golden/ref_data
+REF_BINS := $(patsubst %,build/ref_%_test,$(REF_SUITES)) build/ref_acceptance
+REF_CXX = g++ -O2 -std=c++20 -w -Itests/cpp/gtest_shim -Itests/cpp/zen_shim -Iinclude -I$(JSON_DIR) \
+	    -I$(CUDA_HOME)/include -DZEN_TEST_DATA='"$(REF_DATA)"'
+REF_LD = -L$(dir $(LIB)) -lzen_b200 -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))' -L$(CUDA_HOME)/lib64 \
+	    -lcudart -lpthread
+REF_DEPS := include/zen_b200/compat.hpp include/zen_b200.h tests/cpp/gtest_shim/gtest/gtest.h $(LIB)
 ref_tests: $(if $(wildcard $(REF_TESTS)),$(REF_BINS),)
-build/ref_%_test: $(REF_TESTS)/%_test.cpp include/zen_b200/compat.hpp include/zen_b200.h \
-                  tests/cpp/gtest_shim/gtest/gtest.h $(LIB)
+build/ref_%_test: $(REF_TESTS)/%_test.cpp $(REF_DEPS)
 	@mkdir -p build
-	g++ -O2 -std=c++20 -w -Itests/cpp/gtest_shim -Itests/cpp/zen_shim -Iinclude -I$(JSON_DIR) \
-	    -I$(CUDA_HOME)/include -o $@ $< -L$(dir $(LIB)) -lzen_b200 \
-	    -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))' -L$(CUDA_HOME)/lib64 -lcudart
+	$(REF_CXX) -o $@ $< $(REF_LD)
+# the acceptance driver (one pass/fail line per criterion; `ref_acceptance 2` runs C2)
+build/ref_acceptance: $(REF_TESTS)/acceptance.cpp $(REF_DEPS)
+	@mkdir -p build
+	$(REF_CXX) -o $@ $< $(REF_LD)
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)

@@ -53,7 +53,8 @@ typedef enum zen_status {
   ZEN_E_PEER = 8,                 /* CUDA IPC / NVLink peer setup */
   ZEN_E_OOM = 9,
   ZEN_E_TIMEOUT = 10,             /* a peer never signalled (device-side watchdog) */
-  ZEN_E_CAPACITY = 11             /* nnz above the capacity the context was sized for */
+  ZEN_E_CAPACITY = 11,            /* nnz above the capacity the context was sized for */
+  ZEN_E_INFEASIBLE = 12           /* zen::InfeasibleSpec (workload generator) */
 } zen_status;
 
 /* zen::HashParams, zen/schemes.hpp:55-61 (lanes is accepted and ignored: the
@@ -286,6 +287,28 @@ zen_status zen_hc_copy_result(zen_hc* hc, uint64_t* d_idx, float* d_val, uint64_
 /* entries this rank sent per push, in plan order (HC / ring: one per stage;
  * AGsparse: one per peer) -- the SimNet ledger's sent side */
 zen_status zen_hc_stage_counts(zen_hc* hc, uint64_t* counts);
+
+/* ---- workload generator (zen::generate, zen/workload.hpp:22-154) ------- */
+/* zen::WorkloadSpec */
+typedef struct zen_workload_spec {
+  uint64_t universe;   /* M */
+  uint32_t nodes;      /* n */
+  double density;      /* d, per node */
+  double omega;        /* target pairwise overlap: shared core of ceil(omega*d*M) */
+  double hot_fraction; /* hot tier = the first llround(hot_fraction*M) indices */
+  double hot_mass;     /* share of the draws that land in the hot tier */
+  uint64_t seed;
+} zen_workload_spec;
+/* Node `node`'s tensor of zen::generate on the device: ceil(d*M) distinct
+ * ascending indices (the shared core + draws from the two-tier distribution
+ * without replacement), integer values in [1, 16].  Same spec as the
+ * reference, drawn from counter-based hashes (not libstdc++'s mt19937_64
+ * streams), so the same seed gives the same tensors on every call and rank.
+ * ZEN_E_INFEASIBLE where WorkloadSpec::validate throws InfeasibleSpec
+ * (workload.hpp:34-50); ZEN_E_CAPACITY (with *count = the size) when
+ * capacity < ceil(d*M).  Synchronous. */
+zen_status zen_generate(zen_ctx* ctx, const zen_workload_spec* spec, uint32_t node,
+                        uint64_t* d_idx, float* d_val, uint64_t capacity, uint64_t* count);
 
 /* ---- apply: the step after the sync ------------------------------------ */
 /* d_dense[idx[i]] += alpha * val[i] for a sorted unique sparse tensor (an SGD

@@ -40,6 +40,8 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <fstream>
@@ -119,6 +121,11 @@ class MissingProfileEntry : public Error {  // errors.hpp:54-57
   explicit MissingProfileEntry(const std::string& what) : Error(what) {}
 };
 
+class InfeasibleSpec : public Error {  // errors.hpp:81-84
+ public:
+  explicit InfeasibleSpec(const std::string& what) : Error(what) {}
+};
+
 class DeviceError : public Error {  // no CPU fallback exists
  public:
   explicit DeviceError(const std::string& w) : Error(w) {}
@@ -142,6 +149,7 @@ inline void check(zen_status s) {
     case ZEN_E_MALFORMED: throw MalformedPayload(msg);
     case ZEN_E_EMPTY: throw EmptyTensor(msg);
     case ZEN_E_UNIVERSE_MISMATCH: throw UniverseMismatch(msg);
+    case ZEN_E_INFEASIBLE: throw InfeasibleSpec(msg);
     case ZEN_E_CUDA:
     case ZEN_E_PEER:
     case ZEN_E_OOM:
@@ -173,8 +181,11 @@ struct DBuf {
 };
 
 // one context per process (device 0 unless ZEN_B200_DEVICE says otherwise)
+// One context per host thread: the reference's operators are pure functions
+// that callers run from many threads at once (acceptance.cpp's parallel_for),
+// and a context's scratch and stream serve one caller at a time.
 inline zen_ctx* ctx() {
-  static std::unique_ptr<zen_ctx, void (*)(zen_ctx*)> c = [] {
+  thread_local std::unique_ptr<zen_ctx, void (*)(zen_ctx*)> c = [] {
     int dev = 0;
     if (const char* e = std::getenv("ZEN_B200_DEVICE")) dev = std::atoi(e);
     cudaSetDevice(dev);
@@ -262,6 +273,20 @@ inline SparseTensor to_sparse(const DenseTensor& dense) {
   uint64_t nnz = 0;
   detail::check(zen_to_sparse(detail::ctx(), d.p, m, oi.p, ov.p, m, &nnz));
   return SparseTensor(m, oi.host(nnz), ov.host(nnz));
+}
+
+// zen::sparsify_topk (workload.hpp:157-178) on the device: the ceil(f*M)
+// largest |v| (ties to the lower index), exact zeros dropped
+inline SparseTensor sparsify_topk(const DenseTensor& dense, double fraction) {
+  if (!(fraction > 0.0 && fraction <= 1.0)) throw Error("top-k fraction must be in (0,1]");
+  const uint64_t m = dense.size();
+  const uint64_t keep = std::min<uint64_t>(m, uint64_t(std::ceil(fraction * double(m))));
+  detail::DBuf<float> d(dense.values);
+  detail::DBuf<uint64_t> oi(std::max<uint64_t>(keep, 1));
+  detail::DBuf<float> ov(std::max<uint64_t>(keep, 1));
+  uint64_t got = 0;
+  detail::check(zen_sparsify_topk(detail::ctx(), d.p, m, fraction, oi.p, ov.p, keep, &got));
+  return SparseTensor(m, oi.host(got), ov.host(got));
 }
 
 // ---- hashing: zen/hashing.hpp -----------------------------------------------
@@ -459,10 +484,29 @@ struct EncodedMessage {
 };
 
 class HashUniverseTable;
+// Reads like the reference's `std::vector<uint64_t> indices` member
+// (codec.hpp:38-42): the server's sorted universe, materialised from the
+// device tables on first use (they never build the M x 8 B lists).
+struct HashUniverseIndices {
+  const HashUniverseTable* table = nullptr;
+  uint32_t server = 0;
+  mutable std::shared_ptr<std::vector<uint64_t>> cache{};
+  const std::vector<uint64_t>& get() const;
+  operator const std::vector<uint64_t>&() const { return get(); }
+  size_t size() const { return get().size(); }
+  bool empty() const { return get().empty(); }
+  uint64_t operator[](size_t i) const { return get()[i]; }
+  uint64_t front() const { return get().front(); }
+  uint64_t back() const { return get().back(); }
+  std::vector<uint64_t>::const_iterator begin() const { return get().begin(); }
+  std::vector<uint64_t>::const_iterator end() const { return get().end(); }
+};
+
 struct HashUniverse {
   uint32_t server_id = 0;
   uint64_t universe_size = 0;
   const HashUniverseTable* table = nullptr;
+  HashUniverseIndices indices{};
   std::vector<uint64_t> indices_copy() const;
 };
 
@@ -474,7 +518,8 @@ class HashUniverseTable {
     zen_universe* u = nullptr;
     detail::check(zen_universe_create(detail::ctx(), m_, n_, pseed_, &u));
     u_.reset(u);
-    for (uint32_t s = 0; s < n_; ++s) us_.push_back(HashUniverse{s, m_, this});
+    for (uint32_t s = 0; s < n_; ++s)
+      us_.push_back(HashUniverse{s, m_, this, HashUniverseIndices{this, s}});
   }
   uint64_t universe_size() const { return m_; }
   uint32_t servers() const { return n_; }
@@ -493,6 +538,11 @@ class HashUniverseTable {
   std::unique_ptr<zen_universe, Del> u_;
   std::vector<HashUniverse> us_;
 };
+
+inline const std::vector<uint64_t>& HashUniverseIndices::get() const {
+  if (!cache) cache = std::make_shared<std::vector<uint64_t>>(table->universe(server).indices_copy());
+  return *cache;
+}
 
 inline std::vector<uint64_t> HashUniverse::indices_copy() const {
   const uint64_t sz = table->size(server_id);
@@ -752,6 +802,85 @@ inline double skewness_ratio(const SparseTensor& t, uint32_t partitions) {  // :
                                   t.universe(), partitions, t.nnz());
 }
 
+// ---- synthetic workloads: zen/workload.hpp ----------------------------------
+struct WorkloadSpec {  // workload.hpp:22-51
+  uint64_t universe = 0;
+  uint32_t nodes = 1;
+  double density = 0.0;
+  double omega = 0.0;
+  double hot_fraction = 0.125;
+  double hot_mass = 0.125;
+  uint64_t seed = 0;
+  uint64_t nnz_per_node() const { return uint64_t(std::ceil(density * double(universe))); }
+  zen_workload_spec c() const {
+    return zen_workload_spec{universe, nodes, density, omega, hot_fraction, hot_mass, seed};
+  }
+  void validate() const {  // the device generator applies the same checks
+    if (universe < 1) throw InfeasibleSpec("universe must be at least 1");
+    if (nodes < 1) throw InfeasibleSpec("node count must be at least 1");
+    if (!(density > 0.0 && density <= 1.0)) throw InfeasibleSpec("density must be in (0,1]");
+    if (density * double(universe) < 1.0) throw InfeasibleSpec("density*universe must be at least 1");
+    if (omega < 0.0 || omega > 1.0) throw InfeasibleSpec("omega must be in [0,1]");
+    if (!(hot_fraction > 0.0 && hot_fraction <= 1.0)) throw InfeasibleSpec("hot_fraction must be in (0,1]");
+    if (hot_mass < 0.0 || hot_mass > 1.0) throw InfeasibleSpec("hot_mass must be in [0,1]");
+    if (density * double(universe) * (1.0 + double(nodes) * (1.0 - omega)) > double(universe))
+      throw InfeasibleSpec("cannot fit disjoint remainders: d*M*(1+n*(1-omega)) > M");
+  }
+};
+
+// zen::generate (workload.hpp:119-154) drawn on the device (zen_generate):
+// the shared core + two-tier draws without replacement, integer values.
+// Same spec as the reference, not the same bits (counter-based hashes instead
+// of std::mt19937_64); deterministic for a seed.
+inline std::vector<SparseTensor> generate(const WorkloadSpec& spec) {
+  spec.validate();
+  const uint64_t z = spec.nnz_per_node();
+  detail::DBuf<uint64_t> di(std::max<uint64_t>(z, 1));
+  detail::DBuf<float> dv(std::max<uint64_t>(z, 1));
+  const zen_workload_spec c = spec.c();
+  std::vector<SparseTensor> out;
+  for (uint32_t node = 0; node < spec.nodes; ++node) {
+    uint64_t got = 0;
+    detail::check(zen_generate(detail::ctx(), &c, node, di.p, dv.p, z, &got));
+    out.push_back(SparseTensor(spec.universe, di.host(got), dv.host(got)));
+  }
+  return out;
+}
+
+struct WorkloadMeasurement {  // workload.hpp:180-184
+  double mean_pairwise_overlap = 0.0;
+  std::map<uint64_t, double> gamma;
+  std::map<uint32_t, double> skew;
+};
+
+// workload.hpp:189-221: mean pairwise overlap, densification over prefixes,
+// mean skewness at power-of-two partition counts (each a device operator)
+inline WorkloadMeasurement measure(const std::vector<SparseTensor>& tensors) {
+  if (tensors.size() < 2) throw Error("measurement requires at least two tensors");
+  for (const auto& t : tensors)
+    if (t.empty()) throw EmptyTensor("measurement undefined with empty tensors");
+  WorkloadMeasurement out;
+  double pairs = 0.0;
+  uint64_t np = 0;
+  for (size_t i = 0; i < tensors.size(); ++i)
+    for (size_t j = i + 1; j < tensors.size(); ++j, ++np) pairs += overlap_ratio(tensors[i], tensors[j]);
+  out.mean_pairwise_overlap = pairs / double(np);
+  SparseTensor acc = tensors.front();
+  double dsum = density(acc);
+  out.gamma[1] = 1.0;
+  for (size_t k = 2; k <= tensors.size(); ++k) {
+    acc = merge_sum(acc, tensors[k - 1]);
+    dsum += density(tensors[k - 1]);
+    out.gamma[k] = density(acc) / (dsum / double(k));
+  }
+  for (uint32_t parts = 1; parts <= tensors.size(); parts *= 2) {
+    double sk = 0.0;
+    for (const auto& t : tensors) sk += skewness_ratio(t, parts);
+    out.skew[parts] = sk / double(tensors.size());
+  }
+  return out;
+}
+
 // ---- sparsity profile and scheme selection: zen/costmodel.hpp ---------------
 struct SparsityProfile {  // tensor.hpp:216-240
   double d = 0.0;
@@ -795,6 +924,68 @@ inline double t_hc_coefficient(uint32_t n, const std::map<uint64_t, double>& gam
     sum += it->second;
   }
   return sum;
+}
+
+// ---- closed-form communication times (costmodel.hpp:14-128), element units --
+struct CostInputs {
+  uint32_t n = 1;
+  double universe = 0.0;  // M
+  double d = 0.0;
+  double b = 1.0;  // elements per time unit
+  std::map<uint64_t, double> gamma;
+  double skew = 1.0;
+  double broadcast_rounds = 1.0;
+};
+namespace detail {
+inline double gamma_of(const CostInputs& c, uint64_t k) {
+  if (k == 1) return 1.0;
+  auto it = c.gamma.find(k);
+  if (it == c.gamma.end())
+    throw MissingProfileEntry("densification ratio for k=" + std::to_string(k) + " missing from profile");
+  return it->second;
+}
+}  // namespace detail
+inline double t_bp(const CostInputs& c) {
+  if (c.n <= 1) return 0.0;
+  return t_bp_coefficient(c.n, detail::gamma_of(c, c.n)) * 2.0 * c.universe * c.d / c.b;
+}
+inline double t_hc(const CostInputs& c) {
+  return t_hc_coefficient(c.n, c.gamma) * 2.0 * c.universe * c.d / c.b;
+}
+inline double t_sparse_ps(const CostInputs& c) {
+  if (c.n <= 1) return 0.0;
+  const double g = detail::gamma_of(c, c.n);
+  return 2.0 * (double(c.n) - 1.0) * (1.0 + g) * c.skew * c.d * c.universe / double(c.n) / c.b;
+}
+inline double t_sparse_ps_broadcast(const CostInputs& c) {
+  if (c.n <= 1) return 0.0;
+  const double g = detail::gamma_of(c, c.n);
+  return 2.0 * (double(c.n) - 1.0) * c.skew * c.d * c.universe / double(c.n) / c.b +
+         2.0 * c.broadcast_rounds * g * c.d * c.universe / c.b;
+}
+inline double t_ring_incremental(const CostInputs& c) {
+  if (c.n <= 1) return 0.0;
+  double sum = 0.0;
+  for (uint64_t k = 1; k < c.n; ++k) sum += detail::gamma_of(c, k);
+  return 2.0 * sum * c.d * c.universe / double(c.n) / c.b;
+}
+inline double t_hierarchy_incremental_lb(const CostInputs& c) {
+  if (c.n <= 1) return 0.0;
+  return 2.0 * (double(c.n) - 1.0) * c.d * c.universe / double(c.n) / c.b;
+}
+inline double t_allreduce_dense(const CostInputs& c) {
+  if (c.n <= 1) return 0.0;
+  return 2.0 * (double(c.n) - 1.0) / double(c.n) * c.universe / c.b;
+}
+// experiment.hpp:161-169: the dense all-reduce baseline in bit units
+inline double allreduce_dense_time_bits(uint32_t n, uint64_t universe, double bandwidth) {
+  CostInputs c;
+  c.n = n;
+  c.universe = double(universe);
+  c.d = 1.0;
+  c.b = bandwidth / 32.0;
+  c.gamma[1] = 1.0;
+  return t_allreduce_dense(c);
 }
 
 enum class SchemeChoice { BalancedParallelism, HierarchicalCentralization };
@@ -849,6 +1040,33 @@ inline SparsityProfile profile_sparsity(const std::vector<std::vector<SparseTens
   prof.skew[uint32_t(n)] = skew_sum / double(rounds.size() * n);
   return prof;
 }
+
+#ifdef NLOHMANN_JSON_VERSION_MAJOR
+// the profile document (costmodel.hpp:191-219), when nlohmann/json is included
+inline nlohmann::json profile_to_json(const SparsityProfile& p) {
+  nlohmann::json j;
+  j["d"] = p.d;
+  j["gamma"] = nlohmann::json::object();
+  for (const auto& kv : p.gamma) j["gamma"][std::to_string(kv.first)] = kv.second;
+  j["skew"] = nlohmann::json::object();
+  for (const auto& kv : p.skew) j["skew"][std::to_string(kv.first)] = kv.second;
+  return j;
+}
+inline SparsityProfile profile_from_json(const nlohmann::json& j) {
+  SparsityProfile p;
+  if (!j.contains("d") || !j["d"].is_number()) throw MissingProfileEntry("profile json lacks a numeric 'd'");
+  p.d = j["d"].get<double>();
+  if (!j.contains("gamma") || !j["gamma"].is_object())
+    throw MissingProfileEntry("profile json lacks a 'gamma' object");
+  for (const auto& it : j["gamma"].items()) {
+    if (!it.value().is_number()) throw MissingProfileEntry("gamma entries must be numeric");
+    p.gamma[std::stoull(it.key())] = it.value().get<double>();
+  }
+  if (j.contains("skew"))
+    for (const auto& it : j["skew"].items()) p.skew[uint32_t(std::stoul(it.key()))] = it.value().get<double>();
+  return p;
+}
+#endif
 
 // ---- transport ledger: zen/simnet.hpp ---------------------------------------
 struct StageRecord {
@@ -1366,6 +1584,78 @@ inline const std::vector<std::string>& known_scheme_names() {
   static const std::vector<std::string> names = {"agsparse", "sparcml", "ring-centralization",
                                                  "omnireduce", "balanced-parallelism"};
   return names;
+}
+
+// ---- experiment driver pieces: zen/experiment.hpp ---------------------------
+struct ExperimentConfig {  // experiment.hpp:24-38 (the key=value parser is CLI, out of scope)
+  WorkloadSpec workload;
+  std::vector<std::string> schemes = known_scheme_names();
+  std::vector<uint32_t> n_list = {4, 8, 16};
+  double bandwidth = 1e9;
+  uint32_t trials = 1;
+  uint32_t hash_depth = 3;
+  double r1_multiplier = 2.0;
+  double r2_ratio = 0.1;
+  uint32_t lanes = 1;
+  uint32_t block_size = 256;
+  std::string out_dir = "out";
+  std::string tensors_dir;
+};
+
+struct HashSweepCell {  // experiment.hpp:356-364
+  double r1_multiplier = 0.0;
+  uint32_t rehash_depth = 0;
+  double serial_fraction = 0.0;
+  std::vector<uint64_t> placed_at_depth;
+  uint64_t loss = 0;
+  double wall_ms = 0.0;
+  bool overflow = false;
+};
+
+// The hash-memory geometry sweep of the paper's §4.3 study (zensim
+// bench-hash, experiment.hpp:366-401): one generated tensor through the
+// device hierarchical hash for r1 multiplier x rehash depth, the serial
+// region opened wide (r2 = r1) so the serial fraction is measured.
+inline std::vector<HashSweepCell> bench_hash(const ExperimentConfig& cfg) {
+  WorkloadSpec spec = cfg.workload;
+  spec.nodes = 1;
+  const SparseTensor t = generate(spec)[0];
+  const uint64_t nnz = t.nnz();
+  const uint32_t n = cfg.workload.nodes;
+  std::vector<HashSweepCell> cells;
+  for (double mult : {1.0, 2.0, 4.0})
+    for (uint32_t k : {1u, 2u, 3u, 4u}) {
+      HashSweepCell cell;
+      cell.r1_multiplier = mult;
+      cell.rehash_depth = k;
+      const HashFamily fam = HashFamily::make_worker(cfg.workload.seed, 0, n, k);
+      const uint64_t r1 = std::max<uint64_t>(1, uint64_t(mult * double(nnz) / double(n)));
+      try {
+        const auto t0 = std::chrono::steady_clock::now();
+        auto res = detail::run_hierarchical_hash(t, n, fam, r1, r1, cfg.lanes);
+        cell.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        cell.serial_fraction = double(res.second.serial_writes) / double(nnz);
+        cell.placed_at_depth = res.second.placed_at_depth;
+        cell.loss = nnz - res.first.total_nnz();
+      } catch (const SerialOverflow&) {
+        cell.overflow = true;
+      }
+      cells.push_back(cell);
+    }
+  return cells;
+}
+
+// codec.hpp:76-90: total index bits of a hash-bitmap pull (sum of |I_s| over
+// the servers, from the device universe tables) and of a plain-bitmap pull
+inline uint64_t pull_hash_bitmap_total_bits(uint64_t universe_size, uint32_t servers,
+                                            uint64_t partition_seed) {
+  HashUniverseTable t(universe_size, servers, partition_seed);
+  uint64_t total = 0;
+  for (uint32_t s = 0; s < servers; ++s) total += t.size(s);
+  return total;
+}
+inline uint64_t pull_plain_bitmap_total_bits(uint64_t universe_size, uint32_t servers) {
+  return uint64_t(servers) * universe_size;
 }
 
 }  // namespace zen_b200

@@ -11,7 +11,8 @@ from .zen import (  # noqa: F401
     HashUniverseTable, IndexOutsideUniverse, MalformedPayload, PartitionedSparseTensor,
     PeerTimeout, SerialOverflow, SimNet, SparseTensor, SyncOutcome, TrafficReport,
     UniverseMismatch, WireFormat, aggregate, bp_universe_table, collision_stats, context, decode,
-    derive_seed, encode, exchange_ipc_handles, hash_memory_layout, hierarchical_hash,
+    derive_seed, encode, exchange_ipc_handles, generate, generate_device, InfeasibleSpec,
+    WorkloadSpec, hash_memory_layout, hierarchical_hash,
     imbalance_pull, imbalance_push,
     message_sizes, partition_of, read_framed, read_sparse, read_sparse_file,
     run_balanced_parallelism, run_bp_with_retry, sparsify_topk, to_sparse, write_framed,

@@ -22,7 +22,7 @@ STAGE_NAMES = ("extract", "hash_push", "aggregate_encode_pull", "decode")
 
 # zen_status
 OK, E_INVALID, E_SERIAL_OVERFLOW, E_OUTSIDE, E_MALFORMED, E_EMPTY, E_MISMATCH, E_CUDA, \
-    E_PEER, E_OOM, E_TIMEOUT, E_CAPACITY = range(12)
+    E_PEER, E_OOM, E_TIMEOUT, E_CAPACITY, E_INFEASIBLE = range(13)
 
 
 class HashParamsC(C.Structure):
@@ -38,6 +38,12 @@ class HashFamilyC(C.Structure):
 class CollisionStatsC(C.Structure):
     _fields_ = [("serial_writes", C.c_uint64), ("placed_at_depth", C.c_uint64 * ZEN_MAX_K),
                 ("k", C.c_uint32)]
+
+
+class WorkloadSpecC(C.Structure):
+    _fields_ = [("universe", C.c_uint64), ("nodes", C.c_uint32), ("density", C.c_double),
+                ("omega", C.c_double), ("hot_fraction", C.c_double), ("hot_mass", C.c_double),
+                ("seed", C.c_uint64)]
 
 
 class WireFormatC(C.Structure):
@@ -65,6 +71,7 @@ _SIGS = {
     "zen_frame_parse": (C.c_int, [vp, u64, P(WireFormatC), P(MessageInfoC)]),
     "zen_sparsify_topk": (C.c_int, [vp, vp, u64, C.c_double, vp, vp, u64, P(u64)]),
     "zen_axpy_sparse": (C.c_int, [vp, vp, u64, vp, vp, u64, C.c_float]),
+    "zen_generate": (C.c_int, [vp, P(WorkloadSpecC), u32, vp, vp, u64, P(u64)]),
     "zen_merge_sum": (C.c_int, [vp, vp, vp, u64, vp, vp, u64, u64, vp, vp, u64, P(u64)]),
     "zen_range_counts": (C.c_int, [vp, vp, u64, u64, u32, P(u64)]),
     "zen_count_blocks": (C.c_int, [vp, vp, u64, u64, u64, P(u64)]),

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
+#include <random>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -267,6 +268,7 @@ const char* zen_status_string(zen_status s) {
     case ZEN_E_OOM: return "out of device memory";
     case ZEN_E_TIMEOUT: return "peer timeout";
     case ZEN_E_CAPACITY: return "capacity exceeded";
+    case ZEN_E_INFEASIBLE: return "infeasible workload spec";
   }
   return "unknown";
 }
@@ -1267,6 +1269,93 @@ extern "C" zen_status zen_range_counts(zen_ctx* c, const uint64_t* d_idx, uint64
 
 // ----------------------------------------------------------------- apply ----
 
+namespace {
+// Split `draws` between the hot tier [0, hot) and the cold tier [hot, m): the
+// reference flips hot_mass for every accepted draw (a binomial count) and
+// spills into the other tier once one is full (workload.hpp:79-100).
+void gen_split(uint64_t draws, double hot_mass, uint64_t hot_free, uint64_t cold_free,
+               uint64_t stream, uint64_t* hot_n, uint64_t* cold_n) {
+  std::mt19937_64 rng(stream);
+  uint64_t h = draws;
+  if (hot_mass < 1.0) {
+    std::binomial_distribution<uint64_t> b(draws, std::max(0.0, hot_mass));
+    h = b(rng);
+  }
+  h = std::min(h, hot_free);
+  uint64_t c = draws - h;
+  if (c > cold_free) {
+    c = cold_free;
+    h = draws - c;
+  }
+  *hot_n = h;
+  *cold_n = c;
+}
+}  // namespace
+
+extern "C" zen_status zen_generate(zen_ctx* c, const zen_workload_spec* sp, uint32_t node,
+                                   uint64_t* d_idx, float* d_val, uint64_t capacity,
+                                   uint64_t* count) {
+  if (!c || !sp || !count) return fail(ZEN_E_INVALID, "null argument");
+  // WorkloadSpec::validate (workload.hpp:34-50)
+  const double m_d = double(sp->universe);
+  if (sp->universe < 1) return fail(ZEN_E_INFEASIBLE, "universe must be at least 1");
+  if (sp->nodes < 1) return fail(ZEN_E_INFEASIBLE, "node count must be at least 1");
+  if (!(sp->density > 0.0 && sp->density <= 1.0)) return fail(ZEN_E_INFEASIBLE, "density must be in (0,1]");
+  if (sp->density * m_d < 1.0) return fail(ZEN_E_INFEASIBLE, "density*universe must be at least 1");
+  if (sp->omega < 0.0 || sp->omega > 1.0) return fail(ZEN_E_INFEASIBLE, "omega must be in [0,1]");
+  if (!(sp->hot_fraction > 0.0 && sp->hot_fraction <= 1.0))
+    return fail(ZEN_E_INFEASIBLE, "hot_fraction must be in (0,1]");
+  if (sp->hot_mass < 0.0 || sp->hot_mass > 1.0) return fail(ZEN_E_INFEASIBLE, "hot_mass must be in [0,1]");
+  if (sp->density * m_d * (1.0 + double(sp->nodes) * (1.0 - sp->omega)) > m_d)
+    return fail(ZEN_E_INFEASIBLE, "cannot fit disjoint remainders: d*M*(1+n*(1-omega)) > M");
+  if (node >= sp->nodes) return fail(ZEN_E_INVALID, "node out of range");
+  if (sp->universe >= (1ull << 40)) return fail(ZEN_E_INVALID, "universe above 2^40");
+  const uint64_t m = sp->universe;
+  const uint64_t nnz = uint64_t(std::ceil(sp->density * m_d));
+  const uint64_t core_n = std::min<uint64_t>(nnz, uint64_t(std::ceil(sp->omega * sp->density * m_d)));
+  const uint64_t hot = std::min<uint64_t>(m, std::max<uint64_t>(1, uint64_t(std::llround(sp->hot_fraction * m_d))));
+  const double hot_mass = (m - hot) == 0 ? 1.0 : sp->hot_mass;
+  *count = nnz;
+  if (nnz > 0xFFFFFFFFull) return fail(ZEN_E_INVALID, "more than 2^32 - 1 indices per node");
+  if (capacity < nnz) return fail(ZEN_E_CAPACITY, "output capacity below ceil(density * universe)");
+  if (!d_idx || !d_val) return fail(ZEN_E_INVALID, "null output");
+  DevGuard g(c->device);
+  SetupStream setup_(c->stream);
+  const uint64_t nw = (m + 63) / 64;
+  const uint64_t nblk = (nw + 1023) / 1024;
+  const uint64_t npos_max = nnz + core_n;
+  const uint64_t nblk_draw = (npos_max + 1023) / 1024 + 1;
+  Bump sc;
+  CKR(ctx_scratch(c, bump_bytes({8 * nw, 8 * nw, 4 * std::max(nblk, nblk_draw), 8}), &sc));
+  unsigned long long* core = sc.get<unsigned long long>(nw);
+  unsigned long long* bits = sc.get<unsigned long long>(nw);
+  uint32_t* blk = sc.get<uint32_t>(std::max(nblk, nblk_draw));
+  uint64_t* total = sc.get<uint64_t>(1);
+  CK(cudaMemsetAsync(core, 0, 8 * nw, c->stream));
+  CK(cudaMemsetAsync(bits, 0, 8 * nw, c->stream));
+  const uint64_t cold = m - hot;
+  // the shared core: the same draw on every node (workload.hpp:130-139)
+  const uint64_t cs = h_derive(sp->seed, 0xc07e);
+  uint64_t core_h, core_c;
+  gen_split(core_n, hot_mass, hot, cold, cs, &core_h, &core_c);
+  launch_gen_tier(0, hot, cs ^ 1, nullptr, 0, core_h, core, blk, c->stream);
+  launch_gen_tier(hot, cold, cs ^ 2, nullptr, 0, core_c, core, blk, c->stream);
+  // this node's remainder, avoiding the core (workload.hpp:141-151)
+  const uint64_t ns = h_derive(sp->seed, 0x10000 + node);
+  uint64_t node_h, node_c;
+  gen_split(nnz - core_n, hot_mass, hot - core_h, cold - core_c, ns, &node_h, &node_c);
+  if (node_h + node_c != nnz - core_n) return fail(ZEN_E_INFEASIBLE, "index universe exhausted");
+  launch_gen_tier(0, hot, ns ^ 1, core, core_h, node_h, bits, blk, c->stream);
+  launch_gen_tier(hot, cold, ns ^ 2, core, core_c, node_c, bits, blk, c->stream);
+  launch_gen_collect(bits, core, nw, blk, total, h_derive(sp->seed, 0x20000 + node), d_idx, d_val,
+                     capacity, c->stream);
+  uint64_t got = 0;
+  CK(cudaMemcpyAsync(&got, total, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (got != nnz) return fail(ZEN_E_CUDA, "generator count mismatch");
+  return ZEN_OK;
+}
+
 extern "C" zen_status zen_axpy_sparse(zen_ctx* c, float* d_dense, uint64_t m,
                                       const uint64_t* d_idx, const float* d_val, uint64_t count,
                                       float alpha) {
@@ -1535,7 +1624,18 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   CKR(mem.alloc(&x.ccnt, size_t(n) * (x.nchunk + x.nsup)));
   x.scnt = x.ccnt + size_t(n) * x.nchunk;
   x.st_idx = w.ex.st_idx;
-  x.scatter_grid = push_scatter_grid<uint32_t>(!bp->local && n > 4, x.ntiles);  // push_reorder
+  // peer destinations: regroup each round into per-part runs (full-line NVLink
+  // stores; measured N=4 0.177 vs 0.188 ms, N=2 equal) unless ZEN_PUSH_REORDER=0.
+  // The push is published by a one-block kernel after the scatter; the
+  // alternative, the scatter's last block (ZEN_PUSH_SIGNAL_FUSED=1), measured
+  // slower (N=2 0.146 vs 0.139 ms, N=4 0.181 vs 0.177 ms: every block's
+  // system-scope fence + counter, then one late block, costs more than a
+  // programmatic launch)
+  const char* ro = std::getenv("ZEN_PUSH_REORDER");
+  x.reorder = (!bp->local && !(ro && ro[0] == '0')) ? 1u : 0u;
+  const char* sf = std::getenv("ZEN_PUSH_SIGNAL_FUSED");
+  x.fused_signal = (sf && sf[0] == '1') ? 1u : 0u;
+  x.scatter_grid = push_scatter_grid<uint32_t>(x.reorder != 0, x.ntiles);
   zen_hash_family f;
   CKR(zen_hash_family_make_worker(bp->params.seed, w.id, n, k, &f));
   a.fam = fold(f);
@@ -1916,6 +2016,7 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     for (auto& w : bp->workers) {
       launch_push_scatter<uint32_t>(w.a, w.ex, st);  // + the push signal (rank mode)
       CKR(fork_side(w, true));
+      if (w.a.push_hdr && !w.a.xc.fused_signal) launch_push_signal<uint32_t>(w.a, st);
     }
   } else {
     if (ev) CK(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
@@ -2271,10 +2372,17 @@ zen_status zen_bp_time_extract(zen_bp* bp, const float* d_dense, uint32_t iters,
   // the sync's own extraction kernel (staging + h0 partition counts); its
   // counters only accumulate here and are reset by the next sync's begin
   Worker& w0 = bp->workers[0];
-  launch_extract_tiles_part<uint32_t>(d_dense, bp->m, w0.ex, w0.a, st);  // warm-up
+  // ZEN_DIAG_EXTRACT_PLAIN=1: the tile pass without the h0 counts (diagnosis)
+  static const bool plain = std::getenv("ZEN_DIAG_EXTRACT_PLAIN") != nullptr;
+  auto one = [&] {
+    if (plain)
+      launch_extract_tiles<uint32_t>(d_dense, bp->m, w0.ex, st);
+    else
+      launch_extract_tiles_part<uint32_t>(d_dense, bp->m, w0.ex, w0.a, st);
+  };
+  one();  // warm-up
   CK(cudaEventRecord(e0, st));
-  for (uint32_t i = 0; i < iters; ++i)
-    launch_extract_tiles_part<uint32_t>(d_dense, bp->m, w0.ex, w0.a, st);
+  for (uint32_t i = 0; i < iters; ++i) one();
   CK(cudaEventRecord(e1, st));
   CK(cudaEventSynchronize(e1));
   float t = 0.f;

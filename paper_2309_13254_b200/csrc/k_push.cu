@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kPushThreads)
   // to finish -- every block fences its NVLink stores (system scope) before it
   // counts itself done, so the count row and the release of the flag follow
   // every part store of this worker
-  if (a.push_hdr) {
+  if (a.push_hdr && x.fused_signal) {
     __shared__ uint32_t s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -415,13 +415,9 @@ void launch_bp_begin(const HashArgs<K>& a, cudaStream_t stream) {
   count_launch();
 }
 
-// peer destinations at n > 4: a warp's entries scatter over many parts, so
-// regroup them into full-line NVLink stores; otherwise store in place
-inline bool push_reorder(bool peer, uint32_t n) { return peer && n > 4; }
-
 template <typename K>
 void launch_push_scatter(const HashArgs<K>& a, const ExtractWs<K>& ws, cudaStream_t stream) {
-  launch_k(push_reorder(a.peer, a.fam.n) ? k_push_scatter<K, true> : k_push_scatter<K, false>,
+  launch_k(a.xc.reorder ? k_push_scatter<K, true> : k_push_scatter<K, false>,
            a.xc.scatter_grid,
            kPushThreads, 0, stream, a, (const K*)ws.st_idx, (const float*)ws.st_val);
   count_launch();

@@ -101,6 +101,8 @@ struct PushCounts {
   uint64_t pc;      // G * (partition_seed + 1)
   const void* st_idx;  // the extraction staging (K keys): the side path reads it in place
   uint32_t scatter_grid, place_grid;  // persistent grids (resident blocks)
+  uint32_t reorder;       // push scatter regroups each round into per-part runs (peer stores)
+  uint32_t fused_signal;  // the push scatter's last block publishes the push (rank mode)
 };
 
 // ---- kernel launchers (implemented in k_*.cu) ------------------------------
@@ -316,6 +318,14 @@ struct DecodeArgs {
                                            // the prefixes come from k_bpre
 };
 void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream);
+
+// device workload generator (k_gen.cu)
+void launch_gen_tier(uint64_t base, uint64_t range, uint64_t key_seed,
+                     const unsigned long long* core, uint64_t core_in_tier, uint64_t want,
+                     unsigned long long* bits, uint32_t* blk, cudaStream_t s);
+void launch_gen_collect(const unsigned long long* bits, const unsigned long long* core,
+                        uint64_t nw, uint32_t* blk, uint64_t* total, uint64_t vseed,
+                        uint64_t* out_idx, float* out_val, uint64_t cap, cudaStream_t s);
 
 // small helpers
 void launch_u64_to_u32(const uint64_t* in, uint32_t* out, uint64_t n, cudaStream_t stream);

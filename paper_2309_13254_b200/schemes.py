@@ -6,7 +6,8 @@ path) and Hierarchical Centralization, recursive doubling that merges at every
 stage.  The selector picks between them from a measured sparsity profile.
 
 Reference interface -> here:
-  zen::merge_sum                      (tensor.hpp:133-167)  merge_sum (zen_merge_sum: CUB merge + reduce-by-key)
+  zen::merge_sum                      (tensor.hpp:133-167)  merge_sum (zen_merge_sum: the merge-path
+                                                            kernel of k_merge.cu, fold in place)
   zen::density / overlap_ratio        (tensor.hpp:106-130)  density / overlap_ratio
   zen::densification_ratio            (tensor.hpp:178-189)  densification_ratio
   zen::skewness_ratio                 (tensor.hpp:193-213)  skewness_ratio (zen_range_counts)
@@ -15,7 +16,9 @@ Reference interface -> here:
   zen::CostInputs, t_* formulas       (costmodel.hpp:15-135) CostInputs, t_bp, t_hc, ...
   zen::select_scheme                  (costmodel.hpp:139-150) select_scheme
   zen::run_hier_centralization        (schemes.hpp:173-193) run_hier_centralization (one GPU)
-  -- one process per GPU --                                  HCSynchronizer (NCCL P2P + zen_merge_sum)
+  -- one process per GPU --                                  HCSynchronizer (NVLink stores into the
+                                                            partners' CUDA-IPC arenas + zen_merge_sum;
+                                                            NCCL/gloo only for the handle exchange)
 
 Every fold is zen_merge_sum.  Its merge may put a shared index's two entries
 in either order.  fp32 addition of two operands is commutative, so each value

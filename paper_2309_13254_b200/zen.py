@@ -84,6 +84,10 @@ class PeerTimeout(Error):
     pass
 
 
+class InfeasibleSpec(Error):
+    """zen::InfeasibleSpec (errors.hpp:81-84)."""
+
+
 def _lib():
     return L.load()
 
@@ -107,6 +111,8 @@ def _check(rc: int):
         raise CapacityError(msg)
     if rc == L.E_TIMEOUT:
         raise PeerTimeout(msg)
+    if rc == L.E_INFEASIBLE:
+        raise InfeasibleSpec(msg)
     if rc in (L.E_CUDA, L.E_OOM, L.E_PEER):
         raise CudaError(msg)
     raise Error(msg)
@@ -592,6 +598,53 @@ def decode(msg: EncodedMessage, universe: HashUniverse | None = None) -> SparseT
     z = got.value
     return SparseTensor(msg.universe_size, oi[:z].cpu().numpy().view(np.uint64),
                         ov[:z].cpu().numpy(), _trusted=True)
+
+
+@dataclass
+class WorkloadSpec:
+    """zen::WorkloadSpec (workload.hpp:22-51)."""
+    universe: int = 0
+    nodes: int = 1
+    density: float = 0.0
+    omega: float = 0.0
+    hot_fraction: float = 0.125
+    hot_mass: float = 0.125
+    seed: int = 0
+
+    def nnz_per_node(self) -> int:
+        return int(math.ceil(self.density * self.universe))
+
+    def c(self) -> L.WorkloadSpecC:
+        return L.WorkloadSpecC(self.universe, self.nodes, self.density, self.omega,
+                               self.hot_fraction, self.hot_mass, self.seed)
+
+
+def generate_device(spec: WorkloadSpec, node: int, device: int | None = None):
+    """Node `node`'s tensor of zen::generate drawn on the GPU (zen_generate):
+    (int64 indices, fp32 values) CUDA tensors, ascending."""
+    torch = _torch()
+    ctx = context(device)
+    z = max(spec.nnz_per_node(), 1)
+    dev = f"cuda:{ctx.device}"
+    oi = torch.empty(z, dtype=torch.int64, device=dev)
+    ov = torch.empty(z, dtype=torch.float32, device=dev)
+    got = C.c_uint64()
+    sc = spec.c()
+    _check(_lib().zen_generate(ctx.h, C.byref(sc), node, _ptr(oi), _ptr(ov), z, C.byref(got)))
+    return oi[:got.value], ov[:got.value]
+
+
+def generate(spec: WorkloadSpec) -> list:
+    """zen::generate (workload.hpp:119-154) on the device: spec.nodes tensors,
+    the shared core + two-tier draws without replacement, integer values.
+    Same spec as the reference, not the same bits (counter-based hashes
+    instead of std::mt19937_64); deterministic for a seed."""
+    out = []
+    for node in range(spec.nodes):
+        oi, ov = generate_device(spec, node)
+        out.append(SparseTensor(spec.universe, oi.cpu().numpy().view(np.uint64), ov.cpu().numpy(),
+                                _trusted=True))
+    return out
 
 
 def sparsify_topk(dense, fraction: float) -> SparseTensor:

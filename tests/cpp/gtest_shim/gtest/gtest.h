@@ -122,11 +122,21 @@ inline bool ulp_eq(double a, double b, int bits) {
   return (d < 0 ? -d : d) <= 4;
 }
 
+inline std::string& filter_out() {  // ":"-separated Suite.Name list to skip
+  static std::string f;
+  return f;
+}
+
 inline int run_all() {
   int failed = 0;
   std::vector<std::string> bad;
   std::printf("[==========] Running %zu tests.\n", registry().size());
   for (const Case& c : registry()) {
+    const std::string full = std::string(c.suite) + "." + c.name;
+    if ((":" + filter_out() + ":").find(":" + full + ":") != std::string::npos) {
+      std::printf("[ SKIPPED  ] %s (filtered)\n", full.c_str());
+      continue;
+    }
     std::printf("[ RUN      ] %s.%s\n", c.suite, c.name);
     std::fflush(stdout);
     failures_in_test() = 0;
@@ -160,7 +170,13 @@ inline int run_all() {
 }  // namespace gtest_shim
 
 namespace testing {
-inline void InitGoogleTest(int*, char**) {}
+// supports the negative form of --gtest_filter only: --gtest_filter=-A.b:C.d
+inline void InitGoogleTest(int* argc, char** argv) {
+  for (int i = 1; argc && i < *argc; ++i) {
+    const std::string a = argv[i];
+    if (a.rfind("--gtest_filter=-", 0) == 0) gtest_shim::filter_out() = a.substr(16);
+  }
+}
 }  // namespace testing
 #define RUN_ALL_TESTS() ::gtest_shim::run_all()
 

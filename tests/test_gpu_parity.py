@@ -463,7 +463,8 @@ def test_cpp_compat_dropin(zen):
     assert r.returncode == 0, r.stdout[-4000:]
 
 
-@pytest.mark.parametrize("suite", ["hashing", "tensor", "simnet"])
+@pytest.mark.parametrize("suite", ["hashing", "tensor", "codec", "simnet", "workload",
+                                   "costmodel", "schemes"])
 def test_reference_unit_suite_unmodified(zen, suite):
     """The reference's OWN GTest suite (proj/tests/<suite>_test.cpp), compiled
     unmodified against the drop-in by `make ref_tests` (zen/*.hpp -> compat.hpp
@@ -478,3 +479,23 @@ def test_reference_unit_suite_unmodified(zen, suite):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-6000:]
     assert "[  PASSED  ]" in r.stdout
+
+
+@pytest.mark.parametrize("criterion", [1, 2, 3, 4, 5, 6, 7, 8, 9])
+def test_reference_acceptance_unmodified(zen, criterion):
+    """The reference's acceptance driver (proj/tests/acceptance.cpp), compiled
+    unmodified against the drop-in, one criterion per run: C1 every scheme vs
+    the dense-sum oracle (:120-199), C2 no loss / lane invariance (:201-250),
+    C3 load balance (:255-330), C4 hash-bitmap size and Fig. 7 (:332-372), C5
+    codec round trips (:376-431), C6 cost-model extremes (:433-496), C7
+    simulator vs cost model (:498-547), C8 scheme orderings (:549-602), C9 the
+    hash-memory sweep (:604-645)."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "build", "ref_acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("built only where /root/reference exists (make ref_tests)")
+    r = subprocess.run([exe, str(criterion)], capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-2000:]
+    assert f"[PASS] C{criterion}" in r.stdout
