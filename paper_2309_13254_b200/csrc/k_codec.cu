@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
 
 constexpr int kAggThreads = 256;
 constexpr int kPrefixThreads = 512;  // union / bpre blocks
-constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (4)
+constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (8)
 
 __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
   if (a.in_hdr) return *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s];  // peers (rank mode)
