@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
 
 constexpr int kAggThreads = 256;
 constexpr int kPrefixThreads = 512;  // union / bpre blocks
-constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (8)
+constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (4)
 
 __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
   if (a.in_hdr) return *(volatile const uint32_t*)&a.in_hdr[w]->counts[a.s];  // peers (rank mode)
@@ -356,6 +356,8 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
   const uint64_t wbase = first ? __shfl_sync(0xffffffffu, ubase, first - 1) : 0ull;
   const uint32_t row0 = threadIdx.x & ~31u;
   __syncwarp();
+  // (unrolling this loop 4x with every value load of the pass issued first
+  // measured no faster: 0.1085 ms either way, aggregate 44.3 vs 43.2 us)
   for (uint32_t k0 = 0; k0 < T; k0 += 32) {
     const uint32_t k = k0 + lane;
     uint32_t L = 0;
@@ -623,28 +625,39 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecodeArgs a, uint64_t n
   const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
   const uint32_t row0 = threadIdx.x & ~31u;
   const uint64_t wrow = (w & ~31ull);
-  for (uint32_t k0 = 0; k0 < T; k0 += 32) {
-    const uint32_t k = k0 + lane;
-    uint32_t L = 0;
+  constexpr int UNR = 4;  // outputs per lane per pass, loads issued first
+  for (uint32_t k0 = 0; k0 < T; k0 += 32 * UNR) {
+    float v[UNR];
+    uint64_t oidx[UNR];
 #pragma unroll
-    for (uint32_t step = 16; step >= 1; step >>= 1) {
-      const uint32_t xc = __shfl_sync(0xffffffffu, x, L + step);
-      if (xc <= k) L += step;
+    for (int q = 0; q < UNR; ++q) {
+      const uint32_t k = k0 + q * 32 + lane;
+      uint32_t L = 0;
+#pragma unroll
+      for (uint32_t step = 16; step >= 1; step >>= 1) {
+        const uint32_t xc = __shfl_sync(0xffffffffu, x, L + step);
+        if (xc <= k) L += step;
+      }
+      const unsigned long long GL = __shfl_sync(0xffffffffu, G, L);
+      const uint32_t xL = __shfl_sync(0xffffffffu, x, L);
+      if (k < T) {
+        const uint32_t bit = (GL == ~0ull) ? k - xL : select64(GL, k - xL);  // full rows: direct
+        uint32_t s = 0;  // owner of the bit, from the word's owner planes
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j)
+          if (j < np) s |= (uint32_t)((spl[row0 + L][j] >> bit) & 1ull) << j;
+        const unsigned long long p = spres[row0 + L][s];
+        v[q] = a.vals[s][svb[row0 + L][s] + __popcll(p & lowmask64(bit))];
+        oidx[q] = (wrow + L) * 64 + bit;
+      }
     }
-    const unsigned long long GL = __shfl_sync(0xffffffffu, G, L);
-    const uint32_t xL = __shfl_sync(0xffffffffu, x, L);
-    if (k < T) {
-      const uint32_t bit = (GL == ~0ull) ? k - xL : select64(GL, k - xL);  // full rows: direct
-      uint32_t s = 0;  // owner of the bit, from the word's owner planes
 #pragma unroll
-      for (uint32_t j = 0; j < 4; ++j)
-        if (j < np) s |= (uint32_t)((spl[row0 + L][j] >> bit) & 1ull) << j;
-      const unsigned long long p = spres[row0 + L][s];
-      const float v = a.vals[s][svb[row0 + L][s] + __popcll(p & lowmask64(bit))];
+    for (int q = 0; q < UNR; ++q) {
+      const uint32_t k = k0 + q * 32 + lane;
       const uint64_t pos = ob + k;
-      if (pos < a.out_cap) {
-        a.out_idx[pos] = (wrow + L) * 64 + bit;
-        a.out_val[pos] = v;
+      if (k < T && pos < a.out_cap) {
+        a.out_idx[pos] = oidx[q];
+        a.out_val[pos] = v[q];
       }
     }
   }

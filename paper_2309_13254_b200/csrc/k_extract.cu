@@ -105,10 +105,14 @@ __global__ void __launch_bounds__(kThreads, 4)
   }
   if (lane == 0) s_warp_tot[warp] = wrun;
   if (PART) {
-    // 8-bit per-partition counters per lane (<= 32 non-zeros per lane)
+    // the h0 partition counts: 8-bit per-partition counters per lane
+    // (<= 32 non-zeros per lane), one warp reduction per partition, summed
+    // across warps after the block's one barrier
     uint64_t c0 = 0, c1 = 0;
     const bool any = __ballot_sync(0xffffffffu, nzbits != 0) != 0;
-    if (any) {
+    if (any && pc.n == 1) {
+      c0 = __popc(nzbits);  // map_to_range(h, 1) == 0: one partition, no hash
+    } else if (any) {
       for (uint32_t b = nzbits; b; b &= b - 1) {
         const uint32_t q = __ffs(b) - 1;
         const uint64_t e = (unit0 + (uint64_t)(q >> 3) * 32) * kUnit + (q & 7u);
@@ -123,16 +127,18 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
   }
   __syncthreads();
-  if (PART && threadIdx.x < pc.n) {
-    const uint32_t p = threadIdx.x;
-    uint32_t c = 0;
+  if (PART) {
+    if (threadIdx.x < pc.n) {
+      const uint32_t p = threadIdx.x;
+      uint32_t c = 0;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) c += s_wpc[w][p];
-    pc.tcnt[(uint64_t)p * pc.ntiles + tile] = c;
-    if (c) {
-      atomicAdd(pc.ccnt + (uint64_t)p * pc.nchunk + (tile >> 5), c);
-      atomicAdd(pc.scnt + (uint64_t)p * pc.nsup + (tile >> 10), c);
-      atomicAdd(load + p, c);
+      for (int w = 0; w < kThreads / 32; ++w) c += s_wpc[w][p];
+      pc.tcnt[(uint64_t)p * pc.ntiles + tile] = c;
+      if (c) {  // (no per-partition total here: thousands of tiles on one word
+                // would serialise at its L2 slice; the scatter sums the super chunks)
+        atomicAdd(pc.ccnt + (uint64_t)p * pc.nchunk + (tile >> 5), c);
+        atomicAdd(pc.scnt + (uint64_t)p * pc.nsup + (tile >> 10), c);
+      }
     }
   }
   uint32_t wbase = 0, total = 0;

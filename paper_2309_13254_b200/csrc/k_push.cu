@@ -127,11 +127,16 @@ __global__ void __launch_bounds__(kPushThreads)
   const PushCounts& x = a.xc;
   const uint32_t n = a.fam.n, lane = lane_id(), warp = threadIdx.x >> 5;
   HashHdr* h = a.hdr;
-  if (warp == 0) {
-    const uint64_t l = lane < n ? (uint64_t)a.load[lane] : 0ull;
-    uint64_t z = l;
+  if (warp == 0) {  // z = sum of the super-chunk counts (block 0 also publishes the loads)
+    uint64_t z = 0;
+    for (uint32_t p = 0; p < n; ++p) {
+      uint64_t l = 0;
+      for (uint32_t i = lane; i < x.nsup; i += 32) l += x.scnt[(uint64_t)p * x.nsup + i];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+      for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+      if (blockIdx.x == 0 && lane == 0) a.load[p] = (uint32_t)l;
+      z += l;
+    }
     if (lane == 0) s_z = z;
   }
   __syncthreads();

@@ -15,7 +15,7 @@ constexpr uint32_t kMaxWorkers = 16;    // n for the fused BP pipeline
 constexpr uint32_t kHashTile = 256;     // keys per hash tile (one per thread)
 constexpr uint32_t kExtractTile = 8192; // floats per extraction tile
 constexpr uint32_t kDecodeTileWords = 128;  // 64-index words per decode tile (= block size)
-constexpr uint32_t kPrefixBlockWords = 4096;  // bitmap words per popcount-prefix block (512 threads x 8)
+constexpr uint32_t kPrefixBlockWords = 2048;  // bitmap words per popcount-prefix block (512 threads x 4)
                                               // (256 threads x 8 consecutive words)
 constexpr uint64_t kKeyBits = 40;       // slot word: [63:40] epoch, [39:0] index+1
 constexpr uint64_t kKeyMask = (1ull << kKeyBits) - 1ull;

@@ -92,7 +92,7 @@ def main(tag):
                   "", "Cold-cache, serialised per-launch times (ncu replays each launch); "
                   "the SHARE of the sync is what compares with bench.py's live numbers.", "",
                   f"syncs captured: {nsync}; one sync = sum of per-kernel means: {step:.1f} us "
-                  "(k_place/k_depth/k_serial_*/k_fallback run on the forked side stream, "
+                  "(k_place[_tiles]/k_depth[_scan]/k_serial_*/k_fallback run on the forked side stream, "
                   "overlapped with the data path in the live run)", "",
                   "| kernel | launches | mean us | share of sync |", "|---|---|---|---|"]
         for k, v in per.items():
