@@ -1643,6 +1643,13 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   return ZEN_OK;
 }
 
+// rank mode: gate the peers' arrival inside the consumer kernels (one polling
+// block + a local release) unless ZEN_WAIT_KERNEL=1 (a one-warp wait kernel)
+bool gate_waits() {
+  const char* e = std::getenv("ZEN_WAIT_KERNEL");
+  return !(e && e[0] == '1');
+}
+
 zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   const uint32_t n = bp->n;
   DevMem& mem = bp->mem;
@@ -1687,6 +1694,7 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   a.agg_count = s.agg_count;
   a.wait_push = bp->local ? 0 : 1;
   a.peer = bp->local ? 0 : 1;
+  a.gate = gate_waits() ? 1 : 0;
   return ZEN_OK;
 }
 
@@ -1872,6 +1880,7 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
   da.out_cap = bp->out_cap;
   da.hdr = bp->workers[0].a.hdr;
   da.wait_pull = bp->local ? 0 : 1;
+  da.gate = gate_waits() ? 1 : 0;
   for (auto& s : bp->servers) {
     const Worker* w = nullptr;
     for (auto& ww : bp->workers)

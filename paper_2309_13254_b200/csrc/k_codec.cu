@@ -140,6 +140,9 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
   zen_dev::pdl_entry();
   __shared__ uint64_t pre[kMaxWorkers + 1];
   const uint32_t n = a.n;
+  if (a.wait_push && a.gate)  // rank mode: the n pushes have arrived (no k_wait_push)
+    arrival_gate(n, [&](uint32_t w) { return (const unsigned long long*)&a.in_hdr[w]->flag; },
+                 &a.hdr->go[0], *(volatile uint32_t*)&a.hdr->iter, &a.hdr->status);
   if (threadIdx.x == 0) {
     uint64_t acc = 0;
     for (uint32_t w = 0; w < n; ++w) {
@@ -523,6 +526,12 @@ __device__ __forceinline__ uint32_t field16(uint64_t v, int g) {
 template <int NMAX>
 __global__ void __launch_bounds__(kDecThreads) k_decode(DecodeArgs a, uint64_t nwords) {
   zen_dev::pdl_entry();
+  if (a.wait_pull && a.gate)  // rank mode: the n pulls have arrived (no k_wait_pull)
+    arrival_gate(a.n,
+                 [&](uint32_t s) {
+                   return a.bits[s] ? (const unsigned long long*)&a.pull_hdr[s]->flag : nullptr;
+                 },
+                 &a.hdr->go[1], *(volatile uint32_t*)&a.hdr->iter, &a.hdr->status);
   constexpr int kDecGroup = NMAX < 4 ? NMAX : 4;  // servers per packed scan
   __shared__ unsigned long long spres[kDecThreads][NMAX];
   __shared__ uint32_t svb[kDecThreads][NMAX];
@@ -697,7 +706,7 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
 
 void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
   // a.pw is all-zero here: zeroed at allocation, re-zeroed by k_agg_values
-  if (a.wait_push) {
+  if (a.wait_push && !a.gate) {
     launch_k(k_wait_push, 1, 32, 0, stream, a);
     count_launch();
   }
@@ -722,7 +731,7 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
 void launch_decode_parts(const DecodeArgs& a, cudaStream_t stream) {
   const uint64_t nwords = (a.m + 63) / 64;
   const uint32_t ntiles = (uint32_t)((nwords + kDecThreads - 1) / kDecThreads);
-  if (a.wait_pull) {
+  if (a.wait_pull && !a.gate) {
     launch_k(k_wait_pull, 1, 32, 0, stream, a);
     count_launch();
   }

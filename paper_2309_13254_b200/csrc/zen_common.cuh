@@ -355,6 +355,14 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 // Spin until *flag >= want (acquire, system scope). Returns false on timeout.
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ bool wait_flag(const unsigned long long* flag, uint64_t want,
                                           uint64_t timeout_ns) {
   const uint64_t t0 = globaltimer_ns();
@@ -363,6 +371,31 @@ __device__ __forceinline__ bool wait_flag(const unsigned long long* flag, uint64
     __nanosleep(64);
   }
   return true;
+}
+
+// Rank mode arrival gate inside a consumer kernel: warp 0 of block 0 polls
+// the n peers' system-scope flags (lane s: flag s, with the watchdog) and then
+// releases a LOCAL word; every block's thread 0 acquires that word at gpu
+// scope.  Acquire (sys) -> release (gpu) -> acquire (gpu) is a causality
+// chain, so every block sees the peers' data; and no grid of CTAs spins on
+// NVLink lines (which slows the stores being waited for).
+template <typename FlagOf>
+__device__ __forceinline__ void arrival_gate(uint32_t n, FlagOf flag_of, uint32_t* go,
+                                             uint32_t iter, uint32_t* status) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const unsigned long long* f = threadIdx.x < n ? flag_of(threadIdx.x) : nullptr;
+    if (f && !wait_flag(f, iter, zen::kPeerTimeoutNs)) atomicOr(status, zen::kErrTimeout);
+    __syncwarp();
+    if (threadIdx.x == 0) st_release_gpu(go, iter);
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_gpu(go) != iter) {
+      if (globaltimer_ns() - t0 > zen::kPeerTimeoutNs) break;  // the poller reports it
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
 }
 
 // 256-bit streaming load (sm_100 ld.v8): read once, no L1 allocation, evict

@@ -55,6 +55,7 @@ struct HashHdr {
   double r1_mult, r2_ratio;
   uint64_t bad_index;    // IndexOutsideUniverse witness (min), ~0 = none
   uint32_t work[3];      // push-scatter groups, claim groups, push-scatter blocks done (per sync)
+  uint32_t go[2];        // rank mode: push / pull arrival, released by the one polling block
 };
 
 constexpr uint32_t kErrTimeout = 1u, kErrOutside = 2u, kErrCapacity = 4u;
@@ -277,6 +278,7 @@ struct AggArgs {
   uint64_t* agg_count;            // U_s (device)
   HashHdr* hdr;                   // iteration / error bits / bad index
   int wait_push;                  // wait for in_hdr[w]->flag >= hdr->iter
+  int gate;                       // 1: the wait is gated inside k_agg_mark (no k_wait_push)
   int peer;                       // destinations include other GPUs (system-scope release)
   // BP pull: per 32-word chunk of the GLOBAL index space, the number of U_s
   // bits before the chunk's first position in I_s -- the receivers' decode
@@ -313,6 +315,7 @@ struct DecodeArgs {
   uint64_t out_cap;
   HashHdr* hdr;
   int wait_pull;
+  int gate;                                // 1: the wait is gated inside k_decode (no k_wait_pull)
   uint32_t* popc_total;                    // [n] per-server popcount (malformed check)
   const uint32_t* const* cbase;            // [n] pulled per-chunk value bases (BP), or null:
                                            // the prefixes come from k_bpre

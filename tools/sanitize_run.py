@@ -63,7 +63,7 @@ def main():
     # standalone hash with the layout dump, tight sizes (serial + fallback)
     idx, val = pairs[0]
     fam = zen.HashFamily.make_worker(3, 1, 4, 3)
-    r1 = max(1, idx.size // 5)
+    r1 = max(1, idx.size // 3)  # loads ~z/4 < r1: no overflow, a tight r2 -> fallback
     got = zen.hash_memory_layout(zen.SparseTensor(m, idx, val), 4, fam, r1, max(1, r1 // 50))
     ref = co.hierarchical_hash(m, idx, val, co.family(3, 4, 3, worker=1), r1, max(1, r1 // 50),
                                layout=True)
