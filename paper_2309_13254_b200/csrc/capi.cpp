@@ -1643,11 +1643,14 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   return ZEN_OK;
 }
 
-// rank mode: gate the peers' arrival inside the consumer kernels (one polling
-// block + a local release) unless ZEN_WAIT_KERNEL=1 (a one-warp wait kernel)
+// rank mode: the peers' arrival is awaited by a one-warp kernel before the
+// consumer.  Gating it inside the consumer instead (one polling block releases
+// a local word, ZEN_WAIT_GATE=1) measured slower: N=2 0.149 vs 0.141 ms, N=4
+// 0.185 vs 0.180 ms (every block of the consumer holds an SM slot while it
+// waits, where the one-warp kernel lets the consumer's blocks launch at once)
 bool gate_waits() {
-  const char* e = std::getenv("ZEN_WAIT_KERNEL");
-  return !(e && e[0] == '1');
+  const char* e = std::getenv("ZEN_WAIT_GATE");
+  return e && e[0] == '1';
 }
 
 zen_status bp_alloc_server(zen_bp* bp, Server& s) {
@@ -1995,8 +1998,10 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   // at millions of keys it needs the whole GPU not to become the tail (rank
   // mode keeps it narrower: its aggregate waits on the peers, and measured at
   // n=4 one more CTA per SM costs the critical path 10 us)
-  const unsigned side_ctas = (unsigned)std::min<uint64_t>(
-      6, std::max<uint64_t>(2, bp->cap >> (bp->local ? 18 : 20)));
+  static const char* side_env = std::getenv("ZEN_SIDE_CTAS");  // tuning override
+  const unsigned side_ctas = side_env ? (unsigned)std::max(1, std::atoi(side_env))
+                                      : (unsigned)std::min<uint64_t>(
+                                            6, std::max<uint64_t>(2, bp->cap >> (bp->local ? 18 : 20)));
   auto fork_side = [&](Worker& w, bool dense_path) -> zen_status {
     CK(cudaEventRecord(bp->fork, st));
     CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
