@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) k_tables_own(uint64_t m, uint32_t n, uint
 // ------------------------------------------------------------- aggregate ----
 
 constexpr int kAggThreads = 256;
-constexpr int kPrefixThreads = 512;  // union / bpre blocks
+constexpr int kPrefixThreads = 512;  // union / bpre blocks (256-thread blocks measured no faster)
 constexpr int kWPT = kPrefixBlockWords / kPrefixThreads;  // consecutive words per thread (4)
 
 __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
