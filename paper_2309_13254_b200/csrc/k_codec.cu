@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
       if (v) {
         b = a.pre[(uint64_t)w * a.nws + j];  // part index of the word's first entry (k_agg_mark)
         a.pw[(uint64_t)w * a.nws + j] = 0ull;  // last reader: clean for the next sync
+        a.pre[(uint64_t)w * a.nws + j] = ~0u;  // (the push scatter's marks take atomicMin)
       }
     }
     spw[threadIdx.x][w] = v;
@@ -704,13 +705,16 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
   count_launch();
 }
 
-void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
+void launch_aggregate(const AggArgs& a, cudaStream_t stream, bool marked) {
   // a.pw is all-zero here: zeroed at allocation, re-zeroed by k_agg_values
   if (a.wait_push && !a.gate) {
     launch_k(k_wait_push, 1, 32, 0, stream, a);
     count_launch();
   }
-  launch_k(k_agg_mark, 148 * 8, kAggThreads, 0, stream, a);
+  if (!marked) {
+    launch_k(k_agg_mark, 148 * 8, kAggThreads, 0, stream, a);
+    count_launch();
+  }
   launch_k(k_agg_union, a.nblk, kPrefixThreads, 0, stream, a);
   const unsigned g = (unsigned)((a.nw + kValThreads - 1) / kValThreads);
   if (a.n <= 2)
@@ -721,7 +725,7 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream) {
     launch_k(k_agg_values<8>, g, kValThreads, 0, stream, a);
   else
     launch_k(k_agg_values<16>, g, kValThreads, 0, stream, a);
-  for (int i = 0; i < 3; ++i) count_launch();
+  for (int i = 0; i < 2; ++i) count_launch();
   if (a.dst_hdr) {
     launch_k(k_agg_signal, 1, 32, 0, stream, a);
     count_launch();

@@ -247,9 +247,10 @@ __global__ void __launch_bounds__(kPushThreads)
         for (int j = 0; j < kPushPer; ++j) {
           const uint32_t p = pv[j];
           const uint64_t b = __shfl_sync(0xffffffffu, mybase + run + woff, p < kMaxWorkers ? p : 0u);
+          const uint64_t pos = b + rk[j];
+          const bool st = p != 0xFFFFFFFFu && pos < a.dst_cap;
           if (p != 0xFFFFFFFFu) {
-            const uint64_t pos = b + rk[j];
-            if (pos < a.dst_cap) {
+            if (st) {
               a.dst_idx[p][pos] = xv[j];
               a.dst_val[p][pos] = vv[j];
             } else {
@@ -257,6 +258,30 @@ __global__ void __launch_bounds__(kPushThreads)
             }
             if (pos == lim)
               atomicMin((unsigned long long*)&h->ovf_word, (((uint64_t)xv[j] + 1) << 16) | p);
+          }
+          if (x.mark) {
+            // k_agg_mark's work, for servers on this GPU: the entry's rank in
+            // I_p (zen/codec.hpp:146-158) sets its bit in this worker's
+            // presence row of server p, one atomicOr per (server, word) per
+            // warp; the word's first part index (the value base the fold
+            // needs) by atomicMin -- the group leader holds the smallest
+            uint64_t word = ~0ull;
+            uint64_t bit = 0;
+            if (st) {
+              const uint64_t key = xv[j];
+              const OwnWord ow = x.mk_own[p][key >> 6];
+              const uint32_t r = ow.prefix + (uint32_t)__popcll(ow.mask & lowmask64(key & 63u));
+              word = ((uint64_t)p << 40) | (r >> 6);
+              bit = 1ull << (r & 63u);
+            }
+            const uint32_t g = __match_any_sync(0xffffffffu, word);
+            const uint32_t lo = __reduce_or_sync(g, (uint32_t)bit);
+            const uint32_t hi = __reduce_or_sync(g, (uint32_t)(bit >> 32));
+            if (st && lane == (uint32_t)(__ffs(g) - 1)) {
+              const uint64_t row = (uint64_t)a.me * x.mk_nws[p] + (word & ((1ull << 40) - 1));
+              atomicOr(x.mk_pw[p] + row, ((unsigned long long)hi << 32) | lo);
+              atomicMin(x.mk_pre[p] + row, (uint32_t)pos);
+            }
           }
         }
         run += tot;

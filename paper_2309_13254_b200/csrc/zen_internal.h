@@ -104,6 +104,13 @@ struct PushCounts {
   uint32_t scatter_grid, place_grid;  // persistent grids (resident blocks)
   uint32_t reorder;       // push scatter regroups each round into per-part runs (peer stores)
   uint32_t fused_signal;  // the push scatter's last block publishes the push (rank mode)
+  // local mode (every server on this GPU): the scatter also marks each entry
+  // in its server's presence bitmap (k_agg_mark's work), per server p:
+  uint32_t mark;
+  const OwnWord* const* mk_own;        // [n] server p's {mask, prefix} per 64-index word
+  unsigned long long* const* mk_pw;    // [n] server p's presence rows (row w: + w * nws_p)
+  uint32_t* const* mk_pre;             // [n] server p's value-base rows (atomicMin, ~0 = none)
+  const uint64_t* mk_nws;              // [n] server p's row stride in words
 };
 
 // ---- kernel launchers (implemented in k_*.cu) ------------------------------
@@ -288,7 +295,9 @@ struct AggArgs {
   const unsigned long long* own_bits;  // this server's local copy of U (a dst_bits entry)
   uint32_t* const* dst_cbase;     // [ndst] -> (nchunks + 1) u32 per receiver
 };
-void launch_aggregate(const AggArgs& a, cudaStream_t stream);
+// marked: the presence bitmaps and value bases were already written by the
+// push scatter (local mode, dense syncs), so k_agg_mark is skipped
+void launch_aggregate(const AggArgs& a, cudaStream_t stream, bool marked = false);
 
 // decode of all servers' HashBitmap messages into the global sorted result
 struct DecodeArgs {
