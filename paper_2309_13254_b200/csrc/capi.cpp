@@ -1874,6 +1874,7 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
     // 8 emulated workers 1.55 vs 1.19 ms: the rank lookups and atomics lengthen
     // the scatter on the critical path by more than the mark kernel they save
     const char* mk = std::getenv("ZEN_SCATTER_MARK");
+    for (auto& s : bp->servers) s.a.pre_min = (mk && mk[0] == '1') ? 1 : 0;
     for (auto& w : bp->workers) {
       w.a.xc.mark = (mk && mk[0] == '1') ? 1u : 0u;
       w.a.xc.mk_own = d_own;

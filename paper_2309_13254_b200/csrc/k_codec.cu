@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
       if (v) {
         b = a.pre[(uint64_t)w * a.nws + j];  // part index of the word's first entry (k_agg_mark)
         a.pw[(uint64_t)w * a.nws + j] = 0ull;  // last reader: clean for the next sync
-        a.pre[(uint64_t)w * a.nws + j] = ~0u;  // (the push scatter's marks take atomicMin)
+        if (a.pre_min) a.pre[(uint64_t)w * a.nws + j] = ~0u;  // scatter marks: atomicMin
       }
     }
     spw[threadIdx.x][w] = v;

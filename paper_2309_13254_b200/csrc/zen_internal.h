@@ -294,6 +294,8 @@ struct AggArgs {
   uint64_t nchunks;               // ceil(M / 2048)
   const unsigned long long* own_bits;  // this server's local copy of U (a dst_bits entry)
   uint32_t* const* dst_cbase;     // [ndst] -> (nchunks + 1) u32 per receiver
+  int pre_min;                    // value bases come from the scatter's atomicMin marks:
+                                  // reset each word read to ~0 (ZEN_SCATTER_MARK=1)
 };
 // marked: the presence bitmaps and value bases were already written by the
 // push scatter (local mode, dense syncs), so k_agg_mark is skipped
