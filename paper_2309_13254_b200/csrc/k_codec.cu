@@ -249,7 +249,8 @@ __global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
 #pragma unroll
   for (int i = 0; i < kWPT; ++i) U[i] = 0;
   if (live) {
-    for (uint32_t x = 0; x < n; ++x) {
+#pragma unroll 4
+    for (uint32_t x = 0; x < n; ++x) {  // (unrolled: several rows' loads in flight)
       unsigned long long v[kWPT];
       load8(a.pw + (uint64_t)x * a.nws + j0, v);
 #pragma unroll
@@ -332,22 +333,25 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
   }
   const bool valid = j < a.nw;
   const uint32_t pb = (uint32_t)(j / kPrefixBlockWords);
-  unsigned long long U = 0;
+  // every worker's presence word first, then the value bases, then the
+  // clean-up stores: stores between the loads would serialise them (the rows
+  // share one array, so the compiler cannot move a load above a store)
+  unsigned long long U = 0, v[NMAX];
+  uint32_t b[NMAX];
+#pragma unroll
+  for (int w = 0; w < NMAX; ++w) v[w] = (w < (int)n && valid) ? a.pw[(uint64_t)w * a.nws + j] : 0ull;
+#pragma unroll
+  for (int w = 0; w < NMAX; ++w)  // part index of the word's first entry (k_agg_mark)
+    b[w] = v[w] ? a.pre[(uint64_t)w * a.nws + j] : 0u;
 #pragma unroll
   for (int w = 0; w < NMAX; ++w) {
-    unsigned long long v = 0;
-    uint32_t b = 0;
-    if (w < (int)n && valid) {
-      v = a.pw[(uint64_t)w * a.nws + j];
-      if (v) {
-        b = a.pre[(uint64_t)w * a.nws + j];  // part index of the word's first entry (k_agg_mark)
-        a.pw[(uint64_t)w * a.nws + j] = 0ull;  // last reader: clean for the next sync
-        if (a.pre_min) a.pre[(uint64_t)w * a.nws + j] = ~0u;  // scatter marks: atomicMin
-      }
+    if (v[w]) {
+      a.pw[(uint64_t)w * a.nws + j] = 0ull;  // last reader: clean for the next sync
+      if (a.pre_min) a.pre[(uint64_t)w * a.nws + j] = ~0u;  // scatter marks: atomicMin
     }
-    spw[threadIdx.x][w] = v;
-    sbase[threadIdx.x][w] = b;
-    U |= v;
+    spw[threadIdx.x][w] = v[w];
+    sbase[threadIdx.x][w] = b[w];
+    U |= v[w];
   }
   const uint64_t ubase = (valid && U) ? (uint64_t)a.blk[(uint64_t)n * a.nblk + pb] +
                                             a.pre[(uint64_t)n * a.nws + j] : 0ull;
