@@ -1642,6 +1642,7 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   zen_hash_family f;
   CKR(zen_hash_family_make_worker(bp->params.seed, w.id, n, k, &f));
   a.fam = fold(f);
+  a.fam.db = std::getenv("ZEN_SLOT_REHASH") ? 0u : slot_probe_bits(k, bp->m);  // (env: A/B only)
   x.pc = a.fam.pc;
   return ZEN_OK;
 }
@@ -1980,6 +1981,7 @@ zen_status zen_bp_set_params(zen_bp* bp, const zen_hash_params* p) {
     zen_hash_family f;
     CKR(zen_hash_family_make_worker(p->seed, w.id, bp->n, p->rehash_depth, &f));
     w.a.fam = fold(f);
+    w.a.fam.db = std::getenv("ZEN_SLOT_REHASH") ? 0u : slot_probe_bits(p->rehash_depth, bp->m);
   }
   bp->stride_cap = std::max(bp->stride_cap, sc);
   if (bp->gexec) cudaGraphExecDestroy(bp->gexec);
@@ -2041,7 +2043,11 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   const unsigned side_ctas = side_env ? (unsigned)std::max(1, std::atoi(side_env))
                                       : (unsigned)std::min<uint64_t>(
                                             6, std::max<uint64_t>(2, bp->cap >> (bp->local ? 18 : 20)));
+  // diagnostic only (timeline studies): no hash-memory side path at all, so
+  // no CollisionStats -- never set for a result that is checked or reported
+  static const bool diag_no_side = std::getenv("ZEN_DIAG_NO_SIDE") != nullptr;
   auto fork_side = [&](Worker& w, bool dense_path) -> zen_status {
+    if (diag_no_side) return ZEN_OK;
     CK(cudaEventRecord(bp->fork, st));
     CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
     LaunchScope low(/*pdl=*/false, /*low_priority=*/true);
@@ -2088,8 +2094,10 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   if (ev) CK(cudaEventRecordWithFlags(ev[3], st, cudaEventRecordExternal));
   bp->dec.launch(bp->da, st);
   if (ev) CK(cudaEventRecordWithFlags(ev[4], st, cudaEventRecordExternal));
-  CK(cudaEventRecord(bp->join, bp->side));
-  CK(cudaStreamWaitEvent(st, bp->join, 0));
+  if (!diag_no_side) {
+    CK(cudaEventRecord(bp->join, bp->side));
+    CK(cudaStreamWaitEvent(st, bp->join, 0));
+  }
   CK(cudaGetLastError());
   return ZEN_OK;
 }

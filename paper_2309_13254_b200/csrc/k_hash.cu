@@ -465,7 +465,7 @@ __device__ __forceinline__ void fallback_place(const HashArgs<K>& a, SlotOf<K>* 
       if (fbp < r1) slot = (int64_t)fbp;
     }
   }
-  if (slot >= 0) base[slot] = S::make(ew, key);
+  if (slot >= 0) base[slot] = S::make(ew, key, depth ? depth - 1 : 0u, sizeof(SlotOf<K>) == 4 ? a.fam.db : 0u);
 }
 
 template <typename K>
@@ -593,6 +593,7 @@ __global__ void __launch_bounds__(kThreads) k_depth_scan(HashArgs<K> a) {
   using W = SlotOf<K>;
   using S = Slot<W>;
   W* region = a.slots + (uint64_t)p * stride;
+  const uint32_t db = sizeof(W) == 4 ? a.fam.db : 0u;
   const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
   constexpr int R = 4;  // slots per thread per round, loads issued together
   for (uint64_t c0 = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); ok && c0 < r1;
@@ -615,10 +616,14 @@ __global__ void __launch_bounds__(kThreads) k_depth_scan(HashArgs<K> a) {
       const uint64_t c = c0 + (uint64_t)j * nthr + lane;
       uint32_t d = 0;
       if (!S::vacant(w[j], ew)) {  // held in this sync (c < r1 implied)
-        const uint64_t key = S::key(w[j]);
-        uint32_t t = 0;
-        while (t + 1 < k && slot_of(a.fam, key, t, r1) != c) ++t;
-        d = t + 1;
+        if (db) {  // the claiming probe is in the word
+          d = S::probe(w[j], db) + 1;
+        } else {
+          const uint64_t key = S::key(w[j]);
+          uint32_t t = 0;
+          while (t + 1 < k && slot_of(a.fam, key, t, r1) != c) ++t;
+          d = t + 1;
+        }
       }
       const uint32_t g = __match_any_sync(0xffffffffu, d);
       if (d && lane == (uint32_t)(__ffs(g) - 1)) atomicAdd(&s_hist[p * (k + 1) + d], (uint32_t)__popc(g));

@@ -19,21 +19,39 @@ __device__ __forceinline__ uint64_t epoch_word(uint32_t epoch) {
 // words it read, which keeps the memory vacant between syncs.
 template <typename W>
 struct Slot;
+// The u32 words also carry the claiming probe t below the key when
+// DevFamily.db > 0: (index+1) << db | t.  The min-claim order is unchanged
+// (a key meets itself at no slot), and the probe a key holds a slot by is
+// always its FIRST probe onto that slot (a key displaced from slot c by a
+// smaller key can never win c back), so readers take the depth from the word
+// instead of re-hashing.
 template <>
 struct Slot<unsigned long long> {
   static constexpr unsigned long long kVacant = ~0ull;
-  __device__ __forceinline__ static unsigned long long make(uint64_t ew, uint64_t key) { return ew | key; }
+  __device__ __forceinline__ static unsigned long long make(uint64_t ew, uint64_t key, uint32_t = 0,
+                                                            uint32_t = 0) {
+    return ew | key;
+  }
   __device__ __forceinline__ static bool vacant(unsigned long long w, uint64_t ew) {
     return w > (ew | zen::kKeyMask);  // empty or an older epoch
   }
-  __device__ __forceinline__ static uint64_t key(unsigned long long w) { return w & zen::kKeyMask; }
+  __device__ __forceinline__ static uint64_t key(unsigned long long w, uint32_t = 0) {
+    return w & zen::kKeyMask;
+  }
+  __device__ __forceinline__ static uint32_t probe(unsigned long long, uint32_t) { return 0; }
 };
 template <>
 struct Slot<unsigned int> {
   static constexpr unsigned int kVacant = 0xFFFFFFFFu;
-  __device__ __forceinline__ static unsigned int make(uint64_t, uint64_t key) { return (unsigned int)key; }
+  __device__ __forceinline__ static unsigned int make(uint64_t, uint64_t key, uint32_t t = 0,
+                                                      uint32_t db = 0) {
+    return ((unsigned int)key << db) | (db ? t : 0u);
+  }
   __device__ __forceinline__ static bool vacant(unsigned int w, uint64_t) { return w == kVacant; }
-  __device__ __forceinline__ static uint64_t key(unsigned int w) { return w; }
+  __device__ __forceinline__ static uint64_t key(unsigned int w, uint32_t db = 0) { return w >> db; }
+  __device__ __forceinline__ static uint32_t probe(unsigned int w, uint32_t db) {
+    return w & ((1u << db) - 1u);
+  }
 };
 
 // Priority claim of one key (deferred acceptance, smallest key wins):
@@ -48,15 +66,19 @@ __device__ __forceinline__ void place_key(const zen::DevFamily& fam, W* slots, u
   uint64_t cur = key;
   uint32_t t = 0;
   const uint32_t k = fam.k;
+  const uint32_t db = sizeof(W) == 4 ? fam.db : 0u;
   while (true) {
     const uint64_t c = slot_of(fam, cur, t, r1);
-    const W old = atomicMin(base + c, S::make(ew, cur));
+    const W old = atomicMin(base + c, S::make(ew, cur, t, db));
     if (S::vacant(old, ew)) break;  // empty or stale epoch: cur now holds c
-    const uint64_t ok = S::key(old);
+    const uint64_t ok = S::key(old, db);
     if (ok > cur) {  // cur displaced a larger key: it resumes after its first c
       cur = ok;
       uint32_t f = 0;
-      while (f < k && slot_of(fam, cur, f, r1) != c) ++f;
+      if (db)
+        f = S::probe(old, db);
+      else
+        while (f < k && slot_of(fam, cur, f, r1) != c) ++f;
       t = f + 1;
     } else {
       ++t;  // rejected by a smaller key
@@ -80,6 +102,7 @@ __device__ __forceinline__ void place_keys(const zen::DevFamily& fam, W* slots,
   uint32_t t[KPT];
   bool act[KPT];
   const uint32_t k = fam.k;
+  const uint32_t db = sizeof(W) == 4 ? fam.db : 0u;
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
     act[j] = (uint32_t)j < nvalid;
@@ -95,7 +118,7 @@ __device__ __forceinline__ void place_keys(const zen::DevFamily& fam, W* slots,
     for (int j = 0; j < KPT; ++j) {
       if (act[j]) {
         c[j] = slot_of(fam, cur[j], t[j], r1);
-        old[j] = atomicMin(base[j] + c[j], S::make(ew, cur[j]));
+        old[j] = atomicMin(base[j] + c[j], S::make(ew, cur[j], t[j], db));
       }
     }
     any = false;
@@ -106,11 +129,14 @@ __device__ __forceinline__ void place_keys(const zen::DevFamily& fam, W* slots,
         act[j] = false;
         continue;
       }
-      const uint64_t ok = S::key(old[j]);
+      const uint64_t ok = S::key(old[j], db);
       if (ok > cur[j]) {  // displaced a larger key: it resumes after its first c
         cur[j] = ok;
         uint32_t f = 0;
-        while (f < k && slot_of(fam, ok, f, r1) != c[j]) ++f;
+        if (db)
+          f = S::probe(old[j], db);
+        else
+          while (f < k && slot_of(fam, ok, f, r1) != c[j]) ++f;
         t[j] = f + 1;
       } else {
         ++t[j];

@@ -28,7 +28,17 @@ struct DevFamily {
   uint64_t sc[kMaxK];
   uint32_t n;
   uint32_t k;
+  uint32_t db;  // u32 slot words: low bits holding the claiming probe (0 = none)
 };
+
+// probe bits packed under the key in the BP pipeline's u32 slot words:
+// word = (index + 1) << db | probe.  Needs 2^db >= k and (m + 1) << db < 2^32;
+// otherwise 0 and the readers recompute the probe from the hashes.
+inline uint32_t slot_probe_bits(uint32_t k, uint64_t m) {
+  for (uint32_t db = 1; db <= 4; ++db)
+    if ((1u << db) >= k) return ((m + 1) << db) < 0xFFFFFFFFull ? db : 0u;
+  return 0u;
+}
 
 struct LookbackCtl {
   uint32_t ticket;
