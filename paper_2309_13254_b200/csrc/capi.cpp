@@ -1436,16 +1436,18 @@ namespace {
 // Byte layout of one node's receive arena (identical on every rank, so peers
 // can compute each other's sub-pointers from the base alone).
 struct ArenaLayout {
-  size_t inbox_idx = 0, inbox_val = 0, push_hdr = 0, pull_hdr = 0;
+  size_t inbox_idx = 0, inbox_val = 0, push_hdr = 0, pull_hdr = 0, inbox_gbase = 0;
   std::vector<size_t> pull_bits, pull_vals, pull_cbase;
   size_t bytes = 0;
 };
 
 ArenaLayout make_layout(uint32_t n, uint64_t cap, const std::vector<uint64_t>& nw,
                         const std::vector<uint64_t>& valcap, bool with_pull,
-                        uint64_t nchunks) {
+                        uint64_t nchunks, uint64_t ngroups) {
   ArenaLayout L;
   size_t off = 0;
+  L.inbox_gbase = off;  // [n workers][ngroups] entries before each 8-tile group
+  off += align256(size_t(n) * ngroups * 4);
   L.inbox_idx = off;
   off += align256(size_t(n) * cap * 4);
   L.inbox_val = off;
@@ -1479,6 +1481,7 @@ struct Arena {
   char* base = nullptr;
   bool owned = false;
   uint32_t* inbox_idx(const ArenaLayout& L) const { return (uint32_t*)(base + L.inbox_idx); }
+  uint32_t* inbox_gbase(const ArenaLayout& L) const { return (uint32_t*)(base + L.inbox_gbase); }
   float* inbox_val(const ArenaLayout& L) const { return (float*)(base + L.inbox_val); }
   PushHdr* push_hdr(const ArenaLayout& L) const { return (PushHdr*)(base + L.push_hdr); }
   PullHdr* pull_hdr(const ArenaLayout& L) const { return (PullHdr*)(base + L.pull_hdr); }
@@ -1504,6 +1507,7 @@ struct Server {
   uint32_t id = 0;
   AggArgs a{};
   uint64_t* agg_count = nullptr;
+  bool fused = false;  // dense syncs take k_agg_fused (local mode)
 };
 
 constexpr int kRing = 1024;
@@ -1515,6 +1519,7 @@ struct zen_bp {
   uint32_t n = 0, rank = 0;
   bool local = true;
   uint64_t m = 0, cap = 0, stride_cap = 0;
+  uint32_t ngroups = 0;  // 8-tile groups of the dense path (fused aggregate blocks)
   zen_hash_params params{};
   std::unique_ptr<zen_universe> uni;
   DevMem mem;
@@ -1604,6 +1609,9 @@ zen_status bp_alloc_worker(zen_bp* bp, Worker& w) {
   a.dst_idx = dst_idx;
   a.dst_val = dst_val;
   a.push_hdr = push_hdr;
+  uint32_t** dst_gbase;
+  CKR(mem.alloc(&dst_gbase, n));
+  a.dst_gbase = dst_gbase;
   HashHdr h{};
   h.derive = 1;
   h.r1_mult = bp->params.r1_multiplier;
@@ -1705,6 +1713,34 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   return ZEN_OK;
 }
 
+// fused aggregate: the static group table of every server and its
+// shared-memory span (the group entry bases are wired with the arenas)
+zen_status bp_setup_fused(zen_bp* bp) {
+  uint32_t* d_span;
+  CKR(bp->mem.alloc(&d_span, 1));
+  const uint32_t ntiles = bp->workers[0].a.xc.ntiles;
+  for (auto& s : bp->servers) {
+    AggArgs& a = s.a;
+    a.ntiles = ntiles;
+    a.ngroups = bp->ngroups;
+    uint4* gtab;
+    CKR(bp->mem.alloc(&gtab, size_t(a.ngroups) + 1));
+    a.gtab = gtab;
+    CKR(bp->mem.alloc(&a.lbf, a.ngroups));  // zeroed: no iteration tag matches
+    const uint32_t** ig;
+    CKR(bp->mem.alloc(&ig, bp->n));
+    a.in_gbase = ig;
+    CK(cudaMemsetAsync(d_span, 0, sizeof(uint32_t), bp->ctx->stream));
+    launch_agg_groups(a, d_span, bp->ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(bp->ctx->stream));
+    CK(cudaMemcpy(&a.span, d_span, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    a.span = std::max(a.span, 1u);
+    s.fused = agg_fused_smem(bp->n, a.span) <= 227 * 1024;  // (always at n <= 16)
+  }
+  return ZEN_OK;
+}
+
 // fill the device pointer tables once all arenas are known
 zen_status bp_wire(zen_bp* bp) {
   const uint32_t n = bp->n;
@@ -1722,6 +1758,10 @@ zen_status bp_wire(zen_bp* bp) {
     CKR(upload(const_cast<uint32_t**>(w.a.dst_idx), di.data(), n));
     CKR(upload(const_cast<float**>(w.a.dst_val), dv.data(), n));
     CKR(upload(const_cast<PushHdr**>(w.a.push_hdr), ph.data(), n));
+    std::vector<uint32_t*> dg(n);
+    for (uint32_t p = 0; p < n; ++p)
+      dg[p] = bp->arena_of(p).inbox_gbase(bp->layout_of(p)) + size_t(w.id) * bp->ngroups;
+    CKR(upload(const_cast<uint32_t**>(w.a.dst_gbase), dg.data(), n));
     // local mode: the servers read the workers' counters directly, so there
     // is no push header / signal kernel
     if (bp->local) w.a.push_hdr = nullptr;
@@ -1742,6 +1782,11 @@ zen_status bp_wire(zen_bp* bp) {
     CKR(upload(const_cast<const uint32_t**>(s.a.in_idx), ii.data(), n));
     CKR(upload(const_cast<const float**>(s.a.in_val), iv.data(), n));
     CKR(upload(const_cast<const PushHdr**>(s.a.in_hdr), ih.data(), n));
+    if (s.a.in_gbase) {
+      std::vector<const uint32_t*> ig(n);
+      for (uint32_t w = 0; w < n; ++w) ig[w] = A.inbox_gbase(L) + size_t(w) * bp->ngroups;
+      CKR(upload(const_cast<const uint32_t**>(s.a.in_gbase), ig.data(), n));
+    }
     if (bp->local) {
       CKR(upload(const_cast<const uint32_t**>(s.a.in_load), loads.data(), n));
       s.a.in_hdr = nullptr;
@@ -1832,8 +1877,9 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
     bp->nw[s] = (bp->uni->bs[s] + 63) / 64;
     bp->valcap[s] = std::min<uint64_t>(bp->uni->bs[s], uint64_t(n) * bp->cap);
   }
-  bp->L = make_layout(n, bp->cap, bp->nw, bp->valcap, true, bp->uni->nchunks);
-  bp->L0 = make_layout(n, bp->cap, bp->nw, bp->valcap, false, bp->uni->nchunks);
+  bp->ngroups = uint32_t(((bp->m + kExtractTile - 1) / kExtractTile + 7) / 8);
+  bp->L = make_layout(n, bp->cap, bp->nw, bp->valcap, true, bp->uni->nchunks, bp->ngroups);
+  bp->L0 = make_layout(n, bp->cap, bp->nw, bp->valcap, false, bp->uni->nchunks, bp->ngroups);
   CK(cudaStreamCreateWithFlags(&bp->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&bp->fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&bp->join, cudaEventDisableTiming));
@@ -1884,6 +1930,15 @@ zen_status zen_bp_create(zen_ctx* c, uint32_t n, uint32_t rank, uint64_t univers
       w.a.xc.mk_nws = d_nws;
     }
   }
+  // The fused aggregate (dense syncs) replaces mark + union + values by one
+  // kernel per server.  Measured (profiles/r07/fused_aggregate_ab.txt), it
+  // wins from 4 workers up -- 8 emulated on one GPU: aggregate 0.342 vs 0.408
+  // ms; rank mode N=4: 0.180 vs 0.184 ms -- and loses below (N=1: 0.121 vs
+  // 0.109 ms, N=2: 0.152 vs 0.143 ms: each block runs its phases back to back
+  // where the three kernels overlap them).  ZEN_AGG_FUSED=1 / =0 forces it.
+  const char* fz = std::getenv("ZEN_AGG_FUSED");
+  const bool fused = fz ? fz[0] == '1' : n >= 4;
+  if (fused) CKR(bp_setup_fused(bp.get()));
   // arenas
   bp->arenas.assign(n, Arena{});
   for (uint32_t r = 0; r < n; ++r) {
@@ -2090,7 +2145,7 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   // dense syncs in local mode: the push scatter already marked every entry
   const bool marked = from_dense && bp->local && !bp->workers.empty() &&
                       bp->workers[0].a.xc.mark;
-  for (auto& s : bp->servers) launch_aggregate(s.a, st, marked);
+  for (auto& s : bp->servers) launch_aggregate(s.a, st, marked, from_dense && s.fused);
   if (ev) CK(cudaEventRecordWithFlags(ev[3], st, cudaEventRecordExternal));
   bp->dec.launch(bp->da, st);
   if (ev) CK(cudaEventRecordWithFlags(ev[4], st, cudaEventRecordExternal));

@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
       key[q] = in[q] ? a.in_idx[w[q]][e[q]] : 0u;
     }
 #pragma unroll
-    for (int q = 0; q < R; ++q) ow[q] = a.own[in[q] ? key[q] >> 6 : 0];
+    for (int q = 0; q < R; ++q)  // (one server: I_0 is every index, rank = index)
+      ow[q] = n == 1 ? OwnWord{~0ull, key[q] & ~63u, 0u} : a.own[in[q] ? key[q] >> 6 : 0];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       if (base + q * stride >= total) break;  // warp-uniform
@@ -395,6 +396,284 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
       const uint64_t pos = wbase + k;
       if (pos < a.val_cap)
         for (uint32_t d = 0; d < a.ndst; ++d) a.dst_vals[d][pos] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------- fused aggregate ----
+// Dense syncs: mark + union + prefix + fold + pull in ONE kernel.  Block
+// g owns the 8 extraction tiles [8g, 8g + 8) -- indices [65536 g, 65536 (g+1))
+// -- whose I_s positions are [R0(g), R0(g+1)) (static: the universe chunk
+// prefixes).  It takes the bitmap words [jA, jB) with jA = ceil(R0 / 64), so
+// every word has one owner; the owner of a word that straddles two groups
+// also reads up to 63 entries past its own (the next group's first ones) and
+// skips its leading entries below 64 jA (the previous owner took them).
+//  * each worker's entries of the group are a contiguous run of its part,
+//    from the base its push scatter wrote for the group (no search);
+//  * presence rows in shared memory (warp-aggregated atomicOr), no global
+//    presence bitmaps, no clean-up stores;
+//  * one block scan gives every worker's and U's word prefixes; a decoupled
+//    look-back over the groups gives the block's first output position;
+//  * then the HashBitmap words, the folded values (worker order,
+//    zen/tensor.hpp:151-153) and the receivers' per-chunk value bases.
+constexpr int kFusedThreads = 256;
+constexpr uint32_t kFusedTiles = 8;  // tiles per group (65536 indices = 32 chunks)
+
+// setup: per group g in [0, ngroups]: R0, jA = ceil(R0 / 64) (nw at the end),
+// the first universe chunk c with cprefix >= 64 jA (nchunks at the end), and
+// the largest span jA(g + 1) - jA(g)
+__global__ void k_agg_groups(AggArgs a, uint32_t* span) {
+  zen_dev::pdl_entry();
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > a.ngroups) return;
+  auto jA_of = [&](uint32_t q, uint64_t* R0) {
+    const uint64_t r = q < a.ngroups ? (uint64_t)a.cprefix[(uint64_t)q * 32 * a.n + a.s] : a.bs;
+    if (R0) *R0 = r;
+    return q < a.ngroups ? (r + 63) / 64 : a.nw;
+  };
+  uint64_t R0;
+  const uint64_t jA = jA_of(g, &R0);
+  uint64_t cs = a.nchunks;
+  if (g < a.ngroups) {  // lower bound over the (nondecreasing) chunk prefixes
+    uint64_t lo = 0, hi = a.nchunks;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      if ((uint64_t)a.cprefix[mid * a.n + a.s] >= 64 * jA)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    cs = lo;
+    atomicMax(span, (uint32_t)(jA_of(g + 1, nullptr) - jA));
+  }
+  const_cast<uint4*>(a.gtab)[g] = make_uint4((uint32_t)R0, (uint32_t)jA, (uint32_t)cs, 0u);
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(kFusedThreads, 7) k_agg_fused(AggArgs a) {  // 7/SM: one wave at 64M
+  zen_dev::pdl_entry();
+  extern __shared__ unsigned long long fsm[];
+  __shared__ uint32_t s_lo[kMaxWorkers], s_skip[kMaxWorkers], s_off[kMaxWorkers + 1];
+  __shared__ uint32_t s_stop[kFusedThreads / 32], s_sum[kFusedThreads / 32];
+  __shared__ uint32_t s_wsum[33];
+  const uint32_t n = a.n, s = a.s, lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t WB = a.span;
+  unsigned long long* spw = fsm;                  // [n][WB] presence rows
+  unsigned long long* sU = fsm + (size_t)n * WB;  // [WB] union
+  uint32_t* spre = reinterpret_cast<uint32_t*>(sU + WB);  // [(n + 1) * WB] flat exclusive scan
+  for (uint32_t i = threadIdx.x; i < n * WB; i += kFusedThreads) spw[i] = 0ull;
+  if (threadIdx.x < n) s_skip[threadIdx.x] = 0;
+  __syncthreads();
+  // groups in block order: a block only waits on lower blocks, which were
+  // dispatched before it (the single-pass scan's usual assumption)
+  const uint32_t g = blockIdx.x;
+  const uint4 G0 = a.gtab[g], G1 = a.gtab[g + 1];
+  const uint32_t jA = G0.y, nwb = G1.y - G0.y;
+  const uint64_t rA = 64ull * jA, rB = 64ull * G1.y;
+  const bool ext = rB > (uint64_t)G1.x;  // the last word reaches into the next group
+  if (threadIdx.x < n) {  // worker w's entries of the group: [gbase[g], gbase[g + 1])
+    const uint32_t w = threadIdx.x;
+    const uint32_t cnt = part_count(a, w);
+    const uint32_t lo = a.in_gbase[w][g];
+    const uint32_t hi = g + 1 < a.ngroups ? a.in_gbase[w][g + 1] : cnt;
+    s_lo[w] = lo;
+    s_off[w + 1] = (hi - lo) + (ext ? min(64u, cnt - hi) : 0u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (uint32_t w = 0; w < n; ++w) {
+      const uint32_t l = s_off[w + 1];
+      s_off[w] = acc;
+      acc += l;
+    }
+    s_off[n] = acc;
+  }
+  __syncthreads();
+  // phase 1: entries -> presence bits (4 per thread per round, loads first)
+  const uint32_t E = s_off[n];
+  constexpr int R = 4;
+  for (uint32_t base = warp * 32; base < E; base += R * kFusedThreads) {  // warp-uniform
+    uint32_t w[R], key[R];
+    bool in[R];
+    OwnWord ow[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const uint32_t i = base + q * kFusedThreads + lane;
+      in[q] = i < E;
+      w[q] = 0;
+      if (in[q])
+        while (i >= s_off[w[q] + 1]) ++w[q];
+      key[q] = in[q] ? a.in_idx[w[q]][s_lo[w[q]] + (i - s_off[w[q]])] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q)  // (one server: I_0 is every index, rank = index)
+      ow[q] = n == 1 ? OwnWord{~0ull, key[q] & ~63u, 0u} : a.own[in[q] ? key[q] >> 6 : 0];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (base + q * kFusedThreads >= E) break;  // warp-uniform
+      bool live = in[q] && ((ow[q].mask >> (key[q] & 63u)) & 1ull);
+      if (in[q] && !live) {
+        atomicMin((unsigned long long*)&a.hdr->bad_index, (unsigned long long)key[q]);
+        atomicOr(&a.hdr->status, kErrOutside);
+      }
+      const uint64_t r = ow[q].prefix + (uint64_t)__popcll(ow[q].mask & lowmask64(key[q] & 63u));
+      if (live && r < rA) {
+        atomicAdd(&s_skip[w[q]], 1u);  // the previous group's last word
+        live = false;
+      }
+      live = live && r < rB;
+      unsigned long long* word = live ? spw + (size_t)w[q] * WB + (uint32_t)((r >> 6) - jA) : nullptr;
+      const uint64_t bit = live ? 1ull << (r & 63u) : 0ull;
+      const uint32_t grp = __match_any_sync(0xffffffffu, (unsigned long long)word);
+      const uint32_t lo = __reduce_or_sync(grp, (uint32_t)bit);
+      const uint32_t hi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
+      if (live && lane == (uint32_t)(__ffs(grp) - 1)) atomicOr(word, ((unsigned long long)hi << 32) | lo);
+    }
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < nwb; j += kFusedThreads) {
+    unsigned long long u = 0;
+    for (uint32_t w = 0; w < n; ++w) u |= spw[(size_t)w * WB + j];
+    sU[j] = u;
+  }
+  __syncthreads();
+  // phase 2: one exclusive scan over the rows [w0 .. w(n-1), U] of nwb words
+  const uint32_t L = (n + 1) * nwb;
+  const uint32_t per = (L + kFusedThreads - 1) / kFusedThreads;
+  const uint32_t f0 = min(threadIdx.x * per, L), f1 = min(f0 + per, L);
+  uint32_t sum = 0;
+  if (f0 < f1) {
+    uint32_t row = f0 / nwb, j = f0 - row * nwb;
+    for (uint32_t f = f0; f < f1; ++f) {
+      sum += __popcll(row < n ? spw[(size_t)row * WB + j] : sU[j]);
+      if (++j == nwb) { j = 0; ++row; }
+    }
+  }
+  uint32_t tot;
+  uint32_t run = block_exclusive_sum(sum, s_wsum, &tot);
+  if (f0 < f1) {
+    uint32_t row = f0 / nwb, j = f0 - row * nwb;
+    for (uint32_t f = f0; f < f1; ++f) {
+      spre[(size_t)row * WB + j] = run;
+      run += __popcll(row < n ? spw[(size_t)row * WB + j] : sU[j]);
+      if (++j == nwb) { j = 0; ++row; }
+    }
+  }
+  __syncthreads();
+  const uint32_t urow = n * WB;
+  const uint32_t ub0 = nwb ? spre[urow] : tot;  // flat prefix where the U row starts
+  // phase 3: decoupled look-back over the groups -> the block's first position.
+  // The whole block reads 256 predecessors per round (nearest first) and stops
+  // at the nearest one that already holds its inclusive prefix.
+  const uint32_t utot = tot - ub0;
+  const unsigned long long tag =
+      (unsigned long long)(*(volatile uint32_t*)&a.hdr->iter & 0x3FFFFFFFu) << 34;
+  // (relaxed: the look-back consumes nothing but these words themselves)
+  if (threadIdx.x == 0) st_relaxed_gpu(&a.lbf[g], tag | ((g == 0 ? 2ull : 1ull) << 32) | utot);
+  uint32_t excl = 0;
+  // One worker: U is its own part, so the groups before g hold exactly the
+  // part's entries before g -- the push scatter's base -- and no look-back.
+  if (n == 1) excl = s_lo[0];
+  for (int64_t k = n == 1 ? 0 : g; k > 0; k -= kFusedThreads) {  // block-uniform
+    const int64_t idx = k - 1 - (int64_t)threadIdx.x;
+    unsigned long long v = tag | (2ull << 32);  // before group 0: inclusive 0
+    if (idx >= 0) {
+      do {
+        v = ld_relaxed_gpu(&a.lbf[idx]);
+      } while ((v >> 34) != (tag >> 34) || ((v >> 32) & 3ull) == 0);
+    }
+    const uint32_t incl = __ballot_sync(0xffffffffu, ((v >> 32) & 3ull) == 2);
+    if (lane == 0) s_stop[warp] = incl ? warp * 32 + (uint32_t)(__ffs(incl) - 1) : 0xFFFFFFFFu;
+    __syncthreads();
+    uint32_t stop = 0xFFFFFFFFu;
+#pragma unroll
+    for (int q = 0; q < kFusedThreads / 32; ++q) stop = min(stop, s_stop[q]);
+    const uint32_t part = __reduce_add_sync(0xffffffffu, threadIdx.x <= stop ? (uint32_t)v : 0u);
+    if (lane == 0) s_sum[warp] = part;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kFusedThreads / 32; ++q) excl += s_sum[q];
+    __syncthreads();  // s_stop / s_sum reuse
+    if (stop != 0xFFFFFFFFu) break;
+  }
+  if (threadIdx.x == 0 && g != 0) st_relaxed_gpu(&a.lbf[g], tag | (2ull << 32) | (excl + utot));
+  // phase 4a: the HashBitmap words
+  for (uint32_t j = threadIdx.x; j < nwb; j += kFusedThreads)
+    for (uint32_t d = 0; d < a.ndst; ++d) a.dst_bits[d][jA + j] = sU[j];
+  // phase 4b: the receivers' value base per universe chunk
+  for (uint32_t c = G0.z + threadIdx.x; c < G1.z; c += kFusedThreads) {
+    const uint64_t P = a.cprefix[(uint64_t)c * n + s];
+    uint32_t b = excl + utot;
+    if (P < rB) {
+      const uint32_t lj = (uint32_t)((P >> 6) - jA);
+      b = excl + (spre[urow + lj] - ub0) + (uint32_t)__popcll(sU[lj] & lowmask64((uint32_t)(P & 63)));
+    }
+    for (uint32_t d = 0; d < a.ndst; ++d) a.dst_cbase[d][c] = b;
+  }
+  if (g == a.ngroups - 1 && threadIdx.x == 0) {
+    for (uint32_t d = 0; d < a.ndst; ++d) a.dst_cbase[d][a.nchunks] = excl + utot;
+    *a.agg_count = excl + utot;
+  }
+  // phase 4c: values, warps over 32-word spans; lanes expand set bits together
+  for (uint32_t j0 = warp * 32; j0 < nwb; j0 += kFusedThreads) {
+    const uint32_t j = j0 + lane;
+    const unsigned long long U = j < nwb ? sU[j] : 0ull;
+    const uint32_t c = __popcll(U);
+    const uint32_t inc = warp_inclusive_sum(c);
+    const uint32_t x = inc - c;
+    const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+    const uint64_t wbase = (uint64_t)excl + (spre[urow + j0] - ub0);
+    constexpr int B = NMAX <= 2 ? 4 : (NMAX <= 4 ? 2 : 1);  // expansions in flight per lane
+    for (uint32_t k0 = 0; k0 < T; k0 += 32 * B) {  // warp-uniform
+      float t[B][NMAX];
+      uint32_t pres[B];
+      uint64_t pos[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const uint32_t k = k0 + b * 32 + lane;
+        uint32_t Lw = 0;
+#pragma unroll
+        for (uint32_t step = 16; step >= 1; step >>= 1) {
+          const uint32_t xc = __shfl_sync(0xffffffffu, x, Lw + step);
+          if (xc <= k) Lw += step;
+        }
+        const unsigned long long UL = __shfl_sync(0xffffffffu, U, Lw);
+        const uint32_t xL = __shfl_sync(0xffffffffu, x, Lw);
+        pres[b] = 0;
+        pos[b] = wbase + k;
+        if (k < T) {
+          const uint32_t bit = (UL == ~0ull) ? k - xL : select64(UL, k - xL);
+          const uint64_t lm = lowmask64(bit);
+          const uint32_t jj = j0 + Lw;
+#pragma unroll
+          for (int w = 0; w < NMAX; ++w) {
+            if (w >= (int)n) break;
+            const unsigned long long pwv = spw[(size_t)w * WB + jj];
+            if ((pwv >> bit) & 1ull) {  // every present worker's value load issued first
+              const uint32_t e = s_lo[w] + s_skip[w] +
+                                 (spre[(size_t)w * WB + jj] - spre[(size_t)w * WB]) +
+                                 (uint32_t)__popcll(pwv & lm);
+              t[b][w] = a.in_val[w][e];
+              pres[b] |= 1u << w;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (!pres[b]) continue;
+        float v = 0.0f;
+        bool seen = false;
+#pragma unroll
+        for (int w = 0; w < NMAX; ++w)
+          if ((pres[b] >> w) & 1u) {  // worker order (zen/tensor.hpp:151-153)
+            v = seen ? v + t[b][w] : t[b][w];
+            seen = true;
+          }
+        if (pos[b] < a.val_cap)
+          for (uint32_t d = 0; d < a.ndst; ++d) a.dst_vals[d][pos[b]] = v;
+      }
     }
   }
 }
@@ -709,7 +988,32 @@ void launch_tables_own(uint64_t m, uint32_t n, uint32_t s, uint32_t nplanes,
   count_launch();
 }
 
-void launch_aggregate(const AggArgs& a, cudaStream_t stream, bool marked) {
+void launch_agg_groups(const AggArgs& a, uint32_t* span, cudaStream_t stream) {
+  launch_k(k_agg_groups, (a.ngroups + 1 + 255) / 256, 256, 0, stream, a, span);
+  count_launch();
+}
+
+void launch_aggregate(const AggArgs& a, cudaStream_t stream, bool marked, bool fused) {
+  if (fused) {
+    if (a.wait_push) {
+      launch_k(k_wait_push, 1, 32, 0, stream, a);
+      count_launch();
+    }
+    const size_t sm = agg_fused_smem(a.n, a.span);
+    auto kern = a.n <= 1 ? k_agg_fused<1>
+              : a.n <= 2 ? k_agg_fused<2>
+              : a.n <= 4 ? k_agg_fused<4>
+              : a.n <= 8 ? k_agg_fused<8> : k_agg_fused<16>;
+    if (sm > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(kern, a.ngroups, kFusedThreads, sm, stream, a);
+    count_launch();
+    if (a.dst_hdr) {
+      launch_k(k_agg_signal, 1, 32, 0, stream, a);
+      count_launch();
+    }
+    return;
+  }
   // a.pw is all-zero here: zeroed at allocation, re-zeroed by k_agg_values
   if (a.wait_push && !a.gate) {
     launch_k(k_wait_push, 1, 32, 0, stream, a);

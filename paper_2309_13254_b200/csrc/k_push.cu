@@ -26,6 +26,8 @@
 // pass, k_hash.cu) runs on the side stream, off the critical path.  Before it:
 // k_bp_begin (first kernel of a sync: header + counter reset, its latency
 // hidden under the extraction's first loads).
+#include <cstdlib>
+
 #include "zen_common.cuh"
 #include "zen_hash_dev.cuh"
 
@@ -177,7 +179,10 @@ __global__ void __launch_bounds__(kPushThreads)
         for (uint32_t i = lane; i < sup; i += 32) acc += sc[i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) s_base[p] = acc;
+        if (lane == 0) {
+          s_base[p] = acc;
+          if (a.dst_gbase) a.dst_gbase[p][g] = (uint32_t)acc;  // owner p's range of this group
+        }
       }
     }
     __syncthreads();
@@ -435,6 +440,111 @@ __global__ void __launch_bounds__(kPushThreads) k_place_tiles(HashArgs<K> a) {
   }
 }
 
+// Two-phase claims (default): every entry of a 1024-entry round makes its
+// FIRST claim (four atomics in flight per thread); only the entries that were
+// rejected or displaced a key -- a minority at the reference's load factor --
+// are compacted into a shared-memory list and continue (place_from), so a
+// warp no longer runs until the longest chain among its 128 keys ends with
+// most lanes idle.  Same protocol, same matching (schedule-independent).
+template <typename K>
+__global__ void __launch_bounds__(kPushThreads) k_place_tiles2(HashArgs<K> a) {
+  zen_dev::pdl_entry();
+  using W = SlotOf<K>;
+  using S = Slot<W>;
+  __shared__ uint32_t s_tpre[kPushTiles + 1];
+  __shared__ uint32_t s_group, s_np[2];  // pending counts, alternating rounds
+  __shared__ uint32_t s_key[kPushRound];  // pending: key (index + 1)
+  __shared__ uint16_t s_pt[kPushRound];   // pending: partition << 5 | next probe
+  const PushCounts& x = a.xc;
+  HashHdr* h = a.hdr;
+  if (h->status & kErrCapacity) return;
+  const K* st = static_cast<const K*>(x.st_idx);
+  const uint32_t n = a.fam.n, k = a.fam.k, warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t db = sizeof(W) == 4 ? a.fam.db : 0u;
+  const uint64_t r1 = h->r1, stride = h->stride;
+  const uint64_t ew = epoch_word(h->epoch);
+  const uint32_t ngroups = (x.ntiles + kPushTiles - 1) / kPushTiles;
+  if (threadIdx.x == 0) s_np[0] = s_np[1] = 0;
+  uint32_t par = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_group = atomicAdd(&h->work[1], 1u);
+    __syncthreads();
+    const uint32_t g = s_group;
+    if (g >= ngroups) break;
+    const uint32_t t0 = g * kPushTiles;
+    if (warp == 0) group_prefix(x, n, t0, s_tpre);
+    __syncthreads();
+    const uint32_t T = s_tpre[kPushTiles];
+    for (uint32_t e0 = 0; e0 < T; e0 += kPushRound) {
+      uint64_t key[kPushPer];
+      uint32_t part[kPushPer], c[kPushPer];
+      W old[kPushPer];
+      bool v[kPushPer];
+#pragma unroll
+      for (int j = 0; j < kPushPer; ++j) {
+        const uint32_t e = e0 + j * kPushThreads + threadIdx.x;
+        v[j] = e < T;
+        key[j] = v[j] ? (uint64_t)st[group_src(s_tpre, t0, e)] + 1 : 0ull;
+      }
+#pragma unroll
+      for (int j = 0; j < kPushPer; ++j) {
+        part[j] = (v[j] && n > 1) ? part_of(a.fam, key[j]) : 0u;
+        if (v[j]) {
+          c[j] = (uint32_t)slot_of(a.fam, key[j], 0, r1);
+          old[j] = atomicMin(a.slots + (uint64_t)part[j] * stride + c[j], S::make(ew, key[j], 0, db));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kPushPer; ++j) {
+        uint64_t nk = key[j];
+        uint32_t nt = 1;
+        bool go = v[j] && !S::vacant(old[j], ew);
+        if (go) {
+          const uint64_t ok = S::key(old[j], db);
+          if (ok > key[j]) {  // displaced a larger key: it resumes after its first c
+            nk = ok;
+            uint32_t f = 0;
+            if (db)
+              f = S::probe(old[j], db);
+            else
+              while (f < k && slot_of(a.fam, ok, f, r1) != c[j]) ++f;
+            nt = f + 1;
+          }
+          go = nt < k;  // else: ends serial
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, go);
+        uint32_t b = 0;
+        if (bal && lane == 0) b = atomicAdd(&s_np[par], (uint32_t)__popc(bal));
+        b = __shfl_sync(0xffffffffu, b, 0) + __popc(bal & lanemask_lt());
+        if (go) {
+          s_key[b] = (uint32_t)nk;
+          s_pt[b] = (uint16_t)((part[j] << 5) | nt);
+        }
+      }
+      __syncthreads();
+      const uint32_t np = s_np[par];
+      if (threadIdx.x == 0) s_np[par ^ 1] = 0;  // the next round's (its pushes follow a barrier)
+      for (uint32_t i0 = 0; i0 < np; i0 += 2 * kPushThreads) {
+        uint64_t cur[2];
+        uint32_t t[2], pp[2], nv = 0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t i = i0 + j * kPushThreads + threadIdx.x;  // valid items: a prefix in j
+          cur[j] = i < np ? s_key[i] : 0ull;
+          const uint32_t q = i < np ? s_pt[i] : 0u;
+          pp[j] = q >> 5;
+          t[j] = q & 31u;
+          nv += i < np ? 1u : 0u;
+        }
+        place_from<2>(a.fam, a.slots, cur, t, pp, nv, r1, stride, ew);
+      }
+      __syncthreads();  // the list is consumed
+      par ^= 1;
+    }
+    __syncthreads();  // s_tpre / s_group / s_np reuse
+  }
+}
+
 }  // namespace
 
 template <typename K>
@@ -456,8 +566,9 @@ void launch_push_scatter(const HashArgs<K>& a, const ExtractWs<K>& ws, cudaStrea
 template <typename K>
 void launch_place_tiles(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm) {
   const unsigned groups = (a.xc.ntiles + kPushTiles - 1) / kPushTiles;
-  launch_k(k_place_tiles<K>, std::max(1u, std::min(groups, 148u * ctas_per_sm)), kPushThreads, 0,
-           stream, a);
+  static const bool v1 = std::getenv("ZEN_PLACE_V1") != nullptr;  // (A/B: one-phase claims)
+  launch_k(v1 ? k_place_tiles<K> : k_place_tiles2<K>,
+           std::max(1u, std::min(groups, 148u * ctas_per_sm)), kPushThreads, 0, stream, a);
   count_launch();
 }
 

@@ -147,6 +147,59 @@ __device__ __forceinline__ void place_keys(const zen::DevFamily& fam, W* slots,
   }
 }
 
+// Continuation of claims already under way: item j is key cur[j] of
+// partition part[j] about to try probe t[j] (same protocol as place_keys).
+template <int KPT, typename W>
+__device__ __forceinline__ void place_from(const zen::DevFamily& fam, W* slots, uint64_t (&cur)[KPT],
+                                           uint32_t (&t)[KPT], const uint32_t (&part)[KPT],
+                                           uint32_t nvalid, uint64_t r1, uint64_t stride,
+                                           uint64_t ew) {
+  using S = Slot<W>;
+  W* base[KPT];
+  bool act[KPT];
+  const uint32_t k = fam.k;
+  const uint32_t db = sizeof(W) == 4 ? fam.db : 0u;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    act[j] = (uint32_t)j < nvalid && t[j] < k;
+    base[j] = slots + (act[j] ? (uint64_t)part[j] * stride : 0ull);
+  }
+  bool any = true;
+  while (any) {
+    uint64_t c[KPT];
+    W old[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+      if (act[j]) {
+        c[j] = slot_of(fam, cur[j], t[j], r1);
+        old[j] = atomicMin(base[j] + c[j], S::make(ew, cur[j], t[j], db));
+      }
+    any = false;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      if (!act[j]) continue;
+      if (S::vacant(old[j], ew)) {
+        act[j] = false;
+        continue;
+      }
+      const uint64_t ok = S::key(old[j], db);
+      if (ok > cur[j]) {
+        cur[j] = ok;
+        uint32_t f = 0;
+        if (db)
+          f = S::probe(old[j], db);
+        else
+          while (f < k && slot_of(fam, ok, f, r1) != c[j]) ++f;
+        t[j] = f + 1;
+      } else {
+        ++t[j];
+      }
+      if (t[j] >= k) act[j] = false;
+      any |= act[j];
+    }
+  }
+}
+
 // meta word of a key after the post pass: partition (9 bits), depth (5),
 // stable rank in its 256-key tile among same-partition keys (8) and among
 // same-partition serial keys (8).

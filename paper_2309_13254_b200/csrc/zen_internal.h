@@ -196,6 +196,8 @@ struct HashArgs {
   uint64_t stride_cap;        // r1 + r2 capacity of the hash memory
   // push signalling (pipeline): headers in each server's inbox
   PushHdr* const* push_hdr;   // [n] or nullptr
+  uint32_t* const* dst_gbase; // [n] owner p's row for this worker: entries before each
+                              // 8-tile group (the fused aggregate's ranges) or nullptr
   uint32_t me;
   int peer;                   // destinations include other GPUs (system-scope release)
   PushCounts xc;              // dense data path (zero-initialised otherwise)
@@ -306,10 +308,22 @@ struct AggArgs {
   uint32_t* const* dst_cbase;     // [ndst] -> (nchunks + 1) u32 per receiver
   int pre_min;                    // value bases come from the scatter's atomicMin marks:
                                   // reset each word read to ~0 (ZEN_SCATTER_MARK=1)
+  // Fused aggregate (local mode, dense syncs; k_agg_fused): one block per 8
+  // extraction tiles (65536 indices) does mark + union + prefix + fold.
+  const uint32_t* const* in_gbase; // [n] worker w's entries before each group (its push scatter)
+  uint32_t ntiles;                 // extraction tiles
+  uint32_t ngroups;                // ceil(ntiles / 8): the fused grid
+  const uint4* gtab;               // [ngroups + 1] {R0, jA, first chunk, 0} (k_agg_groups)
+  uint32_t span;                   // max bitmap words of one group (shared-memory rows)
+  unsigned long long* lbf;         // [ngroups] look-back words (iteration-tagged)
 };
+// static group table of the fused aggregate (setup): gtab, and *span
+void launch_agg_groups(const AggArgs& a, uint32_t* span, cudaStream_t stream);
+inline size_t agg_fused_smem(uint32_t n, uint32_t span) { return size_t(12) * (n + 1) * span + 16; }
 // marked: the presence bitmaps and value bases were already written by the
 // push scatter (local mode, dense syncs), so k_agg_mark is skipped
-void launch_aggregate(const AggArgs& a, cudaStream_t stream, bool marked = false);
+void launch_aggregate(const AggArgs& a, cudaStream_t stream, bool marked = false,
+                      bool fused = false);
 
 // decode of all servers' HashBitmap messages into the global sorted result
 struct DecodeArgs {

@@ -379,6 +379,44 @@ def test_bp_dense_pipeline_rows(zen, co):
     np.testing.assert_array_equal(bits(hv[:c]), bits(want.val))
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("n", [1, 2, 5])
+def test_bp_dense_aggregate_paths(zen, co, monkeypatch, fused, n):
+    """Both aggregates of the dense path -- the fused one-block-per-8-tiles kernel
+    (k_agg_fused, group ranges from the push scatter + look-back) and the
+    three-kernel mark/union/values -- against the oracle, on a universe whose
+    size is not a multiple of the group, the word or the chunk (so the groups'
+    words straddle and the last group is partial)."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("ZEN_AGG_FUSED", fused)
+    rows, d = 30_011, 17
+    m = rows * d
+    rng = np.random.default_rng(40 + n)
+    dense, pairs = [], []
+    core = rng.choice(rows, 300, replace=False)
+    for w in range(n):
+        live = np.unique(np.concatenate([core, rng.choice(rows, 900, replace=False)]))
+        g = np.zeros((rows, d), np.float32)
+        g[live] = rng.integers(1, 17, (live.size, d)).astype(np.float32)
+        g.ravel()[rng.choice(m, 2000, replace=False)] = 3.0  # scattered singletons
+        dense.append(torch.from_numpy(g.ravel()).cuda())
+        pairs.append(co.to_sparse(g.ravel()))
+    # (the reference's BP needs n >= 2, zen/schemes.hpp:66; n = 1 is the input itself)
+    want = co.bp_sync(m, pairs, seed=1) if n > 1 else None
+    want_idx, want_val = (want.idx, want.val) if n > 1 else pairs[0]
+    bp = zen.BPSynchronizer(n, m, max_nnz=m // 4)
+    for _ in range(3):  # eager, then graph replays (look-back tags per sync)
+        bp.sync_dense(dense)
+        bp.wait()
+        oi, ov = bp.result()
+        np.testing.assert_array_equal(oi.cpu().numpy().view(np.uint64), want_idx)
+        np.testing.assert_array_equal(bits(ov.cpu().numpy()), bits(want_val))
+        if n > 1:
+            led, counts, agg = bp.ledger()
+            np.testing.assert_array_equal(led, want.ledger)
+            np.testing.assert_array_equal(agg, want.agg_counts)
+
+
 def test_bp_single_worker_pipeline(zen, co):
     """n = 1 (the 1-GPU bench case): extraction + hash + self aggregate/encode/decode."""
     torch = pytest.importorskip("torch")

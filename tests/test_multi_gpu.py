@@ -83,8 +83,11 @@ def _ngpus():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("fused", [None, "1"])
 @pytest.mark.parametrize("shape", [(20000, 64, 0.01), (100000, 64, 0.01)])
-def test_bp_multi_gpu_parity(shape):
+def test_bp_multi_gpu_parity(shape, fused):
+    """fused="1": the one-kernel aggregate in rank mode (its group ranges are
+    written by the peers' push scatters into this rank's arena)."""
     n = min(_ngpus(), 4)
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -92,7 +95,10 @@ def test_bp_multi_gpu_parity(shape):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
            f"--nproc-per-node={n}", os.path.join(ROOT, "tests", "mgpu_worker.py"),
            str(rows), str(width), str(density)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ)
+    if fused:
+        env["ZEN_AGG_FUSED"] = fused
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MGPU OK" in r.stdout
 
