@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
       uint32_t prev_j = __shfl_up_sync(0xffffffffu, jw, 1);
       if (in[q] && owned && (lane == 0 || prev_w != w[q]) && e[q] > 0) {
         const uint32_t pk = a.in_idx[w[q]][e[q] - 1];  // previous entry of the same part
-        const OwnWord po = a.own[pk >> 6];
+        const OwnWord po = n == 1 ? OwnWord{~0ull, pk & ~63u, 0u} : a.own[pk >> 6];
         prev_w = w[q];
         prev_j = (po.prefix + (uint32_t)__popcll(po.mask & lowmask64(pk & 63u))) >> 6;
       }

@@ -187,6 +187,39 @@ __global__ void __launch_bounds__(kPushThreads)
     }
     __syncthreads();
     T = s_tpre[kPushTiles];
+    if (!REORDER && n == 1 && !x.mark) {
+      // one partition: the stable split is the identity, entry e of the group
+      // goes to base + e -- a plain gather-copy, no ranks, no barriers
+      const uint64_t b0 = s_base[0];
+      for (uint32_t e0 = threadIdx.x; e0 < T; e0 += kPushRound) {
+        K xv[kPushPer];
+        float vv[kPushPer];
+#pragma unroll
+        for (int j = 0; j < kPushPer; ++j) {
+          const uint32_t e = e0 + j * kPushThreads;
+          if (e < T) {
+            const uint64_t src = group_src(s_tpre, t0, e);
+            xv[j] = st_idx[src];
+            vv[j] = st_val[src];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kPushPer; ++j) {
+          const uint32_t e = e0 + j * kPushThreads;
+          const uint64_t pos = b0 + e;
+          if (e < T) {
+            if (pos < a.dst_cap) {
+              a.dst_idx[0][pos] = xv[j];
+              a.dst_val[0][pos] = vv[j];
+            } else {
+              atomicOr(&h->status, kErrCapacity);
+            }
+            if (pos == lim) atomicMin((unsigned long long*)&h->ovf_word, ((uint64_t)xv[j] + 1) << 16);
+          }
+        }
+      }
+      continue;  // the loop head's barrier orders the next group's shared writes
+    }
     if (!REORDER) {
       // lane p < n keeps partition p's running offset; rounds are pipelined
       uint32_t run = 0;
