@@ -1688,6 +1688,7 @@ zen_status bp_alloc_server(zen_bp* bp, Server& s) {
   a.in_load = in_load;
   a.in_count = nullptr;
   a.own = bp->uni->own[s.id];
+  a.whole = n == 1 ? 1 : 0;
   a.bs = bp->uni->bs[s.id];
   CKR(alloc_agg_ws(mem, a, n, a.bs));
   a.ndst = bp->local ? 1 : n;

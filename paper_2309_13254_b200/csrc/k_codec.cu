@@ -173,8 +173,8 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
       key[q] = in[q] ? a.in_idx[w[q]][e[q]] : 0u;
     }
 #pragma unroll
-    for (int q = 0; q < R; ++q)  // (one server: I_0 is every index, rank = index)
-      ow[q] = n == 1 ? OwnWord{~0ull, key[q] & ~63u, 0u} : a.own[in[q] ? key[q] >> 6 : 0];
+    for (int q = 0; q < R; ++q)  // (a one-server universe: I_0 is every index, rank = index)
+      ow[q] = a.whole ? OwnWord{~0ull, key[q] & ~63u, 0u} : a.own[in[q] ? key[q] >> 6 : 0];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       if (base + q * stride >= total) break;  // warp-uniform
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
       uint32_t prev_j = __shfl_up_sync(0xffffffffu, jw, 1);
       if (in[q] && owned && (lane == 0 || prev_w != w[q]) && e[q] > 0) {
         const uint32_t pk = a.in_idx[w[q]][e[q] - 1];  // previous entry of the same part
-        const OwnWord po = n == 1 ? OwnWord{~0ull, pk & ~63u, 0u} : a.own[pk >> 6];
+        const OwnWord po = a.whole ? OwnWord{~0ull, pk & ~63u, 0u} : a.own[pk >> 6];
         prev_w = w[q];
         prev_j = (po.prefix + (uint32_t)__popcll(po.mask & lowmask64(pk & 63u))) >> 6;
       }
@@ -507,8 +507,8 @@ __global__ void __launch_bounds__(kFusedThreads, 7) k_agg_fused(AggArgs a) {  //
       key[q] = in[q] ? a.in_idx[w[q]][s_lo[w[q]] + (i - s_off[w[q]])] : 0u;
     }
 #pragma unroll
-    for (int q = 0; q < R; ++q)  // (one server: I_0 is every index, rank = index)
-      ow[q] = n == 1 ? OwnWord{~0ull, key[q] & ~63u, 0u} : a.own[in[q] ? key[q] >> 6 : 0];
+    for (int q = 0; q < R; ++q)  // (a one-server universe: I_0 is every index, rank = index)
+      ow[q] = a.whole ? OwnWord{~0ull, key[q] & ~63u, 0u} : a.own[in[q] ? key[q] >> 6 : 0];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       if (base + q * kFusedThreads >= E) break;  // warp-uniform
@@ -692,11 +692,8 @@ __global__ void k_agg_signal(AggArgs a) {
     a.dst_hdr[d]->agg_count = u;
     a.dst_hdr[d]->status = st;
     a.dst_hdr[d]->bad_index = bad;
+    st_release_sys(&a.dst_hdr[d]->flag, (unsigned long long)iter);  // orders the three above
   }
-  __syncthreads();
-  __threadfence_system();
-  for (uint32_t d = threadIdx.x; d < a.ndst; d += blockDim.x)
-    st_release_sys(&a.dst_hdr[d]->flag, (unsigned long long)iter);
 }
 
 // Rank mode: ONE warp waits for the n peers' flags (lane w polls flag w), so

@@ -269,17 +269,17 @@ __global__ void k_push_signal(HashArgs<K> a) {
   const uint64_t ovf = *(volatile uint64_t*)&h->ovf_word;
   const uint32_t st = *(volatile uint32_t*)&h->status;
   const uint64_t z = h->count;
+  const uint32_t iter = h->iter;
   for (uint32_t s = threadIdx.x; s < n; s += blockDim.x) {
     PushHdr* ph = a.push_hdr[s];
     ph->nnz = z;
     ph->ovf_word = ovf;
     ph->status = st;
     for (uint32_t q = 0; q < n; ++q) ph->counts[q] = cap_ok ? a.load[q] : 0u;
+    // the release orders this thread's header stores before the flag (no
+    // second fence: the same thread wrote them)
+    st_release_sys(&ph->flag, (unsigned long long)iter);
   }
-  __syncthreads();
-  fence_for(a.peer);
-  for (uint32_t s = threadIdx.x; s < n; s += blockDim.x)
-    st_release_sys(&a.push_hdr[s]->flag, (unsigned long long)h->iter);
 }
 
 // ------------------------------------------------------------- side path ----

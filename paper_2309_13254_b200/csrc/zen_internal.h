@@ -306,6 +306,7 @@ struct AggArgs {
   uint64_t nchunks;               // ceil(M / 2048)
   const unsigned long long* own_bits;  // this server's local copy of U (a dst_bits entry)
   uint32_t* const* dst_cbase;     // [ndst] -> (nchunks + 1) u32 per receiver
+  int whole;                      // the universe has one server: rank in I_0 = index (no own table)
   int pre_min;                    // value bases come from the scatter's atomicMin marks:
                                   // reset each word read to ~0 (ZEN_SCATTER_MARK=1)
   // Fused aggregate (local mode, dense syncs; k_agg_fused): one block per 8
