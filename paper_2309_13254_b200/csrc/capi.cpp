@@ -2107,13 +2107,14 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     CK(cudaEventRecord(bp->fork, st));
     CK(cudaStreamWaitEvent(bp->side, bp->fork, 0));
     // Programmatic launch inside the side chain (claims -> depth -> replay)
-    // measured faster with several local workers (8 emulated 1.057 -> 1.007
-    // ms, 10 % N=1 0.361 -> 0.352) and slower otherwise (1 % N=1 0.1060 ->
+    // measured faster with several local workers or many keys (8 emulated
+    // 1.057 -> 1.007 ms, 10 % N=1 0.361 -> 0.352) and slower otherwise (1 % N=1 0.1060 ->
     // 0.1073, rank N=2 0.138 -> 0.149, N=4 0.178 -> 0.186: the early-launched
     // blocks hold SM slots the critical path needs); profiles/r07/side_pdl_ab.txt
     static const char* spdl = std::getenv("ZEN_SIDE_PDL");  // (=0/1 forces it)
     static const char* sprio = std::getenv("ZEN_SIDE_PRIO");
-    const bool side_pdl = spdl ? spdl[0] == '1' : (bp->local && bp->n > 1);
+    // (one worker: taken at large key capacities, where the claims run long)
+    const bool side_pdl = spdl ? spdl[0] == '1' : (bp->local && (bp->n > 1 || bp->cap >= (4u << 20)));
     LaunchScope low(side_pdl, /*low_priority=*/!(sprio && sprio[0] == '0'));
     // claims (dense: straight from the extraction staging) + table-scan depth
     // pass (CollisionStats) + the data-dependent fallback replay
