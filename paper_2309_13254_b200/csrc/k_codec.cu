@@ -134,6 +134,11 @@ __device__ __forceinline__ uint32_t part_count(const AggArgs& a, uint32_t w) {
   return (uint32_t)a.in_count[w];
 }
 
+// one worker, one-server universe, no scatter marks: U is the worker's row
+__device__ __forceinline__ bool solo_part(const AggArgs& a) {
+  return a.whole && a.n == 1 && !a.pre_min;
+}
+
 // Phase 1: every received entry sets its HashBitmap position (its rank in I_s,
 // zen/codec.hpp:146-158) in its worker's presence bitmap.
 __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
@@ -195,6 +200,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_mark(AggArgs a) {
       // The part is ascending, so its entries in bitmap word j are consecutive:
       // the first of them is at part index = worker w's popcount prefix at j,
       // which the fold needs -- written here instead of scanned later.
+      if (solo_part(a)) continue;  // (no value bases: the union copies the values)
       const uint32_t jw = owned ? (r >> 6) : 0xFFFFFFFFu;
       uint32_t prev_w = __shfl_up_sync(0xffffffffu, w[q], 1);
       uint32_t prev_j = __shfl_up_sync(0xffffffffu, jw, 1);
@@ -259,6 +265,34 @@ __global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
     }
     // the union bitmap (the HashBitmap: LSB-first = little-endian words)
     for (uint32_t d = 0; d < a.ndst; ++d) store8(a.dst_bits[d] + j0, U);
+    if (solo_part(a)) {  // the last reader of the presence row: clean it for the next sync
+      bool any = false;
+#pragma unroll
+      for (int i = 0; i < kWPT; ++i) any |= U[i] != 0ull;
+      if (any) {
+        unsigned long long z[kWPT];
+#pragma unroll
+        for (int i = 0; i < kWPT; ++i) z[i] = 0ull;
+        store8(a.pw + j0, z);
+      }
+    }
+  }
+  if (solo_part(a)) {
+    // One worker of a one-server universe: U = its presence row, so the U rank
+    // of entry e's bit is e itself and the folded values are the part's values
+    // in order -- the fold is a copy, done here (no dependence on the prefix).
+    const uint64_t cnt = min((uint64_t)part_count(a, 0), a.val_cap);
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const float* src = a.in_val[0];
+    for (uint32_t d = 0; d < a.ndst; ++d) {
+      float* dst = a.dst_vals[d];
+      const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0;
+      const uint64_t nv = vec ? cnt / 4 : 0;
+      for (uint64_t i = t; i < nv; i += nth)
+        reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+      for (uint64_t i = nv * 4 + t; i < cnt; i += nth) dst[i] = src[i];
+    }
   }
   uint32_t t = 0;
 #pragma unroll
@@ -332,6 +366,7 @@ __global__ void __launch_bounds__(kValThreads) k_agg_values(AggArgs a) {
       for (uint32_t d = 0; d < a.ndst; ++d) a.dst_cbase[d][c] = b;
     }
   }
+  if (solo_part(a)) return;  // the union copied the values (and cleaned the row)
   const bool valid = j < a.nw;
   const uint32_t pb = (uint32_t)(j / kPrefixBlockWords);
   // every worker's presence word first, then the value bases, then the
@@ -1021,7 +1056,9 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream, bool marked, bool f
     count_launch();
   }
   launch_k(k_agg_union, a.nblk, kPrefixThreads, 0, stream, a);
-  const unsigned g = (unsigned)((a.nw + kValThreads - 1) / kValThreads);
+  // (one worker of a one-server universe: the values kernel only writes the chunk bases)
+  const bool solo = a.whole && a.n == 1 && !a.pre_min;
+  const unsigned g = (unsigned)(((solo ? a.nchunks + 1 : a.nw) + kValThreads - 1) / kValThreads);
   if (a.n <= 2)
     launch_k(k_agg_values<2>, g, kValThreads, 0, stream, a);
   else if (a.n <= 4)

@@ -2,7 +2,7 @@
 """NVLink evidence for the BP exchange (rank mode, one process per GPU).
 
 The push (k_push_scatter: NVLink stores into the owners' inboxes) and the pull
-(k_agg_union + k_agg_values: NVLink stores of the HashBitmap, the values and
+(k_agg_union + k_agg_values, or k_agg_fused from 4 workers up: NVLink stores of the HashBitmap, the values and
 the per-chunk bases into every receiver) have no kernel of their own, so
 their link rate is measured on the kernels that carry them:
 
@@ -30,7 +30,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 PUSH = ("k_push_scatter",)
-PULL = ("k_agg_union", "k_agg_values")
+PULL = ("k_agg_union", "k_agg_values", "k_agg_fused")
 
 
 def nvlink_kib(handle, pynvml):
