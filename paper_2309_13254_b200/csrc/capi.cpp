@@ -2102,6 +2102,9 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   // diagnostic only (timeline studies): no hash-memory side path at all, so
   // no CollisionStats -- never set for a result that is checked or reported
   static const bool diag_no_side = std::getenv("ZEN_DIAG_NO_SIDE") != nullptr;
+  static const char* fe = std::getenv("ZEN_FORK_EARLY");
+  const bool fork_early =
+      fe ? fe[0] == '1' : (bp->cap < (4u << 20) && !(bp->local && bp->n > 1));
   auto fork_side = [&](Worker& w, bool dense_path) -> zen_status {
     if (diag_no_side) return ZEN_OK;
     CK(cudaEventRecord(bp->fork, st));
@@ -2120,6 +2123,7 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     // pass (CollisionStats) + the data-dependent fallback replay
     HashArgs<uint32_t> sa = w.a;
     if (dense_path) {
+      sa.xc.early = fork_early ? 1u : 0u;  // sizes from the extraction's counts
       launch_place_tiles<uint32_t>(sa, bp->side, side_ctas);
     } else {
       sa.xc.st_idx = nullptr;  // the ascending key list, not the staging
@@ -2137,9 +2141,18 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     // stage 1: the push -- one kernel from the staging into the owners'
     // inboxes; the hash-memory side path of each worker forks onto bp->side
     // and joins at the end of the sync
+    // The side chain (claims + depth + replay) reads only the extraction's
+    // staging and counts, so it can fork right after the extraction and run
+    // beside the push; measured (profiles/r07/fork_early_ab.txt) that wins
+    // when the claims are short -- N=1 1 % 0.1011 -> 0.0968 ms, rank N=4
+    // 0.179 -> 0.168 ms (N=2 0.1395 -> 0.1416) -- and loses with many keys
+    // (10 % N=1 0.341 -> 0.366: the claims take the SMs the push needs) or
+    // several local workers (8 emulated 1.024 -> 1.034).  ZEN_FORK_EARLY=0/1.
+    if (fork_early)
+      for (auto& w : bp->workers) CKR(fork_side(w, true));
     for (auto& w : bp->workers) {
       launch_push_scatter<uint32_t>(w.a, w.ex, st);  // + the push signal (rank mode)
-      CKR(fork_side(w, true));
+      if (!fork_early) CKR(fork_side(w, true));
       if (w.a.push_hdr && !w.a.xc.fused_signal) launch_push_signal<uint32_t>(w.a, st);
     }
   } else {

@@ -478,11 +478,15 @@ __global__ void __launch_bounds__(kThreads) k_fallback(HashArgs<K> a) {
   __shared__ uint32_t fstat[kMaxK + 1];
   HashHdr* h = a.hdr;
   const uint32_t n = a.fam.n, k = a.fam.k, lane = lane_id(), warp = threadIdx.x >> 5;
-  const bool ok = !(h->status & kErrCapacity) && h->ovf_word == ~0ull && h->fallback_any;
+  // (early side chain: the scatter's overflow witness may still be pending;
+  // an overflowing partition is never flagged -- its load exceeds r1 + r2 --
+  // and the overflow fails the whole sync on the host)
+  const SideSizes sz = side_sizes(a);
+  const bool ok = !sz.bad && (a.xc.early || h->ovf_word == ~0ull) && h->fallback_any;
   const K* st = static_cast<const K*>(a.xc.st_idx);
   for (uint32_t p = blockIdx.x; ok && p < n; p += gridDim.x) {
     if (!a.fallback[p]) continue;
-    const uint64_t z = h->count, r1 = h->r1, stride = h->stride;
+    const uint64_t z = sz.z, r1 = sz.r1, stride = sz.stride;
     const uint64_t ew = epoch_word(h->epoch);
     using S = Slot<SlotOf<K>>;
     SlotOf<K>* base = a.slots + (uint64_t)p * stride;
@@ -583,8 +587,9 @@ __global__ void __launch_bounds__(kThreads) k_depth_scan(HashArgs<K> a) {
   __shared__ uint32_t s_last;
   HashHdr* h = a.hdr;
   const uint32_t n = a.fam.n, k = a.fam.k, lane = lane_id();
-  const bool ok = !(h->status & kErrCapacity);
-  const uint64_t r1 = h->r1, r2 = h->r2, stride = h->stride;
+  const SideSizes sz = side_sizes(a);
+  const bool ok = !sz.bad;
+  const uint64_t r1 = sz.r1, r2 = sz.r2, stride = sz.stride;
   const uint64_t ew = epoch_word(h->epoch);
   for (uint32_t i = threadIdx.x; i < n * (k + 1); i += kThreads) s_hist[i] = 0;
   __syncthreads();
@@ -645,9 +650,10 @@ __global__ void __launch_bounds__(kThreads) k_depth_scan(HashArgs<K> a) {
     volatile uint32_t* st = a.stats + q * (k + 1);
     uint32_t held = 0;
     for (uint32_t d = 1; d <= k; ++d) held += st[d];
-    const uint32_t serial = a.load[q] - held;
+    const uint32_t load = side_load(a, q);
+    const uint32_t serial = load - held;
     st[0] = serial;
-    const uint32_t fb = (ok && serial > r2 && (uint64_t)a.load[q] <= stride) ? 1u : 0u;
+    const uint32_t fb = (ok && serial > r2 && (uint64_t)load <= stride) ? 1u : 0u;
     a.fallback[q] = fb;
     if (fb) atomicOr(&h->fallback_any, 1u);
   }

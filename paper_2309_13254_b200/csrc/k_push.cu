@@ -490,11 +490,12 @@ __global__ void __launch_bounds__(kPushThreads) k_place_tiles2(HashArgs<K> a) {
   __shared__ uint16_t s_pt[kPushRound];   // pending: partition << 5 | next probe
   const PushCounts& x = a.xc;
   HashHdr* h = a.hdr;
-  if (h->status & kErrCapacity) return;
+  const SideSizes sz = side_sizes(a);
+  if (sz.bad) return;
   const K* st = static_cast<const K*>(x.st_idx);
   const uint32_t n = a.fam.n, k = a.fam.k, warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t db = sizeof(W) == 4 ? a.fam.db : 0u;
-  const uint64_t r1 = h->r1, stride = h->stride;
+  const uint64_t r1 = sz.r1, stride = sz.stride;
   const uint64_t ew = epoch_word(h->epoch);
   const uint32_t ngroups = (x.ntiles + kPushTiles - 1) / kPushTiles;
   if (threadIdx.x == 0) s_np[0] = s_np[1] = 0;

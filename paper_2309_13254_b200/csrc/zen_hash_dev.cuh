@@ -200,6 +200,48 @@ __device__ __forceinline__ void place_from(const zen::DevFamily& fam, W* slots, 
   }
 }
 
+// Hash-memory sizes of this sync from the extraction's h0 counts: the same
+// arithmetic as the push scatter's first block (zen/schemes.hpp:363-367), so
+// a side chain forked right after the extraction depends on nothing the
+// scatter writes.  Every thread computes it (the super-chunk sums are a few
+// L2-resident words per partition).
+struct SideSizes {
+  uint64_t z, r1, r2, stride;
+  bool bad;
+};
+template <typename K>
+__device__ __forceinline__ SideSizes side_sizes(const zen::HashArgs<K>& a) {
+  const zen::PushCounts& x = a.xc;
+  const zen::HashHdr* h = a.hdr;
+  SideSizes q{};
+  if (!x.early) {
+    q.z = h->count;
+    q.r1 = h->r1;
+    q.r2 = h->r2;
+    q.stride = h->stride;
+    q.bad = (h->status & zen::kErrCapacity) != 0;
+    return q;
+  }
+  const uint32_t n = a.fam.n;
+  for (uint64_t i = 0; i < (uint64_t)n * x.nsup; ++i) q.z += x.scnt[i];
+  q.r1 = (uint64_t)ceil(h->r1_mult * (double)q.z / (double)n);
+  if (q.r1 < 1) q.r1 = 1;
+  q.r2 = (uint64_t)ceil(h->r2_ratio * (double)q.r1);
+  if (q.r2 < 1) q.r2 = 1;
+  q.stride = q.r1 + q.r2;
+  q.bad = q.z > a.cap || q.stride > a.stride_cap;
+  return q;
+}
+// partition p's load (early side chain) or the scatter's count
+template <typename K>
+__device__ __forceinline__ uint32_t side_load(const zen::HashArgs<K>& a, uint32_t p) {
+  const zen::PushCounts& x = a.xc;
+  if (!x.early) return a.load[p];
+  uint32_t l = 0;
+  for (uint32_t i = 0; i < x.nsup; ++i) l += x.scnt[(uint64_t)p * x.nsup + i];
+  return l;
+}
+
 // meta word of a key after the post pass: partition (9 bits), depth (5),
 // stable rank in its 256-key tile among same-partition keys (8) and among
 // same-partition serial keys (8).

@@ -121,6 +121,9 @@ struct PushCounts {
   unsigned long long* const* mk_pw;    // [n] server p's presence rows (row w: + w * nws_p)
   uint32_t* const* mk_pre;             // [n] server p's value-base rows (atomicMin, ~0 = none)
   const uint64_t* mk_nws;              // [n] server p's row stride in words
+  // the side chain forks right after the extraction and takes z, the loads
+  // and r1 / r2 from these counts itself (nothing the push scatter writes)
+  uint32_t early;
 };
 
 // ---- kernel launchers (implemented in k_*.cu) ------------------------------
