@@ -439,6 +439,38 @@ def test_bp_single_worker_pipeline(zen, co):
     assert st.serial_writes == ref.serial_writes and st.placed_at_depth == ref.placed_at_depth
 
 
+@pytest.mark.parametrize("rehash", [None, "1"])
+def test_bp_dense_collision_stats_probe_bits(zen, co, ro, monkeypatch, rehash):
+    """Dense syncs, CollisionStats vs the reference's collision_stats with the
+    claiming probe packed in the slot words (default) and with the readers
+    re-hashing instead (ZEN_SLOT_REHASH=1, the path for M >= 2^30 - 1)."""
+    torch = pytest.importorskip("torch")
+    if rehash:
+        monkeypatch.setenv("ZEN_SLOT_REHASH", rehash)
+    rows, d, n = 40_000, 32, 3
+    m = rows * d
+    rng = np.random.default_rng(77)
+    dense, pairs = [], []
+    for w in range(n):
+        live = rng.choice(rows, 2500, replace=False)
+        g = np.zeros((rows, d), np.float32)
+        g[live] = rng.integers(1, 17, (live.size, d)).astype(np.float32)
+        dense.append(torch.from_numpy(g.ravel()).cuda())
+        pairs.append(co.to_sparse(g.ravel()))
+    # a tight r1 multiplier: long displacement chains, many serial keys
+    params = zen.HashParams(seed=5, r1_multiplier=1.1)
+    bp = zen.BPSynchronizer(n, m, max_nnz=m // 4, params=params)
+    for _ in range(2):
+        bp.sync_dense(dense)
+        bp.wait()
+    for w in range(n):
+        r1, r2 = co.bp_sizes(1.1, 0.1, pairs[w][0].size, n)
+        want = ro.hierarchical_hash(m, pairs[w][0], pairs[w][1], 5, n, 3, r1, r2, worker=w)
+        st = bp.collision_stats(w)
+        assert st.serial_writes == want.serial_writes
+        assert st.placed_at_depth == want.placed_at_depth
+
+
 def test_bp_collision_stats_match_reference(zen, co, ro):
     m, n = 200_000, 4
     ins = ro.generate(m, n, 0.01, 0.5, 5)
