@@ -1783,6 +1783,12 @@ zen_status bp_wire(zen_bp* bp) {
     CKR(upload(const_cast<const uint32_t**>(s.a.in_idx), ii.data(), n));
     CKR(upload(const_cast<const float**>(s.a.in_val), iv.data(), n));
     CKR(upload(const_cast<const PushHdr**>(s.a.in_hdr), ih.data(), n));
+    // one local worker: the union builds U from its entries (dense syncs)
+    const char* ue = std::getenv("ZEN_UNION_ENTRIES");  // (=0: mark + union, A/B)
+    if (bp->local && n == 1 && !(ue && ue[0] == '0')) {
+      s.a.solo_gbase = A.inbox_gbase(L);
+      s.a.ngroups = bp->ngroups;
+    }
     if (s.a.in_gbase) {
       std::vector<const uint32_t*> ig(n);
       for (uint32_t w = 0; w < n; ++w) ig[w] = A.inbox_gbase(L) + size_t(w) * bp->ngroups;
@@ -2104,7 +2110,8 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   static const bool diag_no_side = std::getenv("ZEN_DIAG_NO_SIDE") != nullptr;
   static const char* fe = std::getenv("ZEN_FORK_EARLY");
   const bool fork_early =
-      fe ? fe[0] == '1' : (bp->cap < (4u << 20) && !(bp->local && bp->n > 1));
+      fe ? fe[0] == '1'
+         : (bp->cap < (4u << 20) && (bp->local ? bp->n == 1 : bp->n >= 4));
   auto fork_side = [&](Worker& w, bool dense_path) -> zen_status {
     if (diag_no_side) return ZEN_OK;
     CK(cudaEventRecord(bp->fork, st));
@@ -2145,9 +2152,10 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     // staging and counts, so it can fork right after the extraction and run
     // beside the push; measured (profiles/r07/fork_early_ab.txt) that wins
     // when the claims are short -- N=1 1 % 0.1011 -> 0.0968 ms, rank N=4
-    // 0.179 -> 0.168 ms (N=2 0.1395 -> 0.1416) -- and loses with many keys
-    // (10 % N=1 0.341 -> 0.366: the claims take the SMs the push needs) or
-    // several local workers (8 emulated 1.024 -> 1.034).  ZEN_FORK_EARLY=0/1.
+    // 0.179 -> 0.168 ms -- and loses with many keys (10 % N=1 0.341 ->
+    // 0.366: the claims take the SMs the push needs), several local workers
+    // (8 emulated 1.024 -> 1.034) or two ranks (N=2 0.1395 -> 0.1416).
+    // ZEN_FORK_EARLY=0/1 forces it.
     if (fork_early)
       for (auto& w : bp->workers) CKR(fork_side(w, true));
     for (auto& w : bp->workers) {
@@ -2168,7 +2176,11 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   // dense syncs in local mode: the push scatter already marked every entry
   const bool marked = from_dense && bp->local && !bp->workers.empty() &&
                       bp->workers[0].a.xc.mark;
-  for (auto& s : bp->servers) launch_aggregate(s.a, st, marked, from_dense && s.fused);
+  for (auto& s : bp->servers) {
+    AggArgs aa = s.a;
+    if (!from_dense) aa.solo_gbase = nullptr;  // (sparse inputs: no push-group bases)
+    launch_aggregate(aa, st, marked, from_dense && s.fused);
+  }
   if (ev) CK(cudaEventRecordWithFlags(ev[3], st, cudaEventRecordExternal));
   bp->dec.launch(bp->da, st);
   if (ev) CK(cudaEventRecordWithFlags(ev[4], st, cudaEventRecordExternal));

@@ -255,7 +255,38 @@ __global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
   unsigned long long U[kWPT];
 #pragma unroll
   for (int i = 0; i < kWPT; ++i) U[i] = 0;
-  if (live) {
+  const bool from_entries = solo_part(a) && a.solo_gbase != nullptr;
+  if (from_entries) {
+    // One worker, dense sync: U is its part, so the block builds its 2048
+    // words from the part's entries of its two 8-tile groups (their range
+    // from the push scatter's group bases) in shared memory -- the mark
+    // kernel and the presence row are not needed.
+    __shared__ unsigned long long sU[kPrefixBlockWords];
+    for (uint32_t i = threadIdx.x; i < kPrefixBlockWords; i += kPrefixThreads) sU[i] = 0ull;
+    __syncthreads();
+    static_assert(kPrefixBlockWords * 64 == 2 * 8 * kExtractTile, "two push groups per block");
+    const uint32_t g0 = 2 * blockIdx.x;
+    const uint32_t cnt = part_count(a, 0);
+    const uint32_t lo = g0 < a.ngroups ? a.solo_gbase[g0] : cnt;
+    const uint32_t hi = g0 + 2 < a.ngroups ? a.solo_gbase[g0 + 2] : cnt;
+    const uint64_t kbase = (uint64_t)blockIdx.x * kPrefixBlockWords * 64;
+    const uint32_t* keys = a.in_idx[0];
+    for (uint32_t e0 = lo + warp * 32; e0 < hi; e0 += kPrefixThreads) {  // warp-uniform
+      const uint32_t e = e0 + lane;
+      const bool v = e < hi;
+      const uint32_t key = v ? keys[e] : 0u;
+      const uint32_t jw = v ? (uint32_t)(((uint64_t)key - kbase) >> 6) : 0xFFFFFFFFu;
+      const uint64_t bit = v ? 1ull << (key & 63u) : 0ull;
+      const uint32_t grp = __match_any_sync(0xffffffffu, jw);
+      const uint32_t blo = __reduce_or_sync(grp, (uint32_t)bit);
+      const uint32_t bhi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
+      if (v && lane == (uint32_t)(__ffs(grp) - 1))
+        atomicOr(&sU[jw], ((unsigned long long)bhi << 32) | blo);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kWPT; ++i) U[i] = sU[threadIdx.x * kWPT + i];
+  } else if (live) {
 #pragma unroll 4
     for (uint32_t x = 0; x < n; ++x) {  // (unrolled: several rows' loads in flight)
       unsigned long long v[kWPT];
@@ -263,9 +294,11 @@ __global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
 #pragma unroll
       for (int i = 0; i < kWPT; ++i) U[i] |= v[i];
     }
+  }
+  if (live) {
     // the union bitmap (the HashBitmap: LSB-first = little-endian words)
     for (uint32_t d = 0; d < a.ndst; ++d) store8(a.dst_bits[d] + j0, U);
-    if (solo_part(a)) {  // the last reader of the presence row: clean it for the next sync
+    if (solo_part(a) && !from_entries) {  // the last reader of the presence row: clean it
       bool any = false;
 #pragma unroll
       for (int i = 0; i < kWPT; ++i) any |= U[i] != 0ull;
@@ -1051,7 +1084,9 @@ void launch_aggregate(const AggArgs& a, cudaStream_t stream, bool marked, bool f
     launch_k(k_wait_push, 1, 32, 0, stream, a);
     count_launch();
   }
-  if (!marked) {
+  // (one worker, dense sync: the union builds U from the entries, no marks)
+  const bool from_entries = a.whole && a.n == 1 && !a.pre_min && a.solo_gbase;
+  if (!marked && !from_entries) {
     launch_k(k_agg_mark, 148 * 8, kAggThreads, 0, stream, a);
     count_launch();
   }

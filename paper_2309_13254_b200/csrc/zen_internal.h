@@ -310,6 +310,9 @@ struct AggArgs {
   const unsigned long long* own_bits;  // this server's local copy of U (a dst_bits entry)
   uint32_t* const* dst_cbase;     // [ndst] -> (nchunks + 1) u32 per receiver
   int whole;                      // the universe has one server: rank in I_0 = index (no own table)
+  const uint32_t* solo_gbase;     // one worker, dense sync: its entries before each 8-tile
+                                  // group (push scatter) -> the union builds U from the
+                                  // entries and k_agg_mark is skipped; else nullptr
   int pre_min;                    // value bases come from the scatter's atomicMin marks:
                                   // reset each word read to ~0 (ZEN_SCATTER_MARK=1)
   // Fused aggregate (local mode, dense syncs; k_agg_fused): one block per 8
