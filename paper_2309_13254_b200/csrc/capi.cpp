@@ -2108,6 +2108,16 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
   // diagnostic only (timeline studies): no hash-memory side path at all, so
   // no CollisionStats -- never set for a result that is checked or reported
   static const bool diag_no_side = std::getenv("ZEN_DIAG_NO_SIDE") != nullptr;
+  // The claims can keep the depth histogram themselves (+1 / -1 per slot
+  // change, shared-memory counters) instead of the table-scan depth pass;
+  // measured (profiles/r07/hist_inline_ab.txt) faster with several local
+  // workers or many keys (8 emulated 1.026 -> 1.008 ms, 10 % 0.334 -> 0.331)
+  // and slower at 1 % N=1 (0.0958 -> 0.102: the counters lengthen the claims,
+  // which run beside the aggregate).  ZEN_HIST_INLINE=0/1 forces it.
+  static const char* ih = std::getenv("ZEN_HIST_INLINE");
+  const bool inline_hist =
+      (ih ? ih[0] == '1' : (bp->local && (bp->n > 1 || bp->cap >= (4u << 20)))) &&
+      !std::getenv("ZEN_PLACE_V1");  // (the one-phase claims keep no histogram)
   static const char* fe = std::getenv("ZEN_FORK_EARLY");
   const bool fork_early =
       fe ? fe[0] == '1'
@@ -2131,6 +2141,7 @@ zen_status bp_enqueue(zen_bp* bp, bool from_dense, const float* const* dense, cu
     HashArgs<uint32_t> sa = w.a;
     if (dense_path) {
       sa.xc.early = fork_early ? 1u : 0u;  // sizes from the extraction's counts
+      sa.xc.inline_hist = inline_hist ? 1u : 0u;
       launch_place_tiles<uint32_t>(sa, bp->side, side_ctas);
     } else {
       sa.xc.st_idx = nullptr;  // the ascending key list, not the staging

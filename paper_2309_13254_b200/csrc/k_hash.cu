@@ -760,6 +760,12 @@ void launch_hash_side_bp(const HashArgs<K>& a, cudaStream_t stream, unsigned cta
     launch_k(k_place<K>, grid_for(a.cap, kThreads * 4, 148 * ctas_per_sm), kThreads, 0, stream, a);
     count_launch();
   }
+  if (a.xc.inline_hist) {  // the claims kept the histogram: only vacate the memory
+    launch_vacate<K>(a, stream);
+    launch_k(k_fallback<K>, grid_for(a.fam.n, 1, 148), kThreads, 0, stream, a);
+    count_launch();
+    return;
+  }
   const unsigned gx = std::max(1u, grid_for(a.stride_cap, kThreads * 4, 148 * ctas_per_sm) / a.fam.n);
   launch_k(k_depth_scan<K>, dim3(gx, a.fam.n), kThreads, 0, stream, a);
   // the replay is data dependent: it returns at once unless a partition was flagged

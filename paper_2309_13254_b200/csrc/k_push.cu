@@ -488,10 +488,14 @@ __global__ void __launch_bounds__(kPushThreads) k_place_tiles2(HashArgs<K> a) {
   __shared__ uint32_t s_group, s_np[2];  // pending counts, alternating rounds
   __shared__ uint32_t s_key[kPushRound];  // pending: key (index + 1)
   __shared__ uint16_t s_pt[kPushRound];   // pending: partition << 5 | next probe
+  __shared__ int s_hist[kMaxWorkers * (kMaxK + 1)];  // inline depth histogram (this block)
+  __shared__ uint32_t s_last;
   const PushCounts& x = a.xc;
   HashHdr* h = a.hdr;
   const SideSizes sz = side_sizes(a);
   if (sz.bad) return;
+  int* hist = x.inline_hist ? s_hist : nullptr;
+  for (uint32_t i = threadIdx.x; i < kMaxWorkers * (kMaxK + 1); i += kPushThreads) s_hist[i] = 0;
   const K* st = static_cast<const K*>(x.st_idx);
   const uint32_t n = a.fam.n, k = a.fam.k, warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t db = sizeof(W) == 4 ? a.fam.db : 0u;
@@ -533,6 +537,7 @@ __global__ void __launch_bounds__(kPushThreads) k_place_tiles2(HashArgs<K> a) {
         uint64_t nk = key[j];
         uint32_t nt = 1;
         bool go = v[j] && !S::vacant(old[j], ew);
+        if (hist && v[j] && !go) atomicAdd(&hist[part[j] * (k + 1) + 1], 1);  // took c at probe 0
         if (go) {
           const uint64_t ok = S::key(old[j], db);
           if (ok > key[j]) {  // displaced a larger key: it resumes after its first c
@@ -543,6 +548,10 @@ __global__ void __launch_bounds__(kPushThreads) k_place_tiles2(HashArgs<K> a) {
             else
               while (f < k && slot_of(a.fam, ok, f, r1) != c[j]) ++f;
             nt = f + 1;
+            if (hist) {
+              atomicAdd(&hist[part[j] * (k + 1) + 1], 1);
+              atomicAdd(&hist[part[j] * (k + 1) + f + 1], -1);
+            }
           }
           go = nt < k;  // else: ends serial
         }
@@ -570,12 +579,60 @@ __global__ void __launch_bounds__(kPushThreads) k_place_tiles2(HashArgs<K> a) {
           t[j] = q & 31u;
           nv += i < np ? 1u : 0u;
         }
-        place_from<2>(a.fam, a.slots, cur, t, pp, nv, r1, stride, ew);
+        place_from<2>(a.fam, a.slots, cur, t, pp, nv, r1, stride, ew, hist);
       }
       __syncthreads();  // the list is consumed
       par ^= 1;
     }
     __syncthreads();  // s_tpre / s_group / s_np reuse
+  }
+  if (!hist) return;
+  // inline histogram: this block's net counts, then the last block turns the
+  // totals into CollisionStats and the fallback flags (k_depth_scan's job)
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n * (k + 1); i += kPushThreads)
+    if (s_hist[i]) atomicAdd(&a.stats[i], (uint32_t)s_hist[i]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (atomicAdd(&h->done, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < n) {  // serial = keys of p holding no slot
+    const uint32_t q = threadIdx.x;
+    volatile uint32_t* stq = a.stats + q * (k + 1);
+    uint32_t held = 0;
+    for (uint32_t d = 1; d <= k; ++d) held += stq[d];
+    const uint32_t load = side_load(a, q);
+    const uint32_t serial = load - held;
+    stq[0] = serial;
+    const uint32_t fb = (serial > sz.r2 && (uint64_t)load <= sz.stride) ? 1u : 0u;
+    a.fallback[q] = fb;
+    if (fb) atomicOr(&h->fallback_any, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x <= k && !((volatile uint32_t*)&h->fallback_any)[0]) {
+    uint64_t sum = 0;
+    for (uint32_t q = 0; q < n; ++q) sum += ((volatile uint32_t*)a.stats)[q * (k + 1) + threadIdx.x];
+    a.stats_out[threadIdx.x] = sum;
+  }
+  if (threadIdx.x == 0) h->done = 0;
+}
+
+// inline-histogram side chain: vacate the parallel regions the claims used
+template <typename K>
+__global__ void __launch_bounds__(256) k_vacate(HashArgs<K> a) {
+  zen_dev::pdl_entry();
+  using W = SlotOf<K>;
+  const SideSizes sz = side_sizes(a);
+  if (sz.bad) return;
+  const uint64_t tot = (uint64_t)a.fam.n * sz.r1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = i / sz.r1, c = i - p * sz.r1;
+    a.slots[p * sz.stride + c] = Slot<W>::kVacant;
   }
 }
 
@@ -594,6 +651,14 @@ void launch_push_scatter(const HashArgs<K>& a, const ExtractWs<K>& ws, cudaStrea
   launch_k(a.xc.reorder ? k_push_scatter<K, true> : k_push_scatter<K, false>,
            a.xc.scatter_grid,
            kPushThreads, 0, stream, a, (const K*)ws.st_idx, (const float*)ws.st_val);
+  count_launch();
+}
+
+template <typename K>
+void launch_vacate(const HashArgs<K>& a, cudaStream_t stream) {
+  const uint64_t cells = (uint64_t)a.fam.n * a.stride_cap;
+  launch_k(k_vacate<K>, (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((cells + 1023) / 1024, 148 * 8)),
+           256, 0, stream, a);
   count_launch();
 }
 
@@ -624,8 +689,10 @@ unsigned push_scatter_grid(bool peer, uint32_t ntiles) {
   template void launch_bp_begin<K>(const HashArgs<K>&, cudaStream_t);                        \
   template void launch_push_scatter<K>(const HashArgs<K>&, const ExtractWs<K>&, cudaStream_t); \
   template void launch_place_tiles<K>(const HashArgs<K>&, cudaStream_t, unsigned);            \
+  template void launch_vacate<K>(const HashArgs<K>&, cudaStream_t);                            \
   template unsigned push_scatter_grid<K>(bool, uint32_t);
 ZEN_INST(uint32_t)
 #undef ZEN_INST
+template void launch_vacate<uint64_t>(const HashArgs<uint64_t>&, cudaStream_t);
 
 }  // namespace zen

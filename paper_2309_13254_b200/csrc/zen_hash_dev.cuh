@@ -149,11 +149,14 @@ __device__ __forceinline__ void place_keys(const zen::DevFamily& fam, W* slots,
 
 // Continuation of claims already under way: item j is key cur[j] of
 // partition part[j] about to try probe t[j] (same protocol as place_keys).
+// hist (optional, shared memory, [part][depth] with depth = probe + 1): the
+// final occupants' depth histogram kept incrementally -- +1 when a key takes
+// a slot, -1 at the displaced key's depth when it loses one.
 template <int KPT, typename W>
 __device__ __forceinline__ void place_from(const zen::DevFamily& fam, W* slots, uint64_t (&cur)[KPT],
                                            uint32_t (&t)[KPT], const uint32_t (&part)[KPT],
                                            uint32_t nvalid, uint64_t r1, uint64_t stride,
-                                           uint64_t ew) {
+                                           uint64_t ew, int* hist = nullptr) {
   using S = Slot<W>;
   W* base[KPT];
   bool act[KPT];
@@ -179,6 +182,7 @@ __device__ __forceinline__ void place_from(const zen::DevFamily& fam, W* slots, 
     for (int j = 0; j < KPT; ++j) {
       if (!act[j]) continue;
       if (S::vacant(old[j], ew)) {
+        if (hist) atomicAdd(&hist[part[j] * (k + 1) + t[j] + 1], 1);
         act[j] = false;
         continue;
       }
@@ -190,6 +194,10 @@ __device__ __forceinline__ void place_from(const zen::DevFamily& fam, W* slots, 
           f = S::probe(old[j], db);
         else
           while (f < k && slot_of(fam, ok, f, r1) != c[j]) ++f;
+        if (hist) {
+          atomicAdd(&hist[part[j] * (k + 1) + t[j] + 1], 1);  // the displacer holds c
+          atomicAdd(&hist[part[j] * (k + 1) + f + 1], -1);    // the displaced lost it
+        }
         t[j] = f + 1;
       } else {
         ++t[j];

@@ -124,6 +124,10 @@ struct PushCounts {
   // the side chain forks right after the extraction and takes z, the loads
   // and r1 / r2 from these counts itself (nothing the push scatter writes)
   uint32_t early;
+  // the claims keep the depth histogram themselves (+1 when a key takes a
+  // slot, -1 when a key is displaced from one): no table scan, the memory is
+  // vacated by a plain clear kernel
+  uint32_t inline_hist;
 };
 
 // ---- kernel launchers (implemented in k_*.cu) ------------------------------
@@ -251,6 +255,8 @@ void launch_hash_side_bp(const HashArgs<K>& a, cudaStream_t stream, unsigned cta
 // the claims of a dense sync, straight from the extraction staging (k_push.cu)
 template <typename K>
 void launch_place_tiles(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm);
+template <typename K>
+void launch_vacate(const HashArgs<K>& a, cudaStream_t stream);
 // resident blocks of the persistent push scatter
 template <typename K>
 unsigned push_scatter_grid(bool peer, uint32_t ntiles);
