@@ -628,11 +628,19 @@ __global__ void __launch_bounds__(256) k_vacate(HashArgs<K> a) {
   using W = SlotOf<K>;
   const SideSizes sz = side_sizes(a);
   if (sz.bad) return;
-  const uint64_t tot = (uint64_t)a.fam.n * sz.r1;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t p = i / sz.r1, c = i - p * sz.r1;
-    a.slots[p * sz.stride + c] = Slot<W>::kVacant;
+  // per partition, no division per word; 16-byte stores over the aligned middle
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr uint32_t kPer = 16 / sizeof(W);  // words per 16-byte store
+  for (uint32_t p = 0; p < a.fam.n; ++p) {
+    W* base = a.slots + (uint64_t)p * sz.stride;
+    const uint64_t mis = ((16 - (reinterpret_cast<uintptr_t>(base) & 15)) & 15) / sizeof(W);
+    const uint64_t head = mis < sz.r1 ? mis : sz.r1;
+    const uint64_t nvec = (sz.r1 - head) / kPer;
+    for (uint64_t c = t; c < head; c += nth) base[c] = Slot<W>::kVacant;
+    uint4* v = reinterpret_cast<uint4*>(base + head);
+    for (uint64_t c = t; c < nvec; c += nth) v[c] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (uint64_t c = head + nvec * kPer + t; c < sz.r1; c += nth) base[c] = Slot<W>::kVacant;
   }
 }
 
