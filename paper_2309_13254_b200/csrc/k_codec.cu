@@ -271,17 +271,26 @@ __global__ void __launch_bounds__(kPrefixThreads) k_agg_union(AggArgs a) {
     const uint32_t hi = g0 + 2 < a.ngroups ? a.solo_gbase[g0 + 2] : cnt;
     const uint64_t kbase = (uint64_t)blockIdx.x * kPrefixBlockWords * 64;
     const uint32_t* keys = a.in_idx[0];
-    for (uint32_t e0 = lo + warp * 32; e0 < hi; e0 += kPrefixThreads) {  // warp-uniform
-      const uint32_t e = e0 + lane;
-      const bool v = e < hi;
-      const uint32_t key = v ? keys[e] : 0u;
-      const uint32_t jw = v ? (uint32_t)(((uint64_t)key - kbase) >> 6) : 0xFFFFFFFFu;
-      const uint64_t bit = v ? 1ull << (key & 63u) : 0ull;
-      const uint32_t grp = __match_any_sync(0xffffffffu, jw);
-      const uint32_t blo = __reduce_or_sync(grp, (uint32_t)bit);
-      const uint32_t bhi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
-      if (v && lane == (uint32_t)(__ffs(grp) - 1))
-        atomicOr(&sU[jw], ((unsigned long long)bhi << 32) | blo);
+    constexpr int R = 4;  // rounds of keys in flight per warp (loads first)
+    for (uint32_t e0 = lo + warp * 32; e0 < hi; e0 += R * kPrefixThreads) {  // warp-uniform
+      uint32_t key[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const uint32_t e = e0 + q * kPrefixThreads + lane;
+        key[q] = e < hi ? keys[e] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (e0 + q * kPrefixThreads >= hi) break;  // warp-uniform
+        const bool v = e0 + q * kPrefixThreads + lane < hi;
+        const uint32_t jw = v ? (uint32_t)(((uint64_t)key[q] - kbase) >> 6) : 0xFFFFFFFFu;
+        const uint64_t bit = v ? 1ull << (key[q] & 63u) : 0ull;
+        const uint32_t grp = __match_any_sync(0xffffffffu, jw);
+        const uint32_t blo = __reduce_or_sync(grp, (uint32_t)bit);
+        const uint32_t bhi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
+        if (v && lane == (uint32_t)(__ffs(grp) - 1))
+          atomicOr(&sU[jw], ((unsigned long long)bhi << 32) | blo);
+      }
     }
     __syncthreads();
 #pragma unroll
