@@ -992,6 +992,30 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecodeArgs a, uint64_t n
   const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
   const uint32_t row0 = threadIdx.x & ~31u;
   const uint64_t wrow = (w & ~31ull);
+  if (n == 1) {
+    // One server and every non-empty word of the chunk full (dense rows):
+    // the warp expands word by word, lane l taking bits l and 32 + l --
+    // consecutive outputs and consecutive values, no per-bit search.
+    const uint32_t nz = __ballot_sync(0xffffffffu, G != 0ull);
+    if (__ballot_sync(0xffffffffu, G == ~0ull) == nz) {
+      for (uint32_t m = nz; m; m &= m - 1) {
+        const uint32_t L = (uint32_t)(__ffs(m) - 1);
+        const uint64_t o = ob + __shfl_sync(0xffffffffu, x, L);
+        const uint32_t vb = svb[row0 + L][0];
+        const uint64_t idx0 = (wrow + L) * 64;
+        const float v0 = a.vals[0][vb + lane], v1 = a.vals[0][vb + 32 + lane];
+        if (o + lane < a.out_cap) {
+          a.out_idx[o + lane] = idx0 + lane;
+          a.out_val[o + lane] = v0;
+        }
+        if (o + 32 + lane < a.out_cap) {
+          a.out_idx[o + 32 + lane] = idx0 + 32 + lane;
+          a.out_val[o + 32 + lane] = v1;
+        }
+      }
+      return;
+    }
+  }
   constexpr int UNR = 4;  // outputs per lane per pass, loads issued first
   for (uint32_t k0 = 0; k0 < T; k0 += 32 * UNR) {
     float v[UNR];

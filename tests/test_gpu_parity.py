@@ -417,6 +417,31 @@ def test_bp_dense_aggregate_paths(zen, co, monkeypatch, fused, n):
             np.testing.assert_array_equal(agg, want.agg_counts)
 
 
+@pytest.mark.parametrize("density", [0.01, 0.1, 0.5])
+def test_bp_single_worker_full_rows(zen, co, density):
+    """n = 1 with 64-wide rows (every non-empty bitmap word full: the decode's
+    word-by-word path) mixed with a few partial rows (the generic path), vs the
+    oracle; two syncs (graph replay)."""
+    torch = pytest.importorskip("torch")
+    rows, d = 200_000, 64
+    m = rows * d
+    rng = np.random.default_rng(int(density * 1000))
+    g = np.zeros((rows, d), np.float32)
+    live = rng.choice(rows, int(rows * density), replace=False)
+    g[live] = rng.standard_normal((live.size, d)).astype(np.float32)
+    part = rng.choice(rows, 50, replace=False)
+    g[part, : d // 2] = 0.0  # some half rows
+    dense = torch.from_numpy(g.ravel()).cuda()
+    want_i, want_v = co.to_sparse(g.ravel())
+    bp = zen.BPSynchronizer(1, m, max_nnz=want_i.size + 4096)
+    for _ in range(2):
+        bp.sync_dense([dense])
+        bp.wait()
+        oi, ov = bp.result()
+        np.testing.assert_array_equal(oi.cpu().numpy().view(np.uint64), want_i)
+        np.testing.assert_array_equal(bits(ov.cpu().numpy()), bits(want_v))
+
+
 def test_bp_single_worker_pipeline(zen, co):
     """n = 1 (the 1-GPU bench case): extraction + hash + self aggregate/encode/decode."""
     torch = pytest.importorskip("torch")
