@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kPushThreads) k_place_tiles(HashArgs<K> a) {
 // are compacted into a shared-memory list and continue (place_from), so a
 // warp no longer runs until the longest chain among its 128 keys ends with
 // most lanes idle.  Same protocol, same matching (schedule-independent).
-template <typename K>
+template <typename K, bool HIST>
 __global__ void __launch_bounds__(kPushThreads) k_place_tiles2(HashArgs<K> a) {
   zen_dev::pdl_entry();
   using W = SlotOf<K>;
@@ -494,8 +494,11 @@ __global__ void __launch_bounds__(kPushThreads) k_place_tiles2(HashArgs<K> a) {
   HashHdr* h = a.hdr;
   const SideSizes sz = side_sizes(a);
   if (sz.bad) return;
-  int* hist = x.inline_hist ? s_hist : nullptr;
-  for (uint32_t i = threadIdx.x; i < kMaxWorkers * (kMaxK + 1); i += kPushThreads) s_hist[i] = 0;
+  // HIST: the variant with the counter code (the counters themselves are on
+  // only with x.inline_hist); !HIST: the lean variant (48 vs 59 registers)
+  int* hist = (HIST && x.inline_hist) ? s_hist : nullptr;
+  if (hist)
+    for (uint32_t i = threadIdx.x; i < kMaxWorkers * (kMaxK + 1); i += kPushThreads) s_hist[i] = 0;
   const K* st = static_cast<const K*>(x.st_idx);
   const uint32_t n = a.fam.n, k = a.fam.k, warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t db = sizeof(W) == 4 ? a.fam.db : 0u;
@@ -674,7 +677,13 @@ template <typename K>
 void launch_place_tiles(const HashArgs<K>& a, cudaStream_t stream, unsigned ctas_per_sm) {
   const unsigned groups = (a.xc.ntiles + kPushTiles - 1) / kPushTiles;
   static const bool v1 = std::getenv("ZEN_PLACE_V1") != nullptr;  // (A/B: one-phase claims)
-  launch_k(v1 ? k_place_tiles<K> : k_place_tiles2<K>,
+  // Rank mode takes the lean variant; local mode the counter-carrying one even
+  // with the counters off: measured (profiles/r07/place_variant_ab.txt), the
+  // lean one is faster with peers (N=2 0.1427 -> 0.1388 ms, N=4 0.1715 ->
+  // 0.1682) but slower beside the one-worker aggregate (N=1 0.0938 -> 0.0965
+  // ms: more claim blocks fit next to the union and crowd it)
+  launch_k(v1 ? k_place_tiles<K>
+              : (a.xc.inline_hist || !a.peer) ? k_place_tiles2<K, true> : k_place_tiles2<K, false>,
            std::max(1u, std::min(groups, 148u * ctas_per_sm)), kPushThreads, 0, stream, a);
   count_launch();
 }

@@ -1,0 +1,9 @@
+mkdir -p gpurun_out/$1
+for r in 1 2; do for N in 2 4; do for L in base ab; do for F in def 1; do
+ if [ $L = ab ]; then export ZEN_B200_LIB=$PWD/paper_2309_13254_b200/lib/libzen_b200_ab.so; else unset ZEN_B200_LIB; fi
+ if [ $F = 1 ]; then export ZEN_FORK_EARLY=1; else unset ZEN_FORK_EARLY; fi
+ [ $N = 4 ] && [ $F = 1 ] && continue
+ timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2$r$N$([ $L = ab ] && echo 1 || echo 0)$([ $F = 1 ] && echo 1 || echo 0) bench.py --gpus $N --steps 100 --warmup 10 --no-cpu --no-extras --no-e2e 2>/dev/null | grep -v NCCL | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$L early=$F N=$N', d['value'])" >> gpurun_out/$1/ab.txt
+done; done; done; done
+unset ZEN_B200_LIB ZEN_FORK_EARLY
+unset ZEN_B200_LIB
